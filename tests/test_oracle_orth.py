@@ -1,0 +1,193 @@
+"""Pins for oracle/orth.py (§2, Algorithms 1-8, Table 1).
+
+Pins: Table 1 rounding counts (golden), the closed forms of the shared-tail construction
+(R = R_M, Gram = M^T M, q_i = B Q_M[:, i]), the orthonormal-input fixed point, dense
+Gram-Schmidt / Householder QR on the densified vectors, the Householder hand cases and
+identities of PAPER.md:286-303, literal == lazy, breakdown behaviour, and the paper's
+order-of-magnitude LOO statements (Eqs. (10)-(12)).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dense, orth, rounding, tt
+from ttinputs import CONFIGS, make_shared_tail_set
+
+HERE = os.path.dirname(__file__)
+TABLE1 = json.load(open(os.path.join(HERE, "golden", "table1_rounding_counts.json")))
+GOLD = json.load(open(os.path.join(HERE, "golden", "spec_examples.json")))
+KINDS = ["cgs", "mgs", "cgs2", "mgs2", "gram", "householder"]
+
+
+def _sign_fix(R):
+    s = np.sign(np.diag(R))
+    s[s == 0] = 1
+    return s[:, None] * R, s
+
+
+def _tt_diff_norm(x, y):
+    """||x - y|| by an exact (delta = 0) rounding of the difference: the sweep norm ||C_1||_F
+    (never sqrt(<a,a> - 2<a,b> + <b,b>))."""
+    _, info = rounding.tt_round(tt.tt_sum([x, y], [1.0, -1.0]), 0.0)
+    return info.norm
+
+
+@pytest.fixture(scope="module")
+def well_conditioned():
+    return make_shared_tail_set(4, 8, 3, 10, 1e2, seed=991)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_rounding_counts_table1(kind, well_conditioned):
+    A = well_conditioned.tensors[:5]
+    a, b = TABLE1["per_m"][kind]
+    for literal in (False, True):
+        res = orth.orth(kind, A, 1e-10, literal=literal)
+        assert res.rounding_calls == a * 5 + b
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_closed_form_well_conditioned(kind, well_conditioned):
+    st = well_conditioned
+    res = orth.orth(kind, st.tensors, 1e-12)
+    qm, rm = st.qr_exact()
+    R = res.R
+    s = np.ones(st.m)
+    if kind == "householder":
+        R, s = _sign_fix(R)   # R(i,i) sign is set by Alg. 6's rule
+    assert np.linalg.norm(R - rm) <= 1e-9 * np.linalg.norm(rm)
+    assert np.all(R[np.tril_indices(st.m, -1)] == 0.0)  # structural zeros
+    for i in range(st.m):
+        assert _tt_diff_norm(tt.tt_scale(res.Q[i], s[i]), st.q_exact(i)) <= 1e-9
+    assert res.loo_per_step()[-1] <= 1e-9
+
+
+def test_gram_closed_form_c3_shape():
+    """Gram(A) = M^T M exactly for the shared-tail construction (C3 shape, reduced m)."""
+    c = CONFIGS["C3"]
+    st = make_shared_tail_set(c.d, c.n, c.r, 6, c.kappa, c.seed)
+    G = orth.gram_matrix(st.tensors)
+    assert np.linalg.norm(G - st.gram_exact()) <= 1e-13 * np.linalg.norm(st.gram_exact())
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_literal_equals_lazy(kind, well_conditioned):
+    A = well_conditioned.tensors[:6]
+    r1 = orth.orth(kind, A, 1e-10, literal=True)
+    r2 = orth.orth(kind, A, 1e-10, literal=False)
+    assert np.linalg.norm(r1.R - r2.R) <= 1e-12 * np.linalg.norm(r1.R)
+    assert [i.ranks for i in r1.infos] == [i.ranks for i in r2.infos]
+    for q1, q2 in zip(r1.Q, r2.Q):
+        assert _tt_diff_norm(q1, q2) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_orthonormal_input_fixed_point(kind):
+    """canonical inputs -> Q = input, R = I."""
+    n = [4, 3, 5]
+    A = [tt.canonical_tt(i, n) for i in (1, 2, 3, 4, 5)]
+    res = orth.orth(kind, A, 1e-8)
+    R, s = _sign_fix(res.R)
+    assert np.allclose(R, np.eye(5), atol=1e-12)
+    for i in range(5):
+        np.testing.assert_allclose(s[i] * tt.densify(res.Q[i]), tt.densify(A[i]), atol=1e-12)
+
+
+def _dense_gs(Ad, kind):
+    """Plain dense Gram-Schmidt family on the unfolded vectors (matrix framework of §2.1,
+    PAPER.md:80-82, 135, 141-142) and Cholesky-QR (Gram)."""
+    n, m = Ad.shape
+    Q = np.zeros((n, m))
+    R = np.zeros((m, m))
+    if kind == "gram":
+        L = np.linalg.cholesky(Ad.T @ Ad)
+        R = L.T
+        return Ad @ np.linalg.inv(R), R
+    passes = 2 if kind.endswith("2") else 1
+    for i in range(m):
+        v = Ad[:, i].copy()
+        for _ in range(passes):
+            w = v.copy()
+            for j in range(i):
+                c = Q[:, j] @ (w if kind.startswith("mgs") else v)
+                R[j, i] += c
+                w -= c * Q[:, j]
+            v = w
+        R[i, i] = np.linalg.norm(v)
+        Q[:, i] = v / R[i, i]
+    return Q, R
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_dense_equivalence_unfolded(kind):
+    """d=3, n=5, m=8, tiny delta: TT kernels == dense counterparts on the
+    densified vectors (Householder: numpy QR, i.e. LAPACK Householder, up to column signs)."""
+    st = make_shared_tail_set(3, 5, 3, 8, 1e3, seed=77)
+    Ad = np.stack([tt.densify(a) for a in st.tensors], axis=1)
+    res = orth.orth(kind, st.tensors, 1e-14)
+    Qt = np.stack([tt.densify(q) for q in res.Q], axis=1)
+    if kind == "householder":
+        Qd, Rd = np.linalg.qr(Ad)
+        Rd, s = _sign_fix(Rd)
+        Qd = Qd * s[None, :]
+        Rt, st_ = _sign_fix(res.R)
+        Qt = Qt * st_[None, :]
+    else:
+        Qd, Rd = _dense_gs(Ad, kind)
+        Rt = res.R
+    assert np.linalg.norm(Rt - Rd) <= 1e-10 * np.linalg.norm(Rd)
+    assert np.max(np.abs(np.abs(np.sum(Qt * Qd, axis=0)) - 1.0)) <= 1e-9
+
+
+def test_tth_vec_hand_cases():
+    g_e2, g_e1 = GOLD["householder_2d"]
+    n = g_e2["n"]
+    u, r, _, _ = orth.tth_vec_literal(tt.canonical_tt(2, n), 1, 1e-12, 0.0)
+    assert r[0] == g_e2["r1"]
+    v = tt.densify(u)
+    assert v[0] == pytest.approx(g_e2["u_entries"]["1"], abs=1e-15)
+    assert v[1] == pytest.approx(g_e2["u_entries"]["2"], abs=1e-15)
+    u, r, _, _ = orth.tth_vec_literal(tt.canonical_tt(1, n), 1, 1e-12, 0.0)
+    assert u is None and r[0] == g_e1["r1"]
+
+
+def test_householder_maps_w_into_span():
+    """with u from Eq. (5), H x = ||x|| y; here H_i w_i = sum_{j<=i} r(j) e_j."""
+    st = make_shared_tail_set(3, 4, 2, 4, 10.0, seed=5)
+    w = st.tensors[0]
+    for i in (1, 2, 3):
+        u, r, _, _ = orth.tth_vec_literal(w, i, 1e-14, 0.0)
+        hw, _ = orth.apply_h_vec(w, u)
+        v = tt.densify(hw)
+        target = np.zeros_like(v)
+        target[:i] = r
+        assert np.linalg.norm(v - target) <= 1e-12 * np.linalg.norm(v)
+        # apply-H-vec is an involution
+        back, _ = orth.apply_h_vec(hw, u)
+        np.testing.assert_allclose(tt.densify(back), tt.densify(w), atol=1e-13)
+
+
+def test_breakdowns():
+    st = make_shared_tail_set(3, 4, 2, 3, 10.0, seed=6)
+    A = [st.tensors[0], st.tensors[0]]
+    with pytest.raises(dense.SingularGram):
+        orth.orth("gram", A, 1e-8)
+    with pytest.raises(orth.LinearDependence) as ei:
+        orth.orth("mgs", A, 1e-8)
+    assert ei.value.index == 1
+
+
+def test_paper_loo_statements_c1():
+    """Order-of-magnitude statements of PAPER.md:509-510 / Eqs. (10)-(12) on C1
+    (kappa = 1e8, delta = 1e-8): Householder LOO ~ delta, MGS ~ u kappa, CGS2/MGS2 ~ u,
+    CGS and Gram far above MGS (kappa^2)."""
+    c = CONFIGS["C1"]
+    st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed)
+    loo = {k: orth.orth(k, st.tensors, c.delta).loo_per_step() for k in KINDS}
+    assert np.max(loo["householder"]) <= 100 * c.delta
+    assert np.max(loo["mgs2"]) <= 1e-11 and np.max(loo["cgs2"]) <= 1e-11
+    assert np.max(loo["mgs"]) <= 1e3 * dense.U_ROUND * c.kappa
+    assert np.max(loo["cgs"]) >= 1e3 * np.max(loo["mgs"])
+    assert np.max(loo["gram"]) >= 1e3 * np.max(loo["mgs"])
