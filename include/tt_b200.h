@@ -1,0 +1,192 @@
+/*
+ * tt_b200.h -- C ABI of the B200-native hot path of arXiv 2211.08770
+ * ("TT-format orthogonalization": TT-rounding of rank-inflated TT-sums plus batched
+ * TT inner products, and the six orthogonalization kernels built on them).
+ *
+ * Every entry point below is implemented by hand-written sm_100a CUDA kernels in
+ * libtt_b200.so (paper_2211_08770_b200/csrc).  No torch types cross this boundary:
+ * plain pointers (host or device, as stated per argument) and sizes.
+ *
+ * Conventions (all calls)
+ *   - fp64 everywhere ("u_64 ~ 1e-16 for 64-bit calculation").
+ *   - A TT-vector of order d has cores X_k of shape (r_{k-1}, n_k, r_k), r_0 = r_d = 1
+ *     (PAPER.md:41-45), stored contiguously in C order with r_k fastest:
+ *     element (a, i, b) of core k is core[k][(a * n_k + i) * r_k + b].
+ *   - Canonical indices are 1-based psi order, mode 1 fastest.
+ *   - Dense m x m outputs (R, Gram) are row-major.
+ *   - Calls are enqueued on the context's stream.  Calls that return host scalars or
+ *     data-dependent ranks (tt_round*, tt_orth, tt_norm, tt_download) synchronise that
+ *     stream; tt_dot_batch, tt_gram, tt_gram_blocks, tt_element do not (device outputs).
+ *   - Errors: every call returns a tt_status; TT_OK = 0.  tt_last_error(ctx) returns a
+ *     NUL-terminated description of the last failure on that context (owned by ctx,
+ *     valid until the next call on it).  No call throws or aborts.
+ *   - Ownership: tt_view arguments are BORROWED (never written; must stay valid until the
+ *     call returns).  tt_tensor results are allocated by the library (their ranks are
+ *     data-dependent) from the context's stream-ordered pool; release with
+ *     tt_tensor_free.  Dense outputs go to caller buffers.
+ */
+#ifndef TT_B200_H
+#define TT_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TT_API __attribute__((visibility("default")))
+#else
+#define TT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TT_OK = 0,
+  TT_EINVAL = 1,          /* bad argument (null pointer, negative size, ...) */
+  TT_ESHAPE = 2,          /* operands disagree in order / mode sizes / ranks */
+  TT_EINDEX = 3,          /* canonical index outside 1..prod(n) */
+  TT_ENOMEM = 4,          /* device allocation failed */
+  TT_ECUDA = 5,           /* CUDA runtime error (text in tt_last_error) */
+  TT_ENOCONV = 6,         /* Jacobi SVD exceeded its sweep limit */
+  TT_ESINGULAR_GRAM = 7,  /* Cholesky of the Gram matrix met a pivot <= 0 */
+  TT_ELINDEP = 8,         /* ||p|| <= 1e3 u ||a_i||: linear dependence */
+  TT_ENUMDEFECT = 9,      /* ||a||^2 - s < -1e-12 ||a||^2 in TTH-vec (literal beta) */
+  TT_ENOTSUP = 10         /* shape outside what this build supports (message says which) */
+} tt_status;
+
+typedef struct tt_ctx_s* tt_ctx;
+typedef struct tt_tensor_s* tt_tensor;
+
+/* A borrowed TT-vector.  n[d], r[d+1] and the array core[d] are HOST arrays; core[k]
+ * points to DEVICE memory except for tt_upload (host memory).  norm = ||y|| when known
+ * (used for the pre-cancellation scale s(x) of the noise floor), NaN when unknown
+ * (the library then computes it). */
+typedef struct {
+  int32_t d;
+  const int64_t* n;
+  const int64_t* r;
+  const double* const* core;
+  double norm;
+} tt_view;
+
+/* TT-rounding options (||x - x~|| <= delta ||x||).
+ *   rel_tol  delta >= 0.  Per-split threshold tau = max(delta ||x|| / sqrt(d-1),
+ *            floor_c * u * s(x)) with s(x) = sum_l |c_l| ||y_l||.
+ *            delta = 0: no truncation, no floor (structural ranks kept).
+ *   max_rank 0 = none; else every rank is capped (SPEC.md:246 MaxRank mode).
+ *   floor_c  noise-floor constant; 0 = paper-pure threshold.  Default 2048.
+ *   qrcp_theta  truncated-SVD stopping fraction theta in (0,1]; 0 selects 0.5.  The
+ *            decision equals the exact-SVD decision. */
+typedef struct {
+  double rel_tol;
+  int64_t max_rank;
+  double floor_c;
+  double qrcp_theta;
+} tt_round_opts;
+
+typedef struct {
+  double norm;   /* ||x|| = ||C_1||_F after the right-to-left sweep */
+  double scale;  /* s(x) */
+  double tau;    /* per-split threshold used */
+  int64_t qrcp_steps;   /* total column-pivoted Householder steps over all splits */
+  int64_t resumes;      /* ambiguous decisions resolved by resuming the QRCP */
+} tt_round_info;
+
+typedef enum { TT_CGS = 0, TT_MGS = 1, TT_CGS2 = 2, TT_MGS2 = 3, TT_GRAM = 4, TT_HOUSEHOLDER = 5 } tt_orth_kind;
+
+typedef struct {
+  tt_round_opts round;
+  int32_t hh_beta_literal;  /* 0: R(i,i) = sign * ||round(w - sum_{j<i} r_j e_j)||;
+                               1: literal sqrt(||w||^2 - s) of Alg. 6 line 10 */
+  int32_t want_loo;         /* fill report->loo_per_step (costs the Q Gram) */
+} tt_orth_opts;
+
+typedef struct {
+  int64_t rounding_calls;      /* Table 1 ledger */
+  int32_t fail_index;          /* 0-based step of a breakdown, -1 otherwise */
+  double* loo_per_step;        /* HOST, m entries or NULL: ||I_k - Q_k^T Q_k||_2, Eq. (9) */
+  int64_t* max_rank_per_call;  /* HOST or NULL: max output rank of each rounding call (sized
+                                  by the Table 1 count) */
+  tt_tensor* householder_u;    /* HOST array of m handles or NULL: Householder TT-vectors */
+} tt_orth_report;
+
+/* ---------------------------------------------------------------- context */
+/* device: CUDA ordinal; stream: a cudaStream_t (NULL = legacy default stream). */
+TT_API tt_status tt_ctx_create(int device, void* stream, tt_ctx* out);
+TT_API tt_status tt_ctx_destroy(tt_ctx ctx);
+TT_API tt_status tt_ctx_set_stream(tt_ctx ctx, void* stream);
+TT_API const char* tt_last_error(tt_ctx ctx);
+TT_API const char* tt_status_string(tt_status s);
+/* Number of this library's kernels launched on ctx so far (evidence for bench.py). */
+TT_API int64_t tt_ctx_launch_count(tt_ctx ctx);
+/* Stream-synchronise ctx. */
+TT_API tt_status tt_ctx_sync(tt_ctx ctx);
+/* Per-kernel-class timing with CUDA events recorded on the ctx stream around every
+ * launch of this library.  enable = 1 starts (and resets) collection, 0 stops it. */
+TT_API tt_status tt_ctx_profile(tt_ctx ctx, int32_t enable);
+/* Class idx (0-based; TT_EINDEX past the end): name (copied into name_buf, NUL-terminated,
+ * truncated to name_len), launches, summed event milliseconds, and the algorithmic flops
+ * and bytes of those launches (the work model of DESIGN.md).  Synchronises the stream. */
+TT_API tt_status tt_ctx_profile_query(tt_ctx ctx, int32_t idx, char* name_buf, int32_t name_len,
+                                      int64_t* launches, double* ms, double* flops, double* bytes);
+
+/* ---------------------------------------------------------------- tensors */
+/* View of a library tensor: pointers stay valid until tt_tensor_free. */
+TT_API tt_status tt_tensor_view(tt_tensor t, tt_view* out);
+TT_API tt_status tt_tensor_free(tt_ctx ctx, tt_tensor t);
+/* Copy a host TT (view with HOST core pointers) to a new device tensor. */
+TT_API tt_status tt_upload(tt_ctx ctx, const tt_view* host, tt_tensor* out);
+/* Copy a device tensor to caller host buffers host_cores[k] (sized r_{k-1} n_k r_k). */
+TT_API tt_status tt_download(tt_ctx ctx, tt_tensor t, double* const* host_cores);
+
+/* ---------------------------------------------------------------- TT algebra */
+/* x = sum_{l<K} coeff[l] terms[l], materialised (ranks add; first cores
+ * concatenated horizontally with c_l applied, interior block-diagonal, last vertical).
+ * coeff: HOST. */
+TT_API tt_status tt_sum(tt_ctx ctx, int32_t K, const double* coeff, const tt_view* terms, tt_tensor* out);
+/* out = alpha x + y. */
+TT_API tt_status tt_axpy(tt_ctx ctx, double alpha, const tt_view* x, const tt_view* y, tt_tensor* out);
+/* out_dev[p] = <x[p], y[p]> for p < P (PAPER.md:19 Euclidean dot through the contraction;
+ * W_k = sum_i X_k(i)^T W_{k-1} Y_k(i)).  out_dev: DEVICE, P doubles. */
+TT_API tt_status tt_dot_batch(tt_ctx ctx, int32_t P, const tt_view* x, const tt_view* y, double* out_dev);
+/* G(i,j) = <a_i, a_j> (Alg. 5 lines 2-6, Eq. (3)); G_dev: DEVICE m*m row-major, symmetric. */
+TT_API tt_status tt_gram(tt_ctx ctx, int32_t m, const tt_view* a, double* G_dev);
+/* Pair blocks of the Gram matrix for sharding: blk (HOST) holds nblk quadruples
+ * (i0, j0, bi, bj); block b writes bi*bj doubles <a_{i0+s}, a_{j0+t}> row-major (s,t)
+ * at packed_dev + sum of previous block sizes.  packed_dev: DEVICE. */
+TT_API tt_status tt_gram_blocks(tt_ctx ctx, int32_t m, const tt_view* a, int32_t nblk,
+                         const int32_t* blk, double* packed_dev);
+/* out_dev[t] = x(phi(lin_idx[t])) = <x, e_{lin_idx[t]}>;
+ * lin_idx: HOST, 1-based psi order.  TT_EINDEX if out of range. */
+TT_API tt_status tt_element(tt_ctx ctx, const tt_view* x, int32_t nidx, const int64_t* lin_idx, double* out_dev);
+/* ||x|| via the right-to-left QR sweep (||C_1||_F), synchronises. */
+TT_API tt_status tt_norm(tt_ctx ctx, const tt_view* x, double* out_host);
+
+/* ---------------------------------------------------------------- TT-rounding */
+/* out = TT-round(sum_{l<K} coeff[l] terms[l], opts) (Oseledets'
+ * right-to-left Householder QR sweep then left-to-right truncated SVD).
+ * The TT-sum is never materialised: block-diagonal cores are read in-kernel.
+ * coeff: HOST.  info may be NULL.  Output: cores 1..d-1 left-orthonormal, core d carries
+ * the norm.  ||x|| = 0 gives a rank-1 zero tensor; d = 1 returns the summed core. */
+TT_API tt_status tt_round(tt_ctx ctx, int32_t K, const double* coeff, const tt_view* terms,
+                   const tt_round_opts* opts, tt_tensor* out, tt_round_info* info);
+/* B independent roundings (C4): item b rounds sum_{l<K[b]} coeff[b][l] terms[b][l].
+ * K, coeff, terms: HOST arrays of length B.  out: HOST array of B handles.
+ * ranks_out: HOST B*(d+1) or NULL. */
+TT_API tt_status tt_round_batch(tt_ctx ctx, int32_t B, const int32_t* K, const double* const* coeff,
+                         const tt_view* const* terms, const tt_round_opts* opts,
+                         tt_tensor* out, int64_t* ranks_out);
+
+/* ---------------------------------------------------------------- drivers */
+/* Q, R = TT-<kind>(A, delta) (Algs. 1-5, 8).  q_out: HOST array of m
+ * handles (library-owned results).  R_host: m*m row-major upper triangular, R(j,i) =
+ * coefficient of q_j in a_i.  report may be NULL.  Returns TT_ELINDEP /
+ * TT_ESINGULAR_GRAM with report->fail_index on breakdown. */
+TT_API tt_status tt_orth(tt_ctx ctx, tt_orth_kind kind, int32_t m, const tt_view* a,
+                  const tt_orth_opts* opts, tt_tensor* q_out, double* R_host,
+                  tt_orth_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_B200_H */

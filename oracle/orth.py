@@ -42,6 +42,9 @@ class OrthResult:
     infos: List[RoundInfo] = field(default_factory=list)
     U: List[Optional[TT]] = field(default_factory=list)   # Householder vectors
     coeffs: List[np.ndarray] = field(default_factory=list)  # per rounding: the sum's coefficients
+    terms: List[list] = field(default_factory=list)         # per rounding (lazy form): the sum's terms
+    outputs: List[TT] = field(default_factory=list)         # per rounding (lazy form): its output
+    term_norms: List[list] = field(default_factory=list)    # per rounding (lazy form): ||y_l|| used in s(x)
 
     def loo_per_step(self) -> np.ndarray:
         """LOO_k = ||I_k - Q_k^T Q_k||_2 over prefixes."""
@@ -51,6 +54,15 @@ class OrthResult:
             for j in range(i + 1):
                 G[i, j] = G[j, i] = tt_dot(self.Q[i], self.Q[j])
         return np.array([loo(G[:k, :k]) for k in range(1, m + 1)])
+
+
+def _record(res: "OrthResult", terms, coefs, norms, out, info) -> None:
+    res.rounding_calls += 1
+    res.infos.append(info)
+    res.coeffs.append(np.array(coefs))
+    res.terms.append(list(terms))
+    res.term_norms.append(list(norms))
+    res.outputs.append(out)
 
 
 def _last_core_norm(p: TT) -> float:
@@ -147,12 +159,9 @@ def gs_lazy(A: Sequence[TT], delta: float, kind: str, floor_c: float = DEFAULT_F
             terms = [base] + Q[:i]
             coefs = [1.0] + list(-c)
             scale = base_norm + float(np.sum(np.abs(c)))
-            out, info = tt_round_sum(terms, coefs, delta, floor_c=floor_c,
-                                     term_norms=[base_norm] + [1.0] * i)
-            info.scale = scale
-            res.rounding_calls += 1
-            res.infos.append(info)
-            res.coeffs.append(np.array(coefs))
+            tn = [base_norm] + [1.0] * i
+            out, info = tt_round_sum(terms, coefs, delta, floor_c=floor_c, term_norms=tn)
+            _record(res, terms, coefs, tn, out, info)
             base = out
             base_norm = _last_core_norm(out)
         nrm = base_norm
@@ -201,9 +210,11 @@ def gram_orth(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLOOR_C,
         else:
             out, info = tt_round_sum(list(A[:i + 1]), coefs, delta, floor_c=floor_c,
                                      term_norms=a_norms[:i + 1])
-        res.rounding_calls += 1
-        res.infos.append(info)
-        res.coeffs.append(np.array(coefs))
+            _record(res, list(A[:i + 1]), coefs, a_norms[:i + 1], out, info)
+        if literal:
+            res.rounding_calls += 1
+            res.infos.append(info)
+            res.coeffs.append(np.array(coefs))
         res.Q.append(out)                                    # Alg. 5 line 12
     return res
 
@@ -322,17 +333,16 @@ def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLO
         s = float(np.sum(r[:i - 1] ** 2))
         terms = [w] + [canonical_tt(j, n) for j in range(1, i)]
         coefs = [1.0] + list(-r[:i - 1])
-        w1, info1 = tt_round_sum(terms, coefs, delta, floor_c=floor_c,
-                                 term_norms=[w_norm] + [1.0] * (i - 1))
+        tn1 = [w_norm] + [1.0] * (i - 1)
+        w1, info1 = tt_round_sum(terms, coefs, delta, floor_c=floor_c, term_norms=tn1)
+        _record(res, terms, coefs, tn1, w1, info1)
         sg = _sign(ew[i - 1])
         beta = np.sqrt(max(w_norm ** 2 - s, 0.0)) if hh_beta == "literal" else _last_core_norm(w1)
         r[i - 1] = sg * beta
         w1n = _last_core_norm(w1)
-        w2, info2 = tt_round_sum([w1, canonical_tt(i, n)], [1.0, -r[i - 1]], delta,
-                                 floor_c=floor_c, term_norms=[w1n, 1.0])
-        res.rounding_calls += 2
-        res.infos += [info1, info2]
-        res.coeffs += [np.array(coefs), np.array([1.0, -r[i - 1]])]
+        t2, c2 = [w1, canonical_tt(i, n)], [1.0, -r[i - 1]]
+        w2, info2 = tt_round_sum(t2, c2, delta, floor_c=floor_c, term_norms=[w1n, 1.0])
+        _record(res, t2, c2, [w1n, 1.0], w2, info2)
         nw = _last_core_norm(w2)
         u = None if nw == 0.0 else _normalise(w2, nw)
         U.append(u)
@@ -351,11 +361,9 @@ def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLO
             live = [l for l in range(i) if U[l] is not None]
             terms = [A[i]] + [U[l] for l in live]
             coefs = [1.0] + [-gamma[i, l] for l in live]
-            w, info = tt_round_sum(terms, coefs, delta, floor_c=floor_c,
-                                   term_norms=[a_norms[i]] + [1.0] * len(live))
-            res.rounding_calls += 1
-            res.infos.append(info)
-            res.coeffs.append(np.array(coefs))
+            tn = [a_norms[i]] + [1.0] * len(live)
+            w, info = tt_round_sum(terms, coefs, delta, floor_c=floor_c, term_norms=tn)
+            _record(res, terms, coefs, tn, w, info)
             w_norm = _last_core_norm(w)
     res.U = U
     for i in range(1, m + 1):
@@ -370,11 +378,8 @@ def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLO
         live = [j for j in range(i, 0, -1) if U[j - 1] is not None]
         terms = [canonical_tt(i, n)] + [U[j - 1] for j in live]
         coefs = [1.0] + [-beta[j - 1] for j in live]
-        q, info = tt_round_sum(terms, coefs, delta, floor_c=floor_c,
-                               term_norms=[1.0] * len(terms))
-        res.rounding_calls += 1
-        res.infos.append(info)
-        res.coeffs.append(np.array(coefs))
+        q, info = tt_round_sum(terms, coefs, delta, floor_c=floor_c, term_norms=[1.0] * len(terms))
+        _record(res, terms, coefs, [1.0] * len(terms), q, info)
         res.Q.append(q)
     return res
 

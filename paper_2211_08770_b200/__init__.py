@@ -1,0 +1,23 @@
+"""B200-native hot path of arXiv 2211.08770 (TT-format orthogonalization).
+
+TT-rounding of rank-inflated TT-sums, batched TT inner products / Gram matrices and the
+six orthogonalization drivers (CGS, MGS, CGS2, MGS2, Gram, Householder), implemented as
+hand-written sm_100a CUDA behind the C ABI of include/tt_b200.h.  This package is the
+binding (argument marshalling) plus the multi-GPU sharding helpers; it never imports the
+CPU oracle and has no CPU fallback.
+"""
+from . import _native  # noqa: F401
+from .api import (  # noqa: F401
+    Context,
+    DeviceTT,
+    LibTT,
+    tt_dot_batch,
+    tt_element,
+    tt_gram,
+    tt_gram_blocks,
+    tt_norm,
+    tt_orth,
+    tt_round,
+    tt_round_batch,
+    tt_sum,
+)

@@ -1,0 +1,291 @@
+"""Thin Python binding over libtt_b200 (same names as include/tt_b200.h).
+
+Argument marshalling only: every arithmetic step runs in the sm_100a kernels of the
+shared library.  torch provides device memory (input cores) and the CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+DEFAULT_FLOOR_C = 2048.0
+
+
+class _CoreArray:
+    """Zero-copy __cuda_array_interface__ over a library-owned core."""
+
+    def __init__(self, ptr: int, shape, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+class Context:
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2211_08770_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+        self.lib = N.load()
+        self.device = device
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        st = self.lib.tt_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if st != 0:
+            raise N.TTError(st, "tt_ctx_create failed")
+        self.handle = h
+
+    def check(self, st: int):
+        if st != 0:
+            raise N.TTError(st, self.lib.tt_last_error(self.handle).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.tt_ctx_launch_count(self.handle))
+
+    def profile(self, enable: bool):
+        self.check(self.lib.tt_ctx_profile(self.handle, int(enable)))
+
+    def profile_report(self) -> dict:
+        """{class: {launches, ms, flops, bytes}} from the event timing of tt_ctx_profile."""
+        out = {}
+        i = 0
+        while True:
+            name = C.create_string_buffer(64)
+            l, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            st = self.lib.tt_ctx_profile_query(self.handle, i, name, 64, C.byref(l), C.byref(ms), C.byref(fl),
+                                               C.byref(by))
+            if st != 0:
+                break
+            out[name.value.decode()] = {"launches": l.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+            i += 1
+        return out
+
+    def sync(self):
+        self.check(self.lib.tt_ctx_sync(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.tt_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceTT:
+    """Caller-owned TT-vector whose cores are torch CUDA float64 tensors (r_{k-1}, n_k, r_k)."""
+
+    def __init__(self, cores: Sequence[torch.Tensor], norm: float = float("nan")):
+        self.cores = [c.contiguous() for c in cores]
+        for c in self.cores:
+            if not (c.is_cuda and c.dtype == torch.float64 and c.dim() == 3):
+                raise ValueError("cores must be 3-D float64 CUDA tensors")
+        self.norm = float(norm)
+
+    @staticmethod
+    def from_numpy(cores: Sequence[np.ndarray], device="cuda", norm: float = float("nan")) -> "DeviceTT":
+        return DeviceTT([torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64)).to(device) for c in cores], norm)
+
+    @property
+    def d(self):
+        return len(self.cores)
+
+    @property
+    def ranks(self):
+        return [self.cores[0].shape[0]] + [c.shape[2] for c in self.cores]
+
+    @property
+    def modes(self):
+        return [c.shape[1] for c in self.cores]
+
+    def _view(self):
+        d = self.d
+        n = (C.c_int64 * d)(*self.modes)
+        r = (C.c_int64 * (d + 1))(*self.ranks)
+        core = (C.c_void_p * d)(*[c.data_ptr() for c in self.cores])
+        v = N.TTView(d, C.cast(n, C.POINTER(C.c_int64)), C.cast(r, C.POINTER(C.c_int64)),
+                     C.cast(core, C.POINTER(C.c_void_p)), self.norm)
+        return v, (n, r, core, self)
+
+    def to_numpy(self) -> List[np.ndarray]:
+        return [c.cpu().numpy() for c in self.cores]
+
+
+class LibTT:
+    """Library-owned TT-vector (result of a rounding / sum); freed with the object."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx = ctx
+        self.handle = handle
+        v = N.TTView()
+        ctx.check(ctx.lib.tt_tensor_view(handle, C.byref(v)))
+        self.d = v.d
+        self.modes = [v.n[k] for k in range(v.d)]
+        self.ranks = [v.r[k] for k in range(v.d + 1)]
+        self.norm = v.norm
+        self._ptrs = [v.core[k] for k in range(v.d)]
+
+    def _view(self):
+        v = N.TTView()
+        self.ctx.check(self.ctx.lib.tt_tensor_view(self.handle, C.byref(v)))
+        return v, (self,)
+
+    def to_numpy(self) -> List[np.ndarray]:
+        shapes = [(self.ranks[k], self.modes[k], self.ranks[k + 1]) for k in range(self.d)]
+        outs = [np.empty(s, dtype=np.float64) for s in shapes]
+        ptrs = (C.c_void_p * self.d)(*[o.ctypes.data for o in outs])
+        self.ctx.check(self.ctx.lib.tt_download(self.ctx.handle, self.handle, ptrs))
+        return outs
+
+    def cores_torch(self) -> List[torch.Tensor]:
+        """Zero-copy torch views of the cores (valid while this object lives)."""
+        out = []
+        for k in range(self.d):
+            shp = (self.ranks[k], self.modes[k], self.ranks[k + 1])
+            out.append(torch.as_tensor(_CoreArray(self._ptrs[k], shp, self), device=f"cuda:{self.ctx.device}"))
+        return out
+
+    def free(self):
+        if self.handle is not None and self.ctx.handle is not None:
+            self.ctx.lib.tt_tensor_free(self.ctx.handle, self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _views(tts):
+    arr = (N.TTView * len(tts))()
+    keep = []
+    for i, t in enumerate(tts):
+        v, k = t._view()
+        arr[i] = v
+        keep.append(k)
+    return arr, keep
+
+
+def _opts(rel_tol, floor_c, max_rank, theta):
+    return N.RoundOpts(float(rel_tol), int(max_rank), float(floor_c), float(theta))
+
+
+# ----------------------------------------------------------------------------- entry points
+def tt_round(ctx: Context, terms, coeffs, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C,
+             max_rank: int = 0, theta: float = 0.5) -> Tuple[LibTT, dict]:
+    arr, keep = _views(terms)
+    cf = (C.c_double * len(terms))(*[float(c) for c in coeffs])
+    o = _opts(rel_tol, floor_c, max_rank, theta)
+    h = C.c_void_p()
+    info = N.RoundInfo()
+    ctx.check(ctx.lib.tt_round(ctx.handle, len(terms), cf, arr, C.byref(o), C.byref(h), C.byref(info)))
+    return LibTT(ctx, h), {"norm": info.norm, "scale": info.scale, "tau": info.tau,
+                           "qrcp_steps": info.qrcp_steps, "resumes": info.resumes}
+
+
+def tt_round_batch(ctx: Context, items, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0,
+                   theta: float = 0.5) -> List[LibTT]:
+    B = len(items)
+    Ks = (C.c_int32 * B)(*[len(t) for t, _ in items])
+    keep = []
+    vptrs = (C.POINTER(N.TTView) * B)()
+    cptrs = (C.POINTER(C.c_double) * B)()
+    for b, (terms, coeffs) in enumerate(items):
+        arr, k = _views(terms)
+        cf = (C.c_double * len(coeffs))(*[float(c) for c in coeffs])
+        keep += [arr, k, cf]
+        vptrs[b] = C.cast(arr, C.POINTER(N.TTView))
+        cptrs[b] = C.cast(cf, C.POINTER(C.c_double))
+    outs = (C.c_void_p * B)()
+    o = _opts(rel_tol, floor_c, max_rank, theta)
+    ctx.check(ctx.lib.tt_round_batch(ctx.handle, B, Ks, cptrs, vptrs, C.byref(o), outs, None))
+    return [LibTT(ctx, C.c_void_p(outs[b])) for b in range(B)]
+
+
+def tt_sum(ctx: Context, terms, coeffs) -> LibTT:
+    arr, keep = _views(terms)
+    cf = (C.c_double * len(terms))(*[float(c) for c in coeffs])
+    h = C.c_void_p()
+    ctx.check(ctx.lib.tt_sum(ctx.handle, len(terms), cf, arr, C.byref(h)))
+    return LibTT(ctx, h)
+
+
+def tt_dot_batch(ctx: Context, xs, ys) -> torch.Tensor:
+    P = len(xs)
+    out = torch.empty(P, dtype=torch.float64, device=f"cuda:{ctx.device}")
+    ax, k1 = _views(xs)
+    ay, k2 = _views(ys)
+    ctx.check(ctx.lib.tt_dot_batch(ctx.handle, P, ax, ay, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def tt_gram(ctx: Context, tensors) -> torch.Tensor:
+    m = len(tensors)
+    G = torch.empty((m, m), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    arr, keep = _views(tensors)
+    ctx.check(ctx.lib.tt_gram(ctx.handle, m, arr, C.c_void_p(G.data_ptr())))
+    return G
+
+
+def tt_gram_blocks(ctx: Context, tensors, blocks: Sequence[Tuple[int, int, int, int]]) -> torch.Tensor:
+    m = len(tensors)
+    total = sum(bi * bj for _, _, bi, bj in blocks)
+    out = torch.empty(max(total, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    flat = (C.c_int32 * (4 * len(blocks)))(*[int(v) for b in blocks for v in b])
+    arr, keep = _views(tensors)
+    ctx.check(ctx.lib.tt_gram_blocks(ctx.handle, m, arr, len(blocks), flat, C.c_void_p(out.data_ptr())))
+    return out[:total]
+
+
+def tt_element(ctx: Context, x, lin_idx: Sequence[int]) -> torch.Tensor:
+    out = torch.empty(len(lin_idx), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    v, keep = x._view()
+    idx = (C.c_int64 * len(lin_idx))(*[int(i) for i in lin_idx])
+    ctx.check(ctx.lib.tt_element(ctx.handle, C.byref(v), len(lin_idx), idx, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def tt_norm(ctx: Context, x) -> float:
+    v, keep = x._view()
+    o = C.c_double()
+    ctx.check(ctx.lib.tt_norm(ctx.handle, C.byref(v), C.byref(o)))
+    return o.value
+
+
+def tt_orth(ctx: Context, kind: str, tensors, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C,
+            theta: float = 0.5, hh_beta_literal: bool = False, want_loo: bool = False,
+            keep_u: bool = False):
+    m = len(tensors)
+    arr, keep = _views(tensors)
+    o = N.OrthOpts(_opts(rel_tol, floor_c, 0, theta), int(hh_beta_literal), int(want_loo))
+    qs = (C.c_void_p * m)()
+    R = np.zeros((m, m), dtype=np.float64)
+    ncalls = {"cgs": m, "mgs": m, "cgs2": 2 * m, "mgs2": 2 * m, "gram": m, "householder": 4 * m - 1}[kind]
+    loo = (C.c_double * m)()
+    ranks = (C.c_int64 * ncalls)()
+    us = (C.c_void_p * m)() if keep_u else None
+    rep = N.OrthReport(0, -1, C.cast(loo, C.POINTER(C.c_double)) if want_loo else None,
+                       C.cast(ranks, C.POINTER(C.c_int64)),
+                       C.cast(us, C.POINTER(C.c_void_p)) if keep_u else None)
+    st = ctx.lib.tt_orth(ctx.handle, N.KINDS[kind], m, arr, C.byref(o), qs,
+                         R.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+    if st != 0:
+        err = N.TTError(st, ctx.lib.tt_last_error(ctx.handle).decode())
+        err.fail_index = rep.fail_index
+        raise err
+    Q = [LibTT(ctx, C.c_void_p(qs[i])) for i in range(m)]
+    report = {"rounding_calls": rep.rounding_calls, "max_rank_per_call": list(ranks[:rep.rounding_calls]),
+              "loo_per_step": np.array(loo[:m]) if want_loo else None}
+    if keep_u:
+        report["u"] = [LibTT(ctx, C.c_void_p(us[i])) if us[i] else None for i in range(m)]
+    return Q, R, report

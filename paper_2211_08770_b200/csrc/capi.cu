@@ -1,0 +1,314 @@
+// extern "C" boundary of libtt_b200 (include/tt_b200.h).  Every entry point converts
+// internal errors into a tt_status plus tt_last_error text; nothing throws across it.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <new>
+
+#include "orth.cuh"
+#include "round.cuh"
+#include "ttops.cuh"
+
+using namespace ttb;
+
+namespace {
+
+template <typename F>
+tt_status guarded(tt_ctx ctx, F f) {
+  try {
+    f();
+    return TT_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.msg;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return TT_ENOMEM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return TT_EINVAL;
+  }
+}
+
+tt_round_opts resolve(const tt_round_opts* o) {
+  tt_round_opts r = default_round_opts();
+  if (o) r = *o;
+  return r;
+}
+
+SumInput sum_of(int K, const double* coeff, const tt_view* terms) {
+  if (K < 1 || !coeff || !terms) fail(TT_EINVAL, "TT-sum needs K >= 1 terms and coefficients");
+  SumInput s;
+  for (int l = 0; l < K; ++l) s.add(terms[l], coeff[l]);
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_ctx_create(int device, void* stream, tt_ctx* out) {
+  if (!out) return TT_EINVAL;
+  *out = nullptr;
+  tt_ctx c = new (std::nothrow) tt_ctx_s();
+  if (!c) return TT_ENOMEM;
+  tt_status st = guarded(c, [&] {
+    TTB_CUDA(cudaSetDevice(device));
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    TTB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    // keep freed pool memory cached across calls (stream-ordered allocator)
+    cudaMemPool_t pool;
+    TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    TTB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  });
+  if (st != TT_OK) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return TT_OK;
+}
+
+tt_status tt_ctx_destroy(tt_ctx ctx) {
+  if (!ctx) return TT_EINVAL;
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  delete ctx;
+  return TT_OK;
+}
+
+tt_status tt_ctx_set_stream(tt_ctx ctx, void* stream) {
+  if (!ctx) return TT_EINVAL;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return TT_OK;
+}
+
+const char* tt_last_error(tt_ctx ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+const char* tt_status_string(tt_status s) {
+  switch (s) {
+    case TT_OK: return "TT_OK";
+    case TT_EINVAL: return "TT_EINVAL";
+    case TT_ESHAPE: return "TT_ESHAPE";
+    case TT_EINDEX: return "TT_EINDEX";
+    case TT_ENOMEM: return "TT_ENOMEM";
+    case TT_ECUDA: return "TT_ECUDA";
+    case TT_ENOCONV: return "TT_ENOCONV";
+    case TT_ESINGULAR_GRAM: return "TT_ESINGULAR_GRAM";
+    case TT_ELINDEP: return "TT_ELINDEP";
+    case TT_ENUMDEFECT: return "TT_ENUMDEFECT";
+    case TT_ENOTSUP: return "TT_ENOTSUP";
+  }
+  return "unknown";
+}
+
+int64_t tt_ctx_launch_count(tt_ctx ctx) { return ctx ? ctx->launches : -1; }
+
+tt_status tt_ctx_sync(tt_ctx ctx) {
+  return guarded(ctx, [&] { TTB_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+tt_status tt_ctx_profile(tt_ctx ctx, int32_t enable) {
+  if (!ctx) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    if (enable) prof_reset(ctx);
+    else prof_resolve(ctx);
+    ctx->prof = enable != 0;
+  });
+}
+
+tt_status tt_ctx_profile_query(tt_ctx ctx, int32_t idx, char* name_buf, int32_t name_len, int64_t* launches,
+                               double* ms, double* flops, double* bytes) {
+  if (!ctx) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    prof_resolve(ctx);
+    if (idx < 0 || idx >= (int32_t)ctx->prof_cls.size()) fail(TT_EINDEX, "no such profile class");
+    const TTProfEntry& e = ctx->prof_cls[(size_t)idx];
+    if (name_buf && name_len > 0) {
+      std::strncpy(name_buf, e.name.c_str(), (size_t)name_len - 1);
+      name_buf[name_len - 1] = 0;
+    }
+    if (launches) *launches = e.launches;
+    if (ms) *ms = e.ms;
+    if (flops) *flops = e.flops;
+    if (bytes) *bytes = e.bytes;
+  });
+}
+
+tt_status tt_tensor_view(tt_tensor t, tt_view* out) {
+  if (!t || !out) return TT_EINVAL;
+  out->d = t->d;
+  out->n = t->n.data();
+  out->r = t->r.data();
+  out->core = t->core_c.data();
+  out->norm = t->norm;
+  return TT_OK;
+}
+
+tt_status tt_tensor_free(tt_ctx ctx, tt_tensor t) {
+  if (!ctx) return TT_EINVAL;
+  if (!t) return TT_OK;
+  tensor_free(ctx, t);
+  return TT_OK;
+}
+
+tt_status tt_upload(tt_ctx ctx, const tt_view* host, tt_tensor* out) {
+  if (!ctx || !host || !out) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    TTShape s = view_shape(*host);
+    tt_tensor t = tensor_alloc(ctx, s.d, s.n, s.r);
+    for (int k = 0; k < s.d; ++k)
+      TTB_CUDA(cudaMemcpyAsync(t->core[(size_t)k], host->core[k], sizeof(double) * (size_t)(s.r[k] * s.n[k] * s.r[k + 1]),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    t->norm = host->norm;
+    *out = t;
+  });
+}
+
+tt_status tt_download(tt_ctx ctx, tt_tensor t, double* const* host_cores) {
+  if (!ctx || !t || !host_cores) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    for (int k = 0; k < t->d; ++k)
+      TTB_CUDA(cudaMemcpyAsync(host_cores[k], t->core[(size_t)k],
+                               sizeof(double) * (size_t)(t->r[(size_t)k] * t->n[(size_t)k] * t->r[(size_t)k + 1]),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+tt_status tt_sum(tt_ctx ctx, int32_t K, const double* coeff, const tt_view* terms, tt_tensor* out) {
+  if (!ctx || !out) return TT_EINVAL;
+  return guarded(ctx, [&] { *out = materialise_sum(ctx, sum_of(K, coeff, terms)); });
+}
+
+tt_status tt_axpy(tt_ctx ctx, double alpha, const tt_view* x, const tt_view* y, tt_tensor* out) {
+  if (!ctx || !x || !y || !out) return TT_EINVAL;
+  tt_view t[2] = {*x, *y};
+  double c[2] = {alpha, 1.0};
+  return tt_sum(ctx, 2, c, t, out);
+}
+
+tt_status tt_dot_batch(tt_ctx ctx, int32_t P, const tt_view* x, const tt_view* y, double* out_dev) {
+  if (!ctx || P < 0 || (P > 0 && (!x || !y || !out_dev))) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    std::vector<TTRef> X, Y;
+    for (int p = 0; p < P; ++p) { X.push_back(TTRef::of(x[p])); Y.push_back(TTRef::of(y[p])); }
+    std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+    for (int p = 0; p < P; ++p) pr.push_back({&X[(size_t)p], &Y[(size_t)p]});
+    dots_device(ctx, pr, out_dev);
+  });
+}
+
+tt_status tt_gram_blocks(tt_ctx ctx, int32_t m, const tt_view* a, int32_t nblk, const int32_t* blk, double* packed_dev) {
+  if (!ctx || m < 1 || !a || nblk < 0 || (nblk > 0 && (!blk || !packed_dev))) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    std::vector<TTRef> A;
+    for (int i = 0; i < m; ++i) A.push_back(TTRef::of(a[i]));
+    std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+    for (int b = 0; b < nblk; ++b) {
+      const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
+      if (i0 < 0 || j0 < 0 || bi < 0 || bj < 0 || i0 + bi > m || j0 + bj > m) fail(TT_EINDEX, "Gram block out of range");
+      for (int s = 0; s < bi; ++s)
+        for (int t = 0; t < bj; ++t) pr.push_back({&A[(size_t)(i0 + s)], &A[(size_t)(j0 + t)]});
+    }
+    dots_device(ctx, pr, packed_dev);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void gram_unpack_kernel(const double* __restrict__ packed, int m, double* G) {
+  // packed holds the lower triangle row by row (i >= j)
+  const int64_t total = (int64_t)m * (m + 1) / 2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
+    int ii = i;
+    while ((int64_t)ii * (ii + 1) / 2 > t) --ii;
+    while ((int64_t)(ii + 1) * (ii + 2) / 2 <= t) ++ii;
+    const int j = (int)(t - (int64_t)ii * (ii + 1) / 2);
+    const double v = packed[t];
+    G[(int64_t)ii * m + j] = v;
+    G[(int64_t)j * m + ii] = v;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+tt_status tt_gram(tt_ctx ctx, int32_t m, const tt_view* a, double* G_dev) {
+  if (!ctx || m < 1 || !a || !G_dev) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    std::vector<TTRef> A;
+    for (int i = 0; i < m; ++i) A.push_back(TTRef::of(a[i]));
+    std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j <= i; ++j) pr.push_back({&A[(size_t)i], &A[(size_t)j]});
+    DBuf packed(ctx, pr.size());
+    dots_device(ctx, pr, packed.p);
+    const int blocks = (int)std::min<int64_t>(ceil_div((int64_t)pr.size(), 256), 1024);
+    TTB_RUN(ctx, "aux", 0, 16.0 * pr.size(), gram_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(packed.p, m, G_dev));
+  });
+}
+
+tt_status tt_element(tt_ctx ctx, const tt_view* x, int32_t nidx, const int64_t* lin_idx, double* out_dev) {
+  if (!ctx || !x || nidx < 0 || (nidx > 0 && (!lin_idx || !out_dev))) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    TTRef t = TTRef::of(*x);
+    int64_t total = 1;
+    for (int64_t v : t.n) total *= v;
+    std::vector<int64_t> idx;
+    for (int q = 0; q < nidx; ++q) {
+      const int64_t l = lin_idx[q];
+      if (l < 1 || l > total) fail(TT_EINDEX, "element index out of range 1..prod(n) (SPEC.md:145)");
+      int64_t rem = l - 1;
+      for (int k = 0; k < t.d; ++k) { idx.push_back(rem % t.n[(size_t)k]); rem /= t.n[(size_t)k]; }
+    }
+    elements(ctx, t.d, t.n, t.core, t.r, idx, nidx, out_dev);
+  });
+}
+
+tt_status tt_norm(tt_ctx ctx, const tt_view* x, double* out_host) {
+  if (!ctx || !x || !out_host) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    double c = 1.0;
+    *out_host = sweep_norm(ctx, sum_of(1, &c, x));
+  });
+}
+
+tt_status tt_round(tt_ctx ctx, int32_t K, const double* coeff, const tt_view* terms, const tt_round_opts* opts,
+                   tt_tensor* out, tt_round_info* info) {
+  if (!ctx || !out) return TT_EINVAL;
+  return guarded(ctx, [&] { *out = round_sum(ctx, sum_of(K, coeff, terms), resolve(opts), info); });
+}
+
+tt_status tt_round_batch(tt_ctx ctx, int32_t B, const int32_t* K, const double* const* coeff,
+                         const tt_view* const* terms, const tt_round_opts* opts, tt_tensor* out, int64_t* ranks_out) {
+  if (!ctx || B < 0 || (B > 0 && (!K || !coeff || !terms || !out))) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    const tt_round_opts o = resolve(opts);
+    int done = 0;
+    try {
+      for (int b = 0; b < B; ++b) {
+        out[b] = round_sum(ctx, sum_of(K[b], coeff[b], terms[b]), o, nullptr);
+        if (ranks_out) std::memcpy(ranks_out + (size_t)b * (out[b]->d + 1), out[b]->r.data(), sizeof(int64_t) * (out[b]->d + 1));
+        ++done;
+      }
+    } catch (...) {
+      for (int b = 0; b < done; ++b) { tensor_free(ctx, out[b]); out[b] = nullptr; }
+      throw;
+    }
+  });
+}
+
+tt_status tt_orth(tt_ctx ctx, tt_orth_kind kind, int32_t m, const tt_view* a, const tt_orth_opts* opts,
+                  tt_tensor* q_out, double* R_host, tt_orth_report* report) {
+  if (!ctx) return TT_EINVAL;
+  tt_orth_opts o;
+  if (opts) o = *opts;
+  else { o.round = default_round_opts(); o.hh_beta_literal = 0; o.want_loo = 0; }
+  return guarded(ctx, [&] { orth_run(ctx, kind, m, a, o, q_out, R_host, report); });
+}
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+#include <cstring>
+#include <sstream>
+
+#include "common.cuh"
+
+namespace ttb {
+
+void fail(tt_status s, const std::string& msg) { throw Error{s, msg}; }
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  std::ostringstream os;
+  os << "CUDA error '" << cudaGetErrorString(e) << "' in " << what << " at " << file << ":" << line;
+  fail(e == cudaErrorMemoryAllocation ? TT_ENOMEM : TT_ECUDA, os.str());
+}
+
+void DBuf::alloc(tt_ctx c, size_t n) {
+  release();
+  ctx = c;
+  count = n;
+  if (n == 0) return;
+  void* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, n * sizeof(double), c->stream);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    fail(TT_ENOMEM, "device allocation of " + std::to_string(n * 8) + " bytes failed");
+  }
+  p = static_cast<double*>(q);
+}
+
+void DBuf::release() {
+  if (p && ctx) cudaFreeAsync(p, ctx->stream);
+  p = nullptr;
+  count = 0;
+}
+
+void IBuf::alloc(tt_ctx c, size_t n) {
+  release();
+  ctx = c;
+  count = n;
+  if (n == 0) return;
+  void* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, n * sizeof(int), c->stream);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    fail(TT_ENOMEM, "device allocation failed");
+  }
+  p = static_cast<int*>(q);
+}
+
+void IBuf::release() {
+  if (p && ctx) cudaFreeAsync(p, ctx->stream);
+  p = nullptr;
+  count = 0;
+}
+
+void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
+  if (p && ctx) cudaFreeAsync(p, ctx->stream);
+  ctx = c;
+  p = nullptr;
+  if (bytes == 0) return;
+  cudaError_t e = cudaMallocAsync(&p, bytes, c->stream);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    p = nullptr;
+    fail(TT_ENOMEM, "descriptor allocation failed");
+  }
+  TTB_CUDA(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, c->stream));
+}
+
+static cudaEvent_t pool_event(tt_ctx ctx) {
+  if (!ctx->prof_pool.empty()) {
+    cudaEvent_t e = ctx->prof_pool.back();
+    ctx->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  TTB_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+int prof_begin(tt_ctx ctx) {
+  if (!ctx->prof) return -1;
+  TTProfPending p;
+  p.start = pool_event(ctx);
+  p.stop = pool_event(ctx);
+  p.cls = -1;
+  p.flops = p.bytes = 0.0;
+  TTB_CUDA(cudaEventRecord(p.start, ctx->stream));
+  ctx->prof_pending.push_back(p);
+  return (int)ctx->prof_pending.size() - 1;
+}
+
+void prof_end(tt_ctx ctx, int token, const char* cls, double flops, double bytes) {
+  if (token < 0 || !ctx->prof) return;
+  TTProfPending& p = ctx->prof_pending[(size_t)token];
+  TTB_CUDA(cudaEventRecord(p.stop, ctx->stream));
+  int idx = -1;
+  for (size_t i = 0; i < ctx->prof_cls.size(); ++i)
+    if (ctx->prof_cls[i].name == cls) { idx = (int)i; break; }
+  if (idx < 0) {
+    ctx->prof_cls.push_back(TTProfEntry{cls});
+    idx = (int)ctx->prof_cls.size() - 1;
+  }
+  p.cls = idx;
+  p.flops = flops;
+  p.bytes = bytes;
+  if (ctx->prof_pending.size() > 4096) prof_resolve(ctx);
+}
+
+void prof_resolve(tt_ctx ctx) {
+  if (ctx->prof_pending.empty()) return;
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (TTProfPending& p : ctx->prof_pending) {
+    if (p.cls >= 0) {
+      float ms = 0.f;
+      TTB_CUDA(cudaEventElapsedTime(&ms, p.start, p.stop));
+      TTProfEntry& e = ctx->prof_cls[(size_t)p.cls];
+      e.launches++;
+      e.ms += ms;
+      e.flops += p.flops;
+      e.bytes += p.bytes;
+    }
+    ctx->prof_pool.push_back(p.start);
+    ctx->prof_pool.push_back(p.stop);
+  }
+  ctx->prof_pending.clear();
+}
+
+void prof_reset(tt_ctx ctx) {
+  prof_resolve(ctx);
+  ctx->prof_cls.clear();
+}
+
+static void ensure_pinned(tt_ctx ctx, size_t bytes) {
+  if (ctx->h_pinned_bytes >= bytes) return;
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  size_t b = bytes < 4096 ? 4096 : bytes;
+  TTB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_pinned), b));
+  ctx->h_pinned_bytes = b;
+}
+
+void d2h_small(tt_ctx ctx, double* host, const double* dev, size_t n) {
+  if (n == 0) return;
+  ensure_pinned(ctx, n * sizeof(double));
+  TTB_CUDA(cudaMemcpyAsync(ctx->h_pinned, dev, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(host, ctx->h_pinned, n * sizeof(double));
+}
+
+void d2h_small_int(tt_ctx ctx, int* host, const int* dev, size_t n) {
+  if (n == 0) return;
+  ensure_pinned(ctx, n * sizeof(int));
+  TTB_CUDA(cudaMemcpyAsync(ctx->h_pinned, dev, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(host, ctx->h_pinned, n * sizeof(int));
+}
+
+tt_tensor tensor_alloc(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& r) {
+  tt_tensor t = new tt_tensor_s();
+  t->d = d;
+  t->n = n;
+  t->r = r;
+  size_t total = 0;
+  for (int k = 0; k < d; ++k) total += (size_t)(r[k] * n[k] * r[k + 1]);
+  void* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, (total ? total : 1) * sizeof(double), ctx->stream);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    delete t;
+    fail(TT_ENOMEM, "tensor allocation failed");
+  }
+  t->block = static_cast<double*>(q);
+  t->core.resize(d);
+  t->core_c.resize(d);
+  size_t off = 0;
+  for (int k = 0; k < d; ++k) {
+    t->core[k] = t->block + off;
+    t->core_c[k] = t->core[k];
+    off += (size_t)(r[k] * n[k] * r[k + 1]);
+  }
+  return t;
+}
+
+void tensor_free(tt_ctx ctx, tt_tensor t) {
+  if (!t) return;
+  if (t->block) cudaFreeAsync(t->block, ctx->stream);
+  delete t;
+}
+
+TTShape view_shape(const tt_view& v) {
+  if (v.d < 1) fail(TT_EINVAL, "TT order d must be >= 1");
+  if (!v.n || !v.r || !v.core) fail(TT_EINVAL, "null shape/core pointer in tt_view");
+  TTShape s;
+  s.d = v.d;
+  s.n.assign(v.n, v.n + v.d);
+  s.r.assign(v.r, v.r + v.d + 1);
+  if (s.r[0] != 1 || s.r[v.d] != 1) fail(TT_ESHAPE, "boundary ranks must be r_0 = r_d = 1 (PAPER.md:45)");
+  for (int k = 0; k < v.d; ++k) {
+    if (s.n[k] < 1 || s.r[k] < 1 || s.r[k + 1] < 1) fail(TT_ESHAPE, "mode sizes and ranks must be >= 1");
+    if (!v.core[k]) fail(TT_EINVAL, "null core pointer");
+  }
+  return s;
+}
+
+}  // namespace ttb

@@ -1,0 +1,504 @@
+// Orthogonalization drivers (PAPER.md Algs. 1-8) on top of the GPU TT-rounding and
+// TT-dot kernels.  Running TT-sums are kept as coefficients over stored tensors and
+// materialised (rounded) only at the paper's rounding points; the counts are exactly
+// Table 1's (m, m, 2m, 2m, m, 4m-1).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "orth.cuh"
+#include "ttops.cuh"
+
+namespace ttb {
+
+TTRef TTRef::of(const tt_view& v) {
+  TTShape s = view_shape(v);
+  TTRef t;
+  t.d = s.d;
+  t.n = s.n;
+  t.r = s.r;
+  t.core.assign(v.core, v.core + v.d);
+  t.norm = v.norm;
+  return t;
+}
+
+TTRef TTRef::of(tt_tensor x) {
+  TTRef t;
+  t.d = x->d;
+  t.n = x->n;
+  t.r = x->r;
+  t.core = x->core_c;
+  t.norm = x->norm;
+  return t;
+}
+
+void dots_device(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs, double* out_dev) {
+  if (pairs.empty()) return;
+  DotBatch b;
+  b.d = pairs[0].first->d;
+  b.n = pairs[0].first->n;
+  b.P = (int)pairs.size();
+  for (auto& pr : pairs) {
+    const TTRef& x = *pr.first;
+    const TTRef& y = *pr.second;
+    if (x.d != b.d || y.d != b.d || x.n != b.n || y.n != b.n) fail(TT_ESHAPE, "TT-dot operands differ in shape");
+    b.xc.insert(b.xc.end(), x.core.begin(), x.core.end());
+    b.yc.insert(b.yc.end(), y.core.begin(), y.core.end());
+    b.xr.insert(b.xr.end(), x.r.begin(), x.r.end());
+    b.yr.insert(b.yr.end(), y.r.begin(), y.r.end());
+  }
+  dot_batch(ctx, b, out_dev);
+}
+
+std::vector<double> dots_host(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs) {
+  std::vector<double> h(pairs.size(), 0.0);
+  if (pairs.empty()) return h;
+  DBuf o(ctx, pairs.size());
+  dots_device(ctx, pairs, o.p);
+  d2h_small(ctx, h.data(), o.p, pairs.size());
+  return h;
+}
+
+int cholesky_host(std::vector<double>& G, int m) {
+  // symmetrise, then L in the lower triangle (row-major)
+  std::vector<double> L((size_t)m * m, 0.0);
+  for (int j = 0; j < m; ++j) {
+    double s = 0.5 * (G[(size_t)j * m + j] + G[(size_t)j * m + j]);
+    for (int k = 0; k < j; ++k) s -= L[(size_t)j * m + k] * L[(size_t)j * m + k];
+    if (!(s > 0.0)) return j;
+    L[(size_t)j * m + j] = std::sqrt(s);
+    for (int i = j + 1; i < m; ++i) {
+      double t = 0.5 * (G[(size_t)i * m + j] + G[(size_t)j * m + i]);
+      for (int k = 0; k < j; ++k) t -= L[(size_t)i * m + k] * L[(size_t)j * m + k];
+      L[(size_t)i * m + j] = t / L[(size_t)j * m + j];
+    }
+  }
+  G = L;
+  return -1;
+}
+
+// eigenvalues of a small symmetric matrix by cyclic Jacobi (host)
+static std::vector<double> sym_eig(std::vector<double> A, int n) {
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += A[(size_t)i * n + j] * A[(size_t)i * n + j];
+        if (i != j) off += A[(size_t)i * n + j] * A[(size_t)i * n + j];
+      }
+    if (off <= 1e-36 * tot || off == 0.0) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A[(size_t)p * n + q];
+        if (apq == 0.0) continue;
+        const double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::hypot(1.0, theta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
+        for (int k = 0; k < n; ++k) {
+          const double akp = A[(size_t)k * n + p], akq = A[(size_t)k * n + q];
+          A[(size_t)k * n + p] = c * akp - s * akq;
+          A[(size_t)k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = A[(size_t)p * n + k], aqk = A[(size_t)q * n + k];
+          A[(size_t)p * n + k] = c * apk - s * aqk;
+          A[(size_t)q * n + k] = s * apk + c * aqk;
+        }
+      }
+  }
+  std::vector<double> ev((size_t)n);
+  for (int i = 0; i < n; ++i) ev[(size_t)i] = A[(size_t)i * n + i];
+  return ev;
+}
+
+double loo_host(const std::vector<double>& Gq, int m, int k) {
+  // ||I_k - Q_k^T Q_k||_2, Eq. (9): largest |eigenvalue| of the symmetrised defect
+  std::vector<double> D((size_t)k * k);
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j)
+      D[(size_t)i * k + j] = (i == j ? 1.0 : 0.0) - 0.5 * (Gq[(size_t)i * m + j] + Gq[(size_t)j * m + i]);
+  std::vector<double> ev = sym_eig(D, k);
+  double mx = 0.0;
+  for (double v : ev) mx = std::max(mx, std::fabs(v));
+  return mx;
+}
+
+tt_tensor make_canonical(tt_ctx ctx, const std::vector<int64_t>& n, int64_t lin1) {
+  const int d = (int)n.size();
+  int64_t total = 1;
+  for (int64_t v : n) total *= v;
+  if (lin1 < 1 || lin1 > total) fail(TT_EINDEX, "canonical index out of range (PAPER.md:337)");
+  tt_tensor t = tensor_alloc(ctx, d, n, std::vector<int64_t>((size_t)d + 1, 1));
+  int64_t sz = 0;
+  for (int64_t v : n) sz += v;
+  std::vector<double> h((size_t)sz, 0.0);
+  int64_t rem = lin1 - 1, off = 0;
+  for (int k = 0; k < d; ++k) {
+    h[(size_t)(off + rem % n[(size_t)k])] = 1.0;
+    rem /= n[(size_t)k];
+    off += n[(size_t)k];
+  }
+  TTB_CUDA(cudaMemcpyAsync(t->block, h.data(), sizeof(double) * (size_t)sz, cudaMemcpyHostToDevice, ctx->stream));
+  t->norm = 1.0;
+  return t;
+}
+
+namespace {
+
+struct Owned {  // RAII for library tensors produced inside a driver
+  tt_ctx ctx;
+  tt_tensor t = nullptr;
+  explicit Owned(tt_ctx c, tt_tensor x = nullptr) : ctx(c), t(x) {}
+  ~Owned() { if (t) tensor_free(ctx, t); }
+  tt_tensor release() { tt_tensor x = t; t = nullptr; return x; }
+  void reset(tt_tensor x) { if (t) tensor_free(ctx, t); t = x; }
+};
+
+double last_core_norm(tt_ctx ctx, tt_tensor t) {
+  const int d = t->d;
+  const int64_t n = t->r[(size_t)d - 1] * t->n[(size_t)d - 1] * t->r[(size_t)d];
+  DBuf s(ctx, 1);
+  sumsq(ctx, t->core[(size_t)d - 1], n, s.p);
+  double h = 0.0;
+  d2h_small(ctx, &h, s.p, 1);
+  return std::sqrt(h);
+}
+
+void scale_last_core(tt_ctx ctx, tt_tensor t, double a) {
+  const int d = t->d;
+  scale_inplace(ctx, t->core[(size_t)d - 1], t->r[(size_t)d - 1] * t->n[(size_t)d - 1] * t->r[(size_t)d], a);
+}
+
+int64_t max_rank(tt_tensor t) {
+  int64_t m = 1;
+  for (int64_t v : t->r) m = std::max(m, v);
+  return m;
+}
+
+struct Ledger {
+  int64_t calls = 0;
+  std::vector<int64_t> max_ranks;
+  tt_tensor round(tt_ctx ctx, const SumInput& in, const tt_round_opts& o) {
+    tt_tensor t = round_sum(ctx, in, o, nullptr);
+    ++calls;
+    max_ranks.push_back(max_rank(t));
+    return t;
+  }
+};
+
+void add_ref(SumInput& s, const TTRef& x, double c) {
+  tt_view v;
+  v.d = x.d;
+  v.n = x.n.data();
+  v.r = x.r.data();
+  v.core = x.core.data();
+  v.norm = x.norm;
+  s.add(v, c);
+}
+
+std::vector<int64_t> phi0(const std::vector<int64_t>& n, int64_t lin1) {
+  std::vector<int64_t> idx(n.size());
+  int64_t rem = lin1 - 1;
+  for (size_t k = 0; k < n.size(); ++k) {
+    idx[k] = rem % n[k];
+    rem /= n[k];
+  }
+  return idx;
+}
+
+std::vector<double> elements_host(tt_ctx ctx, const TTRef& x, const std::vector<int64_t>& lins) {
+  std::vector<int64_t> idx;
+  for (int64_t l : lins) {
+    std::vector<int64_t> v = phi0(x.n, l);
+    idx.insert(idx.end(), v.begin(), v.end());
+  }
+  DBuf o(ctx, lins.size());
+  elements(ctx, x.d, x.n, x.core, x.r, idx, (int)lins.size(), o.p);
+  std::vector<double> h(lins.size());
+  d2h_small(ctx, h.data(), o.p, lins.size());
+  return h;
+}
+
+// ----------------------------------------------------------------- Gram-Schmidt family
+void run_gs(tt_ctx ctx, tt_orth_kind kind, int m, const std::vector<TTRef>& A, const std::vector<double>& an,
+            const tt_orth_opts& o, std::vector<tt_tensor>& Q, std::vector<double>& R, std::vector<double>& GQ,
+            Ledger& led, int* fail_index) {
+  const int passes = (kind == TT_CGS2 || kind == TT_MGS2) ? 2 : 1;
+  const bool modified = (kind == TT_MGS || kind == TT_MGS2);
+  std::vector<TTRef> QR;  // refs of finished q's
+  for (int i = 0; i < m; ++i) {
+    TTRef base = A[(size_t)i];
+    base.norm = an[(size_t)i];
+    Owned prev(ctx);
+    for (int ps = 0; ps < passes; ++ps) {
+      std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+      for (int j = 0; j < i; ++j) pr.push_back({&base, &QR[(size_t)j]});
+      std::vector<double> dbq = dots_host(ctx, pr);
+      std::vector<double> c((size_t)i, 0.0);
+      for (int j = 0; j < i; ++j) {
+        double v = dbq[(size_t)j];
+        if (modified)
+          for (int l = 0; l < j; ++l) v -= c[(size_t)l] * GQ[(size_t)l * m + j];
+        c[(size_t)j] = v;
+        R[(size_t)j * m + i] += v;  // R = R_1 + R_2 (Algs. 3-4, last line)
+      }
+      SumInput s;
+      add_ref(s, base, 1.0);
+      for (int j = 0; j < i; ++j) add_ref(s, QR[(size_t)j], -c[(size_t)j]);
+      tt_tensor p = led.round(ctx, s, o.round);
+      const double pn = last_core_norm(ctx, p);
+      p->norm = pn;
+      prev.reset(p);
+      base = TTRef::of(p);
+    }
+    const double nrm = base.norm;
+    if (nrm <= 1e3 * U_ROUND * an[(size_t)i]) {
+      *fail_index = i;
+      fail(TT_ELINDEP, "linear dependence at step " + std::to_string(i) + " (SPEC.md:473)");
+    }
+    R[(size_t)i * m + i] = nrm;
+    tt_tensor q = prev.release();
+    scale_last_core(ctx, q, 1.0 / nrm);  // q_i = p / R(i,i)
+    q->norm = 1.0;
+    Q.push_back(q);
+    QR.push_back(TTRef::of(q));
+    if (modified || o.want_loo) {
+      std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+      for (int j = 0; j <= i; ++j) pr.push_back({&QR[(size_t)j], &QR[(size_t)i]});
+      std::vector<double> g = dots_host(ctx, pr);
+      for (int j = 0; j <= i; ++j) GQ[(size_t)j * m + i] = GQ[(size_t)i * m + j] = g[(size_t)j];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- Gram (Alg. 5)
+void run_gram(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::vector<double>& an, const tt_orth_opts& o,
+              std::vector<tt_tensor>& Q, std::vector<double>& R, Ledger& led, int* fail_index) {
+  std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j <= i; ++j) pr.push_back({&A[(size_t)i], &A[(size_t)j]});
+  std::vector<double> g = dots_host(ctx, pr);
+  std::vector<double> G((size_t)m * m);
+  size_t t = 0;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j <= i; ++j, ++t) G[(size_t)i * m + j] = G[(size_t)j * m + i] = g[t];
+  int piv = cholesky_host(G, m);
+  if (piv >= 0) {
+    *fail_index = piv;
+    fail(TT_ESINGULAR_GRAM, "Cholesky of the Gram matrix failed at pivot " + std::to_string(piv) +
+                                " (numerically singular, PAPER.md:224-226)");
+  }
+  // R = L^T, R^{-1} by back substitution (Remark 3)
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) R[(size_t)i * m + j] = (j >= i) ? G[(size_t)j * m + i] : 0.0;
+  std::vector<double> X((size_t)m * m, 0.0);
+  for (int j = 0; j < m; ++j) {
+    X[(size_t)j * m + j] = 1.0 / R[(size_t)j * m + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1; k <= j; ++k) s += R[(size_t)i * m + k] * X[(size_t)k * m + j];
+      X[(size_t)i * m + j] = -s / R[(size_t)i * m + i];
+    }
+  }
+  for (int i = 0; i < m; ++i) {
+    SumInput s;
+    for (int k = 0; k <= i; ++k) {
+      TTRef a = A[(size_t)k];
+      a.norm = an[(size_t)k];
+      add_ref(s, a, X[(size_t)k * m + i]);  // q_i = sum_k R^{-1}(k,i) a_k (A5)
+    }
+    tt_tensor q = led.round(ctx, s, o.round);
+    q->norm = last_core_norm(ctx, q);
+    Q.push_back(q);
+  }
+}
+
+// ----------------------------------------------------------------- Householder (Algs. 6-8)
+void run_householder(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::vector<double>& an,
+                     const tt_orth_opts& o, std::vector<tt_tensor>& Q, std::vector<double>& R, Ledger& led,
+                     std::vector<tt_tensor>& Uout, int* fail_index) {
+  const std::vector<int64_t>& n = A[0].n;
+  std::vector<std::unique_ptr<Owned>> E;  // canonical e_1..e_m
+  std::vector<TTRef> ER;
+  for (int j = 1; j <= m; ++j) {
+    E.emplace_back(new Owned(ctx, make_canonical(ctx, n, j)));
+    ER.push_back(TTRef::of(E.back()->t));
+  }
+  std::vector<tt_tensor> U((size_t)m, nullptr);
+  std::vector<TTRef> UR((size_t)m);
+  std::vector<double> GU((size_t)m * m, 0.0), gamma((size_t)m * m, 0.0);
+  Owned wown(ctx);
+  TTRef w = A[0];
+  w.norm = an[0];
+  for (int i = 1; i <= m; ++i) {
+    // TTH-vec(w, {e_1..e_i}) with element reads <w, e_j> = w(phi(j))
+    std::vector<int64_t> lins;
+    for (int j = 1; j <= i; ++j) lins.push_back(j);
+    std::vector<double> ew = elements_host(ctx, w, lins);
+    std::vector<double> r((size_t)i, 0.0);
+    double s = 0.0;
+    for (int j = 0; j < i - 1; ++j) { r[(size_t)j] = ew[(size_t)j]; s += r[(size_t)j] * r[(size_t)j]; }
+    SumInput s1;
+    add_ref(s1, w, 1.0);
+    for (int j = 0; j < i - 1; ++j) add_ref(s1, ER[(size_t)j], -r[(size_t)j]);
+    Owned w1(ctx, led.round(ctx, s1, o.round));                 // Alg. 6 line 9
+    const double w1n = last_core_norm(ctx, w1.t);
+    w1.t->norm = w1n;
+    const double sg = (ew[(size_t)i - 1] >= 0.0) ? 1.0 : -1.0;  // sign(0) = +1 (A8)
+    double beta;
+    if (o.hh_beta_literal) {
+      const double d2 = w.norm * w.norm - s;
+      if (d2 < -1e-12 * w.norm * w.norm) {
+        *fail_index = i - 1;
+        fail(TT_ENUMDEFECT, "||a||^2 - s < 0 in TTH-vec (SPEC.md:436)");
+      }
+      beta = std::sqrt(std::max(d2, 0.0));
+    } else {
+      beta = w1n;  // A9
+    }
+    r[(size_t)i - 1] = sg * beta;
+    SumInput s2;
+    add_ref(s2, TTRef::of(w1.t), 1.0);
+    add_ref(s2, ER[(size_t)i - 1], -r[(size_t)i - 1]);
+    Owned w2(ctx, led.round(ctx, s2, o.round));                 // Alg. 6 line 12
+    const double nw = last_core_norm(ctx, w2.t);
+    for (int j = 0; j < i; ++j) R[(size_t)j * m + (i - 1)] = r[(size_t)j];
+    if (nw > 0.0) {
+      scale_last_core(ctx, w2.t, 1.0 / nw);                     // u = w / ||w|| (A7)
+      w2.t->norm = 1.0;
+      U[(size_t)i - 1] = w2.release();
+      UR[(size_t)i - 1] = TTRef::of(U[(size_t)i - 1]);
+      std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+      for (int p = 0; p < i; ++p)
+        if (U[(size_t)p]) pr.push_back({&UR[(size_t)p], &UR[(size_t)i - 1]});
+      std::vector<double> g = dots_host(ctx, pr);
+      size_t t = 0;
+      for (int p = 0; p < i; ++p)
+        if (U[(size_t)p]) { GU[(size_t)p * m + i - 1] = GU[(size_t)(i - 1) * m + p] = g[t++]; }
+      // gamma_{j,i} = 2(<a_j, u_i> - sum_{p<i} gamma_{j,p} <u_p, u_i>) for j > i
+      std::vector<std::pair<const TTRef*, const TTRef*>> pa;
+      for (int j = i + 1; j <= m; ++j) pa.push_back({&A[(size_t)j - 1], &UR[(size_t)i - 1]});
+      std::vector<double> da = dots_host(ctx, pa);
+      for (int j = i + 1; j <= m; ++j) {
+        double v = da[(size_t)(j - i - 1)];
+        for (int p = 0; p < i - 1; ++p) v -= gamma[(size_t)(j - 1) * m + p] * GU[(size_t)p * m + i - 1];
+        gamma[(size_t)(j - 1) * m + i - 1] = 2.0 * v;
+      }
+    }
+    if (i < m) {                                                 // Alg. 8 lines 9-11
+      SumInput sw;
+      TTRef a = A[(size_t)i];
+      a.norm = an[(size_t)i];
+      add_ref(sw, a, 1.0);
+      for (int l = 0; l < i; ++l)
+        if (U[(size_t)l]) add_ref(sw, UR[(size_t)l], -gamma[(size_t)i * m + l]);
+      wown.reset(led.round(ctx, sw, o.round));
+      wown.t->norm = last_core_norm(ctx, wown.t);
+      w = TTRef::of(wown.t);
+    }
+  }
+  // phase 2: q_i = round(e_i - sum_{j<=i} beta_ij u_j) (Alg. 8 lines 13-19)
+  std::vector<double> EU((size_t)m * m, 0.0);  // EU[j*m + i] = u_j(phi(i))
+  for (int j = 0; j < m; ++j) {
+    if (!U[(size_t)j]) continue;
+    std::vector<int64_t> lins;
+    for (int i = j; i < m; ++i) lins.push_back(i + 1);
+    std::vector<double> e = elements_host(ctx, UR[(size_t)j], lins);
+    for (int i = j; i < m; ++i) EU[(size_t)j * m + i] = e[(size_t)(i - j)];
+  }
+  for (int i = 1; i <= m; ++i) {
+    std::vector<double> bt((size_t)m, 0.0);
+    for (int j = i; j >= 1; --j) {
+      if (!U[(size_t)j - 1]) continue;
+      double v = EU[(size_t)(j - 1) * m + (i - 1)];
+      for (int l = j + 1; l <= i; ++l) v -= bt[(size_t)l - 1] * GU[(size_t)(l - 1) * m + (j - 1)];
+      bt[(size_t)j - 1] = 2.0 * v;
+    }
+    SumInput sq;
+    add_ref(sq, ER[(size_t)i - 1], 1.0);
+    for (int j = i; j >= 1; --j)
+      if (U[(size_t)j - 1]) add_ref(sq, UR[(size_t)j - 1], -bt[(size_t)j - 1]);
+    tt_tensor q = led.round(ctx, sq, o.round);
+    q->norm = last_core_norm(ctx, q);
+    Q.push_back(q);
+  }
+  Uout = U;
+  (void)fail_index;
+}
+
+}  // namespace
+
+tt_status orth_run(tt_ctx ctx, tt_orth_kind kind, int m, const tt_view* a, const tt_orth_opts& o, tt_tensor* q_out,
+                   double* R_host, tt_orth_report* rep) {
+  if (m < 1 || !a || !q_out || !R_host) fail(TT_EINVAL, "tt_orth: bad arguments");
+  std::vector<TTRef> A;
+  for (int i = 0; i < m; ++i) {
+    A.push_back(TTRef::of(a[i]));
+    if (A.back().d != A[0].d || A.back().n != A[0].n) fail(TT_ESHAPE, "tt_orth: inputs differ in shape");
+  }
+  // ||a_i|| from one batched TT-dot
+  std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+  for (int i = 0; i < m; ++i) pr.push_back({&A[(size_t)i], &A[(size_t)i]});
+  std::vector<double> an2 = dots_host(ctx, pr);
+  std::vector<double> an((size_t)m);
+  for (int i = 0; i < m; ++i) an[(size_t)i] = std::sqrt(std::max(an2[(size_t)i], 0.0));
+  std::vector<tt_tensor> Q, U;
+  std::vector<double> R((size_t)m * m, 0.0), GQ((size_t)m * m, 0.0);
+  Ledger led;
+  int fidx = -1;
+  if (rep) rep->fail_index = -1;
+  try {
+    switch (kind) {
+      case TT_CGS: case TT_MGS: case TT_CGS2: case TT_MGS2:
+        run_gs(ctx, kind, m, A, an, o, Q, R, GQ, led, &fidx);
+        break;
+      case TT_GRAM:
+        run_gram(ctx, m, A, an, o, Q, R, led, &fidx);
+        break;
+      case TT_HOUSEHOLDER:
+        run_householder(ctx, m, A, an, o, Q, R, led, U, &fidx);
+        break;
+      default:
+        fail(TT_EINVAL, "unknown orthogonalization kind");
+    }
+  } catch (...) {
+    for (tt_tensor t : Q) tensor_free(ctx, t);
+    for (tt_tensor t : U) if (t) tensor_free(ctx, t);
+    if (rep) { rep->fail_index = fidx; rep->rounding_calls = led.calls; }
+    throw;
+  }
+  std::memcpy(R_host, R.data(), sizeof(double) * (size_t)m * m);
+  for (int i = 0; i < m; ++i) q_out[i] = Q[(size_t)i];
+  if (rep) {
+    rep->rounding_calls = led.calls;
+    if (rep->max_rank_per_call)
+      std::memcpy(rep->max_rank_per_call, led.max_ranks.data(), sizeof(int64_t) * led.max_ranks.size());
+    if (rep->loo_per_step) {
+      bool have = (kind == TT_MGS || kind == TT_MGS2 || ((kind == TT_CGS || kind == TT_CGS2) && o.want_loo));
+      if (!have) {
+        std::vector<TTRef> QR;
+        for (tt_tensor t : Q) QR.push_back(TTRef::of(t));
+        std::vector<std::pair<const TTRef*, const TTRef*>> pq;
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j <= i; ++j) pq.push_back({&QR[(size_t)i], &QR[(size_t)j]});
+        std::vector<double> g = dots_host(ctx, pq);
+        size_t t = 0;
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j <= i; ++j, ++t) GQ[(size_t)i * m + j] = GQ[(size_t)j * m + i] = g[t];
+      }
+      for (int k = 1; k <= m; ++k) rep->loo_per_step[k - 1] = loo_host(GQ, m, k);
+    }
+    if (rep->householder_u) {
+      for (int i = 0; i < m; ++i) rep->householder_u[i] = (i < (int)U.size()) ? U[(size_t)i] : nullptr;
+    } else {
+      for (tt_tensor t : U) if (t) tensor_free(ctx, t);
+    }
+  } else {
+    for (tt_tensor t : U) if (t) tensor_free(ctx, t);
+  }
+  return TT_OK;
+}
+
+}  // namespace ttb

@@ -1,0 +1,521 @@
+// Householder QR kernels (FP64, sm_100a).
+//
+//  * tsqr_leaf_kernel   : one CTA factors a <=256-row chunk of a <=32-column panel in
+//                         shared memory (LAPACK dgeqr2 arithmetic), writes its R to the
+//                         stack of the next tree level and its explicit Q.
+//  * tsqr_combine_kernel: Q_panel(chunk p) = Q_leaf(chunk p) * Q_next(p-th w x w block).
+//  * hr_kernel          : Householder reconstruction (LU with sign choice of Q_1 - S) so the
+//                         TSQR panel becomes compact-WY (Y, T) with H[:, :w] = Q S, R_h = S R.
+//  * qrcp_kernel        : unblocked Householder QR with column pivoting and a Frobenius
+//                         stopping test (truncated-SVD stage of the left-to-right sweep).
+#include <algorithm>
+
+#include "gemm.cuh"
+#include "qr.cuh"
+
+namespace ttb {
+
+namespace {
+
+constexpr int LEAF_THREADS = 256;
+
+// In-smem Householder QR of the h x w column-major matrix S (ld = ldh).
+__device__ void smem_geqr2(double* S, int ldh, int h, int w, double* tau, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int kmax = min(h, w);
+  for (int j = 0; j < kmax; ++j) {
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < h; i += blockDim.x) {
+      const double v = S[j * ldh + i];
+      part += v * v;
+    }
+    const double sigma = block_sum(part, red);
+    const double alpha = S[j * ldh + j];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (sigma != 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = j + 1 + tid; i < h; i += blockDim.x) S[j * ldh + i] *= scal;
+    __syncthreads();
+    if (tid == 0) {
+      S[j * ldh + j] = beta;
+      tau[j] = t;
+    }
+    if (t != 0.0) {
+      for (int c = j + 1 + warp; c < w; c += nw) {
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < h; i += 32) s += S[j * ldh + i] * S[c * ldh + i];
+        s = warp_sum(s);
+        s = t * (s + S[c * ldh + j]);
+        for (int i = j + 1 + lane; i < h; i += 32) S[c * ldh + i] -= s * S[j * ldh + i];
+        __syncwarp();
+        if (lane == 0) S[c * ldh + j] -= s;
+      }
+    }
+    __syncthreads();
+  }
+  for (int j = kmax + tid; j < w; j += blockDim.x) tau[j] = 0.0;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(LEAF_THREADS) tsqr_leaf_kernel(const double* __restrict__ A, int64_t lda, int m,
+                                                                 int w, int P, double* Qout, int64_t ldq,
+                                                                 double* Rst, int64_t ldr) {
+  extern __shared__ double sm[];
+  const int p = blockIdx.x;
+  const int base = m / P, rem = m % P;
+  const int r0 = p * base + min(p, rem);
+  const int h = base + (p < rem ? 1 : 0);
+  double* S = sm;
+  double* Qs = sm + (size_t)h * w;
+  double* tau = Qs + (size_t)h * w;
+  double* red = tau + 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int idx = tid; idx < h * w; idx += blockDim.x) {
+    const int col = idx / h, row = idx - col * h;
+    S[idx] = A[(int64_t)(r0 + row) + (int64_t)col * lda];
+    Qs[idx] = (row == col) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  smem_geqr2(S, h, h, w, tau, red);
+  // R_p (w x w upper) -> rows [p*w, p*w + w) of the next level's stack
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    const int col = idx / w, row = idx - col * w;
+    Rst[(int64_t)(p * w + row) + (int64_t)col * ldr] = (row <= col && row < h) ? S[col * h + row] : 0.0;
+  }
+  // explicit Q_p = H_0 ... H_{w-1} [I; 0]
+  for (int j = min(h, w) - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t != 0.0) {
+      for (int c = j + warp; c < w; c += nw) {
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < h; i += 32) s += S[j * h + i] * Qs[c * h + i];
+        s = warp_sum(s);
+        s = t * (s + Qs[c * h + j]);
+        for (int i = j + 1 + lane; i < h; i += 32) Qs[c * h + i] -= s * S[j * h + i];
+        __syncwarp();
+        if (lane == 0) Qs[c * h + j] -= s;
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < h * w; idx += blockDim.x) {
+    const int col = idx / h, row = idx - col * h;
+    Qout[(int64_t)(r0 + row) + (int64_t)col * ldq] = Qs[idx];
+  }
+}
+
+__global__ void __launch_bounds__(256) tsqr_combine_kernel(const double* __restrict__ Ql, int64_t ldl,
+                                                           const double* __restrict__ QS, int64_t lds, int m, int w,
+                                                           int P, double* Qout, int64_t ldq) {
+  __shared__ double Bs[32 * 33];
+  const int p = blockIdx.x;
+  const int base = m / P, rem = m % P;
+  const int r0 = p * base + min(p, rem);
+  const int h = base + (p < rem ? 1 : 0);
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    const int c = idx / w, k = idx - c * w;
+    Bs[c * 33 + k] = QS[(int64_t)(p * w + k) + (int64_t)c * lds];
+  }
+  __syncthreads();
+  for (int row = threadIdx.x; row < h; row += blockDim.x) {
+    double a[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) a[k] = (k < w) ? Ql[(int64_t)(r0 + row) + (int64_t)k * ldl] : 0.0;
+    for (int c = 0; c < w; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) s += a[k] * Bs[c * 33 + k];
+      Qout[(int64_t)(r0 + row) + (int64_t)c * ldq] = s;
+    }
+  }
+}
+
+// Householder reconstruction (Ballard et al.): find S = diag(+-1), unit-lower Y_1 and upper
+// U with Q_1 - S = ... such that [I; 0] - Q S = Y U (LU without pivoting, |U_jj| >= 1),
+// Y_2 = -Q_2 S U^{-1}, T = U Y_1^{-T}; then I - Y T Y^T has first columns Q S, R_h = S R.
+__global__ void __launch_bounds__(256) hr_kernel(const double* __restrict__ Q, int64_t ldq, int m, int w,
+                                                 const double* __restrict__ Rp, int64_t ldrp, double* Y,
+                                                 int64_t ldy, double* T, int64_t ldt, double* Rh, int64_t ldrh) {
+  __shared__ double Ls[32][33], Us[32][33], Ss[32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {
+    for (int j = 0; j < w; ++j) {
+      double z = (lane < w) ? Q[lane + (int64_t)j * ldq] : 0.0;
+      for (int k = 0; k < j; ++k) {
+        const double zk = __shfl_sync(0xffffffffu, z, k);
+        if (lane > k && lane < w) z -= Ls[lane][k] * zk;
+      }
+      const double zj = __shfl_sync(0xffffffffu, z, j);
+      const double s = (zj >= 0.0) ? -1.0 : 1.0;  // pivot 1 + |z_j| >= 1
+      const double ujj = 1.0 - s * zj;
+      if (lane < j) { Us[lane][j] = -s * z; Ls[lane][j] = 0.0; }
+      if (lane == j) { Us[j][j] = ujj; Ls[j][j] = 1.0; Ss[j] = s; }
+      if (lane > j && lane < w) { Ls[lane][j] = (-s * z) / ujj; Us[lane][j] = 0.0; }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + tid; i < m; i += gridDim.x * blockDim.x) {
+    if (i < w) {
+      for (int j = 0; j < w; ++j) Y[i + (int64_t)j * ldy] = Ls[i][j];
+    } else {
+      double y[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < w) {
+          double acc = -Ss[j] * Q[i + (int64_t)j * ldq];
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (k < j) acc -= y[k] * Us[k][j];
+          y[j] = acc / Us[j][j];
+          Y[i + (int64_t)j * ldy] = y[j];
+        } else {
+          y[j] = 0.0;
+        }
+      }
+    }
+  }
+  if (blockIdx.x == 0 && tid < 32) {
+    // row `lane` of T: T[i,j] = U[i,j] - sum_{k<j} T[i,k] Y1[j,k]
+    double trow[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      double t = 0.0;
+      if (j < w && lane < w) {
+        t = Us[lane][j];
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < j) t -= trow[k] * Ls[j][k];
+      }
+      trow[j] = t;
+    }
+    if (lane < w)
+      for (int j = 0; j < w; ++j) T[lane + (int64_t)j * ldt] = (j >= lane) ? trow[j] : 0.0;
+  }
+  if (blockIdx.x == 0) {
+    for (int idx = tid; idx < w * w; idx += blockDim.x) {
+      const int c = idx / w, r = idx - c * w;
+      if (r <= c) Rh[r + (int64_t)c * ldrh] = Ss[r] * Rp[r + (int64_t)c * ldrp];
+    }
+  }
+}
+
+__global__ void copy_upper_kernel(const double* A, int64_t lda, int rows, int cols, double* R, int64_t ldr) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % rows), c = (int)(idx / rows);
+    R[r + (int64_t)c * ldr] = (r <= c) ? A[r + (int64_t)c * lda] : 0.0;
+  }
+}
+
+__global__ void set_identity_kernel(double* Q, int64_t ldq, int m, int k) {
+  const int64_t total = (int64_t)m * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % m), c = (int)(idx / m);
+    Q[r + (int64_t)c * ldq] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+int grid_for(int64_t n, int threads, int cap = 4096) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), cap));
+}
+
+// Recursive TSQR of the m x w matrix A (w <= 32): explicit Q (m x w) and R (w x w, ld w).
+void tsqr(tt_ctx ctx, const double* A, int64_t lda, int64_t m, int w, double* Qout, int64_t ldq, double* Rout) {
+  const size_t smem_leaf = (size_t)(2 * QR_LEAF * 32 + 64) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    TTB_CUDA(cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf));
+    attr_set = true;
+  }
+  if (m <= QR_LEAF) {
+    const size_t sm = (size_t)(2 * m * w + 64) * sizeof(double);
+    TTB_RUN(ctx, "tsqr_leaf", 4.0 * m * w * w, 16.0 * m * w,
+            tsqr_leaf_kernel<<<1, LEAF_THREADS, sm, ctx->stream>>>(A, lda, (int)m, w, 1, Qout, ldq, Rout, w));
+    return;
+  }
+  const int P = (int)ceil_div(m, QR_LEAF);
+  const int64_t ms = (int64_t)P * w;
+  DBuf Qleaf(ctx, (size_t)m * w), S(ctx, (size_t)ms * w), QS(ctx, (size_t)ms * w);
+  const int hmax = (int)ceil_div(m, P);
+  const size_t sm = (size_t)(2 * hmax * w + 64) * sizeof(double);
+  TTB_RUN(ctx, "tsqr_leaf", 4.0 * m * w * w, 16.0 * m * w + 8.0 * ms * w,
+          tsqr_leaf_kernel<<<P, LEAF_THREADS, sm, ctx->stream>>>(A, lda, (int)m, w, P, Qleaf.p, m, S.p, ms));
+  tsqr(ctx, S.p, ms, ms, w, QS.p, ms, Rout);
+  TTB_RUN(ctx, "tsqr_combine", 2.0 * m * w * w, 16.0 * m * w + 8.0 * ms * w,
+          tsqr_combine_kernel<<<P, 256, 0, ctx->stream>>>(Qleaf.p, m, QS.p, ms, (int)m, w, P, Qout, ldq));
+}
+
+// ---------------------------------------------------------------- QRCP
+__global__ void __launch_bounds__(1024) qrcp_kernel(double* Y, int64_t ldy, int m, int c, int k_start, double stop2,
+                                                    int kcap, double* tau, double* norms_g, int* perm_g,
+                                                    double* scalars) {
+  extern __shared__ double sm[];
+  double* nrm = sm;
+  double* nrm0 = sm + c;
+  int* perm = reinterpret_cast<int*>(sm + 2 * c);
+  __shared__ double red[32];
+  __shared__ double redv[32];
+  __shared__ int redi[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+
+  if (k_start == 0) {
+    for (int j = warp; j < c; j += nw) {
+      double s = 0.0;
+      for (int i = lane; i < m; i += 32) { const double v = Y[i + (int64_t)j * ldy]; s += v * v; }
+      s = warp_sum(s);
+      if (lane == 0) { nrm[j] = s; nrm0[j] = s; perm[j] = j; }
+    }
+  } else {
+    for (int j = tid; j < c; j += blockDim.x) { nrm[j] = norms_g[j]; nrm0[j] = norms_g[c + j]; perm[j] = perm_g[j]; }
+  }
+  __syncthreads();
+  const int kmax = min(min(m, c), kcap);
+  int s = k_start;
+  for (; s < kmax; ++s) {
+    double part = 0.0;
+    for (int j = s + tid; j < c; j += blockDim.x) part += nrm[j];
+    double tot = block_sum(part, red);
+    if (tot <= 4.0 * stop2 || s == k_start) {
+      // exact recomputation of the trailing column norms (rows >= s)
+      for (int j = s + warp; j < c; j += nw) {
+        double q = 0.0;
+        for (int i = s + lane; i < m; i += 32) { const double v = Y[i + (int64_t)j * ldy]; q += v * v; }
+        q = warp_sum(q);
+        if (lane == 0) { nrm[j] = q; nrm0[j] = q; }
+      }
+      __syncthreads();
+      part = 0.0;
+      for (int j = s + tid; j < c; j += blockDim.x) part += nrm[j];
+      tot = block_sum(part, red);
+    }
+    if (tot <= stop2) break;
+    // pivot: argmax_{j >= s} nrm[j], ties -> smallest j
+    double bv = -1.0;
+    int bi = c;
+    for (int j = s + tid; j < c; j += blockDim.x) {
+      const double v = nrm[j];
+      if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { redv[warp] = bv; redi[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+      bv = (lane < nw) ? redv[lane] : -1.0;
+      bi = (lane < nw) ? redi[lane] : c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) redi[0] = bi;
+    }
+    __syncthreads();
+    const int pv = redi[0];
+    __syncthreads();
+    if (pv != s) {
+      for (int i = tid; i < m; i += blockDim.x) {
+        const double a = Y[i + (int64_t)s * ldy];
+        Y[i + (int64_t)s * ldy] = Y[i + (int64_t)pv * ldy];
+        Y[i + (int64_t)pv * ldy] = a;
+      }
+      if (tid == 0) {
+        double t = nrm[s]; nrm[s] = nrm[pv]; nrm[pv] = t;
+        t = nrm0[s]; nrm0[s] = nrm0[pv]; nrm0[pv] = t;
+        const int q = perm[s]; perm[s] = perm[pv]; perm[pv] = q;
+      }
+      __syncthreads();
+    }
+    // Householder vector of column s (rows s..m-1), LAPACK dlarfg
+    double pp = 0.0;
+    for (int i = s + 1 + tid; i < m; i += blockDim.x) { const double v = Y[i + (int64_t)s * ldy]; pp += v * v; }
+    const double sigma = block_sum(pp, red);
+    const double alpha = Y[s + (int64_t)s * ldy];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (sigma != 0.0) {
+      const double nr = sqrt(alpha * alpha + sigma);
+      beta = alpha >= 0.0 ? -nr : nr;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = s + 1 + tid; i < m; i += blockDim.x) Y[i + (int64_t)s * ldy] *= scal;
+    __syncthreads();
+    if (tid == 0) { Y[s + (int64_t)s * ldy] = beta; tau[s] = t; }
+    // apply to the trailing columns and downdate their norms
+    for (int j = s + 1 + warp; j < c; j += nw) {
+      double* col = Y + (int64_t)j * ldy;
+      if (t != 0.0) {
+        double q = 0.0;
+        for (int i = s + 1 + lane; i < m; i += 32) q += Y[i + (int64_t)s * ldy] * col[i];
+        q = warp_sum(q);
+        q = t * (q + col[s]);
+        for (int i = s + 1 + lane; i < m; i += 32) col[i] -= q * Y[i + (int64_t)s * ldy];
+        __syncwarp();
+        if (lane == 0) col[s] -= q;
+        __syncwarp();
+      }
+      const double rs = col[s];
+      double nn = nrm[j] - rs * rs;
+      if (!(nn > 1e-8 * nrm0[j])) {
+        double q = 0.0;
+        for (int i = s + 1 + lane; i < m; i += 32) { const double v = col[i]; q += v * v; }
+        q = warp_sum(q);
+        nn = q;
+        if (lane == 0) nrm0[j] = q;
+      }
+      __syncwarp();
+      if (lane == 0) nrm[j] = nn;
+    }
+    __syncthreads();
+  }
+  // exact trailing mass
+  double part = 0.0;
+  for (int j = s + warp; j < c; j += nw)
+    for (int i = s + lane; i < m; i += 32) { const double v = Y[i + (int64_t)j * ldy]; part += v * v; }
+  const double e2 = block_sum(part, red);
+  for (int j = tid; j < c; j += blockDim.x) { norms_g[j] = nrm[j]; norms_g[c + j] = nrm0[j]; perm_g[j] = perm[j]; }
+  if (tid == 0) { scalars[0] = (double)s; scalars[1] = e2; }
+}
+
+__global__ void __launch_bounds__(1024) apply_reflectors_kernel(const double* __restrict__ Y, int64_t ldy,
+                                                                const double* __restrict__ tau, int m, int k,
+                                                                double* X, int64_t ldx, int nc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = k - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t != 0.0) {
+      for (int c = warp; c < nc; c += nw) {
+        double* col = X + (int64_t)c * ldx;
+        double q = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) q += Y[i + (int64_t)j * ldy] * col[i];
+        q = warp_sum(q);
+        q = t * (q + col[j]);
+        for (int i = j + 1 + lane; i < m; i += 32) col[i] -= q * Y[i + (int64_t)j * ldy];
+        __syncwarp();
+        if (lane == 0) col[j] -= q;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void copy_upper(tt_ctx ctx, const double* A, int64_t lda, int64_t rows, int64_t cols, double* R, int64_t ldr) {
+  if (rows <= 0 || cols <= 0) return;
+  TTB_RUN(ctx, "aux", 0, 16.0 * rows * cols,
+          copy_upper_kernel<<<grid_for(rows * cols, 256), 256, 0, ctx->stream>>>(A, lda, (int)rows, (int)cols, R, ldr));
+}
+
+void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& f) {
+  f.m = m;
+  f.c = c;
+  f.kmax = std::min(m, c);
+  if (f.kmax <= 0) return;
+  f.Y.alloc(ctx, (size_t)m * f.kmax);
+  f.T.alloc(ctx, (size_t)QR_NB * f.kmax);
+  DBuf Qp(ctx, (size_t)m * QR_NB), Rp(ctx, (size_t)QR_NB * QR_NB);
+  DBuf W(ctx, (size_t)QR_NB * std::max<int64_t>(c, 1)), W2(ctx, (size_t)QR_NB * std::max<int64_t>(c, 1));
+  // rows above the panel inside Y must read as zero for the explicit-Y GEMMs
+  TTB_CUDA(cudaMemsetAsync(f.Y.p, 0, sizeof(double) * (size_t)m * f.kmax, ctx->stream));
+  for (int64_t s = 0; s < f.kmax; s += QR_NB) {
+    const int w = (int)std::min<int64_t>(QR_NB, f.kmax - s);
+    const int64_t ms = m - s;
+    double* P = A + s + s * lda;
+    tsqr(ctx, P, lda, ms, w, Qp.p, ms, Rp.p);
+    double* Yp = f.Y.p + s + s * m;
+    double* Tp = f.T.p + s * QR_NB;
+    TTB_RUN(ctx, "householder_reconstruct", 1.0 * ms * w * w, 16.0 * ms * w,
+            hr_kernel<<<grid_for(ms, 256, 1024), 256, 0, ctx->stream>>>(Qp.p, ms, (int)ms, w, Rp.p, w, Yp, m, Tp, QR_NB, P,
+                                                                lda));
+    const int64_t n2 = c - s - w;
+    if (n2 > 0) {
+      double* C = A + s + (s + w) * lda;
+      GemmDesc g1;  // W = Y^T C
+      g1.M = w; g1.N = n2; g1.K = ms; g1.A = Yp; g1.lda = m; g1.ta = true; g1.B = C; g1.ldb = lda; g1.C = W.p; g1.ldc = w;
+      gemm(ctx, g1);
+      GemmDesc g2;  // W2 = T^T W
+      g2.M = w; g2.N = n2; g2.K = w; g2.A = Tp; g2.lda = QR_NB; g2.ta = true; g2.B = W.p; g2.ldb = w; g2.C = W2.p; g2.ldc = w;
+      gemm(ctx, g2);
+      GemmDesc g3;  // C -= Y W2
+      g3.M = ms; g3.N = n2; g3.K = w; g3.A = Yp; g3.lda = m; g3.B = W2.p; g3.ldb = w; g3.C = C; g3.ldc = lda;
+      g3.alpha = -1.0; g3.beta = 1.0;
+      gemm(ctx, g3);
+    }
+  }
+}
+
+void orgqr(tt_ctx ctx, const QRFactors& f, double* Q, int64_t ldq) {
+  const int64_t m = f.m, kq = f.kmax;
+  if (kq <= 0) return;
+  TTB_RUN(ctx, "aux", 0, 8.0 * m * kq,
+          set_identity_kernel<<<grid_for(m * kq, 256), 256, 0, ctx->stream>>>(Q, ldq, (int)m, (int)kq));
+  DBuf W(ctx, (size_t)QR_NB * kq), W2(ctx, (size_t)QR_NB * kq);
+  const int64_t npan = ceil_div(kq, QR_NB);
+  for (int64_t pnl = npan - 1; pnl >= 0; --pnl) {
+    const int64_t s = pnl * QR_NB;
+    const int w = (int)std::min<int64_t>(QR_NB, kq - s);
+    const int64_t ms = m - s, ncols = kq - s;
+    const double* Yp = f.Y.p + s + s * m;
+    const double* Tp = f.T.p + s * QR_NB;
+    double* E = Q + s + s * ldq;
+    GemmDesc g1;  // W = Y^T E
+    g1.M = w; g1.N = ncols; g1.K = ms; g1.A = Yp; g1.lda = m; g1.ta = true; g1.B = E; g1.ldb = ldq; g1.C = W.p; g1.ldc = w;
+    gemm(ctx, g1);
+    GemmDesc g2;  // W2 = T W
+    g2.M = w; g2.N = ncols; g2.K = w; g2.A = Tp; g2.lda = QR_NB; g2.B = W.p; g2.ldb = w; g2.C = W2.p; g2.ldc = w;
+    gemm(ctx, g2);
+    GemmDesc g3;  // E -= Y W2
+    g3.M = ms; g3.N = ncols; g3.K = w; g3.A = Yp; g3.lda = m; g3.B = W2.p; g3.ldb = w; g3.C = E; g3.ldc = ldq;
+    g3.alpha = -1.0; g3.beta = 1.0;
+    gemm(ctx, g3);
+  }
+}
+
+void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int64_t c) {
+  (void)Y; (void)ldy;
+  st.m = m;
+  st.c = c;
+  st.tau.alloc(ctx, (size_t)std::max<int64_t>(c, 1));
+  st.norms.alloc(ctx, (size_t)2 * std::max<int64_t>(c, 1));
+  st.perm.alloc(ctx, (size_t)std::max<int64_t>(c, 1));
+  st.scalars.alloc(ctx, 2);
+  st.k = 0;
+  st.e2 = 0.0;
+}
+
+void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, int kcap) {
+  const size_t smem = (size_t)st.c * (2 * sizeof(double) + sizeof(int)) + 16;
+  if (smem > 200 * 1024) fail(TT_ENOTSUP, "QRCP: too many columns for the shared-memory norm cache");
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    TTB_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024 + 64)));
+    attr = 200 * 1024 + 64;
+  }
+  TTB_RUN(ctx, "qrcp", 0, 16.0 * st.m * st.c,
+          qrcp_kernel<<<1, 1024, smem, ctx->stream>>>(Y, ldy, (int)st.m, (int)st.c, st.k, stop2, kcap, st.tau.p, st.norms.p,
+                                              st.perm.p, st.scalars.p));
+  double h[2];
+  d2h_small(ctx, h, st.scalars.p, 2);
+  st.k = (int)h[0];
+  st.e2 = h[1];
+}
+
+void apply_reflectors_left(tt_ctx ctx, const double* Y, int64_t ldy, const double* tau, int64_t m, int k,
+                           double* target, int64_t ldt, int64_t nc) {
+  if (k <= 0 || nc <= 0) return;
+  TTB_RUN(ctx, "apply_reflectors", 4.0 * m * k * nc, 8.0 * (m * k + 2.0 * m * nc),
+          apply_reflectors_kernel<<<1, 1024, 0, ctx->stream>>>(Y, ldy, tau, (int)m, k, target, ldt, (int)nc));
+}
+
+}  // namespace ttb

@@ -1,0 +1,49 @@
+// Blocked Householder QR in FP64 for the right-to-left orthogonalisation sweep of
+// TT-rounding: tall-skinny panels factored by TSQR (Householder QR of
+// 256-row chunks in shared memory, reduced up a tree), converted back to compact-WY
+// Householder form by Householder reconstruction, trailing updates and the explicit Q
+// as DMMA GEMMs.
+#pragma once
+#include "common.cuh"
+
+namespace ttb {
+
+constexpr int QR_NB = 32;      // panel width
+constexpr int QR_LEAF = 256;   // TSQR leaf chunk rows
+
+struct QRFactors {
+  int64_t m = 0, c = 0, kmax = 0;
+  DBuf Y;  // m x kmax, ld m: explicit unit-lower-trapezoidal Householder vectors per panel
+  DBuf T;  // QR_NB x kmax, ld QR_NB: upper-triangular T of each panel (compact WY)
+};
+
+// In-place QR of the m x c column-major matrix A: on exit the upper trapezoid of
+// A[0:kmax, 0:c] holds R (kmax = min(m, c)); the strict lower part is garbage.
+void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& f);
+// Explicit Q (m x kmax, ld ldq) with orthonormal columns, A = Q R.
+void orgqr(tt_ctx ctx, const QRFactors& f, double* Q, int64_t ldq);
+// R (kmax x c, ld ldr) = upper trapezoid of A with explicit zeros below.
+void copy_upper(tt_ctx ctx, const double* A, int64_t lda, int64_t rows, int64_t cols, double* R, int64_t ldr);
+
+// Unblocked Householder QR with column pivoting of the m x c matrix Y (in place, column-
+// major, one CTA, LAPACK dlaqp2 norms with exact recomputation), stopping as soon as the
+// Frobenius mass of the trailing block drops to stop2 or after kcap steps.
+// On exit: *k_done steps, Householder vectors below the diagonal of Y[:, 0:k], R_1 in
+// rows 0..k-1 (permuted column order), perm[j] = original column of position j,
+// *e2 = exact ||R_22||_F^2 of the trailing block.
+struct QRCPState {
+  int64_t m = 0, c = 0;
+  DBuf tau;    // c
+  DBuf norms;  // 2c: current and reference column norms^2
+  IBuf perm;   // c
+  DBuf scalars;  // [k_done, e2] as doubles
+  int k = 0;
+  double e2 = 0.0;
+};
+void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int64_t c);
+void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, int kcap);
+// target (m x nc) <- H_0 H_1 ... H_{k-1} target, reflectors of a QRCP (unblocked).
+void apply_reflectors_left(tt_ctx ctx, const double* Y, int64_t ldy, const double* tau, int64_t m, int k,
+                           double* target, int64_t ldt, int64_t nc);
+
+}  // namespace ttb

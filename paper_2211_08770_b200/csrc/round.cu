@@ -1,0 +1,282 @@
+// TT-rounding pipeline (host orchestration of the sm_100a kernels).
+//
+//   right-to-left (k = d..2): panel A_k = (X_k x_3 R_{k+1})^T assembled straight from the
+//     terms' cores (block-diagonal TT-sum read in-kernel; one grouped DMMA GEMM over terms),
+//     blocked Householder QR (TSQR panels + compact WY), core k <- Q (its column-major
+//     layout IS the (R'_{k-1}, n_k, R'_k) core layout), R passed left;
+//   norm ||x|| = ||C_1||_F, tau = max(delta ||x|| / sqrt(d-1), floor_c u s(x));
+//   left-to-right (k = 1..d-1): truncated SVD of the unfolding, core k <- U_rho,
+//     core k+1 <- (S V^T) x_1 core k+1 (DMMA GEMM).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "gemm.cuh"
+#include "qr.cuh"
+#include "round.cuh"
+#include "svd.cuh"
+#include "ttops.cuh"
+
+namespace ttb {
+
+void SumInput::add(const tt_view& v, double c) {
+  TTShape s = view_shape(v);
+  if (coef.empty()) {
+    d = s.d;
+    n = s.n;
+  } else {
+    if (s.d != d) fail(TT_ESHAPE, "TT-sum terms differ in order d");
+    for (int k = 0; k < d; ++k)
+      if (s.n[k] != n[k]) fail(TT_ESHAPE, "TT-sum terms differ in mode sizes");
+  }
+  r.push_back(s.r);
+  core.emplace_back(v.core, v.core + v.d);
+  coef.push_back(c);
+  norm.push_back(v.norm);
+}
+
+void SumInput::add_tensor(tt_tensor t, double c) {
+  tt_view v;
+  v.d = t->d;
+  v.n = t->n.data();
+  v.r = t->r.data();
+  v.core = t->core_c.data();
+  v.norm = t->norm;
+  add(v, c);
+}
+
+tt_round_opts default_round_opts() {
+  tt_round_opts o;
+  o.rel_tol = 0.0;
+  o.max_rank = 0;
+  o.floor_c = 2048.0;
+  o.qrcp_theta = 0.5;
+  return o;
+}
+
+namespace {
+
+constexpr double QRCP_EPS = 1e-12;
+
+struct Sweep {
+  std::vector<int64_t> R;     // formal ranks R_0..R_d
+  std::vector<int64_t> Rp;    // ranks after the right-to-left sweep
+  std::vector<DBuf> Q;        // Q[k] = right-orthonormal core k (k = 1..d-1), Q[0] = C_1
+};
+
+std::vector<std::vector<int64_t>> offsets(const SumInput& in, std::vector<int64_t>& R) {
+  const int d = in.d, K = in.K();
+  std::vector<std::vector<int64_t>> off((size_t)d + 1, std::vector<int64_t>((size_t)K, 0));
+  R.assign((size_t)d + 1, 1);
+  for (int k = 1; k < d; ++k) {
+    int64_t s = 0;
+    for (int l = 0; l < K; ++l) {
+      off[(size_t)k][(size_t)l] = s;
+      s += in.r[(size_t)l][(size_t)k];
+    }
+    R[(size_t)k] = s;
+  }
+  return off;
+}
+
+// Right-to-left orthogonalisation of the (never materialised) TT-sum.
+void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
+  const int d = in.d, K = in.K();
+  std::vector<std::vector<int64_t>> off = offsets(in, sw.R);
+  sw.Rp.assign((size_t)d + 1, 1);
+  sw.Q.clear();
+  sw.Q.resize((size_t)d);
+  // panel of the last core: A_d (n_d x R_{d-1})
+  int64_t m = in.n[(size_t)d - 1], c = sw.R[(size_t)d - 1];
+  DBuf A(ctx, (size_t)m * c);
+  {
+    std::vector<TermCore> tc;
+    for (int l = 0; l < K; ++l)
+      tc.push_back({in.core[(size_t)l][(size_t)d - 1], in.r[(size_t)l][(size_t)d - 1], 1, off[(size_t)d - 1][(size_t)l], 0, in.coef[(size_t)l]});
+    gather_last(ctx, tc, in.n[(size_t)d - 1], A.p, m);
+  }
+  for (int k = d; k >= 2; --k) {
+    const int64_t nk = in.n[(size_t)k - 1];
+    m = nk * sw.Rp[(size_t)k];
+    c = sw.R[(size_t)k - 1];
+    const int64_t kq = std::min(m, c);
+    QRFactors f;
+    geqrf(ctx, A.p, m, m, c, f);
+    sw.Q[(size_t)k - 1].alloc(ctx, (size_t)m * kq);
+    orgqr(ctx, f, sw.Q[(size_t)k - 1].p, m);
+    DBuf Rk(ctx, (size_t)kq * c);
+    copy_upper(ctx, A.p, m, kq, c, Rk.p, kq);
+    sw.Rp[(size_t)k - 1] = kq;
+    const int64_t nkm1 = in.n[(size_t)k - 2];
+    if (k - 1 >= 2) {
+      // A_{k-1}[(i kq + b'), off_{k-2,l} + a] = sum_{b in block l} R(b', b) X_{k-1}^(l)(a, i, b)
+      const int64_t m2 = nkm1 * kq, c2 = sw.R[(size_t)k - 2];
+      DBuf A2(ctx, (size_t)m2 * c2);
+      std::vector<GemmDesc> gs;
+      for (int l = 0; l < K; ++l) {
+        GemmDesc g;
+        g.M = kq;
+        g.K = in.r[(size_t)l][(size_t)k - 1];
+        g.N = in.r[(size_t)l][(size_t)k - 2] * nkm1;
+        g.A = Rk.p + off[(size_t)k - 1][(size_t)l] * kq;
+        g.lda = kq;
+        g.B = in.core[(size_t)l][(size_t)k - 2];
+        g.ldb = in.r[(size_t)l][(size_t)k - 1];
+        g.C = A2.p + off[(size_t)k - 2][(size_t)l] * m2;
+        g.ldc = kq;
+        g.ncol_split = nkm1;
+        g.ldc_hi = m2;
+        gs.push_back(g);
+      }
+      gemm_grouped(ctx, gs);
+      A = std::move(A2);
+    } else {
+      // first core: C_1 (1, n_1, kq) = R_2 (kq x R_1) * M1 (R_1 x n_1), M1 = [c_l X_1^(l)]
+      const int64_t R1 = sw.R[1];
+      DBuf M1(ctx, (size_t)R1 * nkm1);
+      std::vector<TermCore> tc;
+      for (int l = 0; l < K; ++l)
+        tc.push_back({in.core[(size_t)l][0], 1, in.r[(size_t)l][1], 0, off[1][(size_t)l], in.coef[(size_t)l]});
+      gather_first(ctx, tc, nkm1, M1.p, R1);
+      sw.Q[0].alloc(ctx, (size_t)kq * nkm1);
+      GemmDesc g;
+      g.M = kq; g.N = nkm1; g.K = R1; g.A = Rk.p; g.lda = kq; g.B = M1.p; g.ldb = R1; g.C = sw.Q[0].p; g.ldc = kq;
+      gemm(ctx, g);
+    }
+  }
+}
+
+double norm_of(tt_ctx ctx, const double* x, int64_t n) {
+  DBuf s(ctx, 1);
+  sumsq(ctx, x, n, s.p);
+  double h = 0.0;
+  d2h_small(ctx, &h, s.p, 1);
+  return std::sqrt(h);
+}
+
+double term_norm(tt_ctx ctx, const SumInput& in, int l) {
+  SumInput one;
+  one.d = in.d;
+  one.n = in.n;
+  one.r.push_back(in.r[(size_t)l]);
+  one.core.push_back(in.core[(size_t)l]);
+  one.coef.push_back(1.0);
+  one.norm.push_back(NAN);
+  return sweep_norm(ctx, one);
+}
+
+}  // namespace
+
+double sweep_norm(tt_ctx ctx, const SumInput& in) {
+  if (in.d == 1) {
+    std::vector<const double*> xs;
+    for (int l = 0; l < in.K(); ++l) xs.push_back(in.core[(size_t)l][0]);
+    DBuf o(ctx, (size_t)in.n[0]);
+    lincomb(ctx, xs, in.coef, in.n[0], o.p);
+    return norm_of(ctx, o.p, in.n[0]);
+  }
+  Sweep sw;
+  right_to_left(ctx, in, sw);
+  return norm_of(ctx, sw.Q[0].p, sw.Rp[1] * in.n[0]);
+}
+
+tt_tensor materialise_sum(tt_ctx ctx, const SumInput& in) {
+  const int d = in.d, K = in.K();
+  std::vector<int64_t> R;
+  std::vector<std::vector<int64_t>> off = offsets(in, R);
+  tt_tensor t = tensor_alloc(ctx, d, in.n, R);
+  for (int k = 0; k < d; ++k) {
+    std::vector<TermCore> tc;
+    for (int l = 0; l < K; ++l) {
+      const int64_t o0 = (k == 0) ? 0 : off[(size_t)k][(size_t)l];
+      const int64_t o1 = (k == d - 1) ? 0 : off[(size_t)k + 1][(size_t)l];
+      tc.push_back({in.core[(size_t)l][(size_t)k], in.r[(size_t)l][(size_t)k], in.r[(size_t)l][(size_t)k + 1], o0, o1,
+                    in.coef[(size_t)l]});
+    }
+    if (d == 1) {
+      std::vector<const double*> xs;
+      for (int l = 0; l < K; ++l) xs.push_back(in.core[(size_t)l][0]);
+      lincomb(ctx, xs, in.coef, in.n[0], t->core[0]);
+    } else {
+      materialise_core(ctx, tc, in.n[(size_t)k], R[(size_t)k], R[(size_t)k + 1], k == 0, k == d - 1, t->core[(size_t)k]);
+    }
+  }
+  return t;
+}
+
+tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_round_info* info) {
+  const int d = in.d, K = in.K();
+  if (K < 1) fail(TT_EINVAL, "TT-round needs at least one term");
+  if (o.rel_tol < 0.0 || !(o.rel_tol == o.rel_tol)) fail(TT_EINVAL, "rel_tol must be >= 0");
+  const double theta = (o.qrcp_theta > 0.0 && o.qrcp_theta <= 1.0) ? o.qrcp_theta : 0.5;
+  const bool keep_all = (o.rel_tol == 0.0);
+  tt_round_info inf{};
+  if (d == 1) {
+    tt_tensor t = tensor_alloc(ctx, 1, in.n, {1, 1});
+    std::vector<const double*> xs;
+    for (int l = 0; l < K; ++l) xs.push_back(in.core[(size_t)l][0]);
+    lincomb(ctx, xs, in.coef, in.n[0], t->core[0]);
+    inf.norm = norm_of(ctx, t->core[0], in.n[0]);
+    inf.scale = inf.norm;
+    t->norm = inf.norm;
+    if (info) *info = inf;
+    return t;
+  }
+  // pre-cancellation scale s(x) = sum_l |c_l| ||y_l||
+  double s = 0.0;
+  if (!keep_all && o.floor_c > 0.0) {
+    for (int l = 0; l < K; ++l) {
+      double nl = in.norm[(size_t)l];
+      if (!(nl == nl)) nl = term_norm(ctx, in, l);
+      s += std::fabs(in.coef[(size_t)l]) * nl;
+    }
+  }
+  Sweep sw;
+  right_to_left(ctx, in, sw);
+  const double nrm = norm_of(ctx, sw.Q[0].p, sw.Rp[1] * in.n[0]);
+  if (keep_all || o.floor_c <= 0.0) s = nrm;
+  double tau = 0.0;
+  if (!keep_all) tau = std::max(o.rel_tol * nrm / std::sqrt((double)(d - 1)), o.floor_c * U_ROUND * s);
+  // QRCP stop: below theta*tau (decision stays exact, see svd.cu) and below QRCP_EPS s(x)
+  // so the kept subspace equals the exact truncated SVD's to the parity tolerance.
+  const double stop_abs = std::min(theta * tau, QRCP_EPS * std::max(s, nrm));
+  inf.norm = nrm;
+  inf.scale = s;
+  inf.tau = tau;
+  if (nrm == 0.0) {
+    tt_tensor t = tensor_alloc(ctx, d, in.n, std::vector<int64_t>((size_t)d + 1, 1));
+    TTB_CUDA(cudaMemsetAsync(t->block, 0, sizeof(double) * (size_t)std::accumulate(in.n.begin(), in.n.end(), (int64_t)0), ctx->stream));
+    t->norm = 0.0;
+    if (info) *info = inf;
+    return t;
+  }
+  // left-to-right truncation
+  std::vector<int64_t> ranks((size_t)d + 1, 1);
+  std::vector<DBuf> outc((size_t)d);
+  DBuf Z = std::move(sw.Q[0]);
+  for (int k = 1; k <= d - 1; ++k) {
+    const int64_t m = ranks[(size_t)k - 1] * in.n[(size_t)k - 1], c = sw.Rp[(size_t)k];
+    DBuf U, SV;
+    TruncResult tr = truncated_svd(ctx, Z.p, m, c, tau, keep_all, o.max_rank, stop_abs, U, SV);
+    inf.qrcp_steps += tr.qrcp_steps;
+    inf.resumes += tr.resumes;
+    ranks[(size_t)k] = tr.rho;
+    outc[(size_t)k - 1] = std::move(U);
+    const int64_t N = in.n[(size_t)k] * sw.Rp[(size_t)k + 1];
+    DBuf Zn(ctx, (size_t)N * tr.rho);
+    GemmDesc g;
+    g.M = N; g.N = tr.rho; g.K = c; g.A = sw.Q[(size_t)k].p; g.lda = N; g.B = SV.p; g.ldb = c; g.C = Zn.p; g.ldc = N;
+    gemm(ctx, g);
+    sw.Q[(size_t)k].release();
+    Z = std::move(Zn);
+  }
+  outc[(size_t)d - 1] = std::move(Z);
+  tt_tensor t = tensor_alloc(ctx, d, in.n, ranks);
+  for (int k = 0; k < d; ++k)
+    copy_d2d(ctx, t->core[(size_t)k], outc[(size_t)k].p, ranks[(size_t)k] * in.n[(size_t)k] * ranks[(size_t)k + 1]);
+  t->norm = nrm;
+  if (info) *info = inf;
+  return t;
+}
+
+}  // namespace ttb

@@ -1,0 +1,116 @@
+"""GPU parity of TT-rounding (tt_round / tt_round_batch) against the oracle.
+
+Bar (north star): ranks identical except where the oracle's tail lies within
+the documented window around tau; reconstructions agree to 1e-10 s(x) (TT-difference norm
+by an exact oracle rounding); the error contract holds on the GPU output.
+"""
+import numpy as np
+import pytest
+
+from oracle import rounding, tt
+from ttinputs import make_batch_sums, make_random_tt, make_shared_tail_set
+
+from gpu_util import ctx, cuda_ok, dev, diff_norm, rank_window_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
+
+
+def _rng(s):
+    return np.random.Generator(np.random.PCG64(s))
+
+
+def _case(seed):
+    rng = _rng(seed)
+    d = int(rng.integers(2, 7))
+    n = [int(v) for v in rng.integers(2, 9, size=d)]
+    K = int(rng.integers(1, 5))
+    terms = []
+    for _ in range(K):
+        r = [1] + [int(v) for v in rng.integers(1, 6, size=d - 1)] + [1]
+        terms.append(make_random_tt(d, n, r, rng))
+    coeffs = [float(v) for v in rng.standard_normal(K)]
+    if K >= 2:
+        terms.append(terms[0])           # exact rank deficiency / cancellation
+        coeffs.append(-0.5 * coeffs[0])
+    return terms, coeffs
+
+
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("delta", [0.0, 1e-2, 1e-8])
+def test_round_random_sums(seed, delta):
+    import paper_2211_08770_b200 as P
+    terms, coeffs = _case(seed)
+    floor_c = 0.0 if delta == 0.0 else rounding.DEFAULT_FLOOR_C
+    norms = [tt.tt_norm(t) for t in terms]
+    ref, info = rounding.tt_round_sum(terms, coeffs, delta, floor_c=floor_c, term_norms=norms)
+    out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, delta, floor_c=floor_c)
+    g = out.to_numpy()
+    assert abs(ginfo["norm"] - info.norm) <= 1e-13 * info.scale
+    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
+    x = tt.tt_sum(terms, coeffs)
+    s = info.scale
+    if out.ranks == info.ranks:
+        assert diff_norm(g, ref) <= 1e-10 * s
+    # the contract ||x - x~|| <= delta ||x|| (+ floor) on the GPU output itself
+    d = len(terms[0])
+    tol = max(delta * info.norm, np.sqrt(d - 1) * info.tau) * (1 + 1e-8) + 1e-13 * s
+    assert diff_norm(x, g) <= tol
+    # left-orthonormal cores 1..d-1
+    for k in range(d - 1):
+        U = g[k].reshape(-1, g[k].shape[2])
+        assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-12
+
+
+def test_round_zero_and_d1():
+    import paper_2211_08770_b200 as P
+    rng = _rng(50)
+    x = make_random_tt(4, 5, [1, 3, 3, 3, 1], rng)
+    out, info = P.tt_round(ctx(), [dev(x), dev(x)], [1.0, -1.0], 1e-8)
+    assert max(out.ranks) == 1
+    assert info["norm"] <= 1e-12 * tt.tt_norm(x)
+    x1 = [rng.standard_normal((1, 7, 1))]
+    out, _ = P.tt_round(ctx(), [dev(x1), dev(x1)], [2.0, 1.0], 1e-3)
+    np.testing.assert_allclose(out.to_numpy()[0], 3.0 * x1[0], rtol=1e-15)
+
+
+def test_round_c2_shape_mgs_like_sum():
+    """One MGS-like sum at the C2 shape (d=8, n=32, r=10, 12 terms), against the oracle."""
+    import paper_2211_08770_b200 as P
+    st = make_shared_tail_set(8, 32, 10, 12, 1e4, seed=77)
+    rng = _rng(51)
+    coeffs = [1.0] + [float(v) for v in rng.standard_normal(11) * 0.3]
+    terms = st.tensors
+    norms = [tt.tt_norm(t) for t in terms]
+    ref, info = rounding.tt_round_sum(terms, coeffs, 1e-10, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
+    out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-10)
+    assert out.ranks == info.ranks == [1] + [10] * 7 + [1]
+    assert diff_norm(out.to_numpy(), ref) <= 1e-10 * info.scale
+
+
+def test_round_c4_closed_form_batch():
+    """C4 items: ranks 32 (even b) / 16 (odd b); distance to y1 + [b even] y2 <= 5e-9 ||x||."""
+    import paper_2211_08770_b200 as P
+    items = make_batch_sums(6)
+    batch = [([dev(t, 1.0) for t in terms], coeffs) for terms, coeffs in items]
+    outs = P.tt_round_batch(ctx(), batch, 1e-6)
+    for b, ((terms, coeffs), o) in enumerate(zip(items, outs)):
+        want = 32 if b % 2 == 0 else 16
+        assert o.ranks == [1] + [want] * 9 + [1]
+        refx = tt.tt_sum(terms[:2], [1.0, 1.0]) if b % 2 == 0 else terms[0]
+        g = o.to_numpy()
+        assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
+        cpu, info = rounding.tt_round_sum(terms, coeffs, 1e-6, floor_c=rounding.DEFAULT_FLOOR_C,
+                                          term_norms=[1.0] * 4)
+        assert info.ranks == o.ranks
+        assert diff_norm(g, cpu) <= 1e-10 * info.scale
+
+
+def test_round_theta_small_equals_exact_decision():
+    """A tiny QRCP stopping fraction must give the same result as the default (the rank
+    decision is the exact-SVD decision either way)."""
+    import paper_2211_08770_b200 as P
+    terms, coeffs = _case(99)
+    o1, _ = P.tt_round(ctx(), [dev(t) for t in terms], coeffs, 1e-3, theta=0.5)
+    o2, _ = P.tt_round(ctx(), [dev(t) for t in terms], coeffs, 1e-3, theta=1e-6)
+    assert o1.ranks == o2.ranks
+    assert diff_norm(o1.to_numpy(), o2.to_numpy()) <= 1e-12 * max(tt.tt_norm(t) for t in terms) * len(terms)

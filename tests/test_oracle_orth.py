@@ -191,3 +191,25 @@ def test_paper_loo_statements_c1():
     assert np.max(loo["mgs"]) <= 1e3 * dense.U_ROUND * c.kappa
     assert np.max(loo["cgs"]) >= 1e3 * np.max(loo["mgs"])
     assert np.max(loo["gram"]) >= 1e3 * np.max(loo["mgs"])
+
+
+def test_oracle_self_spread():
+    """Evidence for the LOO parity rule: two runs of the SAME oracle on inputs perturbed at
+    the unit round-off (first core x (1 + u xi)) give LOO values that differ by more than a
+    factor 2 where LOO is rounding noise (TT-Gram on C1, u kappa^2 regime), while both stay
+    under the noise bound 64 m u kappa_k^2 that the GPU parity test uses there."""
+    c = CONFIGS["C1"]
+    st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed)
+    rng = np.random.Generator(np.random.PCG64(3))
+    pert = []
+    for a in st.tensors:
+        b = [x.copy() for x in a]
+        b[0] = b[0] * (1.0 + dense.U_ROUND * rng.standard_normal(b[0].shape))
+        pert.append(b)
+    l1 = orth.orth("gram", st.tensors, c.delta).loo_per_step()
+    l2 = orth.orth("gram", pert, c.delta).loo_per_step()
+    kap = np.array([np.linalg.cond(st.M[:, :k]) if k > 1 else 1.0 for k in range(1, st.m + 1)])
+    ratio = np.maximum(l1, l2) / np.maximum(np.minimum(l1, l2), 1e-300)
+    noisy = (np.maximum(l1, l2) > 1e-14)
+    assert np.any(ratio[noisy] > 2.0)
+    assert np.all(np.maximum(l1, l2) <= np.maximum(64 * st.m * dense.U_ROUND * kap ** 2, 1e-14))
