@@ -256,8 +256,8 @@ tt_status tt_element(tt_ctx ctx, const tt_view* x, int32_t nidx, const int64_t* 
   if (!ctx || !x || nidx < 0 || (nidx > 0 && (!lin_idx || !out_dev))) return TT_EINVAL;
   return guarded(ctx, [&] {
     TTRef t = TTRef::of(*x);
-    int64_t total = 1;
-    for (int64_t v : t.n) total *= v;
+    int64_t total = 1;  // prod(n), saturated
+    for (int64_t v : t.n) total = (total > INT64_MAX / v) ? INT64_MAX : total * v;
     std::vector<int64_t> idx;
     for (int q = 0; q < nidx; ++q) {
       const int64_t l = lin_idx[q];

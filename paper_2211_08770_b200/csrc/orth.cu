@@ -127,8 +127,8 @@ double loo_host(const std::vector<double>& Gq, int m, int k) {
 
 tt_tensor make_canonical(tt_ctx ctx, const std::vector<int64_t>& n, int64_t lin1) {
   const int d = (int)n.size();
-  int64_t total = 1;
-  for (int64_t v : n) total *= v;
+  int64_t total = 1;  // prod(n), saturated (16^50 overflows int64)
+  for (int64_t v : n) total = (total > INT64_MAX / v) ? INT64_MAX : total * v;
   if (lin1 < 1 || lin1 > total) fail(TT_EINDEX, "canonical index out of range (PAPER.md:337)");
   tt_tensor t = tensor_alloc(ctx, d, n, std::vector<int64_t>((size_t)d + 1, 1));
   int64_t sz = 0;

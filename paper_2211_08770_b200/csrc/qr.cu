@@ -1,8 +1,8 @@
 // Householder QR kernels (FP64, sm_100a).
 //
-//  * tsqr_leaf_kernel   : one CTA factors a <=256-row chunk of a <=32-column panel in
-//                         shared memory (LAPACK dgeqr2 arithmetic), writes its R to the
-//                         stack of the next tree level and its explicit Q.
+//  * tsqr_leaf_reg_kernel: one CTA factors a <=256-row chunk of a <=32-column panel with
+//                         the rows held in registers (LAPACK dgeqr2 arithmetic), writes its R
+//                         to the stack of the next tree level and its explicit Q.
 //  * tsqr_combine_kernel: Q_panel(chunk p) = Q_leaf(chunk p) * Q_next(p-th w x w block).
 //  * hr_kernel          : Householder reconstruction (LU with sign choice of Q_1 - S) so the
 //                         TSQR panel becomes compact-WY (Y, T) with H[:, :w] = Q S, R_h = S R.
@@ -17,94 +17,122 @@ namespace ttb {
 
 namespace {
 
-constexpr int LEAF_THREADS = 256;
-
-// In-smem Householder QR of the h x w column-major matrix S (ld = ldh).
-__device__ void smem_geqr2(double* S, int ldh, int h, int w, double* tau, double* red) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int kmax = min(h, w);
-  for (int j = 0; j < kmax; ++j) {
-    double part = 0.0;
-    for (int i = j + 1 + tid; i < h; i += blockDim.x) {
-      const double v = S[j * ldh + i];
-      part += v * v;
+// Sum a per-lane array p[0..31] over the warp, scattered: on return p[0] of lane l holds
+// sum_lanes p_in[l] (butterfly reduce-scatter: 16 + 8 + 4 + 2 + 1 shuffles).
+__device__ __forceinline__ void warp_reduce_scatter32(double (&p)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const double send = hi ? p[i] : p[o + i];
+      const double keep = hi ? p[o + i] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
-    const double sigma = block_sum(part, red);
-    const double alpha = S[j * ldh + j];
-    double t = 0.0, beta = alpha, scal = 0.0;
-    if (sigma != 0.0) {
-      const double nrm = sqrt(alpha * alpha + sigma);
-      beta = alpha >= 0.0 ? -nrm : nrm;
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    for (int i = j + 1 + tid; i < h; i += blockDim.x) S[j * ldh + i] *= scal;
-    __syncthreads();
-    if (tid == 0) {
-      S[j * ldh + j] = beta;
-      tau[j] = t;
-    }
-    if (t != 0.0) {
-      for (int c = j + 1 + warp; c < w; c += nw) {
-        double s = 0.0;
-        for (int i = j + 1 + lane; i < h; i += 32) s += S[j * ldh + i] * S[c * ldh + i];
-        s = warp_sum(s);
-        s = t * (s + S[c * ldh + j]);
-        for (int i = j + 1 + lane; i < h; i += 32) S[c * ldh + i] -= s * S[j * ldh + i];
-        __syncwarp();
-        if (lane == 0) S[c * ldh + j] -= s;
-      }
-    }
-    __syncthreads();
   }
-  for (int j = kmax + tid; j < w; j += blockDim.x) tau[j] = 0.0;
-  __syncthreads();
 }
 
-__global__ void __launch_bounds__(LEAF_THREADS) tsqr_leaf_kernel(const double* __restrict__ A, int64_t lda, int m,
-                                                                 int w, int P, double* Qout, int64_t ldq,
-                                                                 double* Rst, int64_t ldr) {
-  extern __shared__ double sm[];
+// Register-resident Householder QR of one <= 256-row chunk of a <= 32-column panel:
+// thread t owns row t (32 doubles).  Per column: one block reduction for the norm, one
+// butterfly reduce-scatter + one cross-warp pass for the 31 dot products, 32 FMAs.
+// Writes R (w x w, to the next level's stack) and the explicit Q chunk (h x w).
+constexpr int REG_THREADS = 256;
+__global__ void __launch_bounds__(REG_THREADS) tsqr_leaf_reg_kernel(const double* __restrict__ A, int64_t lda,
+                                                                    int m, int w, int P, double* Qout, int64_t ldq,
+                                                                    double* Rst, int64_t ldr) {
+  constexpr int NW = REG_THREADS / 32;
+  __shared__ double red[NW][33];
+  __shared__ double bc[34];
+  __shared__ double tau_s[32];
   const int p = blockIdx.x;
   const int base = m / P, rem = m % P;
   const int r0 = p * base + min(p, rem);
   const int h = base + (p < rem ? 1 : 0);
-  double* S = sm;
-  double* Qs = sm + (size_t)h * w;
-  double* tau = Qs + (size_t)h * w;
-  double* red = tau + 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int idx = tid; idx < h * w; idx += blockDim.x) {
-    const int col = idx / h, row = idx - col * h;
-    S[idx] = A[(int64_t)(r0 + row) + (int64_t)col * lda];
-    Qs[idx] = (row == col) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  smem_geqr2(S, h, h, w, tau, red);
-  // R_p (w x w upper) -> rows [p*w, p*w + w) of the next level's stack
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    const int col = idx / w, row = idx - col * w;
-    Rst[(int64_t)(p * w + row) + (int64_t)col * ldr] = (row <= col && row < h) ? S[col * h + row] : 0.0;
-  }
-  // explicit Q_p = H_0 ... H_{w-1} [I; 0]
-  for (int j = min(h, w) - 1; j >= 0; --j) {
-    const double t = tau[j];
-    if (t != 0.0) {
-      for (int c = j + warp; c < w; c += nw) {
-        double s = 0.0;
-        for (int i = j + 1 + lane; i < h; i += 32) s += S[j * h + i] * Qs[c * h + i];
-        s = warp_sum(s);
-        s = t * (s + Qs[c * h + j]);
-        for (int i = j + 1 + lane; i < h; i += 32) Qs[c * h + i] -= s * S[j * h + i];
-        __syncwarp();
-        if (lane == 0) Qs[c * h + j] -= s;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = (t < h && c < w) ? A[(int64_t)(r0 + t) + (int64_t)c * lda] : 0.0;
+  // ---------------- factorisation (LAPACK dgeqr2 arithmetic)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double x = (t > j) ? a[j] : 0.0;
+    double s = warp_sum(x * x);
+    if (lane == 0) red[warp][32] = s;
+    if (t == j) bc[32] = a[j];
+    __syncthreads();
+    double sigma = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) sigma += red[q][32];
+    const double alpha = bc[32];
+    double tj = 0.0, beta = alpha, scal = 0.0;
+    if (sigma != 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    const double v = (t > j) ? a[j] * scal : (t == j ? 1.0 : 0.0);
+    if (t > j) a[j] = v;
+    else if (t == j) a[j] = beta;
+    if (t == 0) tau_s[j] = tj;
+    if (j < 31 && tj != 0.0) {
+      double pp[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) pp[c] = (c > j) ? v * a[c] : 0.0;
+      warp_reduce_scatter32(pp, lane);
+      red[warp][lane] = pp[0];
+      __syncthreads();
+      if (warp == 0) {
+        double wc = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) wc += red[q][lane];
+        bc[lane] = tj * wc;
       }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c > j) a[c] -= v * bc[c];
+    } else {
+      __syncthreads();
+    }
+  }
+  // R rows 0..w-1 -> stack rows [p*w, p*w + w)
+  if (t < w) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < w) Rst[(int64_t)(p * w + t) + (int64_t)c * ldr] = (c >= t) ? a[c] : 0.0;
+  }
+  // ---------------- explicit Q = H_0 ... H_31 [I; 0] (backward accumulation)
+  double qv[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) qv[c] = (t == c) ? 1.0 : 0.0;
+#pragma unroll
+  for (int j = 31; j >= 0; --j) {
+    const double tj = tau_s[j];
+    if (tj == 0.0) continue;  // uniform across the block
+    const double v = (t > j) ? a[j] : (t == j ? 1.0 : 0.0);
+    double pp[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) pp[c] = (c >= j) ? v * qv[c] : 0.0;
+    warp_reduce_scatter32(pp, lane);
+    __syncthreads();
+    red[warp][lane] = pp[0];
+    __syncthreads();
+    if (warp == 0) {
+      double wc = 0.0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) wc += red[q][lane];
+      bc[lane] = tj * wc;
     }
     __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c >= j) qv[c] -= v * bc[c];
   }
-  for (int idx = tid; idx < h * w; idx += blockDim.x) {
-    const int col = idx / h, row = idx - col * h;
-    Qout[(int64_t)(r0 + row) + (int64_t)col * ldq] = Qs[idx];
+  if (t < h) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < w) Qout[(int64_t)(r0 + t) + (int64_t)c * ldq] = qv[c];
   }
 }
 
@@ -134,69 +162,88 @@ __global__ void __launch_bounds__(256) tsqr_combine_kernel(const double* __restr
   }
 }
 
-// Householder reconstruction (Ballard et al.): find S = diag(+-1), unit-lower Y_1 and upper
-// U with Q_1 - S = ... such that [I; 0] - Q S = Y U (LU without pivoting, |U_jj| >= 1),
-// Y_2 = -Q_2 S U^{-1}, T = U Y_1^{-T}; then I - Y T Y^T has first columns Q S, R_h = S R.
+// Householder reconstruction (Ballard et al.): choose S = diag(+-1) during an LU without
+// pivoting of W = [I; 0] - Q S (pivots 1 + |.| >= 1), so W = Y U with Y unit lower
+// trapezoidal; then T = U Y_1^{-T} and I - Y T Y^T has first columns Q S, R_h = S R.
+// Warp 0 of every CTA eliminates the w x w top block right-looking (lane i holds row i in
+// registers), inverts U and Y_1 into shared memory; every thread then writes its rows
+// Y_2(i, :) = -Q_2(i, :) S U^{-1} (statically indexed 32 x 32 product).
 __global__ void __launch_bounds__(256) hr_kernel(const double* __restrict__ Q, int64_t ldq, int m, int w,
                                                  const double* __restrict__ Rp, int64_t ldrp, double* Y,
                                                  int64_t ldy, double* T, int64_t ldt, double* Rh, int64_t ldrh) {
-  __shared__ double Ls[32][33], Us[32][33], Ss[32];
+  __shared__ double Us[32][33];   // U (upper, final)
+  __shared__ double Ls[32][33];   // Y_1 = L (unit lower)
+  __shared__ double Ss[32];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 32) {
-    for (int j = 0; j < w; ++j) {
-      double z = (lane < w) ? Q[lane + (int64_t)j * ldq] : 0.0;
-      for (int k = 0; k < j; ++k) {
-        const double zk = __shfl_sync(0xffffffffu, z, k);
-        if (lane > k && lane < w) z -= Ls[lane][k] * zk;
+    double z[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) z[c] = (lane < w && c < w) ? Q[lane + (int64_t)c * ldq] : 0.0;
+    double sj[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      sj[j] = 1.0;
+      if (j < w) {
+        const double piv = __shfl_sync(0xffffffffu, z[j], j);
+        const double s = (piv >= 0.0) ? -1.0 : 1.0;
+        const double ujj = 1.0 + fabs(piv);
+        sj[j] = s;
+        const double lij = (lane > j && lane < w) ? (-s * z[j] / ujj) : 0.0;
+#pragma unroll
+        for (int c = j + 1; c < 32; ++c) {
+          const double rjc = __shfl_sync(0xffffffffu, z[c], j);
+          z[c] -= lij * rjc;
+        }
+        if (lane == j) z[j] = ujj;
+        else if (lane > j) z[j] = lij;
       }
-      const double zj = __shfl_sync(0xffffffffu, z, j);
-      const double s = (zj >= 0.0) ? -1.0 : 1.0;  // pivot 1 + |z_j| >= 1
-      const double ujj = 1.0 - s * zj;
-      if (lane < j) { Us[lane][j] = -s * z; Ls[lane][j] = 0.0; }
-      if (lane == j) { Us[j][j] = ujj; Ls[j][j] = 1.0; Ss[j] = s; }
-      if (lane > j && lane < w) { Ls[lane][j] = (-s * z) / ujj; Us[lane][j] = 0.0; }
-      __syncwarp();
     }
+    // row `lane`: z[c] holds L(lane, c) for c < lane, U(lane, lane) at c == lane, and the
+    // raw eliminated M(lane, c) for c > lane with U(lane, c) = -s_c M(lane, c)
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const bool in = (lane < w && c < w);
+      Ls[lane][c] = !in ? (lane == c ? 1.0 : 0.0) : (c < lane ? z[c] : (c == lane ? 1.0 : 0.0));
+      Us[lane][c] = !in ? (lane == c ? 1.0 : 0.0) : (c < lane ? 0.0 : (c == lane ? z[c] : -sj[c] * z[c]));
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (lane == c) Ss[lane] = sj[c];
+    __syncwarp();
   }
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + tid; i < m; i += gridDim.x * blockDim.x) {
     if (i < w) {
-      for (int j = 0; j < w; ++j) Y[i + (int64_t)j * ldy] = Ls[i][j];
+      for (int c = 0; c < w; ++c) Y[i + (int64_t)c * ldy] = Ls[i][c];
     } else {
+      // row solve y U = -q S (forward substitution over columns, y in registers)
       double y[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j < w) {
-          double acc = -Ss[j] * Q[i + (int64_t)j * ldq];
+      for (int c = 0; c < 32; ++c) {
+        y[c] = 0.0;
+        if (c < w) {
+          double acc = -Ss[c] * Q[i + (int64_t)c * ldq];
 #pragma unroll
-          for (int k = 0; k < 32; ++k)
-            if (k < j) acc -= y[k] * Us[k][j];
-          y[j] = acc / Us[j][j];
-          Y[i + (int64_t)j * ldy] = y[j];
-        } else {
-          y[j] = 0.0;
+          for (int k = 0; k < c; ++k) acc -= y[k] * Us[k][c];
+          y[c] = acc / Us[c][c];
+          Y[i + (int64_t)c * ldy] = y[c];
         }
       }
     }
   }
-  if (blockIdx.x == 0 && tid < 32) {
-    // row `lane` of T: T[i,j] = U[i,j] - sum_{k<j} T[i,k] Y1[j,k]
-    double trow[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      double t = 0.0;
-      if (j < w && lane < w) {
-        t = Us[lane][j];
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < j) t -= trow[k] * Ls[j][k];
-      }
-      trow[j] = t;
-    }
-    if (lane < w)
-      for (int j = 0; j < w; ++j) T[lane + (int64_t)j * ldt] = (j >= lane) ? trow[j] : 0.0;
-  }
   if (blockIdx.x == 0) {
+    if (tid < 32 && tid < w) {
+      // T Y_1^T = U, row `tid`: T(i, j) = U(i, j) - sum_{k<j} T(i, k) Y_1(j, k) (T upper)
+      double trow[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        double acc = (j < w && j >= tid) ? Us[tid][j] : 0.0;
+#pragma unroll
+        for (int k = 0; k < j; ++k) acc -= trow[k] * Ls[j][k];
+        trow[j] = (j >= tid) ? acc : 0.0;
+        if (j < w) T[tid + (int64_t)j * ldt] = trow[j];
+      }
+    }
     for (int idx = tid; idx < w * w; idx += blockDim.x) {
       const int c = idx / w, r = idx - c * w;
       if (r <= c) Rh[r + (int64_t)c * ldrh] = Ss[r] * Rp[r + (int64_t)c * ldrp];
@@ -226,25 +273,16 @@ int grid_for(int64_t n, int threads, int cap = 4096) {
 
 // Recursive TSQR of the m x w matrix A (w <= 32): explicit Q (m x w) and R (w x w, ld w).
 void tsqr(tt_ctx ctx, const double* A, int64_t lda, int64_t m, int w, double* Qout, int64_t ldq, double* Rout) {
-  const size_t smem_leaf = (size_t)(2 * QR_LEAF * 32 + 64) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    TTB_CUDA(cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf));
-    attr_set = true;
-  }
   if (m <= QR_LEAF) {
-    const size_t sm = (size_t)(2 * m * w + 64) * sizeof(double);
     TTB_RUN(ctx, "tsqr_leaf", 4.0 * m * w * w, 16.0 * m * w,
-            tsqr_leaf_kernel<<<1, LEAF_THREADS, sm, ctx->stream>>>(A, lda, (int)m, w, 1, Qout, ldq, Rout, w));
+            tsqr_leaf_reg_kernel<<<1, REG_THREADS, 0, ctx->stream>>>(A, lda, (int)m, w, 1, Qout, ldq, Rout, w));
     return;
   }
   const int P = (int)ceil_div(m, QR_LEAF);
   const int64_t ms = (int64_t)P * w;
   DBuf Qleaf(ctx, (size_t)m * w), S(ctx, (size_t)ms * w), QS(ctx, (size_t)ms * w);
-  const int hmax = (int)ceil_div(m, P);
-  const size_t sm = (size_t)(2 * hmax * w + 64) * sizeof(double);
   TTB_RUN(ctx, "tsqr_leaf", 4.0 * m * w * w, 16.0 * m * w + 8.0 * ms * w,
-          tsqr_leaf_kernel<<<P, LEAF_THREADS, sm, ctx->stream>>>(A, lda, (int)m, w, P, Qleaf.p, m, S.p, ms));
+          tsqr_leaf_reg_kernel<<<P, REG_THREADS, 0, ctx->stream>>>(A, lda, (int)m, w, P, Qleaf.p, m, S.p, ms));
   tsqr(ctx, S.p, ms, ms, w, QS.p, ms, Rout);
   TTB_RUN(ctx, "tsqr_combine", 2.0 * m * w * w, 16.0 * m * w + 8.0 * ms * w,
           tsqr_combine_kernel<<<P, 256, 0, ctx->stream>>>(Qleaf.p, m, QS.p, ms, (int)m, w, P, Qout, ldq));
@@ -482,6 +520,31 @@ void orgqr(tt_ctx ctx, const QRFactors& f, double* Q, int64_t ldq) {
   }
 }
 
+void ormqr_left(tt_ctx ctx, const QRFactors& f, double* B, int64_t ldb, int64_t nb) {
+  const int64_t m = f.m, kq = f.kmax;
+  if (kq <= 0 || nb <= 0) return;
+  DBuf W(ctx, (size_t)QR_NB * nb), W2(ctx, (size_t)QR_NB * nb);
+  const int64_t npan = ceil_div(kq, QR_NB);
+  for (int64_t pnl = npan - 1; pnl >= 0; --pnl) {
+    const int64_t s = pnl * QR_NB;
+    const int w = (int)std::min<int64_t>(QR_NB, kq - s);
+    const int64_t ms = m - s;
+    const double* Yp = f.Y.p + s + s * m;
+    const double* Tp = f.T.p + s * QR_NB;
+    double* E = B + s;
+    GemmDesc g1;  // W = Y^T E
+    g1.M = w; g1.N = nb; g1.K = ms; g1.A = Yp; g1.lda = m; g1.ta = true; g1.B = E; g1.ldb = ldb; g1.C = W.p; g1.ldc = w;
+    gemm(ctx, g1);
+    GemmDesc g2;  // W2 = T W
+    g2.M = w; g2.N = nb; g2.K = w; g2.A = Tp; g2.lda = QR_NB; g2.B = W.p; g2.ldb = w; g2.C = W2.p; g2.ldc = w;
+    gemm(ctx, g2);
+    GemmDesc g3;  // E -= Y W2
+    g3.M = ms; g3.N = nb; g3.K = w; g3.A = Yp; g3.lda = m; g3.B = W2.p; g3.ldb = w; g3.C = E; g3.ldc = ldb;
+    g3.alpha = -1.0; g3.beta = 1.0;
+    gemm(ctx, g3);
+  }
+}
+
 void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int64_t c) {
   (void)Y; (void)ldy;
   st.m = m;
@@ -497,11 +560,8 @@ void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int
 void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, int kcap) {
   const size_t smem = (size_t)st.c * (2 * sizeof(double) + sizeof(int)) + 16;
   if (smem > 200 * 1024) fail(TT_ENOTSUP, "QRCP: too many columns for the shared-memory norm cache");
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  if (smem > 48 * 1024)  // idempotent and thread-safe (several contexts may run concurrently)
     TTB_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024 + 64)));
-    attr = 200 * 1024 + 64;
-  }
   TTB_RUN(ctx, "qrcp", 0, 16.0 * st.m * st.c,
           qrcp_kernel<<<1, 1024, smem, ctx->stream>>>(Y, ldy, (int)st.m, (int)st.c, st.k, stop2, kcap, st.tau.p, st.norms.p,
                                               st.perm.p, st.scalars.p));

@@ -22,6 +22,9 @@ struct QRFactors {
 void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& f);
 // Explicit Q (m x kmax, ld ldq) with orthonormal columns, A = Q R.
 void orgqr(tt_ctx ctx, const QRFactors& f, double* Q, int64_t ldq);
+// B (m x nb, ld ldb) <- H B with H = H_0 H_1 ... H_{kmax-1} the full m x m orthogonal factor
+// (so Q X = H [X; 0]); compact-WY panels applied last to first, 3 DMMA GEMMs each.
+void ormqr_left(tt_ctx ctx, const QRFactors& f, double* B, int64_t ldb, int64_t nb);
 // R (kmax x c, ld ldr) = upper trapezoid of A with explicit zeros below.
 void copy_upper(tt_ctx ctx, const double* A, int64_t lda, int64_t rows, int64_t cols, double* R, int64_t ldr);
 

@@ -61,7 +61,10 @@ constexpr double QRCP_EPS = 1e-12;
 struct Sweep {
   std::vector<int64_t> R;     // formal ranks R_0..R_d
   std::vector<int64_t> Rp;    // ranks after the right-to-left sweep
-  std::vector<DBuf> Q;        // Q[k] = right-orthonormal core k (k = 1..d-1), Q[0] = C_1
+  DBuf C1;                    // C_1 (1, n_1, R'_1)
+  // compact-WY Householder factors of core k's QR (k = 2..d): the right-orthonormal core
+  // k is Q_k^T, never formed; the left-to-right sweep applies Q_k to the thin S V^T.
+  std::vector<QRFactors> F;
 };
 
 std::vector<std::vector<int64_t>> offsets(const SumInput& in, std::vector<int64_t>& R) {
@@ -84,8 +87,8 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
   const int d = in.d, K = in.K();
   std::vector<std::vector<int64_t>> off = offsets(in, sw.R);
   sw.Rp.assign((size_t)d + 1, 1);
-  sw.Q.clear();
-  sw.Q.resize((size_t)d);
+  sw.F.clear();
+  sw.F.resize((size_t)d);
   // panel of the last core: A_d (n_d x R_{d-1})
   int64_t m = in.n[(size_t)d - 1], c = sw.R[(size_t)d - 1];
   DBuf A(ctx, (size_t)m * c);
@@ -100,10 +103,8 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
     m = nk * sw.Rp[(size_t)k];
     c = sw.R[(size_t)k - 1];
     const int64_t kq = std::min(m, c);
-    QRFactors f;
+    QRFactors& f = sw.F[(size_t)k - 1];
     geqrf(ctx, A.p, m, m, c, f);
-    sw.Q[(size_t)k - 1].alloc(ctx, (size_t)m * kq);
-    orgqr(ctx, f, sw.Q[(size_t)k - 1].p, m);
     DBuf Rk(ctx, (size_t)kq * c);
     copy_upper(ctx, A.p, m, kq, c, Rk.p, kq);
     sw.Rp[(size_t)k - 1] = kq;
@@ -138,9 +139,9 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
       for (int l = 0; l < K; ++l)
         tc.push_back({in.core[(size_t)l][0], 1, in.r[(size_t)l][1], 0, off[1][(size_t)l], in.coef[(size_t)l]});
       gather_first(ctx, tc, nkm1, M1.p, R1);
-      sw.Q[0].alloc(ctx, (size_t)kq * nkm1);
+      sw.C1.alloc(ctx, (size_t)kq * nkm1);
       GemmDesc g;
-      g.M = kq; g.N = nkm1; g.K = R1; g.A = Rk.p; g.lda = kq; g.B = M1.p; g.ldb = R1; g.C = sw.Q[0].p; g.ldc = kq;
+      g.M = kq; g.N = nkm1; g.K = R1; g.A = Rk.p; g.lda = kq; g.B = M1.p; g.ldb = R1; g.C = sw.C1.p; g.ldc = kq;
       gemm(ctx, g);
     }
   }
@@ -177,7 +178,7 @@ double sweep_norm(tt_ctx ctx, const SumInput& in) {
   }
   Sweep sw;
   right_to_left(ctx, in, sw);
-  return norm_of(ctx, sw.Q[0].p, sw.Rp[1] * in.n[0]);
+  return norm_of(ctx, sw.C1.p, sw.Rp[1] * in.n[0]);
 }
 
 tt_tensor materialise_sum(tt_ctx ctx, const SumInput& in) {
@@ -233,7 +234,7 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
   }
   Sweep sw;
   right_to_left(ctx, in, sw);
-  const double nrm = norm_of(ctx, sw.Q[0].p, sw.Rp[1] * in.n[0]);
+  const double nrm = norm_of(ctx, sw.C1.p, sw.Rp[1] * in.n[0]);
   if (keep_all || o.floor_c <= 0.0) s = nrm;
   double tau = 0.0;
   if (!keep_all) tau = std::max(o.rel_tol * nrm / std::sqrt((double)(d - 1)), o.floor_c * U_ROUND * s);
@@ -253,7 +254,7 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
   // left-to-right truncation
   std::vector<int64_t> ranks((size_t)d + 1, 1);
   std::vector<DBuf> outc((size_t)d);
-  DBuf Z = std::move(sw.Q[0]);
+  DBuf Z = std::move(sw.C1);
   for (int k = 1; k <= d - 1; ++k) {
     const int64_t m = ranks[(size_t)k - 1] * in.n[(size_t)k - 1], c = sw.Rp[(size_t)k];
     DBuf U, SV;
@@ -262,12 +263,14 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
     inf.resumes += tr.resumes;
     ranks[(size_t)k] = tr.rho;
     outc[(size_t)k - 1] = std::move(U);
+    // core k+1 <- (S V^T) x_1 Q_{k+1}^T, i.e. Z_{k+1}^T = Q_{k+1} (S V^T)^T = H [ (SV)^T ; 0 ]
     const int64_t N = in.n[(size_t)k] * sw.Rp[(size_t)k + 1];
     DBuf Zn(ctx, (size_t)N * tr.rho);
-    GemmDesc g;
-    g.M = N; g.N = tr.rho; g.K = c; g.A = sw.Q[(size_t)k].p; g.lda = N; g.B = SV.p; g.ldb = c; g.C = Zn.p; g.ldc = N;
-    gemm(ctx, g);
-    sw.Q[(size_t)k].release();
+    TTB_CUDA(cudaMemsetAsync(Zn.p, 0, sizeof(double) * (size_t)N * tr.rho, ctx->stream));
+    TTB_CUDA(cudaMemcpy2DAsync(Zn.p, sizeof(double) * N, SV.p, sizeof(double) * c, sizeof(double) * c, (size_t)tr.rho,
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+    ormqr_left(ctx, sw.F[(size_t)k], Zn.p, N, tr.rho);
+    sw.F[(size_t)k] = QRFactors();
     Z = std::move(Zn);
   }
   outc[(size_t)d - 1] = std::move(Z);

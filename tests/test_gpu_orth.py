@@ -167,3 +167,31 @@ def test_orth_canonical_fixed_point():
         assert np.allclose(s[:, None] * R, np.eye(5), atol=1e-12)
         for i in range(5):
             np.testing.assert_allclose(s[i] * tt.densify(Q[i].to_numpy()), tt.densify(A[i]), atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["cgs2", "gram"])
+def test_orth_c3_shape_teacher_forced(kind):
+    """C3 shape (d=16, n=64, r=20, kappa=1e6, delta=1e-5) with m reduced to 6 (the oracle's
+    full-size run takes hours on CPU): every rounding replayed at 1e-10 s(x)."""
+    c = CONFIGS["C3"]
+    st = make_shared_tail_set(c.d, c.n, c.r, 6, c.kappa, c.seed)
+    ref = _oracle(kind, st, c.delta)
+    _teacher_forced(kind, st, c.delta, ref)
+    import paper_2211_08770_b200 as P
+    Q, R, rep = P.tt_orth(ctx(), kind, [dev(a) for a in st.tensors], c.delta)
+    assert rep["rounding_calls"] == ref.rounding_calls
+    assert rep["max_rank_per_call"] == [max(i.ranks) for i in ref.infos]
+    qm, rm = st.qr_exact()
+    assert np.linalg.norm(R - rm) <= 1e-9 * np.linalg.norm(rm)
+
+
+def test_orth_c5_shape_householder_teacher_forced():
+    """C5 shape (d=50, n=16, r=30, kappa=1e12, delta=1e-12), m reduced to 3."""
+    c = CONFIGS["C5"]
+    st = make_shared_tail_set(c.d, c.n, c.r, 3, c.kappa, c.seed)
+    ref = _oracle("householder", st, c.delta)
+    _teacher_forced("householder", st, c.delta, ref)
+    import paper_2211_08770_b200 as P
+    Q, R, rep = P.tt_orth(ctx(), "householder", [dev(a) for a in st.tensors], c.delta)
+    assert rep["rounding_calls"] == 4 * 3 - 1
+    assert rep["max_rank_per_call"] == [max(i.ranks) for i in ref.infos]
