@@ -76,12 +76,17 @@ typedef struct {
  *   max_rank 0 = none; else every rank is capped (SPEC.md:246 MaxRank mode).
  *   floor_c  noise-floor constant; 0 = paper-pure threshold.  Default 2048.
  *   qrcp_theta  truncated-SVD stopping fraction theta in (0,1]; 0 selects 0.5.  The
- *            decision equals the exact-SVD decision. */
+ *            decision equals the exact-SVD decision.
+ *   rank_revealing  1 (default): the right-to-left sweep uses column-pivoted Householder QR
+ *            stopped at the panel's numerical rank in working precision (trailing block
+ *            <= 16 u ||A_k||_F); 0: full Householder QR (structural ranks).  Ignored
+ *            when rel_tol = 0 (always full). */
 typedef struct {
   double rel_tol;
   int64_t max_rank;
   double floor_c;
   double qrcp_theta;
+  int32_t rank_revealing;
 } tt_round_opts;
 
 typedef struct {

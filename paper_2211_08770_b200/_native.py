@@ -33,7 +33,7 @@ class TTView(C.Structure):
 
 class RoundOpts(C.Structure):
     _fields_ = [("rel_tol", C.c_double), ("max_rank", C.c_int64), ("floor_c", C.c_double),
-                ("qrcp_theta", C.c_double)]
+                ("qrcp_theta", C.c_double), ("rank_revealing", C.c_int32)]
 
 
 class RoundInfo(C.Structure):

@@ -176,16 +176,16 @@ def _views(tts):
     return arr, keep
 
 
-def _opts(rel_tol, floor_c, max_rank, theta):
-    return N.RoundOpts(float(rel_tol), int(max_rank), float(floor_c), float(theta))
+def _opts(rel_tol, floor_c, max_rank, theta, rank_revealing=True):
+    return N.RoundOpts(float(rel_tol), int(max_rank), float(floor_c), float(theta), int(bool(rank_revealing)))
 
 
 # ----------------------------------------------------------------------------- entry points
 def tt_round(ctx: Context, terms, coeffs, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C,
-             max_rank: int = 0, theta: float = 0.5) -> Tuple[LibTT, dict]:
+             max_rank: int = 0, theta: float = 0.5, rank_revealing: bool = True) -> Tuple[LibTT, dict]:
     arr, keep = _views(terms)
     cf = (C.c_double * len(terms))(*[float(c) for c in coeffs])
-    o = _opts(rel_tol, floor_c, max_rank, theta)
+    o = _opts(rel_tol, floor_c, max_rank, theta, rank_revealing)
     h = C.c_void_p()
     info = N.RoundInfo()
     ctx.check(ctx.lib.tt_round(ctx.handle, len(terms), cf, arr, C.byref(o), C.byref(h), C.byref(info)))
@@ -194,7 +194,7 @@ def tt_round(ctx: Context, terms, coeffs, rel_tol: float, floor_c: float = DEFAU
 
 
 def tt_round_batch(ctx: Context, items, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0,
-                   theta: float = 0.5) -> List[LibTT]:
+                   theta: float = 0.5, rank_revealing: bool = True) -> List[LibTT]:
     B = len(items)
     Ks = (C.c_int32 * B)(*[len(t) for t, _ in items])
     keep = []
@@ -207,7 +207,7 @@ def tt_round_batch(ctx: Context, items, rel_tol: float, floor_c: float = DEFAULT
         vptrs[b] = C.cast(arr, C.POINTER(N.TTView))
         cptrs[b] = C.cast(cf, C.POINTER(C.c_double))
     outs = (C.c_void_p * B)()
-    o = _opts(rel_tol, floor_c, max_rank, theta)
+    o = _opts(rel_tol, floor_c, max_rank, theta, rank_revealing)
     ctx.check(ctx.lib.tt_round_batch(ctx.handle, B, Ks, cptrs, vptrs, C.byref(o), outs, None))
     return [LibTT(ctx, C.c_void_p(outs[b])) for b in range(B)]
 
@@ -264,10 +264,10 @@ def tt_norm(ctx: Context, x) -> float:
 
 def tt_orth(ctx: Context, kind: str, tensors, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C,
             theta: float = 0.5, hh_beta_literal: bool = False, want_loo: bool = False,
-            keep_u: bool = False):
+            keep_u: bool = False, rank_revealing: bool = True):
     m = len(tensors)
     arr, keep = _views(tensors)
-    o = N.OrthOpts(_opts(rel_tol, floor_c, 0, theta), int(hh_beta_literal), int(want_loo))
+    o = N.OrthOpts(_opts(rel_tol, floor_c, 0, theta, rank_revealing), int(hh_beta_literal), int(want_loo))
     qs = (C.c_void_p * m)()
     R = np.zeros((m, m), dtype=np.float64)
     ncalls = {"cgs": m, "mgs": m, "cgs2": 2 * m, "mgs2": 2 * m, "gram": m, "householder": 4 * m - 1}[kind]

@@ -1,6 +1,7 @@
 // extern "C" boundary of libtt_b200 (include/tt_b200.h).  Every entry point converts
 // internal errors into a tt_status plus tt_last_error text; nothing throws across it.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -57,6 +58,8 @@ tt_status tt_ctx_create(int device, void* stream, tt_ctx* out) {
     c->device = device;
     c->stream = static_cast<cudaStream_t>(stream);
     TTB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    const char* dbg = std::getenv("TT_B200_DEBUG_SYNC");
+    c->debug_sync = dbg && dbg[0] == '1';
     // keep freed pool memory cached across calls (stream-ordered allocator)
     cudaMemPool_t pool;
     TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

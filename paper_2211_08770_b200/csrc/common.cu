@@ -7,6 +7,15 @@ namespace ttb {
 
 void fail(tt_status s, const std::string& msg) { throw Error{s, msg}; }
 
+void debug_check(tt_ctx ctx, const char* cls, const char* file, int line) {
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    std::ostringstream os;
+    os << "kernel class '" << cls << "' launched at " << file << ":" << line << " failed: " << cudaGetErrorString(e);
+    fail(TT_ECUDA, os.str());
+  }
+}
+
 void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
   if (e == cudaSuccess) return;
   std::ostringstream os;

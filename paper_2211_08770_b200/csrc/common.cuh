@@ -30,6 +30,7 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
     __VA_ARGS__;                                            \
     TTB_LAUNCHED(ctx);                                      \
     ::ttb::prof_end(ctx, _ttb_tok, cls, (double)(fl), (double)(by)); \
+    if ((ctx)->debug_sync) ::ttb::debug_check(ctx, cls, __FILE__, __LINE__); \
   } while (0)
 
 }  // namespace ttb
@@ -50,6 +51,7 @@ struct tt_ctx_s {
   int device = 0;
   // per-kernel-class CUDA-event timing (tt_ctx_profile); events recorded on ctx->stream
   bool prof = false;
+  bool debug_sync = false;  // TT_B200_DEBUG_SYNC=1: synchronise and check after every launch
   std::vector<TTProfEntry> prof_cls;
   std::vector<TTProfPending> prof_pending;
   std::vector<cudaEvent_t> prof_pool;
@@ -121,6 +123,7 @@ int prof_begin(tt_ctx ctx);  // returns a token (-1 when profiling is off)
 void prof_end(tt_ctx ctx, int token, const char* cls, double flops, double bytes);
 void prof_resolve(tt_ctx ctx);  // synchronises and folds pending events into the classes
 void prof_reset(tt_ctx ctx);
+void debug_check(tt_ctx ctx, const char* cls, const char* file, int line);
 
 // device -> host copy of a few doubles through the pinned staging buffer (synchronises)
 void d2h_small(tt_ctx ctx, double* host, const double* dev, size_t n);

@@ -17,6 +17,20 @@ namespace ttb {
 
 namespace {
 
+// a[j] / a[j] = v for a runtime j without dynamic register indexing (32 predicated moves)
+__device__ __forceinline__ double sel32(const double (&a)[32], int j) {
+  double r = 0.0;
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    if (c == j) r = a[c];
+  return r;
+}
+__device__ __forceinline__ void put32(double (&a)[32], int j, double v) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    if (c == j) a[c] = v;
+}
+
 // Sum a per-lane array p[0..31] over the warp, scattered: on return p[0] of lane l holds
 // sum_lanes p_in[l] (butterfly reduce-scatter: 16 + 8 + 4 + 2 + 1 shuffles).
 __device__ __forceinline__ void warp_reduce_scatter32(double (&p)[32], int lane) {
@@ -52,13 +66,16 @@ __global__ void __launch_bounds__(REG_THREADS) tsqr_leaf_reg_kernel(const double
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = (t < h && c < w) ? A[(int64_t)(r0 + t) + (int64_t)c * lda] : 0.0;
-  // ---------------- factorisation (LAPACK dgeqr2 arithmetic)
-#pragma unroll
+  // ---------------- factorisation (LAPACK dgeqr2 arithmetic).  The column loop stays rolled
+  // (an unrolled body is ~360 KB of SASS and thrashes the instruction cache); register
+  // entries are addressed through static selects.
+#pragma unroll 1
   for (int j = 0; j < 32; ++j) {
-    double x = (t > j) ? a[j] : 0.0;
+    const double aj = sel32(a, j);
+    double x = (t > j) ? aj : 0.0;
     double s = warp_sum(x * x);
     if (lane == 0) red[warp][32] = s;
-    if (t == j) bc[32] = a[j];
+    if (t == j) bc[32] = aj;
     __syncthreads();
     double sigma = 0.0;
 #pragma unroll
@@ -71,9 +88,8 @@ __global__ void __launch_bounds__(REG_THREADS) tsqr_leaf_reg_kernel(const double
       tj = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    const double v = (t > j) ? a[j] * scal : (t == j ? 1.0 : 0.0);
-    if (t > j) a[j] = v;
-    else if (t == j) a[j] = beta;
+    const double v = (t > j) ? aj * scal : (t == j ? 1.0 : 0.0);
+    put32(a, j, (t > j) ? v : (t == j ? beta : aj));
     if (t == 0) tau_s[j] = tj;
     if (j < 31 && tj != 0.0) {
       double pp[32];
@@ -106,11 +122,11 @@ __global__ void __launch_bounds__(REG_THREADS) tsqr_leaf_reg_kernel(const double
   double qv[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) qv[c] = (t == c) ? 1.0 : 0.0;
-#pragma unroll
+#pragma unroll 1
   for (int j = 31; j >= 0; --j) {
     const double tj = tau_s[j];
     if (tj == 0.0) continue;  // uniform across the block
-    const double v = (t > j) ? a[j] : (t == j ? 1.0 : 0.0);
+    const double v = (t > j) ? sel32(a, j) : (t == j ? 1.0 : 0.0);
     double pp[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) pp[c] = (c >= j) ? v * qv[c] : 0.0;
@@ -179,36 +195,31 @@ __global__ void __launch_bounds__(256) hr_kernel(const double* __restrict__ Q, i
     double z[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) z[c] = (lane < w && c < w) ? Q[lane + (int64_t)c * ldq] : 0.0;
-    double sj[32];
+    Ss[lane] = 1.0;
+#pragma unroll 1
+    for (int j = 0; j < w; ++j) {  // rolled: the unrolled body thrashes the instruction cache
+      const double zj = sel32(z, j);
+      const double piv = __shfl_sync(0xffffffffu, zj, j);
+      const double s = (piv >= 0.0) ? -1.0 : 1.0;
+      const double ujj = 1.0 + fabs(piv);
+      if (lane == 0) Ss[j] = s;
+      const double lij = (lane > j && lane < w) ? (-s * zj / ujj) : 0.0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      sj[j] = 1.0;
-      if (j < w) {
-        const double piv = __shfl_sync(0xffffffffu, z[j], j);
-        const double s = (piv >= 0.0) ? -1.0 : 1.0;
-        const double ujj = 1.0 + fabs(piv);
-        sj[j] = s;
-        const double lij = (lane > j && lane < w) ? (-s * z[j] / ujj) : 0.0;
-#pragma unroll
-        for (int c = j + 1; c < 32; ++c) {
-          const double rjc = __shfl_sync(0xffffffffu, z[c], j);
-          z[c] -= lij * rjc;
-        }
-        if (lane == j) z[j] = ujj;
-        else if (lane > j) z[j] = lij;
+      for (int c = 0; c < 32; ++c) {
+        const double rjc = __shfl_sync(0xffffffffu, z[c], j);
+        if (c > j) z[c] -= lij * rjc;
       }
+      put32(z, j, lane == j ? ujj : (lane > j ? lij : zj));
     }
+    __syncwarp();
     // row `lane`: z[c] holds L(lane, c) for c < lane, U(lane, lane) at c == lane, and the
     // raw eliminated M(lane, c) for c > lane with U(lane, c) = -s_c M(lane, c)
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       const bool in = (lane < w && c < w);
       Ls[lane][c] = !in ? (lane == c ? 1.0 : 0.0) : (c < lane ? z[c] : (c == lane ? 1.0 : 0.0));
-      Us[lane][c] = !in ? (lane == c ? 1.0 : 0.0) : (c < lane ? 0.0 : (c == lane ? z[c] : -sj[c] * z[c]));
+      Us[lane][c] = !in ? (lane == c ? 1.0 : 0.0) : (c < lane ? 0.0 : (c == lane ? z[c] : -Ss[c] * z[c]));
     }
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-      if (lane == c) Ss[lane] = sj[c];
     __syncwarp();
   }
   __syncthreads();
@@ -466,16 +477,25 @@ void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& 
   DBuf W(ctx, (size_t)QR_NB * std::max<int64_t>(c, 1)), W2(ctx, (size_t)QR_NB * std::max<int64_t>(c, 1));
   // rows above the panel inside Y must read as zero for the explicit-Y GEMMs
   TTB_CUDA(cudaMemsetAsync(f.Y.p, 0, sizeof(double) * (size_t)m * f.kmax, ctx->stream));
-  for (int64_t s = 0; s < f.kmax; s += QR_NB) {
-    const int w = (int)std::min<int64_t>(QR_NB, f.kmax - s);
+  f.pan_s.clear();
+  f.pan_w.clear();
+  for (int64_t s = 0; s < f.kmax;) {
     const int64_t ms = m - s;
+    int w = (int)std::min<int64_t>(QR_NB, f.kmax - s);
+    // narrower panels when that lets one cluster hold the panel
+    if (ms > panel_cluster_max_rows(w) && ms <= panel_cluster_max_rows(16)) w = std::min(w, 16);
     double* P = A + s + s * lda;
-    tsqr(ctx, P, lda, ms, w, Qp.p, ms, Rp.p);
     double* Yp = f.Y.p + s + s * m;
     double* Tp = f.T.p + s * QR_NB;
-    TTB_RUN(ctx, "householder_reconstruct", 1.0 * ms * w * w, 16.0 * ms * w,
-            hr_kernel<<<grid_for(ms, 256, 1024), 256, 0, ctx->stream>>>(Qp.p, ms, (int)ms, w, Rp.p, w, Yp, m, Tp, QR_NB, P,
-                                                                lda));
+    if (!panel_qr_cluster(ctx, P, lda, ms, w, Yp, m, Tp, QR_NB)) {
+      // taller than a cluster: TSQR tree + Householder reconstruction
+      tsqr(ctx, P, lda, ms, w, Qp.p, ms, Rp.p);
+      TTB_RUN(ctx, "householder_reconstruct", 1.0 * ms * w * w, 16.0 * ms * w,
+              hr_kernel<<<grid_for(ms, 256, 1024), 256, 0, ctx->stream>>>(Qp.p, ms, (int)ms, w, Rp.p, w, Yp, m, Tp,
+                                                                          QR_NB, P, lda));
+    }
+    f.pan_s.push_back(s);
+    f.pan_w.push_back(w);
     const int64_t n2 = c - s - w;
     if (n2 > 0) {
       double* C = A + s + (s + w) * lda;
@@ -490,6 +510,7 @@ void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& 
       g3.alpha = -1.0; g3.beta = 1.0;
       gemm(ctx, g3);
     }
+    s += w;
   }
 }
 
@@ -499,10 +520,9 @@ void orgqr(tt_ctx ctx, const QRFactors& f, double* Q, int64_t ldq) {
   TTB_RUN(ctx, "aux", 0, 8.0 * m * kq,
           set_identity_kernel<<<grid_for(m * kq, 256), 256, 0, ctx->stream>>>(Q, ldq, (int)m, (int)kq));
   DBuf W(ctx, (size_t)QR_NB * kq), W2(ctx, (size_t)QR_NB * kq);
-  const int64_t npan = ceil_div(kq, QR_NB);
-  for (int64_t pnl = npan - 1; pnl >= 0; --pnl) {
-    const int64_t s = pnl * QR_NB;
-    const int w = (int)std::min<int64_t>(QR_NB, kq - s);
+  for (int64_t pnl = (int64_t)f.pan_s.size() - 1; pnl >= 0; --pnl) {
+    const int64_t s = f.pan_s[(size_t)pnl];
+    const int w = f.pan_w[(size_t)pnl];
     const int64_t ms = m - s, ncols = kq - s;
     const double* Yp = f.Y.p + s + s * m;
     const double* Tp = f.T.p + s * QR_NB;
@@ -524,10 +544,9 @@ void ormqr_left(tt_ctx ctx, const QRFactors& f, double* B, int64_t ldb, int64_t 
   const int64_t m = f.m, kq = f.kmax;
   if (kq <= 0 || nb <= 0) return;
   DBuf W(ctx, (size_t)QR_NB * nb), W2(ctx, (size_t)QR_NB * nb);
-  const int64_t npan = ceil_div(kq, QR_NB);
-  for (int64_t pnl = npan - 1; pnl >= 0; --pnl) {
-    const int64_t s = pnl * QR_NB;
-    const int w = (int)std::min<int64_t>(QR_NB, kq - s);
+  for (int64_t pnl = (int64_t)f.pan_s.size() - 1; pnl >= 0; --pnl) {
+    const int64_t s = f.pan_s[(size_t)pnl];
+    const int w = f.pan_w[(size_t)pnl];
     const int64_t ms = m - s;
     const double* Yp = f.Y.p + s + s * m;
     const double* Tp = f.T.p + s * QR_NB;
@@ -551,13 +570,36 @@ void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int
   st.c = c;
   st.tau.alloc(ctx, (size_t)std::max<int64_t>(c, 1));
   st.norms.alloc(ctx, (size_t)2 * std::max<int64_t>(c, 1));
-  st.perm.alloc(ctx, (size_t)std::max<int64_t>(c, 1));
+  st.perm.alloc(ctx, (size_t)2 * std::max<int64_t>(c, 1));  // second half: write-back scratch
+  std::vector<int> ident((size_t)std::max<int64_t>(c, 1));
+  for (int64_t j = 0; j < c; ++j) ident[(size_t)j] = (int)j;
+  TTB_CUDA(cudaMemcpyAsync(st.perm.p, ident.data(), sizeof(int) * ident.size(), cudaMemcpyHostToDevice, ctx->stream));
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));  // `ident` is pageable and local
   st.scalars.alloc(ctx, 2);
   st.k = 0;
   st.e2 = 0.0;
+  st.cluster = -1;
 }
 
 void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, int kcap) {
+  // cluster-resident QRCP when the matrix fits the distributed shared memory of <= 16 CTAs
+  if (st.cluster != 0) {
+    const int kmax = (int)std::min<int64_t>(std::min(st.m, st.c), kcap);
+    bool ok = true;
+    while (ok) {
+      ok = qrcp_cluster_run(ctx, Y, ldy, st.m, st.c, st.k, stop2, kcap, st.tau.p, st.perm.p, st.scalars.p);
+      if (!ok) break;
+      double h[2];
+      d2h_small(ctx, h, st.scalars.p, 2);
+      const int before = st.k;
+      st.k = (int)h[0];
+      st.e2 = h[1];
+      st.cluster = 1;
+      if (st.k >= kmax || st.e2 <= stop2 || st.k == before) return;  // else: step cap per launch hit
+    }
+    if (st.cluster == 1) fail(TT_ENOTSUP, "QRCP: cluster path lost mid-factorisation");
+    st.cluster = 0;
+  }
   const size_t smem = (size_t)st.c * (2 * sizeof(double) + sizeof(int)) + 16;
   if (smem > 200 * 1024) fail(TT_ENOTSUP, "QRCP: too many columns for the shared-memory norm cache");
   if (smem > 48 * 1024)  // idempotent and thread-safe (several contexts may run concurrently)

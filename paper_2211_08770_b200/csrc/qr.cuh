@@ -15,7 +15,16 @@ struct QRFactors {
   int64_t m = 0, c = 0, kmax = 0;
   DBuf Y;  // m x kmax, ld m: explicit unit-lower-trapezoidal Householder vectors per panel
   DBuf T;  // QR_NB x kmax, ld QR_NB: upper-triangular T of each panel (compact WY)
+  std::vector<int64_t> pan_s;  // panel start columns
+  std::vector<int> pan_w;      // panel widths (<= QR_NB)
 };
+
+// Cluster-resident panel factorisation (panel.cu): m x w panel at A (ld lda) -> explicit Y,
+// T (ld ldt) and R in the panel's top w x w block.  Returns false when m exceeds what one
+// 16-CTA cluster holds in registers (8192 rows at w <= 32, 16384 rows at w <= 16).
+bool panel_qr_cluster(tt_ctx ctx, double* A, int64_t lda, int64_t m, int w, double* Y, int64_t ldy, double* T,
+                      int64_t ldt);
+int panel_cluster_max_rows(int w);
 
 // In-place QR of the m x c column-major matrix A: on exit the upper trapezoid of
 // A[0:kmax, 0:c] holds R (kmax = min(m, c)); the strict lower part is garbage.
@@ -42,7 +51,16 @@ struct QRCPState {
   DBuf scalars;  // [k_done, e2] as doubles
   int k = 0;
   double e2 = 0.0;
+  int cluster = -1;  // -1 undecided, 1 cluster-resident path, 0 single-CTA path
 };
+// m x c fits the distributed shared memory of one <= 16-CTA cluster
+bool qrcp_cluster_fits(int64_t m, int64_t c);
+// out[:, perm[j]] = in[:, j] (undo a column pivoting)
+void unpermute_cols(tt_ctx ctx, const double* in, int64_t ldi, int64_t rows, int64_t c, const int* perm, double* out,
+                    int64_t ldo);
+// One launch of the cluster-resident QRCP (qrcp_cluster.cu); false if the matrix does not fit.
+bool qrcp_cluster_run(tt_ctx ctx, double* Y, int64_t ldy, int64_t m, int64_t c, int k_start, double stop2, int kcap,
+                      double* tau, int* perm2c, double* scalars);
 void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int64_t c);
 void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, int kcap);
 // target (m x nc) <- H_0 H_1 ... H_{k-1} target, reflectors of a QRCP (unblocked).

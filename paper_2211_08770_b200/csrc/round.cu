@@ -51,6 +51,7 @@ tt_round_opts default_round_opts() {
   o.max_rank = 0;
   o.floor_c = 2048.0;
   o.qrcp_theta = 0.5;
+  o.rank_revealing = 1;
   return o;
 }
 
@@ -62,9 +63,29 @@ struct Sweep {
   std::vector<int64_t> R;     // formal ranks R_0..R_d
   std::vector<int64_t> Rp;    // ranks after the right-to-left sweep
   DBuf C1;                    // C_1 (1, n_1, R'_1)
-  // compact-WY Householder factors of core k's QR (k = 2..d): the right-orthonormal core
-  // k is Q_k^T, never formed; the left-to-right sweep applies Q_k to the thin S V^T.
+  // Householder factors of core k's QR (k = 2..d): the right-orthonormal core k is Q_k^T,
+  // never formed; the left-to-right sweep applies Q_k to the thin S V^T.  Either blocked
+  // compact-WY factors (F) or, for the rank-revealing sweep, the unblocked column-pivoted
+  // reflectors (P: m x c matrix with the reflectors in columns 0..k-1, tau).
   std::vector<QRFactors> F;
+  std::vector<DBuf> P, Ptau;
+  std::vector<int64_t> Pm;
+  std::vector<char> rr;
+};
+
+// Rank-revealing sweep: the column-pivoted QR of a right-to-left panel A_k stops once the
+// trailing block R_22 satisfies ||X_{<k}||_F ||R_22||_F <= RR_EPS s(x): the tensor x =
+// X_{<k} A_k^T Q_{>k}^T with X_{<k} = [X^(1)_{<k} .. X^(K)_{<k}] (block columns), so dropping
+// R_22 perturbs x by at most ||X_{<k}||_F ||R_22||_F in the Frobenius norm -- independent of
+// how the terms distribute their scale over the cores (gauge).  Summed over the d-1 panels the
+// perturbation stays below (d-1) RR_EPS s(x), orders of magnitude under the noise floor
+// floor_c u s(x).  ||X^(l)_{<k}||_F^2 = trace of the TT-dot recursion's W after core k-1
+// (x = y = term l).  DESIGN.md section 8.
+constexpr double RR_EPS = 16.0 * U_ROUND;
+
+struct RRBound {
+  double s = 0.0;               // s(x) = sum_l |c_l| ||y_l||
+  std::vector<double> left;     // left[j] = ||X_{<=j}||_F (cores 1..j of all terms), j = 0..d
 };
 
 std::vector<std::vector<int64_t>> offsets(const SumInput& in, std::vector<int64_t>& R) {
@@ -83,13 +104,58 @@ std::vector<std::vector<int64_t>> offsets(const SumInput& in, std::vector<int64_
 }
 
 // Right-to-left orthogonalisation of the (never materialised) TT-sum.
-void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
+double norm_of(tt_ctx ctx, const double* x, int64_t n);
+
+// Left-part norms of all terms after every core (one batched self-dot launch) and s(x).
+RRBound rr_bound(tt_ctx ctx, const SumInput& in) {
+  const int d = in.d, K = in.K();
+  DotBatch b;
+  b.d = d;
+  b.n = in.n;
+  b.P = K;
+  for (int l = 0; l < K; ++l) {
+    for (int k = 0; k < d; ++k) {
+      b.xc.push_back(in.core[(size_t)l][(size_t)k]);
+      b.yc.push_back(in.core[(size_t)l][(size_t)k]);
+    }
+    for (int k = 0; k <= d; ++k) {
+      b.xr.push_back(in.r[(size_t)l][(size_t)k]);
+      b.yr.push_back(in.r[(size_t)l][(size_t)k]);
+    }
+  }
+  DBuf out(ctx, (size_t)K), tr(ctx, (size_t)K * (d + 1));
+  dot_batch(ctx, b, out.p, tr.p);
+  std::vector<double> h((size_t)K * (d + 1));
+  d2h_small(ctx, h.data(), tr.p, h.size());
+  RRBound rb;
+  rb.left.assign((size_t)d + 1, 0.0);
+  for (int l = 0; l < K; ++l) {
+    for (int j = 0; j <= d; ++j) rb.left[(size_t)j] += std::max(h[(size_t)l * (d + 1) + j], 0.0);
+    double nl = in.norm[(size_t)l];
+    if (!(nl == nl)) nl = std::sqrt(std::max(h[(size_t)l * (d + 1) + d], 0.0));
+    rb.s += std::fabs(in.coef[(size_t)l]) * nl;
+  }
+  for (double& v : rb.left) v = std::sqrt(v);
+  return rb;
+}
+
+void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw, const RRBound* rrb) {
+  const bool rank_revealing = rrb != nullptr;
   const int d = in.d, K = in.K();
   std::vector<std::vector<int64_t>> off = offsets(in, sw.R);
   sw.Rp.assign((size_t)d + 1, 1);
   sw.F.clear();
   sw.F.resize((size_t)d);
-  // panel of the last core: A_d (n_d x R_{d-1})
+  sw.P.clear();
+  sw.P.resize((size_t)d);
+  sw.Ptau.clear();
+  sw.Ptau.resize((size_t)d);
+  sw.Pm.assign((size_t)d, 0);
+  sw.rr.assign((size_t)d, 0);
+  // panel of the last core: A_d (n_d x R_{d-1}).  The coefficients c_l are applied to the
+  // terms' LAST cores here (same tensor: c_l may scale any core of term l), so every column
+  // block of every panel carries its term's real magnitude -- what the rank-revealing stop
+  // criterion needs (rounding outputs, the usual terms, are left-orthonormal in cores 1..d-1).
   int64_t m = in.n[(size_t)d - 1], c = sw.R[(size_t)d - 1];
   DBuf A(ctx, (size_t)m * c);
   {
@@ -102,11 +168,34 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
     const int64_t nk = in.n[(size_t)k - 1];
     m = nk * sw.Rp[(size_t)k];
     c = sw.R[(size_t)k - 1];
-    const int64_t kq = std::min(m, c);
-    QRFactors& f = sw.F[(size_t)k - 1];
-    geqrf(ctx, A.p, m, m, c, f);
-    DBuf Rk(ctx, (size_t)kq * c);
-    copy_upper(ctx, A.p, m, kq, c, Rk.p, kq);
+    int64_t kq = std::min(m, c);
+    DBuf Rk;
+    bool done = false;
+    if (rank_revealing && qrcp_cluster_fits(m, c)) {
+      QRCPState st;
+      qrcp_init(ctx, st, A.p, m, m, c);
+      const double lk = rrb->left[(size_t)k - 1];
+      const double stop = lk > 0.0 ? RR_EPS * rrb->s / lk : 0.0;
+      qrcp_run(ctx, st, A.p, m, stop * stop, (int)kq);
+      if (st.k == 0) qrcp_run(ctx, st, A.p, m, -1.0, 1);  // keep rank >= 1
+      kq = st.k;
+      // L_k^T = R_1 P^T (kq x c): R_1 in pivoted order, columns put back in original order
+      DBuf R1(ctx, (size_t)kq * c);
+      copy_upper(ctx, A.p, m, kq, c, R1.p, kq);
+      Rk.alloc(ctx, (size_t)kq * c);
+      unpermute_cols(ctx, R1.p, kq, kq, c, st.perm.p, Rk.p, kq);
+      sw.rr[(size_t)k - 1] = 1;
+      sw.Pm[(size_t)k - 1] = m;
+      sw.Ptau[(size_t)k - 1] = std::move(st.tau);
+      sw.P[(size_t)k - 1] = std::move(A);  // keeps the reflectors (columns 0..kq-1)
+      done = true;
+    }
+    if (!done) {
+      QRFactors& f = sw.F[(size_t)k - 1];
+      geqrf(ctx, A.p, m, m, c, f);
+      Rk.alloc(ctx, (size_t)kq * c);
+      copy_upper(ctx, A.p, m, kq, c, Rk.p, kq);
+    }
     sw.Rp[(size_t)k - 1] = kq;
     const int64_t nkm1 = in.n[(size_t)k - 2];
     if (k - 1 >= 2) {
@@ -137,7 +226,7 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw) {
       DBuf M1(ctx, (size_t)R1 * nkm1);
       std::vector<TermCore> tc;
       for (int l = 0; l < K; ++l)
-        tc.push_back({in.core[(size_t)l][0], 1, in.r[(size_t)l][1], 0, off[1][(size_t)l], in.coef[(size_t)l]});
+        tc.push_back({in.core[(size_t)l][0], 1, in.r[(size_t)l][1], 0, off[1][(size_t)l], 1.0});
       gather_first(ctx, tc, nkm1, M1.p, R1);
       sw.C1.alloc(ctx, (size_t)kq * nkm1);
       GemmDesc g;
@@ -177,7 +266,7 @@ double sweep_norm(tt_ctx ctx, const SumInput& in) {
     return norm_of(ctx, o.p, in.n[0]);
   }
   Sweep sw;
-  right_to_left(ctx, in, sw);
+  right_to_left(ctx, in, sw, nullptr);
   return norm_of(ctx, sw.C1.p, sw.Rp[1] * in.n[0]);
 }
 
@@ -225,7 +314,12 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
   }
   // pre-cancellation scale s(x) = sum_l |c_l| ||y_l||
   double s = 0.0;
-  if (!keep_all && o.floor_c > 0.0) {
+  const bool rank_revealing = !keep_all && o.rank_revealing;
+  RRBound rrb;
+  if (rank_revealing) {
+    rrb = rr_bound(ctx, in);
+    s = rrb.s;
+  } else if (!keep_all && o.floor_c > 0.0) {
     for (int l = 0; l < K; ++l) {
       double nl = in.norm[(size_t)l];
       if (!(nl == nl)) nl = term_norm(ctx, in, l);
@@ -233,7 +327,7 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
     }
   }
   Sweep sw;
-  right_to_left(ctx, in, sw);
+  right_to_left(ctx, in, sw, rank_revealing ? &rrb : nullptr);
   const double nrm = norm_of(ctx, sw.C1.p, sw.Rp[1] * in.n[0]);
   if (keep_all || o.floor_c <= 0.0) s = nrm;
   double tau = 0.0;
@@ -269,8 +363,15 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
     TTB_CUDA(cudaMemsetAsync(Zn.p, 0, sizeof(double) * (size_t)N * tr.rho, ctx->stream));
     TTB_CUDA(cudaMemcpy2DAsync(Zn.p, sizeof(double) * N, SV.p, sizeof(double) * c, sizeof(double) * c, (size_t)tr.rho,
                                cudaMemcpyDeviceToDevice, ctx->stream));
-    ormqr_left(ctx, sw.F[(size_t)k], Zn.p, N, tr.rho);
-    sw.F[(size_t)k] = QRFactors();
+    if (sw.rr[(size_t)k]) {
+      apply_reflectors_left(ctx, sw.P[(size_t)k].p, sw.Pm[(size_t)k], sw.Ptau[(size_t)k].p, N, (int)c, Zn.p, N,
+                            tr.rho);
+      sw.P[(size_t)k].release();
+      sw.Ptau[(size_t)k].release();
+    } else {
+      ormqr_left(ctx, sw.F[(size_t)k], Zn.p, N, tr.rho);
+      sw.F[(size_t)k] = QRFactors();
+    }
     Z = std::move(Zn);
   }
   outc[(size_t)d - 1] = std::move(Z);

@@ -42,7 +42,7 @@ __global__ void gather_last_kernel(const __grid_constant__ TermTab tab, int64_t 
   const int64_t total = tab.r0[l] * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = idx / n, i = idx % n;
-    A[i + (tab.off0[l] + a) * lda] = X[idx];
+    A[i + (tab.off0[l] + a) * lda] = tab.coef[l] * X[idx];
   }
 }
 
@@ -55,7 +55,7 @@ __global__ void gather_first_kernel(const __grid_constant__ TermTab tab, int64_t
   const double c = tab.coef[l];
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx / r1, b = idx % r1;
-    M1[(tab.off1[l] + b) + i * R1] = c * X[idx];
+    M1[(tab.off1[l] + b) + i * R1] = c * X[idx];  // callers pass coef = 1 when c_l sits on the last core
   }
 }
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) dot_kernel(int d, const int64_t* __restri
                                                   const double* const* __restrict__ yc,
                                                   const int64_t* __restrict__ xr, const int64_t* __restrict__ yr,
                                                   double* out, double* scratch, int64_t wcap, int64_t tcap,
-                                                  int use_smem) {
+                                                  int use_smem, double* traces) {
   extern __shared__ double sm[];
   const int p = blockIdx.x;
   double* base = use_smem ? sm : scratch + (int64_t)p * (2 * wcap + tcap);
@@ -177,8 +177,16 @@ __global__ void __launch_bounds__(256) dot_kernel(int d, const int64_t* __restri
     double* tmp = W;
     W = Wn;
     Wn = tmp;
+    if (traces && tid == 0) {  // x == y: trace(W_k) = ||left part through core k||_F^2
+      double tr = 0.0;
+      for (int64_t a = 0; a < rx1 && a < ry1; ++a) tr += W[a * ry1 + a];
+      traces[(int64_t)p * (d + 1) + k + 1] = tr;
+    }
   }
-  if (tid == 0) out[p] = W[0];
+  if (tid == 0) {
+    out[p] = W[0];
+    if (traces) traces[(int64_t)p * (d + 1)] = 1.0;
+  }
 }
 
 __global__ void __launch_bounds__(256) element_kernel(int d, const int64_t* __restrict__ n,
@@ -270,7 +278,7 @@ void lincomb(tt_ctx ctx, const std::vector<const double*>& xs, const std::vector
   }
 }
 
-void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev) {
+void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev) {
   if (b.P <= 0) return;
   const int d = b.d;
   int64_t wcap = 1, tcap = 1;
@@ -308,7 +316,8 @@ void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev) {
   TTB_RUN(ctx, "tt_dot", dot_flops, dot_bytes,
           dot_kernel<<<b.P, 256, smem, ctx->stream>>>(d, (const int64_t*)dn.p, (const double* const*)dxc.p,
                                               (const double* const*)dyc.p, (const int64_t*)dxr.p,
-                                              (const int64_t*)dyr.p, out_dev, scratch.p, wcap, tcap, use_smem));
+                                              (const int64_t*)dyr.p, out_dev, scratch.p, wcap, tcap, use_smem,
+                                              traces_dev));
 }
 
 void elements(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<const double*>& core,
