@@ -1,0 +1,885 @@
+// Batched TT-rounding of many independent, uniformly shaped TT-sums (BASELINE.json
+// configs[3], "C4": 4096 sums of 4 rank-16 TTs).  PAPER.md:64 (TT-sum ranks add; rounding
+// contract ||x - x~|| <= delta ||x||), PAPER.md:69 (O(d n r^3) rounding); algorithm =
+// Oseledets' TT-SVD rounding (readings A1-A3, A11, A12).
+//
+// One CTA per item; each launch runs ONE phase of the rounding for every item of a wave, so
+// the GPU is filled by the batch, not by the (small) matrices of one item:
+//
+//   br_r2l_kernel (core k = d..2)  assembles the right-to-left panel A_k = C_k^T
+//       ((n_k R'_k) x R_{k-1}) stack by stack straight from the terms' cores (block-diagonal
+//       TT-sum read in-kernel; coefficient c_l applied on term l's last core) and factors it
+//       by a flat-tree Householder QR: a 64-row R block in shared memory plus 128-row chunks
+//       held in registers (warp w owns columns w, w+8, ...; lane owns rows lane+32t).  One
+//       __syncthreads per reflector.  Reflectors go to HBM, R is passed to core k-1.
+//   br_l2r_kernel (split k = 1..d-1)  Y_k ((rho_{k-1} n_k) x R'_k) -> Householder QR when it
+//       has more than 64 rows -> one-sided Jacobi SVD (<= 64 x 64, shared memory) -> rho_k =
+//       smallest rho with sqrt(sum_{j>rho} sigma_j^2) <= tau -> output core k = Q_Y U_rho and
+//       Z_{k+1} = H_{k+1} [(S_rho V_rho^T)^T; 0]: the right-orthonormal core k+1 is never
+//       formed, its reflectors are applied to the thin S V^T.
+//   br_compact_kernel  moves the cores from the worst-case workspace to the exact-size arena
+//       shared by the batch's result tensors (ranks are known only after the sweep).
+//
+// Unlike round.cu, the right-to-left QR is not rank-revealing: panels keep their structural
+// ranks R'_{k-1} = min(n_k R'_k, R_{k-1}) (identical tensor; the truncation decisions come from
+// the same SVDs).  Supported shapes: d >= 2, every formal rank R_k <= 64, K <= 16 terms.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "batch_round.cuh"
+#include "ttops.cuh"
+
+namespace ttb {
+
+namespace {
+
+constexpr int BR_T = 256;              // threads per CTA
+constexpr int BR_W = BR_T / 32;        // warps
+constexpr int BR_C = 64;               // max columns (formal ranks)
+constexpr int BR_CH = 128;             // chunk rows held in registers
+constexpr int BR_RPL = BR_CH / 32;     // chunk rows per lane
+constexpr int BR_CPW = BR_C / BR_W;    // columns per warp
+constexpr int BR_S0 = BR_C + BR_CH;    // rows of stack 0 (R block + first chunk)
+constexpr int BR_MAXD = 64;
+constexpr int BR_MAXK = 16;
+constexpr int BR_JAC_SWEEPS = 60;
+
+struct BRShape {
+  int d, K;
+  int n[BR_MAXD];
+  int R[BR_MAXD + 1];             // formal ranks R_k = sum_l r_k^(l)
+  int Rp[BR_MAXD + 1];            // ranks after the right-to-left sweep
+  int r[BR_MAXK][BR_MAXD + 1];    // term ranks
+  int off[BR_MAXD + 1][BR_MAXK];  // offset of term l inside R_k
+  int64_t voff[BR_MAXD];          // core index kc: offset of its panel reflectors (per item)
+  int64_t toff[BR_MAXD];          // core index kc: offset of its taus (per item)
+  int64_t ooff[BR_MAXD];          // core index kc: worst-case output core offset (per item)
+  int64_t vstride, tstride, ystride, ytstride, zstride, ostride;
+};
+
+struct BRArgs {
+  const BRShape* sh;
+  const double* const* cores;  // [gitem][l][kc]
+  const double* coef;          // [gitem][l]
+  const double* scale;         // [gitem] s(x)
+  double* V;                   // right-to-left reflectors   [item][vstride]
+  double* T;                   // their taus                 [item][tstride]
+  double* L;                   // R factors, 2 slots         [item][2][64*64]
+  double* YV;                  // left-to-right QR reflectors [item][ystride]
+  double* YT;                  // their taus                 [item][ytstride]
+  double* Z;                   // Y_{k+1} staging, 2 slots   [item][2][zstride]
+  double* out;                 // worst-case output cores    [item][ostride]
+  int* ranks;                  // [item][d+1]
+  double* scal;                // [item][4]: ||x||, tau, s, zero flag
+  int* info;                   // [item]: 1 = Jacobi hit its sweep limit
+  double rel_tol, floor_c;
+  int64_t max_rank;
+  int keep_all;
+  int item0;                   // global index of this wave's first item
+};
+
+__host__ __device__ inline int br_stacks(int64_t m) {
+  return m <= BR_S0 ? 1 : 1 + (int)((m - BR_S0 + BR_CH - 1) / BR_CH);
+}
+__host__ __device__ inline int64_t br_stack_off(int q, int c) {  // reflector storage offset of stack q
+  return q == 0 ? 0 : (int64_t)BR_S0 * c + (int64_t)BR_CH * c * (q - 1);
+}
+__host__ __device__ inline int64_t br_vsize(int64_t m, int c) { return br_stack_off(br_stacks(m), c); }
+
+template <int N>
+__device__ __forceinline__ double sel(const double (&a)[N], int j) {
+  double r = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c)
+    if (c == j) r = a[c];
+  return r;
+}
+
+// Shared-memory work areas of one CTA.
+struct BRSmem {
+  double Rs[BR_C * BR_C];     // R block (column-major, ld 64); Jacobi matrix in the l2r kernel
+  double Aux[BR_C * BR_C];    // L^T for the panel assembly; V of the Jacobi SVD
+  double vb[2][BR_S0];        // reflector broadcast (double-buffered)
+  double tb[2];
+  double sig[BR_C];
+  double red[32];
+  int perm[BR_C];
+  int cterm[BR_C], ca[BR_C];
+  int flag;
+  int rho;
+};
+
+// Flat-tree Householder QR step over one stack: R block in sm.Rs (rows 0..63, column-major;
+// a full block for stack 0, upper triangular afterwards) stacked on the 128-row chunk in
+// registers a[t][s] (row 32t + lane, column 8s + warp).  LAPACK dlarfg arithmetic per column j;
+// on return the strictly lower part of Rs holds stack 0's R-block reflector parts, a[][] holds
+// the chunk reflector parts, taus go to tau_out[j] (global).
+__device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, double* tau_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll 1
+  for (int j = 0; j < ncol; ++j) {
+    const int buf = j & 1;
+    if (warp == (j & (BR_W - 1))) {
+      const int s = j / BR_W;
+      double x[BR_RPL];
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) x[t] = sel(a[t], s);
+      double* Rc = sm.Rs + j * BR_C;
+      const double r0 = Rc[lane], r1 = Rc[lane + 32];
+      double ss = 0.0;
+      if (lane > j) ss += r0 * r0;
+      if (lane + 32 > j) ss += r1 * r1;
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) ss += x[t] * x[t];
+      const double sigma = warp_sum(ss);
+      const double alpha = Rc[j];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (sigma != 0.0) {
+        const double nr = sqrt(alpha * alpha + sigma);
+        beta = alpha >= 0.0 ? -nr : nr;
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      const double v0 = lane > j ? r0 * scal : (lane == j ? 1.0 : 0.0);
+      const double v1 = lane + 32 > j ? r1 * scal : (lane + 32 == j ? 1.0 : 0.0);
+      sm.vb[buf][lane] = v0;
+      sm.vb[buf][lane + 32] = v1;
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) {
+        const double v = x[t] * scal;
+        sm.vb[buf][BR_C + 32 * t + lane] = v;
+#pragma unroll
+        for (int c = 0; c < BR_CPW; ++c)
+          if (c == s) a[t][c] = v;
+      }
+      __syncwarp();
+      if (lane > j) Rc[lane] = v0;
+      if (lane + 32 > j) Rc[lane + 32] = v1;
+      if (lane == j) Rc[lane] = beta;
+      if (lane + 32 == j) Rc[lane + 32] = beta;
+      if (lane == 0) { sm.tb[buf] = tau; tau_out[j] = tau; }
+    }
+    __syncthreads();
+    const double tau = sm.tb[buf];
+    if (tau != 0.0) {
+      const double* v = sm.vb[buf];
+      const double v0 = v[lane], v1 = v[lane + 32];
+      double vc[BR_RPL];
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) vc[t] = v[BR_C + 32 * t + lane];
+#pragma unroll
+      for (int s = 0; s < BR_CPW; ++s) {
+        const int col = s * BR_W + warp;
+        if (col > j && col < ncol) {
+          double* Rc = sm.Rs + col * BR_C;
+          const double r0 = Rc[lane], r1 = Rc[lane + 32];
+          double dt = v0 * r0 + v1 * r1;
+#pragma unroll
+          for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * a[t][s];
+          dt = tau * warp_sum(dt);
+          Rc[lane] = r0 - dt * v0;
+          Rc[lane + 32] = r1 - dt * v1;
+#pragma unroll
+          for (int t = 0; t < BR_RPL; ++t) a[t][s] -= dt * vc[t];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Store one stack's reflectors (column-major, ld = stack rows) and, for stack 0, move the
+// R-block reflector parts out of Rs (its strictly lower part is zeroed for the next stacks).
+__device__ void br_store_stack(const double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int q, int ncol, double* Vq) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ld = q == 0 ? BR_S0 : BR_CH, roff = q == 0 ? BR_C : 0;
+#pragma unroll
+  for (int s = 0; s < BR_CPW; ++s) {
+    const int col = s * BR_W + warp;
+    if (col < ncol) {
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) Vq[(int64_t)col * ld + roff + 32 * t + lane] = a[t][s];
+    }
+  }
+  if (q == 0) {
+    for (int idx = tid; idx < BR_C * ncol; idx += BR_T) {
+      const int col = idx / BR_C, row = idx % BR_C;
+      if (row > col) {
+        Vq[(int64_t)col * ld + row] = sm.Rs[col * BR_C + row];
+        sm.Rs[col * BR_C + row] = 0.0;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// target <- H_q target for one stack's reflectors (j = ncol-1 .. 0).  The target's R-block
+// rows live in tr[0/1][s] (rows lane, lane+32), its chunk rows in tc[t][s]; column 8s + warp.
+__device__ void br_stack_apply(double (&tr)[2][BR_CPW], double (&tc)[BR_RPL][BR_CPW], const double* __restrict__ Vq,
+                               const double* __restrict__ tq, int q, int ncol, int ntgt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ld = q == 0 ? BR_S0 : BR_CH, roff = q == 0 ? BR_C : 0;
+#pragma unroll 1
+  for (int j = ncol - 1; j >= 0; --j) {
+    const double tau = __ldg(tq + j);
+    if (tau == 0.0) continue;
+    const double* v = Vq + (int64_t)j * ld;
+    double v0, v1;
+    if (q == 0) {
+      v0 = lane > j ? __ldg(v + lane) : (lane == j ? 1.0 : 0.0);
+      v1 = lane + 32 > j ? __ldg(v + lane + 32) : (lane + 32 == j ? 1.0 : 0.0);
+    } else {
+      v0 = lane == j ? 1.0 : 0.0;
+      v1 = lane + 32 == j ? 1.0 : 0.0;
+    }
+    double vc[BR_RPL];
+#pragma unroll
+    for (int t = 0; t < BR_RPL; ++t) vc[t] = __ldg(v + roff + 32 * t + lane);
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      if (s * BR_W + warp < ntgt) {
+        double dt = v0 * tr[0][s] + v1 * tr[1][s];
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * tc[t][s];
+        dt = tau * warp_sum(dt);
+        tr[0][s] -= dt * v0;
+        tr[1][s] -= dt * v1;
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= dt * vc[t];
+      }
+    }
+  }
+}
+
+// out(row, col) = Q [T; 0] for the m-row factor whose stacks are at V (taus Tq, ncol reflectors
+// per stack); T = tr (R-block rows) on entry.  Output address: out[row * rs + col * cs].
+__device__ void br_apply_q(double (&tr)[2][BR_CPW], const double* V, const double* Tq, int64_t m, int ncol, int ntgt,
+                           double* out, int64_t rs, int64_t cs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nst = br_stacks(m);
+  double tc[BR_RPL][BR_CPW];
+#pragma unroll 1
+  for (int q = nst - 1; q >= 0; --q) {
+#pragma unroll
+    for (int t = 0; t < BR_RPL; ++t)
+#pragma unroll
+      for (int s = 0; s < BR_CPW; ++s) tc[t][s] = 0.0;
+    br_stack_apply(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt);
+    const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+      if (col < ntgt) {
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) {
+          const int64_t row = base + 32 * t + lane;
+          if (row < m) out[row * rs + col * cs] = tc[t][s];
+        }
+        if (q == 0) {
+          if (lane < m) out[(int64_t)lane * rs + col * cs] = tr[0][s];
+          if (lane + 32 < m) out[(int64_t)(lane + 32) * rs + col * cs] = tr[1][s];
+        }
+      }
+    }
+  }
+}
+
+// Flat-tree QR of an m x ncol matrix given by elem(row, col) (zero outside); reflectors to V,
+// taus to Tq; on return sm.Rs holds R (upper triangle; strictly lower part zero).
+template <class Elem>
+__device__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem& sm, double* V, double* Tq) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nst = br_stacks(m);
+  double a[BR_RPL][BR_CPW];
+#pragma unroll 1
+  for (int q = 0; q < nst; ++q) {
+    if (q == 0) {
+      for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {
+        const int col = idx / BR_C, row = idx % BR_C;
+        sm.Rs[idx] = (row < m && col < ncol) ? elem(row, col) : 0.0;
+      }
+    }
+    const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) {
+        const int64_t row = base + 32 * t + lane;
+        a[t][s] = (row < m && col < ncol) ? elem(row, col) : 0.0;
+      }
+    }
+    __syncthreads();
+    br_stack_qr(a, sm, ncol, Tq + (int64_t)q * BR_C);
+    br_store_stack(a, sm, q, ncol, V + br_stack_off(q, ncol));
+  }
+}
+
+// A_k[(i, b'), col] = sum_beta L_{k+1}[b', off_l + beta] X_k^(l)[a, i, beta], col = off_{k-1,l} + a;
+// for k = d: c_l X_d^(l)[a, i, 0].  LT (smem) = L^T, column-major ld 64 (LT[c*64 + b']).
+struct PanelElem {
+  const double* const* cores;  // this item's [l][kc]
+  const BRShape* sh;
+  const double* LT;
+  const int* cterm;
+  const int* ca;
+  int kc, d, n, Rpk, last;
+  __device__ double operator()(int64_t row, int col) const {
+    const int i = (int)(row / Rpk), bp = (int)(row % Rpk);
+    const int l = cterm[col], aa = ca[col];
+    const double* X = cores[l * d + kc];
+    if (last) return LT[l * BR_C] * __ldg(X + (int64_t)aa * n + i);
+    const int rl = sh->r[l][kc + 1], o = sh->off[kc + 1][l];
+    const double* xp = X + ((int64_t)aa * n + i) * rl;
+    const double* lp = LT + (int64_t)o * BR_C + bp;
+    double s = 0.0;
+    for (int be = 0; be < rl; ++be) s += lp[be * BR_C] * __ldg(xp + be);
+    return s;
+  }
+};
+
+// Y_1[i, b'] = sum_{l, beta} X_1^(l)[0, i, beta] L_2[b', off_{1,l} + beta]
+struct FirstElem {
+  const double* const* cores;
+  const BRShape* sh;
+  const double* LT;
+  int d, K;
+  __device__ double operator()(int64_t row, int col) const {
+    double s = 0.0;
+    for (int l = 0; l < K; ++l) {
+      const int rl = sh->r[l][1], o = sh->off[1][l];
+      const double* xp = cores[l * d] + row * rl;
+      const double* lp = LT + (int64_t)o * BR_C + col;
+      for (int be = 0; be < rl; ++be) s += lp[be * BR_C] * __ldg(xp + be);
+    }
+    return s;
+  }
+};
+
+struct RowMajorElem {  // Y[row, col] = Z[row * ld + col]
+  const double* Z;
+  int ld;
+  __device__ double operator()(int64_t row, int col) const { return Z[row * ld + col]; }
+};
+
+// Load L^T (rows x cols of the row-major ld-64 L) into sm.Aux: Aux[c * 64 + b'] = L[b' * 64 + c].
+__device__ void br_load_lt(BRSmem& sm, const double* L, int rows, int cols) {
+  for (int idx = threadIdx.x; idx < BR_C * BR_C; idx += BR_T) {
+    const int c = idx / BR_C, bp = idx % BR_C;
+    sm.Aux[idx] = (bp < rows && c < cols) ? L[bp * BR_C + c] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x, gb = A.item0 + b;
+  const int d = S->d, K = S->K;
+  const int k = kc + 1;                 // 1-based core index, 2..d
+  const int n = S->n[kc], Rpk = S->Rp[k], c = S->R[k - 1];
+  const int64_t m = (int64_t)n * Rpk;
+  const bool last = (k == d);
+  const int tid = threadIdx.x;
+  if (tid < BR_C) {
+    int l = 0;
+    while (l + 1 < K && tid >= S->off[k - 1][l + 1]) ++l;
+    sm.cterm[tid] = l;
+    sm.ca[tid] = tid - S->off[k - 1][l];
+  }
+  if (last) {
+    for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = 0.0;
+    __syncthreads();
+    if (tid < K) sm.Aux[tid * BR_C] = A.coef[(int64_t)gb * K + tid];
+  } else {
+    br_load_lt(sm, A.L + (int64_t)b * 2 * BR_C * BR_C + ((k + 1) & 1) * BR_C * BR_C, Rpk, S->R[k]);
+  }
+  __syncthreads();
+  PanelElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, sm.cterm, sm.ca, kc, d, n, Rpk, last ? 1 : 0};
+  double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
+  double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kc];
+  br_qr(e, m, c, sm, V, Tq);
+  // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
+  double* Lout = A.L + (int64_t)b * 2 * BR_C * BR_C + (k & 1) * BR_C * BR_C;
+  const int rows = S->Rp[k - 1];
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {
+    const int row = idx / BR_C, col = idx % BR_C;
+    Lout[idx] = (row < rows && col < c && row <= col) ? sm.Rs[col * BR_C + row] : 0.0;
+  }
+}
+
+// One-sided (Hestenes) Jacobi SVD of the rows x nc matrix in sm.Rs (column-major, ld 64),
+// round-robin pair ordering, one warp per pair; V (nc x nc) in sm.Aux.  On return
+// sm.sig[j] = j-th largest singular value, sm.perm[j] = its column; returns false on
+// non-convergence (|<c_i,c_j>| <= sqrt(rows) u ||c_i|| ||c_j||).
+__device__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
+  const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
+  const int kk = nc + (nc & 1);
+  bool conv = nc < 2;
+  // Columns with ||c||_2 <= u ||A||_F are numerically zero: rotating them against the others
+  // only shrinks them geometrically (each projection leaves rounding residue) and the
+  // relative test never settles, so they are left alone (their sigma stays <= u ||A||_F).
+  double fro = 0.0;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; fro += v * v; }
+  const double negl = block_sum(fro, sm.red) * U_ROUND * U_ROUND;
+  __syncthreads();
+#pragma unroll 1
+  for (int sweep = 0; sweep < BR_JAC_SWEEPS && !conv; ++sweep) {
+    if (tid == 0) sm.flag = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (int r = 0; r < kk - 1; ++r) {
+      for (int q = warp; q < kk / 2; q += BR_W) {
+        int p0, p1;
+        if (q == 0) { p0 = kk - 1; p1 = r; }
+        else { p0 = (r + q) % (kk - 1); p1 = (r + kk - 1 - q) % (kk - 1); }
+        if (p0 >= nc || p1 >= nc) continue;
+        if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
+        double* ca = sm.Rs + p0 * BR_C;
+        double* cb = sm.Rs + p1 * BR_C;
+        const double x0 = ca[lane], x1 = ca[lane + 32], y0 = cb[lane], y1 = cb[lane + 32];
+        double al = x0 * x0 + x1 * x1, be = y0 * y0 + y1 * y1, ga = x0 * y0 + x1 * y1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga != 0.0 && al > negl && be > negl && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double az = fabs(zeta);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (az > 1e150 ? 2.0 * az : az + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          ca[lane] = cs * x0 - sn * y0;
+          ca[lane + 32] = cs * x1 - sn * y1;
+          cb[lane] = sn * x0 + cs * y0;
+          cb[lane + 32] = sn * x1 + cs * y1;
+          double* va = sm.Aux + p0 * BR_C;
+          double* vbp = sm.Aux + p1 * BR_C;
+          const double a0 = va[lane], a1 = va[lane + 32], b0 = vbp[lane], b1 = vbp[lane + 32];
+          va[lane] = cs * a0 - sn * b0;
+          va[lane + 32] = cs * a1 - sn * b1;
+          vbp[lane] = sn * a0 + cs * b0;
+          vbp[lane + 32] = sn * a1 + cs * b1;
+          if (lane == 0) sm.flag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    conv = (sm.flag == 0);
+    __syncthreads();
+  }
+  // singular values = column norms, sorted descending (ties: lower column first)
+  for (int j = warp; j < nc; j += BR_W) {
+    const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
+    const double s = warp_sum(x0 * x0 + x1 * x1);
+    if (lane == 0) sm.vb[0][j] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid < nc) {
+    const double v = sm.vb[0][tid];
+    int rk = 0;
+    for (int i = 0; i < nc; ++i) {
+      const double w = sm.vb[0][i];
+      if (w > v || (w == v && i < tid)) ++rk;
+    }
+    sm.sig[rk] = v;
+    sm.perm[rk] = tid;
+  }
+  __syncthreads();
+  return conv;
+}
+
+__global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x, gb = A.item0 + b;
+  const int d = S->d, K = S->K;
+  const int kc = k - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* rk = A.ranks + (int64_t)b * (d + 1);
+  double* sc = A.scal + (int64_t)b * 4;
+  double* out = A.out + (int64_t)b * S->ostride;
+  const int n = S->n[kc], cp = S->Rp[k];
+  if (k > 1 && sc[3] != 0.0) {  // ||x|| = 0: rank-1 zero tensor
+    for (int i = tid; i < n; i += BR_T) out[S->ooff[kc] + i] = 0.0;
+    if (k + 1 == d)
+      for (int i = tid; i < S->n[d - 1]; i += BR_T) out[S->ooff[d - 1] + i] = 0.0;
+    if (tid == 0) { rk[k] = 1; if (k + 1 == d) rk[d] = 1; }
+    return;
+  }
+  const int64_t p = (k == 1) ? (int64_t)n : (int64_t)rk[k - 1] * n;
+  double* YV = A.YV + (int64_t)b * S->ystride;
+  double* YT = A.YT + (int64_t)b * S->ytstride;
+  const bool tall = p > BR_C;
+  if (k == 1) {
+    br_load_lt(sm, A.L + (int64_t)b * 2 * BR_C * BR_C + 0, cp, S->R[1]);  // L_2 lives in slot 0
+    __syncthreads();
+    FirstElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, d, K};
+    if (tall) br_qr(e, p, cp, sm, YV, YT);
+    else {
+      for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {
+        const int col = idx / BR_C, row = idx % BR_C;
+        sm.Rs[idx] = (row < p && col < cp) ? e(row, col) : 0.0;
+      }
+      __syncthreads();
+    }
+  } else {
+    RowMajorElem e{A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride, cp};
+    if (tall) br_qr(e, p, cp, sm, YV, YT);
+    else {
+      for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {
+        const int col = idx / BR_C, row = idx % BR_C;
+        sm.Rs[idx] = (row < p && col < cp) ? e(row, col) : 0.0;
+      }
+      __syncthreads();
+    }
+  }
+  const int jrows = tall ? cp : (int)p;
+  if (k == 1) {
+    double q = 0.0;
+    for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; q += v * v; }
+    const double nrm = sqrt(block_sum(q, sm.red));
+    if (tid == 0) {
+      const double s = A.scale[gb];
+      double tau = 0.0;
+      if (!A.keep_all) tau = fmax(A.rel_tol * nrm / sqrt((double)(d - 1)), A.floor_c * U_ROUND * s);
+      sc[0] = nrm;
+      sc[1] = tau;
+      sc[2] = s;
+      sc[3] = nrm == 0.0 ? 1.0 : 0.0;
+      rk[0] = 1;
+      rk[d] = 1;
+    }
+    if (nrm == 0.0) {
+      for (int i = tid; i < n; i += BR_T) out[S->ooff[0] + i] = 0.0;
+      if (d == 2)
+        for (int i = tid; i < S->n[1]; i += BR_T) out[S->ooff[1] + i] = 0.0;
+      if (tid == 0) { rk[1] = 1; rk[d] = 1; }
+      return;
+    }
+    __syncthreads();
+  }
+  const bool conv = br_jacobi(sm, jrows, cp);
+  if (tid == 0) {
+    if (!conv) A.info[b] = 1;
+    const int nsv = (int)(p < cp ? p : cp);
+    int rho = nsv;
+    if (!A.keep_all) {
+      const double tau = sc[1];
+      // tail[rho] = sqrt(sum_{j >= rho} sigma_j^2), accumulated from the smallest value up
+      double tail2 = 0.0;
+      rho = nsv;
+      for (int r = nsv - 1; r >= 1; --r) {
+        tail2 += sm.sig[r] * sm.sig[r];
+        if (sqrt(tail2) <= tau) rho = r; else break;
+      }
+    }
+    if (A.max_rank > 0 && rho > A.max_rank) rho = (int)A.max_rank;
+    rho = rho < 1 ? 1 : rho;
+    sm.rho = rho;
+    rk[k] = rho;
+  }
+  __syncthreads();
+  const int rho = sm.rho;
+  // ---- output core k = Q_Y U_rho ((rho_{k-1} n_k) x rho, row-major)
+  double* ok = out + S->ooff[kc];
+  if (tall) {
+    double tr[2][BR_CPW];
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+      const bool ok2 = col < rho;
+      const int pc = ok2 ? sm.perm[col] : 0;
+      const double inv = (ok2 && sm.sig[col] > 0.0) ? 1.0 / sm.sig[col] : 0.0;
+      tr[0][s] = (ok2 && lane < cp) ? sm.Rs[pc * BR_C + lane] * inv : 0.0;
+      tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Rs[pc * BR_C + lane + 32] * inv : 0.0;
+    }
+    br_apply_q(tr, YV, YT, p, cp, rho, ok, rho, 1);
+  } else {
+    for (int idx = tid; idx < p * rho; idx += BR_T) {
+      const int row = idx / rho, col = idx % rho;
+      const double sg = sm.sig[col];
+      ok[idx] = sg > 0.0 ? sm.Rs[sm.perm[col] * BR_C + row] / sg : 0.0;
+    }
+  }
+  // ---- Z_{k+1} = H_{k+1} [(S V^T)^T; 0]   (m_{k+1} x rho, column-major)
+  {
+    const int kn = kc + 1;  // core index of core k+1
+    const int64_t m1 = (int64_t)S->n[kn] * S->Rp[k + 1];
+    const int c1 = S->R[k];
+    double tr[2][BR_CPW];
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+      const bool ok2 = col < rho;
+      const int pc = ok2 ? sm.perm[col] : 0;
+      const double sg = ok2 ? sm.sig[col] : 0.0;
+      tr[0][s] = (ok2 && lane < cp) ? sm.Aux[pc * BR_C + lane] * sg : 0.0;
+      tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Aux[pc * BR_C + lane + 32] * sg : 0.0;
+    }
+    double* dst = (k + 1 == d) ? out + S->ooff[kn] : A.Z + (int64_t)b * 2 * S->zstride + ((k + 1) & 1) * S->zstride;
+    const double* V = A.V + (int64_t)b * S->vstride + S->voff[kn];
+    const double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kn];
+    br_apply_q(tr, V, Tq, m1, c1, rho, dst, 1, m1);
+  }
+}
+
+// Copy item b's cores from the worst-case workspace to the exact-size arena.
+__global__ void br_compact_kernel(const double* __restrict__ work, int64_t ostride, const int64_t* __restrict__ ooff,
+                                  const int64_t* __restrict__ dst_off, const int64_t* __restrict__ sizes, int d,
+                                  double* arena) {
+  const int b = blockIdx.x;
+  for (int kc = 0; kc < d; ++kc) {
+    const double* src = work + (int64_t)b * ostride + ooff[kc];
+    double* dst = arena + dst_off[(int64_t)b * d + kc];
+    const int64_t sz = sizes[(int64_t)b * d + kc];
+    for (int64_t i = threadIdx.x; i < sz; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+}  // namespace
+
+bool batch_uniform_supported(int B, const std::vector<SumInput>& items, std::string* why) {
+  auto no = [&](const char* w) { if (why) *why = w; return false; };
+  if (B < 1) return no("empty batch");
+  const SumInput& f = items[0];
+  const int d = f.d, K = f.K();
+  if (d < 2) return no("d < 2");
+  if (d > BR_MAXD) return no("d > 64");
+  if (K < 1 || K > BR_MAXK) return no("K outside 1..16");
+  std::vector<int64_t> R((size_t)d + 1, 0);
+  for (int k = 0; k <= d; ++k)
+    for (int l = 0; l < K; ++l) R[(size_t)k] += f.r[(size_t)l][(size_t)k];
+  for (int k = 1; k < d; ++k)
+    if (R[(size_t)k] > BR_C) return no("formal rank > 64");
+  for (const SumInput& it : items) {
+    if (it.d != d || it.K() != K || it.n != f.n || it.r != f.r) return no("items differ in shape");
+  }
+  return true;
+}
+
+void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
+                         int64_t* ranks_out) {
+  const int B = (int)items.size();
+  const SumInput& f = items[0];
+  const int d = f.d, K = f.K();
+  // ---------------------------------------------------------------- shape tables (uniform)
+  BRShape sh;
+  std::memset(&sh, 0, sizeof(sh));
+  sh.d = d;
+  sh.K = K;
+  for (int k = 0; k < d; ++k) sh.n[k] = (int)f.n[(size_t)k];
+  for (int k = 0; k <= d; ++k) {
+    int s = 0;
+    for (int l = 0; l < K; ++l) {
+      sh.r[l][k] = (int)f.r[(size_t)l][(size_t)k];
+      sh.off[k][l] = s;
+      s += sh.r[l][k];
+    }
+    sh.R[k] = s;
+  }
+  sh.R[0] = 1;
+  sh.R[d] = 1;
+  sh.Rp[d] = 1;
+  for (int k = d; k >= 2; --k) sh.Rp[k - 1] = (int)std::min<int64_t>((int64_t)sh.n[k - 1] * sh.Rp[k], sh.R[k - 1]);
+  sh.Rp[0] = 1;
+  int64_t v = 0, t = 0, omax = 0, yv = 0, zmax = 0;
+  for (int kc = 1; kc < d; ++kc) {  // panels of cores 2..d
+    const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
+    const int c = sh.R[kc];
+    sh.voff[kc] = v;
+    sh.toff[kc] = t;
+    v += br_vsize(m, c);
+    t += (int64_t)br_stacks(m) * BR_C;
+  }
+  for (int kc = 0; kc < d; ++kc) {
+    sh.ooff[kc] = omax;
+    omax += (int64_t)sh.Rp[kc] * sh.n[kc] * sh.Rp[kc + 1];
+  }
+  int64_t yt = 0;
+  for (int k = 1; k < d; ++k) {  // left-to-right QR of Y_k, p <= Rp_{k-1} n_k
+    const int64_t p = (int64_t)sh.Rp[k - 1] * sh.n[k - 1];
+    if (p > BR_C) {
+      yv = std::max<int64_t>(yv, br_vsize(p, sh.Rp[k]));
+      yt = std::max<int64_t>(yt, (int64_t)br_stacks(p) * BR_C);
+    }
+    if (k + 1 < d) zmax = std::max<int64_t>(zmax, (int64_t)sh.n[k] * sh.Rp[k + 1] * sh.Rp[k]);
+  }
+  sh.vstride = std::max<int64_t>(v, 1);
+  sh.tstride = std::max<int64_t>(t, 1);
+  sh.ystride = std::max<int64_t>(yv, 1);
+  sh.ytstride = std::max<int64_t>(yt, 1);
+  sh.zstride = std::max<int64_t>(zmax, 1);
+  sh.ostride = omax;
+  const int64_t per_item = sh.vstride + sh.tstride + 2 * BR_C * BR_C + sh.ystride + sh.ytstride + 2 * sh.zstride +
+                           sh.ostride + 8;
+  // ---------------------------------------------------------------- s(x) per item
+  const bool keep_all = (o.rel_tol == 0.0);
+  std::vector<double> scale((size_t)B, 0.0);
+  {
+    std::vector<std::pair<int, int>> need;
+    for (int b = 0; b < B; ++b)
+      for (int l = 0; l < K; ++l)
+        if (!(items[(size_t)b].norm[(size_t)l] == items[(size_t)b].norm[(size_t)l])) need.push_back({b, l});
+    std::vector<double> nn(need.size());
+    if (!need.empty() && !keep_all && o.floor_c > 0.0) {
+      DotBatch db;
+      db.d = d;
+      db.n = f.n;
+      db.P = (int)need.size();
+      for (auto& bl : need) {
+        const SumInput& it = items[(size_t)bl.first];
+        for (int k = 0; k < d; ++k) {
+          db.xc.push_back(it.core[(size_t)bl.second][(size_t)k]);
+          db.yc.push_back(it.core[(size_t)bl.second][(size_t)k]);
+        }
+        for (int k = 0; k <= d; ++k) {
+          db.xr.push_back(it.r[(size_t)bl.second][(size_t)k]);
+          db.yr.push_back(it.r[(size_t)bl.second][(size_t)k]);
+        }
+      }
+      DBuf dd(ctx, need.size());
+      dot_batch(ctx, db, dd.p, nullptr);
+      d2h_small(ctx, nn.data(), dd.p, nn.size());
+      for (double& x : nn) x = std::sqrt(std::max(x, 0.0));
+    }
+    size_t q = 0;
+    for (int b = 0; b < B; ++b)
+      for (int l = 0; l < K; ++l) {
+        double nl = items[(size_t)b].norm[(size_t)l];
+        if (!(nl == nl)) nl = (q < nn.size()) ? nn[q++] : 0.0;
+        scale[(size_t)b] += std::fabs(items[(size_t)b].coef[(size_t)l]) * nl;
+      }
+  }
+  // ---------------------------------------------------------------- device tables
+  BBuf dsh;
+  dsh.upload(ctx, &sh, sizeof(sh));
+  std::vector<const double*> tab((size_t)B * K * d);
+  std::vector<double> coef((size_t)B * K);
+  for (int b = 0; b < B; ++b)
+    for (int l = 0; l < K; ++l) {
+      coef[(size_t)b * K + l] = items[(size_t)b].coef[(size_t)l];
+      for (int k = 0; k < d; ++k) tab[((size_t)b * K + l) * d + k] = items[(size_t)b].core[(size_t)l][(size_t)k];
+    }
+  BBuf dtab, dcoef, dscale;
+  dtab.upload(ctx, tab.data(), tab.size() * sizeof(double*));
+  dcoef.upload(ctx, coef.data(), coef.size() * sizeof(double));
+  dscale.upload(ctx, scale.data(), scale.size() * sizeof(double));
+  // ---------------------------------------------------------------- waves
+  size_t free_b = 0, total_b = 0;
+  TTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = std::min<double>(0.5 * (double)free_b, 48e9);
+  int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
+  const size_t smem = sizeof(BRSmem);
+  TTB_CUDA(cudaFuncSetAttribute(br_r2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TTB_CUDA(cudaFuncSetAttribute(br_l2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int done = 0;
+  try {
+    for (int w0 = 0; w0 < B; w0 += W) {
+      const int nb = std::min(W, B - w0);
+      DBuf V(ctx, (size_t)nb * sh.vstride), T(ctx, (size_t)nb * sh.tstride), L(ctx, (size_t)nb * 2 * BR_C * BR_C);
+      DBuf YV(ctx, (size_t)nb * sh.ystride), YT(ctx, (size_t)nb * sh.ytstride), Z(ctx, (size_t)nb * 2 * sh.zstride);
+      DBuf O(ctx, (size_t)nb * std::max<int64_t>(sh.ostride, 1)), SC(ctx, (size_t)nb * 4);
+      IBuf RK(ctx, (size_t)nb * (d + 1)), INF(ctx, (size_t)nb);
+      TTB_CUDA(cudaMemsetAsync(INF.p, 0, sizeof(int) * nb, ctx->stream));
+      BRArgs a;
+      a.sh = static_cast<const BRShape*>(dsh.p);
+      a.cores = static_cast<const double* const*>(dtab.p);
+      a.coef = static_cast<const double*>(dcoef.p);
+      a.scale = static_cast<const double*>(dscale.p);
+      a.V = V.p; a.T = T.p; a.L = L.p; a.YV = YV.p; a.YT = YT.p; a.Z = Z.p; a.out = O.p;
+      a.ranks = RK.p; a.scal = SC.p; a.info = INF.p;
+      a.rel_tol = o.rel_tol;
+      a.floor_c = o.floor_c;
+      a.max_rank = o.max_rank;
+      a.keep_all = keep_all ? 1 : 0;
+      a.item0 = w0;
+      for (int kc = d - 1; kc >= 1; --kc) {
+        const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
+        const double c = sh.R[kc];
+        double rl = 0.0;  // assembly flops per row and column: r_k of the column's term
+        for (int l = 0; l < K; ++l) rl += (double)sh.r[l][kc] * sh.r[l][kc + 1];
+        const double mm = (double)m;
+        const double fl = nb * (2.0 * mm * rl + (mm >= c ? 2.0 * mm * c * c - 2.0 * c * c * c / 3.0
+                                                         : 2.0 * c * mm * mm - 2.0 * mm * mm * mm / 3.0));
+        TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
+                br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
+      }
+      for (int k = 1; k < d; ++k)
+        TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, k));
+      // ranks (the one host synchronisation of the wave), then compaction
+      std::vector<int> hr((size_t)nb * (d + 1)), hinf((size_t)nb);
+      d2h_small_int(ctx, hr.data(), RK.p, hr.size());
+      d2h_small_int(ctx, hinf.data(), INF.p, hinf.size());
+      for (int b = 0; b < nb; ++b)
+        if (hinf[(size_t)b]) fail(TT_ENOCONV, "Jacobi SVD did not converge (batch item " + std::to_string(w0 + b) + ")");
+      std::vector<double> hsc((size_t)nb * 4);
+      d2h_small(ctx, hsc.data(), SC.p, hsc.size());
+      std::vector<int64_t> dst((size_t)nb * d), sz((size_t)nb * d);
+      int64_t tot = 0;
+      double l2r_fl = 0.0;
+      for (int b = 0; b < nb; ++b) {
+        const int* r = hr.data() + (size_t)b * (d + 1);
+        for (int kc = 0; kc < d; ++kc) {
+          dst[(size_t)b * d + kc] = tot;
+          sz[(size_t)b * d + kc] = (int64_t)r[kc] * sh.n[kc] * r[kc + 1];
+          tot += sz[(size_t)b * d + kc];
+        }
+        if (hsc[(size_t)b * 4 + 3] != 0.0) continue;
+        for (int k = 1; k < d; ++k) {  // LAPACK-standard counts of the l2r operations
+          const double pp = (double)r[k - 1] * sh.n[k - 1], cp = sh.Rp[k], rho = r[k];
+          const double a1 = std::max(pp, cp), b1 = std::min(pp, cp);
+          const double m1 = (double)sh.n[k] * sh.Rp[k + 1], c1 = sh.R[k];
+          l2r_fl += 6.0 * a1 * b1 * b1 + 11.0 * b1 * b1 * b1;  // R-SVD (GVL nominal)
+          if (pp > BR_C) l2r_fl += 4.0 * pp * cp * rho - 2.0 * cp * cp * rho;
+          l2r_fl += 4.0 * m1 * std::min(m1, c1) * rho - 2.0 * std::min(m1, c1) * std::min(m1, c1) * rho;
+        }
+      }
+      prof_credit(ctx, "batch_l2r_svd", l2r_fl);
+      void* arena = nullptr;
+      if (cudaMallocAsync(&arena, (size_t)std::max<int64_t>(tot, 1) * sizeof(double), ctx->stream) != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(TT_ENOMEM, "batch result arena allocation failed");
+      }
+      int64_t* refs = new int64_t(nb);
+      BBuf ddst, dsz, dooff;
+      ddst.upload(ctx, dst.data(), dst.size() * sizeof(int64_t));
+      dsz.upload(ctx, sz.data(), sz.size() * sizeof(int64_t));
+      dooff.upload(ctx, sh.ooff, sizeof(int64_t) * d);
+      TTB_RUN(ctx, "batch_compact", 0.0, 16.0 * (double)tot,
+              br_compact_kernel<<<nb, 256, 0, ctx->stream>>>(O.p, sh.ostride, static_cast<const int64_t*>(dooff.p),
+                                                             static_cast<const int64_t*>(ddst.p),
+                                                             static_cast<const int64_t*>(dsz.p), d,
+                                                             static_cast<double*>(arena)));
+      for (int b = 0; b < nb; ++b) {
+        tt_tensor tt = new tt_tensor_s();
+        tt->d = d;
+        tt->n = f.n;
+        tt->r.assign(hr.begin() + (size_t)b * (d + 1), hr.begin() + (size_t)(b + 1) * (d + 1));
+        tt->core.resize((size_t)d);
+        tt->core_c.resize((size_t)d);
+        for (int kc = 0; kc < d; ++kc) {
+          tt->core[(size_t)kc] = static_cast<double*>(arena) + dst[(size_t)b * d + kc];
+          tt->core_c[(size_t)kc] = tt->core[(size_t)kc];
+        }
+        tt->norm = hsc[(size_t)b * 4 + 0];
+        tt->arena = arena;
+        tt->arena_refs = refs;
+        out[w0 + b] = tt;
+        if (ranks_out)
+          for (int k = 0; k <= d; ++k) ranks_out[(size_t)(w0 + b) * (d + 1) + k] = tt->r[(size_t)k];
+        ++done;
+      }
+    }
+  } catch (...) {
+    for (int b = 0; b < done; ++b) { tensor_free(ctx, out[b]); out[b] = nullptr; }
+    throw;
+  }
+}
+
+}  // namespace ttb

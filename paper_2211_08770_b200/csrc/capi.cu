@@ -6,6 +6,7 @@
 #include <exception>
 #include <new>
 
+#include "batch_round.cuh"
 #include "orth.cuh"
 #include "round.cuh"
 #include "ttops.cuh"
@@ -291,10 +292,21 @@ tt_status tt_round_batch(tt_ctx ctx, int32_t B, const int32_t* K, const double* 
   if (!ctx || B < 0 || (B > 0 && (!K || !coeff || !terms || !out))) return TT_EINVAL;
   return guarded(ctx, [&] {
     const tt_round_opts o = resolve(opts);
+    std::vector<SumInput> items;
+    items.reserve((size_t)B);
+    for (int b = 0; b < B; ++b) items.push_back(sum_of(K[b], coeff[b], terms[b]));
+    if (B == 0) return;
+    // uniform batches (C4) run the one-CTA-per-item batched engine; TT_B200_BATCH_SERIAL=1
+    // forces the per-item path (used by the tests to compare the two).
+    const char* ser = std::getenv("TT_B200_BATCH_SERIAL");
+    if (!(ser && ser[0] == '1') && batch_uniform_supported(B, items, nullptr)) {
+      round_batch_uniform(ctx, items, o, out, ranks_out);
+      return;
+    }
     int done = 0;
     try {
       for (int b = 0; b < B; ++b) {
-        out[b] = round_sum(ctx, sum_of(K[b], coeff[b], terms[b]), o, nullptr);
+        out[b] = round_sum(ctx, items[(size_t)b], o, nullptr);
         if (ranks_out) std::memcpy(ranks_out + (size_t)b * (out[b]->d + 1), out[b]->r.data(), sizeof(int64_t) * (out[b]->d + 1));
         ++done;
       }

@@ -136,6 +136,12 @@ void prof_resolve(tt_ctx ctx) {
   ctx->prof_pending.clear();
 }
 
+void prof_credit(tt_ctx ctx, const char* cls, double flops) {
+  if (!ctx->prof) return;
+  for (TTProfEntry& e : ctx->prof_cls)
+    if (e.name == cls) { e.flops += flops; return; }
+}
+
 void prof_reset(tt_ctx ctx) {
   prof_resolve(ctx);
   ctx->prof_cls.clear();
@@ -194,6 +200,10 @@ tt_tensor tensor_alloc(tt_ctx ctx, int d, const std::vector<int64_t>& n, const s
 void tensor_free(tt_ctx ctx, tt_tensor t) {
   if (!t) return;
   if (t->block) cudaFreeAsync(t->block, ctx->stream);
+  if (t->arena_refs && --*t->arena_refs == 0) {
+    cudaFreeAsync(t->arena, ctx->stream);
+    delete t->arena_refs;
+  }
   delete t;
 }
 

@@ -70,6 +70,10 @@ struct tt_tensor_s {
   std::vector<const double*> core_c;
   double norm = NAN;
   double* block = nullptr;  // one allocation holding every core
+  // Batched results share one arena (batch_round.cu): block stays null, the cores point into
+  // `arena`, freed when the last tensor of the batch is freed (host refcount).
+  void* arena = nullptr;
+  int64_t* arena_refs = nullptr;
 };
 
 namespace ttb {
@@ -123,6 +127,8 @@ int prof_begin(tt_ctx ctx);  // returns a token (-1 when profiling is off)
 void prof_end(tt_ctx ctx, int token, const char* cls, double flops, double bytes);
 void prof_resolve(tt_ctx ctx);  // synchronises and folds pending events into the classes
 void prof_reset(tt_ctx ctx);
+// add algorithmic flops to a class after the fact (work known only once ranks are read back)
+void prof_credit(tt_ctx ctx, const char* cls, double flops);
 void debug_check(tt_ctx ctx, const char* cls, const char* file, int line);
 
 // device -> host copy of a few doubles through the pinned staging buffer (synchronises)

@@ -1,0 +1,146 @@
+"""GPU parity of the batched TT-rounding engine (tt_round_batch on uniform batches,
+csrc/batch_round.cu) against the oracle (BASELINE.json configs[3], "C4").
+
+Every item is compared with oracle.rounding.tt_round_sum on the same bytes: ranks identical
+(or inside the documented window around tau), reconstruction within 1e-10 s(x) (TT-difference
+norm through an exact oracle rounding), the rounding contract on the GPU output, and
+left-orthonormal cores 1..d-1.  Shapes span one stack (<= 192 panel rows), several stacks with
+a ragged tail, d = 2, single-term sums, exact cancellation, delta = 0, max_rank and unknown
+term norms (computed on the device).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import rounding, tt
+from ttinputs import make_batch_sums, make_random_tt
+
+from gpu_util import ctx, cuda_ok, dev, diff_norm, rank_window_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
+
+
+def _rng(s):
+    return np.random.Generator(np.random.PCG64(s))
+
+
+def _batch(seed):
+    """B items sharing d, n, K and term ranks (formal ranks <= 64)."""
+    rng = _rng(1000 + seed)
+    d = int(rng.integers(2, 7))
+    n = [int(v) for v in rng.integers(2, 41, size=d)]
+    K = int(rng.integers(1, 5))
+    rmax = max(1, 60 // (K + 1))
+    ranks = []
+    for _ in range(K):
+        ranks.append([1] + [int(v) for v in rng.integers(1, rmax + 1, size=d - 1)] + [1])
+    dup = K >= 2 and seed % 2 == 0      # last term repeats the first: exact cancellation
+    B = int(rng.integers(1, 6))
+    items = []
+    for _ in range(B):
+        terms = [make_random_tt(d, n, r, rng) for r in ranks]
+        coeffs = [float(v) for v in rng.standard_normal(K)]
+        if dup:
+            terms.append(terms[0])
+            coeffs.append(-0.5 * coeffs[0])
+        items.append((terms, coeffs))
+    return items
+
+
+def _check_item(g, ranks, terms, coeffs, delta, floor_c, norms=None, max_rank=None):
+    if norms is None:
+        norms = [tt.tt_norm(t) for t in terms]
+    ref, info = rounding.tt_round_sum(terms, coeffs, delta, floor_c=floor_c, term_norms=norms, max_rank=max_rank)
+    assert rank_window_ok(ranks, info), (ranks, info.ranks)
+    s = info.scale
+    if list(ranks) == list(info.ranks):
+        assert diff_norm(g, ref) <= 1e-10 * s
+    d = len(terms[0])
+    if max_rank is None:
+        x = tt.tt_sum(terms, coeffs)
+        tol = max(delta * info.norm, np.sqrt(d - 1) * info.tau) * (1 + 1e-8) + 1e-13 * s
+        assert diff_norm(x, g) <= tol
+    if delta > 0.0:
+        for k in range(d - 1):
+            U = g[k].reshape(-1, g[k].shape[2])
+            assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-12
+    return info
+
+
+@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("delta", [0.0, 1e-2, 1e-8])
+def test_batch_random_uniform(seed, delta):
+    import paper_2211_08770_b200 as P
+    items = _batch(seed)
+    floor_c = 0.0 if delta == 0.0 else rounding.DEFAULT_FLOOR_C
+    norms = [[tt.tt_norm(t) for t in terms] for terms, _ in items]
+    batch = [([dev(t, nr) for t, nr in zip(terms, nb)], coeffs) for (terms, coeffs), nb in zip(items, norms)]
+    outs = P.tt_round_batch(ctx(), batch, delta, floor_c=floor_c)
+    for (terms, coeffs), nb, o in zip(items, norms, outs):
+        _check_item(o.to_numpy(), o.ranks, terms, coeffs, delta, floor_c, norms=nb)
+
+
+def test_batch_matches_serial_path():
+    """The batched engine and the per-item rounding (TT_B200_BATCH_SERIAL=1) agree."""
+    import paper_2211_08770_b200 as P
+    items = _batch(3) + _batch(3)
+    batch = [([dev(t) for t in terms], coeffs) for terms, coeffs in items]
+    outs = P.tt_round_batch(ctx(), batch, 1e-6)
+    os.environ["TT_B200_BATCH_SERIAL"] = "1"
+    try:
+        ser = P.tt_round_batch(ctx(), batch, 1e-6)
+    finally:
+        del os.environ["TT_B200_BATCH_SERIAL"]
+    for (terms, coeffs), a, b in zip(items, outs, ser):
+        s = sum(abs(c) * tt.tt_norm(t) for t, c in zip(terms, coeffs))
+        assert a.ranks == b.ranks
+        assert diff_norm(a.to_numpy(), b.to_numpy()) <= 1e-10 * s
+
+
+def test_batch_unknown_norms_and_max_rank():
+    import paper_2211_08770_b200 as P
+    items = _batch(5)
+    batch = [([dev(t) for t in terms], coeffs) for terms, coeffs in items]   # norms NaN
+    outs = P.tt_round_batch(ctx(), batch, 1e-8)
+    for (terms, coeffs), o in zip(items, outs):
+        _check_item(o.to_numpy(), o.ranks, terms, coeffs, 1e-8, rounding.DEFAULT_FLOOR_C)
+    outs = P.tt_round_batch(ctx(), batch, 1e-8, max_rank=3)
+    for (terms, coeffs), o in zip(items, outs):
+        assert max(o.ranks) <= 3
+        _check_item(o.to_numpy(), o.ranks, terms, coeffs, 1e-8, rounding.DEFAULT_FLOOR_C, max_rank=3)
+
+
+def test_batch_zero_items():
+    """||x|| = 0 (all coefficients zero) gives the rank-1 zero tensor, next to normal items."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(77)
+    d, n = 5, [6, 9, 4, 7, 5]
+    rk = [1, 4, 6, 5, 3, 1]
+    items = []
+    for b in range(4):
+        terms = [make_random_tt(d, n, rk, rng) for _ in range(2)]
+        coeffs = [0.0, 0.0] if b % 2 else [1.0, 0.5]
+        items.append((terms, coeffs))
+    outs = P.tt_round_batch(ctx(), [([dev(t) for t in ts], cs) for ts, cs in items], 1e-8)
+    for b, ((terms, coeffs), o) in enumerate(zip(items, outs)):
+        if b % 2:
+            assert o.ranks == [1] * (d + 1)
+            assert all(np.all(c == 0.0) for c in o.to_numpy())
+        else:
+            _check_item(o.to_numpy(), o.ranks, terms, coeffs, 1e-8, rounding.DEFAULT_FLOOR_C)
+
+
+def test_batch_c4_shape():
+    """C4 items at full shape (d = 10, n = 32, 4 x rank 16): closed form and oracle parity."""
+    import paper_2211_08770_b200 as P
+    items = make_batch_sums(8)
+    outs = P.tt_round_batch(ctx(), [([dev(t, 1.0) for t in terms], coeffs) for terms, coeffs in items], 1e-6)
+    for b, ((terms, coeffs), o) in enumerate(zip(items, outs)):
+        want = 32 if b % 2 == 0 else 16
+        assert o.ranks == [1] + [want] * 9 + [1]
+        g = o.to_numpy()
+        refx = tt.tt_sum(terms[:2], [1.0, 1.0]) if b % 2 == 0 else terms[0]
+        assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
+        if b < 4:
+            _check_item(g, o.ranks, terms, coeffs, 1e-6, rounding.DEFAULT_FLOOR_C, norms=[1.0] * 4)

@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""Time tt_round_batch on C4-shaped items (d=10, n=32, 4 x rank 16, delta 1e-6).
+
+  python tools/bench_batch.py [--B 512] [--reps 3]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--B", type=int, default=512)
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+    from paper_2211_08770_b200 import _build
+    _build.build_library()
+    import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums
+    t0 = time.time()
+    items = make_batch_sums(args.B)
+    print(f"generated {args.B} items in {time.time() - t0:.1f} s", flush=True)
+    ctx = P.Context(0)
+    batch = [([P.DeviceTT.from_numpy(t, norm=1.0) for t in terms], coeffs) for terms, coeffs in items]
+    outs = P.tt_round_batch(ctx, batch, 1e-6)
+    torch.cuda.synchronize()
+    ranks = [o.ranks for o in outs[:4]]
+    del outs
+    ctx.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.reps):
+        outs = P.tt_round_batch(ctx, batch, 1e-6)
+        del outs
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.reps
+    rep = ctx.profile_report()
+    ctx.profile(False)
+    print(json.dumps({"B": args.B, "ms_per_batch": ms, "roundings_per_s": args.B / ms * 1e3, "ranks": ranks}))
+    for k, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"]):
+        print(f"{k:20s} launches={v['launches']:6d} ms/batch={v['ms'] / args.reps:9.3f} "
+              f"TF={v['flops'] / max(v['ms'], 1e-9) / 1e9:7.3f}")
+
+
+if __name__ == "__main__":
+    main()
