@@ -56,6 +56,7 @@ typedef enum {
 
 typedef struct tt_ctx_s* tt_ctx;
 typedef struct tt_tensor_s* tt_tensor;
+typedef struct tt_batch_s* tt_batch;
 
 /* A borrowed TT-vector.  n[d], r[d+1] and the array core[d] are HOST arrays; core[k]
  * points to DEVICE memory except for tt_upload (host memory).  norm = ||y|| when known
@@ -181,6 +182,31 @@ TT_API tt_status tt_round(tt_ctx ctx, int32_t K, const double* coeff, const tt_v
 TT_API tt_status tt_round_batch(tt_ctx ctx, int32_t B, const int32_t* K, const double* const* coeff,
                          const tt_view* const* terms, const tt_round_opts* opts,
                          tt_tensor* out, int64_t* ranks_out);
+
+/* B independent roundings of equally shaped TT-sums (BASELINE.json configs[3], "C4"), all
+ * in one call of the batched engine (one CTA per item; csrc/batch_round.cu).  Item b rounds
+ * x_b = sum_{l<K} coeff[b*K + l] y_{b,l} (PAPER.md:64 TT-sum, rounding contract as tt_round).
+ *   n[d], r[K*(d+1)]        HOST: mode sizes; ranks of term l at r[l*(d+1) + k] (same for every b).
+ *   core[K*d]               HOST array of DEVICE base pointers: core k of term l of item b is
+ *                           core[l*d + k] + b * item_stride[l*d + k] (doubles), C order as tt_view.
+ *   coeff[B*K]              HOST.
+ *   norms[B*K]              HOST ||y_{b,l}|| for the noise floor s(x), or NULL / NaN entries
+ *                           (then computed on the device).
+ * Supported: d >= 2, every formal rank sum_l r_k^(l) <= 64, K <= 16 (TT_ENOTSUP otherwise:
+ * use tt_round_batch).  The right-to-left QR keeps structural ranks (opts->rank_revealing and
+ * qrcp_theta are ignored); truncation as tt_round.  out: a batch handle owning every result
+ * (free with tt_batch_free); synchronises the stream once per wave of items. */
+TT_API tt_status tt_round_batch_strided(tt_ctx ctx, int32_t B, int32_t K, int32_t d, const int64_t* n,
+                                        const int64_t* r, const double* const* core, const int64_t* item_stride,
+                                        const double* coeff, const double* norms, const tt_round_opts* opts,
+                                        tt_batch* out);
+/* Number of items and order of a batch result. */
+TT_API tt_status tt_batch_shape(tt_batch bt, int32_t* B, int32_t* d);
+/* ranks[b*(d+1) + k] (HOST, B*(d+1)) and norms[b] = ||x_b|| (HOST, B, may be NULL). */
+TT_API tt_status tt_batch_ranks(tt_batch bt, int64_t* ranks, double* norms);
+/* View of item b (0-based); pointers valid until tt_batch_free.  TT_EINDEX if out of range. */
+TT_API tt_status tt_batch_view(tt_batch bt, int32_t b, tt_view* out);
+TT_API tt_status tt_batch_free(tt_ctx ctx, tt_batch bt);
 
 /* ---------------------------------------------------------------- drivers */
 /* Q, R = TT-<kind>(A, delta) (Algs. 1-5, 8).  q_out: HOST array of m

@@ -8,6 +8,7 @@ CPU oracle and has no CPU fallback.
 """
 from . import _native  # noqa: F401
 from .api import (  # noqa: F401
+    BatchTT,
     Context,
     DeviceTT,
     LibTT,
@@ -19,5 +20,6 @@ from .api import (  # noqa: F401
     tt_orth,
     tt_round,
     tt_round_batch,
+    tt_round_batch_strided,
     tt_sum,
 )

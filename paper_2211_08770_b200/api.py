@@ -212,6 +212,88 @@ def tt_round_batch(ctx: Context, items, rel_tol: float, floor_c: float = DEFAULT
     return [LibTT(ctx, C.c_void_p(outs[b])) for b in range(B)]
 
 
+class BatchTT:
+    """Result of tt_round_batch_strided: B rounded TT-vectors owned by one library handle."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p):
+        self.ctx = ctx
+        self.handle = handle
+        B, d = C.c_int32(), C.c_int32()
+        ctx.check(ctx.lib.tt_batch_shape(handle, C.byref(B), C.byref(d)))
+        self.B, self.d = B.value, d.value
+        rk = np.empty((self.B, self.d + 1), dtype=np.int64)
+        nr = np.empty(self.B, dtype=np.float64)
+        if self.B:
+            ctx.check(ctx.lib.tt_batch_ranks(handle, rk.ctypes.data_as(C.POINTER(C.c_int64)),
+                                             nr.ctypes.data_as(C.POINTER(C.c_double))))
+        self.ranks = rk
+        self.norms = nr
+
+    def __len__(self):
+        return self.B
+
+    def view(self, b: int):
+        v = N.TTView()
+        self.ctx.check(self.ctx.lib.tt_batch_view(self.handle, int(b), C.byref(v)))
+        return v
+
+    def cores_torch(self, b: int) -> List[torch.Tensor]:
+        """Zero-copy torch views of item b's cores (valid while this object lives)."""
+        v = self.view(b)
+        out = []
+        for k in range(self.d):
+            shp = (int(v.r[k]), int(v.n[k]), int(v.r[k + 1]))
+            out.append(torch.as_tensor(_CoreArray(v.core[k], shp, self), device=f"cuda:{self.ctx.device}"))
+        return out
+
+    def item_numpy(self, b: int) -> List[np.ndarray]:
+        return [c.cpu().numpy() for c in self.cores_torch(b)]
+
+    def free(self):
+        if self.handle is not None and self.ctx.handle is not None:
+            self.ctx.lib.tt_batch_free(self.ctx.handle, self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def tt_round_batch_strided(ctx: Context, terms, coeffs, rel_tol: float, norms=None,
+                           floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0) -> BatchTT:
+    """terms[l][k]: CUDA float64 tensor (B, r_{k-1}, n_k, r_k) holding core k of term l of every
+    item (item stride = its first-dimension stride); coeffs, norms: (B, K) array-likes (norms
+    optional: computed on the device)."""
+    K = len(terms)
+    d = len(terms[0])
+    B = int(terms[0][0].shape[0])
+    n = (C.c_int64 * d)(*[int(terms[0][k].shape[2]) for k in range(d)])
+    r = (C.c_int64 * (K * (d + 1)))()
+    base = (C.c_void_p * (K * d))()
+    stride = (C.c_int64 * (K * d))()
+    for l in range(K):
+        r[l * (d + 1)] = int(terms[l][0].shape[1])
+        for k in range(d):
+            t = terms[l][k]
+            if not (t.is_cuda and t.dtype == torch.float64 and t.dim() == 4 and t[0].is_contiguous()):
+                raise ValueError("terms[l][k] must be (B, r0, n, r1) float64 CUDA tensors with contiguous items")
+            if int(t.shape[0]) != B:
+                raise ValueError("all term cores need the same batch size B")
+            r[l * (d + 1) + k + 1] = int(t.shape[3])
+            base[l * d + k] = t.data_ptr()
+            stride[l * d + k] = int(t.stride(0)) if B > 1 else 0
+    cf = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64).reshape(B, K))
+    nr = None if norms is None else np.ascontiguousarray(np.asarray(norms, dtype=np.float64).reshape(B, K))
+    o = _opts(rel_tol, floor_c, max_rank, 0.5, False)
+    h = C.c_void_p()
+    ctx.check(ctx.lib.tt_round_batch_strided(
+        ctx.handle, B, K, d, n, r, base, stride, cf.ctypes.data_as(C.POINTER(C.c_double)),
+        None if nr is None else nr.ctypes.data_as(C.POINTER(C.c_double)), C.byref(o), C.byref(h)))
+    return BatchTT(ctx, h)
+
+
 def tt_sum(ctx: Context, terms, coeffs) -> LibTT:
     arr, keep = _views(terms)
     cf = (C.c_double * len(terms))(*[float(c) for c in coeffs])

@@ -216,37 +216,49 @@ __device__ void br_store_stack(const double (&a)[BR_RPL][BR_CPW], BRSmem& sm, in
 
 // target <- H_q target for one stack's reflectors (j = ncol-1 .. 0).  The target's R-block
 // rows live in tr[0/1][s] (rows lane, lane+32), its chunk rows in tc[t][s]; column 8s + warp.
-__device__ void br_stack_apply(double (&tr)[2][BR_CPW], double (&tc)[BR_RPL][BR_CPW], const double* __restrict__ Vq,
+template <int NS>
+__device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], const double* __restrict__ Vq,
                                const double* __restrict__ tq, int q, int ncol, int ntgt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ld = q == 0 ? BR_S0 : BR_CH, roff = q == 0 ? BR_C : 0;
+  // software pipeline: the next reflector's vector is loaded while the current one is applied
+  double ntau = ncol > 0 ? __ldg(tq + ncol - 1) : 0.0;
+  double nv[2 + BR_RPL];
+  auto load_v = [&](int j, double (&dst)[2 + BR_RPL]) {
+    const double* v = Vq + (int64_t)j * ld;
+    if (q == 0) {
+      dst[0] = lane > j ? __ldg(v + lane) : (lane == j ? 1.0 : 0.0);
+      dst[1] = lane + 32 > j ? __ldg(v + lane + 32) : (lane + 32 == j ? 1.0 : 0.0);
+    } else {
+      dst[0] = lane == j ? 1.0 : 0.0;
+      dst[1] = lane + 32 == j ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < BR_RPL; ++t) dst[2 + t] = __ldg(v + roff + 32 * t + lane);
+  };
+  if (ncol > 0) load_v(ncol - 1, nv);
 #pragma unroll 1
   for (int j = ncol - 1; j >= 0; --j) {
-    const double tau = __ldg(tq + j);
-    if (tau == 0.0) continue;
-    const double* v = Vq + (int64_t)j * ld;
-    double v0, v1;
-    if (q == 0) {
-      v0 = lane > j ? __ldg(v + lane) : (lane == j ? 1.0 : 0.0);
-      v1 = lane + 32 > j ? __ldg(v + lane + 32) : (lane + 32 == j ? 1.0 : 0.0);
-    } else {
-      v0 = lane == j ? 1.0 : 0.0;
-      v1 = lane + 32 == j ? 1.0 : 0.0;
+    const double tau = ntau;
+    double cv[2 + BR_RPL];
+#pragma unroll
+    for (int t = 0; t < 2 + BR_RPL; ++t) cv[t] = nv[t];
+    if (j > 0) {
+      ntau = __ldg(tq + j - 1);
+      load_v(j - 1, nv);
     }
-    double vc[BR_RPL];
+    if (tau == 0.0) continue;
 #pragma unroll
-    for (int t = 0; t < BR_RPL; ++t) vc[t] = __ldg(v + roff + 32 * t + lane);
-#pragma unroll
-    for (int s = 0; s < BR_CPW; ++s) {
+    for (int s = 0; s < NS; ++s) {
       if (s * BR_W + warp < ntgt) {
-        double dt = v0 * tr[0][s] + v1 * tr[1][s];
+        double dt = cv[0] * tr[0][s] + cv[1] * tr[1][s];
 #pragma unroll
-        for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * tc[t][s];
+        for (int t = 0; t < BR_RPL; ++t) dt += cv[2 + t] * tc[t][s];
         dt = tau * warp_sum(dt);
-        tr[0][s] -= dt * v0;
-        tr[1][s] -= dt * v1;
+        tr[0][s] -= dt * cv[0];
+        tr[1][s] -= dt * cv[1];
 #pragma unroll
-        for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= dt * vc[t];
+        for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= dt * cv[2 + t];
       }
     }
   }
@@ -254,21 +266,22 @@ __device__ void br_stack_apply(double (&tr)[2][BR_CPW], double (&tc)[BR_RPL][BR_
 
 // out(row, col) = Q [T; 0] for the m-row factor whose stacks are at V (taus Tq, ncol reflectors
 // per stack); T = tr (R-block rows) on entry.  Output address: out[row * rs + col * cs].
-__device__ void br_apply_q(double (&tr)[2][BR_CPW], const double* V, const double* Tq, int64_t m, int ncol, int ntgt,
+template <int NS>
+__device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, const double* Tq, int64_t m, int ncol, int ntgt,
                            double* out, int64_t rs, int64_t cs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nst = br_stacks(m);
-  double tc[BR_RPL][BR_CPW];
+  double tc[BR_RPL][NS];
 #pragma unroll 1
   for (int q = nst - 1; q >= 0; --q) {
 #pragma unroll
     for (int t = 0; t < BR_RPL; ++t)
 #pragma unroll
-      for (int s = 0; s < BR_CPW; ++s) tc[t][s] = 0.0;
+      for (int s = 0; s < NS; ++s) tc[t][s] = 0.0;
     br_stack_apply(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt);
     const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
 #pragma unroll
-    for (int s = 0; s < BR_CPW; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int col = s * BR_W + warp;
       if (col < ntgt) {
 #pragma unroll
@@ -288,7 +301,7 @@ __device__ void br_apply_q(double (&tr)[2][BR_CPW], const double* V, const doubl
 // Flat-tree QR of an m x ncol matrix given by elem(row, col) (zero outside); reflectors to V,
 // taus to Tq; on return sm.Rs holds R (upper triangle; strictly lower part zero).
 template <class Elem>
-__device__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem& sm, double* V, double* Tq) {
+__device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem& sm, double* V, double* Tq) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nst = br_stacks(m);
   double a[BR_RPL][BR_CPW];
@@ -413,7 +426,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
 // round-robin pair ordering, one warp per pair; V (nc x nc) in sm.Aux.  On return
 // sm.sig[j] = j-th largest singular value, sm.perm[j] = its column; returns false on
 // non-convergence (|<c_i,c_j>| <= sqrt(rows) u ||c_i|| ||c_j||).
-__device__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
+__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
   const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
@@ -432,41 +445,64 @@ __device__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
     __syncthreads();
 #pragma unroll 1
     for (int r = 0; r < kk - 1; ++r) {
-      for (int q = warp; q < kk / 2; q += BR_W) {
+      // this warp's (up to 4) disjoint pairs of the round, processed together for ILP
+      constexpr int NP = BR_C / 2 / BR_W;
+      int pa[NP], pb[NP];
+      double x0[NP], x1[NP], y0[NP], y1[NP], al[NP], be[NP], ga[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        const int q = warp + i * BR_W;
         int p0, p1;
         if (q == 0) { p0 = kk - 1; p1 = r; }
         else { p0 = (r + q) % (kk - 1); p1 = (r + kk - 1 - q) % (kk - 1); }
-        if (p0 >= nc || p1 >= nc) continue;
         if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
-        double* ca = sm.Rs + p0 * BR_C;
-        double* cb = sm.Rs + p1 * BR_C;
-        const double x0 = ca[lane], x1 = ca[lane + 32], y0 = cb[lane], y1 = cb[lane + 32];
-        double al = x0 * x0 + x1 * x1, be = y0 * y0 + y1 * y1, ga = x0 * y0 + x1 * y1;
+        const bool act = q < kk / 2 && p1 < nc;
+        pa[i] = act ? p0 : -1;
+        pb[i] = p1;
+        const double* ca = sm.Rs + (act ? p0 : 0) * BR_C;
+        const double* cb = sm.Rs + (act ? p1 : 0) * BR_C;
+        x0[i] = act ? ca[lane] : 0.0;
+        x1[i] = act ? ca[lane + 32] : 0.0;
+        y0[i] = act ? cb[lane] : 0.0;
+        y1[i] = act ? cb[lane + 32] : 0.0;
+        al[i] = x0[i] * x0[i] + x1[i] * x1[i];
+        be[i] = y0[i] * y0[i] + y1[i] * y1[i];
+        ga[i] = x0[i] * y0[i] + x1[i] * y1[i];
+      }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          al[i] += __shfl_xor_sync(0xffffffffu, al[i], o);
+          be[i] += __shfl_xor_sync(0xffffffffu, be[i], o);
+          ga[i] += __shfl_xor_sync(0xffffffffu, ga[i], o);
         }
-        if (ga != 0.0 && al > negl && be > negl && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-          const double zeta = (be - al) / (2.0 * ga);
+      }
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        if (pa[i] >= 0 && ga[i] != 0.0 && al[i] > negl && be[i] > negl && fabs(ga[i]) > tol * sqrt(al[i] * be[i])) {
+          const double zeta = (be[i] - al[i]) / (2.0 * ga[i]);
           const double az = fabs(zeta);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (az > 1e150 ? 2.0 * az : az + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          ca[lane] = cs * x0 - sn * y0;
-          ca[lane + 32] = cs * x1 - sn * y1;
-          cb[lane] = sn * x0 + cs * y0;
-          cb[lane + 32] = sn * x1 + cs * y1;
-          double* va = sm.Aux + p0 * BR_C;
-          double* vbp = sm.Aux + p1 * BR_C;
+          const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+          double* ca = sm.Rs + pa[i] * BR_C;
+          double* cb = sm.Rs + pb[i] * BR_C;
+          ca[lane] = cs * x0[i] - sn * y0[i];
+          ca[lane + 32] = cs * x1[i] - sn * y1[i];
+          cb[lane] = sn * x0[i] + cs * y0[i];
+          cb[lane + 32] = sn * x1[i] + cs * y1[i];
+          double* va = sm.Aux + pa[i] * BR_C;
+          double* vbp = sm.Aux + pb[i] * BR_C;
           const double a0 = va[lane], a1 = va[lane + 32], b0 = vbp[lane], b1 = vbp[lane + 32];
           va[lane] = cs * a0 - sn * b0;
           va[lane + 32] = cs * a1 - sn * b1;
           vbp[lane] = sn * a0 + cs * b0;
           vbp[lane + 32] = sn * a1 + cs * b1;
-          if (lane == 0) sm.flag = 1;
+          any = true;
         }
       }
+      if (any && lane == 0) sm.flag = 1;
       __syncthreads();
     }
     conv = (sm.flag == 0);
@@ -491,6 +527,41 @@ __device__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
   }
   __syncthreads();
   return conv;
+}
+
+// Output core k = Q_Y [U_rho; 0] (U_rho = normalised Jacobi columns, rows <= 64), row-major.
+template <int NS>
+__device__ void br_out_core(BRSmem& sm, int rho, int cp, int64_t p, const double* YV, const double* YT, double* ok) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double tr[2][NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int col = s * BR_W + warp;
+    const bool ok2 = col < rho;
+    const int pc = ok2 ? sm.perm[col] : 0;
+    const double inv = (ok2 && sm.sig[col] > 0.0) ? 1.0 / sm.sig[col] : 0.0;
+    tr[0][s] = (ok2 && lane < cp) ? sm.Rs[pc * BR_C + lane] * inv : 0.0;
+    tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Rs[pc * BR_C + lane + 32] * inv : 0.0;
+  }
+  br_apply_q<NS>(tr, YV, YT, p, cp, rho, ok, rho, 1);
+}
+
+// Z_{k+1} = H_{k+1} [(S_rho V_rho^T)^T; 0] (m1 x rho, column-major ld m1).
+template <int NS>
+__device__ void br_next_core(BRSmem& sm, int rho, int cp, int64_t m1, int c1, const double* V, const double* Tq,
+                             double* dst) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double tr[2][NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int col = s * BR_W + warp;
+    const bool ok2 = col < rho;
+    const int pc = ok2 ? sm.perm[col] : 0;
+    const double sg = ok2 ? sm.sig[col] : 0.0;
+    tr[0][s] = (ok2 && lane < cp) ? sm.Aux[pc * BR_C + lane] * sg : 0.0;
+    tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Aux[pc * BR_C + lane + 32] * sg : 0.0;
+  }
+  br_apply_q<NS>(tr, V, Tq, m1, c1, rho, dst, 1, m1);
 }
 
 __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
@@ -589,17 +660,8 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
   // ---- output core k = Q_Y U_rho ((rho_{k-1} n_k) x rho, row-major)
   double* ok = out + S->ooff[kc];
   if (tall) {
-    double tr[2][BR_CPW];
-#pragma unroll
-    for (int s = 0; s < BR_CPW; ++s) {
-      const int col = s * BR_W + warp;
-      const bool ok2 = col < rho;
-      const int pc = ok2 ? sm.perm[col] : 0;
-      const double inv = (ok2 && sm.sig[col] > 0.0) ? 1.0 / sm.sig[col] : 0.0;
-      tr[0][s] = (ok2 && lane < cp) ? sm.Rs[pc * BR_C + lane] * inv : 0.0;
-      tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Rs[pc * BR_C + lane + 32] * inv : 0.0;
-    }
-    br_apply_q(tr, YV, YT, p, cp, rho, ok, rho, 1);
+    if (rho <= BR_C / 2) br_out_core<BR_CPW / 2>(sm, rho, cp, p, YV, YT, ok);
+    else br_out_core<BR_CPW>(sm, rho, cp, p, YV, YT, ok);
   } else {
     for (int idx = tid; idx < p * rho; idx += BR_T) {
       const int row = idx / rho, col = idx % rho;
@@ -608,25 +670,14 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
     }
   }
   // ---- Z_{k+1} = H_{k+1} [(S V^T)^T; 0]   (m_{k+1} x rho, column-major)
-  {
-    const int kn = kc + 1;  // core index of core k+1
-    const int64_t m1 = (int64_t)S->n[kn] * S->Rp[k + 1];
-    const int c1 = S->R[k];
-    double tr[2][BR_CPW];
-#pragma unroll
-    for (int s = 0; s < BR_CPW; ++s) {
-      const int col = s * BR_W + warp;
-      const bool ok2 = col < rho;
-      const int pc = ok2 ? sm.perm[col] : 0;
-      const double sg = ok2 ? sm.sig[col] : 0.0;
-      tr[0][s] = (ok2 && lane < cp) ? sm.Aux[pc * BR_C + lane] * sg : 0.0;
-      tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Aux[pc * BR_C + lane + 32] * sg : 0.0;
-    }
-    double* dst = (k + 1 == d) ? out + S->ooff[kn] : A.Z + (int64_t)b * 2 * S->zstride + ((k + 1) & 1) * S->zstride;
-    const double* V = A.V + (int64_t)b * S->vstride + S->voff[kn];
-    const double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kn];
-    br_apply_q(tr, V, Tq, m1, c1, rho, dst, 1, m1);
-  }
+  const int kn = kc + 1;  // core index of core k+1
+  const int64_t m1 = (int64_t)S->n[kn] * S->Rp[k + 1];
+  const int c1 = S->R[k];
+  double* dst = (k + 1 == d) ? out + S->ooff[kn] : A.Z + (int64_t)b * 2 * S->zstride + ((k + 1) & 1) * S->zstride;
+  const double* V = A.V + (int64_t)b * S->vstride + S->voff[kn];
+  const double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kn];
+  if (rho <= BR_C / 2) br_next_core<BR_CPW / 2>(sm, rho, cp, m1, c1, V, Tq, dst);
+  else br_next_core<BR_CPW>(sm, rho, cp, m1, c1, V, Tq, dst);
 }
 
 // Copy item b's cores from the worst-case workspace to the exact-size arena.
@@ -648,36 +699,36 @@ bool batch_uniform_supported(int B, const std::vector<SumInput>& items, std::str
   auto no = [&](const char* w) { if (why) *why = w; return false; };
   if (B < 1) return no("empty batch");
   const SumInput& f = items[0];
-  const int d = f.d, K = f.K();
+  for (const SumInput& it : items)
+    if (it.d != f.d || it.K() != f.K() || it.n != f.n || it.r != f.r) return no("items differ in shape");
+  return batch_shape_supported(f.d, f.K(), f.r, why);
+}
+
+bool batch_shape_supported(int d, int K, const std::vector<std::vector<int64_t>>& r, std::string* why) {
+  auto no = [&](const char* w) { if (why) *why = w; return false; };
   if (d < 2) return no("d < 2");
   if (d > BR_MAXD) return no("d > 64");
   if (K < 1 || K > BR_MAXK) return no("K outside 1..16");
-  std::vector<int64_t> R((size_t)d + 1, 0);
-  for (int k = 0; k <= d; ++k)
-    for (int l = 0; l < K; ++l) R[(size_t)k] += f.r[(size_t)l][(size_t)k];
-  for (int k = 1; k < d; ++k)
-    if (R[(size_t)k] > BR_C) return no("formal rank > 64");
-  for (const SumInput& it : items) {
-    if (it.d != d || it.K() != K || it.n != f.n || it.r != f.r) return no("items differ in shape");
+  for (int k = 1; k < d; ++k) {
+    int64_t R = 0;
+    for (int l = 0; l < K; ++l) R += r[(size_t)l][(size_t)k];
+    if (R > BR_C) return no("formal rank > 64");
   }
   return true;
 }
 
-void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
-                         int64_t* ranks_out) {
-  const int B = (int)items.size();
-  const SumInput& f = items[0];
-  const int d = f.d, K = f.K();
+void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut& res) {
+  const int B = in.B, d = in.d, K = in.K;
   // ---------------------------------------------------------------- shape tables (uniform)
   BRShape sh;
   std::memset(&sh, 0, sizeof(sh));
   sh.d = d;
   sh.K = K;
-  for (int k = 0; k < d; ++k) sh.n[k] = (int)f.n[(size_t)k];
+  for (int k = 0; k < d; ++k) sh.n[k] = (int)in.n[(size_t)k];
   for (int k = 0; k <= d; ++k) {
     int s = 0;
     for (int l = 0; l < K; ++l) {
-      sh.r[l][k] = (int)f.r[(size_t)l][(size_t)k];
+      sh.r[l][k] = (int)in.r[(size_t)l][(size_t)k];
       sh.off[k][l] = s;
       s += sh.r[l][k];
     }
@@ -722,25 +773,24 @@ void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const t
   const bool keep_all = (o.rel_tol == 0.0);
   std::vector<double> scale((size_t)B, 0.0);
   {
-    std::vector<std::pair<int, int>> need;
-    for (int b = 0; b < B; ++b)
-      for (int l = 0; l < K; ++l)
-        if (!(items[(size_t)b].norm[(size_t)l] == items[(size_t)b].norm[(size_t)l])) need.push_back({b, l});
-    std::vector<double> nn(need.size());
+    std::vector<int64_t> need;  // b * K + l with unknown ||y_l||
+    for (int64_t q = 0; q < (int64_t)B * K; ++q)
+      if (!(in.norm[(size_t)q] == in.norm[(size_t)q])) need.push_back(q);
+    std::vector<double> nn(need.size(), 0.0);
     if (!need.empty() && !keep_all && o.floor_c > 0.0) {
       DotBatch db;
       db.d = d;
-      db.n = f.n;
+      db.n = in.n;
       db.P = (int)need.size();
-      for (auto& bl : need) {
-        const SumInput& it = items[(size_t)bl.first];
+      for (int64_t q : need) {
+        const int l = (int)(q % K);
         for (int k = 0; k < d; ++k) {
-          db.xc.push_back(it.core[(size_t)bl.second][(size_t)k]);
-          db.yc.push_back(it.core[(size_t)bl.second][(size_t)k]);
+          db.xc.push_back(in.tab[(size_t)q * d + k]);
+          db.yc.push_back(in.tab[(size_t)q * d + k]);
         }
         for (int k = 0; k <= d; ++k) {
-          db.xr.push_back(it.r[(size_t)bl.second][(size_t)k]);
-          db.yr.push_back(it.r[(size_t)bl.second][(size_t)k]);
+          db.xr.push_back(in.r[(size_t)l][(size_t)k]);
+          db.yr.push_back(in.r[(size_t)l][(size_t)k]);
         }
       }
       DBuf dd(ctx, need.size());
@@ -748,37 +798,35 @@ void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const t
       d2h_small(ctx, nn.data(), dd.p, nn.size());
       for (double& x : nn) x = std::sqrt(std::max(x, 0.0));
     }
-    size_t q = 0;
-    for (int b = 0; b < B; ++b)
-      for (int l = 0; l < K; ++l) {
-        double nl = items[(size_t)b].norm[(size_t)l];
-        if (!(nl == nl)) nl = (q < nn.size()) ? nn[q++] : 0.0;
-        scale[(size_t)b] += std::fabs(items[(size_t)b].coef[(size_t)l]) * nl;
-      }
+    size_t q2 = 0;
+    for (int64_t q = 0; q < (int64_t)B * K; ++q) {
+      double nl = in.norm[(size_t)q];
+      if (!(nl == nl)) nl = nn[q2++];
+      scale[(size_t)(q / K)] += std::fabs(in.coef[(size_t)q]) * nl;
+    }
   }
   // ---------------------------------------------------------------- device tables
-  BBuf dsh;
+  BBuf dsh, dtab, dcoef, dscale;
   dsh.upload(ctx, &sh, sizeof(sh));
-  std::vector<const double*> tab((size_t)B * K * d);
-  std::vector<double> coef((size_t)B * K);
-  for (int b = 0; b < B; ++b)
-    for (int l = 0; l < K; ++l) {
-      coef[(size_t)b * K + l] = items[(size_t)b].coef[(size_t)l];
-      for (int k = 0; k < d; ++k) tab[((size_t)b * K + l) * d + k] = items[(size_t)b].core[(size_t)l][(size_t)k];
-    }
-  BBuf dtab, dcoef, dscale;
-  dtab.upload(ctx, tab.data(), tab.size() * sizeof(double*));
-  dcoef.upload(ctx, coef.data(), coef.size() * sizeof(double));
+  dtab.upload(ctx, in.tab.data(), in.tab.size() * sizeof(double*));
+  dcoef.upload(ctx, in.coef.data(), in.coef.size() * sizeof(double));
   dscale.upload(ctx, scale.data(), scale.size() * sizeof(double));
   // ---------------------------------------------------------------- waves
   size_t free_b = 0, total_b = 0;
   TTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double budget = std::min<double>(0.5 * (double)free_b, 48e9);
-  int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
+  const int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
   const size_t smem = sizeof(BRSmem);
   TTB_CUDA(cudaFuncSetAttribute(br_r2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   TTB_CUDA(cudaFuncSetAttribute(br_l2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int done = 0;
+  res.B = B;
+  res.d = d;
+  res.n = in.n;
+  res.ranks.assign((size_t)B * (d + 1), 1);
+  res.norm.assign((size_t)B, 0.0);
+  res.core.assign((size_t)B * d, nullptr);
+  res.wave_first.clear();
+  res.arenas.clear();
   try {
     for (int w0 = 0; w0 < B; w0 += W) {
       const int nb = std::min(W, B - w0);
@@ -802,7 +850,7 @@ void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const t
       for (int kc = d - 1; kc >= 1; --kc) {
         const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
         const double c = sh.R[kc];
-        double rl = 0.0;  // assembly flops per row and column: r_k of the column's term
+        double rl = 0.0;  // panel assembly: 2 r_k^(l) flops per element of term l's columns
         for (int l = 0; l < K; ++l) rl += (double)sh.r[l][kc] * sh.r[l][kc + 1];
         const double mm = (double)m;
         const double fl = nb * (2.0 * mm * rl + (mm >= c ? 2.0 * mm * c * c - 2.0 * c * c * c / 3.0
@@ -846,7 +894,8 @@ void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const t
         (void)cudaGetLastError();
         fail(TT_ENOMEM, "batch result arena allocation failed");
       }
-      int64_t* refs = new int64_t(nb);
+      res.arenas.push_back(arena);
+      res.wave_first.push_back(w0);
       BBuf ddst, dsz, dooff;
       ddst.upload(ctx, dst.data(), dst.size() * sizeof(int64_t));
       dsz.upload(ctx, sz.data(), sz.size() * sizeof(int64_t));
@@ -857,28 +906,59 @@ void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const t
                                                              static_cast<const int64_t*>(dsz.p), d,
                                                              static_cast<double*>(arena)));
       for (int b = 0; b < nb; ++b) {
-        tt_tensor tt = new tt_tensor_s();
-        tt->d = d;
-        tt->n = f.n;
-        tt->r.assign(hr.begin() + (size_t)b * (d + 1), hr.begin() + (size_t)(b + 1) * (d + 1));
-        tt->core.resize((size_t)d);
-        tt->core_c.resize((size_t)d);
-        for (int kc = 0; kc < d; ++kc) {
-          tt->core[(size_t)kc] = static_cast<double*>(arena) + dst[(size_t)b * d + kc];
-          tt->core_c[(size_t)kc] = tt->core[(size_t)kc];
-        }
-        tt->norm = hsc[(size_t)b * 4 + 0];
-        tt->arena = arena;
-        tt->arena_refs = refs;
-        out[w0 + b] = tt;
-        if (ranks_out)
-          for (int k = 0; k <= d; ++k) ranks_out[(size_t)(w0 + b) * (d + 1) + k] = tt->r[(size_t)k];
-        ++done;
+        for (int k = 0; k <= d; ++k) res.ranks[(size_t)(w0 + b) * (d + 1) + k] = hr[(size_t)b * (d + 1) + k];
+        for (int kc = 0; kc < d; ++kc)
+          res.core[(size_t)(w0 + b) * d + kc] = static_cast<double*>(arena) + dst[(size_t)b * d + kc];
+        res.norm[(size_t)(w0 + b)] = hsc[(size_t)b * 4 + 0];
       }
     }
   } catch (...) {
-    for (int b = 0; b < done; ++b) { tensor_free(ctx, out[b]); out[b] = nullptr; }
+    for (void* p : res.arenas) cudaFreeAsync(p, ctx->stream);
+    res.arenas.clear();
     throw;
+  }
+}
+
+void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
+                         int64_t* ranks_out) {
+  BatchDesc in;
+  const SumInput& f = items[0];
+  in.B = (int)items.size();
+  in.K = f.K();
+  in.d = f.d;
+  in.n = f.n;
+  in.r = f.r;
+  const int B = in.B, K = in.K, d = in.d;
+  in.tab.resize((size_t)B * K * d);
+  in.coef.resize((size_t)B * K);
+  in.norm.resize((size_t)B * K);
+  for (int b = 0; b < B; ++b)
+    for (int l = 0; l < K; ++l) {
+      in.coef[(size_t)b * K + l] = items[(size_t)b].coef[(size_t)l];
+      in.norm[(size_t)b * K + l] = items[(size_t)b].norm[(size_t)l];
+      for (int k = 0; k < d; ++k) in.tab[((size_t)b * K + l) * d + k] = items[(size_t)b].core[(size_t)l][(size_t)k];
+    }
+  BatchOut res;
+  run_batch(ctx, in, o, res);
+  // one refcount per wave arena, shared by that wave's tensors
+  for (size_t w = 0; w < res.arenas.size(); ++w) {
+    const int b0 = res.wave_first[w];
+    const int b1 = (w + 1 < res.arenas.size()) ? res.wave_first[w + 1] : B;
+    int64_t* refs = new int64_t(b1 - b0);
+    for (int b = b0; b < b1; ++b) {
+      tt_tensor tt = new tt_tensor_s();
+      tt->d = d;
+      tt->n = f.n;
+      tt->r.assign(res.ranks.begin() + (size_t)b * (d + 1), res.ranks.begin() + (size_t)(b + 1) * (d + 1));
+      tt->core.assign(res.core.begin() + (size_t)b * d, res.core.begin() + (size_t)(b + 1) * d);
+      tt->core_c.assign(tt->core.begin(), tt->core.end());
+      tt->norm = res.norm[(size_t)b];
+      tt->arena = res.arenas[w];
+      tt->arena_refs = refs;
+      out[b] = tt;
+      if (ranks_out)
+        for (int k = 0; k <= d; ++k) ranks_out[(size_t)b * (d + 1) + k] = tt->r[(size_t)k];
+    }
   }
 }
 

@@ -7,10 +7,32 @@
 
 namespace ttb {
 
-// All items share d, n, K and the term ranks; d >= 2; formal ranks <= 64; K <= 16.
+// B items sharing d, n, K and the term ranks.  tab[(b*K + l)*d + k] = device pointer to core k
+// of term l of item b; coef / norm [b*K + l] (norm NaN = unknown, computed on the device).
+struct BatchDesc {
+  int B = 0, K = 0, d = 0;
+  std::vector<int64_t> n;
+  std::vector<std::vector<int64_t>> r;  // r[l][0..d]
+  std::vector<const double*> tab;
+  std::vector<double> coef, norm;
+};
+
+// Results: item b's core k at core[b*d + k] (inside arenas[w] of its wave), ranks[b*(d+1) + k].
+struct BatchOut {
+  int B = 0, d = 0;
+  std::vector<int64_t> n;
+  std::vector<int64_t> ranks;
+  std::vector<double*> core;
+  std::vector<double> norm;
+  std::vector<void*> arenas;   // one exact-size allocation per wave (caller frees)
+  std::vector<int> wave_first; // first item of each wave
+};
+
+// d >= 2, every formal rank R_k <= 64, K <= 16.
+bool batch_shape_supported(int d, int K, const std::vector<std::vector<int64_t>>& r, std::string* why);
 bool batch_uniform_supported(int B, const std::vector<SumInput>& items, std::string* why);
-// out[b] = TT-round(items[b]) for every b (library-owned tensors sharing one arena per wave);
-// ranks_out (host, B*(d+1)) optional.  Throws ttb::Error.
+void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut& res);
+// out[b] = TT-round(items[b]) as library tensors (sharing one refcounted arena per wave).
 void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
                          int64_t* ranks_out);
 

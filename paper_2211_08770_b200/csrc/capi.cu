@@ -13,6 +13,10 @@
 
 using namespace ttb;
 
+struct tt_batch_s {
+  BatchOut res;
+};
+
 namespace {
 
 template <typename F>
@@ -315,6 +319,84 @@ tt_status tt_round_batch(tt_ctx ctx, int32_t B, const int32_t* K, const double* 
       throw;
     }
   });
+}
+
+tt_status tt_round_batch_strided(tt_ctx ctx, int32_t B, int32_t K, int32_t d, const int64_t* n, const int64_t* r,
+                                 const double* const* core, const int64_t* item_stride, const double* coeff,
+                                 const double* norms, const tt_round_opts* opts, tt_batch* out) {
+  if (!ctx || !out || B < 0 || K < 1 || d < 1 || !n || !r || !core || !item_stride || (B > 0 && !coeff))
+    return TT_EINVAL;
+  return guarded(ctx, [&] {
+    BatchDesc in;
+    in.B = B;
+    in.K = K;
+    in.d = d;
+    in.n.assign(n, n + d);
+    in.r.resize((size_t)K);
+    for (int l = 0; l < K; ++l) {
+      in.r[(size_t)l].assign(r + (size_t)l * (d + 1), r + (size_t)(l + 1) * (d + 1));
+      if (in.r[(size_t)l][0] != 1 || in.r[(size_t)l][(size_t)d] != 1) fail(TT_ESHAPE, "boundary ranks must be 1");
+      for (int k = 0; k < d; ++k) {
+        if (n[k] < 1 || in.r[(size_t)l][(size_t)k] < 1) fail(TT_ESHAPE, "mode sizes and ranks must be >= 1");
+        if (!core[(size_t)l * d + k]) fail(TT_EINVAL, "null core base pointer");
+      }
+    }
+    std::string why;
+    if (!batch_shape_supported(d, K, in.r, &why)) fail(TT_ENOTSUP, "tt_round_batch_strided: " + why);
+    in.tab.resize((size_t)B * K * d);
+    for (int64_t b = 0; b < B; ++b)
+      for (int l = 0; l < K; ++l)
+        for (int k = 0; k < d; ++k) {
+          const size_t q = (size_t)l * d + k;
+          in.tab[((size_t)b * K + l) * d + k] = core[q] + b * item_stride[q];
+        }
+    in.coef.assign(coeff, coeff + (size_t)B * K);
+    if (norms) in.norm.assign(norms, norms + (size_t)B * K);
+    else in.norm.assign((size_t)B * K, NAN);
+    tt_batch bt = new tt_batch_s();
+    try {
+      if (B > 0) run_batch(ctx, in, resolve(opts), bt->res);
+      else { bt->res.d = d; bt->res.n = in.n; }
+    } catch (...) {
+      delete bt;
+      throw;
+    }
+    *out = bt;
+  });
+}
+
+tt_status tt_batch_shape(tt_batch bt, int32_t* B, int32_t* d) {
+  if (!bt) return TT_EINVAL;
+  if (B) *B = bt->res.B;
+  if (d) *d = bt->res.d;
+  return TT_OK;
+}
+
+tt_status tt_batch_ranks(tt_batch bt, int64_t* ranks, double* norms) {
+  if (!bt) return TT_EINVAL;
+  if (ranks) std::memcpy(ranks, bt->res.ranks.data(), sizeof(int64_t) * bt->res.ranks.size());
+  if (norms) std::memcpy(norms, bt->res.norm.data(), sizeof(double) * bt->res.norm.size());
+  return TT_OK;
+}
+
+tt_status tt_batch_view(tt_batch bt, int32_t b, tt_view* out) {
+  if (!bt || !out) return TT_EINVAL;
+  if (b < 0 || b >= bt->res.B) return TT_EINDEX;
+  const int d = bt->res.d;
+  out->d = d;
+  out->n = bt->res.n.data();
+  out->r = bt->res.ranks.data() + (size_t)b * (d + 1);
+  out->core = const_cast<const double* const*>(bt->res.core.data() + (size_t)b * d);
+  out->norm = bt->res.norm[(size_t)b];
+  return TT_OK;
+}
+
+tt_status tt_batch_free(tt_ctx ctx, tt_batch bt) {
+  if (!ctx) return TT_EINVAL;
+  if (!bt) return TT_OK;
+  for (void* p : bt->res.arenas) cudaFreeAsync(p, ctx->stream);
+  delete bt;
+  return TT_OK;
 }
 
 tt_status tt_orth(tt_ctx ctx, tt_orth_kind kind, int32_t m, const tt_view* a, const tt_orth_opts* opts,

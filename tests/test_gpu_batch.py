@@ -144,3 +144,51 @@ def test_batch_c4_shape():
         assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
         if b < 4:
             _check_item(g, o.ranks, terms, coeffs, 1e-6, rounding.DEFAULT_FLOOR_C, norms=[1.0] * 4)
+
+
+def _stack(items):
+    """Per-item (terms, coeffs) -> stacked (B, r0, n, r1) CUDA tensors per (term, core)."""
+    import torch
+    K, d = len(items[0][0]), len(items[0][0][0])
+    cores = [[torch.from_numpy(np.ascontiguousarray(np.stack([it[0][l][k] for it in items]))).cuda()
+              for k in range(d)] for l in range(K)]
+    coeffs = np.array([it[1] for it in items], dtype=np.float64)
+    return cores, coeffs
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 6, 9, 12])
+def test_batch_strided_api(seed):
+    """tt_round_batch_strided (base pointer + item stride per term core, one result handle)
+    equals the oracle item by item; norms given and unknown."""
+    import paper_2211_08770_b200 as P
+    items = _batch(seed)
+    cores, coeffs = _stack(items)
+    norms = np.array([[tt.tt_norm(t) for t in terms] for terms, _ in items])
+    for nr in (norms, None):
+        res = P.tt_round_batch_strided(ctx(), cores, coeffs, 1e-8, norms=nr)
+        assert len(res) == len(items)
+        for b, (terms, cf) in enumerate(items):
+            g = res.item_numpy(b)
+            assert [1] + [c.shape[2] for c in g] == list(res.ranks[b])
+            _check_item(g, list(res.ranks[b]), terms, cf, 1e-8, rounding.DEFAULT_FLOOR_C, norms=list(norms[b]))
+
+
+def test_batch_strided_c4_stacked_generator():
+    """C4 through the stacked generator and the strided API: closed-form ranks 32/16, distance
+    to y1 + [b even] y2, and oracle parity on a sample."""
+    import torch
+    import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums_stacked
+    B = 40
+    cores, coeffs = make_batch_sums_stacked(B)
+    dc = [[torch.from_numpy(c).cuda() for c in term] for term in cores]
+    res = P.tt_round_batch_strided(ctx(), dc, coeffs, 1e-6, norms=np.ones((B, 4)))
+    for b in range(B):
+        want = 32 if b % 2 == 0 else 16
+        assert list(res.ranks[b]) == [1] + [want] * 9 + [1]
+    for b in (0, 1, 17, 38, 39):
+        terms = [[cores[s][k][b] for k in range(10)] for s in range(4)]
+        g = res.item_numpy(b)
+        refx = tt.tt_sum(terms[:2], [1.0, 1.0]) if b % 2 == 0 else terms[0]
+        assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
+        _check_item(g, list(res.ranks[b]), terms, list(coeffs[b]), 1e-6, rounding.DEFAULT_FLOOR_C, norms=[1.0] * 4)

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Time tt_round_batch on C4-shaped items (d=10, n=32, 4 x rank 16, delta 1e-6).
+"""Time tt_round_batch_strided on C4 items (d=10, n=32, 4 x rank 16, delta 1e-6).
 
   python tools/bench_batch.py [--B 512] [--reps 3]
 """
@@ -18,26 +18,28 @@ def main():
     ap.add_argument("--B", type=int, default=512)
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
+    import numpy as np
     import torch
     from paper_2211_08770_b200 import _build
     _build.build_library()
     import paper_2211_08770_b200 as P
-    from ttinputs import make_batch_sums
+    from ttinputs import make_batch_sums_stacked
     t0 = time.time()
-    items = make_batch_sums(args.B)
+    cores, coeffs = make_batch_sums_stacked(args.B)
     print(f"generated {args.B} items in {time.time() - t0:.1f} s", flush=True)
     ctx = P.Context(0)
-    batch = [([P.DeviceTT.from_numpy(t, norm=1.0) for t in terms], coeffs) for terms, coeffs in items]
-    outs = P.tt_round_batch(ctx, batch, 1e-6)
+    dc = [[torch.from_numpy(c).cuda() for c in term] for term in cores]
+    norms = np.ones((args.B, 4))
+    res = P.tt_round_batch_strided(ctx, dc, coeffs, 1e-6, norms=norms)
     torch.cuda.synchronize()
-    ranks = [o.ranks for o in outs[:4]]
-    del outs
+    ranks = res.ranks[:4].tolist()
+    del res
     ctx.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.reps):
-        outs = P.tt_round_batch(ctx, batch, 1e-6)
-        del outs
+        res = P.tt_round_batch_strided(ctx, dc, coeffs, 1e-6, norms=norms)
+        del res
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.reps

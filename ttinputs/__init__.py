@@ -12,6 +12,7 @@ from .generate import (  # noqa: F401
     config_spec,
     make_shared_tail_set,
     make_batch_sums,
+    make_batch_sums_stacked,
     make_random_tt,
     tt_ranks_capped,
 )

@@ -137,21 +137,53 @@ def make_batch_sums(B: int, d: int = 10, n: int = 32, r: int = 16, seed: int = S
                     start: int = 0):
     """C4: x_b = y_1 + w_b y_2 + eps3 y_3 + eps4 y_4 with unit-norm y.
 
-    w_b = 1 for even b, omega_odd for odd b.  Draw order: b-major, then s = 1..4, then the
-    cores of y_{b,s} (core 1 first).  Items [start, start+B) of the full stream are returned
-    (the stream is re-drawn from the beginning so any slice is reproducible).
-    Returns a list of (terms, coeffs) with terms a list of 4 core-lists.
+    w_b = 1 for even b, omega_odd for odd b.  Each y has random right-orthonormal cores 2..d
+    and a Gaussian first core scaled to unit Frobenius norm (norm exactly 1 by construction).
+    Draw order: b-major, then s = 1..4, then the cores of y_{b,s} (core 1 first); items
+    [start, start+B) of the full stream are returned.  Same bytes as make_batch_sums_stacked
+    (this is its per-item view).  Returns a list of (terms, coeffs), terms a list of 4 core-lists.
     """
+    cores, coeffs = make_batch_sums_stacked(B, d, n, r, seed, eps3, eps4, omega_odd, start)
+    return [([[cores[s][k][b] for k in range(d)] for s in range(4)], [float(v) for v in coeffs[b]])
+            for b in range(B)]
+
+
+def _qfactor_batched(g: np.ndarray) -> np.ndarray:
+    """_qfactor over a stack (..., M, N): LAPACK per matrix, same result as one at a time."""
+    q, r = np.linalg.qr(g, mode="reduced")
+    s = np.sign(np.diagonal(r, axis1=-2, axis2=-1)).copy()
+    s[s == 0] = 1.0
+    return q * s[..., None, :]
+
+
+def make_batch_sums_stacked(B: int, d: int = 10, n: int = 32, r: int = 16, seed: int = SEED_BASE + 4,
+                            eps3: float = 1e-9, eps4: float = 1e-10, omega_odd: float = 1e-9,
+                            start: int = 0):
+    """Same bytes as make_batch_sums(B, ..., start), stacked for the batched API: returns
+    (cores, coeffs) with cores[s][k] of shape (B, r_{k-1}, n, r_k) = core k of y_{b,s} for
+    b in [start, start+B), coeffs (B, 4).  One standard_normal draw in the documented order
+    (b-major, then s, then the cores of y_{b,s}), then the per-core QRs batched."""
     ranks = tt_ranks_capped(d, [n] * d, r)
+    sizes = [ranks[k] * n * ranks[k + 1] for k in range(d)]
+    per = sum(sizes)
     rng = _rng(seed)
-    out = []
-    for b in range(start + B):
-        ys = [make_random_tt(d, n, ranks, rng, unit_right_orth=True) for _ in range(4)]
-        if b < start:
-            continue
-        w = 1.0 if b % 2 == 0 else omega_odd
-        out.append((ys, [1.0, w, eps3, eps4]))
-    return out
+    g = rng.standard_normal((start + B) * 4 * per)[start * 4 * per:].reshape(B, 4, per)
+    cores = [[None] * d for _ in range(4)]
+    off = 0
+    for k in range(d):
+        blk = g[:, :, off:off + sizes[k]].reshape(B, 4, ranks[k], n, ranks[k + 1])
+        off += sizes[k]
+        if k == 0:
+            c = blk / np.linalg.norm(blk.reshape(B, 4, -1), axis=2)[:, :, None, None, None]
+        else:
+            r0, r1 = ranks[k], ranks[k + 1]
+            q = _qfactor_batched(np.swapaxes(blk.reshape(B, 4, r0, n * r1), -1, -2))  # (B,4,n r1,r0)
+            c = np.swapaxes(q, -1, -2).reshape(B, 4, r0, n, r1)
+        for s in range(4):
+            cores[s][k] = np.ascontiguousarray(c[:, s])
+    w = np.where((np.arange(start, start + B) % 2) == 0, 1.0, omega_odd)
+    coeffs = np.stack([np.ones(B), w, np.full(B, eps3), np.full(B, eps4)], axis=1)
+    return cores, coeffs
 
 
 @dataclass(frozen=True)
