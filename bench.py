@@ -1,17 +1,21 @@
 #!/usr/bin/env python
-"""Benchmark of the TT-orthogonalization hot path on B200 (contract: one JSON line on rank 0).
+"""Benchmark of the TT-rounding hot path on B200 (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], "C2"): MGS and MGS2 on m = 30 TT-vectors, d = 8, n = 32,
-ranks 10, kappa = 1e10 (shared-tail mixing), rounding tolerance
-1e-10, plus the TT-dot Gram matrix of the 30 inputs.  One step = tt_orth(MGS) +
-tt_orth(MGS2) + tt_gram: 90 TT-roundings, 2 x 465 + 435 + ... TT-dots.  Metric: TT-roundings
-per second (whole job), with fp64 TFLOP/s of the dominant kernel against the measured FP64
-DMMA peak and Gram pairs/s reported alongside.
+Workload (BASELINE.json configs[3], "C4" -- the configuration the metric "TT-roundings/sec ...
+vs B200 peak" is quoted on): a batch of 4096 independent TT-roundings, item b the TT-sum
+y1 + w_b y2 + 1e-9 y3 + 1e-10 y4 of four unit-norm rank-16 TT-vectors (d = 10, n = 32; formal
+rank 64), relative tolerance 1e-6 (ranks 32 / 16).  One
+step = one tt_round_batch_strided call over the batch (right-to-left Householder sweep, norm and
+threshold, left-to-right truncated SVDs, for every item).  The TT-dot Gram matrix of C3
+(configs[2], 50 TT-vectors d = 16, n = 64, r = 20: 1275 pairs) and the C2 (configs[1])
+TT-MGS + TT-MGS2 drivers are timed alongside and reported in their own keys.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--batch B]
 
-N > 1 (torchrun): every rank runs an independent replica (its own seed) -- the MGS chain
-does not shard; scaling "weak", time = max over ranks.
+N > 1 (torchrun, one process per GPU): the 4096-item batch is split into N contiguous slices
+(no data-path collective: the roundings are independent); time = max over ranks; "scaling":
+"strong".  --impl reference times the CPU oracle (oracle/, the slow fp64 reference written from
+the paper) on a bounded sample of the same items.
 """
 from __future__ import annotations
 
@@ -28,8 +32,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TT-roundings/sec (fp64 TFLOP/s vs B200 FP64 peak; TT-dot Gram pairs/sec alongside)"
-FP64_PEAK_TFLOPS = 37.07   # measured: tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak_r01.json)
-CPU_SAMPLE_M = 16          # oracle sample: MGS on the first 16 C2 vectors
+# measured on this pool's B200 by tools/fp64_peak.cu (profiles/fp64_peak_r01.json): FP64 FMA
+# pipe (DFMA, what the batched rounding kernels issue) and FP64 tensor (DMMA m8n8k4)
+FP64_DFMA_PEAK_TFLOPS = 34.18
+FP64_DMMA_PEAK_TFLOPS = 37.07
+C4_DELTA = 1e-6
+C4_BATCH = 4096
+CPU_SAMPLE_SECONDS = 15.0
 
 
 def _peaks():
@@ -89,51 +98,67 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def build_inputs(seed_offset: int):
-    from ttinputs import CONFIGS, make_shared_tail_set
-    c = CONFIGS["C2"]
-    st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed + seed_offset)
-    return c, st
+def _slice(batch: int, rank: int, world: int):
+    base, rem = divmod(batch, world)
+    start = rank * base + min(rank, rem)
+    return start, base + (1 if rank < rem else 0)
+
+
+def _blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info()) or 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _config(batch: int, world: int):
+    return {"workload": f"C4 (BASELINE.json configs[3]): batch of {batch} independent TT-roundings, "
+                        "each the TT-sum of 4 unit-norm rank-16 TT-vectors (d=10, n=32, formal rank 64)",
+            "batch": batch, "d": 10, "n": 32, "terms": 4, "term_rank": 16, "delta": C4_DELTA,
+            "floor_c": 2048.0, "parallelism": f"batch split x{world}",
+            "l2": "inputs (8.7 GB at B=4096) exceed L2; L2 also flushed (256 MB write) between timed steps"}
+
+
+def oracle_sample(seconds: float, offset: int = 0):
+    """The CPU oracle (as it stands) on C4 items in order until `seconds` have elapsed."""
+    from oracle import rounding
+    from ttinputs import make_batch_sums
+    done, t0 = 0, time.perf_counter()
+    while True:
+        items = make_batch_sums(4, start=offset + done)
+        for terms, coeffs in items:
+            rounding.tt_round_sum(terms, coeffs, C4_DELTA, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=[1.0] * 4)
+        done += len(items)
+        if time.perf_counter() - t0 >= seconds:
+            break
+    # generation of the 4-item blocks is timed too but is < 1 % of the oracle's time
+    return done, time.perf_counter() - t0
 
 
 def run_reference(args, rank: int, world: int):
-    """Reference arm: the CPU oracle (as it stands) on a bounded sample of the workload."""
+    """Reference arm: the CPU oracle on a bounded sample of the C4 items (rank 0 only)."""
     if rank != 0:
         return
-    import numpy as np
-    from oracle import orth, tt
-    c, st = build_inputs(0)
-    A = st.tensors[:CPU_SAMPLE_M]
-    times = []
+    times, counts = [], []
     for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        orth.orth("mgs", A, c.delta)
-        t1 = time.perf_counter()
+        n, t = oracle_sample(CPU_SAMPLE_SECONDS / max(args.steps, 1) if it >= args.warmup else 1.0)
         if it >= args.warmup:
-            times.append(t1 - t0)
+            times.append(t)
+            counts.append(n)
     T = sum(times)
-    value = CPU_SAMPLE_M * len(times) / T
-    sample = f"oracle TT-MGS on the first {CPU_SAMPLE_M} of the 30 C2 vectors ({CPU_SAMPLE_M} roundings per step)"
+    value = sum(counts) / T
+    cores = _blas_threads()
+    sample = (f"oracle (numpy/LAPACK fp64) TT-rounding of the first {max(counts)} C4 items per step, "
+              f"{T:.1f} s over {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 (BASELINE.json configs[1]) MGS sample", "m": c.m, "d": c.d, "n": c.n,
-                       "r": c.r, "kappa": c.kappa, "delta": c.delta},
-            "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": os.cpu_count(), "kind": "oracle",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args.batch, world),
+            "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "roundings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def cpu_baseline():
-    from oracle import orth
-    c, st = build_inputs(0)
-    A = st.tensors[:CPU_SAMPLE_M]
-    t0 = time.perf_counter()
-    orth.orth("mgs", A, c.delta)
-    t = time.perf_counter() - t0
-    return {"value": CPU_SAMPLE_M / t, "unit": "roundings/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"oracle TT-MGS on the first {CPU_SAMPLE_M} of the 30 C2 vectors, {t:.1f} s"}
 
 
 def main():
@@ -142,7 +167,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=C4_BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the Gram / driver side measurements")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -152,118 +179,44 @@ def main():
         run_reference(args, rank, world)
         return
 
+    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2211_08770_b200 import _build
     _build.build_library()
     import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums_stacked
 
     torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     stream = torch.cuda.current_stream(local_rank)
-    # the three independent parts of a step (MGS chain, MGS2 chain, Gram matrix) run
-    # concurrently, one library context + CUDA stream + host thread each
-    ctxs = [P.Context(local_rank, stream=torch.cuda.Stream(local_rank)) for _ in range(3)]
-    c, st = build_inputs(rank)
-    A = [P.DeviceTT.from_numpy(a) for a in st.tensors]
-    rounds_per_step = 3 * c.m
-    gram_pairs = c.m * (c.m + 1) // 2
+    ctx = P.Context(local_rank, stream=stream)
 
-    def step(inputs):
-        fork = torch.cuda.Event()
-        fork.record(stream)
-        res = [None, None, None]
-        err = []
-
-        def part(i):
-            try:
-                cx = ctxs[i]
-                cx.stream.wait_event(fork)
-                with torch.cuda.stream(cx.stream):
-                    if i == 0:
-                        res[0] = P.tt_orth(cx, "mgs", inputs, c.delta)
-                    elif i == 1:
-                        res[1] = P.tt_orth(cx, "mgs2", inputs, c.delta)
-                    else:
-                        res[2] = P.tt_gram(cx, inputs)
-            except Exception as e:  # surfaced after join
-                err.append(e)
-
-        th = [threading.Thread(target=part, args=(i,)) for i in range(3)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-        if err:
-            raise err[0]
-        for cx in ctxs:  # join: the caller's stream waits for all three
-            ev = torch.cuda.Event()
-            ev.record(cx.stream)
-            stream.wait_event(ev)
-        (Q1, R1, r1), (Q2, R2, r2), G = res
-        return Q1, Q2, R1, R2, G, r1["rounding_calls"] + r2["rounding_calls"]
-
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=f"cuda:{local_rank}")
+    start, B = _slice(args.batch, rank, world)
+    cores_h, coeffs = make_batch_sums_stacked(B, start=start)
+    norms = np.ones((B, 4))
+    cores = [[torch.from_numpy(c).to(dev) for c in term] for term in cores_h]
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def step(inp):
+        return P.tt_round_batch_strided(ctx, inp, coeffs, C4_DELTA, norms=norms)
+
     for _ in range(args.warmup):
-        out = step(A)
-        del out
+        res = step(cores)
+        del res
     torch.cuda.synchronize()
 
     # ------------------------------------------------------------ timed (device-resident inputs)
     sampler = ClockSampler(local_rank)
     sampler.start()
-    launches0 = sum(cx.launches for cx in ctxs)
+    launches0 = ctx.launches
     step_ms = []
-    calls = 0
-    for _ in range(args.steps):
-        flush.zero_()  # L2 flush between timed iterations (256 MB > 126 MB L2), not timed
-        torch.cuda.synchronize()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        out = step(A)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
-        calls += out[-1]
-        del out
-    barrier()
-    launches = sum(cx.launches for cx in ctxs) - launches0
-    clocks = sampler.stop()
-    for cx in ctxs:
-        cx.profile(False)
-    # Per-kernel durations: events around every launch of one extra step run on ONE stream
-    # (under the 3-stream overlap an event pair would also time the other streams' work).
-    cx0 = ctxs[0]
-    cx0.profile(True)
-    with torch.cuda.stream(cx0.stream):
-        P.tt_orth(cx0, "mgs", A, c.delta)
-        P.tt_orth(cx0, "mgs2", A, c.delta)
-        P.tt_gram(cx0, A)
-    prof = cx0.profile_report()
-    cx0.profile(False)
-    t_local = sum(step_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([t_local], device=f"cuda:{local_rank}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-    else:
-        t_max = t_local
-    assert calls == rounds_per_step * args.steps, (calls, rounds_per_step)
-    value = rounds_per_step * args.steps * world / t_max
-
-    # ------------------------------------------------------------ end to end (host buffers)
-    host = [[torch.from_numpy(x).pin_memory() for x in a] for a in st.tensors]
-    h2d = sum(x.numel() * 8 for a in host for x in a)
-    e2e_ms = []
-    d2h = 0
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -271,64 +224,138 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        dev_in = [P.DeviceTT([x.to(f"cuda:{local_rank}", non_blocking=True) for x in a]) for a in host]
-        Q1, Q2, R1, R2, G, _ = step(dev_in)
-        outs = [q.to_numpy() for q in Q1 + Q2]
-        Gh = G.cpu()
+        res = step(cores)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        ranks = res.ranks
+        del res
+    barrier()
+    launches = ctx.launches - launches0
+    clocks = sampler.stop()
+    t_local = sum(step_ms) / 1e3
+    if world > 1:
+        t = torch.tensor([t_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    else:
+        t_max = t_local
+    value = args.batch * args.steps / t_max
+    rank_ok = bool(np.all(ranks[:, 1:-1] == np.where((np.arange(start, start + B) % 2 == 0), 32, 16)[:, None]))
+
+    # ------------------------------------------------------------ per-kernel profile (one extra step)
+    ctx.profile(True)
+    res = step(cores)
+    prof = ctx.profile_report()
+    ctx.profile(False)
+    out_doubles = res.total_doubles()
+    del res
+
+    # ------------------------------------------------------------ end to end (pinned host buffers)
+    host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores_h]
+    h2d = sum(x.numel() * 8 for term in host for x in term)
+    out_host = torch.empty(out_doubles + 1024, dtype=torch.float64).pin_memory()
+    e2e_ms, d2h = [], 0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dev_in = [[x.to(dev, non_blocking=True) for x in term] for term in host]
+        res = step(dev_in)
+        cnt = res.download(out_host)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-        d2h = sum(x.nbytes for q in outs for x in q) + Gh.numel() * 8 + R1.nbytes + R2.nbytes
-        del Q1, Q2, outs
+        d2h = cnt * 8 + res.ranks.nbytes
+        del res, dev_in
     te = sum(e2e_ms) / 1e3
     if world > 1:
-        t = torch.tensor([te], device=f"cuda:{local_rank}", dtype=torch.float64)
+        t = torch.tensor([te], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
-    e2e_value = rounds_per_step * args.steps * world / te
+    e2e_value = args.batch * args.steps / te
 
     # ------------------------------------------------------------ roofline of the dominant kernel
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     total_ms = sum(v["ms"] for v in prof.values())
-    peaks = _peaks()
-    if dom["flops"] > 0:
-        achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "peak_source": "measured FP64 DMMA (tools/fp64_peak.cu, profiles/fp64_peak_r01.json)"}
-    else:
-        achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("_fallback") else "")}
-    roof.update({"kernel": dom_name, "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / dom["launches"],
-                 "share_of_kernel_time": dom["ms"] / total_ms})
+    achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": None,
+            "peak_source": "measured FP64 FMA (DFMA) throughput, tools/fp64_peak.cu -> profiles/fp64_peak_r01.json "
+                           "(nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TF)",
+            "kernel": dom_name, "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / dom["launches"],
+            "share_of_kernel_time": dom["ms"] / total_ms,
+            "work_model": "LAPACK-standard flop counts of the operations each launch performs (DESIGN.md §7)"}
     all_flops = sum(v["flops"] for v in prof.values())
     kernel_classes = {k: {"launches": v["launches"], "ms": round(v["ms"], 3), "share": round(v["ms"] / total_ms, 4),
                           "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 else 0.0}
                       for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
 
+    # ------------------------------------------------------------ alongside: Gram (C3), drivers (C2)
+    extras = {}
+    if not args.no_extras:
+        from ttinputs import CONFIGS, make_shared_tail_set
+        c3 = CONFIGS["C3"]
+        st3 = make_shared_tail_set(c3.d, c3.n, c3.r, c3.m, c3.kappa, c3.seed + rank)
+        A3 = [P.DeviceTT.from_numpy(a) for a in st3.tensors]
+        G = P.tt_gram(ctx, A3)
+        torch.cuda.synchronize()
+        gms = []
+        for _ in range(3):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            G = P.tt_gram(ctx, A3)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            gms.append(e0.elapsed_time(e1))
+        pairs = c3.m * (c3.m + 1) // 2
+        gerr = float(np.linalg.norm(G.cpu().numpy() - st3.gram_exact()) / np.linalg.norm(st3.gram_exact()))
+        extras["gram_pairs_per_s"] = pairs / (statistics.median(gms) * 1e-3)
+        extras["gram"] = {"workload": "C3 (configs[2]) TT-dot Gram matrix, m=50, d=16, n=64, r=20",
+                          "pairs": pairs, "ms": statistics.median(gms), "rel_err_vs_MtM": gerr}
+        c2 = CONFIGS["C2"]
+        st2 = make_shared_tail_set(c2.d, c2.n, c2.r, c2.m, c2.kappa, c2.seed + rank)
+        A2 = [P.DeviceTT.from_numpy(a) for a in st2.tensors]
+        P.tt_orth(ctx, "mgs", A2, c2.delta)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, _, r1 = P.tt_orth(ctx, "mgs", A2, c2.delta)
+        _, _, r2 = P.tt_orth(ctx, "mgs2", A2, c2.delta)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        calls = r1["rounding_calls"] + r2["rounding_calls"]
+        extras["drivers_c2"] = {"workload": "C2 (configs[1]) TT-MGS + TT-MGS2, m=30, d=8, n=32, r=10",
+                                "roundings": calls, "ms": e0.elapsed_time(e1),
+                                "roundings_per_s": calls / (e0.elapsed_time(e1) * 1e-3)}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 (BASELINE.json configs[1]): TT-MGS + TT-MGS2 + TT-dot Gram",
-                       "m": c.m, "d": c.d, "n": c.n, "r": c.r, "kappa": c.kappa, "delta": c.delta,
-                       "floor_c": 2048.0, "roundings_per_step": rounds_per_step, "gram_pairs_per_step": gram_pairs,
-                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"replicas x{world}",
-                       "streams": "MGS | MGS2 | Gram concurrently on 3 CUDA streams"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(args.batch, world),
             "e2e": {"value": e2e_value, "unit": "roundings/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": roof,
-            "kernel_profile": "CUDA events around every launch of one extra step on a single stream",
-            "fp64_tflops_step": all_flops / t_local / 1e12,
-            "gram_pairs_per_s": gram_pairs * args.steps * world / t_max,
+            "kernel_profile": "CUDA events around every launch of one extra step (ctx stream)",
+            "fp64_tflops_step": all_flops / (t_local / args.steps) / 1e12,
             "kernel_classes": kernel_classes,
+            "ranks_closed_form_ok": rank_ok,
             "clocks": clocks,
         }
+        line.update(extras)
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline()
+            n, t = oracle_sample(CPU_SAMPLE_SECONDS)
+            line["cpu_baseline"] = {"value": n / t, "unit": "roundings/s", "cores": _blas_threads(), "kind": "oracle",
+                                    "sample": f"oracle TT-rounding of the first {n} C4 items, {t:.1f} s "
+                                              "(numpy/LAPACK fp64, BLAS threads = cores)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -206,6 +206,10 @@ TT_API tt_status tt_batch_shape(tt_batch bt, int32_t* B, int32_t* d);
 TT_API tt_status tt_batch_ranks(tt_batch bt, int64_t* ranks, double* norms);
 /* View of item b (0-based); pointers valid until tt_batch_free.  TT_EINDEX if out of range. */
 TT_API tt_status tt_batch_view(tt_batch bt, int32_t b, tt_view* out);
+/* Copy every result core to host (HOST, capacity doubles): items in order, each item's cores
+ * in order, each core (r_{k-1}, n_k, r_k) C order; *count = doubles in the batch (also set
+ * when capacity is too small: TT_EINVAL).  Synchronises. */
+TT_API tt_status tt_batch_download(tt_ctx ctx, tt_batch bt, double* host, int64_t capacity, int64_t* count);
 TT_API tt_status tt_batch_free(tt_ctx ctx, tt_batch bt);
 
 /* ---------------------------------------------------------------- drivers */

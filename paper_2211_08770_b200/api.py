@@ -246,6 +246,21 @@ class BatchTT:
             out.append(torch.as_tensor(_CoreArray(v.core[k], shp, self), device=f"cuda:{self.ctx.device}"))
         return out
 
+    def total_doubles(self) -> int:
+        cnt = C.c_int64()
+        st = self.ctx.lib.tt_batch_download(self.ctx.handle, self.handle, None, 0, C.byref(cnt))
+        if st not in (0, 1):
+            self.ctx.check(st)
+        return int(cnt.value)
+
+    def download(self, host: torch.Tensor) -> int:
+        """Copy every result core into the (pinned) float64 CPU tensor `host`, items in order;
+        returns the number of doubles written."""
+        cnt = C.c_int64()
+        self.ctx.check(self.ctx.lib.tt_batch_download(self.ctx.handle, self.handle, C.c_void_p(host.data_ptr()),
+                                                      int(host.numel()), C.byref(cnt)))
+        return int(cnt.value)
+
     def item_numpy(self, b: int) -> List[np.ndarray]:
         return [c.cpu().numpy() for c in self.cores_torch(b)]
 

@@ -827,6 +827,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   res.core.assign((size_t)B * d, nullptr);
   res.wave_first.clear();
   res.arenas.clear();
+  res.arena_size.clear();
   try {
     for (int w0 = 0; w0 < B; w0 += W) {
       const int nb = std::min(W, B - w0);
@@ -895,6 +896,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         fail(TT_ENOMEM, "batch result arena allocation failed");
       }
       res.arenas.push_back(arena);
+      res.arena_size.push_back(tot);
       res.wave_first.push_back(w0);
       BBuf ddst, dsz, dooff;
       ddst.upload(ctx, dst.data(), dst.size() * sizeof(int64_t));

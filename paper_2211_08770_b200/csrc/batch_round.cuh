@@ -25,6 +25,7 @@ struct BatchOut {
   std::vector<double*> core;
   std::vector<double> norm;
   std::vector<void*> arenas;   // one exact-size allocation per wave (caller frees)
+  std::vector<int64_t> arena_size;  // doubles in each arena (items in order, cores in order)
   std::vector<int> wave_first; // first item of each wave
 };
 

@@ -391,6 +391,23 @@ tt_status tt_batch_view(tt_batch bt, int32_t b, tt_view* out) {
   return TT_OK;
 }
 
+tt_status tt_batch_download(tt_ctx ctx, tt_batch bt, double* host, int64_t capacity, int64_t* count) {
+  if (!ctx || !bt || (!host && capacity > 0)) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    int64_t tot = 0;
+    for (int64_t a : bt->res.arena_size) tot += a;
+    if (count) *count = tot;
+    if (tot > capacity) fail(TT_EINVAL, "tt_batch_download: host buffer too small");
+    int64_t off = 0;
+    for (size_t w = 0; w < bt->res.arenas.size(); ++w) {
+      TTB_CUDA(cudaMemcpyAsync(host + off, bt->res.arenas[w], sizeof(double) * (size_t)bt->res.arena_size[w],
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      off += bt->res.arena_size[w];
+    }
+    TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 tt_status tt_batch_free(tt_ctx ctx, tt_batch bt) {
   if (!ctx) return TT_EINVAL;
   if (!bt) return TT_OK;

@@ -167,7 +167,12 @@ def make_batch_sums_stacked(B: int, d: int = 10, n: int = 32, r: int = 16, seed:
     sizes = [ranks[k] * n * ranks[k + 1] for k in range(d)]
     per = sum(sizes)
     rng = _rng(seed)
-    g = rng.standard_normal((start + B) * 4 * per)[start * 4 * per:].reshape(B, 4, per)
+    skip = start * 4 * per
+    while skip > 0:  # advance the stream past items [0, start) without holding them
+        c = min(skip, 1 << 26)
+        rng.standard_normal(c)
+        skip -= c
+    g = rng.standard_normal(B * 4 * per).reshape(B, 4, per)
     cores = [[None] * d for _ in range(4)]
     off = 0
     for k in range(d):
