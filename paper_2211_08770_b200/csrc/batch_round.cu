@@ -25,6 +25,9 @@
 // the same SVDs).  Supported shapes: d >= 2, every formal rank R_k <= 64, K <= 16 terms.
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "batch_round.cuh"
@@ -41,6 +44,7 @@ constexpr int BR_CH = 128;             // chunk rows held in registers
 constexpr int BR_RPL = BR_CH / 32;     // chunk rows per lane
 constexpr int BR_CPW = BR_C / BR_W;    // columns per warp
 constexpr int BR_S0 = BR_C + BR_CH;    // rows of stack 0 (R block + first chunk)
+constexpr int BR_SL = 8;               // reflectors per staged slice of the applications
 constexpr int BR_MAXD = 64;
 constexpr int BR_MAXK = 16;
 constexpr int BR_JAC_SWEEPS = 60;
@@ -56,6 +60,13 @@ struct BRShape {
   int64_t toff[BR_MAXD];          // core index kc: offset of its taus (per item)
   int64_t ooff[BR_MAXD];          // core index kc: worst-case output core offset (per item)
   int64_t vstride, tstride, ystride, ytstride, zstride, ostride;
+};
+
+struct LBuf {  // long long device buffer (debug counters)
+  tt_ctx ctx = nullptr;
+  long long* p = nullptr;
+  void alloc(tt_ctx c, size_t n) { ctx = c; TTB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(long long), c->stream)); }
+  ~LBuf() { if (p) cudaFreeAsync(p, ctx->stream); }
 };
 
 struct BRArgs {
@@ -77,6 +88,7 @@ struct BRArgs {
   int64_t max_rank;
   int keep_all;
   int item0;                   // global index of this wave's first item
+  long long* dbg;              // TT_B200_BR_DEBUG: CTA 0 phase cycle counters (else null)
 };
 
 __host__ __device__ inline int br_stacks(int64_t m) {
@@ -96,6 +108,33 @@ __device__ __forceinline__ double sel(const double (&a)[N], int j) {
   return r;
 }
 
+// ---- 1-D bulk copies global -> shared (TMA engine) completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
+}
+
+// Reflector slices (8 consecutive reflectors of one stack, stored contiguously) staged in shared
+// memory by the TMA engine, double-buffered; the next slice is in flight while one is applied.
+struct VStage {
+  alignas(16) double buf[2][BR_SL * BR_S0];
+  uint64_t bar[2];
+  uint32_t phase[2];  // (kept per thread, uniform)
+};
+
 // Shared-memory work areas of one CTA.
 struct BRSmem {
   double Rs[BR_C * BR_C];     // R block (column-major, ld 64); Jacobi matrix in the l2r kernel
@@ -108,6 +147,7 @@ struct BRSmem {
   int cterm[BR_C], ca[BR_C];
   int flag;
   int rho;
+  VStage vst;
 };
 
 // Flat-tree Householder QR step over one stack: R block in sm.Rs (rows 0..63, column-major;
@@ -216,49 +256,60 @@ __device__ void br_store_stack(const double (&a)[BR_RPL][BR_CPW], BRSmem& sm, in
 
 // target <- H_q target for one stack's reflectors (j = ncol-1 .. 0).  The target's R-block
 // rows live in tr[0/1][s] (rows lane, lane+32), its chunk rows in tc[t][s]; column 8s + warp.
+// target <- H_q target for one stack's reflectors (j = ncol-1 .. 0), reflector vectors read
+// from the staged slices.  The target's R-block rows live in tr[0/1][s] (rows lane, lane+32),
+// its chunk rows in tc[t][s]; column 8s + warp.
 template <int NS>
 __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], const double* __restrict__ Vq,
-                               const double* __restrict__ tq, int q, int ncol, int ntgt) {
+                               const double* __restrict__ tq, int q, int ncol, int ntgt, VStage& vs,
+                               uint32_t (&ph)[2]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ld = q == 0 ? BR_S0 : BR_CH, roff = q == 0 ? BR_C : 0;
-  // software pipeline: the next reflector's vector is loaded while the current one is applied
-  double ntau = ncol > 0 ? __ldg(tq + ncol - 1) : 0.0;
-  double nv[2 + BR_RPL];
-  auto load_v = [&](int j, double (&dst)[2 + BR_RPL]) {
-    const double* v = Vq + (int64_t)j * ld;
-    if (q == 0) {
-      dst[0] = lane > j ? __ldg(v + lane) : (lane == j ? 1.0 : 0.0);
-      dst[1] = lane + 32 > j ? __ldg(v + lane + 32) : (lane + 32 == j ? 1.0 : 0.0);
-    } else {
-      dst[0] = lane == j ? 1.0 : 0.0;
-      dst[1] = lane + 32 == j ? 1.0 : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < BR_RPL; ++t) dst[2 + t] = __ldg(v + roff + 32 * t + lane);
+  const int nsl = (ncol + BR_SL - 1) / BR_SL;
+  auto issue = [&](int sl, int b) {
+    const int j0 = sl * BR_SL, cnt = min(BR_SL, ncol - j0);
+    bulk_load(vs.buf[b], Vq + (int64_t)j0 * ld, (uint32_t)(cnt * ld * sizeof(double)), &vs.bar[b]);
   };
-  if (ncol > 0) load_v(ncol - 1, nv);
+  __syncthreads();  // previous users of both buffers are done
+  if (threadIdx.x == 0) issue(nsl - 1, 0);
 #pragma unroll 1
-  for (int j = ncol - 1; j >= 0; --j) {
-    const double tau = ntau;
-    double cv[2 + BR_RPL];
-#pragma unroll
-    for (int t = 0; t < 2 + BR_RPL; ++t) cv[t] = nv[t];
-    if (j > 0) {
-      ntau = __ldg(tq + j - 1);
-      load_v(j - 1, nv);
+  for (int sl = nsl - 1, b = 0; sl >= 0; --sl, b ^= 1) {
+    if (sl > 0) {
+      __syncthreads();  // everyone finished reading buffer b^1 (slice sl+1)
+      if (threadIdx.x == 0) issue(sl - 1, b ^ 1);
     }
-    if (tau == 0.0) continue;
+    mbar_wait(&vs.bar[b], ph[b]);
+    ph[b] ^= 1u;
+    const double* sv = vs.buf[b];
+    const int j0 = sl * BR_SL, j1 = min(j0 + BR_SL, ncol);
+#pragma unroll 1
+    for (int j = j1 - 1; j >= j0; --j) {
+      const double tau = __ldg(tq + j);
+      if (tau == 0.0) continue;
+      const double* v = sv + (j - j0) * ld;
+      double v0, v1;
+      if (q == 0) {
+        v0 = lane > j ? v[lane] : (lane == j ? 1.0 : 0.0);
+        v1 = lane + 32 > j ? v[lane + 32] : (lane + 32 == j ? 1.0 : 0.0);
+      } else {
+        v0 = lane == j ? 1.0 : 0.0;
+        v1 = lane + 32 == j ? 1.0 : 0.0;
+      }
+      double vc[BR_RPL];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s * BR_W + warp < ntgt) {
-        double dt = cv[0] * tr[0][s] + cv[1] * tr[1][s];
+      for (int t = 0; t < BR_RPL; ++t) vc[t] = v[roff + 32 * t + lane];
 #pragma unroll
-        for (int t = 0; t < BR_RPL; ++t) dt += cv[2 + t] * tc[t][s];
-        dt = tau * warp_sum(dt);
-        tr[0][s] -= dt * cv[0];
-        tr[1][s] -= dt * cv[1];
+      for (int s = 0; s < NS; ++s) {
+        if (s * BR_W + warp < ntgt) {
+          double dt = v0 * tr[0][s] + v1 * tr[1][s];
 #pragma unroll
-        for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= dt * cv[2 + t];
+          for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * tc[t][s];
+          dt = tau * warp_sum(dt);
+          tr[0][s] -= dt * v0;
+          tr[1][s] -= dt * v1;
+#pragma unroll
+          for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= dt * vc[t];
+        }
       }
     }
   }
@@ -267,10 +318,11 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
 // out(row, col) = Q [T; 0] for the m-row factor whose stacks are at V (taus Tq, ncol reflectors
 // per stack); T = tr (R-block rows) on entry.  Output address: out[row * rs + col * cs].
 template <int NS>
-__device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, const double* Tq, int64_t m, int ncol, int ntgt,
-                           double* out, int64_t rs, int64_t cs) {
+__device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, const double* Tq, int64_t m, int ncol,
+                                        int ntgt, double* out, int64_t rs, int64_t cs, VStage& vs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nst = br_stacks(m);
+  uint32_t ph[2] = {vs.phase[0], vs.phase[1]};
   double tc[BR_RPL][NS];
 #pragma unroll 1
   for (int q = nst - 1; q >= 0; --q) {
@@ -278,7 +330,7 @@ __device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, co
     for (int t = 0; t < BR_RPL; ++t)
 #pragma unroll
       for (int s = 0; s < NS; ++s) tc[t][s] = 0.0;
-    br_stack_apply(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt);
+    br_stack_apply(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt, vs, ph);
     const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -296,14 +348,19 @@ __device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, co
       }
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) { vs.phase[0] = ph[0]; vs.phase[1] = ph[1]; }
+  __syncthreads();
 }
 
 // Flat-tree QR of an m x ncol matrix given by elem(row, col) (zero outside); reflectors to V,
 // taus to Tq; on return sm.Rs holds R (upper triangle; strictly lower part zero).
 template <class Elem>
-__device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem& sm, double* V, double* Tq) {
+__device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem& sm, double* V, double* Tq,
+                                   long long* dbg) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nst = br_stacks(m);
+  long long c0 = clock64();
   double a[BR_RPL][BR_CPW];
 #pragma unroll 1
   for (int q = 0; q < nst; ++q) {
@@ -324,8 +381,12 @@ __device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem
       }
     }
     __syncthreads();
+    const long long c1 = clock64();
     br_stack_qr(a, sm, ncol, Tq + (int64_t)q * BR_C);
+    const long long c2 = clock64();
     br_store_stack(a, sm, q, ncol, V + br_stack_off(q, ncol));
+    if (dbg && tid == 0) { dbg[0] += c1 - c0; dbg[1] += c2 - c1; dbg[2] += clock64() - c2; }
+    c0 = clock64();
   }
 }
 
@@ -346,9 +407,16 @@ struct PanelElem {
     const int rl = sh->r[l][kc + 1], o = sh->off[kc + 1][l];
     const double* xp = X + ((int64_t)aa * n + i) * rl;
     const double* lp = LT + (int64_t)o * BR_C + bp;
-    double s = 0.0;
-    for (int be = 0; be < rl; ++be) s += lp[be * BR_C] * __ldg(xp + be);
-    return s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four chains: loads in flight together
+    int be = 0;
+    for (; be + 4 <= rl; be += 4) {
+      s0 += lp[be * BR_C] * __ldg(xp + be);
+      s1 += lp[(be + 1) * BR_C] * __ldg(xp + be + 1);
+      s2 += lp[(be + 2) * BR_C] * __ldg(xp + be + 2);
+      s3 += lp[(be + 3) * BR_C] * __ldg(xp + be + 3);
+    }
+    for (; be < rl; ++be) s0 += lp[be * BR_C] * __ldg(xp + be);
+    return (s0 + s1) + (s2 + s3);
   }
 };
 
@@ -412,7 +480,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
   PanelElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, sm.cterm, sm.ca, kc, d, n, Rpk, last ? 1 : 0};
   double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
   double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kc];
-  br_qr(e, m, c, sm, V, Tq);
+  br_qr(e, m, c, sm, V, Tq, (A.dbg && blockIdx.x == 0) ? A.dbg : nullptr);
   // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
   double* Lout = A.L + (int64_t)b * 2 * BR_C * BR_C + (k & 1) * BR_C * BR_C;
   const int rows = S->Rp[k - 1];
@@ -445,64 +513,53 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
     __syncthreads();
 #pragma unroll 1
     for (int r = 0; r < kk - 1; ++r) {
-      // this warp's (up to 4) disjoint pairs of the round, processed together for ILP
-      constexpr int NP = BR_C / 2 / BR_W;
-      int pa[NP], pb[NP];
-      double x0[NP], x1[NP], y0[NP], y1[NP], al[NP], be[NP], ga[NP];
+      // 4 pairs per warp, 8 lanes per pair: lane = 8 pp + r8 holds rows 8 ((k + pp) & 7) + r8,
+      // k = 0..7 (the row-block stagger keeps the two pairs of a half-warp on different banks)
+      const int pp = lane >> 3, r8 = lane & 7;
+      const int q = warp + pp * BR_W;
+      int p0, p1;
+      if (q == 0) { p0 = kk - 1; p1 = r; }
+      else { p0 = (r + q) % (kk - 1); p1 = (r + kk - 1 - q) % (kk - 1); }
+      if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
+      const bool act = q < kk / 2 && p1 < nc;
+      double* ca = sm.Rs + (act ? p0 : 0) * BR_C;
+      double* cb = sm.Rs + (act ? p1 : 0) * BR_C;
+      double x[8], y[8];
+      double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-      for (int i = 0; i < NP; ++i) {
-        const int q = warp + i * BR_W;
-        int p0, p1;
-        if (q == 0) { p0 = kk - 1; p1 = r; }
-        else { p0 = (r + q) % (kk - 1); p1 = (r + kk - 1 - q) % (kk - 1); }
-        if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
-        const bool act = q < kk / 2 && p1 < nc;
-        pa[i] = act ? p0 : -1;
-        pb[i] = p1;
-        const double* ca = sm.Rs + (act ? p0 : 0) * BR_C;
-        const double* cb = sm.Rs + (act ? p1 : 0) * BR_C;
-        x0[i] = act ? ca[lane] : 0.0;
-        x1[i] = act ? ca[lane + 32] : 0.0;
-        y0[i] = act ? cb[lane] : 0.0;
-        y1[i] = act ? cb[lane + 32] : 0.0;
-        al[i] = x0[i] * x0[i] + x1[i] * x1[i];
-        be[i] = y0[i] * y0[i] + y1[i] * y1[i];
-        ga[i] = x0[i] * y0[i] + x1[i] * y1[i];
+      for (int k = 0; k < 8; ++k) {
+        const int row = 8 * ((k + pp) & 7) + r8;
+        x[k] = act ? ca[row] : 0.0;
+        y[k] = act ? cb[row] : 0.0;
+        al += x[k] * x[k];
+        be += y[k] * y[k];
+        ga += x[k] * y[k];
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+      for (int o = 4; o > 0; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      const bool rot = act && ga != 0.0 && al > negl && be > negl && fabs(ga) > tol * sqrt(al * be);
+      if (rot) {
+        const double zeta = (be - al) / (2.0 * ga);
+        const double az = fabs(zeta);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (az > 1e150 ? 2.0 * az : az + sqrt(1.0 + zeta * zeta));
+        const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+        double* va = sm.Aux + p0 * BR_C;
+        double* vbp = sm.Aux + p1 * BR_C;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          al[i] += __shfl_xor_sync(0xffffffffu, al[i], o);
-          be[i] += __shfl_xor_sync(0xffffffffu, be[i], o);
-          ga[i] += __shfl_xor_sync(0xffffffffu, ga[i], o);
+        for (int k = 0; k < 8; ++k) {
+          const int row = 8 * ((k + pp) & 7) + r8;
+          ca[row] = cs * x[k] - sn * y[k];
+          cb[row] = sn * x[k] + cs * y[k];
+          const double a0 = va[row], b0 = vbp[row];
+          va[row] = cs * a0 - sn * b0;
+          vbp[row] = sn * a0 + cs * b0;
         }
       }
-      bool any = false;
-#pragma unroll
-      for (int i = 0; i < NP; ++i) {
-        if (pa[i] >= 0 && ga[i] != 0.0 && al[i] > negl && be[i] > negl && fabs(ga[i]) > tol * sqrt(al[i] * be[i])) {
-          const double zeta = (be[i] - al[i]) / (2.0 * ga[i]);
-          const double az = fabs(zeta);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (az > 1e150 ? 2.0 * az : az + sqrt(1.0 + zeta * zeta));
-          const double cs = rsqrt(1.0 + t * t), sn = cs * t;
-          double* ca = sm.Rs + pa[i] * BR_C;
-          double* cb = sm.Rs + pb[i] * BR_C;
-          ca[lane] = cs * x0[i] - sn * y0[i];
-          ca[lane + 32] = cs * x1[i] - sn * y1[i];
-          cb[lane] = sn * x0[i] + cs * y0[i];
-          cb[lane + 32] = sn * x1[i] + cs * y1[i];
-          double* va = sm.Aux + pa[i] * BR_C;
-          double* vbp = sm.Aux + pb[i] * BR_C;
-          const double a0 = va[lane], a1 = va[lane + 32], b0 = vbp[lane], b1 = vbp[lane + 32];
-          va[lane] = cs * a0 - sn * b0;
-          va[lane + 32] = cs * a1 - sn * b1;
-          vbp[lane] = sn * a0 + cs * b0;
-          vbp[lane + 32] = sn * a1 + cs * b1;
-          any = true;
-        }
-      }
-      if (any && lane == 0) sm.flag = 1;
+      if (__any_sync(0xffffffffu, rot) && lane == 0) sm.flag = 1;
       __syncthreads();
     }
     conv = (sm.flag == 0);
@@ -543,7 +600,7 @@ __device__ void br_out_core(BRSmem& sm, int rho, int cp, int64_t p, const double
     tr[0][s] = (ok2 && lane < cp) ? sm.Rs[pc * BR_C + lane] * inv : 0.0;
     tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Rs[pc * BR_C + lane + 32] * inv : 0.0;
   }
-  br_apply_q<NS>(tr, YV, YT, p, cp, rho, ok, rho, 1);
+  br_apply_q<NS>(tr, YV, YT, p, cp, rho, ok, rho, 1, sm.vst);
 }
 
 // Z_{k+1} = H_{k+1} [(S_rho V_rho^T)^T; 0] (m1 x rho, column-major ld m1).
@@ -561,7 +618,7 @@ __device__ void br_next_core(BRSmem& sm, int rho, int cp, int64_t m1, int c1, co
     tr[0][s] = (ok2 && lane < cp) ? sm.Aux[pc * BR_C + lane] * sg : 0.0;
     tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Aux[pc * BR_C + lane + 32] * sg : 0.0;
   }
-  br_apply_q<NS>(tr, V, Tq, m1, c1, rho, dst, 1, m1);
+  br_apply_q<NS>(tr, V, Tq, m1, c1, rho, dst, 1, m1, sm.vst);
 }
 
 __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
@@ -576,6 +633,13 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
   double* sc = A.scal + (int64_t)b * 4;
   double* out = A.out + (int64_t)b * S->ostride;
   const int n = S->n[kc], cp = S->Rp[k];
+  if (tid == 0) {
+    mbar_init(&sm.vst.bar[0], 1);
+    mbar_init(&sm.vst.bar[1], 1);
+    sm.vst.phase[0] = sm.vst.phase[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   if (k > 1 && sc[3] != 0.0) {  // ||x|| = 0: rank-1 zero tensor
     for (int i = tid; i < n; i += BR_T) out[S->ooff[kc] + i] = 0.0;
     if (k + 1 == d)
@@ -591,7 +655,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
     br_load_lt(sm, A.L + (int64_t)b * 2 * BR_C * BR_C + 0, cp, S->R[1]);  // L_2 lives in slot 0
     __syncthreads();
     FirstElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, d, K};
-    if (tall) br_qr(e, p, cp, sm, YV, YT);
+    if (tall) br_qr(e, p, cp, sm, YV, YT, (A.dbg && blockIdx.x == 0) ? A.dbg + 4 : nullptr);
     else {
       for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {
         const int col = idx / BR_C, row = idx % BR_C;
@@ -601,7 +665,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
     }
   } else {
     RowMajorElem e{A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride, cp};
-    if (tall) br_qr(e, p, cp, sm, YV, YT);
+    if (tall) br_qr(e, p, cp, sm, YV, YT, (A.dbg && blockIdx.x == 0) ? A.dbg + 4 : nullptr);
     else {
       for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {
         const int col = idx / BR_C, row = idx % BR_C;
@@ -635,7 +699,9 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
     }
     __syncthreads();
   }
+  const long long cj0 = clock64();
   const bool conv = br_jacobi(sm, jrows, cp);
+  if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[8] += clock64() - cj0;
   if (tid == 0) {
     if (!conv) A.info[b] = 1;
     const int nsv = (int)(p < cp ? p : cp);
@@ -658,6 +724,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
   __syncthreads();
   const int rho = sm.rho;
   // ---- output core k = Q_Y U_rho ((rho_{k-1} n_k) x rho, row-major)
+  const long long co0 = clock64();
   double* ok = out + S->ooff[kc];
   if (tall) {
     if (rho <= BR_C / 2) br_out_core<BR_CPW / 2>(sm, rho, cp, p, YV, YT, ok);
@@ -669,6 +736,8 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
       ok[idx] = sg > 0.0 ? sm.Rs[sm.perm[col] * BR_C + row] / sg : 0.0;
     }
   }
+  if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[9] += clock64() - co0;
+  const long long cz0 = clock64();
   // ---- Z_{k+1} = H_{k+1} [(S V^T)^T; 0]   (m_{k+1} x rho, column-major)
   const int kn = kc + 1;  // core index of core k+1
   const int64_t m1 = (int64_t)S->n[kn] * S->Rp[k + 1];
@@ -678,6 +747,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
   const double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kn];
   if (rho <= BR_C / 2) br_next_core<BR_CPW / 2>(sm, rho, cp, m1, c1, V, Tq, dst);
   else br_next_core<BR_CPW>(sm, rho, cp, m1, c1, V, Tq, dst);
+  if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[10] += clock64() - cz0;
 }
 
 // Copy item b's cores from the worst-case workspace to the exact-size arena.
@@ -718,6 +788,14 @@ bool batch_shape_supported(int d, int K, const std::vector<std::vector<int64_t>>
 }
 
 void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut& res) {
+  const char* hdbg = std::getenv("TT_B200_BR_DEBUG");
+  const bool hd = hdbg && hdbg[0] == '1';
+  const auto t_start = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what) {
+    if (!hd) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    std::fprintf(stderr, "[br_host] %8.2f ms  %s\n", ms, what);
+  };
   const int B = in.B, d = in.d, K = in.K;
   // ---------------------------------------------------------------- shape tables (uniform)
   BRShape sh;
@@ -761,11 +839,11 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
     }
     if (k + 1 < d) zmax = std::max<int64_t>(zmax, (int64_t)sh.n[k] * sh.Rp[k + 1] * sh.Rp[k]);
   }
-  sh.vstride = std::max<int64_t>(v, 1);
-  sh.tstride = std::max<int64_t>(t, 1);
-  sh.ystride = std::max<int64_t>(yv, 1);
-  sh.ytstride = std::max<int64_t>(yt, 1);
-  sh.zstride = std::max<int64_t>(zmax, 1);
+  sh.vstride = (std::max<int64_t>(v, 2) + 1) & ~(int64_t)1;
+  sh.tstride = (std::max<int64_t>(t, 2) + 1) & ~(int64_t)1;
+  sh.ystride = (std::max<int64_t>(yv, 2) + 1) & ~(int64_t)1;
+  sh.ytstride = (std::max<int64_t>(yt, 2) + 1) & ~(int64_t)1;
+  sh.zstride = (std::max<int64_t>(zmax, 2) + 1) & ~(int64_t)1;
   sh.ostride = omax;
   const int64_t per_item = sh.vstride + sh.tstride + 2 * BR_C * BR_C + sh.ystride + sh.ytstride + 2 * sh.zstride +
                            sh.ostride + 8;
@@ -812,10 +890,18 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   dcoef.upload(ctx, in.coef.data(), in.coef.size() * sizeof(double));
   dscale.upload(ctx, scale.data(), scale.size() * sizeof(double));
   // ---------------------------------------------------------------- waves
+  stamp("tables uploaded");
   size_t free_b = 0, total_b = 0;
   TTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double budget = std::min<double>(0.5 * (double)free_b, 48e9);
+  // one wave when the whole batch fits in ~60 % of the device (the workspace is the context's
+  // grow-only scratch: no allocation churn between calls)
+  const double budget = std::min<double>(0.6 * ((double)free_b + (double)ctx->scratch_bytes), 100e9);
   const int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
+  const int nb_max = std::min(W, B);
+  const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 2 * BR_C * BR_C + sh.ystride +
+                                              sh.ytstride + 2 * sh.zstride + std::max<int64_t>(sh.ostride, 1) + 4) +
+                            (size_t)nb_max * (d + 2) + 64;
+  double* ws = static_cast<double*>(ctx_scratch(ctx, ws_doubles * sizeof(double)));
   const size_t smem = sizeof(BRSmem);
   TTB_CUDA(cudaFuncSetAttribute(br_r2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   TTB_CUDA(cudaFuncSetAttribute(br_l2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -829,12 +915,26 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   res.arenas.clear();
   res.arena_size.clear();
   try {
+    if (hd) std::fprintf(stderr, "[br_host] W = %d of B = %d, per item %.1f MB, free %.1f GB\n", W, B, 8e-6 * per_item, 1e-9 * free_b);
     for (int w0 = 0; w0 < B; w0 += W) {
       const int nb = std::min(W, B - w0);
-      DBuf V(ctx, (size_t)nb * sh.vstride), T(ctx, (size_t)nb * sh.tstride), L(ctx, (size_t)nb * 2 * BR_C * BR_C);
-      DBuf YV(ctx, (size_t)nb * sh.ystride), YT(ctx, (size_t)nb * sh.ytstride), Z(ctx, (size_t)nb * 2 * sh.zstride);
-      DBuf O(ctx, (size_t)nb * std::max<int64_t>(sh.ostride, 1)), SC(ctx, (size_t)nb * 4);
-      IBuf RK(ctx, (size_t)nb * (d + 1)), INF(ctx, (size_t)nb);
+      stamp("wave start");
+      struct { double* p; } V, T, L, YV, YT, Z, O, SC;
+      struct { int* p; } RK, INF;
+      {
+        double* w = ws;  // carve the scratch (every piece a multiple of 2 doubles: 16-B aligned)
+        auto take = [&](size_t n) { double* r = w; w += (n + 1) & ~(size_t)1; return r; };
+        V.p = take((size_t)nb * sh.vstride);
+        T.p = take((size_t)nb * sh.tstride);
+        L.p = take((size_t)nb * 2 * BR_C * BR_C);
+        YV.p = take((size_t)nb * sh.ystride);
+        YT.p = take((size_t)nb * sh.ytstride);
+        Z.p = take((size_t)nb * 2 * sh.zstride);
+        O.p = take((size_t)nb * std::max<int64_t>(sh.ostride, 1));
+        SC.p = take((size_t)nb * 4);
+        RK.p = reinterpret_cast<int*>(take(((size_t)nb * (d + 1) + 1) / 2));
+        INF.p = reinterpret_cast<int*>(take(((size_t)nb + 1) / 2));
+      }
       TTB_CUDA(cudaMemsetAsync(INF.p, 0, sizeof(int) * nb, ctx->stream));
       BRArgs a;
       a.sh = static_cast<const BRShape*>(dsh.p);
@@ -848,6 +948,13 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       a.max_rank = o.max_rank;
       a.keep_all = keep_all ? 1 : 0;
       a.item0 = w0;
+      const char* dbe = std::getenv("TT_B200_BR_DEBUG");
+      LBuf dbg;
+      if (dbe && dbe[0] == '1') {
+        dbg.alloc(ctx, 16);
+        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 16 * sizeof(long long), ctx->stream));
+      }
+      a.dbg = dbg.p;
       for (int kc = d - 1; kc >= 1; --kc) {
         const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
         const double c = sh.R[kc];
@@ -861,9 +968,18 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       }
       for (int k = 1; k < d; ++k)
         TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, k));
+      if (dbg.p) {
+        long long h[16];
+        TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld outcore %lld nextcore %lld (cycles, CTA 0)\n",
+                     h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[9], h[10]);
+      }
       // ranks (the one host synchronisation of the wave), then compaction
       std::vector<int> hr((size_t)nb * (d + 1)), hinf((size_t)nb);
+      stamp("launched");
       d2h_small_int(ctx, hr.data(), RK.p, hr.size());
+      stamp("synced (ranks)");
       d2h_small_int(ctx, hinf.data(), INF.p, hinf.size());
       for (int b = 0; b < nb; ++b)
         if (hinf[(size_t)b]) fail(TT_ENOCONV, "Jacobi SVD did not converge (batch item " + std::to_string(w0 + b) + ")");
@@ -902,6 +1018,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       ddst.upload(ctx, dst.data(), dst.size() * sizeof(int64_t));
       dsz.upload(ctx, sz.data(), sz.size() * sizeof(int64_t));
       dooff.upload(ctx, sh.ooff, sizeof(int64_t) * d);
+      stamp("arena allocated");
       TTB_RUN(ctx, "batch_compact", 0.0, 16.0 * (double)tot,
               br_compact_kernel<<<nb, 256, 0, ctx->stream>>>(O.p, sh.ostride, static_cast<const int64_t*>(dooff.p),
                                                              static_cast<const int64_t*>(ddst.p),
@@ -913,6 +1030,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
           res.core[(size_t)(w0 + b) * d + kc] = static_cast<double*>(arena) + dst[(size_t)b * d + kc];
         res.norm[(size_t)(w0 + b)] = hsc[(size_t)b * 4 + 0];
       }
+      stamp("wave done (host)");
     }
   } catch (...) {
     for (void* p : res.arenas) cudaFreeAsync(p, ctx->stream);

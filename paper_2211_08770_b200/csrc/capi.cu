@@ -82,6 +82,7 @@ tt_status tt_ctx_create(int device, void* stream, tt_ctx* out) {
 tt_status tt_ctx_destroy(tt_ctx ctx) {
   if (!ctx) return TT_EINVAL;
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->scratch) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->scratch); }
   delete ctx;
   return TT_OK;
 }

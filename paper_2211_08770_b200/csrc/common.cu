@@ -171,6 +171,22 @@ void d2h_small_int(tt_ctx ctx, int* host, const int* dev, size_t n) {
   std::memcpy(host, ctx->h_pinned, n * sizeof(int));
 }
 
+void* ctx_scratch(tt_ctx ctx, size_t bytes) {
+  if (bytes <= ctx->scratch_bytes) return ctx->scratch;
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  ctx->scratch = nullptr;
+  ctx->scratch_bytes = 0;
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    (void)cudaGetLastError();
+    fail(TT_ENOMEM, "workspace allocation of " + std::to_string(bytes) + " bytes failed");
+  }
+  ctx->scratch = p;
+  ctx->scratch_bytes = bytes;
+  return p;
+}
+
 tt_tensor tensor_alloc(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& r) {
   tt_tensor t = new tt_tensor_s();
   t->d = d;

@@ -61,6 +61,8 @@ struct tt_ctx_s {
   int64_t launches = 0;
   double* h_pinned = nullptr;   // small pinned staging area for scalar reads
   size_t h_pinned_bytes = 0;
+  void* scratch = nullptr;      // grow-only device workspace of the batched engine
+  size_t scratch_bytes = 0;
 };
 
 struct tt_tensor_s {
@@ -134,6 +136,8 @@ void debug_check(tt_ctx ctx, const char* cls, const char* file, int line);
 // device -> host copy of a few doubles through the pinned staging buffer (synchronises)
 void d2h_small(tt_ctx ctx, double* host, const double* dev, size_t n);
 void d2h_small_int(tt_ctx ctx, int* host, const int* dev, size_t n);
+// grow-only context workspace (cudaMalloc, kept until tt_ctx_destroy); synchronises on growth
+void* ctx_scratch(tt_ctx ctx, size_t bytes);
 
 // ------------------------------------------------------------------ tensors
 tt_tensor tensor_alloc(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& r);
