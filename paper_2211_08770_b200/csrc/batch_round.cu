@@ -157,71 +157,73 @@ struct BRSmem {
 // the chunk reflector parts, taus go to tau_out[j] (global).
 __device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, double* tau_out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // j = 8 S + ww: the slot S of column j in its owner warp ww is a compile-time index
+#pragma unroll
+  for (int S = 0; S < BR_CPW; ++S) {
 #pragma unroll 1
-  for (int j = 0; j < ncol; ++j) {
-    const int buf = j & 1;
-    if (warp == (j & (BR_W - 1))) {
-      const int s = j / BR_W;
-      double x[BR_RPL];
+    for (int ww = 0; ww < BR_W; ++ww) {
+      const int j = S * BR_W + ww;
+      if (j >= ncol) break;
+      const int buf = j & 1;
+      if (warp == ww) {
+        double* Rc = sm.Rs + j * BR_C;
+        const double r0 = Rc[lane], r1 = Rc[lane + 32];
+        double ss = 0.0;
+        if (lane > j) ss += r0 * r0;
+        if (lane + 32 > j) ss += r1 * r1;
 #pragma unroll
-      for (int t = 0; t < BR_RPL; ++t) x[t] = sel(a[t], s);
-      double* Rc = sm.Rs + j * BR_C;
-      const double r0 = Rc[lane], r1 = Rc[lane + 32];
-      double ss = 0.0;
-      if (lane > j) ss += r0 * r0;
-      if (lane + 32 > j) ss += r1 * r1;
+        for (int t = 0; t < BR_RPL; ++t) ss += a[t][S] * a[t][S];
+        const double sigma = warp_sum(ss);
+        const double alpha = Rc[j];
+        double tau = 0.0, beta = alpha, scal = 0.0;
+        if (sigma != 0.0) {
+          // dlarfg with one reciprocal: inv = 1 / (beta (alpha - beta)) (never 0: signs differ)
+          const double nr = sqrt(alpha * alpha + sigma);
+          beta = alpha >= 0.0 ? -nr : nr;
+          const double am = alpha - beta;
+          const double inv = 1.0 / (beta * am);
+          tau = -am * am * inv;  // (beta - alpha) / beta
+          scal = beta * inv;     // 1 / (alpha - beta)
+        }
+        const double v0 = lane > j ? r0 * scal : (lane == j ? 1.0 : 0.0);
+        const double v1 = lane + 32 > j ? r1 * scal : (lane + 32 == j ? 1.0 : 0.0);
+        sm.vb[buf][lane] = v0;
+        sm.vb[buf][lane + 32] = v1;
 #pragma unroll
-      for (int t = 0; t < BR_RPL; ++t) ss += x[t] * x[t];
-      const double sigma = warp_sum(ss);
-      const double alpha = Rc[j];
-      double tau = 0.0, beta = alpha, scal = 0.0;
-      if (sigma != 0.0) {
-        const double nr = sqrt(alpha * alpha + sigma);
-        beta = alpha >= 0.0 ? -nr : nr;
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
+        for (int t = 0; t < BR_RPL; ++t) {
+          a[t][S] *= scal;
+          sm.vb[buf][BR_C + 32 * t + lane] = a[t][S];
+        }
+        __syncwarp();
+        if (lane > j) Rc[lane] = v0;
+        if (lane + 32 > j) Rc[lane + 32] = v1;
+        if (lane == j) Rc[lane] = beta;
+        if (lane + 32 == j) Rc[lane + 32] = beta;
+        if (lane == 0) { sm.tb[buf] = tau; tau_out[j] = tau; }
       }
-      const double v0 = lane > j ? r0 * scal : (lane == j ? 1.0 : 0.0);
-      const double v1 = lane + 32 > j ? r1 * scal : (lane + 32 == j ? 1.0 : 0.0);
-      sm.vb[buf][lane] = v0;
-      sm.vb[buf][lane + 32] = v1;
+      __syncthreads();
+      const double tau = sm.tb[buf];
+      if (tau != 0.0) {
+        const double* v = sm.vb[buf];
+        const double v0 = v[lane], v1 = v[lane + 32];
+        double vc[BR_RPL];
 #pragma unroll
-      for (int t = 0; t < BR_RPL; ++t) {
-        const double v = x[t] * scal;
-        sm.vb[buf][BR_C + 32 * t + lane] = v;
+        for (int t = 0; t < BR_RPL; ++t) vc[t] = v[BR_C + 32 * t + lane];
 #pragma unroll
-        for (int c = 0; c < BR_CPW; ++c)
-          if (c == s) a[t][c] = v;
-      }
-      __syncwarp();
-      if (lane > j) Rc[lane] = v0;
-      if (lane + 32 > j) Rc[lane + 32] = v1;
-      if (lane == j) Rc[lane] = beta;
-      if (lane + 32 == j) Rc[lane + 32] = beta;
-      if (lane == 0) { sm.tb[buf] = tau; tau_out[j] = tau; }
-    }
-    __syncthreads();
-    const double tau = sm.tb[buf];
-    if (tau != 0.0) {
-      const double* v = sm.vb[buf];
-      const double v0 = v[lane], v1 = v[lane + 32];
-      double vc[BR_RPL];
+        for (int s = S; s < BR_CPW; ++s) {  // columns 8s + warp > j (slots below S are done)
+          const int col = s * BR_W + warp;
+          if ((s > S || warp > ww) && col < ncol) {
+            double* Rc = sm.Rs + col * BR_C;
+            const double r0 = Rc[lane], r1 = Rc[lane + 32];
+            double dt = v0 * r0 + v1 * r1;
 #pragma unroll
-      for (int t = 0; t < BR_RPL; ++t) vc[t] = v[BR_C + 32 * t + lane];
+            for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * a[t][s];
+            dt = tau * warp_sum(dt);
+            Rc[lane] = r0 - dt * v0;
+            Rc[lane + 32] = r1 - dt * v1;
 #pragma unroll
-      for (int s = 0; s < BR_CPW; ++s) {
-        const int col = s * BR_W + warp;
-        if (col > j && col < ncol) {
-          double* Rc = sm.Rs + col * BR_C;
-          const double r0 = Rc[lane], r1 = Rc[lane + 32];
-          double dt = v0 * r0 + v1 * r1;
-#pragma unroll
-          for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * a[t][s];
-          dt = tau * warp_sum(dt);
-          Rc[lane] = r0 - dt * v0;
-          Rc[lane + 32] = r1 - dt * v1;
-#pragma unroll
-          for (int t = 0; t < BR_RPL; ++t) a[t][s] -= dt * vc[t];
+            for (int t = 0; t < BR_RPL; ++t) a[t][s] -= dt * vc[t];
+          }
         }
       }
     }
@@ -371,15 +373,7 @@ __device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem
       }
     }
     const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
-#pragma unroll
-    for (int s = 0; s < BR_CPW; ++s) {
-      const int col = s * BR_W + warp;
-#pragma unroll
-      for (int t = 0; t < BR_RPL; ++t) {
-        const int64_t row = base + 32 * t + lane;
-        a[t][s] = (row < m && col < ncol) ? elem(row, col) : 0.0;
-      }
-    }
+    elem.chunk(a, base, m, ncol);
     __syncthreads();
     const long long c1 = clock64();
     br_stack_qr(a, sm, ncol, Tq + (int64_t)q * BR_C);
@@ -418,6 +412,52 @@ struct PanelElem {
     for (; be < rl; ++be) s0 += lp[be * BR_C] * __ldg(xp + be);
     return (s0 + s1) + (s2 + s3);
   }
+
+  // chunk loader: per column (term l, index a) the four rows' beta sums run as four
+  // independent chains (loads of both operands in flight together)
+  __device__ void chunk(double (&a)[BR_RPL][BR_CPW], int64_t base, int64_t m, int ncol) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // rows of this lane: row_t = base + 32 t + lane -> (i_t, b'_t); packed in one int each
+    int ib[BR_RPL];
+#pragma unroll
+    for (int t = 0; t < BR_RPL; ++t) {
+      const int64_t row = base + 32 * t + lane;
+      ib[t] = row < m ? (int)((row / Rpk) << 8 | (row % Rpk)) : -1;
+    }
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+      if (col >= ncol) {
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) a[t][s] = 0.0;
+        continue;
+      }
+      const int l = cterm[col], aa = ca[col];
+      const double* X = cores[l * d + kc];
+      if (last) {
+        const double c = LT[l * BR_C];
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) a[t][s] = ib[t] >= 0 ? c * __ldg(X + (int64_t)aa * n + (ib[t] >> 8)) : 0.0;
+        continue;
+      }
+      const int rl = sh->r[l][kc + 1], o = sh->off[kc + 1][l];
+      const double* xa = X + (int64_t)aa * n * rl;
+      double acc[BR_RPL];
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) acc[t] = 0.0;
+#pragma unroll 2
+      for (int be = 0; be < rl; ++be) {
+        const double* lrow = LT + (int64_t)(o + be) * BR_C;
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) {
+          const int q = ib[t] < 0 ? 0 : ib[t];
+          acc[t] += lrow[q & 255] * __ldg(xa + (int64_t)(q >> 8) * rl + be);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) a[t][s] = ib[t] >= 0 ? acc[t] : 0.0;
+    }
+  }
 };
 
 // Y_1[i, b'] = sum_{l, beta} X_1^(l)[0, i, beta] L_2[b', off_{1,l} + beta]
@@ -436,12 +476,40 @@ struct FirstElem {
     }
     return s;
   }
+
+  // chunk rows base + 32t + lane, columns 8s + warp (zero outside the matrix)
+  __device__ void chunk(double (&a)[BR_RPL][BR_CPW], int64_t base, int64_t m, int ncol) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) {
+        const int64_t row = base + 32 * t + lane;
+        a[t][s] = (row < m && col < ncol) ? (*this)(row, col) : 0.0;
+      }
+    }
+  }
 };
 
 struct RowMajorElem {  // Y[row, col] = Z[row * ld + col]
   const double* Z;
   int ld;
   __device__ double operator()(int64_t row, int col) const { return Z[row * ld + col]; }
+
+  // chunk rows base + 32t + lane, columns 8s + warp (zero outside the matrix)
+  __device__ void chunk(double (&a)[BR_RPL][BR_CPW], int64_t base, int64_t m, int ncol) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int s = 0; s < BR_CPW; ++s) {
+      const int col = s * BR_W + warp;
+#pragma unroll
+      for (int t = 0; t < BR_RPL; ++t) {
+        const int64_t row = base + 32 * t + lane;
+        a[t][s] = (row < m && col < ncol) ? (*this)(row, col) : 0.0;
+      }
+    }
+  }
 };
 
 // Load L^T (rows x cols of the row-major ld-64 L) into sm.Aux: Aux[c * 64 + b'] = L[b' * 64 + c].
