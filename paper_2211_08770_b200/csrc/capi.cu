@@ -7,6 +7,7 @@
 #include <new>
 
 #include "batch_round.cuh"
+#include "gram.cuh"
 #include "orth.cuh"
 #include "round.cuh"
 #include "ttops.cuh"
@@ -251,6 +252,18 @@ tt_status tt_gram(tt_ctx ctx, int32_t m, const tt_view* a, double* G_dev) {
   return guarded(ctx, [&] {
     std::vector<TTRef> A;
     for (int i = 0; i < m; ++i) A.push_back(TTRef::of(a[i]));
+    bool uniform = true;
+    for (int i = 1; i < m; ++i)
+      uniform = uniform && A[(size_t)i].d == A[0].d && A[(size_t)i].n == A[0].n && A[(size_t)i].r == A[0].r;
+    const char* gt = std::getenv("TT_B200_GRAM_PAIRWISE");  // tests: force the per-pair kernel
+    if (uniform && !(gt && gt[0] == '1')) {
+      std::vector<const double*> cores;
+      for (int i = 0; i < m; ++i) cores.insert(cores.end(), A[(size_t)i].core.begin(), A[(size_t)i].core.end());
+      if (gram_tiled_supported(cores, m, A[0].d, A[0].n, A[0].r)) {
+        gram_tiled(ctx, cores, m, A[0].d, A[0].n, A[0].r, G_dev);
+        return;
+      }
+    }
     std::vector<std::pair<const TTRef*, const TTRef*>> pr;
     for (int i = 0; i < m; ++i)
       for (int j = 0; j <= i; ++j) pr.push_back({&A[(size_t)i], &A[(size_t)j]});

@@ -1,0 +1,16 @@
+// Pair-tiled TT-dot Gram matrix of equally shaped TT-vectors (gram.cu).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace ttb {
+
+// cores[t*d + k]: core k of tensor t (device); every tensor has modes n[0..d-1], ranks r[0..d].
+bool gram_tiled_supported(const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
+                          const std::vector<int64_t>& r);
+// G_dev (m x m row-major, device) = <a_i, a_j>, symmetric; enqueued on the ctx stream.
+void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
+                const std::vector<int64_t>& r, double* G_dev);
+
+}  // namespace ttb

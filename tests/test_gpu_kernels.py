@@ -122,3 +122,30 @@ def test_norm_sweep():
     rng = _rng(7)
     x = make_random_tt(5, 6, [1, 4, 9, 9, 4, 1], rng)
     assert P.tt_norm(ctx(), dev(x)) == pytest.approx(tt.tt_norm(x), rel=1e-13)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_gram_tiled_matches_oracle_and_pairwise(seed):
+    """Pair-tiled Gram kernel (equal shapes; odd m, ragged ranks up to 32, d from 1) against the
+    oracle (1e-12 ||a_i|| ||a_j||) and the per-pair kernel (TT_B200_GRAM_PAIRWISE)."""
+    import os
+    import paper_2211_08770_b200 as P
+    from oracle import tt
+    from ttinputs import make_random_tt
+    rng = np.random.Generator(np.random.PCG64(500 + seed))
+    d = int(rng.integers(1, 6))
+    n = [int(v) for v in rng.integers(1, 12, size=d)]
+    r = [1] + [int(v) for v in rng.integers(1, 33, size=d - 1)] + [1]
+    m = int(rng.integers(1, 12))
+    A = [make_random_tt(d, n, r, rng) for _ in range(m)]
+    G = P.tt_gram(ctx(), [dev(a) for a in A]).cpu().numpy()
+    nr = np.array([tt.tt_norm(a) for a in A])
+    Go = np.array([[tt.tt_dot(a, b) for b in A] for a in A])
+    assert np.all(np.abs(G - Go) <= 1e-12 * np.outer(nr, nr))
+    assert np.array_equal(G, G.T)
+    os.environ["TT_B200_GRAM_PAIRWISE"] = "1"
+    try:
+        Gp = P.tt_gram(ctx(), [dev(a) for a in A]).cpu().numpy()
+    finally:
+        del os.environ["TT_B200_GRAM_PAIRWISE"]
+    assert np.all(np.abs(G - Gp) <= 1e-13 * np.outer(nr, nr))
