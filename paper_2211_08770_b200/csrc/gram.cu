@@ -31,16 +31,18 @@ __host__ __device__ inline int ceil4(int x) { return (x + 3) & ~3; }
 template <int GT_T>  // threads per CTA; one V micro-tile per thread
 __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __restrict__ cores, GramShape sh, int m,
                                                           int nbj, const int* __restrict__ tiles, int RP,
-                                                          double* __restrict__ G) {
+                                                          int S, int PS, double* __restrict__ G) {
   extern __shared__ __align__(16) double gsm[];
-  const int RR = RP * RP;
+  // smem blocks of PS doubles (per pair / per staged tensor), rows of stride S >= RP: padded so
+  // the 4x4 micro-tile accesses of a warp spread over the banks
+  const int RR = PS;
   double* W = gsm;                 // [p][c][a]  (column-major W: W[p][c * RP + a] = W(a, c))
   double* U = W + GT_P * RR;       // [p][a][c'] (row-major)
   double* XB = U + GT_P * RR;      // 2 buffers x [t][a][a'] (row-major slices X(a, s, a')), I then J
   const int tid = threadIdx.x;
   const int i0 = tiles[2 * blockIdx.x] * GT_I, j0 = tiles[2 * blockIdx.x + 1] * GT_J;
   const int d = sh.d;
-  for (int idx = tid; idx < GT_P * RR; idx += GT_T) W[idx] = (idx % RR == 0) ? 1.0 : 0.0;
+  for (int idx = tid; idx < GT_P * RR; idx += GT_T) W[idx] = (idx % RR == 0) ? 1.0 : 0.0;  // W_0 = 1 (1 x 1)
 #pragma unroll 1
   for (int k = 0; k < d; ++k) {
     const int n = sh.n[k], R0 = sh.r[k], R1 = sh.r[k + 1];
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
         const int t = idx / (R0 * R1), e = idx % (R0 * R1), a = e / R1, b = e % R1;
         int tens = t < GT_I ? i0 + t : j0 + (t - GT_I);
         if (tens >= m) tens = m - 1;  // padding tensor: its pairs are never written
-        __pipeline_memcpy_async(buf + t * RR + a * RP + b,
+        __pipeline_memcpy_async(buf + t * RR + a * S + b,
                                 cores[(int64_t)tens * d + k] + ((int64_t)a * n + s) * R1 + b, sizeof(double));
       }
       __pipeline_commit();
@@ -82,10 +84,10 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
           for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
 #pragma unroll 2
         for (int c = 0; c < R0; ++c) {
-          const double2 w01 = *reinterpret_cast<const double2*>(Wp + c * RP + 4 * ta);
-          const double2 w23 = *reinterpret_cast<const double2*>(Wp + c * RP + 4 * ta + 2);
-          const double2 x01 = *reinterpret_cast<const double2*>(Xj + c * RP + 4 * tc);
-          const double2 x23 = *reinterpret_cast<const double2*>(Xj + c * RP + 4 * tc + 2);
+          const double2 w01 = *reinterpret_cast<const double2*>(Wp + c * S + 4 * ta);
+          const double2 w23 = *reinterpret_cast<const double2*>(Wp + c * S + 4 * ta + 2);
+          const double2 x01 = *reinterpret_cast<const double2*>(Xj + c * S + 4 * tc);
+          const double2 x23 = *reinterpret_cast<const double2*>(Xj + c * S + 4 * tc + 2);
           const double wv[4] = {w01.x, w01.y, w23.x, w23.y}, xv[4] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
           for (int x = 0; x < 4; ++x)
@@ -95,8 +97,8 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
         double* Up = U + p * RR;
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          *reinterpret_cast<double2*>(Up + (4 * ta + x) * RP + 4 * tc) = make_double2(c4[x][0], c4[x][1]);
-          *reinterpret_cast<double2*>(Up + (4 * ta + x) * RP + 4 * tc + 2) = make_double2(c4[x][2], c4[x][3]);
+          *reinterpret_cast<double2*>(Up + (4 * ta + x) * S + 4 * tc) = make_double2(c4[x][0], c4[x][1]);
+          *reinterpret_cast<double2*>(Up + (4 * ta + x) * S + 4 * tc + 2) = make_double2(c4[x][2], c4[x][3]);
         }
       }
       __syncthreads();
@@ -109,10 +111,10 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
           const double* Up = U + p * RR;
 #pragma unroll 2
           for (int a = 0; a < R0; ++a) {
-            const double2 x01 = *reinterpret_cast<const double2*>(Xi + a * RP + 4 * ta);
-            const double2 x23 = *reinterpret_cast<const double2*>(Xi + a * RP + 4 * ta + 2);
-            const double2 u01 = *reinterpret_cast<const double2*>(Up + a * RP + 4 * tc);
-            const double2 u23 = *reinterpret_cast<const double2*>(Up + a * RP + 4 * tc + 2);
+            const double2 x01 = *reinterpret_cast<const double2*>(Xi + a * S + 4 * ta);
+            const double2 x23 = *reinterpret_cast<const double2*>(Xi + a * S + 4 * ta + 2);
+            const double2 u01 = *reinterpret_cast<const double2*>(Up + a * S + 4 * tc);
+            const double2 u23 = *reinterpret_cast<const double2*>(Up + a * S + 4 * tc + 2);
             const double xv[4] = {x01.x, x01.y, x23.x, x23.y}, uv[4] = {u01.x, u01.y, u23.x, u23.y};
 #pragma unroll
             for (int x = 0; x < 4; ++x)
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
 #pragma unroll
           for (int y = 0; y < 4; ++y) {
             const int a1 = 4 * ta + x, c1 = 4 * tc + y;
-            if (a1 < R1 && c1 < R1) Wp[c1 * RP + a1] = acc[x * 4 + y];
+            if (a1 < R1 && c1 < R1) Wp[c1 * S + a1] = acc[x * 4 + y];
           }
       }
     }
@@ -183,6 +185,9 @@ void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int 
     rmax = std::max<int>(rmax, (int)r[(size_t)k]);
   }
   const int RP = ceil4(rmax);
+  // row stride / block stride chosen for the fewest shared-memory bank conflicts (offline model)
+  const int S = (RP == 8 || RP == 12 || RP == 20 || RP == 24) ? RP + 2 : RP;
+  const int PS = S * RP + 2;
   const int nbi = (m + GT_I - 1) / GT_I, nbj = (m + GT_J - 1) / GT_J;
   std::vector<int> tiles;
   for (int bi = 0; bi < nbi; ++bi)
@@ -195,7 +200,7 @@ void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int 
   BBuf dt, dc;
   dt.upload(ctx, tiles.data(), tiles.size() * sizeof(int));
   dc.upload(ctx, cores.data(), cores.size() * sizeof(double*));
-  const size_t smem = sizeof(double) * (size_t)(2 * GT_P + 2 * (GT_I + GT_J)) * RP * RP;
+  const size_t smem = sizeof(double) * (size_t)(2 * GT_P + 2 * (GT_I + GT_J)) * PS;
   const double pairs = 0.5 * m * (m + 1.0);
   const double bytes = 8.0 * (double)m * [&] { double e = 0; for (int k = 0; k < d; ++k) e += (double)r[(size_t)k] * n[(size_t)k] * r[(size_t)k + 1]; return e; }();
   const int nv = GT_P * (RP / 4) * (RP / 4);
@@ -203,12 +208,12 @@ void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int 
     TTB_CUDA(cudaFuncSetAttribute(gram_tile_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TTB_RUN(ctx, "tt_gram_tiled", flops * pairs, bytes,
             gram_tile_kernel<128><<<ntiles, 128, smem, ctx->stream>>>(static_cast<const double* const*>(dc.p), sh, m,
-                                                                        nbj, static_cast<const int*>(dt.p), RP, G_dev));
+                                                                        nbj, static_cast<const int*>(dt.p), RP, S, PS, G_dev));
   } else {
     TTB_CUDA(cudaFuncSetAttribute(gram_tile_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TTB_RUN(ctx, "tt_gram_tiled", flops * pairs, bytes,
             gram_tile_kernel<256><<<ntiles, 256, smem, ctx->stream>>>(static_cast<const double* const*>(dc.p), sh, m,
-                                                                        nbj, static_cast<const int*>(dt.p), RP, G_dev));
+                                                                        nbj, static_cast<const int*>(dt.p), RP, S, PS, G_dev));
   }
 }
 
