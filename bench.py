@@ -282,8 +282,15 @@ def main():
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     total_ms = sum(v["ms"] for v in prof.values())
     achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+    traffic = None
+    try:  # DRAM bytes per launch of this kernel class from the committed ncu --set full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json"))).get(dom_name)
+        traffic = tr["dram_bytes_per_launch"] if tr else None
+    except Exception:
+        traffic = None
     roof = {"bound": "alu", "achieved": achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": None,
+            "frac": achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": traffic,
+            "traffic_source": "profiles/ncu_traffic_r01.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
             "peak_source": "measured FP64 FMA (DFMA) throughput, tools/fp64_peak.cu -> profiles/fp64_peak_r01.json "
                            "(nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TF)",
             "kernel": dom_name, "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / dom["launches"],

@@ -19,7 +19,7 @@ def launches(path):
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        name = r[ki].split("(")[0].split("<")[0].split("::")[-1]
+        name = r[ki].replace("<unnamed>", "anon").split("(")[0].split("<")[0].split("::")[-1]
         v = float(r[vi].replace(",", ""))
         u = r[ui]
         us = v / 1e3 if u in ("ns", "nsecond") else (v * 1e3 if u in ("ms", "msecond") else v)
