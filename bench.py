@@ -99,9 +99,10 @@ class ClockSampler:
 
 
 def _slice(batch: int, rank: int, world: int):
-    base, rem = divmod(batch, world)
-    start = rank * base + min(rank, rem)
-    return start, base + (1 if rank < rem else 0)
+    """(start, count) of this rank's contiguous slice of the batch (parallel.batch_slice)."""
+    from paper_2211_08770_b200.parallel import batch_slice
+    start, end = batch_slice(batch, world, rank)
+    return start, end - start
 
 
 def _blas_threads() -> int:
