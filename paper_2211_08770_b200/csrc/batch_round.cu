@@ -209,21 +209,34 @@ __device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, d
         double vc[BR_RPL];
 #pragma unroll
         for (int t = 0; t < BR_RPL; ++t) vc[t] = v[BR_C + 32 * t + lane];
+        // columns 8s + warp > j (slots below S are done): all partial dots first, the
+        // reductions interleaved (branch-free: an inactive column gets a zero update)
+        double dt[BR_CPW], r0[BR_CPW], r1[BR_CPW];
 #pragma unroll
-        for (int s = S; s < BR_CPW; ++s) {  // columns 8s + warp > j (slots below S are done)
+        for (int s = S; s < BR_CPW; ++s) {
+          const int col = min(s * BR_W + warp, BR_C - 1);
+          r0[s] = sm.Rs[col * BR_C + lane];
+          r1[s] = sm.Rs[col * BR_C + lane + 32];
+          double q = (v0 * r0[s] + v1 * r1[s]) + (vc[0] * a[0][s] + vc[1] * a[1][s]);
+#pragma unroll
+          for (int t = 2; t < BR_RPL; ++t) q += vc[t] * a[t][s];
+          dt[s] = q;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+#pragma unroll
+        for (int s = S; s < BR_CPW; ++s) {
           const int col = s * BR_W + warp;
-          if ((s > S || warp > ww) && col < ncol) {
-            double* Rc = sm.Rs + col * BR_C;
-            const double r0 = Rc[lane], r1 = Rc[lane + 32];
-            double dt = v0 * r0 + v1 * r1;
-#pragma unroll
-            for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * a[t][s];
-            dt = tau * warp_sum(dt);
-            Rc[lane] = r0 - dt * v0;
-            Rc[lane + 32] = r1 - dt * v1;
-#pragma unroll
-            for (int t = 0; t < BR_RPL; ++t) a[t][s] -= dt * vc[t];
+          const bool act = (s > S || warp > ww) && col < ncol;
+          const double w = act ? tau * dt[s] : 0.0;
+          if (act) {
+            sm.Rs[col * BR_C + lane] = r0[s] - w * v0;
+            sm.Rs[col * BR_C + lane + 32] = r1[s] - w * v1;
           }
+#pragma unroll
+          for (int t = 0; t < BR_RPL; ++t) a[t][s] -= w * vc[t];
         }
       }
     }
@@ -300,18 +313,26 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
       double vc[BR_RPL];
 #pragma unroll
       for (int t = 0; t < BR_RPL; ++t) vc[t] = v[roff + 32 * t + lane];
+      // inactive target columns are zero and stay zero: no branches, reductions interleaved
+      double dt[NS];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        if (s * BR_W + warp < ntgt) {
-          double dt = v0 * tr[0][s] + v1 * tr[1][s];
+        double q = (v0 * tr[0][s] + v1 * tr[1][s]) + (vc[0] * tc[0][s] + vc[1] * tc[1][s]);
 #pragma unroll
-          for (int t = 0; t < BR_RPL; ++t) dt += vc[t] * tc[t][s];
-          dt = tau * warp_sum(dt);
-          tr[0][s] -= dt * v0;
-          tr[1][s] -= dt * v1;
+        for (int t = 2; t < BR_RPL; ++t) q += vc[t] * tc[t][s];
+        dt[s] = q;
+      }
 #pragma unroll
-          for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= dt * vc[t];
-        }
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const double w = tau * dt[s];
+        tr[0][s] -= w * v0;
+        tr[1][s] -= w * v1;
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= w * vc[t];
       }
     }
   }
