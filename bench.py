@@ -253,10 +253,14 @@ def main():
     del res
 
     # ------------------------------------------------------------ end to end (pinned host buffers)
+    # the public host-to-host call: inputs copied from pinned memory and results copied back
+    # inside the timed region, pipelined over 2 slices (tt_round_batch_host)
     host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores_h]
     h2d = sum(x.numel() * 8 for term in host for x in term)
-    out_host = torch.empty(out_doubles + 1024, dtype=torch.float64).pin_memory()
+    out_host = torch.empty(out_doubles + 4096, dtype=torch.float64).pin_memory()
     e2e_ms, d2h = [], 0
+    # one untimed call first (the torch caching allocator sizes the slice buffers)
+    out_host, _, _, _ = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=2, out_host=out_host)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -264,14 +268,12 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        dev_in = [[x.to(dev, non_blocking=True) for x in term] for term in host]
-        res = step(dev_in)
-        cnt = res.download(out_host)
+        out_host, rk_h, nr_h, cnt = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=2,
+                                                          out_host=out_host, start_event=e0)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-        d2h = cnt * 8 + res.ranks.nbytes
-        del res, dev_in
+        d2h = cnt * 8 + rk_h.nbytes + nr_h.nbytes
     te = sum(e2e_ms) / 1e3
     if world > 1:
         t = torch.tensor([te], device=dev, dtype=torch.float64)

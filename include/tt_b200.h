@@ -210,6 +210,10 @@ TT_API tt_status tt_batch_view(tt_batch bt, int32_t b, tt_view* out);
  * in order, each core (r_{k-1}, n_k, r_k) C order; *count = doubles in the batch (also set
  * when capacity is too small: TT_EINVAL).  Synchronises. */
 TT_API tt_status tt_batch_download(tt_ctx ctx, tt_batch bt, double* host, int64_t capacity, int64_t* count);
+/* Result arena w (0-based) of the batch: *ptr = DEVICE pointer, *count = doubles; the arenas in
+ * order hold the items in order, each item's cores in order (C order).  TT_EINDEX past the
+ * last arena. */
+TT_API tt_status tt_batch_arena(tt_batch bt, int32_t w, const double** ptr, int64_t* count);
 TT_API tt_status tt_batch_free(tt_ctx ctx, tt_batch bt);
 
 /* ---------------------------------------------------------------- drivers */

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     tt_orth,
     tt_round,
     tt_round_batch,
+    tt_round_batch_host,
     tt_round_batch_strided,
     tt_sum,
 )

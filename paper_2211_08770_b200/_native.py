@@ -23,7 +23,7 @@ EXPORTED = [
     "tt_ctx_launch_count", "tt_ctx_sync", "tt_ctx_profile", "tt_ctx_profile_query", "tt_tensor_view", "tt_tensor_free", "tt_upload", "tt_download",
     "tt_sum", "tt_axpy", "tt_dot_batch", "tt_gram", "tt_gram_blocks", "tt_element", "tt_norm",
     "tt_round", "tt_round_batch", "tt_orth",
-    "tt_round_batch_strided", "tt_batch_shape", "tt_batch_ranks", "tt_batch_view", "tt_batch_download", "tt_batch_free",
+    "tt_round_batch_strided", "tt_batch_shape", "tt_batch_ranks", "tt_batch_view", "tt_batch_download", "tt_batch_arena", "tt_batch_free",
 ]
 
 
@@ -107,6 +107,7 @@ def load() -> C.CDLL:
         "tt_batch_ranks": (C.c_int, [P, C.POINTER(i64), C.POINTER(dbl)]),
         "tt_batch_view": (C.c_int, [P, i32, VP]),
         "tt_batch_download": (C.c_int, [P, P, P, i64, C.POINTER(i64)]),
+        "tt_batch_arena": (C.c_int, [P, i32, C.POINTER(P), C.POINTER(i64)]),
         "tt_batch_free": (C.c_int, [P, P]),
         "tt_orth": (C.c_int, [P, C.c_int, i32, VP, C.POINTER(OrthOpts), C.POINTER(P), C.POINTER(dbl),
                               C.POINTER(OrthReport)]),

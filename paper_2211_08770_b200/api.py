@@ -246,6 +246,18 @@ class BatchTT:
             out.append(torch.as_tensor(_CoreArray(v.core[k], shp, self), device=f"cuda:{self.ctx.device}"))
         return out
 
+    def arenas(self):
+        """[(device pointer, doubles)] of the result arenas: items in order, cores in order."""
+        out, w = [], 0
+        while True:
+            ptr, cnt = C.c_void_p(), C.c_int64()
+            st = self.ctx.lib.tt_batch_arena(self.handle, w, C.byref(ptr), C.byref(cnt))
+            if st == 3:  # TT_EINDEX: past the last arena
+                return out
+            self.ctx.check(st)
+            out.append((int(ptr.value or 0), int(cnt.value)))
+            w += 1
+
     def total_doubles(self) -> int:
         cnt = C.c_int64()
         st = self.ctx.lib.tt_batch_download(self.ctx.handle, self.handle, None, 0, C.byref(cnt))
@@ -307,6 +319,74 @@ def tt_round_batch_strided(ctx: Context, terms, coeffs, rel_tol: float, norms=No
         ctx.handle, B, K, d, n, r, base, stride, cf.ctypes.data_as(C.POINTER(C.c_double)),
         None if nr is None else nr.ctypes.data_as(C.POINTER(C.c_double)), C.byref(o), C.byref(h)))
     return BatchTT(ctx, h)
+
+
+def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=None,
+                        floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0, chunks: int = 2,
+                        out_host: Optional[torch.Tensor] = None, start_event=None):
+    """End-to-end batched rounding from HOST inputs to HOST results, pipelined over `chunks`
+    contiguous slices of the batch: the host->device copy of slice c+1 and the device->host
+    copy of slice c-1's results run on a copy stream while slice c is rounded on the context's
+    stream (stream orchestration only; the rounding is tt_round_batch_strided).
+    host_terms[l][k]: pinned CPU float64 tensors (B, r_{k-1}, n_k, r_k).  Results go to
+    out_host (pinned float64, items in order, cores in order, each core C order; allocated if
+    None).  Returns (out_host, ranks (B, d+1), norms (B,), doubles written)."""
+    K, d = len(host_terms), len(host_terms[0])
+    B = int(host_terms[0][0].shape[0])
+    coeffs = np.asarray(coeffs, dtype=np.float64).reshape(B, K)
+    norms_a = None if norms is None else np.asarray(norms, dtype=np.float64).reshape(B, K)
+    dev = f"cuda:{ctx.device}"
+    copy = torch.cuda.Stream(ctx.device)
+    if start_event is not None:
+        copy.wait_event(start_event)
+    bounds = [(B * c) // chunks for c in range(chunks + 1)]
+    staged, events = [], []
+
+    def h2d(c):
+        a, b = bounds[c], bounds[c + 1]
+        with torch.cuda.stream(copy):
+            t = [[x[a:b].to(dev, non_blocking=True) for x in term] for term in host_terms]
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        return t, ev
+
+    staged.append(h2d(0))
+    ranks, nrm, pending = [], [], []
+    offset = 0
+    for c in range(chunks):
+        if c + 1 < chunks:
+            staged.append(h2d(c + 1))
+        t, ev = staged[c]
+        ctx.stream.wait_event(ev)
+        a, b = bounds[c], bounds[c + 1]
+        with torch.cuda.stream(ctx.stream):
+            res = tt_round_batch_strided(ctx, t, coeffs[a:b], rel_tol,
+                                         norms=None if norms_a is None else norms_a[a:b],
+                                         floor_c=floor_c, max_rank=max_rank)
+        ranks.append(res.ranks)
+        nrm.append(res.norms)
+        n = res.total_doubles()
+        if out_host is None:
+            out_host = torch.empty(0, dtype=torch.float64)
+        if out_host.numel() < offset + n:
+            grown = torch.empty(int((offset + n) * (chunks / (c + 1)) * 1.05) + 1024, dtype=torch.float64).pin_memory()
+            grown[:offset].copy_(out_host[:offset])
+            out_host = grown
+        # device -> host of this slice on the copy stream, overlapping the next slice's rounding
+        done = torch.cuda.Event()
+        done.record(ctx.stream)
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            for w, (ptr, cnt) in enumerate(res.arenas()):
+                dst = out_host[offset:offset + cnt]
+                src = torch.as_tensor(_CoreArray(ptr, (cnt,), res), device=dev)
+                dst.copy_(src, non_blocking=True)
+                offset += cnt
+        pending.append(res)  # keep the device results alive until their copies finished
+        del t
+    copy.synchronize()
+    del pending
+    return out_host, np.concatenate(ranks), np.concatenate(nrm), offset
 
 
 def tt_sum(ctx: Context, terms, coeffs) -> LibTT:

@@ -422,6 +422,14 @@ tt_status tt_batch_download(tt_ctx ctx, tt_batch bt, double* host, int64_t capac
   });
 }
 
+tt_status tt_batch_arena(tt_batch bt, int32_t w, const double** ptr, int64_t* count) {
+  if (!bt || !ptr || !count) return TT_EINVAL;
+  if (w < 0 || (size_t)w >= bt->res.arenas.size()) return TT_EINDEX;
+  *ptr = static_cast<const double*>(bt->res.arenas[(size_t)w]);
+  *count = bt->res.arena_size[(size_t)w];
+  return TT_OK;
+}
+
 tt_status tt_batch_free(tt_ctx ctx, tt_batch bt) {
   if (!ctx) return TT_EINVAL;
   if (!bt) return TT_OK;

@@ -192,3 +192,22 @@ def test_batch_strided_c4_stacked_generator():
         refx = tt.tt_sum(terms[:2], [1.0, 1.0]) if b % 2 == 0 else terms[0]
         assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
         _check_item(g, list(res.ranks[b]), terms, list(coeffs[b]), 1e-6, rounding.DEFAULT_FLOOR_C, norms=[1.0] * 4)
+
+
+def test_batch_host_pipeline_matches_device_call():
+    """tt_round_batch_host (host inputs -> host results, 3 pipelined slices) returns the same
+    bytes as tt_round_batch_strided on the device copies, items and cores in order."""
+    import torch
+    import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums_stacked
+    B = 10
+    cores, coeffs = make_batch_sums_stacked(B, d=6, n=9, r=5)
+    host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores]
+    out, ranks, norms, cnt = P.tt_round_batch_host(ctx(), host, coeffs, 1e-6, norms=np.ones((B, 4)), chunks=3)
+    res = P.tt_round_batch_strided(ctx(), [[c.cuda() for c in term] for term in host], coeffs, 1e-6,
+                                   norms=np.ones((B, 4)))
+    assert np.array_equal(ranks, res.ranks)
+    flat = np.concatenate([np.concatenate([c.ravel() for c in res.item_numpy(b)]) for b in range(B)])
+    assert cnt == flat.size
+    assert np.array_equal(out[:cnt].numpy(), flat)
+    np.testing.assert_array_equal(norms, res.norms)
