@@ -351,7 +351,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(args.batch, world),
-            "e2e": {"value": e2e_value, "unit": "roundings/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": "roundings/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_steps": [round(x, 2) for x in e2e_ms], "api": "tt_round_batch_host (2 pipelined slices)"},
             "gpu_launches": launches,
             "roofline": roof,
             "kernel_profile": "CUDA events around every launch of one extra step (ctx stream)",

@@ -350,6 +350,10 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
             ev.record(copy)
         return t, ev
 
+    import os
+    import time
+    dbg = os.environ.get("TT_B200_HOST_DEBUG") == "1"
+    t0 = time.perf_counter()
     staged.append(h2d(0))
     ranks, nrm, pending = [], [], []
     offset = 0
@@ -384,7 +388,11 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
                 offset += cnt
         pending.append(res)  # keep the device results alive until their copies finished
         del t
+        if dbg:
+            print(f"[host_pipeline] slice {c} done at {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
     copy.synchronize()
+    if dbg:
+        print(f"[host_pipeline] copies done at {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
     del pending
     return out_host, np.concatenate(ranks), np.concatenate(nrm), offset
 
