@@ -24,6 +24,7 @@
 // ranks R'_{k-1} = min(n_k R'_k, R_{k-1}) (identical tensor; the truncation decisions come from
 // the same SVDs).  Supported shapes: d >= 2, every formal rank R_k <= 64, K <= 16 terms.
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -81,6 +82,8 @@ struct BRArgs {
   double* YT;                  // their taus                 [item][ytstride]
   double* Z;                   // Y_{k+1} staging, 2 slots   [item][2][zstride]
   double* out;                 // worst-case output cores    [item][ostride]
+  double* JM;                  // l2r: Jacobi input (R_Y or Y), 64 x 64 per item
+  double* TT;                  // l2r: apply targets U_rho and V_rho S, 2 x 64 x 64 per item
   int* ranks;                  // [item][d+1]
   double* scal;                // [item][4]: ||x||, tau, s, zero flag
   int* info;                   // [item]: 1 = Jacobi hit its sweep limit
@@ -339,25 +342,25 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
 }
 
 // out(row, col) = Q [T; 0] for the m-row factor whose stacks are at V (taus Tq, ncol reflectors
-// per stack); T = tr (R-block rows) on entry.  Output address: out[row * rs + col * cs].
-template <int NS>
-__device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, const double* Tq, int64_t m, int ncol,
-                                        int ntgt, double* out, int64_t rs, int64_t cs, VStage& vs) {
+// per stack); this warp's target columns col0 + 8 s + warp (s < 4, col < ntgt) with the R-block
+// rows of T in tr on entry.  Output address: out[row * rs + col * cs].
+__device__ __noinline__ void br_apply_q(double (&tr)[2][4], const double* V, const double* Tq, int64_t m, int ncol,
+                                        int col0, int ntgt, double* out, int64_t rs, int64_t cs, VStage& vs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nst = br_stacks(m);
   uint32_t ph[2] = {vs.phase[0], vs.phase[1]};
-  double tc[BR_RPL][NS];
+  double tc[BR_RPL][4];
 #pragma unroll 1
   for (int q = nst - 1; q >= 0; --q) {
 #pragma unroll
     for (int t = 0; t < BR_RPL; ++t)
 #pragma unroll
-      for (int s = 0; s < NS; ++s) tc[t][s] = 0.0;
-    br_stack_apply(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt, vs, ph);
+      for (int s = 0; s < 4; ++s) tc[t][s] = 0.0;
+    br_stack_apply<4>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
     const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const int col = s * BR_W + warp;
+    for (int s = 0; s < 4; ++s) {
+      const int col = col0 + s * BR_W + warp;
       if (col < ntgt) {
 #pragma unroll
         for (int t = 0; t < BR_RPL; ++t) {
@@ -374,6 +377,25 @@ __device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, co
   __syncthreads();
   if (threadIdx.x == 0) { vs.phase[0] = ph[0]; vs.phase[1] = ph[1]; }
   __syncthreads();
+}
+
+// Q [T; 0] for the rho target columns stored in src (column-major, ld 64, rows < cp), in passes
+// of 32 columns (4 per warp).
+__device__ void br_apply_targets(const double* __restrict__ src, int rho, int cp, const double* V, const double* Tq,
+                                 int64_t m, int ncol, double* out, int64_t rs, int64_t cs, VStage& vs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int col0 = 0; col0 < rho; col0 += 4 * BR_W) {
+    double tr[2][4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int col = col0 + s * BR_W + warp;
+      const bool ok = col < rho;
+      tr[0][s] = (ok && lane < cp) ? src[col * BR_C + lane] : 0.0;
+      tr[1][s] = (ok && lane + 32 < cp) ? src[col * BR_C + lane + 32] : 0.0;
+    }
+    br_apply_q(tr, V, Tq, m, ncol, col0, rho, out, rs, cs, vs);
+  }
 }
 
 // Flat-tree QR of an m x ncol matrix given by elem(row, col) (zero outside); reflectors to V,
@@ -675,60 +697,25 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
   return conv;
 }
 
-// Output core k = Q_Y [U_rho; 0] (U_rho = normalised Jacobi columns, rows <= 64), row-major.
-template <int NS>
-__device__ void br_out_core(BRSmem& sm, int rho, int cp, int64_t p, const double* YV, const double* YT, double* ok) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double tr[2][NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int col = s * BR_W + warp;
-    const bool ok2 = col < rho;
-    const int pc = ok2 ? sm.perm[col] : 0;
-    const double inv = (ok2 && sm.sig[col] > 0.0) ? 1.0 / sm.sig[col] : 0.0;
-    tr[0][s] = (ok2 && lane < cp) ? sm.Rs[pc * BR_C + lane] * inv : 0.0;
-    tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Rs[pc * BR_C + lane + 32] * inv : 0.0;
-  }
-  br_apply_q<NS>(tr, YV, YT, p, cp, rho, ok, rho, 1, sm.vst);
-}
-
-// Z_{k+1} = H_{k+1} [(S_rho V_rho^T)^T; 0] (m1 x rho, column-major ld m1).
-template <int NS>
-__device__ void br_next_core(BRSmem& sm, int rho, int cp, int64_t m1, int c1, const double* V, const double* Tq,
-                             double* dst) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double tr[2][NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int col = s * BR_W + warp;
-    const bool ok2 = col < rho;
-    const int pc = ok2 ? sm.perm[col] : 0;
-    const double sg = ok2 ? sm.sig[col] : 0.0;
-    tr[0][s] = (ok2 && lane < cp) ? sm.Aux[pc * BR_C + lane] * sg : 0.0;
-    tr[1][s] = (ok2 && lane + 32 < cp) ? sm.Aux[pc * BR_C + lane + 32] * sg : 0.0;
-  }
-  br_apply_q<NS>(tr, V, Tq, m1, c1, rho, dst, 1, m1, sm.vst);
-}
-
-__global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
+// ---- left-to-right step at split k, in three launches over the batch:
+//   br_l2r_qr_kernel     Y_k -> (tall: flat-tree QR, reflectors to YV/YT) -> Jacobi input JM;
+//                        split 1 also computes ||x|| and tau
+//   br_l2r_svd_kernel    one-sided Jacobi of JM, rank rho_k, targets U_rho and V_rho S to TT
+//                        (short Y_k: output core k written directly)
+//   br_l2r_apply_kernel  output core k = Q_Y [U_rho; 0] and Z_{k+1} = H_{k+1} [(S V^T)^T; 0]
+// (split so that the register-light Jacobi and applications run three CTAs per SM).
+__global__ void __launch_bounds__(BR_T, 2) br_l2r_qr_kernel(BRArgs A, int k) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
   const BRShape* S = A.sh;
   const int b = blockIdx.x, gb = A.item0 + b;
   const int d = S->d, K = S->K;
   const int kc = k - 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   int* rk = A.ranks + (int64_t)b * (d + 1);
   double* sc = A.scal + (int64_t)b * 4;
   double* out = A.out + (int64_t)b * S->ostride;
   const int n = S->n[kc], cp = S->Rp[k];
-  if (tid == 0) {
-    mbar_init(&sm.vst.bar[0], 1);
-    mbar_init(&sm.vst.bar[1], 1);
-    sm.vst.phase[0] = sm.vst.phase[1] = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   if (k > 1 && sc[3] != 0.0) {  // ||x|| = 0: rank-1 zero tensor
     for (int i = tid; i < n; i += BR_T) out[S->ooff[kc] + i] = 0.0;
     if (k + 1 == d)
@@ -763,7 +750,6 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
       __syncthreads();
     }
   }
-  const int jrows = tall ? cp : (int)p;
   if (k == 1) {
     double q = 0.0;
     for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; q += v * v; }
@@ -786,8 +772,29 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
       if (tid == 0) { rk[1] = 1; rk[d] = 1; }
       return;
     }
-    __syncthreads();
   }
+  double* jm = A.JM + (int64_t)b * BR_C * BR_C;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) jm[idx] = sm.Rs[idx];
+}
+
+__global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x;
+  const int d = S->d;
+  const int kc = k - 1;
+  const int tid = threadIdx.x;
+  int* rk = A.ranks + (int64_t)b * (d + 1);
+  const double* sc = A.scal + (int64_t)b * 4;
+  if (sc[3] != 0.0) return;
+  const int n = S->n[kc], cp = S->Rp[k];
+  const int64_t p = (k == 1) ? (int64_t)n : (int64_t)rk[k - 1] * n;
+  const bool tall = p > BR_C;
+  const int jrows = tall ? cp : (int)p;
+  const double* jm = A.JM + (int64_t)b * BR_C * BR_C;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Rs[idx] = jm[idx];
+  __syncthreads();
   const long long cj0 = clock64();
   const bool conv = br_jacobi(sm, jrows, cp);
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[8] += clock64() - cj0;
@@ -812,30 +819,70 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_kernel(BRArgs A, int k) {
   }
   __syncthreads();
   const int rho = sm.rho;
-  // ---- output core k = Q_Y U_rho ((rho_{k-1} n_k) x rho, row-major)
-  const long long co0 = clock64();
-  double* ok = out + S->ooff[kc];
-  if (tall) {
-    if (rho <= BR_C / 2) br_out_core<BR_CPW / 2>(sm, rho, cp, p, YV, YT, ok);
-    else br_out_core<BR_CPW>(sm, rho, cp, p, YV, YT, ok);
-  } else {
+  double* tt = A.TT + (int64_t)b * 2 * BR_C * BR_C;
+  if (tall) {  // U_rho (cp x rho), the target of Q_Y
+    for (int idx = tid; idx < BR_C * rho; idx += BR_T) {
+      const int col = idx / BR_C, row = idx % BR_C;
+      const double sg = sm.sig[col];
+      tt[idx] = (sg > 0.0 && row < cp) ? sm.Rs[sm.perm[col] * BR_C + row] / sg : 0.0;
+    }
+  } else {  // short Y_k: output core k = U_rho directly ((rho_{k-1} n_k) x rho, row-major)
+    double* ok = A.out + (int64_t)b * S->ostride + S->ooff[kc];
     for (int idx = tid; idx < p * rho; idx += BR_T) {
       const int row = idx / rho, col = idx % rho;
       const double sg = sm.sig[col];
       ok[idx] = sg > 0.0 ? sm.Rs[sm.perm[col] * BR_C + row] / sg : 0.0;
     }
   }
+  for (int idx = tid; idx < BR_C * rho; idx += BR_T) {  // V_rho S (cp x rho), the target of H_{k+1}
+    const int col = idx / BR_C, row = idx % BR_C;
+    tt[BR_C * BR_C + idx] = row < cp ? sm.Aux[sm.perm[col] * BR_C + row] * sm.sig[col] : 0.0;
+  }
+}
+
+struct BRSmemA {
+  VStage vst;
+};
+
+__global__ void __launch_bounds__(BR_T, 3) br_l2r_apply_kernel(BRArgs A, int k) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  BRSmemA& sm = *reinterpret_cast<BRSmemA*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x;
+  const int d = S->d;
+  const int kc = k - 1;
+  const int tid = threadIdx.x;
+  const int* rk = A.ranks + (int64_t)b * (d + 1);
+  const double* sc = A.scal + (int64_t)b * 4;
+  if (sc[3] != 0.0) return;
+  if (tid == 0) {
+    mbar_init(&sm.vst.bar[0], 1);
+    mbar_init(&sm.vst.bar[1], 1);
+    sm.vst.phase[0] = sm.vst.phase[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double* out = A.out + (int64_t)b * S->ostride;
+  const int n = S->n[kc], cp = S->Rp[k];
+  const int64_t p = (k == 1) ? (int64_t)n : (int64_t)rk[k - 1] * n;
+  const bool tall = p > BR_C;
+  const int rho = rk[k];
+  const double* tt = A.TT + (int64_t)b * 2 * BR_C * BR_C;
+  const long long co0 = clock64();
+  if (tall) {
+    const double* YV = A.YV + (int64_t)b * S->ystride;
+    const double* YT = A.YT + (int64_t)b * S->ytstride;
+    br_apply_targets(tt, rho, cp, YV, YT, p, cp, out + S->ooff[kc], rho, 1, sm.vst);
+  }
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[9] += clock64() - co0;
   const long long cz0 = clock64();
-  // ---- Z_{k+1} = H_{k+1} [(S V^T)^T; 0]   (m_{k+1} x rho, column-major)
   const int kn = kc + 1;  // core index of core k+1
   const int64_t m1 = (int64_t)S->n[kn] * S->Rp[k + 1];
   const int c1 = S->R[k];
   double* dst = (k + 1 == d) ? out + S->ooff[kn] : A.Z + (int64_t)b * 2 * S->zstride + ((k + 1) & 1) * S->zstride;
   const double* V = A.V + (int64_t)b * S->vstride + S->voff[kn];
   const double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kn];
-  if (rho <= BR_C / 2) br_next_core<BR_CPW / 2>(sm, rho, cp, m1, c1, V, Tq, dst);
-  else br_next_core<BR_CPW>(sm, rho, cp, m1, c1, V, Tq, dst);
+  br_apply_targets(tt + BR_C * BR_C, rho, cp, V, Tq, m1, c1, dst, 1, m1, sm.vst);
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[10] += clock64() - cz0;
 }
 
@@ -987,13 +1034,16 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   const double budget = std::min<double>(0.6 * ((double)free_b + (double)ctx->scratch_bytes), 100e9);
   const int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
   const int nb_max = std::min(W, B);
-  const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 2 * BR_C * BR_C + sh.ystride +
+  const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 5 * BR_C * BR_C + sh.ystride +
                                               sh.ytstride + 2 * sh.zstride + std::max<int64_t>(sh.ostride, 1) + 4) +
                             (size_t)nb_max * (d + 2) + 64;
   double* ws = static_cast<double*>(ctx_scratch(ctx, ws_doubles * sizeof(double)));
-  const size_t smem = sizeof(BRSmem);
+  // kernels that do not stage reflector slices leave out the VStage buffers
+  const size_t smem = offsetof(BRSmem, vst), smem_q = offsetof(BRSmem, vst), smem_a = sizeof(BRSmemA);
   TTB_CUDA(cudaFuncSetAttribute(br_r2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  TTB_CUDA(cudaFuncSetAttribute(br_l2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TTB_CUDA(cudaFuncSetAttribute(br_l2r_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
+  TTB_CUDA(cudaFuncSetAttribute(br_l2r_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
+  TTB_CUDA(cudaFuncSetAttribute(br_l2r_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
   res.B = B;
   res.d = d;
   res.n = in.n;
@@ -1008,7 +1058,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
     for (int w0 = 0; w0 < B; w0 += W) {
       const int nb = std::min(W, B - w0);
       stamp("wave start");
-      struct { double* p; } V, T, L, YV, YT, Z, O, SC;
+      struct { double* p; } V, T, L, YV, YT, Z, O, SC, JM, TT;
       struct { int* p; } RK, INF;
       {
         double* w = ws;  // carve the scratch (every piece a multiple of 2 doubles: 16-B aligned)
@@ -1020,6 +1070,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         YT.p = take((size_t)nb * sh.ytstride);
         Z.p = take((size_t)nb * 2 * sh.zstride);
         O.p = take((size_t)nb * std::max<int64_t>(sh.ostride, 1));
+        JM.p = take((size_t)nb * BR_C * BR_C);
+        TT.p = take((size_t)nb * 2 * BR_C * BR_C);
         SC.p = take((size_t)nb * 4);
         RK.p = reinterpret_cast<int*>(take(((size_t)nb * (d + 1) + 1) / 2));
         INF.p = reinterpret_cast<int*>(take(((size_t)nb + 1) / 2));
@@ -1030,7 +1082,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       a.cores = static_cast<const double* const*>(dtab.p);
       a.coef = static_cast<const double*>(dcoef.p);
       a.scale = static_cast<const double*>(dscale.p);
-      a.V = V.p; a.T = T.p; a.L = L.p; a.YV = YV.p; a.YT = YT.p; a.Z = Z.p; a.out = O.p;
+      a.V = V.p; a.T = T.p; a.L = L.p; a.YV = YV.p; a.YT = YT.p; a.Z = Z.p; a.out = O.p; a.JM = JM.p; a.TT = TT.p;
       a.ranks = RK.p; a.scal = SC.p; a.info = INF.p;
       a.rel_tol = o.rel_tol;
       a.floor_c = o.floor_c;
@@ -1055,8 +1107,11 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
                 br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
       }
-      for (int k = 1; k < d; ++k)
-        TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, k));
+      for (int k = 1; k < d; ++k) {
+        TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
+        TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_svd_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
+        TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
+      }
       if (dbg.p) {
         long long h[16];
         TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1076,7 +1131,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       d2h_small(ctx, hsc.data(), SC.p, hsc.size());
       std::vector<int64_t> dst((size_t)nb * d), sz((size_t)nb * d);
       int64_t tot = 0;
-      double l2r_fl = 0.0;
+      double l2r_svd_fl = 0.0, l2r_qr_fl = 0.0, l2r_ap_fl = 0.0;
       for (int b = 0; b < nb; ++b) {
         const int* r = hr.data() + (size_t)b * (d + 1);
         for (int kc = 0; kc < d; ++kc) {
@@ -1089,12 +1144,18 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
           const double pp = (double)r[k - 1] * sh.n[k - 1], cp = sh.Rp[k], rho = r[k];
           const double a1 = std::max(pp, cp), b1 = std::min(pp, cp);
           const double m1 = (double)sh.n[k] * sh.Rp[k + 1], c1 = sh.R[k];
-          l2r_fl += 6.0 * a1 * b1 * b1 + 11.0 * b1 * b1 * b1;  // R-SVD (GVL nominal)
-          if (pp > BR_C) l2r_fl += 4.0 * pp * cp * rho - 2.0 * cp * cp * rho;
-          l2r_fl += 4.0 * m1 * std::min(m1, c1) * rho - 2.0 * std::min(m1, c1) * std::min(m1, c1) * rho;
+          // R-SVD (GVL nominal 6ab^2 + 11b^3): the QR part 2ab^2 - 2b^3/3 is the qr
+          // launch, the rest the svd launch
+          const double qrf = (pp > BR_C) ? 2.0 * a1 * b1 * b1 - 2.0 * b1 * b1 * b1 / 3.0 : 0.0;
+          l2r_qr_fl += qrf;
+          l2r_svd_fl += 6.0 * a1 * b1 * b1 + 11.0 * b1 * b1 * b1 - qrf;
+          if (pp > BR_C) l2r_ap_fl += 4.0 * pp * cp * rho - 2.0 * cp * cp * rho;
+          l2r_ap_fl += 4.0 * m1 * std::min(m1, c1) * rho - 2.0 * std::min(m1, c1) * std::min(m1, c1) * rho;
         }
       }
-      prof_credit(ctx, "batch_l2r_svd", l2r_fl);
+      prof_credit(ctx, "batch_l2r_svd", l2r_svd_fl);
+      prof_credit(ctx, "batch_l2r_qr", l2r_qr_fl);
+      prof_credit(ctx, "batch_l2r_apply", l2r_ap_fl);
       void* arena = nullptr;
       if (cudaMallocAsync(&arena, (size_t)std::max<int64_t>(tot, 1) * sizeof(double), ctx->stream) != cudaSuccess) {
         (void)cudaGetLastError();
