@@ -158,8 +158,9 @@ struct BRSmem {
 // registers a[t][s] (row 32t + lane, column 8s + warp).  LAPACK dlarfg arithmetic per column j;
 // on return the strictly lower part of Rs holds stack 0's R-block reflector parts, a[][] holds
 // the chunk reflector parts, taus go to tau_out[j] (global).
-__device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, double* tau_out) {
+__device__ void br_stack_qr_first(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, double* tau_out, long long* sdbg) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long c0 = 0, c1 = 0, c2 = 0;
   // j = 8 S + ww: the slot S of column j in its owner warp ww is a compile-time index
 #pragma unroll
   for (int S = 0; S < BR_CPW; ++S) {
@@ -168,6 +169,7 @@ __device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, d
       const int j = S * BR_W + ww;
       if (j >= ncol) break;
       const int buf = j & 1;
+      if (sdbg) c0 = clock64();
       if (warp == ww) {
         double* Rc = sm.Rs + j * BR_C;
         const double r0 = Rc[lane], r1 = Rc[lane + 32];
@@ -204,7 +206,9 @@ __device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, d
         if (lane + 32 == j) Rc[lane + 32] = beta;
         if (lane == 0) { sm.tb[buf] = tau; tau_out[j] = tau; }
       }
+      if (sdbg) c1 = clock64();
       __syncthreads();
+      if (sdbg) c2 = clock64();
       const double tau = sm.tb[buf];
       if (tau != 0.0) {
         const double* v = sm.vb[buf];
@@ -242,6 +246,93 @@ __device__ void br_stack_qr(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, d
           for (int t = 0; t < BR_RPL; ++t) a[t][s] -= w * vc[t];
         }
       }
+      if (sdbg && tid == 0) {
+        const long long c3 = clock64();
+        if (ww == 0) { sdbg[0] += c1 - c0; sdbg[3] += 1; } else { sdbg[4] += c1 - c0; }
+        sdbg[1] += c2 - c1;
+        sdbg[2] += c3 - c2;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Stacks after the first: the R block is upper triangular, so the reflector's R-block part is
+// the unit vector e_j: the R block enters the column dot products and updates only through row j.
+__device__ void br_stack_qr_later(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, double* tau_out, long long* sdbg) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+  for (int S = 0; S < BR_CPW; ++S) {
+#pragma unroll 1
+    for (int ww = 0; ww < BR_W; ++ww) {
+      const int j = S * BR_W + ww;
+      if (j >= ncol) break;
+      const int buf = j & 1;
+      if (sdbg) c0 = clock64();
+      if (warp == ww) {
+        double* Rc = sm.Rs + j * BR_C;
+        double ss = 0.0;
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) ss += a[t][S] * a[t][S];
+        const double sigma = warp_sum(ss);
+        const double alpha = Rc[j];
+        double tau = 0.0, beta = alpha, scal = 0.0;
+        if (sigma != 0.0) {
+          const double nr = sqrt(alpha * alpha + sigma);
+          beta = alpha >= 0.0 ? -nr : nr;
+          const double am = alpha - beta;
+          const double inv = 1.0 / (beta * am);
+          tau = -am * am * inv;
+          scal = beta * inv;
+        }
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) {
+          a[t][S] *= scal;
+          sm.vb[buf][BR_C + 32 * t + lane] = a[t][S];
+        }
+        __syncwarp();
+        if (lane == 0) { Rc[j] = beta; sm.tb[buf] = tau; tau_out[j] = tau; }
+      }
+      if (sdbg) c1 = clock64();
+      __syncthreads();
+      if (sdbg) c2 = clock64();
+      const double tau = sm.tb[buf];
+      if (tau != 0.0) {
+        const double* v = sm.vb[buf];
+        double vc[BR_RPL];
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) vc[t] = v[BR_C + 32 * t + lane];
+        double dt[BR_CPW], rj[BR_CPW];
+#pragma unroll
+        for (int s = S; s < BR_CPW; ++s) {
+          const int col = min(s * BR_W + warp, BR_C - 1);
+          rj[s] = sm.Rs[col * BR_C + j];  // broadcast: row j of the R block
+          double q = vc[0] * a[0][s] + vc[1] * a[1][s];
+#pragma unroll
+          for (int t = 2; t < BR_RPL; ++t) q += vc[t] * a[t][s];
+          dt[s] = q;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+#pragma unroll
+        for (int s = S; s < BR_CPW; ++s) {
+          const int col = s * BR_W + warp;
+          const bool act = (s > S || warp > ww) && col < ncol;
+          const double w = act ? tau * (rj[s] + dt[s]) : 0.0;
+          if (act && lane == 0) sm.Rs[col * BR_C + j] = rj[s] - w;
+#pragma unroll
+          for (int t = 0; t < BR_RPL; ++t) a[t][s] -= w * vc[t];
+        }
+      }
+      if (sdbg && tid == 0) {
+        const long long c3 = clock64();
+        if (ww == 0) { sdbg[0] += c1 - c0; sdbg[3] += 1; } else { sdbg[4] += c1 - c0; }
+        sdbg[1] += c2 - c1;
+        sdbg[2] += c3 - c2;
+      }
     }
   }
   __syncthreads();
@@ -277,7 +368,7 @@ __device__ void br_store_stack(const double (&a)[BR_RPL][BR_CPW], BRSmem& sm, in
 // target <- H_q target for one stack's reflectors (j = ncol-1 .. 0), reflector vectors read
 // from the staged slices.  The target's R-block rows live in tr[0/1][s] (rows lane, lane+32),
 // its chunk rows in tc[t][s]; column 8s + warp.
-template <int NS>
+template <int NS, bool FIRST>
 __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], const double* __restrict__ Vq,
                                const double* __restrict__ tq, int q, int ncol, int ntgt, VStage& vs,
                                uint32_t (&ph)[2]) {
@@ -305,13 +396,10 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
       const double tau = __ldg(tq + j);
       if (tau == 0.0) continue;
       const double* v = sv + (j - j0) * ld;
-      double v0, v1;
-      if (q == 0) {
+      double v0 = 0.0, v1 = 0.0;
+      if (FIRST) {
         v0 = lane > j ? v[lane] : (lane == j ? 1.0 : 0.0);
         v1 = lane + 32 > j ? v[lane + 32] : (lane + 32 == j ? 1.0 : 0.0);
-      } else {
-        v0 = lane == j ? 1.0 : 0.0;
-        v1 = lane + 32 == j ? 1.0 : 0.0;
       }
       double vc[BR_RPL];
 #pragma unroll
@@ -320,7 +408,10 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
       double dt[NS];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        double q = (v0 * tr[0][s] + v1 * tr[1][s]) + (vc[0] * tc[0][s] + vc[1] * tc[1][s]);
+        // later stacks: the reflector's R-block part is e_j (row j held by lane j & 31)
+        const double rpart = FIRST ? (v0 * tr[0][s] + v1 * tr[1][s])
+                                   : (lane == (j & 31) ? (j < 32 ? tr[0][s] : tr[1][s]) : 0.0);
+        double q = rpart + (vc[0] * tc[0][s] + vc[1] * tc[1][s]);
 #pragma unroll
         for (int t = 2; t < BR_RPL; ++t) q += vc[t] * tc[t][s];
         dt[s] = q;
@@ -332,8 +423,12 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const double w = tau * dt[s];
-        tr[0][s] -= w * v0;
-        tr[1][s] -= w * v1;
+        if (FIRST) {
+          tr[0][s] -= w * v0;
+          tr[1][s] -= w * v1;
+        } else if (lane == (j & 31)) {
+          if (j < 32) tr[0][s] -= w; else tr[1][s] -= w;
+        }
 #pragma unroll
         for (int t = 0; t < BR_RPL; ++t) tc[t][s] -= w * vc[t];
       }
@@ -356,7 +451,8 @@ __device__ __noinline__ void br_apply_q(double (&tr)[2][4], const double* V, con
     for (int t = 0; t < BR_RPL; ++t)
 #pragma unroll
       for (int s = 0; s < 4; ++s) tc[t][s] = 0.0;
-    br_stack_apply<4>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
+    if (q == 0) br_stack_apply<4, true>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
+    else br_stack_apply<4, false>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
     const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -419,7 +515,8 @@ __device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem
     elem.chunk(a, base, m, ncol);
     __syncthreads();
     const long long c1 = clock64();
-    br_stack_qr(a, sm, ncol, Tq + (int64_t)q * BR_C);
+    if (q == 0) br_stack_qr_first(a, sm, ncol, Tq, dbg ? dbg + 16 : nullptr);
+    else br_stack_qr_later(a, sm, ncol, Tq + (int64_t)q * BR_C, dbg ? dbg + 16 : nullptr);
     const long long c2 = clock64();
     br_store_stack(a, sm, q, ncol, V + br_stack_off(q, ncol));
     if (dbg && tid == 0) { dbg[0] += c1 - c0; dbg[1] += c2 - c1; dbg[2] += clock64() - c2; }
@@ -1092,8 +1189,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       const char* dbe = std::getenv("TT_B200_BR_DEBUG");
       LBuf dbg;
       if (dbe && dbe[0] == '1') {
-        dbg.alloc(ctx, 16);
-        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 16 * sizeof(long long), ctx->stream));
+        dbg.alloc(ctx, 32);
+        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 32 * sizeof(long long), ctx->stream));
       }
       a.dbg = dbg.p;
       for (int kc = d - 1; kc >= 1; --kc) {
@@ -1113,11 +1210,11 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
       }
       if (dbg.p) {
-        long long h[16];
+        long long h[32];
         TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         TTB_CUDA(cudaStreamSynchronize(ctx->stream));
-        std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld outcore %lld nextcore %lld (cycles, CTA 0)\n",
-                     h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[9], h[10]);
+        std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld outcore %lld nextcore %lld (cycles, CTA 0) | qr steps: owner(w0) %lld x%lld, pre-barrier(w0 not owner) %lld, barrier %lld, update %lld\n",
+                     h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[9], h[10], h[16], h[19], h[20], h[17], h[18]);
       }
       // ranks (the one host synchronisation of the wave), then compaction
       std::vector<int> hr((size_t)nb * (d + 1)), hinf((size_t)nb);
