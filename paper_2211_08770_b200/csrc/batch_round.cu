@@ -733,16 +733,19 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
       double* ca = sm.Rs + (act ? p0 : 0) * BR_C;
       double* cb = sm.Rs + (act ? p1 : 0) * BR_C;
       double x[8], y[8];
-      double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int row = 8 * ((k + pp) & 7) + r8;
         x[k] = act ? ca[row] : 0.0;
         y[k] = act ? cb[row] : 0.0;
-        al += x[k] * x[k];
-        be += y[k] * y[k];
-        ga += x[k] * y[k];
       }
+      // pairwise (depth-3) sums: shorter dependency chains than sequential accumulation
+      double al = ((x[0] * x[0] + x[1] * x[1]) + (x[2] * x[2] + x[3] * x[3])) +
+                  ((x[4] * x[4] + x[5] * x[5]) + (x[6] * x[6] + x[7] * x[7]));
+      double be = ((y[0] * y[0] + y[1] * y[1]) + (y[2] * y[2] + y[3] * y[3])) +
+                  ((y[4] * y[4] + y[5] * y[5]) + (y[6] * y[6] + y[7] * y[7]));
+      double ga = ((x[0] * y[0] + x[1] * y[1]) + (x[2] * y[2] + x[3] * y[3])) +
+                  ((x[4] * y[4] + x[5] * y[5]) + (x[6] * y[6] + x[7] * y[7]));
 #pragma unroll
       for (int o = 4; o > 0; o >>= 1) {
         al += __shfl_xor_sync(0xffffffffu, al, o);
@@ -751,9 +754,10 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
       }
       const bool rot = act && ga != 0.0 && al > negl && be > negl && fabs(ga) > tol * sqrt(al * be);
       if (rot) {
-        const double zeta = (be - al) / (2.0 * ga);
-        const double az = fabs(zeta);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (az > 1e150 ? 2.0 * az : az + sqrt(1.0 + zeta * zeta));
+        // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga), with one
+        // division: t = 2 ga sign(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2))
+        const double dd = be - al;
+        const double t = (dd >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(dd) + sqrt(dd * dd + 4.0 * ga * ga));
         const double cs = rsqrt(1.0 + t * t), sn = cs * t;
         double* va = sm.Aux + p0 * BR_C;
         double* vbp = sm.Aux + p1 * BR_C;
