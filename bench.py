@@ -259,8 +259,9 @@ def main():
     h2d = sum(x.numel() * 8 for term in host for x in term)
     out_host = torch.empty(out_doubles + 4096, dtype=torch.float64).pin_memory()
     e2e_ms, d2h = [], 0
-    # one untimed call first (the torch caching allocator sizes the slice buffers)
-    out_host, _, _, _ = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=2, out_host=out_host)
+    # untimed calls first (the torch caching allocator sizes the slice buffers)
+    for _ in range(2):
+        out_host, _, _, _ = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=2, out_host=out_host)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
