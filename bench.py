@@ -329,6 +329,26 @@ def main():
         extras["gram_pairs_per_s"] = pairs / (statistics.median(gms) * 1e-3)
         extras["gram"] = {"workload": "C3 (configs[2]) TT-dot Gram matrix, m=50, d=16, n=64, r=20",
                           "pairs": pairs, "ms": statistics.median(gms), "rel_err_vs_MtM": gerr}
+        if world > 1:  # C3 Gram sharded by pair blocks over the ranks (one NCCL all-gather)
+            from paper_2211_08770_b200 import parallel
+            blockfn = lambda blocks: P.tt_gram_blocks(ctx, A3, blocks)  # noqa: E731
+            Gs = parallel.sharded_gram(c3.m, blockfn, block=4)
+            torch.cuda.synchronize()
+            sms = []
+            for _ in range(3):
+                barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                Gs = parallel.sharded_gram(c3.m, blockfn, block=4)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                sms.append(e0.elapsed_time(e1))
+            tg = torch.tensor([statistics.median(sms)], device=dev, dtype=torch.float64)
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+            extras["gram_sharded"] = {"ranks": world, "ms": float(tg.item()), "pairs_per_s": pairs / (float(tg.item()) * 1e-3),
+                                      "rel_err_vs_MtM": float(np.linalg.norm(Gs - st3.gram_exact()) / np.linalg.norm(st3.gram_exact())),
+                                      "collective": "NCCL all_gather_into_tensor of padded pair blocks"}
         c2 = CONFIGS["C2"]
         st2 = make_shared_tail_set(c2.d, c2.n, c2.r, c2.m, c2.kappa, c2.seed + rank)
         A2 = [P.DeviceTT.from_numpy(a) for a in st2.tensors]

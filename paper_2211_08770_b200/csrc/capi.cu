@@ -215,6 +215,22 @@ tt_status tt_gram_blocks(tt_ctx ctx, int32_t m, const tt_view* a, int32_t nblk, 
   return guarded(ctx, [&] {
     std::vector<TTRef> A;
     for (int i = 0; i < m; ++i) A.push_back(TTRef::of(a[i]));
+    for (int b = 0; b < nblk; ++b) {
+      const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
+      if (i0 < 0 || j0 < 0 || bi < 0 || bj < 0 || i0 + bi > m || j0 + bj > m) fail(TT_EINDEX, "Gram block out of range");
+    }
+    bool uniform = true;
+    for (int i = 1; i < m; ++i)
+      uniform = uniform && A[(size_t)i].d == A[0].d && A[(size_t)i].n == A[0].n && A[(size_t)i].r == A[0].r;
+    const char* gt = std::getenv("TT_B200_GRAM_PAIRWISE");  // tests: force the per-pair kernel
+    if (uniform && !(gt && gt[0] == '1')) {
+      std::vector<const double*> cores;
+      for (int i = 0; i < m; ++i) cores.insert(cores.end(), A[(size_t)i].core.begin(), A[(size_t)i].core.end());
+      if (gram_tiled_supported(cores, m, A[0].d, A[0].n, A[0].r)) {
+        gram_tiled_blocks(ctx, cores, m, A[0].d, A[0].n, A[0].r, nblk, blk, packed_dev);
+        return;
+      }
+    }
     std::vector<std::pair<const TTRef*, const TTRef*>> pr;
     for (int b = 0; b < nblk; ++b) {
       const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];

@@ -20,6 +20,14 @@ namespace {
 constexpr int GT_I = 2, GT_J = 2, GT_P = GT_I * GT_J;  // pairs per tile
 constexpr int GT_MAXD = 128;
 
+// One CTA's work: pairs (i, j) with i in [i0, i0 + GT_I), j in [j0, j0 + GT_J).  mode 0: write
+// G(i, j) and G(j, i) for i >= j (symmetric m x m output); mode 1: write the pairs with
+// i < ilim, j < jlim to out[off + (i - bi0) * bj + (j - bj0)] (packed pair block).
+struct GramTile {
+  int i0, j0, ilim, jlim, bi0, bj0, bj, mode;
+  int64_t off;
+};
+
 struct GramShape {
   int d;
   int n[GT_MAXD];
@@ -30,7 +38,7 @@ __host__ __device__ inline int ceil4(int x) { return (x + 3) & ~3; }
 
 template <int GT_T>  // threads per CTA; one V micro-tile per thread
 __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __restrict__ cores, GramShape sh, int m,
-                                                          int nbj, const int* __restrict__ tiles, int RP,
+                                                          int nbj, const GramTile* __restrict__ tiles, int RP,
                                                           int S, int PS, double* __restrict__ G) {
   extern __shared__ __align__(16) double gsm[];
   // smem blocks of PS doubles (per pair / per staged tensor), rows of stride S >= RP: padded so
@@ -40,7 +48,8 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
   double* U = W + GT_P * RR;       // [p][a][c'] (row-major)
   double* XB = U + GT_P * RR;      // 2 buffers x [t][a][a'] (row-major slices X(a, s, a')), I then J
   const int tid = threadIdx.x;
-  const int i0 = tiles[2 * blockIdx.x] * GT_I, j0 = tiles[2 * blockIdx.x + 1] * GT_J;
+  const GramTile tl = tiles[blockIdx.x];
+  const int i0 = tl.i0, j0 = tl.j0;
   const int d = sh.d;
   for (int idx = tid; idx < GT_P * RR; idx += GT_T) W[idx] = (idx % RR == 0) ? 1.0 : 0.0;  // W_0 = 1 (1 x 1)
 #pragma unroll 1
@@ -146,10 +155,14 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
   }
   if (tid < GT_P) {
     const int i = i0 + tid / GT_J, j = j0 + tid % GT_J;
-    if (i < m && j < m && i >= j) {
-      const double g = W[tid * RR];
-      G[(int64_t)i * m + j] = g;
-      G[(int64_t)j * m + i] = g;
+    const double g = W[tid * RR];
+    if (tl.mode == 0) {
+      if (i < m && j < m && i >= j) {
+        G[(int64_t)i * m + j] = g;
+        G[(int64_t)j * m + i] = g;
+      }
+    } else if (i < tl.ilim && j < tl.jlim) {
+      G[tl.off + (int64_t)(i - tl.bi0) * tl.bj + (j - tl.bj0)] = g;
     }
   }
   (void)nbj;
@@ -169,8 +182,9 @@ bool gram_tiled_supported(const std::vector<const double*>& cores, int m, int d,
   return GT_P * (ceil4(rmax) / 4) * (ceil4(rmax) / 4) <= 256;
 }
 
-void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
-                const std::vector<int64_t>& r, double* G_dev) {
+static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d,
+                        const std::vector<int64_t>& n, const std::vector<int64_t>& r,
+                        const std::vector<GramTile>& tiles, double npairs, double* out) {
   GramShape sh{};
   sh.d = d;
   int rmax = 1;
@@ -184,37 +198,56 @@ void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int 
     sh.r[k] = (int)r[(size_t)k];
     rmax = std::max<int>(rmax, (int)r[(size_t)k]);
   }
+  if (tiles.empty()) return;
   const int RP = ceil4(rmax);
   // row stride / block stride chosen for the fewest shared-memory bank conflicts (offline model)
   const int S = (RP == 8 || RP == 12 || RP == 20 || RP == 24) ? RP + 2 : RP;
   const int PS = S * RP + 2;
-  const int nbi = (m + GT_I - 1) / GT_I, nbj = (m + GT_J - 1) / GT_J;
-  std::vector<int> tiles;
-  for (int bi = 0; bi < nbi; ++bi)
-    for (int bj = 0; bj < nbj; ++bj)
-      if ((bi + 1) * GT_I - 1 >= bj * GT_J) {  // the tile holds some pair with i >= j
-        tiles.push_back(bi);
-        tiles.push_back(bj);
-      }
-  const int ntiles = (int)tiles.size() / 2;
   BBuf dt, dc;
-  dt.upload(ctx, tiles.data(), tiles.size() * sizeof(int));
+  dt.upload(ctx, tiles.data(), tiles.size() * sizeof(GramTile));
   dc.upload(ctx, cores.data(), cores.size() * sizeof(double*));
   const size_t smem = sizeof(double) * (size_t)(2 * GT_P + 2 * (GT_I + GT_J)) * PS;
-  const double pairs = 0.5 * m * (m + 1.0);
-  const double bytes = 8.0 * (double)m * [&] { double e = 0; for (int k = 0; k < d; ++k) e += (double)r[(size_t)k] * n[(size_t)k] * r[(size_t)k + 1]; return e; }();
+  double bytes = 0.0;
+  for (int k = 0; k < d; ++k) bytes += 8.0 * (double)m * r[(size_t)k] * n[(size_t)k] * r[(size_t)k + 1];
   const int nv = GT_P * (RP / 4) * (RP / 4);
+  const int ntiles = (int)tiles.size();
+  const GramTile* tp = static_cast<const GramTile*>(dt.p);
   if (nv <= 128) {
     TTB_CUDA(cudaFuncSetAttribute(gram_tile_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TTB_RUN(ctx, "tt_gram_tiled", flops * pairs, bytes,
+    TTB_RUN(ctx, "tt_gram_tiled", flops * npairs, bytes,
             gram_tile_kernel<128><<<ntiles, 128, smem, ctx->stream>>>(static_cast<const double* const*>(dc.p), sh, m,
-                                                                        nbj, static_cast<const int*>(dt.p), RP, S, PS, G_dev));
+                                                                        0, tp, RP, S, PS, out));
   } else {
     TTB_CUDA(cudaFuncSetAttribute(gram_tile_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TTB_RUN(ctx, "tt_gram_tiled", flops * pairs, bytes,
+    TTB_RUN(ctx, "tt_gram_tiled", flops * npairs, bytes,
             gram_tile_kernel<256><<<ntiles, 256, smem, ctx->stream>>>(static_cast<const double* const*>(dc.p), sh, m,
-                                                                        nbj, static_cast<const int*>(dt.p), RP, S, PS, G_dev));
+                                                                        0, tp, RP, S, PS, out));
   }
+}
+
+void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
+                const std::vector<int64_t>& r, double* G_dev) {
+  std::vector<GramTile> tiles;
+  for (int i0 = 0; i0 < m; i0 += GT_I)
+    for (int j0 = 0; j0 < m; j0 += GT_J)
+      if (i0 + GT_I - 1 >= j0) tiles.push_back(GramTile{i0, j0, m, m, 0, 0, 0, 0, 0});  // holds a pair i >= j
+  gram_launch(ctx, cores, m, d, n, r, tiles, 0.5 * m * (m + 1.0), G_dev);
+}
+
+void gram_tiled_blocks(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d,
+                       const std::vector<int64_t>& n, const std::vector<int64_t>& r, int nblk, const int32_t* blk,
+                       double* packed_dev) {
+  std::vector<GramTile> tiles;
+  int64_t off = 0;
+  double npairs = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
+    for (int ti = i0; ti < i0 + bi; ti += GT_I)
+      for (int tj = j0; tj < j0 + bj; tj += GT_J) tiles.push_back(GramTile{ti, tj, i0 + bi, j0 + bj, i0, j0, bj, 1, off});
+    off += (int64_t)bi * bj;
+    npairs += (double)bi * bj;
+  }
+  gram_launch(ctx, cores, m, d, n, r, tiles, npairs, packed_dev);
 }
 
 }  // namespace ttb

@@ -13,4 +13,10 @@ bool gram_tiled_supported(const std::vector<const double*>& cores, int m, int d,
 void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
                 const std::vector<int64_t>& r, double* G_dev);
 
+// Pair blocks (i0, j0, bi, bj) (blk: 4 ints each): block b's pairs row-major at packed_dev + the
+// sizes of the previous blocks (the tt_gram_blocks layout).
+void gram_tiled_blocks(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d,
+                       const std::vector<int64_t>& n, const std::vector<int64_t>& r, int nblk, const int32_t* blk,
+                       double* packed_dev);
+
 }  // namespace ttb
