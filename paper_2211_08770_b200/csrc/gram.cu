@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
   double* W = gsm;                 // [p][c][a]  (column-major W: W[p][c * RP + a] = W(a, c))
   double* U = W + GT_P * RR;       // [p][a][c'] (row-major)
   double* XB = U + GT_P * RR;      // 2 buffers x [t][a][a'] (row-major slices X(a, s, a')), I then J
+  const double** rowsrc = reinterpret_cast<const double**>(XB + 2 * (GT_I + GT_J) * RR);  // <= 4 * 32 rows
+  int* rowdst = reinterpret_cast<int*>(rowsrc + (GT_I + GT_J) * 32);
   const int tid = threadIdx.x;
   const GramTile tl = tiles[blockIdx.x];
   const int i0 = tl.i0, j0 = tl.j0;
@@ -63,13 +65,26 @@ __global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __
     for (int e = 0; e < 16; ++e) acc[e] = 0.0;
     __syncthreads();
     // slices X(:, s, :) of the tile's tensors, staged asynchronously one slice ahead
+    // slices X(:, s, :) of the tile's tensors, staged asynchronously one slice ahead: 16-byte
+    // copies when R1 is even (rows stay 16-byte aligned), per-row source bases tabulated once
+    const bool v16 = (R1 & 1) == 0;
+    const int cpr = v16 ? R1 / 2 : R1;             // copies per slice row
+    const int nrow = (GT_I + GT_J) * R0;
+    for (int rid = tid; rid < nrow; rid += GT_T) {
+      const int t = rid / R0, a = rid - t * R0;
+      int tens = t < GT_I ? i0 + t : j0 + (t - GT_I);
+      if (tens >= m) tens = m - 1;  // padding tensor: its pairs are never written
+      rowsrc[rid] = cores[(int64_t)tens * d + k] + (int64_t)a * n * R1;
+      rowdst[rid] = t * RR + a * S;
+    }
+    __syncthreads();
     auto stage = [&](int s, double* buf) {
-      for (int idx = tid; idx < (GT_I + GT_J) * R0 * R1; idx += GT_T) {
-        const int t = idx / (R0 * R1), e = idx % (R0 * R1), a = e / R1, b = e % R1;
-        int tens = t < GT_I ? i0 + t : j0 + (t - GT_I);
-        if (tens >= m) tens = m - 1;  // padding tensor: its pairs are never written
-        __pipeline_memcpy_async(buf + t * RR + a * S + b,
-                                cores[(int64_t)tens * d + k] + ((int64_t)a * n + s) * R1 + b, sizeof(double));
+      for (int idx = tid; idx < nrow * cpr; idx += GT_T) {
+        const int rid = idx / cpr, c = idx - rid * cpr;
+        const double* src = rowsrc[rid] + (int64_t)s * R1;
+        double* dst = buf + rowdst[rid];
+        if (v16) __pipeline_memcpy_async(dst + 2 * c, src + 2 * c, 2 * sizeof(double));
+        else __pipeline_memcpy_async(dst + c, src + c, sizeof(double));
       }
       __pipeline_commit();
     };
@@ -206,7 +221,8 @@ static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int
   BBuf dt, dc;
   dt.upload(ctx, tiles.data(), tiles.size() * sizeof(GramTile));
   dc.upload(ctx, cores.data(), cores.size() * sizeof(double*));
-  const size_t smem = sizeof(double) * (size_t)(2 * GT_P + 2 * (GT_I + GT_J)) * PS;
+  const size_t smem = sizeof(double) * (size_t)(2 * GT_P + 2 * (GT_I + GT_J)) * PS +
+                      (sizeof(double*) + sizeof(int)) * (GT_I + GT_J) * 32;
   double bytes = 0.0;
   for (int k = 0; k < d; ++k) bytes += 8.0 * (double)m * r[(size_t)k] * n[(size_t)k] * r[(size_t)k + 1];
   const int nv = GT_P * (RP / 4) * (RP / 4);
