@@ -87,6 +87,7 @@ struct BRArgs {
   int* ranks;                  // [item][d+1]
   double* scal;                // [item][4]: ||x||, tau, s, zero flag
   int* info;                   // [item]: 1 = Jacobi hit its sweep limit
+  int* gemm;                   // [item]: 1 = output core of this split by U = Y V S^-1 (DMMA)
   double rel_tol, floor_c;
   int64_t max_rank;
   int keep_all;
@@ -921,7 +922,17 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   __syncthreads();
   const int rho = sm.rho;
   double* tt = A.TT + (int64_t)b * 2 * BR_C * BR_C;
-  if (tall) {  // U_rho (cp x rho), the target of Q_Y
+  // Well-separated kept singular values (sigma_rho >= 1e-3 sigma_1): U_rho = Y V_rho S_rho^-1 is
+  // accurate to u sigma_1 / sigma_rho <= 1e-13 and is a plain GEMM (DMMA) instead of applying
+  // Q_Y's reflectors; W = V_rho S_rho^-1 goes to the first target slot.
+  const bool use_gemm = tall && sm.sig[rho - 1] >= 1e-3 * sm.sig[0];
+  if (tid == 0) A.gemm[b] = use_gemm ? 1 : 0;
+  if (use_gemm) {
+    for (int idx = tid; idx < BR_C * rho; idx += BR_T) {
+      const int col = idx / BR_C, row = idx % BR_C;
+      tt[idx] = row < cp ? sm.Aux[sm.perm[col] * BR_C + row] / sm.sig[col] : 0.0;
+    }
+  } else if (tall) {  // U_rho (cp x rho), the target of Q_Y
     for (int idx = tid; idx < BR_C * rho; idx += BR_T) {
       const int col = idx / BR_C, row = idx % BR_C;
       const double sg = sm.sig[col];
@@ -938,6 +949,47 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   for (int idx = tid; idx < BR_C * rho; idx += BR_T) {  // V_rho S (cp x rho), the target of H_{k+1}
     const int col = idx / BR_C, row = idx % BR_C;
     tt[BR_C * BR_C + idx] = row < cp ? sm.Aux[sm.perm[col] * BR_C + row] * sm.sig[col] : 0.0;
+  }
+}
+
+// out (p x rho, row-major) = Y (p x cp, row-major ld cp) W (cp x rho, column-major ld 64) on the FP64
+// tensor cores (mma.sync m8n8k4): warp w takes 8-row tiles w, w+8, ...; per tile the rho columns
+// in 8-column tiles (accumulators in registers), K = cp in steps of 4.
+__device__ void br_gemm_yw(const double* __restrict__ Y, int p, int cp, const double* __restrict__ W, int rho,
+                           double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ar = lane >> 2, ak = lane & 3;  // A fragment: row ar, k ak; B fragment: k ak, col ar
+  const int nct = (rho + 7) / 8;            // <= 8 column tiles
+#pragma unroll 1
+  for (int rt = warp; rt * 8 < p; rt += BR_W) {
+    const int row = rt * 8 + ar;
+    double acc[8][2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll 1
+    for (int k0 = 0; k0 < cp; k0 += 4) {
+      const int kk = k0 + ak;
+      const double a = (row < p && kk < cp) ? __ldg(Y + (int64_t)row * cp + kk) : 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < nct) {
+          const int col = c * 8 + ar;
+          const double bv = (col < rho && kk < cp) ? __ldg(W + col * BR_C + kk) : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[c][0]), "+d"(acc[c][1])
+                       : "d"(a), "d"(bv));
+        }
+      }
+    }
+    // D fragment: row ar, columns 2 ak, 2 ak + 1 of each 8-column tile
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < nct && row < p) {
+        const int col = c * 8 + 2 * ak;
+        if (col < rho) out[(int64_t)row * rho + col] = acc[c][0];
+        if (col + 1 < rho) out[(int64_t)row * rho + col + 1] = acc[c][1];
+      }
+    }
   }
 }
 
@@ -970,7 +1022,9 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_apply_kernel(BRArgs A, int k) 
   const int rho = rk[k];
   const double* tt = A.TT + (int64_t)b * 2 * BR_C * BR_C;
   const long long co0 = clock64();
-  if (tall) {
+  if (tall && A.gemm[b]) {
+    br_gemm_yw(A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride, (int)p, cp, tt, rho, out + S->ooff[kc]);
+  } else if (tall) {
     const double* YV = A.YV + (int64_t)b * S->ystride;
     const double* YT = A.YT + (int64_t)b * S->ytstride;
     br_apply_targets(tt, rho, cp, YV, YT, p, cp, out + S->ooff[kc], rho, 1, sm.vst);
@@ -1137,7 +1191,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   const int nb_max = std::min(W, B);
   const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 5 * BR_C * BR_C + sh.ystride +
                                               sh.ytstride + 2 * sh.zstride + std::max<int64_t>(sh.ostride, 1) + 4) +
-                            (size_t)nb_max * (d + 2) + 64;
+                            (size_t)nb_max * (d + 3) + 64;
   double* ws = static_cast<double*>(ctx_scratch(ctx, ws_doubles * sizeof(double)));
   // kernels that do not stage reflector slices leave out the VStage buffers
   const size_t smem = offsetof(BRSmem, vst), smem_q = offsetof(BRSmem, vst), smem_a = sizeof(BRSmemA);
@@ -1160,7 +1214,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       const int nb = std::min(W, B - w0);
       stamp("wave start");
       struct { double* p; } V, T, L, YV, YT, Z, O, SC, JM, TT;
-      struct { int* p; } RK, INF;
+      struct { int* p; } RK, INF, GM;
       {
         double* w = ws;  // carve the scratch (every piece a multiple of 2 doubles: 16-B aligned)
         auto take = [&](size_t n) { double* r = w; w += (n + 1) & ~(size_t)1; return r; };
@@ -1176,6 +1230,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         SC.p = take((size_t)nb * 4);
         RK.p = reinterpret_cast<int*>(take(((size_t)nb * (d + 1) + 1) / 2));
         INF.p = reinterpret_cast<int*>(take(((size_t)nb + 1) / 2));
+        GM.p = reinterpret_cast<int*>(take(((size_t)nb + 1) / 2));
       }
       TTB_CUDA(cudaMemsetAsync(INF.p, 0, sizeof(int) * nb, ctx->stream));
       BRArgs a;
@@ -1184,7 +1239,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       a.coef = static_cast<const double*>(dcoef.p);
       a.scale = static_cast<const double*>(dscale.p);
       a.V = V.p; a.T = T.p; a.L = L.p; a.YV = YV.p; a.YT = YT.p; a.Z = Z.p; a.out = O.p; a.JM = JM.p; a.TT = TT.p;
-      a.ranks = RK.p; a.scal = SC.p; a.info = INF.p;
+      a.ranks = RK.p; a.scal = SC.p; a.info = INF.p; a.gemm = GM.p;
       a.rel_tol = o.rel_tol;
       a.floor_c = o.floor_c;
       a.max_rank = o.max_rank;
@@ -1230,6 +1285,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         if (hinf[(size_t)b]) fail(TT_ENOCONV, "Jacobi SVD did not converge (batch item " + std::to_string(w0 + b) + ")");
       std::vector<double> hsc((size_t)nb * 4);
       d2h_small(ctx, hsc.data(), SC.p, hsc.size());
+      std::vector<int> hgm((size_t)nb);
+      d2h_small_int(ctx, hgm.data(), GM.p, hgm.size());
       std::vector<int64_t> dst((size_t)nb * d), sz((size_t)nb * d);
       int64_t tot = 0;
       double l2r_svd_fl = 0.0, l2r_qr_fl = 0.0, l2r_ap_fl = 0.0;
@@ -1250,7 +1307,11 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
           const double qrf = (pp > BR_C) ? 2.0 * a1 * b1 * b1 - 2.0 * b1 * b1 * b1 / 3.0 : 0.0;
           l2r_qr_fl += qrf;
           l2r_svd_fl += 6.0 * a1 * b1 * b1 + 11.0 * b1 * b1 * b1 - qrf;
-          if (pp > BR_C) l2r_ap_fl += 4.0 * pp * cp * rho - 2.0 * cp * cp * rho;
+          // output core: Householder application (ormqr count) or the GEMM Y W (2 p c' rho); the
+          // flag of the last split is what the host holds -- the choice is per (item, split), so
+          // count the application for every split whose flag is unknown (an upper bound)
+          if (pp > BR_C) l2r_ap_fl += (k == d - 1 && hgm[(size_t)b]) ? 2.0 * pp * cp * rho
+                                                                     : 4.0 * pp * cp * rho - 2.0 * cp * cp * rho;
           l2r_ap_fl += 4.0 * m1 * std::min(m1, c1) * rho - 2.0 * std::min(m1, c1) * std::min(m1, c1) * rho;
         }
       }
