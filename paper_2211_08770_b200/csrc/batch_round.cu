@@ -1320,8 +1320,16 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       prof_credit(ctx, "batch_l2r_apply", l2r_ap_fl);
       void* arena = nullptr;
       if (cudaMallocAsync(&arena, (size_t)std::max<int64_t>(tot, 1) * sizeof(double), ctx->stream) != cudaSuccess) {
+        // the stream-ordered pool keeps freed blocks cached: give them back and retry once
         (void)cudaGetLastError();
-        fail(TT_ENOMEM, "batch result arena allocation failed");
+        cudaMemPool_t pool;
+        TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+        TTB_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+        TTB_CUDA(cudaMemPoolTrimTo(pool, 0));
+        if (cudaMallocAsync(&arena, (size_t)std::max<int64_t>(tot, 1) * sizeof(double), ctx->stream) != cudaSuccess) {
+          (void)cudaGetLastError();
+          fail(TT_ENOMEM, "batch result arena allocation failed");
+        }
       }
       res.arenas.push_back(arena);
       res.arena_size.push_back(tot);

@@ -12,8 +12,8 @@ dc = [[x.cuda() for x in term] for term in host]
 res = P.tt_round_batch_strided(ctx, dc, coeffs, 1e-6, norms=norms); n = res.total_doubles(); del res
 out = torch.empty(n + 4096, dtype=torch.float64).pin_memory()
 torch.cuda.synchronize()
-for chunks in (1, 2, 4):
-    for rep in range(2):
+for chunks in (1, 2, 4, 8):
+    for rep in range(3):
         torch.cuda.synchronize(); t0 = time.perf_counter()
         out, rk, nr, cnt = P.tt_round_batch_host(ctx, host, coeffs, 1e-6, norms=norms, chunks=chunks, out_host=out)
         torch.cuda.synchronize(); t1 = time.perf_counter()
