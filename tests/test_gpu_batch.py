@@ -211,3 +211,37 @@ def test_batch_host_pipeline_matches_device_call():
     assert cnt == flat.size
     assert np.array_equal(out[:cnt].numpy(), flat)
     np.testing.assert_array_equal(norms, res.norms)
+
+
+def test_batch_strided_unsupported_shape_and_serial_fallback():
+    """Formal rank > 64 is outside the batched engine: tt_round_batch_strided reports
+    TT_ENOTSUP, tt_round_batch falls back to the per-item rounding (still oracle-exact)."""
+    import paper_2211_08770_b200 as P
+    from paper_2211_08770_b200._native import TTError
+    rng = _rng(404)
+    d, n = 3, [5, 6, 4]
+    ranks = [[1, 20, 20, 1], [1, 25, 25, 1], [1, 22, 22, 1]]  # formal interior rank 67
+    items = []
+    for _ in range(2):
+        terms = [make_random_tt(d, n, r, rng) for r in ranks]
+        items.append((terms, [1.0, -0.5, 0.25]))
+    cores, coeffs = _stack(items)
+    with pytest.raises(TTError) as e:
+        P.tt_round_batch_strided(ctx(), cores, coeffs, 1e-8)
+    assert e.value.name == "TT_ENOTSUP"
+    outs = P.tt_round_batch(ctx(), [([dev(t) for t in ts], cs) for ts, cs in items], 1e-8)
+    for (terms, cf), o in zip(items, outs):
+        _check_item(o.to_numpy(), o.ranks, terms, cf, 1e-8, rounding.DEFAULT_FLOOR_C)
+
+
+def test_batch_exactly_rank_64_and_single_item():
+    """Formal ranks exactly 64 (the engine's limit), one item, one mode size of 1."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(405)
+    d, n = 4, [7, 1, 30, 9]
+    ranks = [[1, 7, 1, 9, 1], [1, 40, 1, 30, 1], [1, 17, 1, 25, 1]]  # R_1 = 64, R_3 = 64
+    terms = [make_random_tt(d, n, r, rng) for r in ranks]
+    items = [(terms, [1.0, 2.0, -1.0])]
+    cores, coeffs = _stack(items)
+    res = P.tt_round_batch_strided(ctx(), cores, coeffs, 1e-10)
+    _check_item(res.item_numpy(0), list(res.ranks[0]), terms, [1.0, 2.0, -1.0], 1e-10, rounding.DEFAULT_FLOOR_C)
