@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--terms", type=int, default=30)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--n", type=int, default=32)
+    ap.add_argument("--d", type=int, default=8)
+    ap.add_argument("--r", type=int, default=10)
+    ap.add_argument("--delta", type=float, default=1e-10)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -28,17 +31,17 @@ def main():
     _build.build_library()
     import paper_2211_08770_b200 as P
     from ttinputs import make_shared_tail_set
-    st = make_shared_tail_set(8, args.n, 10, args.terms, 1e4, seed=5)
+    st = make_shared_tail_set(args.d, args.n, args.r, args.terms, 1e4, seed=5)
     rng = np.random.Generator(np.random.PCG64(1))
     coeffs = [1.0] + list(rng.standard_normal(args.terms - 1) * 0.3)
     ctx = P.Context(0)
     terms = [P.DeviceTT.from_numpy(a, norm=1.0) for a in st.tensors]
-    out, info = P.tt_round(ctx, terms, coeffs, 1e-10)  # warm-up
+    out, info = P.tt_round(ctx, terms, coeffs, args.delta)  # warm-up
     torch.cuda.synchronize()
     ctx.profile(True)
     t0 = time.perf_counter()
     for _ in range(args.reps):
-        out, info = P.tt_round(ctx, terms, coeffs, 1e-10)
+        out, info = P.tt_round(ctx, terms, coeffs, args.delta)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / args.reps
     rep = ctx.profile_report()

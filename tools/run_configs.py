@@ -1,0 +1,91 @@
+#!/usr/bin/env python
+"""Every BASELINE.json configuration through the GPU path, with the closed-form checks the
+shared-tail construction gives: R = R_M (Householder up to signs),
+Gram = M^T M, the Table 1 rounding counts, ||q_i|| = 1, the per-step loss of orthogonality; C4
+against its closed form (ranks 32 / 16, distance to y1 + [b even] y2).  One JSON line per run.
+
+  python tools/run_configs.py [--c5-m 100] [--only C1,C2,...]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c5-m", type=int, default=100)
+    ap.add_argument("--only", default="C1,C2,C3,C4,C5")
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    import paper_2211_08770_b200 as P
+    from ttinputs import CONFIGS, make_batch_sums_stacked, make_shared_tail_set
+    ctx = P.Context(0)
+    only = set(args.only.split(","))
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return out, e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)
+
+    expected_calls = {"cgs": lambda m: m, "mgs": lambda m: m, "cgs2": lambda m: 2 * m, "mgs2": lambda m: 2 * m,
+                      "gram": lambda m: m, "householder": lambda m: 4 * m - 1}
+    for name in ["C1", "C2", "C3", "C5"]:
+        if name not in only:
+            continue
+        c = CONFIGS[name]
+        m = args.c5_m if name == "C5" else c.m
+        st = make_shared_tail_set(c.d, c.n, c.r, m, c.kappa, c.seed)
+        A = [P.DeviceTT.from_numpy(a) for a in st.tensors]
+        qm, rm = st.qr_exact()
+        for kind in c.drivers:
+            P.tt_orth(ctx, kind, A[:2], c.delta)  # warm-up (kernels loaded, pool sized)
+            ctx.profile(True)
+            (Q, R, rep), ms, wall = timed(lambda: P.tt_orth(ctx, kind, A, c.delta, want_loo=True))
+            prof = ctx.profile_report()
+            ctx.profile(False)
+            sg = np.sign(np.diag(R))
+            sg[sg == 0] = 1.0
+            Rn = sg[:, None] * R if kind == "householder" else R
+            rel_r = float(np.linalg.norm(Rn - rm) / np.linalg.norm(rm))
+            norms = [float(np.sqrt(abs(P.tt_dot_batch(ctx, [q], [q]).cpu().item()))) for q in Q]
+            top = sorted(prof.items(), key=lambda kv: -kv[1]["ms"])[:4]
+            line = {"config": name, "driver": kind, "m": m, "d": c.d, "n": c.n, "r": c.r, "kappa": c.kappa,
+                    "delta": c.delta, "rounding_calls": rep["rounding_calls"],
+                    "calls_ok": rep["rounding_calls"] == expected_calls[kind](m),
+                    "gpu_ms": ms, "wall_ms": wall, "roundings_per_s": rep["rounding_calls"] / (wall * 1e-3),
+                    "max_rank": max(rep["max_rank_per_call"]), "R_rel_err_vs_R_M": rel_r,
+                    "q_norm_max_dev": max(abs(x - 1.0) for x in norms),
+                    "loo_last": float(rep["loo_per_step"][-1]), "loo_max": float(np.max(rep["loo_per_step"])),
+                    "kernel_top": {k: {"ms": round(v["ms"], 2), "launches": v["launches"]} for k, v in top}}
+            print(json.dumps(line), flush=True)
+        if name == "C3":
+            G, ms, wall = timed(lambda: P.tt_gram(ctx, A))
+            Gx = st.gram_exact()
+            print(json.dumps({"config": name, "op": "tt_gram", "m": m, "pairs": m * (m + 1) // 2, "gpu_ms": ms,
+                              "rel_err_vs_MtM": float(np.linalg.norm(G.cpu().numpy() - Gx) / np.linalg.norm(Gx))}),
+                  flush=True)
+    if "C4" in only:
+        B = 4096
+        cores, coeffs = make_batch_sums_stacked(B)
+        dc = [[torch.from_numpy(x).cuda() for x in term] for term in cores]
+        P.tt_round_batch_strided(ctx, dc, coeffs, 1e-6, norms=np.ones((B, 4)))
+        res, ms, wall = timed(lambda: P.tt_round_batch_strided(ctx, dc, coeffs, 1e-6, norms=np.ones((B, 4))))
+        want = np.where(np.arange(B) % 2 == 0, 32, 16)
+        print(json.dumps({"config": "C4", "op": "tt_round_batch_strided", "batch": B, "gpu_ms": ms, "wall_ms": wall,
+                          "roundings_per_s": B / (wall * 1e-3),
+                          "ranks_closed_form_ok": bool(np.all(res.ranks[:, 1:-1] == want[:, None]))}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
