@@ -600,6 +600,15 @@ void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, i
     if (st.cluster == 1) fail(TT_ENOTSUP, "QRCP: cluster path lost mid-factorisation");
     st.cluster = 0;
   }
+  // large panels (beyond one cluster): the grid-cooperative QRCP over every SM
+  if (st.m * st.c >= (int64_t)1 << 17 &&
+      qrcp_grid_run(ctx, Y, ldy, st.m, st.c, st.k, stop2, kcap, st.tau.p, st.norms.p, st.perm.p, st.scalars.p)) {
+    double h[2];
+    d2h_small(ctx, h, st.scalars.p, 2);
+    st.k = (int)h[0];
+    st.e2 = h[1];
+    return;
+  }
   const size_t smem = (size_t)st.c * (2 * sizeof(double) + sizeof(int)) + 16;
   if (smem > 200 * 1024) fail(TT_ENOTSUP, "QRCP: too many columns for the shared-memory norm cache");
   if (smem > 48 * 1024)  // idempotent and thread-safe (several contexts may run concurrently)

@@ -61,6 +61,11 @@ void unpermute_cols(tt_ctx ctx, const double* in, int64_t ldi, int64_t rows, int
 // One launch of the cluster-resident QRCP (qrcp_cluster.cu); false if the matrix does not fit.
 bool qrcp_cluster_run(tt_ctx ctx, double* Y, int64_t ldy, int64_t m, int64_t c, int k_start, double stop2, int kcap,
                       double* tau, int* perm2c, double* scalars);
+// Grid-cooperative QRCP (qrcp_grid.cu) for matrices beyond one cluster; same layout and stopping
+// test as the single-CTA kernel; norms (2c) and perm live in global memory.  False if the
+// cooperative launch is not possible.
+bool qrcp_grid_run(tt_ctx ctx, double* Y, int64_t ldy, int64_t m, int64_t c, int k_start, double stop2, int kcap,
+                   double* tau, double* norms, int* perm, double* scalars);
 void qrcp_init(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, int64_t m, int64_t c);
 void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, int kcap);
 // target (m x nc) <- H_0 H_1 ... H_{k-1} target, reflectors of a QRCP (unblocked).

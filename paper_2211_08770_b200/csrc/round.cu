@@ -171,7 +171,7 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw, const RRBound* rrb
     int64_t kq = std::min(m, c);
     DBuf Rk;
     bool done = false;
-    if (rank_revealing && qrcp_cluster_fits(m, c)) {
+    if (rank_revealing) {  // cluster-resident QRCP when it fits, the single-CTA QRCP otherwise
       QRCPState st;
       qrcp_init(ctx, st, A.p, m, m, c);
       const double lk = rrb->left[(size_t)k - 1];
