@@ -458,6 +458,33 @@ __global__ void __launch_bounds__(1024) apply_reflectors_kernel(const double* __
   }
 }
 
+// One CTA per target column (columns are independent): the column lives in shared memory while
+// the k reflectors are applied last to first, each dot product one block reduction.
+__global__ void __launch_bounds__(256) apply_reflectors_col_kernel(const double* __restrict__ Y, int64_t ldy,
+                                                                   const double* __restrict__ tau, int m, int k,
+                                                                   double* X, int64_t ldx) {
+  extern __shared__ double xs[];
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  double* col = X + (int64_t)blockIdx.x * ldx;
+  for (int i = tid; i < m; i += 256) xs[i] = col[i];
+  __syncthreads();
+  for (int j = k - 1; j >= 0; --j) {
+    const double t = __ldg(tau + j);
+    if (t == 0.0) continue;  // uniform
+    const double* v = Y + (int64_t)j * ldy;
+    double q0 = 0.0, q1 = 0.0;
+    int i = j + 1 + tid;
+    for (; i + 256 < m; i += 512) { q0 += __ldg(v + i) * xs[i]; q1 += __ldg(v + i + 256) * xs[i + 256]; }
+    if (i < m) q0 += __ldg(v + i) * xs[i];
+    const double q = t * (block_sum(q0 + q1, red) + xs[j]);
+    for (int r = j + 1 + tid; r < m; r += 256) xs[r] -= q * __ldg(v + r);
+    if (tid == 0) xs[j] -= q;
+    __syncthreads();
+  }
+  for (int r = tid; r < m; r += 256) col[r] = xs[r];
+}
+
 }  // namespace
 
 void copy_upper(tt_ctx ctx, const double* A, int64_t lda, int64_t rows, int64_t cols, double* R, int64_t ldr) {
@@ -625,6 +652,15 @@ void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, i
 void apply_reflectors_left(tt_ctx ctx, const double* Y, int64_t ldy, const double* tau, int64_t m, int k,
                            double* target, int64_t ldt, int64_t nc) {
   if (k <= 0 || nc <= 0) return;
+  const size_t smem = sizeof(double) * (size_t)m;
+  if (smem <= 200 * 1024) {  // one CTA per target column, the column in shared memory
+    if (smem > 48 * 1024)
+      TTB_CUDA(cudaFuncSetAttribute(apply_reflectors_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(200 * 1024)));
+    TTB_RUN(ctx, "apply_reflectors", 4.0 * m * k * nc, 8.0 * (m * k + 2.0 * m * nc),
+            apply_reflectors_col_kernel<<<(unsigned)nc, 256, smem, ctx->stream>>>(Y, ldy, tau, (int)m, k, target, ldt));
+    return;
+  }
   TTB_RUN(ctx, "apply_reflectors", 4.0 * m * k * nc, 8.0 * (m * k + 2.0 * m * nc),
           apply_reflectors_kernel<<<1, 1024, 0, ctx->stream>>>(Y, ldy, tau, (int)m, k, target, ldt, (int)nc));
 }

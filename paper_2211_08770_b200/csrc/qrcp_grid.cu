@@ -59,23 +59,39 @@ __device__ void qg_publish(double mass, double bv, int bp, QGCand* cand, QGCand*
   __syncthreads();
 }
 
-// Every CTA: total mass and global pivot from the G candidates (fixed order: deterministic).
-__device__ void qg_decide(const QGCand* cand, double& tot, int& gp) {
-  tot = 0.0;
-  double gv = -1.0;
-  gp = 0x7fffffff;
-  for (int q = 0; q < (int)gridDim.x; ++q) {
-    const QGCand cd = cand[q];
-    tot += cd.mass;
-    if (qg_better(cd.val, cd.pos, gv, gp)) { gv = cd.val; gp = cd.pos; }
+// Every CTA: total mass and global pivot from the G candidates.  Warp 0 reads them in parallel
+// (lane q: candidates q, q + 32, ...) and reduces in a fixed order (deterministic; identical in
+// every CTA); the result is broadcast through shared memory.
+__device__ void qg_decide(const QGCand* cand, double& tot, int& gp, QGCand* wbuf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    double ms = 0.0, v = -1.0;
+    int p = 0x7fffffff;
+    for (int q = lane; q < (int)gridDim.x; q += 32) {
+      const QGCand cd = cand[q];
+      ms += cd.mass;
+      if (qg_better(cd.val, cd.pos, v, p)) { v = cd.val; p = cd.pos; }
+    }
+    ms = warp_sum(ms);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int op = __shfl_xor_sync(0xffffffffu, p, o);
+      if (qg_better(ov, op, v, p)) { v = ov; p = op; }
+    }
+    if (lane == 0) wbuf[QG_W] = QGCand{ms, v, p, 0};
   }
+  __syncthreads();
+  tot = wbuf[QG_W].mass;
+  gp = wbuf[QG_W].pos;
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(double* Y, int64_t ldy, int m, int c, int k_start, double stop2,
                                                          int kcap, double* tau, double* norms, int* perm,
                                                          double* scalars, QGCand* cand) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ QGCand wbuf[QG_W];
+  __shared__ QGCand wbuf[QG_W + 1];
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gw = blockIdx.x * QG_W + warp, nwg = gridDim.x * QG_W;
@@ -105,12 +121,12 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(double* Y, int64_t ldy,
   for (; s < kmax; ++s) {
     double tot;
     int gp;
-    qg_decide(cand, tot, gp);
+    qg_decide(cand, tot, gp, wbuf);
     if (tot <= 4.0 * stop2 && s > k_start) {  // near the threshold: exact norms before deciding
       grid.sync();                              // every CTA has read the candidates
       recompute(s);
       grid.sync();
-      qg_decide(cand, tot, gp);
+      qg_decide(cand, tot, gp, wbuf);
     }
     if (tot <= stop2 || gp >= c) break;
     // CTA 0: pivot column into position s, reflector of column s (rows s..m-1)
@@ -152,11 +168,25 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(double* Y, int64_t ldy,
     for (int j = s + 1 + gw; j < c; j += nwg) {
       double* col = Y + (int64_t)j * ldy;
       if (t != 0.0) {
-        double q = 0.0;
-        for (int i = s + 1 + lane; i < m; i += 32) q += v[i] * col[i];
-        q = warp_sum(q);
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;  // four independent chains in flight
+        int i = s + 1 + lane;
+        for (; i + 96 < m; i += 128) {
+          q0 += v[i] * col[i];
+          q1 += v[i + 32] * col[i + 32];
+          q2 += v[i + 64] * col[i + 64];
+          q3 += v[i + 96] * col[i + 96];
+        }
+        for (; i < m; i += 32) q0 += v[i] * col[i];
+        double q = warp_sum((q0 + q1) + (q2 + q3));
         q = t * (q + col[s]);
-        for (int i = s + 1 + lane; i < m; i += 32) col[i] -= q * v[i];
+        for (i = s + 1 + lane; i + 96 < m; i += 128) {
+          const double a0 = col[i], a1 = col[i + 32], a2 = col[i + 64], a3 = col[i + 96];
+          col[i] = a0 - q * v[i];
+          col[i + 32] = a1 - q * v[i + 32];
+          col[i + 64] = a2 - q * v[i + 64];
+          col[i + 96] = a3 - q * v[i + 96];
+        }
+        for (; i < m; i += 32) col[i] -= q * v[i];
         __syncwarp();
         if (lane == 0) col[s] -= q;
         __syncwarp();

@@ -8,6 +8,8 @@
 //   left-to-right (k = 1..d-1): truncated SVD of the unfolding, core k <- U_rho,
 //     core k+1 <- (S V^T) x_1 core k+1 (DMMA GEMM).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 
@@ -164,6 +166,11 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw, const RRBound* rrb
       tc.push_back({in.core[(size_t)l][(size_t)d - 1], in.r[(size_t)l][(size_t)d - 1], 1, off[(size_t)d - 1][(size_t)l], 0, in.coef[(size_t)l]});
     gather_last(ctx, tc, in.n[(size_t)d - 1], A.p, m);
   }
+  // The rank-revealing QRCP pays off when the sum's numerical rank is below its structural
+  // rank; once a panel keeps every column (e.g. sums of independently rounded vectors, whose
+  // perturbations sit far above the 16 u s(x) cut), the rest of the sweep uses the blocked
+  // Householder QR, which is cheaper per column than the pivoted one.
+  bool rr_on = rank_revealing;
   for (int k = d; k >= 2; --k) {
     const int64_t nk = in.n[(size_t)k - 1];
     m = nk * sw.Rp[(size_t)k];
@@ -171,13 +178,17 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw, const RRBound* rrb
     int64_t kq = std::min(m, c);
     DBuf Rk;
     bool done = false;
-    if (rank_revealing) {  // cluster-resident QRCP when it fits, the single-CTA QRCP otherwise
+    if (rr_on) {  // cluster-resident QRCP when it fits, the grid / single-CTA QRCP otherwise
       QRCPState st;
       qrcp_init(ctx, st, A.p, m, m, c);
       const double lk = rrb->left[(size_t)k - 1];
       const double stop = lk > 0.0 ? RR_EPS * rrb->s / lk : 0.0;
       qrcp_run(ctx, st, A.p, m, stop * stop, (int)kq);
       if (st.k == 0) qrcp_run(ctx, st, A.p, m, -1.0, 1);  // keep rank >= 1
+      if (std::getenv("TT_B200_RR_DEBUG"))
+        std::fprintf(stderr, "[rr] core %d panel %lld x %lld kept %d of %lld%s\n", k, (long long)m, (long long)c, st.k,
+                     (long long)kq, qrcp_cluster_fits(m, c) ? " (cluster)" : "");
+      if (st.k >= kq && !qrcp_cluster_fits(m, c)) rr_on = false;  // no rank drop: full QR from here
       kq = st.k;
       // L_k^T = R_1 P^T (kq x c): R_1 in pivoted order, columns put back in original order
       DBuf R1(ctx, (size_t)kq * c);

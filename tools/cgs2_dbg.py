@@ -1,0 +1,10 @@
+import sys, os
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
+import paper_2211_08770_b200 as P
+from ttinputs import CONFIGS, make_shared_tail_set
+c = CONFIGS["C3"]
+st = make_shared_tail_set(c.d, c.n, c.r, int(os.environ.get("CGS2_M", "8")), c.kappa, c.seed)
+ctx = P.Context(0)
+A = [P.DeviceTT.from_numpy(a) for a in st.tensors]
+Q, R, rep = P.tt_orth(ctx, "cgs2", A, c.delta)
+print(rep["max_rank_per_call"])
