@@ -179,26 +179,61 @@ void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw, const RRBound* rrb
     DBuf Rk;
     bool done = false;
     if (rr_on) {  // cluster-resident QRCP when it fits, the grid / single-CTA QRCP otherwise
+      // Tall panels beyond L2 (m >= 2c, > 64 MB): blocked Householder QR first (DMMA, one pass
+      // over A), then the pivoted QR of its c x c triangle R, which stays in L2.  A P = Q (R P)
+      // = Q Q' R', so the pivots, the trailing masses and hence the stopping test are those of
+      // the QRCP of A itself (Frobenius norms are invariant under Q); the column-by-column pivoted
+      // sweep never streams the m x c panel.  Q_k = Q diag(Q', I).
+      static const char* pre_env = std::getenv("TT_B200_RR_PRE");
+      const bool dbg = std::getenv("TT_B200_RR_DEBUG") != nullptr;
+      // (only past L2: an L2-resident panel is cheaper to pivot directly, measured in DESIGN.md)
+      bool pre = !qrcp_cluster_fits(m, c) && m >= 2 * c && (double)m * c * sizeof(double) > 64e6;
+      if (pre_env && pre_env[0] == '0') pre = false;
+      if (pre_env && pre_env[0] == '1') pre = !qrcp_cluster_fits(m, c) && m >= 2 * c;
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+      if (dbg) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, ctx->stream);
+      }
+      DBuf Rsq;
+      double* Y = A.p;
+      int64_t my = m;
+      if (pre) {
+        geqrf(ctx, A.p, m, m, c, sw.F[(size_t)k - 1]);
+        Rsq.alloc(ctx, (size_t)c * c);
+        copy_upper(ctx, A.p, m, c, c, Rsq.p, c);
+        Y = Rsq.p;
+        my = c;
+      }
       QRCPState st;
-      qrcp_init(ctx, st, A.p, m, m, c);
+      qrcp_init(ctx, st, Y, my, my, c);
       const double lk = rrb->left[(size_t)k - 1];
       const double stop = lk > 0.0 ? RR_EPS * rrb->s / lk : 0.0;
-      qrcp_run(ctx, st, A.p, m, stop * stop, (int)kq);
-      if (st.k == 0) qrcp_run(ctx, st, A.p, m, -1.0, 1);  // keep rank >= 1
-      if (std::getenv("TT_B200_RR_DEBUG"))
-        std::fprintf(stderr, "[rr] core %d panel %lld x %lld kept %d of %lld%s\n", k, (long long)m, (long long)c, st.k,
-                     (long long)kq, qrcp_cluster_fits(m, c) ? " (cluster)" : "");
+      qrcp_run(ctx, st, Y, my, stop * stop, (int)kq);
+      if (st.k == 0) qrcp_run(ctx, st, Y, my, -1.0, 1);  // keep rank >= 1
+      if (dbg) {
+        float ms = 0.f;
+        cudaEventRecord(ev1, ctx->stream);
+        cudaEventSynchronize(ev1);
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        std::fprintf(stderr, "[rr] core %d panel %lld x %lld kept %d of %lld %.3f ms%s\n", k, (long long)m, (long long)c,
+                     st.k, (long long)kq, ms, pre ? " (qr+qrcp)" : qrcp_cluster_fits(m, c) ? " (cluster)" : "");
+      }
       if (st.k >= kq && !qrcp_cluster_fits(m, c)) rr_on = false;  // no rank drop: full QR from here
       kq = st.k;
       // L_k^T = R_1 P^T (kq x c): R_1 in pivoted order, columns put back in original order
       DBuf R1(ctx, (size_t)kq * c);
-      copy_upper(ctx, A.p, m, kq, c, R1.p, kq);
+      copy_upper(ctx, Y, my, kq, c, R1.p, kq);
       Rk.alloc(ctx, (size_t)kq * c);
       unpermute_cols(ctx, R1.p, kq, kq, c, st.perm.p, Rk.p, kq);
-      sw.rr[(size_t)k - 1] = 1;
-      sw.Pm[(size_t)k - 1] = m;
+      sw.rr[(size_t)k - 1] = pre ? 2 : 1;
+      sw.Pm[(size_t)k - 1] = my;
       sw.Ptau[(size_t)k - 1] = std::move(st.tau);
-      sw.P[(size_t)k - 1] = std::move(A);  // keeps the reflectors (columns 0..kq-1)
+      sw.P[(size_t)k - 1] = pre ? std::move(Rsq) : std::move(A);  // keeps the reflectors (columns 0..kq-1)
+      if (pre) A = DBuf();
       done = true;
     }
     if (!done) {
@@ -374,7 +409,14 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
     TTB_CUDA(cudaMemsetAsync(Zn.p, 0, sizeof(double) * (size_t)N * tr.rho, ctx->stream));
     TTB_CUDA(cudaMemcpy2DAsync(Zn.p, sizeof(double) * N, SV.p, sizeof(double) * c, sizeof(double) * c, (size_t)tr.rho,
                                cudaMemcpyDeviceToDevice, ctx->stream));
-    if (sw.rr[(size_t)k]) {
+    if (sw.rr[(size_t)k] == 2) {  // Q_k = Q diag(Q', I): Q' on the top c rows, then the blocked Q
+      apply_reflectors_left(ctx, sw.P[(size_t)k].p, sw.Pm[(size_t)k], sw.Ptau[(size_t)k].p, sw.Pm[(size_t)k], (int)c,
+                            Zn.p, N, tr.rho);
+      sw.P[(size_t)k].release();
+      sw.Ptau[(size_t)k].release();
+      ormqr_left(ctx, sw.F[(size_t)k], Zn.p, N, tr.rho);
+      sw.F[(size_t)k] = QRFactors();
+    } else if (sw.rr[(size_t)k]) {
       apply_reflectors_left(ctx, sw.P[(size_t)k].p, sw.Pm[(size_t)k], sw.Ptau[(size_t)k].p, N, (int)c, Zn.p, N,
                             tr.rho);
       sw.P[(size_t)k].release();

@@ -114,3 +114,50 @@ def test_round_theta_small_equals_exact_decision():
     o2, _ = P.tt_round(ctx(), [dev(t) for t in terms], coeffs, 1e-3, theta=1e-6)
     assert o1.ranks == o2.ranks
     assert diff_norm(o1.to_numpy(), o2.to_numpy()) <= 1e-12 * max(tt.tt_norm(t) for t in terms) * len(terms)
+
+
+@pytest.mark.parametrize("distinct", [5, 30])
+def test_round_tall_panels_qr_then_qrcp(distinct):
+    """Right-to-left panels taller than 2c and beyond one cluster (4096 x 480, 5120 x 480) take
+    the blocked-QR-then-pivoted-QR-of-R path; with 5 distinct tensors repeated (structural rank
+    480, numerical rank 80) the pivoted QR drops rank, with 30 distinct ones it keeps it."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(60 + distinct)
+    d, n, r = 4, 64, 16
+    base = [make_random_tt(d, [n] * d, [1, r, r, r, 1], rng) for _ in range(distinct)]
+    terms = [base[i % distinct] for i in range(30)]
+    coeffs = [float(v) for v in rng.standard_normal(30)]
+    norms = [tt.tt_norm(t) for t in terms]
+    ref, info = rounding.tt_round_sum(terms, coeffs, 1e-8, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
+    out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-8)
+    assert abs(ginfo["norm"] - info.norm) <= 1e-13 * info.scale
+    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
+    if distinct == 5:
+        assert out.ranks == [1, 64, 80, 64, 1]
+    g = out.to_numpy()
+    if out.ranks == info.ranks:
+        assert diff_norm(g, ref) <= 1e-10 * info.scale
+    x = tt.tt_sum(terms, coeffs)
+    assert diff_norm(x, g) <= 1e-8 * info.norm * (1 + 1e-8) + np.sqrt(d - 1) * info.tau
+
+
+def test_round_wide_panel_grid_qrcp():
+    """A 1024 x 1000 right-to-left panel (beyond one cluster, not tall) goes through the
+    grid-cooperative pivoted QR; 10 distinct tensors repeated 5 times, the left part has rank
+    <= n_1 = 32, so the pivoted QR drops 1000 columns to 32."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(70)
+    d, n, r = 3, 32, 20
+    base = [make_random_tt(d, [n] * d, [1, r, r, 1], rng) for _ in range(10)]
+    terms = [base[i % 10] for i in range(50)]
+    coeffs = [float(v) for v in rng.standard_normal(50)]
+    norms = [tt.tt_norm(t) for t in terms]
+    ref, info = rounding.tt_round_sum(terms, coeffs, 1e-10, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
+    out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-10)
+    assert abs(ginfo["norm"] - info.norm) <= 1e-13 * info.scale
+    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
+    g = out.to_numpy()
+    if out.ranks == info.ranks:
+        assert diff_norm(g, ref) <= 1e-10 * info.scale
+    x = tt.tt_sum(terms, coeffs)
+    assert diff_norm(x, g) <= 1e-10 * info.norm * (1 + 1e-8) + np.sqrt(d - 1) * info.tau

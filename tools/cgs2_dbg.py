@@ -6,5 +6,5 @@ c = CONFIGS["C3"]
 st = make_shared_tail_set(c.d, c.n, c.r, int(os.environ.get("CGS2_M", "8")), c.kappa, c.seed)
 ctx = P.Context(0)
 A = [P.DeviceTT.from_numpy(a) for a in st.tensors]
-Q, R, rep = P.tt_orth(ctx, "cgs2", A, c.delta)
+Q, R, rep = P.tt_orth(ctx, os.environ.get("DRIVER", "cgs2"), A, c.delta)
 print(rep["max_rank_per_call"])

@@ -50,8 +50,9 @@ def main():
         qm, rm = st.qr_exact()
         for kind in c.drivers:
             P.tt_orth(ctx, kind, A[:2], c.delta)  # warm-up (kernels loaded, pool sized)
-            ctx.profile(True)
             (Q, R, rep), ms, wall = timed(lambda: P.tt_orth(ctx, kind, A, c.delta, want_loo=True))
+            ctx.profile(True)  # breakdown from a second, profiled run (events around every launch)
+            P.tt_orth(ctx, kind, A, c.delta)
             prof = ctx.profile_report()
             ctx.profile(False)
             sg = np.sign(np.diag(R))
@@ -59,7 +60,7 @@ def main():
             Rn = sg[:, None] * R if kind == "householder" else R
             rel_r = float(np.linalg.norm(Rn - rm) / np.linalg.norm(rm))
             norms = [float(np.sqrt(abs(P.tt_dot_batch(ctx, [q], [q]).cpu().item()))) for q in Q]
-            top = sorted(prof.items(), key=lambda kv: -kv[1]["ms"])[:4]
+            top = sorted(prof.items(), key=lambda kv: -kv[1]["ms"])[:int(os.environ.get("RC_TOP", "4"))]
             line = {"config": name, "driver": kind, "m": m, "d": c.d, "n": c.n, "r": c.r, "kappa": c.kappa,
                     "delta": c.delta, "rounding_calls": rep["rounding_calls"],
                     "calls_ok": rep["rounding_calls"] == expected_calls[kind](m),
@@ -67,6 +68,8 @@ def main():
                     "max_rank": max(rep["max_rank_per_call"]), "R_rel_err_vs_R_M": rel_r,
                     "q_norm_max_dev": max(abs(x - 1.0) for x in norms),
                     "loo_last": float(rep["loo_per_step"][-1]), "loo_max": float(np.max(rep["loo_per_step"])),
+                    "kernel_total_ms": round(sum(v["ms"] for v in prof.values()), 1),
+                    "launches_total": sum(v["launches"] for v in prof.values()),
                     "kernel_top": {k: {"ms": round(v["ms"], 2), "launches": v["launches"]} for k, v in top}}
             print(json.dumps(line), flush=True)
         if name == "C3":
