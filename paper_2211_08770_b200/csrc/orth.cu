@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 
+#include "gram.cuh"
 #include "orth.cuh"
 #include "ttops.cuh"
 
@@ -33,8 +34,57 @@ TTRef TTRef::of(tt_tensor x) {
   return t;
 }
 
+namespace {
+
+// Equally shaped operands (same modes and ranks, 16-byte aligned cores): the pairs become row /
+// column blocks of a Gram matrix over the distinct tensors and run on the pair-tiled Gram
+// kernel (gram.cu), which stages each mode slice once per tile -- the drivers' dot batches are
+// one vector against a set (CGS/CGS2 projections, MGS rows).  Output in pair order.
+bool dots_gram(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs, double* out_dev) {
+  const TTRef& f = *pairs[0].first;
+  std::vector<const TTRef*> uniq;
+  std::vector<int> ix(pairs.size()), iy(pairs.size());
+  auto id_of = [&](const TTRef* t) -> int {
+    for (size_t u = 0; u < uniq.size(); ++u)
+      if (uniq[u] == t || uniq[u]->core == t->core) return (int)u;
+    uniq.push_back(t);
+    return (int)uniq.size() - 1;
+  };
+  for (size_t q = 0; q < pairs.size(); ++q) {
+    for (const TTRef* t : {pairs[q].first, pairs[q].second}) {
+      if (t->d != f.d || t->n != f.n || t->r != f.r) return false;
+      for (const double* c : t->core)
+        if (reinterpret_cast<uintptr_t>(c) & 15) return false;
+    }
+    ix[q] = id_of(pairs[q].first);
+    iy[q] = id_of(pairs[q].second);
+  }
+  std::vector<const double*> cores;
+  for (const TTRef* t : uniq) cores.insert(cores.end(), t->core.begin(), t->core.end());
+  const int m = (int)uniq.size();
+  if (!gram_tiled_supported(cores, m, f.d, f.n, f.r)) return false;
+  std::vector<int32_t> blk;
+  for (size_t q = 0; q < pairs.size();) {
+    size_t e = q + 1;
+    while (e < pairs.size() && ix[e] == ix[q] && iy[e] == iy[e - 1] + 1) ++e;  // row block
+    if (e - q > 1) {
+      blk.insert(blk.end(), {ix[q], iy[q], 1, (int32_t)(e - q)});
+    } else {
+      while (e < pairs.size() && iy[e] == iy[q] && ix[e] == ix[e - 1] + 1) ++e;  // column block
+      blk.insert(blk.end(), {ix[q], iy[q], (int32_t)(e - q), 1});
+    }
+    q = e;
+  }
+  gram_tiled_blocks(ctx, cores, m, f.d, f.n, f.r, (int)(blk.size() / 4), blk.data(), out_dev);
+  return true;
+}
+
+}  // namespace
+
 void dots_device(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs, double* out_dev) {
   if (pairs.empty()) return;
+  static const bool pairwise = std::getenv("TT_B200_DOT_PAIRWISE") != nullptr;
+  if (!pairwise && dots_gram(ctx, pairs, out_dev)) return;
   DotBatch b;
   b.d = pairs[0].first->d;
   b.n = pairs[0].first->n;

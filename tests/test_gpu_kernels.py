@@ -50,6 +50,21 @@ def test_dot_batch_many_pairs_same_shape():
         assert abs(got[p] - tt.tt_dot(xs[p], ys[p])) <= 1e-12 * tt.tt_norm(xs[p]) * tt.tt_norm(ys[p])
 
 
+def test_dot_batch_uniform_blocks_gram_route():
+    """Equally shaped operands take the pair-tiled Gram route: a row block (one x against a
+    set), a column block, a repeated pair and isolated pairs, output in pair order."""
+    import paper_2211_08770_b200 as P
+    c = ctx()
+    rng = _rng(4)
+    d, n, r = 5, [6, 4, 7, 5, 3], [1, 5, 7, 6, 4, 1]
+    ts = [make_random_tt(d, n, r, rng) for _ in range(9)]
+    dv = [dev(t) for t in ts]
+    pairs = [(0, j) for j in range(1, 9)] + [(i, 8) for i in range(2, 6)] + [(3, 3), (3, 3), (7, 1), (2, 6)]
+    got = P.tt_dot_batch(c, [dv[i] for i, _ in pairs], [dv[j] for _, j in pairs]).cpu().numpy()
+    for q, (i, j) in enumerate(pairs):
+        assert abs(got[q] - tt.tt_dot(ts[i], ts[j])) <= 1e-12 * tt.tt_norm(ts[i]) * tt.tt_norm(ts[j]), q
+
+
 def test_dot_large_rank_global_path():
     """Ranks large enough that the per-pair workspace leaves shared memory."""
     import paper_2211_08770_b200 as P
