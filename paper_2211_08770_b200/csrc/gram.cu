@@ -1,17 +1,22 @@
 // TT-dot Gram matrix of m equally shaped TT-vectors, pair-tiled (Alg. 5 lines 2-6, Eq. (3):
 // G(i,j) = <a_i, a_j>; PAPER.md:19 dot through the core contraction).
 //
-// One CTA per tile of TI x TJ pairs (i in I, j in J, tiles of the lower triangle).  Per pair the
-// left-to-right recursion W_k = sum_s X^(i)_k(s)^T W_{k-1} X^(j)_k(s) runs with every pair's
-// W and the mode slice U = W X^(j)(s) in shared memory and the new W accumulated in registers:
-// per slice s the tile's tensors' slices X(s) are staged once and reused by all pairs of the
-// tile.  Each thread owns 4 x 4 micro-tiles (FP64 FMA, register blocked).  Summation order is
-// fixed (deterministic).
+// One CTA per tile of 2 x 2 pairs (i in I, j in J, tiles of the lower triangle), one warp per
+// pair.  Per pair the left-to-right recursion W_k = sum_s X^(i)_k(s)^T W_{k-1} X^(j)_k(s) runs as
+// two small GEMMs per mode slice on the FP64 tensor cores (DMMA): U = W X^(j)(s), V += X^(i)(s)^T U;
+// the tile's four tensors' slices X(s) are staged once (cp.async) and reused by all its pairs.
+// A tile runs on a cluster of CS CTAs that split the mode slices of every core (more CTAs in
+// flight and better balance: the C3 Gram has only 325 tiles for 148 SMs); the partial V of each
+// CTA meet through distributed shared memory once per core, summed in cluster-rank order.
+// Summation order is fixed (deterministic).
+#include <cooperative_groups.h>
 #include <cuda_pipeline.h>
 
 #include <algorithm>
 
 #include "gram.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ttb {
 
@@ -34,153 +39,209 @@ struct GramShape {
   int r[GT_MAXD + 1];
 };
 
-__host__ __device__ inline int ceil4(int x) { return (x + 3) & ~3; }
 
-template <int GT_T>  // threads per CTA; one V micro-tile per thread
-__global__ void __launch_bounds__(GT_T) gram_tile_kernel(const double* const* __restrict__ cores, GramShape sh, int m,
-                                                          int nbj, const GramTile* __restrict__ tiles, int RP,
-                                                          int S, int PS, double* __restrict__ G) {
+// ---- FP64 tensor-core (DMMA, mma.sync m8n8k4) version: one warp per pair of the 2 x 2 tile.
+// Warp p = 2 i + j keeps W's A fragments in registers for the whole core and V in DMMA
+// accumulators; per mode slice s it forms U = W X^(j)(s) (NT x NT 8x8 tiles, K = R0) into its own
+// shared block and then V += X^(i)(s)^T U -- no cross-warp dependency inside a slice, one
+// __syncthreads per slice for the staged slices (cp.async, double buffered).  One warp per SM
+// sub-partition with >= 2 independent accumulators saturates the DMMA pipe (tools/dmma_bench:
+// latency 26 cycles, 16 cycles per DMMA per sub-partition), so 9 accumulators per warp leave the
+// pipe the only limit.  Ranks are padded to 8 NT with zeros; the row stride L = 4 or 12 (mod 16)
+// keeps the fragment loads free of bank conflicts.
+__device__ __forceinline__ void gmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int GM_T = 128;  // threads per CTA: one warp per pair
+
+template <int NT>
+__global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const double* const* __restrict__ cores,
+                                                                      GramShape sh, int m,
+                                                                      const GramTile* __restrict__ tiles, int L,
+                                                                      double* __restrict__ G) {
   extern __shared__ __align__(16) double gsm[];
-  // smem blocks of PS doubles (per pair / per staged tensor), rows of stride S >= RP: padded so
-  // the 4x4 micro-tile accesses of a warp spread over the banks
-  const int RR = PS;
-  double* W = gsm;                 // [p][c][a]  (column-major W: W[p][c * RP + a] = W(a, c))
-  double* U = W + GT_P * RR;       // [p][a][c'] (row-major)
-  double* XB = U + GT_P * RR;      // 2 buffers x [t][a][a'] (row-major slices X(a, s, a')), I then J
-  const double** rowsrc = reinterpret_cast<const double**>(XB + 2 * (GT_I + GT_J) * RR);  // <= 4 * 32 rows
-  int* rowdst = reinterpret_cast<int*>(rowsrc + (GT_I + GT_J) * 32);
-  const int tid = threadIdx.x;
-  const GramTile tl = tiles[blockIdx.x];
-  const int i0 = tl.i0, j0 = tl.j0;
-  const int d = sh.d;
-  for (int idx = tid; idx < GT_P * RR; idx += GT_T) W[idx] = (idx % RR == 0) ? 1.0 : 0.0;  // W_0 = 1 (1 x 1)
-#pragma unroll 1
-  for (int k = 0; k < d; ++k) {
-    const int n = sh.n[k], R0 = sh.r[k], R1 = sh.r[k + 1];
-    const int T0 = ceil4(R0) / 4, T1 = ceil4(R1) / 4;
-    const int nU = GT_P * T0 * T1, nV = GT_P * T1 * T1;
-    for (int idx = tid; idx < 2 * (GT_I + GT_J) * RR; idx += GT_T) XB[idx] = 0.0;  // pads stay zero
-    double acc[16];
+  constexpr int RP = 8 * NT;
+  constexpr int KT = 2 * NT;                // k-steps of 4 over RP
+  const int MB = RP * L;                    // one matrix block
+  double* U = gsm;                          // [pair][a][c'] row-major, stride L (also W at core ends)
+  double* XB = U + GT_P * MB;               // 2 buffers x [I0, I1, J0, J1][a][a']
+  // staged-row tables (source base, destination) of two consecutive cores
+  const double** rowsrc = reinterpret_cast<const double**>(XB + 2 * (GT_I + GT_J) * MB);
+  int* rowdst = reinterpret_cast<int*>(rowsrc + 2 * (GT_I + GT_J) * RP);
+  const int tid = threadIdx.x, lane = tid & 31, p = tid >> 5, g = lane >> 2, tg = lane & 3;
+  const int pi = p / GT_J, pj = p % GT_J;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+  const GramTile tl = tiles[blockIdx.x / CS];
+  const int i0 = tl.i0, j0 = tl.j0, d = sh.d;
+  double* Up = U + p * MB;
+  // W's A fragments (W[8x + g][4q + tg]) for the whole core, in registers; W_0 = 1 (1 x 1)
+  double wf[NT][KT];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.0;
-    __syncthreads();
-    // slices X(:, s, :) of the tile's tensors, staged asynchronously one slice ahead
-    // slices X(:, s, :) of the tile's tensors, staged asynchronously one slice ahead: 16-byte
-    // copies when R1 is even (rows stay 16-byte aligned), per-row source bases tabulated once
-    const bool v16 = (R1 & 1) == 0;
-    const int cpr = v16 ? R1 / 2 : R1;             // copies per slice row
-    const int nrow = (GT_I + GT_J) * R0;
-    for (int rid = tid; rid < nrow; rid += GT_T) {
+  for (int x = 0; x < NT; ++x)
+#pragma unroll
+    for (int q = 0; q < KT; ++q) wf[x][q] = (x == 0 && q == 0 && g == 0 && tg == 0) ? 1.0 : 0.0;
+  double gv = 0.0;
+  // row table of core kk (slot kk & 1): rows of the tile's four tensors' core kk
+  auto table = [&](int kk) {
+    const int R0 = sh.r[kk], nk = sh.n[kk], R1 = sh.r[kk + 1], nrow = (GT_I + GT_J) * R0;
+    for (int rid = tid; rid < nrow; rid += GM_T) {
       const int t = rid / R0, a = rid - t * R0;
       int tens = t < GT_I ? i0 + t : j0 + (t - GT_I);
       if (tens >= m) tens = m - 1;  // padding tensor: its pairs are never written
-      rowsrc[rid] = cores[(int64_t)tens * d + k] + (int64_t)a * n * R1;
-      rowdst[rid] = t * RR + a * S;
+      rowsrc[(kk & 1) * (GT_I + GT_J) * RP + rid] = cores[(int64_t)tens * d + kk] + (int64_t)a * nk * R1;
+      rowdst[(kk & 1) * (GT_I + GT_J) * RP + rid] = t * MB + a * L;
     }
-    __syncthreads();
-    auto stage = [&](int s, double* buf) {
-      for (int idx = tid; idx < nrow * cpr; idx += GT_T) {
-        const int rid = idx / cpr, c = idx - rid * cpr;
-        const double* src = rowsrc[rid] + (int64_t)s * R1;
-        double* dst = buf + rowdst[rid];
-        if (v16) __pipeline_memcpy_async(dst + 2 * c, src + 2 * c, 2 * sizeof(double));
-        else __pipeline_memcpy_async(dst + c, src + c, sizeof(double));
+  };
+  // cp.async of slice s of core kk into buffer b: one row per warp, one 16-byte copy per lane
+  auto stage = [&](int kk, int s, int b) {
+    const int R0 = sh.r[kk], R1 = sh.r[kk + 1], nrow = (GT_I + GT_J) * R0;
+    const bool v16 = (R1 & 1) == 0;
+    const int cpr = v16 ? R1 / 2 : R1;  // copies per row (<= 32)
+    double* buf = XB + b * (GT_I + GT_J) * MB;
+    const double* const* rs = rowsrc + (kk & 1) * (GT_I + GT_J) * RP;
+    const int* rd = rowdst + (kk & 1) * (GT_I + GT_J) * RP;
+    if (lane < cpr) {
+      for (int rid = p; rid < nrow; rid += GM_T / 32) {
+        const double* src = rs[rid] + (int64_t)s * R1;
+        double* dst = buf + rd[rid];
+        if (v16) __pipeline_memcpy_async(dst + 2 * lane, src + 2 * lane, 2 * sizeof(double));
+        else __pipeline_memcpy_async(dst + lane, src + lane, sizeof(double));
       }
-      __pipeline_commit();
-    };
-    stage(0, XB);
+    }
+    __pipeline_commit();
+  };
+  auto srange = [&](int kk, int& b0, int& b1) {
+    b0 = (int)((int64_t)crank * sh.n[kk] / CS);
+    b1 = (int)((int64_t)(crank + 1) * sh.n[kk] / CS);
+  };
+  int bufc = 0;           // buffer of the next slice to consume
+  bool staged = false;    // core k's first slice already in flight (prefetched by core k-1)
 #pragma unroll 1
-    for (int s = 0; s < n; ++s) {
-      double* XI = XB + (s & 1) * (GT_I + GT_J) * RR;
-      double* XJ = XI + GT_I * RR;
+  for (int k = 0; k < d; ++k) {
+    const int R0 = sh.r[k], R1 = sh.r[k + 1];
+    const int K4 = (R0 + 3) >> 2;  // k-steps
+    int sb, se;
+    srange(k, sb, se);
+    // the next core can be prefetched when its staged slices have the same shape (pads stay zero)
+    const bool pre_next = k + 1 < d && sh.r[k + 1] == R0 && sh.r[k + 2] == R1;
+    if (!staged) {
+      __syncthreads();  // every warp is done reading the previous core's slices
+      for (int idx = tid; idx < 2 * (GT_I + GT_J) * MB; idx += GM_T) XB[idx] = 0.0;  // pads stay zero
+      table(k);
+    }
+    if (pre_next) table(k + 1);
+    __syncthreads();
+    if (!staged && sb < se) stage(k, sb, bufc);
+    staged = false;
+    double v[NT][NT][2];
+#pragma unroll
+    for (int x = 0; x < NT; ++x)
+#pragma unroll
+      for (int y = 0; y < NT; ++y) v[x][y][0] = v[x][y][1] = 0.0;
+#pragma unroll 1
+    for (int s = sb; s < se; ++s) {
+      const double* XS = XB + bufc * (GT_I + GT_J) * MB;
       __pipeline_wait_prior(0);
-      __syncthreads();  // slice s visible; V of slice s-1 done (its buffer may be refilled)
-      if (s + 1 < n) stage(s + 1, XB + ((s + 1) & 1) * (GT_I + GT_J) * RR);
-      // U_p = W_p X^(j_p)(s): (R0 x R0) x (R0 x R1)
-      for (int u = tid; u < nU; u += GT_T) {
-        const int p = u / (T0 * T1), rem = u % (T0 * T1), ta = rem / T1, tc = rem % T1;
-        const double* Wp = W + p * RR;
-        const double* Xj = XJ + (p % GT_J) * RR;
-        double c4[4][4];
+      __syncthreads();  // slice s visible to all; everyone is done with the other buffer
+      if (s + 1 < se) {
+        stage(k, s + 1, bufc ^ 1);
+      } else if (pre_next) {  // first slice of the next core, overlapped with this slice's math
+        int nb, ne;
+        srange(k + 1, nb, ne);
+        if (nb < ne) stage(k + 1, nb, bufc ^ 1);
+        staged = true;
+      }
+      bufc ^= 1;
+      const double* Xi = XS + pi * MB;
+      const double* Xj = XS + (GT_I + pj) * MB;
+      // U = W X_j(s): A[a][c] = W[a][c] (registers), B[c][c'] = X_j[c][c']
+      double u[NT][NT][2];
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < NT; ++x)
 #pragma unroll
-          for (int y = 0; y < 4; ++y) c4[x][y] = 0.0;
-#pragma unroll 2
-        for (int c = 0; c < R0; ++c) {
-          const double2 w01 = *reinterpret_cast<const double2*>(Wp + c * S + 4 * ta);
-          const double2 w23 = *reinterpret_cast<const double2*>(Wp + c * S + 4 * ta + 2);
-          const double2 x01 = *reinterpret_cast<const double2*>(Xj + c * S + 4 * tc);
-          const double2 x23 = *reinterpret_cast<const double2*>(Xj + c * S + 4 * tc + 2);
-          const double wv[4] = {w01.x, w01.y, w23.x, w23.y}, xv[4] = {x01.x, x01.y, x23.x, x23.y};
+        for (int y = 0; y < NT; ++y) u[x][y][0] = u[x][y][1] = 0.0;
 #pragma unroll
-          for (int x = 0; x < 4; ++x)
+      for (int q = 0; q < KT; ++q) {
+        if (q < K4) {
+          double bf[NT];
 #pragma unroll
-            for (int y = 0; y < 4; ++y) c4[x][y] += wv[x] * xv[y];
-        }
-        double* Up = U + p * RR;
+          for (int y = 0; y < NT; ++y) bf[y] = Xj[(4 * q + tg) * L + 8 * y + g];
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          *reinterpret_cast<double2*>(Up + (4 * ta + x) * S + 4 * tc) = make_double2(c4[x][0], c4[x][1]);
-          *reinterpret_cast<double2*>(Up + (4 * ta + x) * S + 4 * tc + 2) = make_double2(c4[x][2], c4[x][3]);
+          for (int x = 0; x < NT; ++x)
+#pragma unroll
+            for (int y = 0; y < NT; ++y) gmma(u[x][y][0], u[x][y][1], wf[x][q], bf[y]);
         }
       }
-      __syncthreads();
-      // V_p += X^(i_p)(s)^T U_p: (R1 x R0) x (R0 x R1), accumulated in registers
-      {
-        const int v = tid;
-        if (v < nV) {
-          const int p = v / (T1 * T1), rem = v % (T1 * T1), ta = rem / T1, tc = rem % T1;
-          const double* Xi = XI + (p / GT_J) * RR;
-          const double* Up = U + p * RR;
-#pragma unroll 2
-          for (int a = 0; a < R0; ++a) {
-            const double2 x01 = *reinterpret_cast<const double2*>(Xi + a * S + 4 * ta);
-            const double2 x23 = *reinterpret_cast<const double2*>(Xi + a * S + 4 * ta + 2);
-            const double2 u01 = *reinterpret_cast<const double2*>(Up + a * S + 4 * tc);
-            const double2 u23 = *reinterpret_cast<const double2*>(Up + a * S + 4 * tc + 2);
-            const double xv[4] = {x01.x, x01.y, x23.x, x23.y}, uv[4] = {u01.x, u01.y, u23.x, u23.y};
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < NT; ++x)
 #pragma unroll
-              for (int y = 0; y < 4; ++y) acc[x * 4 + y] += xv[x] * uv[y];
-          }
+        for (int y = 0; y < NT; ++y)
+          *reinterpret_cast<double2*>(Up + (8 * x + g) * L + 8 * y + 2 * tg) = make_double2(u[x][y][0], u[x][y][1]);
+      __syncwarp();
+      // V += X_i(s)^T U: A[a'][a] = X_i[a][a'], B[a][c'] = U[a][c']
+#pragma unroll
+      for (int q = 0; q < KT; ++q) {
+        if (q < K4) {
+          double af[NT], bf[NT];
+#pragma unroll
+          for (int x = 0; x < NT; ++x) af[x] = Xi[(4 * q + tg) * L + 8 * x + g];
+#pragma unroll
+          for (int y = 0; y < NT; ++y) bf[y] = Up[(4 * q + tg) * L + 8 * y + g];
+#pragma unroll
+          for (int x = 0; x < NT; ++x)
+#pragma unroll
+            for (int y = 0; y < NT; ++y) gmma(v[x][y][0], v[x][y][1], af[x], bf[y]);
         }
       }
+      __syncwarp();  // U reads done before the next slice overwrites it
     }
-    __syncthreads();
-    // W_k (column-major) <- V
-    for (int idx = tid; idx < GT_P * RR; idx += GT_T) W[idx] = 0.0;
-    __syncthreads();
-    {
-      const int v = tid;
-      if (v < nV) {
-        const int p = v / (T1 * T1), rem = v % (T1 * T1), ta = rem / T1, tc = rem % T1;
-        double* Wp = W + p * RR;
+    // W_k = V (summed over the cluster's slice ranges, cluster-rank order) -> A fragments
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+    for (int x = 0; x < NT; ++x)
 #pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            const int a1 = 4 * ta + x, c1 = 4 * tc + y;
-            if (a1 < R1 && c1 < R1) Wp[c1 * S + a1] = acc[x * 4 + y];
-          }
+      for (int y = 0; y < NT; ++y)
+        *reinterpret_cast<double2*>(Up + (8 * x + g) * L + 8 * y + 2 * tg) = make_double2(v[x][y][0], v[x][y][1]);
+    if (CS > 1) {
+      cl.sync();  // every CTA's partial is complete
+#pragma unroll
+      for (int x = 0; x < NT; ++x)
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+          double w = 0.0;
+          for (int c = 0; c < CS; ++c) w += cl.map_shared_rank(Up, c)[(8 * x + g) * L + 4 * q + tg];
+          wf[x][q] = w;
+        }
+      if (k == d - 1) {
+        double w = 0.0;
+        for (int c = 0; c < CS; ++c) w += cl.map_shared_rank(Up, c)[0];
+        gv = w;
       }
+      cl.sync();  // partials read everywhere before U is reused
+    } else {
+      __syncwarp();
+#pragma unroll
+      for (int x = 0; x < NT; ++x)
+#pragma unroll
+        for (int q = 0; q < KT; ++q) wf[x][q] = Up[(8 * x + g) * L + 4 * q + tg];
+      if (k == d - 1) gv = Up[0];
+      __syncwarp();
     }
-    __syncthreads();
   }
-  if (tid < GT_P) {
-    const int i = i0 + tid / GT_J, j = j0 + tid % GT_J;
-    const double g = W[tid * RR];
+  if (lane == 0 && crank == 0) {
+    const int i = i0 + pi, j = j0 + pj;
     if (tl.mode == 0) {
       if (i < m && j < m && i >= j) {
-        G[(int64_t)i * m + j] = g;
-        G[(int64_t)j * m + i] = g;
+        G[(int64_t)i * m + j] = gv;
+        G[(int64_t)j * m + i] = gv;
       }
     } else if (i < tl.ilim && j < tl.jlim) {
-      G[tl.off + (int64_t)(i - tl.bi0) * tl.bj + (j - tl.bj0)] = g;
+      G[tl.off + (int64_t)(i - tl.bi0) * tl.bj + (j - tl.bj0)] = gv;
     }
   }
-  (void)nbj;
 }
 
 }  // namespace
@@ -193,8 +254,7 @@ bool gram_tiled_supported(const std::vector<const double*>& cores, int m, int d,
   for (int k = 0; k <= d; ++k) rmax = std::max<int>(rmax, (int)r[(size_t)k]);
   for (int k = 0; k < d; ++k)
     if (n[(size_t)k] < 1) return false;
-  // one V micro-tile per thread: GT_P * (ceil4(R)/4)^2 <= 256 (R <= 32)
-  return GT_P * (ceil4(rmax) / 4) * (ceil4(rmax) / 4) <= 256;
+  return rmax <= 32;  // ranks padded to 8 NT, NT <= 4 (one pair's fragments per warp)
 }
 
 static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d,
@@ -214,31 +274,48 @@ static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int
     rmax = std::max<int>(rmax, (int)r[(size_t)k]);
   }
   if (tiles.empty()) return;
-  const int RP = ceil4(rmax);
-  // row stride / block stride chosen for the fewest shared-memory bank conflicts (offline model)
-  const int S = (RP == 8 || RP == 12 || RP == 20 || RP == 24) ? RP + 2 : RP;
-  const int PS = S * RP + 2;
   BBuf dt, dc;
   dt.upload(ctx, tiles.data(), tiles.size() * sizeof(GramTile));
   dc.upload(ctx, cores.data(), cores.size() * sizeof(double*));
-  const size_t smem = sizeof(double) * (size_t)(2 * GT_P + 2 * (GT_I + GT_J)) * PS +
-                      (sizeof(double*) + sizeof(int)) * (GT_I + GT_J) * 32;
   double bytes = 0.0;
   for (int k = 0; k < d; ++k) bytes += 8.0 * (double)m * r[(size_t)k] * n[(size_t)k] * r[(size_t)k + 1];
-  const int nv = GT_P * (RP / 4) * (RP / 4);
   const int ntiles = (int)tiles.size();
   const GramTile* tp = static_cast<const GramTile*>(dt.p);
-  if (nv <= 128) {
-    TTB_CUDA(cudaFuncSetAttribute(gram_tile_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TTB_RUN(ctx, "tt_gram_tiled", flops * npairs, bytes,
-            gram_tile_kernel<128><<<ntiles, 128, smem, ctx->stream>>>(static_cast<const double* const*>(dc.p), sh, m,
-                                                                        0, tp, RP, S, PS, out));
-  } else {
-    TTB_CUDA(cudaFuncSetAttribute(gram_tile_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    TTB_RUN(ctx, "tt_gram_tiled", flops * npairs, bytes,
-            gram_tile_kernel<256><<<ntiles, 256, smem, ctx->stream>>>(static_cast<const double* const*>(dc.p), sh, m,
-                                                                        0, tp, RP, S, PS, out));
-  }
+  const int NT = (rmax + 7) / 8;
+  int L = 8 * NT;  // row stride: 4 or 12 (mod 16) keeps the fragment loads conflict-free
+  while (L % 16 != 4 && L % 16 != 12) ++L;
+  const size_t smem_m = sizeof(double) * (size_t)(GT_P + 2 * (GT_I + GT_J)) * (8 * NT) * L +
+                        2 * (sizeof(double*) + sizeof(int)) * (size_t)(GT_I + GT_J) * (8 * NT);
+  auto kern = NT == 1 ? gram_mma_kernel<1> : NT == 2 ? gram_mma_kernel<2> : NT == 3 ? gram_mma_kernel<3>
+                                                                                  : gram_mma_kernel<4>;
+  const int T = GM_T;
+  TTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m));
+  TTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // slice split: the smallest cluster size that fills every resident slot once
+  // (>= 2 slices per CTA, <= 8 CTAs per cluster)
+  int per_sm = 1;
+  TTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem_m));
+  int nmin = 1 << 30;
+  for (int k = 0; k < d; ++k) nmin = std::min(nmin, (int)n[(size_t)k]);
+  static const char* cs_env = std::getenv("TT_B200_GRAM_CS");
+  int CS = 1;
+  while (CS < 8 && 2 * CS <= nmin / 2 && (int64_t)ntiles * CS < (int64_t)ctx->num_sms * std::max(per_sm, 1)) CS *= 2;
+  if (cs_env) CS = std::max(1, std::min(8, std::atoi(cs_env)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ntiles * CS));
+  cfg.blockDim = dim3((unsigned)T);
+  cfg.dynamicSmemBytes = smem_m;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const double* const* cp = static_cast<const double* const*>(dc.p);
+  TTB_RUN(ctx, "tt_gram_tiled", flops * npairs, bytes,
+          TTB_CUDA(cudaLaunchKernelEx(&cfg, kern, cp, sh, m, tp, L, out)));
 }
 
 void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
