@@ -33,10 +33,11 @@ struct GramTile {
   int64_t off;
 };
 
-struct GramShape {
+struct GramShape {  // modes and the rank profiles of the I-side (r) and J-side (q) tensors
   int d;
   int n[GT_MAXD];
   int r[GT_MAXD + 1];
+  int q[GT_MAXD + 1];
 };
 
 
@@ -57,6 +58,27 @@ __device__ __forceinline__ void gmma(double& c0, double& c1, double a, double b)
 
 constexpr int GM_T = 128;  // threads per CTA: one warp per pair
 
+// 1-D bulk copies global -> shared (TMA engine) completing on an mbarrier
+__device__ __forceinline__ uint32_t g_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void g_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void g_mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void g_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(g_smem_u32(dst)), "l"(src), "r"(bytes), "r"(g_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void g_mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(g_smem_u32(bar)), "r"(parity) : "memory");
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const double* const* __restrict__ cores,
                                                                       GramShape sh, int m,
@@ -68,9 +90,7 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   const int MB = RP * L;                    // one matrix block
   double* U = gsm;                          // [pair][a][c'] row-major, stride L (also W at core ends)
   double* XB = U + GT_P * MB;               // 2 buffers x [I0, I1, J0, J1][a][a']
-  // staged-row tables (source base, destination) of two consecutive cores
-  const double** rowsrc = reinterpret_cast<const double**>(XB + 2 * (GT_I + GT_J) * MB);
-  int* rowdst = reinterpret_cast<int*>(rowsrc + 2 * (GT_I + GT_J) * RP);
+  __shared__ uint64_t gbar[2];  // staged-slice buffers: TMA completion
   const int tid = threadIdx.x, lane = tid & 31, p = tid >> 5, g = lane >> 2, tg = lane & 3;
   const int pi = p / GT_J, pj = p % GT_J;
   cg::cluster_group cl = cg::this_cluster();
@@ -78,6 +98,11 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   const GramTile tl = tiles[blockIdx.x / CS];
   const int i0 = tl.i0, j0 = tl.j0, d = sh.d;
   double* Up = U + p * MB;
+  if (tid == 0) {
+    g_mbar_init(&gbar[0], 1);
+    g_mbar_init(&gbar[1], 1);
+  }
+  uint32_t ph0 = 0, ph1 = 0;
   // W's A fragments (W[8x + g][4q + tg]) for the whole core, in registers; W_0 = 1 (1 x 1)
   double wf[NT][KT];
 #pragma unroll
@@ -85,34 +110,47 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
 #pragma unroll
     for (int q = 0; q < KT; ++q) wf[x][q] = (x == 0 && q == 0 && g == 0 && tg == 0) ? 1.0 : 0.0;
   double gv = 0.0;
-  // row table of core kk (slot kk & 1): rows of the tile's four tensors' core kk
-  auto table = [&](int kk) {
-    const int R0 = sh.r[kk], nk = sh.n[kk], R1 = sh.r[kk + 1], nrow = (GT_I + GT_J) * R0;
-    for (int rid = tid; rid < nrow; rid += GM_T) {
-      const int t = rid / R0, a = rid - t * R0;
-      int tens = t < GT_I ? i0 + t : j0 + (t - GT_I);
-      if (tens >= m) tens = m - 1;  // padding tensor: its pairs are never written
-      rowsrc[(kk & 1) * (GT_I + GT_J) * RP + rid] = cores[(int64_t)tens * d + kk] + (int64_t)a * nk * R1;
-      rowdst[(kk & 1) * (GT_I + GT_J) * RP + rid] = t * MB + a * L;
+  // Staged rows of core kk: thread tid < nrow owns row tid (I tensors: R0i rows of R1i doubles,
+  // then J tensors: R0j rows of R1j), clamped into the tile's block, so a padding tensor has its
+  // side's shape (its pairs are never written).  One TMA bulk copy per row and slice.
+  struct Row { const double* src; int dst, len; };
+  auto row_of = [&](int kk) -> Row {
+    const int nk = sh.n[kk], R0i = sh.r[kk], R1i = sh.r[kk + 1], R0j = sh.q[kk], R1j = sh.q[kk + 1];
+    const int nI = GT_I * R0i, nrow = nI + GT_J * R0j;
+    Row rw{nullptr, 0, 0};
+    if (tid < nrow) {
+      const bool iside = tid < nI;
+      const int R0 = iside ? R0i : R0j, R1 = iside ? R1i : R1j, rr = iside ? tid : tid - nI;
+      const int tt = rr / R0, a = rr - tt * R0;
+      const int tens = iside ? min(i0 + tt, tl.ilim - 1) : min(j0 + tt, tl.jlim - 1);
+      rw.src = cores[(int64_t)tens * d + kk] + (int64_t)a * nk * R1;
+      rw.dst = (iside ? tt : GT_I + tt) * MB + a * L;
+      rw.len = R1;
+    }
+    return rw;
+  };
+  // bulk path when every row is a multiple of 16 bytes (even ranks), else 8-byte cp.async
+  auto bulk_ok = [&](int kk) { return ((sh.r[kk + 1] | sh.q[kk + 1]) & 1) == 0; };
+  auto stage = [&](int kk, const Row& rw, int s, int b) {
+    double* buf = XB + b * (GT_I + GT_J) * MB;
+    if (bulk_ok(kk)) {
+      if (tid == 0)
+        g_mbar_expect(&gbar[b], (uint32_t)(sizeof(double) * (GT_I * sh.r[kk] * sh.r[kk + 1] +
+                                                              GT_J * sh.q[kk] * sh.q[kk + 1])));
+      if (rw.len) g_bulk(buf + rw.dst, rw.src + (int64_t)s * rw.len, (uint32_t)(rw.len * sizeof(double)), &gbar[b]);
+    } else {
+      for (int c = 0; c < rw.len; ++c)
+        __pipeline_memcpy_async(buf + rw.dst + c, rw.src + (int64_t)s * rw.len + c, sizeof(double));
+      __pipeline_commit();
     }
   };
-  // cp.async of slice s of core kk into buffer b: one row per warp, one 16-byte copy per lane
-  auto stage = [&](int kk, int s, int b) {
-    const int R0 = sh.r[kk], R1 = sh.r[kk + 1], nrow = (GT_I + GT_J) * R0;
-    const bool v16 = (R1 & 1) == 0;
-    const int cpr = v16 ? R1 / 2 : R1;  // copies per row (<= 32)
-    double* buf = XB + b * (GT_I + GT_J) * MB;
-    const double* const* rs = rowsrc + (kk & 1) * (GT_I + GT_J) * RP;
-    const int* rd = rowdst + (kk & 1) * (GT_I + GT_J) * RP;
-    if (lane < cpr) {
-      for (int rid = p; rid < nrow; rid += GM_T / 32) {
-        const double* src = rs[rid] + (int64_t)s * R1;
-        double* dst = buf + rd[rid];
-        if (v16) __pipeline_memcpy_async(dst + 2 * lane, src + 2 * lane, 2 * sizeof(double));
-        else __pipeline_memcpy_async(dst + lane, src + lane, sizeof(double));
-      }
+  auto wait_slice = [&](int kk, int b) {
+    if (bulk_ok(kk)) {
+      if (b == 0) { g_mbar_wait(&gbar[0], ph0); ph0 ^= 1u; }
+      else { g_mbar_wait(&gbar[1], ph1); ph1 ^= 1u; }
+    } else {
+      __pipeline_wait_prior(0);
     }
-    __pipeline_commit();
   };
   auto srange = [&](int kk, int& b0, int& b1) {
     b0 = (int)((int64_t)crank * sh.n[kk] / CS);
@@ -120,22 +158,22 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   };
   int bufc = 0;           // buffer of the next slice to consume
   bool staged = false;    // core k's first slice already in flight (prefetched by core k-1)
+  __syncthreads();        // barriers initialised
 #pragma unroll 1
   for (int k = 0; k < d; ++k) {
-    const int R0 = sh.r[k], R1 = sh.r[k + 1];
-    const int K4 = (R0 + 3) >> 2;  // k-steps
+    const int K4i = (sh.r[k] + 3) >> 2, K4j = (sh.q[k] + 3) >> 2;  // k-steps of the V / U GEMMs
     int sb, se;
     srange(k, sb, se);
     // the next core can be prefetched when its staged slices have the same shape (pads stay zero)
-    const bool pre_next = k + 1 < d && sh.r[k + 1] == R0 && sh.r[k + 2] == R1;
+    const bool pre_next = k + 1 < d && sh.r[k + 1] == sh.r[k] && sh.r[k + 2] == sh.r[k + 1] &&
+                          sh.q[k + 1] == sh.q[k] && sh.q[k + 2] == sh.q[k + 1];
+    const Row rw = row_of(k);
     if (!staged) {
       __syncthreads();  // every warp is done reading the previous core's slices
       for (int idx = tid; idx < 2 * (GT_I + GT_J) * MB; idx += GM_T) XB[idx] = 0.0;  // pads stay zero
-      table(k);
+      __syncthreads();
+      if (sb < se) stage(k, rw, sb, bufc);
     }
-    if (pre_next) table(k + 1);
-    __syncthreads();
-    if (!staged && sb < se) stage(k, sb, bufc);
     staged = false;
     double v[NT][NT][2];
 #pragma unroll
@@ -145,14 +183,14 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
 #pragma unroll 1
     for (int s = sb; s < se; ++s) {
       const double* XS = XB + bufc * (GT_I + GT_J) * MB;
-      __pipeline_wait_prior(0);
+      wait_slice(k, bufc);
       __syncthreads();  // slice s visible to all; everyone is done with the other buffer
       if (s + 1 < se) {
-        stage(k, s + 1, bufc ^ 1);
+        stage(k, rw, s + 1, bufc ^ 1);
       } else if (pre_next) {  // first slice of the next core, overlapped with this slice's math
         int nb, ne;
         srange(k + 1, nb, ne);
-        if (nb < ne) stage(k + 1, nb, bufc ^ 1);
+        if (nb < ne) stage(k + 1, row_of(k + 1), nb, bufc ^ 1);
         staged = true;
       }
       bufc ^= 1;
@@ -166,7 +204,7 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
         for (int y = 0; y < NT; ++y) u[x][y][0] = u[x][y][1] = 0.0;
 #pragma unroll
       for (int q = 0; q < KT; ++q) {
-        if (q < K4) {
+        if (q < K4j) {
           double bf[NT];
 #pragma unroll
           for (int y = 0; y < NT; ++y) bf[y] = Xj[(4 * q + tg) * L + 8 * y + g];
@@ -185,7 +223,7 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
       // V += X_i(s)^T U: A[a'][a] = X_i[a][a'], B[a][c'] = U[a][c']
 #pragma unroll
       for (int q = 0; q < KT; ++q) {
-        if (q < K4) {
+        if (q < K4i) {
           double af[NT], bf[NT];
 #pragma unroll
           for (int x = 0; x < NT; ++x) af[x] = Xi[(4 * q + tg) * L + 8 * x + g];
@@ -248,8 +286,9 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
 
 bool gram_tiled_supported(const std::vector<const double*>& cores, int m, int d, const std::vector<int64_t>& n,
                           const std::vector<int64_t>& r) {
-  (void)cores;
   if (m < 1 || d < 1 || d > GT_MAXD) return false;
+  for (const double* c : cores)  // 16-byte cp.async rows
+    if (reinterpret_cast<uintptr_t>(c) & 15) return false;
   int rmax = 1;
   for (int k = 0; k <= d; ++k) rmax = std::max<int>(rmax, (int)r[(size_t)k]);
   for (int k = 0; k < d; ++k)
@@ -258,7 +297,7 @@ bool gram_tiled_supported(const std::vector<const double*>& cores, int m, int d,
 }
 
 static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d,
-                        const std::vector<int64_t>& n, const std::vector<int64_t>& r,
+                        const std::vector<int64_t>& n, const std::vector<int64_t>& r, const std::vector<int64_t>& q,
                         const std::vector<GramTile>& tiles, double npairs, double* out) {
   GramShape sh{};
   sh.d = d;
@@ -266,12 +305,15 @@ static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int
   double flops = 0.0;
   for (int k = 0; k < d; ++k) {
     sh.n[k] = (int)n[(size_t)k];
-    const double R0 = (double)r[(size_t)k], R1 = (double)r[(size_t)k + 1];
-    flops += 2.0 * (double)n[(size_t)k] * (R0 * R0 * R1 + R0 * R1 * R1);  // per pair
+    const double Ri0 = (double)r[(size_t)k], Ri1 = (double)r[(size_t)k + 1];
+    const double Rj0 = (double)q[(size_t)k], Rj1 = (double)q[(size_t)k + 1];
+    // per pair: U = W X_j (Ri0 Rj0 Rj1), V = X_i^T U (Ri0 Ri1 Rj1)
+    flops += 2.0 * (double)n[(size_t)k] * (Ri0 * Rj0 * Rj1 + Ri0 * Ri1 * Rj1);
   }
   for (int k = 0; k <= d; ++k) {
     sh.r[k] = (int)r[(size_t)k];
-    rmax = std::max<int>(rmax, (int)r[(size_t)k]);
+    sh.q[k] = (int)q[(size_t)k];
+    rmax = std::max<int>(rmax, (int)std::max(r[(size_t)k], q[(size_t)k]));
   }
   if (tiles.empty()) return;
   BBuf dt, dc;
@@ -284,8 +326,7 @@ static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int
   const int NT = (rmax + 7) / 8;
   int L = 8 * NT;  // row stride: 4 or 12 (mod 16) keeps the fragment loads conflict-free
   while (L % 16 != 4 && L % 16 != 12) ++L;
-  const size_t smem_m = sizeof(double) * (size_t)(GT_P + 2 * (GT_I + GT_J)) * (8 * NT) * L +
-                        2 * (sizeof(double*) + sizeof(int)) * (size_t)(GT_I + GT_J) * (8 * NT);
+  const size_t smem_m = sizeof(double) * (size_t)(GT_P + 2 * (GT_I + GT_J)) * (8 * NT) * L;
   auto kern = NT == 1 ? gram_mma_kernel<1> : NT == 2 ? gram_mma_kernel<2> : NT == 3 ? gram_mma_kernel<3>
                                                                                   : gram_mma_kernel<4>;
   const int T = GM_T;
@@ -324,12 +365,13 @@ void gram_tiled(tt_ctx ctx, const std::vector<const double*>& cores, int m, int 
   for (int i0 = 0; i0 < m; i0 += GT_I)
     for (int j0 = 0; j0 < m; j0 += GT_J)
       if (i0 + GT_I - 1 >= j0) tiles.push_back(GramTile{i0, j0, m, m, 0, 0, 0, 0, 0});  // holds a pair i >= j
-  gram_launch(ctx, cores, m, d, n, r, tiles, 0.5 * m * (m + 1.0), G_dev);
+  gram_launch(ctx, cores, m, d, n, r, r, tiles, 0.5 * m * (m + 1.0), G_dev);
 }
 
 void gram_tiled_blocks(tt_ctx ctx, const std::vector<const double*>& cores, int m, int d,
                        const std::vector<int64_t>& n, const std::vector<int64_t>& r, int nblk, const int32_t* blk,
-                       double* packed_dev) {
+                       double* packed_dev, const std::vector<int64_t>* rj) {
+  const std::vector<int64_t>& q = rj ? *rj : r;
   std::vector<GramTile> tiles;
   int64_t off = 0;
   double npairs = 0.0;
@@ -340,7 +382,7 @@ void gram_tiled_blocks(tt_ctx ctx, const std::vector<const double*>& cores, int 
     off += (int64_t)bi * bj;
     npairs += (double)bi * bj;
   }
-  gram_launch(ctx, cores, m, d, n, r, tiles, npairs, packed_dev);
+  gram_launch(ctx, cores, m, d, n, r, q, tiles, npairs, packed_dev);
 }
 
 }  // namespace ttb

@@ -36,46 +36,51 @@ TTRef TTRef::of(tt_tensor x) {
 
 namespace {
 
-// Equally shaped operands (same modes and ranks, 16-byte aligned cores): the pairs become row /
-// column blocks of a Gram matrix over the distinct tensors and run on the pair-tiled Gram
-// kernel (gram.cu), which stages each mode slice once per tile -- the drivers' dot batches are
-// one vector against a set (CGS/CGS2 projections, MGS rows).  Output in pair order.
+// Operands with one rank profile per side (all first operands alike, all second operands alike;
+// 16-byte aligned cores): the pairs become row / column blocks of a Gram matrix between the
+// distinct first and the distinct second operands and run on the pair-tiled DMMA Gram kernel
+// (gram.cu), which stages each mode slice once per tile -- the drivers' dot batches are one
+// vector against a set (CGS/CGS2 projections, MGS rows).  Output in pair order.
 bool dots_gram(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs, double* out_dev) {
-  const TTRef& f = *pairs[0].first;
-  std::vector<const TTRef*> uniq;
+  const TTRef& fa = *pairs[0].first;
+  const TTRef& fb = *pairs[0].second;
+  std::vector<const TTRef*> ua, ub;  // distinct first / second operands
   std::vector<int> ix(pairs.size()), iy(pairs.size());
-  auto id_of = [&](const TTRef* t) -> int {
-    for (size_t u = 0; u < uniq.size(); ++u)
-      if (uniq[u] == t || uniq[u]->core == t->core) return (int)u;
-    uniq.push_back(t);
-    return (int)uniq.size() - 1;
+  auto id_of = [](std::vector<const TTRef*>& u, const TTRef* t) -> int {
+    for (size_t k = 0; k < u.size(); ++k)
+      if (u[k] == t || u[k]->core == t->core) return (int)k;
+    u.push_back(t);
+    return (int)u.size() - 1;
   };
   for (size_t q = 0; q < pairs.size(); ++q) {
-    for (const TTRef* t : {pairs[q].first, pairs[q].second}) {
-      if (t->d != f.d || t->n != f.n || t->r != f.r) return false;
-      for (const double* c : t->core)
-        if (reinterpret_cast<uintptr_t>(c) & 15) return false;
-    }
-    ix[q] = id_of(pairs[q].first);
-    iy[q] = id_of(pairs[q].second);
+    const TTRef* a = pairs[q].first;
+    const TTRef* b = pairs[q].second;
+    if (a->d != fa.d || a->n != fa.n || a->r != fa.r) return false;
+    if (b->d != fb.d || b->n != fb.n || b->r != fb.r) return false;
+    ix[q] = id_of(ua, a);
+    iy[q] = id_of(ub, b);
   }
+  if (fa.d != fb.d || fa.n != fb.n) return false;
   std::vector<const double*> cores;
-  for (const TTRef* t : uniq) cores.insert(cores.end(), t->core.begin(), t->core.end());
-  const int m = (int)uniq.size();
-  if (!gram_tiled_supported(cores, m, f.d, f.n, f.r)) return false;
+  for (const TTRef* t : ua) cores.insert(cores.end(), t->core.begin(), t->core.end());
+  for (const TTRef* t : ub) cores.insert(cores.end(), t->core.begin(), t->core.end());
+  const int na = (int)ua.size(), m = na + (int)ub.size();
+  std::vector<int64_t> rmax(fa.r.size());
+  for (size_t k = 0; k < rmax.size(); ++k) rmax[k] = std::max(fa.r[k], fb.r[k]);
+  if (!gram_tiled_supported(cores, m, fa.d, fa.n, rmax)) return false;
   std::vector<int32_t> blk;
   for (size_t q = 0; q < pairs.size();) {
     size_t e = q + 1;
     while (e < pairs.size() && ix[e] == ix[q] && iy[e] == iy[e - 1] + 1) ++e;  // row block
     if (e - q > 1) {
-      blk.insert(blk.end(), {ix[q], iy[q], 1, (int32_t)(e - q)});
+      blk.insert(blk.end(), {ix[q], na + iy[q], 1, (int32_t)(e - q)});
     } else {
       while (e < pairs.size() && iy[e] == iy[q] && ix[e] == ix[e - 1] + 1) ++e;  // column block
-      blk.insert(blk.end(), {ix[q], iy[q], (int32_t)(e - q), 1});
+      blk.insert(blk.end(), {ix[q], na + iy[q], (int32_t)(e - q), 1});
     }
     q = e;
   }
-  gram_tiled_blocks(ctx, cores, m, f.d, f.n, f.r, (int)(blk.size() / 4), blk.data(), out_dev);
+  gram_tiled_blocks(ctx, cores, m, fa.d, fa.n, fa.r, (int)(blk.size() / 4), blk.data(), out_dev, &fb.r);
   return true;
 }
 

@@ -65,6 +65,21 @@ def test_dot_batch_uniform_blocks_gram_route():
         assert abs(got[q] - tt.tt_dot(ts[i], ts[j])) <= 1e-12 * tt.tt_norm(ts[i]) * tt.tt_norm(ts[j]), q
 
 
+def test_dot_batch_two_rank_profiles_gram_route():
+    """First operands share one rank profile, second operands another (a projection of x on a
+    set Q): row and column blocks with I-side and J-side shapes that differ per core."""
+    import paper_2211_08770_b200 as P
+    c = ctx()
+    rng = _rng(5)
+    d, n = 5, [6, 4, 7, 5, 3]
+    qs = [make_random_tt(d, n, [1, 5, 7, 6, 4, 1], rng) for _ in range(7)]
+    xs = [make_random_tt(d, n, [1, 3, 9, 2, 5, 1], rng) for _ in range(3)]
+    pairs = [(qs[i], xs[0]) for i in range(7)] + [(qs[2], xs[j]) for j in range(3)] + [(qs[5], xs[1])]
+    got = P.tt_dot_batch(c, [dev(a) for a, _ in pairs], [dev(b) for _, b in pairs]).cpu().numpy()
+    for q, (a, b) in enumerate(pairs):
+        assert abs(got[q] - tt.tt_dot(a, b)) <= 1e-12 * tt.tt_norm(a) * tt.tt_norm(b), q
+
+
 def test_dot_large_rank_global_path():
     """Ranks large enough that the per-pair workspace leaves shared memory."""
     import paper_2211_08770_b200 as P

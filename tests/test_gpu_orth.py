@@ -67,12 +67,25 @@ def _check(kind, st, delta, Q, R, rep, ref):
     m = st.m
     a, b = TABLE1["per_m"][kind]
     assert rep["rounding_calls"] == a * m + b == ref.rounding_calls
-    assert rep["max_rank_per_call"] == [max(i.ranks) for i in ref.infos]
     kap = _kappas(st)
     # Householder's q_i also carry the delta-truncations of the u_j, amplified by kappa
     # (its LOO stagnates at delta): amplification (floor_c u + delta) m kappa.
     extra = delta if kind == "householder" else 0.0
     amp = lambda k: (FLOOR_C * U_ROUND + extra) * m * kap[k] ** POWER[kind]
+    # Free-running, the GPU's rounding inputs differ from the oracle's by the amplified rounding
+    # of all previous steps (relative amp(k)).  Where that is small the truncation decisions must
+    # agree call by call (except within the window of tau); where it reaches O(1) (C1
+    # Householder: (2048 u + delta) m kappa ~ 10) the inputs themselves differ in the truncated
+    # directions and the per-call ranks are checked by the teacher-forced replays instead
+    # (test_orth_c1_teacher_forced: same inputs on both sides).
+    ranks_g = rep["max_rank_per_call"]
+    if amp(m - 1) < 1e-3:
+        for t, info in enumerate(ref.infos):
+            if ranks_g[t] == max(info.ranks):
+                continue
+            lo = min(ranks_g[t], max(info.ranks))
+            gaps = [abs(np.sqrt(np.sum(S[lo:] ** 2)) - info.tau) / info.tau for S in info.sigmas if len(S) > lo]
+            assert gaps and min(gaps) <= max(1e-9, amp(m - 1)), (kind, t, ranks_g[t], max(info.ranks), min(gaps))
     hh = (kind == "householder")
     sg, sc = _signs(R), _signs(ref.R)
     Rg = sg[:, None] * R if hh else R
