@@ -103,7 +103,7 @@ void dots_device(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTR
     b.xr.insert(b.xr.end(), x.r.begin(), x.r.end());
     b.yr.insert(b.yr.end(), y.r.begin(), y.r.end());
   }
-  dot_batch(ctx, b, out_dev);
+  dot_batch(ctx, b, out_dev);  // ranks > 32: grouped DMMA GEMMs per core
 }
 
 std::vector<double> dots_host(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs) {

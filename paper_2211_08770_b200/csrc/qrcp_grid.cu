@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "qr.cuh"
 
@@ -314,7 +315,8 @@ bool qrcp_grid_run(tt_ctx ctx, double* Y, int64_t ldy, int64_t m, int64_t c, int
   int per_sm = 0;
   TTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_grid_kernel, QG_T, smem));
   if (per_sm < 1) return false;
-  per_sm = std::min(per_sm, 4);
+  static const char* ps_env = std::getenv("TT_B200_QG_PERSM");
+  per_sm = std::min(per_sm, ps_env ? std::max(1, std::atoi(ps_env)) : 4);
   const int G = ctx->num_sms * per_sm;
   const int64_t nwg = (int64_t)G * QG_W;
   // rows per chunk: about two (column, chunk) pairs per warp, 128-row multiples, 128..4096

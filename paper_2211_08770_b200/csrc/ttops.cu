@@ -2,7 +2,9 @@
 // batched TT inner products, elements X_1(i_1)...X_d(i_d),
 // norms and small helpers.
 #include <algorithm>
+#include <cstdlib>
 
+#include "gemm.cuh"
 #include "ttops.cuh"
 
 namespace ttb {
@@ -278,8 +280,111 @@ void lincomb(tt_ctx ctx, const std::vector<const double*>& xs, const std::vector
   }
 }
 
+namespace {
+
+__global__ void dot_init_kernel(double* W, int64_t wcap, int P) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < P) W[(int64_t)p * wcap] = 1.0;
+}
+__global__ void dot_out_kernel(const double* W, int64_t wcap, int P, double* out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < P) out[p] = W[(int64_t)p * wcap];
+}
+// traces[p (d+1) + k + 1] = trace(W_p) (rx1 x ry1, ld rx1), one warp per pair
+__global__ void dot_trace_kernel(const double* W, int64_t wcap, const int64_t* __restrict__ xr,
+                                 const int64_t* __restrict__ yr, int d, int k, int P, double* traces) {
+  const int p = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (p >= P) return;
+  const int64_t rx1 = xr[(int64_t)p * (d + 1) + k + 1], ry1 = yr[(int64_t)p * (d + 1) + k + 1];
+  const int64_t nd = rx1 < ry1 ? rx1 : ry1;
+  double t = 0.0;
+  for (int64_t a = lane; a < nd; a += 32) t += W[(int64_t)p * wcap + a + a * rx1];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) {
+    traces[(int64_t)p * (d + 1) + k + 1] = t;
+    if (k == 0) traces[(int64_t)p * (d + 1)] = 1.0;
+  }
+}
+
+}  // namespace
+
+// Large ranks: the per-core recursion of every pair as two grouped DMMA GEMMs per core (gemm.cu),
+// W (rx_k x ry_k, column-major) -> S^T = X_k^T W  (rows (i, a'), columns b: M = n rx1, K = rx0,
+// N = ry0) -> W' = S Y_k with K = (b, i) (M = rx1, N = ry1): both products read the cores in
+// place (no transposes), O(n rx ry (rx + ry)) flops per core on the tensor pipe.
+void dot_batch_gemm(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev) {
+  const int d = b.d, P = b.P;
+  if (P <= 0) return;
+  BBuf dxr, dyr;
+  if (traces_dev) {
+    dxr.upload(ctx, b.xr.data(), sizeof(int64_t) * b.xr.size());
+    dyr.upload(ctx, b.yr.data(), sizeof(int64_t) * b.yr.size());
+  }
+  int64_t wcap = 1, scap = 1;
+  for (int p = 0; p < P; ++p)
+    for (int k = 0; k < d; ++k) {
+      const int64_t rx0 = b.xr[(size_t)p * (d + 1) + k], rx1 = b.xr[(size_t)p * (d + 1) + k + 1];
+      const int64_t ry0 = b.yr[(size_t)p * (d + 1) + k], ry1 = b.yr[(size_t)p * (d + 1) + k + 1];
+      wcap = std::max(wcap, std::max(rx0 * ry0, rx1 * ry1));
+      scap = std::max(scap, b.n[(size_t)k] * rx1 * ry0);
+    }
+  DBuf W(ctx, (size_t)P * wcap), S(ctx, (size_t)P * scap);
+  TTB_RUN(ctx, "aux", 0, 8.0 * P, dot_init_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(W.p, wcap, P));
+  std::vector<GemmDesc> g1, g2;
+  for (int k = 0; k < d; ++k) {
+    const int64_t n = b.n[(size_t)k];
+    g1.clear();
+    g2.clear();
+    for (int p = 0; p < P; ++p) {
+      const int64_t rx0 = b.xr[(size_t)p * (d + 1) + k], rx1 = b.xr[(size_t)p * (d + 1) + k + 1];
+      const int64_t ry0 = b.yr[(size_t)p * (d + 1) + k], ry1 = b.yr[(size_t)p * (d + 1) + k + 1];
+      const double* X = b.xc[(size_t)p * d + k];
+      const double* Y = b.yc[(size_t)p * d + k];
+      GemmDesc a;  // S^T (n rx1 x ry0, ld n rx1) = X^T (n rx1 x rx0, ld n rx1) W (rx0 x ry0, ld rx0)
+      a.M = n * rx1; a.N = ry0; a.K = rx0;
+      a.A = X; a.lda = n * rx1;
+      a.B = W.p + (int64_t)p * wcap; a.ldb = rx0;
+      a.C = S.p + (int64_t)p * scap; a.ldc = n * rx1;
+      g1.push_back(a);
+      GemmDesc c;  // W' (rx1 x ry1, ld rx1) = S (rx1 x (ry0 n), ld rx1) Y ((ry0 n) x ry1, stored ry1 x (ry0 n))
+      c.M = rx1; c.N = ry1; c.K = ry0 * n;
+      c.A = S.p + (int64_t)p * scap; c.lda = rx1;
+      c.B = Y; c.ldb = ry1; c.tb = true;
+      c.C = W.p + (int64_t)p * wcap; c.ldc = rx1;
+      g2.push_back(c);
+    }
+    gemm_grouped(ctx, g1);
+    gemm_grouped(ctx, g2);
+    if (traces_dev)
+      TTB_RUN(ctx, "aux", 0, 8.0 * P, dot_trace_kernel<<<(P + 7) / 8, 256, 0, ctx->stream>>>(
+                                           W.p, wcap, (const int64_t*)dxr.p, (const int64_t*)dyr.p, d, k, P, traces_dev));
+  }
+  TTB_RUN(ctx, "aux", 0, 16.0 * P, dot_out_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(W.p, wcap, P, out_dev));
+}
+
 void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev) {
   if (b.P <= 0) return;
+  static const bool pairwise = std::getenv("TT_B200_DOT_PAIRWISE") != nullptr;
+  // Route: per-core grouped DMMA GEMMs when a pair's recursion is long enough to amortise two
+  // launches per core (one CTA per pair runs at ~15 GFLOP/s; a grouped launch costs ~10 us):
+  // flops per pair > 0.3 MFLOP x d, or ranks beyond the one-CTA workspace (> 32).
+  int64_t rmax = 1;
+  double fl_pair = 0.0;
+  for (int p = 0; p < b.P; ++p) {
+    double f = 0.0;
+    for (int k = 0; k < b.d; ++k) {
+      const double rx0 = (double)b.xr[(size_t)p * (b.d + 1) + k], rx1 = (double)b.xr[(size_t)p * (b.d + 1) + k + 1];
+      const double ry0 = (double)b.yr[(size_t)p * (b.d + 1) + k], ry1 = (double)b.yr[(size_t)p * (b.d + 1) + k + 1];
+      f += 2.0 * b.n[(size_t)k] * (rx0 * ry0 * ry1 + rx0 * rx1 * ry1);
+    }
+    fl_pair = std::max(fl_pair, f);
+  }
+  for (int64_t v : b.xr) rmax = std::max(rmax, v);
+  for (int64_t v : b.yr) rmax = std::max(rmax, v);
+  if (!pairwise && (rmax > 32 || fl_pair > 0.3e6 * b.d)) {
+    dot_batch_gemm(ctx, b, out_dev, traces_dev);
+    return;
+  }
   const int d = b.d;
   int64_t wcap = 1, tcap = 1;
   for (int p = 0; p < b.P; ++p)

@@ -43,6 +43,8 @@ struct DotBatch {
 // traces_dev (optional, P*(d+1)): for x == y pairs, trace(W_k) = ||left part of x through
 // core k||_F^2 after every core (entry 0 = 1).
 void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev = nullptr);
+// Same dots through grouped DMMA GEMMs per core (dot_batch takes this route above rank 32).
+void dot_batch_gemm(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev = nullptr);
 // Elements x(i_1..i_d) for 0-based multi-indices idx[t*d + k].
 void elements(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<const double*>& core,
               const std::vector<int64_t>& r, const std::vector<int64_t>& idx, int nidx, double* out_dev);

@@ -80,6 +80,22 @@ def test_dot_batch_two_rank_profiles_gram_route():
         assert abs(got[q] - tt.tt_dot(a, b)) <= 1e-12 * tt.tt_norm(a) * tt.tt_norm(b), q
 
 
+def test_dot_batch_large_ranks_gemm_route():
+    """Ranks above 32 (unequal profiles) take the per-core grouped DMMA GEMM route: several pairs with different
+    rank profiles (and a pair of small x against large y)."""
+    import paper_2211_08770_b200 as P
+    c = ctx()
+    rng = _rng(6)
+    d, n = 4, [5, 3, 4, 6]
+    xs = [make_random_tt(d, n, [1, 5, 15, 60, 1], rng), make_random_tt(d, n, [1, 3, 9, 6, 1], rng),
+          make_random_tt(d, n, [1, 5, 14, 49, 1], rng)]
+    ys = [make_random_tt(d, n, [1, 5, 15, 55, 1], rng), make_random_tt(d, n, [1, 5, 15, 70, 1], rng),
+          make_random_tt(d, n, [1, 4, 12, 20, 1], rng)]
+    got = P.tt_dot_batch(c, [dev(x) for x in xs], [dev(y) for y in ys]).cpu().numpy()
+    for q in range(3):
+        assert abs(got[q] - tt.tt_dot(xs[q], ys[q])) <= 1e-12 * tt.tt_norm(xs[q]) * tt.tt_norm(ys[q]), q
+
+
 def test_dot_large_rank_global_path():
     """Ranks large enough that the per-pair workspace leaves shared memory."""
     import paper_2211_08770_b200 as P
