@@ -1,4 +1,6 @@
 // Truncated SVD for the left-to-right TT-rounding sweep (FP64, sm_100a).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -100,6 +102,91 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const double* __res
   }
 }
 
+// The same Jacobi over the whole GPU for large k (C5: k ~ 1000, where one CTA would take
+// seconds per SVD): cooperative launch, the k/2 disjoint pairs of a round dealt one per warp
+// over the grid, one grid barrier per round; A and V in global memory (L2-resident).  Same
+// ordering, threshold and rotation formulas as jacobi_kernel, so the result is identical.
+constexpr int JG_T = 256;
+__global__ void __launch_bounds__(JG_T) jacobi_grid_kernel(const double* __restrict__ Ain, int64_t lda, int rows,
+                                                           int k, double* A, double* V, double* nrm, int* flags,
+                                                           double* Ug, double* Vg, double* sig, int* info) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * JG_T + threadIdx.x, nth = (int64_t)gridDim.x * JG_T;
+  const int gw = (int)(gtid >> 5), nwg = (int)(nth >> 5);
+  for (int64_t idx = gtid; idx < (int64_t)rows * k; idx += nth) {
+    const int64_t c = idx / rows, r = idx % rows;
+    A[idx] = Ain[r + c * lda];
+  }
+  for (int64_t idx = gtid; idx < (int64_t)k * k; idx += nth) V[idx] = (idx % k == idx / k) ? 1.0 : 0.0;
+  grid.sync();
+  const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
+  const int kk = k + (k & 1);
+  int sweep = 0;
+  bool conv = (k < 2);
+  for (; sweep < JAC_MAX_SWEEPS && !conv; ++sweep) {
+    for (int r = 0; r < kk - 1; ++r) {
+      for (int q = gw; q < kk / 2; q += nwg) {
+        int a, b;
+        if (q == 0) { a = kk - 1; b = r; }
+        else { a = (r + q) % (kk - 1); b = (r + kk - 1 - q) % (kk - 1); }
+        if (a >= k || b >= k) continue;
+        if (a > b) { const int t = a; a = b; b = t; }
+        double* ca = A + (int64_t)a * rows;
+        double* cb = A + (int64_t)b * rows;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < rows; i += 32) {
+          const double x = ca[i], y = cb[i];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int i = lane; i < rows; i += 32) {
+            const double x = ca[i], y = cb[i];
+            ca[i] = c * x - s * y;
+            cb[i] = s * x + c * y;
+          }
+          double* va = V + (int64_t)a * k;
+          double* vb = V + (int64_t)b * k;
+          for (int i = lane; i < k; i += 32) {
+            const double x = va[i], y = vb[i];
+            va[i] = c * x - s * y;
+            vb[i] = s * x + c * y;
+          }
+          if (lane == 0) flags[sweep] = 1;
+        }
+      }
+      grid.sync();
+    }
+    conv = (flags[sweep] == 0);  // read after the sweep's last barrier: the same in every thread
+  }
+  if (gtid == 0) *info = conv ? 0 : 1;
+  for (int j = gw; j < k; j += nwg) {
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32) { const double x = A[(int64_t)j * rows + i]; s += x * x; }
+    s = warp_sum(s);
+    if (lane == 0) nrm[j] = sqrt(s);
+  }
+  grid.sync();
+  for (int j = gw; j < k; j += nwg) {  // one warp per column: rank, then U and V columns
+    const double v = nrm[j];
+    int rank = 0;
+    for (int i = lane; i < k; i += 32) {
+      const double w = nrm[i];
+      if (w > v || (w == v && i < j)) ++rank;
+    }
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0) sig[rank] = v;
+    const double inv = v > 0.0 ? 1.0 / v : 0.0;
+    for (int i = lane; i < rows; i += 32) Ug[(int64_t)rank * rows + i] = A[(int64_t)j * rows + i] * inv;
+    for (int i = lane; i < k; i += 32) Vg[(int64_t)rank * k + i] = V[(int64_t)j * k + i];
+  }
+}
+
 // SV[j, perm[i]] = sigma[j] * B[i + j ldb]   (SV row-major rho x c)
 __global__ void scale_unpermute_kernel(const double* __restrict__ B, int64_t ldb, const double* __restrict__ sigma,
                                        const int* __restrict__ perm, int c, int rho, double* SV) {
@@ -115,6 +202,31 @@ __global__ void scale_unpermute_kernel(const double* __restrict__ B, int64_t ldb
 void jacobi_svd(tt_ctx ctx, const double* A, int64_t lda, int64_t rows, int64_t k, double* U, double* V,
                 double* sigma) {
   if (k <= 0) return;
+  if (k >= 128) {  // whole-GPU Jacobi
+    int per_sm = 0;
+    TTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, JG_T, 0));
+    if (per_sm >= 1) {
+      const int kk = (int)(k + (k & 1));
+      const int G = std::max(1, std::min(ctx->num_sms * per_sm, (kk / 2 + JG_T / 32 - 1) / (JG_T / 32)));
+      DBuf work(ctx, (size_t)(rows * k + k * k + k));
+      IBuf flags(ctx, (size_t)JAC_MAX_SWEEPS + 1);
+      TTB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (JAC_MAX_SWEEPS + 1), ctx->stream));
+      double* Aw = work.p;
+      double* Vw = work.p + rows * k;
+      double* nw = Vw + k * k;
+      int* fl = flags.p;
+      int* inf = flags.p + JAC_MAX_SWEEPS;
+      int ri = (int)rows, ki = (int)k;
+      void* args[] = {(void*)&A, (void*)&lda, &ri, &ki, &Aw, &Vw, &nw, &fl, &U, &V, &sigma, &inf};
+      TTB_RUN(ctx, "jacobi_svd", 0, 16.0 * rows * k,
+              TTB_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_grid_kernel, dim3(G), dim3(JG_T), args, 0,
+                                                   ctx->stream)));
+      int h = 0;
+      d2h_small_int(ctx, &h, inf, 1);
+      if (h != 0) fail(TT_ENOCONV, "one-sided Jacobi SVD did not converge in " + std::to_string(JAC_MAX_SWEEPS) + " sweeps");
+      return;
+    }
+  }
   const size_t need = sizeof(double) * (size_t)(rows * k + k * k + k);
   int use_smem = need <= 200 * 1024;
   DBuf work;

@@ -282,23 +282,23 @@ void lincomb(tt_ctx ctx, const std::vector<const double*>& xs, const std::vector
 
 namespace {
 
-__global__ void dot_init_kernel(double* W, int64_t wcap, int P) {
+__global__ void dot_init_kernel(double* W, const int64_t* __restrict__ wo, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < P) W[(int64_t)p * wcap] = 1.0;
+  if (p < P) W[wo[p]] = 1.0;
 }
-__global__ void dot_out_kernel(const double* W, int64_t wcap, int P, double* out) {
+__global__ void dot_out_kernel(const double* W, const int64_t* __restrict__ wo, int P, double* out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < P) out[p] = W[(int64_t)p * wcap];
+  if (p < P) out[p] = W[wo[p]];
 }
 // traces[p (d+1) + k + 1] = trace(W_p) (rx1 x ry1, ld rx1), one warp per pair
-__global__ void dot_trace_kernel(const double* W, int64_t wcap, const int64_t* __restrict__ xr,
+__global__ void dot_trace_kernel(const double* W, const int64_t* __restrict__ wo, const int64_t* __restrict__ xr,
                                  const int64_t* __restrict__ yr, int d, int k, int P, double* traces) {
   const int p = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
   if (p >= P) return;
   const int64_t rx1 = xr[(int64_t)p * (d + 1) + k + 1], ry1 = yr[(int64_t)p * (d + 1) + k + 1];
   const int64_t nd = rx1 < ry1 ? rx1 : ry1;
   double t = 0.0;
-  for (int64_t a = lane; a < nd; a += 32) t += W[(int64_t)p * wcap + a + a * rx1];
+  for (int64_t a = lane; a < nd; a += 32) t += W[wo[p] + a + a * rx1];
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) {
     traces[(int64_t)p * (d + 1) + k + 1] = t;
@@ -315,51 +315,80 @@ __global__ void dot_trace_kernel(const double* W, int64_t wcap, const int64_t* _
 void dot_batch_gemm(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev) {
   const int d = b.d, P = b.P;
   if (P <= 0) return;
-  BBuf dxr, dyr;
-  if (traces_dev) {
-    dxr.upload(ctx, b.xr.data(), sizeof(int64_t) * b.xr.size());
-    dyr.upload(ctx, b.yr.data(), sizeof(int64_t) * b.yr.size());
-  }
-  int64_t wcap = 1, scap = 1;
-  for (int p = 0; p < P; ++p)
+  // per-pair workspace: W (max rx_k ry_k) and S^T (max n_k rx_{k+1} ry_k), exact offsets; pairs
+  // are processed in groups of <= 2 GiB of workspace
+  std::vector<int64_t> wsz((size_t)P), ssz((size_t)P);
+  for (int p = 0; p < P; ++p) {
+    int64_t w = 1, sc = 1;
     for (int k = 0; k < d; ++k) {
       const int64_t rx0 = b.xr[(size_t)p * (d + 1) + k], rx1 = b.xr[(size_t)p * (d + 1) + k + 1];
       const int64_t ry0 = b.yr[(size_t)p * (d + 1) + k], ry1 = b.yr[(size_t)p * (d + 1) + k + 1];
-      wcap = std::max(wcap, std::max(rx0 * ry0, rx1 * ry1));
-      scap = std::max(scap, b.n[(size_t)k] * rx1 * ry0);
+      w = std::max(w, std::max(rx0 * ry0, rx1 * ry1));
+      sc = std::max(sc, b.n[(size_t)k] * rx1 * ry0);
     }
-  DBuf W(ctx, (size_t)P * wcap), S(ctx, (size_t)P * scap);
-  TTB_RUN(ctx, "aux", 0, 8.0 * P, dot_init_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(W.p, wcap, P));
-  std::vector<GemmDesc> g1, g2;
-  for (int k = 0; k < d; ++k) {
-    const int64_t n = b.n[(size_t)k];
-    g1.clear();
-    g2.clear();
-    for (int p = 0; p < P; ++p) {
-      const int64_t rx0 = b.xr[(size_t)p * (d + 1) + k], rx1 = b.xr[(size_t)p * (d + 1) + k + 1];
-      const int64_t ry0 = b.yr[(size_t)p * (d + 1) + k], ry1 = b.yr[(size_t)p * (d + 1) + k + 1];
-      const double* X = b.xc[(size_t)p * d + k];
-      const double* Y = b.yc[(size_t)p * d + k];
-      GemmDesc a;  // S^T (n rx1 x ry0, ld n rx1) = X^T (n rx1 x rx0, ld n rx1) W (rx0 x ry0, ld rx0)
-      a.M = n * rx1; a.N = ry0; a.K = rx0;
-      a.A = X; a.lda = n * rx1;
-      a.B = W.p + (int64_t)p * wcap; a.ldb = rx0;
-      a.C = S.p + (int64_t)p * scap; a.ldc = n * rx1;
-      g1.push_back(a);
-      GemmDesc c;  // W' (rx1 x ry1, ld rx1) = S (rx1 x (ry0 n), ld rx1) Y ((ry0 n) x ry1, stored ry1 x (ry0 n))
-      c.M = rx1; c.N = ry1; c.K = ry0 * n;
-      c.A = S.p + (int64_t)p * scap; c.lda = rx1;
-      c.B = Y; c.ldb = ry1; c.tb = true;
-      c.C = W.p + (int64_t)p * wcap; c.ldc = rx1;
-      g2.push_back(c);
-    }
-    gemm_grouped(ctx, g1);
-    gemm_grouped(ctx, g2);
-    if (traces_dev)
-      TTB_RUN(ctx, "aux", 0, 8.0 * P, dot_trace_kernel<<<(P + 7) / 8, 256, 0, ctx->stream>>>(
-                                           W.p, wcap, (const int64_t*)dxr.p, (const int64_t*)dyr.p, d, k, P, traces_dev));
+    wsz[(size_t)p] = (w + 1) & ~int64_t(1);  // 16-byte aligned blocks
+    ssz[(size_t)p] = (sc + 1) & ~int64_t(1);
   }
-  TTB_RUN(ctx, "aux", 0, 16.0 * P, dot_out_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(W.p, wcap, P, out_dev));
+  const int64_t budget = (int64_t)1 << 28;  // doubles (2 GiB)
+  std::vector<GemmDesc> g1, g2;
+  for (int p0 = 0; p0 < P;) {
+    int p1 = p0;
+    int64_t wt = 0, st = 0;
+    while (p1 < P && (p1 == p0 || wt + st + wsz[(size_t)p1] + ssz[(size_t)p1] <= budget)) {
+      wt += wsz[(size_t)p1];
+      st += ssz[(size_t)p1];
+      ++p1;
+    }
+    const int Pg = p1 - p0;
+    std::vector<int64_t> wo((size_t)Pg), so((size_t)Pg);
+    int64_t a0 = 0, b0 = 0;
+    for (int q = 0; q < Pg; ++q) { wo[(size_t)q] = a0; so[(size_t)q] = b0; a0 += wsz[(size_t)(p0 + q)]; b0 += ssz[(size_t)(p0 + q)]; }
+    DBuf W(ctx, (size_t)wt), S(ctx, (size_t)st);
+    BBuf dxr, dyr;
+    if (traces_dev) {
+      dxr.upload(ctx, b.xr.data() + (size_t)p0 * (d + 1), sizeof(int64_t) * (size_t)Pg * (d + 1));
+      dyr.upload(ctx, b.yr.data() + (size_t)p0 * (d + 1), sizeof(int64_t) * (size_t)Pg * (d + 1));
+    }
+    BBuf dwo;
+    dwo.upload(ctx, wo.data(), sizeof(int64_t) * wo.size());
+    TTB_RUN(ctx, "aux", 0, 8.0 * Pg,  // W_0 = 1 (1 x 1) for every pair
+            dot_init_kernel<<<(Pg + 127) / 128, 128, 0, ctx->stream>>>(W.p, (const int64_t*)dwo.p, Pg));
+    for (int k = 0; k < d; ++k) {
+      const int64_t n = b.n[(size_t)k];
+      g1.clear();
+      g2.clear();
+      for (int q = 0; q < Pg; ++q) {
+        const int p = p0 + q;
+        const int64_t rx0 = b.xr[(size_t)p * (d + 1) + k], rx1 = b.xr[(size_t)p * (d + 1) + k + 1];
+        const int64_t ry0 = b.yr[(size_t)p * (d + 1) + k], ry1 = b.yr[(size_t)p * (d + 1) + k + 1];
+        const double* X = b.xc[(size_t)p * d + k];
+        const double* Y = b.yc[(size_t)p * d + k];
+        double* Wp = W.p + wo[(size_t)q];
+        double* Sp = S.p + so[(size_t)q];
+        GemmDesc a;  // S^T (n rx1 x ry0, ld n rx1) = X^T (n rx1 x rx0, ld n rx1) W (rx0 x ry0, ld rx0)
+        a.M = n * rx1; a.N = ry0; a.K = rx0;
+        a.A = X; a.lda = n * rx1;
+        a.B = Wp; a.ldb = rx0;
+        a.C = Sp; a.ldc = n * rx1;
+        g1.push_back(a);
+        GemmDesc c;  // W' (rx1 x ry1, ld rx1) = S (rx1 x (ry0 n), ld rx1) Y ((ry0 n) x ry1, stored ry1 x (ry0 n))
+        c.M = rx1; c.N = ry1; c.K = ry0 * n;
+        c.A = Sp; c.lda = rx1;
+        c.B = Y; c.ldb = ry1; c.tb = true;
+        c.C = Wp; c.ldc = rx1;
+        g2.push_back(c);
+      }
+      gemm_grouped(ctx, g1);
+      gemm_grouped(ctx, g2);
+      if (traces_dev)
+        TTB_RUN(ctx, "aux", 0, 8.0 * Pg, dot_trace_kernel<<<(Pg + 7) / 8, 256, 0, ctx->stream>>>(
+                                             W.p, (const int64_t*)dwo.p, (const int64_t*)dxr.p, (const int64_t*)dyr.p,
+                                             d, k, Pg, traces_dev + (int64_t)p0 * (d + 1)));
+    }
+    TTB_RUN(ctx, "aux", 0, 16.0 * Pg,
+            dot_out_kernel<<<(Pg + 127) / 128, 128, 0, ctx->stream>>>(W.p, (const int64_t*)dwo.p, Pg, out_dev + p0));
+    p0 = p1;
+  }
 }
 
 void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev) {

@@ -161,3 +161,24 @@ def test_round_wide_panel_grid_qrcp():
         assert diff_norm(g, ref) <= 1e-10 * info.scale
     x = tt.tt_sum(terms, coeffs)
     assert diff_norm(x, g) <= 1e-10 * info.norm * (1 + 1e-8) + np.sqrt(d - 1) * info.tau
+
+
+def test_round_large_rank_grid_jacobi():
+    """Kept ranks >= 128 take the whole-GPU Jacobi (same rotations as the one-CTA kernel):
+    10 random rank-14 terms with n = (160, 8, 160) keep rank 140 on both bonds."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(80)
+    n = [160, 8, 160]
+    terms = [make_random_tt(3, n, [1, 14, 14, 1], rng) for _ in range(10)]
+    coeffs = [float(v) for v in rng.standard_normal(10)]
+    norms = [tt.tt_norm(t) for t in terms]
+    ref, info = rounding.tt_round_sum(terms, coeffs, 1e-10, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
+    out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-10)
+    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
+    assert min(out.ranks[1:-1]) >= 128
+    g = out.to_numpy()
+    if out.ranks == info.ranks:
+        assert diff_norm(g, ref) <= 1e-10 * info.scale
+    for k in range(2):
+        U = g[k].reshape(-1, g[k].shape[2])
+        assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-12
