@@ -152,6 +152,12 @@ TT_API tt_status tt_download(tt_ctx ctx, tt_tensor t, double* const* host_cores)
 TT_API tt_status tt_sum(tt_ctx ctx, int32_t K, const double* coeff, const tt_view* terms, tt_tensor* out);
 /* out = alpha x + y. */
 TT_API tt_status tt_axpy(tt_ctx ctx, double alpha, const tt_view* x, const tt_view* y, tt_tensor* out);
+/* y = A x for a TT-matrix A (the paper's Krylov workload: x_{j+1} = -Delta_d a_j).
+ * A: a view whose core k holds the operator core (ra_k, n_k, n_k, ra_{k+1}) row-major (row index
+ * i, then column index j, then ra_{k+1} fastest), passed with modes A->n[k] = n_k^2 (ESHAPE
+ * otherwise); x: DEVICE TT-vector with modes n_k.  out: new library tensor with ranks
+ * ra_k rx_k, cores Y_k((a, alpha), i, (b, beta)) = sum_j A_k(a, i, j, b) X_k(alpha, j, beta). */
+TT_API tt_status tt_matvec(tt_ctx ctx, const tt_view* A, const tt_view* x, tt_tensor* out);
 /* out_dev[p] = <x[p], y[p]> for p < P (PAPER.md:19 Euclidean dot through the contraction;
  * W_k = sum_i X_k(i)^T W_{k-1} Y_k(i)).  out_dev: DEVICE, P doubles. */
 TT_API tt_status tt_dot_batch(tt_ctx ctx, int32_t P, const tt_view* x, const tt_view* y, double* out_dev);

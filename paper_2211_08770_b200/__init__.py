@@ -12,10 +12,17 @@ from .api import (  # noqa: F401
     Context,
     DeviceTT,
     LibTT,
+    compression_gain,
+    compression_ratio,
+    krylov_set,
+    laplacian_cores,
+    storage_count,
+    ttm_device,
     tt_dot_batch,
     tt_element,
     tt_gram,
     tt_gram_blocks,
+    tt_matvec,
     tt_norm,
     tt_orth,
     tt_round,

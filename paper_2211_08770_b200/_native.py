@@ -21,7 +21,7 @@ KINDS = {"cgs": 0, "mgs": 1, "cgs2": 2, "mgs2": 3, "gram": 4, "householder": 5}
 EXPORTED = [
     "tt_ctx_create", "tt_ctx_destroy", "tt_ctx_set_stream", "tt_last_error", "tt_status_string",
     "tt_ctx_launch_count", "tt_ctx_sync", "tt_ctx_profile", "tt_ctx_profile_query", "tt_tensor_view", "tt_tensor_free", "tt_upload", "tt_download",
-    "tt_sum", "tt_axpy", "tt_dot_batch", "tt_gram", "tt_gram_blocks", "tt_element", "tt_norm",
+    "tt_sum", "tt_axpy", "tt_matvec", "tt_dot_batch", "tt_gram", "tt_gram_blocks", "tt_element", "tt_norm",
     "tt_round", "tt_round_batch", "tt_orth",
     "tt_round_batch_strided", "tt_batch_shape", "tt_batch_ranks", "tt_batch_view", "tt_batch_download", "tt_batch_arena", "tt_batch_free",
 ]
@@ -91,6 +91,7 @@ def load() -> C.CDLL:
         "tt_download": (C.c_int, [P, P, C.POINTER(P)]),
         "tt_sum": (C.c_int, [P, i32, C.POINTER(dbl), VP, C.POINTER(P)]),
         "tt_axpy": (C.c_int, [P, dbl, VP, VP, C.POINTER(P)]),
+        "tt_matvec": (C.c_int, [P, VP, VP, C.POINTER(P)]),
         "tt_dot_batch": (C.c_int, [P, i32, VP, VP, P]),
         "tt_gram": (C.c_int, [P, i32, VP, P]),
         "tt_gram_blocks": (C.c_int, [P, i32, VP, i32, C.POINTER(i32), P]),

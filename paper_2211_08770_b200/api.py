@@ -432,6 +432,68 @@ def tt_gram_blocks(ctx: Context, tensors, blocks: Sequence[Tuple[int, int, int, 
     return out[:total]
 
 
+def ttm_device(cores4: Sequence[np.ndarray], device="cuda") -> DeviceTT:
+    """A TT-matrix (operator cores (ra_k, n_k, n_k, ra_{k+1})) as the view tt_matvec takes:
+    core k reshaped to (ra_k, n_k^2, ra_{k+1}) (row index, then column index)."""
+    cs = [np.ascontiguousarray(c, dtype=np.float64) for c in cores4]
+    return DeviceTT.from_numpy([c.reshape(c.shape[0], c.shape[1] * c.shape[2], c.shape[3]) for c in cs], device)
+
+
+def tt_matvec(ctx: Context, A: DeviceTT, x) -> LibTT:
+    """y = A x (include/tt_b200.h tt_matvec)."""
+    va, ka = A._view()
+    vx, kx = x._view()
+    h = C.c_void_p()
+    ctx.check(ctx.lib.tt_matvec(ctx.handle, C.byref(va), C.byref(vx), C.byref(h)))
+    return LibTT(ctx, h)
+
+
+def laplacian_cores(d: int, n: int) -> List[np.ndarray]:
+    """-Delta_d (Dirichlet, unit mesh width: L = tridiag(-1, 2, -1); the 1/h^2 factor cancels in
+    the normalised Krylov set) as TT-matrix cores of ranks (1, 2, .., 2, 1): [L I],
+    [[I 0], [L I]], .., [I; L] (Kazeev 2012).  DESIGN.md readings A24-A26."""
+    L = np.diag(np.full(n, 2.0)) + np.diag(np.full(n - 1, -1.0), 1) + np.diag(np.full(n - 1, -1.0), -1)
+    E = np.identity(n)
+    if d == 1:
+        return [L[None, :, :, None]]
+    cores = [np.stack([L, E], axis=-1)[None]]                                  # (1, n, n, 2)
+    mid = np.zeros((2, n, n, 2))
+    mid[0, :, :, 0], mid[1, :, :, 0], mid[1, :, :, 1] = E, L, E
+    cores += [mid.copy() for _ in range(d - 2)]
+    cores.append(np.stack([E, L], axis=0)[..., None])                          # (2, n, n, 1)
+    return cores
+
+
+def krylov_set(ctx: Context, d: int, n: int, m: int) -> List[LibTT]:
+    """The paper's input sets: a_1 = ones / ||ones||, a_{j+1} = the normalised
+    rank-1 TT-rounding (accuracy replaced by maximum rank 1, floor off) of -Delta_d a_j."""
+    A = ttm_device(laplacian_cores(d, n), device=f"cuda:{ctx.device}")
+    x = DeviceTT.from_numpy([np.ones((1, n, 1)) for _ in range(d)], device=f"cuda:{ctx.device}")
+    out: List[LibTT] = []
+    for _ in range(m):
+        r, _ = tt_round(ctx, [x], [1.0], 0.0, floor_c=0.0, max_rank=1)
+        a = tt_sum(ctx, [r], [1.0 / tt_norm(ctx, r)])  # ||round(x)|| (< ||x|| after truncation)
+        a.norm = 1.0
+        out.append(a)
+        x = tt_matvec(ctx, A, a)
+    return out
+
+
+def storage_count(ranks: Sequence[int], modes: Sequence[int]) -> int:
+    """Numerator of Eq. (1): sum_k r_{k-1} n_k r_k."""
+    return int(sum(ranks[k] * modes[k] * ranks[k + 1] for k in range(len(modes))))
+
+
+def compression_ratio(ranks: Sequence[int], modes: Sequence[int]) -> float:
+    """Eq. (1): TT storage over dense storage."""
+    return storage_count(ranks, modes) / float(np.prod(np.asarray(modes, dtype=np.float64)))
+
+
+def compression_gain(ranks_before: Sequence[int], ranks_after: Sequence[int], modes: Sequence[int]) -> float:
+    """Eq. (2): ratio of the compression ratios of x and of its rounding."""
+    return storage_count(ranks_before, modes) / float(storage_count(ranks_after, modes))
+
+
 def tt_element(ctx: Context, x, lin_idx: Sequence[int]) -> torch.Tensor:
     out = torch.empty(len(lin_idx), dtype=torch.float64, device=f"cuda:{ctx.device}")
     v, keep = x._view()

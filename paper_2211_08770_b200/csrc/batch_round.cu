@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
 // round-robin pair ordering, one warp per pair; V (nc x nc) in sm.Aux.  On return
 // sm.sig[j] = j-th largest singular value, sm.perm[j] = its column; returns false on
 // non-convergence (|<c_i,c_j>| <= sqrt(rows) u ||c_i|| ||c_j||).
-__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
+__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, long long* nsweeps = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
   const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
@@ -776,6 +776,7 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc) {
       __syncthreads();
     }
     conv = (sm.flag == 0);
+    if (nsweeps && tid == 0) *nsweeps += 1;
     __syncthreads();
   }
   // singular values = column norms, sorted descending (ties: lower column first)
@@ -898,7 +899,7 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Rs[idx] = jm[idx];
   __syncthreads();
   const long long cj0 = clock64();
-  const bool conv = br_jacobi(sm, jrows, cp);
+  const bool conv = br_jacobi(sm, jrows, cp, (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[8] += clock64() - cj0;
   if (tid == 0) {
     if (!conv) A.info[b] = 1;
@@ -1272,8 +1273,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         long long h[32];
         TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         TTB_CUDA(cudaStreamSynchronize(ctx->stream));
-        std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld outcore %lld nextcore %lld (cycles, CTA 0) | qr steps: owner(w0) %lld x%lld, pre-barrier(w0 not owner) %lld, barrier %lld, update %lld\n",
-                     h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[9], h[10], h[16], h[19], h[20], h[17], h[18]);
+        std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld (%lld sweeps) outcore %lld nextcore %lld (cycles, CTA 0) | qr steps: owner(w0) %lld x%lld, pre-barrier(w0 not owner) %lld, barrier %lld, update %lld\n",
+                     h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[11], h[9], h[10], h[16], h[19], h[20], h[17], h[18]);
       }
       // ranks (the one host synchronisation of the wave), then compaction
       std::vector<int> hr((size_t)nb * (d + 1)), hinf((size_t)nb);

@@ -199,6 +199,19 @@ tt_status tt_axpy(tt_ctx ctx, double alpha, const tt_view* x, const tt_view* y, 
   return tt_sum(ctx, 2, c, t, out);
 }
 
+tt_status tt_matvec(tt_ctx ctx, const tt_view* A, const tt_view* x, tt_tensor* out) {
+  if (!ctx || !A || !x || !out) return TT_EINVAL;
+  return guarded(ctx, [&] {
+    TTShape sa = view_shape(*A), sx = view_shape(*x);
+    if (sa.d != sx.d) fail(TT_ESHAPE, "tt_matvec: operator and vector orders differ");
+    for (int k = 0; k < sx.d; ++k)
+      if (sa.n[(size_t)k] != sx.n[(size_t)k] * sx.n[(size_t)k])
+        fail(TT_ESHAPE, "tt_matvec: operator core k must have n_k^2 modes (n_k x n_k blocks)");
+    std::vector<const double*> ac(A->core, A->core + A->d), xc(x->core, x->core + x->d);
+    *out = matvec(ctx, sx.d, sx.n, sa.r, ac, sx.r, xc);
+  });
+}
+
 tt_status tt_dot_batch(tt_ctx ctx, int32_t P, const tt_view* x, const tt_view* y, double* out_dev) {
   if (!ctx || P < 0 || (P > 0 && (!x || !y || !out_dev))) return TT_EINVAL;
   return guarded(ctx, [&] {

@@ -282,6 +282,49 @@ void lincomb(tt_ctx ctx, const std::vector<const double*>& xs, const std::vector
 
 namespace {
 
+// Y_k((a, alpha), i, (b, beta)) = sum_j A_k(a, i, j, b) X_k(alpha, j, beta): one thread per output
+// element (a short sum over the n column indices; the operator cores are tiny and L1-resident).
+__global__ void matvec_core_kernel(const double* __restrict__ Ak, const double* __restrict__ Xk, int ra0, int ra1,
+                                   int rx0, int rx1, int n, double* __restrict__ Yk) {
+  const int64_t r1 = (int64_t)ra1 * rx1;
+  const int64_t total = (int64_t)ra0 * rx0 * n * r1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c1 = idx % r1, t = idx / r1;
+    const int i = (int)(t % n);
+    const int64_t c0 = t / n;
+    const int a = (int)(c0 / rx0), al = (int)(c0 % rx0), b = (int)(c1 / rx1), be = (int)(c1 % rx1);
+    const double* ap = Ak + (((int64_t)a * n + i) * n) * ra1 + b;  // A_k(a, i, j, b), j stride ra1
+    const double* xp = Xk + (int64_t)al * n * rx1 + be;             // X_k(alpha, j, beta), j stride rx1
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += ap[(int64_t)j * ra1] * xp[(int64_t)j * rx1];
+    Yk[idx] = s;
+  }
+}
+
+}  // namespace
+
+tt_tensor matvec(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& ra,
+                 const std::vector<const double*>& acore, const std::vector<int64_t>& rx,
+                 const std::vector<const double*>& xcore) {
+  std::vector<int64_t> ry((size_t)d + 1);
+  for (int k = 0; k <= d; ++k) ry[(size_t)k] = ra[(size_t)k] * rx[(size_t)k];
+  tt_tensor y = tensor_alloc(ctx, d, n, ry);
+  for (int k = 0; k < d; ++k) {
+    const int64_t total = ry[(size_t)k] * n[(size_t)k] * ry[(size_t)k + 1];
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 4096));
+    TTB_RUN(ctx, "tt_matvec", 2.0 * total * n[(size_t)k],
+            8.0 * (total + ra[(size_t)k] * n[(size_t)k] * n[(size_t)k] * ra[(size_t)k + 1] +
+                   rx[(size_t)k] * n[(size_t)k] * rx[(size_t)k + 1]),
+            matvec_core_kernel<<<blocks, 256, 0, ctx->stream>>>(
+                acore[(size_t)k], xcore[(size_t)k], (int)ra[(size_t)k], (int)ra[(size_t)k + 1], (int)rx[(size_t)k],
+                (int)rx[(size_t)k + 1], (int)n[(size_t)k], y->core[(size_t)k]));
+  }
+  return y;
+}
+
+namespace {
+
 __global__ void dot_init_kernel(double* W, const int64_t* __restrict__ wo, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < P) W[wo[p]] = 1.0;

@@ -43,6 +43,11 @@ struct DotBatch {
 // traces_dev (optional, P*(d+1)): for x == y pairs, trace(W_k) = ||left part of x through
 // core k||_F^2 after every core (entry 0 = 1).
 void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev = nullptr);
+// y = A x for a TT-matrix A (cores (ra_k, n_k, n_k, ra_{k+1}), row index then column index) and
+// a TT-vector x: a new tensor with ranks ra_k rx_k (the Krylov workload).
+tt_tensor matvec(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& ra,
+                 const std::vector<const double*>& acore, const std::vector<int64_t>& rx,
+                 const std::vector<const double*>& xcore);
 // Same dots through grouped DMMA GEMMs per core (dot_batch takes this route above rank 32).
 void dot_batch_gemm(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev = nullptr);
 // Elements x(i_1..i_d) for 0-based multi-indices idx[t*d + k].
