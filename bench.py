@@ -365,6 +365,23 @@ def main():
         extras["drivers_c2"] = {"workload": "C2 (configs[1]) TT-MGS + TT-MGS2, m=30, d=8, n=32, r=10",
                                 "roundings": calls, "ms": e0.elapsed_time(e1),
                                 "roundings_per_s": calls / (e0.elapsed_time(e1) * 1e-3)}
+        # the paper's own workload (Section 3, experiment 1): Krylov TT-Laplacian set
+        # d=3, n=15, m=20, five schemes (Gram breaks down on it) at delta=1e-5, floor off
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        K1 = P.krylov_set(ctx, 3, 15, 20)
+        kcalls, kloo = 0, {}
+        for kind in ("cgs", "mgs", "cgs2", "mgs2", "householder"):
+            _, _, rk = P.tt_orth(ctx, kind, K1, 1e-5, floor_c=0.0, want_loo=True)
+            kcalls += rk["rounding_calls"]
+            kloo[kind] = float(rk["loo_per_step"][-1])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        extras["krylov_exp1"] = {"workload": "PAPER.md Sec. 3 experiment 1: Krylov TT-Laplacian set d=3, n=15, m=20 "
+                                             "(rank-1 rounded), CGS/MGS/CGS2/MGS2/Householder at delta=1e-5, floor off",
+                                 "roundings": kcalls, "ms": e0.elapsed_time(e1),
+                                 "roundings_per_s": kcalls / (e0.elapsed_time(e1) * 1e-3), "loo_last": kloo}
 
     if rank == 0:
         line = {
