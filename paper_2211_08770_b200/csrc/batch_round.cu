@@ -91,6 +91,7 @@ struct BRArgs {
   double rel_tol, floor_c;
   int64_t max_rank;
   int keep_all;
+  int jac_t;                   // tall splits: one-sided Jacobi on R_Y^T (rows of R) instead of R_Y
   int item0;                   // global index of this wave's first item
   long long* dbg;              // TT_B200_BR_DEBUG: CTA 0 phase cycle counters (else null)
 };
@@ -703,7 +704,12 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
 // round-robin pair ordering, one warp per pair; V (nc x nc) in sm.Aux.  On return
 // sm.sig[j] = j-th largest singular value, sm.perm[j] = its column; returns false on
 // non-convergence (|<c_i,c_j>| <= sqrt(rows) u ||c_i|| ||c_j||).
-__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, long long* nsweeps = nullptr) {
+// Pairs whose columns both have squared norm <= tail2 (tail2 = tau^2 / nc: even all such columns
+// together lie inside the truncation tail) are not rotated: their mutual orthogonality is never
+// used.  The big-small pairs still converge, so the small columns span the orthogonal
+// complement of the kept subspace and their squared norms sum to the exact tail mass: the rank
+// decision, U_rho and S V^T are those of the full Jacobi.
+__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail2, long long* nsweeps = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
   const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
@@ -753,7 +759,8 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, long long* 
         be += __shfl_xor_sync(0xffffffffu, be, o);
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
       }
-      const bool rot = act && ga != 0.0 && al > negl && be > negl && fabs(ga) > tol * sqrt(al * be);
+      const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tail2 || be > tail2) &&
+                       fabs(ga) > tol * sqrt(al * be);
       if (rot) {
         // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga), with one
         // division: t = 2 ga sign(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2))
@@ -896,10 +903,18 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   const bool tall = p > BR_C;
   const int jrows = tall ? cp : (int)p;
   const double* jm = A.JM + (int64_t)b * BR_C * BR_C;
-  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Rs[idx] = jm[idx];
+  // Tall splits: Jacobi on X = R_Y^T (R_Y = W S V^T  <=>  X = V S W^T): the accumulated rotations
+  // are R_Y's left singular vectors W (what Q_Y is applied to), the rotated columns are V S
+  // (the next core's target, no division) -- and the rows of the triangular factor converge in
+  // fewer sweeps than its columns.
+  const bool jt = tall && A.jac_t;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T)
+    sm.Rs[idx] = jt ? jm[(idx % BR_C) * BR_C + idx / BR_C] : jm[idx];
   __syncthreads();
   const long long cj0 = clock64();
-  const bool conv = br_jacobi(sm, jrows, cp, (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
+  static_assert(BR_C == 64, "tail2 below assumes nc <= 64");
+  const double tail2 = (A.keep_all || A.max_rank > 0) ? 0.0 : sc[1] * sc[1] / (double)(cp > 0 ? cp : 1);
+  const bool conv = br_jacobi(sm, jrows, cp, tail2, (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[8] += clock64() - cj0;
   if (tid == 0) {
     if (!conv) A.info[b] = 1;
@@ -928,16 +943,20 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   // Q_Y's reflectors; W = V_rho S_rho^-1 goes to the first target slot.
   const bool use_gemm = tall && sm.sig[rho - 1] >= 1e-3 * sm.sig[0];
   if (tid == 0) A.gemm[b] = use_gemm ? 1 : 0;
-  if (use_gemm) {
+  if (use_gemm) {  // V_rho S^-1
     for (int idx = tid; idx < BR_C * rho; idx += BR_T) {
       const int col = idx / BR_C, row = idx % BR_C;
-      tt[idx] = row < cp ? sm.Aux[sm.perm[col] * BR_C + row] / sm.sig[col] : 0.0;
+      const double sg = sm.sig[col];
+      tt[idx] = row < cp ? (jt ? sm.Rs[sm.perm[col] * BR_C + row] / (sg * sg) : sm.Aux[sm.perm[col] * BR_C + row] / sg)
+                         : 0.0;
     }
   } else if (tall) {  // U_rho (cp x rho), the target of Q_Y
     for (int idx = tid; idx < BR_C * rho; idx += BR_T) {
       const int col = idx / BR_C, row = idx % BR_C;
       const double sg = sm.sig[col];
-      tt[idx] = (sg > 0.0 && row < cp) ? sm.Rs[sm.perm[col] * BR_C + row] / sg : 0.0;
+      tt[idx] = row >= cp ? 0.0
+                          : jt ? sm.Aux[sm.perm[col] * BR_C + row]
+                               : (sg > 0.0 ? sm.Rs[sm.perm[col] * BR_C + row] / sg : 0.0);
     }
   } else {  // short Y_k: output core k = U_rho directly ((rho_{k-1} n_k) x rho, row-major)
     double* ok = A.out + (int64_t)b * S->ostride + S->ooff[kc];
@@ -949,7 +968,9 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   }
   for (int idx = tid; idx < BR_C * rho; idx += BR_T) {  // V_rho S (cp x rho), the target of H_{k+1}
     const int col = idx / BR_C, row = idx % BR_C;
-    tt[BR_C * BR_C + idx] = row < cp ? sm.Aux[sm.perm[col] * BR_C + row] * sm.sig[col] : 0.0;
+    tt[BR_C * BR_C + idx] = row >= cp ? 0.0
+                                      : jt ? sm.Rs[sm.perm[col] * BR_C + row]
+                                           : sm.Aux[sm.perm[col] * BR_C + row] * sm.sig[col];
   }
 }
 
@@ -1245,6 +1266,10 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       a.floor_c = o.floor_c;
       a.max_rank = o.max_rank;
       a.keep_all = keep_all ? 1 : 0;
+      {
+        static const char* jt = std::getenv("TT_B200_BR_JACT");
+        a.jac_t = (jt && jt[0] == '0') ? 0 : 1;
+      }
       a.item0 = w0;
       const char* dbe = std::getenv("TT_B200_BR_DEBUG");
       LBuf dbg;
