@@ -45,7 +45,9 @@ struct GramShape {  // modes and the rank profiles of the I-side (r) and J-side 
 // Warp p = 2 i + j keeps W's A fragments in registers for the whole core and V in DMMA
 // accumulators; per mode slice s it forms U = W X^(j)(s) (NT x NT 8x8 tiles, K = R0) into its own
 // shared block and then V += X^(i)(s)^T U -- no cross-warp dependency inside a slice, one
-// __syncthreads per slice for the staged slices (cp.async, double buffered).  One warp per SM
+// __syncthreads per slice for the staged slices (cp.async from a per-core copy list in shared
+// memory: one 16-byte copy per list entry and thread, no per-copy index arithmetic; double
+// buffered, the next core's first slice prefetched during the last slice of the current one).  One warp per SM
 // sub-partition with >= 2 independent accumulators saturates the DMMA pipe (tools/dmma_bench:
 // latency 26 cycles, 16 cycles per DMMA per sub-partition), so 9 accumulators per warp leave the
 // pipe the only limit.  Ranks are padded to 8 NT with zeros; the row stride L = 4 or 12 (mod 16)
@@ -58,27 +60,6 @@ __device__ __forceinline__ void gmma(double& c0, double& c1, double a, double b)
 
 constexpr int GM_T = 128;  // threads per CTA: one warp per pair
 
-// 1-D bulk copies global -> shared (TMA engine) completing on an mbarrier
-__device__ __forceinline__ uint32_t g_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void g_mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void g_mbar_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void g_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(g_smem_u32(dst)), "l"(src), "r"(bytes), "r"(g_smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void g_mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                 : "=r"(done) : "r"(g_smem_u32(bar)), "r"(parity) : "memory");
-  }
-}
-
 template <int NT>
 __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const double* const* __restrict__ cores,
                                                                       GramShape sh, int m,
@@ -90,7 +71,10 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   const int MB = RP * L;                    // one matrix block
   double* U = gsm;                          // [pair][a][c'] row-major, stride L (also W at core ends)
   double* XB = U + GT_P * MB;               // 2 buffers x [I0, I1, J0, J1][a][a']
-  __shared__ uint64_t gbar[2];  // staged-slice buffers: TMA completion
+  // copy list of the staged slices (16-byte cp.async, even ranks): entry q = {offset of the
+  // chunk inside its tensor's core (doubles, without the slice term), destination | slot << 24}
+  int2* gdesc = reinterpret_cast<int2*>(XB + 2 * (GT_I + GT_J) * MB);
+  __shared__ const double* gbase[2][GT_I + GT_J];  // core pointers of the tile's tensors, by core parity
   const int tid = threadIdx.x, lane = tid & 31, p = tid >> 5, g = lane >> 2, tg = lane & 3;
   const int pi = p / GT_J, pj = p % GT_J;
   cg::cluster_group cl = cg::this_cluster();
@@ -98,11 +82,6 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   const GramTile tl = tiles[blockIdx.x / CS];
   const int i0 = tl.i0, j0 = tl.j0, d = sh.d;
   double* Up = U + p * MB;
-  if (tid == 0) {
-    g_mbar_init(&gbar[0], 1);
-    g_mbar_init(&gbar[1], 1);
-  }
-  uint32_t ph0 = 0, ph1 = 0;
   // W's A fragments (W[8x + g][4q + tg]) for the whole core, in registers; W_0 = 1 (1 x 1)
   double wf[NT][KT];
 #pragma unroll
@@ -110,47 +89,52 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
 #pragma unroll
     for (int q = 0; q < KT; ++q) wf[x][q] = (x == 0 && q == 0 && g == 0 && tg == 0) ? 1.0 : 0.0;
   double gv = 0.0;
-  // Staged rows of core kk: thread tid < nrow owns row tid (I tensors: R0i rows of R1i doubles,
-  // then J tensors: R0j rows of R1j), clamped into the tile's block, so a padding tensor has its
-  // side's shape (its pairs are never written).  One TMA bulk copy per row and slice.
-  struct Row { const double* src; int dst, len; };
-  auto row_of = [&](int kk) -> Row {
+  // Staged rows of core kk: the tile's I tensors (R0i rows of R1i doubles) then its J tensors
+  // (R0j rows of R1j), clamped into the tile's block, so a padding tensor has its side's shape
+  // (its pairs are never written).
+  auto set_bases = [&](int kk) {
+    if (tid < GT_I + GT_J) {
+      const int tens = tid < GT_I ? min(i0 + tid, tl.ilim - 1) : min(j0 + tid - GT_I, tl.jlim - 1);
+      gbase[kk & 1][tid] = cores[(int64_t)tens * d + kk];
+    }
+  };
+  auto even = [&](int kk) { return ((sh.r[kk + 1] | sh.q[kk + 1]) & 1) == 0; };
+  auto nq_of = [&](int kk) { return GT_I * sh.r[kk] * (sh.r[kk + 1] / 2) + GT_J * sh.q[kk] * (sh.q[kk + 1] / 2); };
+  auto build = [&](int kk) {  // copy list of core kk's shape (n, R0i, R1i, R0j, R1j)
     const int nk = sh.n[kk], R0i = sh.r[kk], R1i = sh.r[kk + 1], R0j = sh.q[kk], R1j = sh.q[kk + 1];
-    const int nI = GT_I * R0i, nrow = nI + GT_J * R0j;
-    Row rw{nullptr, 0, 0};
-    if (tid < nrow) {
-      const bool iside = tid < nI;
-      const int R0 = iside ? R0i : R0j, R1 = iside ? R1i : R1j, rr = iside ? tid : tid - nI;
-      const int tt = rr / R0, a = rr - tt * R0;
-      const int tens = iside ? min(i0 + tt, tl.ilim - 1) : min(j0 + tt, tl.jlim - 1);
-      rw.src = cores[(int64_t)tens * d + kk] + (int64_t)a * nk * R1;
-      rw.dst = (iside ? tt : GT_I + tt) * MB + a * L;
-      rw.len = R1;
+    const int nI = GT_I * R0i * (R1i / 2), nq = nI + GT_J * R0j * (R1j / 2);
+    for (int q = tid; q < nq; q += GM_T) {
+      const bool iside = q < nI;
+      const int qq = iside ? q : q - nI, cpr = (iside ? R1i : R1j) / 2, R0 = iside ? R0i : R0j;
+      const int row = qq / cpr, c = qq - row * cpr, tt = row / R0, a = row - tt * R0;
+      const int slot = iside ? tt : GT_I + tt;
+      gdesc[q] = make_int2(a * nk * (iside ? R1i : R1j) + 2 * c, (slot * MB + a * L + 2 * c) | (slot << 24));
     }
-    return rw;
   };
-  // bulk path when every row is a multiple of 16 bytes (even ranks), else 8-byte cp.async
-  auto bulk_ok = [&](int kk) { return ((sh.r[kk + 1] | sh.q[kk + 1]) & 1) == 0; };
-  auto stage = [&](int kk, const Row& rw, int s, int b) {
+  auto stage = [&](int kk, int s, int b) {
     double* buf = XB + b * (GT_I + GT_J) * MB;
-    if (bulk_ok(kk)) {
-      if (tid == 0)
-        g_mbar_expect(&gbar[b], (uint32_t)(sizeof(double) * (GT_I * sh.r[kk] * sh.r[kk + 1] +
-                                                              GT_J * sh.q[kk] * sh.q[kk + 1])));
-      if (rw.len) g_bulk(buf + rw.dst, rw.src + (int64_t)s * rw.len, (uint32_t)(rw.len * sizeof(double)), &gbar[b]);
-    } else {
-      for (int c = 0; c < rw.len; ++c)
-        __pipeline_memcpy_async(buf + rw.dst + c, rw.src + (int64_t)s * rw.len + c, sizeof(double));
-      __pipeline_commit();
+    const int R1i = sh.r[kk + 1], R1j = sh.q[kk + 1];
+    if (even(kk)) {
+      const int nq = nq_of(kk);
+      for (int q = tid; q < nq; q += GM_T) {
+        const int2 e = gdesc[q];
+        const int slot = e.y >> 24;
+        const double* src = gbase[kk & 1][slot] + e.x + (int64_t)s * (slot < GT_I ? R1i : R1j);
+        __pipeline_memcpy_async(buf + (e.y & 0xffffff), src, 2 * sizeof(double));
+      }
+    } else {  // odd ranks: 8-byte copies, indices decoded per element
+      const int nk = sh.n[kk], R0i = sh.r[kk], R0j = sh.q[kk];
+      const int eI = GT_I * R0i * R1i, tot = eI + GT_J * R0j * R1j;
+      for (int q = tid; q < tot; q += GM_T) {
+        const bool iside = q < eI;
+        const int qq = iside ? q : q - eI, R1 = iside ? R1i : R1j, R0 = iside ? R0i : R0j;
+        const int row = qq / R1, c = qq - row * R1, tt = row / R0, a = row - tt * R0;
+        const int slot = iside ? tt : GT_I + tt;
+        __pipeline_memcpy_async(buf + slot * MB + a * L + c,
+                                gbase[kk & 1][slot] + ((int64_t)a * nk + s) * R1 + c, sizeof(double));
+      }
     }
-  };
-  auto wait_slice = [&](int kk, int b) {
-    if (bulk_ok(kk)) {
-      if (b == 0) { g_mbar_wait(&gbar[0], ph0); ph0 ^= 1u; }
-      else { g_mbar_wait(&gbar[1], ph1); ph1 ^= 1u; }
-    } else {
-      __pipeline_wait_prior(0);
-    }
+    __pipeline_commit();
   };
   auto srange = [&](int kk, int& b0, int& b1) {
     b0 = (int)((int64_t)crank * sh.n[kk] / CS);
@@ -158,22 +142,24 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   };
   int bufc = 0;           // buffer of the next slice to consume
   bool staged = false;    // core k's first slice already in flight (prefetched by core k-1)
-  __syncthreads();        // barriers initialised
 #pragma unroll 1
   for (int k = 0; k < d; ++k) {
     const int K4i = (sh.r[k] + 3) >> 2, K4j = (sh.q[k] + 3) >> 2;  // k-steps of the V / U GEMMs
     int sb, se;
     srange(k, sb, se);
-    // the next core can be prefetched when its staged slices have the same shape (pads stay zero)
-    const bool pre_next = k + 1 < d && sh.r[k + 1] == sh.r[k] && sh.r[k + 2] == sh.r[k + 1] &&
-                          sh.q[k + 1] == sh.q[k] && sh.q[k + 2] == sh.q[k + 1];
-    const Row rw = row_of(k);
+    // the next core can be prefetched when its staged slices have the same shape (same copy
+    // list; pads stay zero)
+    const bool pre_next = k + 1 < d && sh.n[k + 1] == sh.n[k] && sh.r[k + 1] == sh.r[k] &&
+                          sh.r[k + 2] == sh.r[k + 1] && sh.q[k + 1] == sh.q[k] && sh.q[k + 2] == sh.q[k + 1];
     if (!staged) {
-      __syncthreads();  // every warp is done reading the previous core's slices
+      __syncthreads();  // every warp is done reading the previous core's slices and copy list
       for (int idx = tid; idx < 2 * (GT_I + GT_J) * MB; idx += GM_T) XB[idx] = 0.0;  // pads stay zero
+      if (even(k)) build(k);
+      set_bases(k);
       __syncthreads();
-      if (sb < se) stage(k, rw, sb, bufc);
+      if (sb < se) stage(k, sb, bufc);
     }
+    if (pre_next) set_bases(k + 1);  // read after the slice loop's first barrier
     staged = false;
     double v[NT][NT][2];
 #pragma unroll
@@ -183,14 +169,14 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
 #pragma unroll 1
     for (int s = sb; s < se; ++s) {
       const double* XS = XB + bufc * (GT_I + GT_J) * MB;
-      wait_slice(k, bufc);
+      __pipeline_wait_prior(0);
       __syncthreads();  // slice s visible to all; everyone is done with the other buffer
       if (s + 1 < se) {
-        stage(k, rw, s + 1, bufc ^ 1);
+        stage(k, s + 1, bufc ^ 1);
       } else if (pre_next) {  // first slice of the next core, overlapped with this slice's math
         int nb, ne;
         srange(k + 1, nb, ne);
-        if (nb < ne) stage(k + 1, row_of(k + 1), nb, bufc ^ 1);
+        if (nb < ne) stage(k + 1, nb, bufc ^ 1);
         staged = true;
       }
       bufc ^= 1;
@@ -326,7 +312,8 @@ static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int
   const int NT = (rmax + 7) / 8;
   int L = 8 * NT;  // row stride: 4 or 12 (mod 16) keeps the fragment loads conflict-free
   while (L % 16 != 4 && L % 16 != 12) ++L;
-  const size_t smem_m = sizeof(double) * (size_t)(GT_P + 2 * (GT_I + GT_J)) * (8 * NT) * L;
+  const size_t smem_m = sizeof(double) * (size_t)(GT_P + 2 * (GT_I + GT_J)) * (8 * NT) * L +
+                        sizeof(int2) * (size_t)(GT_I + GT_J) * (8 * NT) * (4 * NT);  // copy list
   auto kern = NT == 1 ? gram_mma_kernel<1> : NT == 2 ? gram_mma_kernel<2> : NT == 3 ? gram_mma_kernel<3>
                                                                                   : gram_mma_kernel<4>;
   const int T = GM_T;
