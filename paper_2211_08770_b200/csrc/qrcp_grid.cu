@@ -92,30 +92,37 @@ __device__ __forceinline__ double qg_sum_parts(const double* part, int c, int j,
   return warp_sum(v);  // fixed shuffle tree: deterministic
 }
 
-__global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(QGArgs a) {
+__global__ void __launch_bounds__(QG_T, 4) qrcp_grid_kernel(QGArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned char qg_smem[];
-  unsigned char* done = qg_smem;  // c flags (identical in every CTA)
+  // unprocessed columns as a list (alist[0..nalive), apos = position of a column in it): the
+  // (column, chunk) pairs are dealt over the live columns and live chunks only, so every warp
+  // gets the same number of pairs (+-1) at every step; identical in every CTA
+  int* alist = reinterpret_cast<int*>(qg_smem);
+  int* apos = alist + a.c;
+  unsigned char* done = reinterpret_cast<unsigned char*>(apos + a.c);  // c flags
   __shared__ double red_v[QG_W], red_m[QG_W];
   __shared__ int red_p[QG_W];
-  __shared__ int piv_s;
+  __shared__ int piv_s, nalive;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gw = blockIdx.x * QG_W + warp, nwg = gridDim.x * QG_W;
   const int m = a.m, c = a.c, CH = a.CH, RC = a.RC;
   const int64_t ldy = a.ldy;
   double* Y = a.Y;
   const int kmax = min(min(m, c), a.kcap);
-  const int npairs = RC * c;
-  for (int j = tid; j < c; j += QG_T) done[j] = (j < a.k_start) ? 1 : 0;
+  for (int j = tid; j < c; j += QG_T) {
+    done[j] = (j < a.k_start) ? 1 : 0;
+    if (j >= a.k_start) { alist[j - a.k_start] = j; apos[j] = j - a.k_start; }
+  }
+  if (tid == 0) nalive = c - a.k_start;
   if (a.k_start == 0)
     for (int j = blockIdx.x * QG_T + tid; j < c; j += gridDim.x * QG_T) a.perm[j] = j;
   __syncthreads();
   // exact masses of rows >= k_start and >= k_start + 1
   {
-    const int s = a.k_start, lo = s / CH, nact = RC - lo;
-    for (int q = gw; q < npairs; q += nwg) {
-      const int ch = q / c, j = q - ch * c;
-      if (done[j] || ch < lo) continue;
+    const int s = a.k_start, lo = s / CH, nact = RC - lo, na = nalive;
+    for (int q = gw; q < nact * na; q += nwg) {
+      const int ch = lo + q / na, j = alist[q % na];
       const int r0 = max(ch * CH, s), r1 = min(m, (ch + 1) * CH);
       const double* col = Y + (int64_t)j * ldy;
       double m1 = 0.0, m2 = 0.0;
@@ -145,8 +152,8 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(QGArgs a) {
     {
       double ms = 0.0, bv = -1.0;
       int bp = 0x7fffffff;
-      for (int j = tid; j < c; j += QG_T) {
-        if (done[j]) continue;
+      for (int t = tid; t < nalive; t += QG_T) {
+        const int j = alist[t];
         const double v = a.n1[j];
         ms += v;
         if (qg_better(v, j, bv, bp)) { bv = v; bp = j; }
@@ -189,8 +196,14 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(QGArgs a) {
       a.tau[s] = t;
       a.order[s] = p;  // pivot sequence (the gather at the end reads it)
     }
-    __syncthreads();  // every thread has read piv_s / red_m before done[] changes
-    if (tid == 0) done[p] = 1;
+    __syncthreads();  // every thread has read piv_s / red_m before done[] and the list change
+    if (tid == 0) {  // swap-remove p from the live list
+      done[p] = 1;
+      const int ip = apos[p], last = alist[nalive - 1];
+      alist[ip] = last;
+      apos[last] = ip;
+      nalive = nalive - 1;
+    }
     // previous pivot column -> its reflector (nobody reads it any more)
     if (prev_p >= 0) {
       double* col = Y + (int64_t)prev_p * ldy;
@@ -199,11 +212,10 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(QGArgs a) {
     }
     __syncthreads();
     const double* vcol = Y + (int64_t)p * ldy;
-    const int lo = s / CH, nact = RC - lo;
+    const int lo = s / CH, nact = RC - lo, na = nalive;
     // ---- phase 1: w_j = v^T Y[s:, j] with v = [1; scal * Y[s+1:, p]]
-    for (int q = gw; q < npairs; q += nwg) {
-      const int ch = q / c, j = q - ch * c;
-      if (done[j] || ch < lo) continue;
+    for (int q = gw; q < nact * na; q += nwg) {
+      const int ch = lo + q / na, j = alist[q % na];
       const int r0 = max(ch * CH, s + 1), r1 = min(m, (ch + 1) * CH);
       const double* col = Y + (int64_t)j * ldy;
       double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
@@ -225,9 +237,8 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(QGArgs a) {
     }
     grid.sync();
     // ---- phase 2: Y[s:, j] -= tau w_j v; exact masses of rows >= s+1 and >= s+2
-    for (int q = gw; q < npairs; q += nwg) {
-      const int ch = q / c, j = q - ch * c;
-      if (done[j] || ch < lo) continue;
+    for (int q = gw; q < nact * na; q += nwg) {
+      const int ch = lo + q / na, j = alist[q % na];
       const int r0 = max(ch * CH, s + 1), r1 = min(m, (ch + 1) * CH);
       double* col = Y + (int64_t)j * ldy;
       const double qj = t * a.w[j];
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(QG_T) qrcp_grid_kernel(QGArgs a) {
 
 bool qrcp_grid_run(tt_ctx ctx, double* Y, int64_t ldy, int64_t m, int64_t c, int k_start, double stop2, int kcap,
                    double* tau, double* norms, int* perm, double* scalars) {
-  const size_t smem = (size_t)c + 16;
+  const size_t smem = (size_t)c * (1 + 2 * sizeof(int)) + 16;
   if (smem > 160 * 1024) return false;
   if (smem > 48 * 1024)
     TTB_CUDA(cudaFuncSetAttribute(qrcp_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
