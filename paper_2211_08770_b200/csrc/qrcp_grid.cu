@@ -13,9 +13,10 @@
 //           reflector of column p redundantly (alpha = Y[s,p], sigma = n2[p] = mass of rows > s,
 //           kept exactly, never by subtraction).
 //   phase 1 each pair: partial of w_j = v^T Y[s:, j] (v read from the raw pivot column, scaled on
-//           the fly); the last chunk to finish column j sums the partials in chunk order.
+//           the fly).
 //   sync
-//   phase 2 each pair: Y[s:, j] -= tau w_j v, then the partial masses of rows >= s+1 and >= s+2
+//   phase 2 each pair: w_j = the chunk partials summed in chunk order (by every chunk of column
+//           j), Y[s:, j] -= tau w_j v, then the partial masses of rows >= s+1 and >= s+2
 //           of the updated values (no downdating: exact norms every step at no extra traffic);
 //           the last chunk for column j writes n1[j], n2[j].
 //   sync
@@ -230,10 +231,6 @@ __global__ void __launch_bounds__(QG_T, 4) qrcp_grid_kernel(QGArgs a) {
       double part = scal * warp_sum((q0 + q1) + (q2 + q3));
       if (ch == lo) part += col[s];
       if (lane == 0) a.wpart[(int64_t)ch * c + j] = part;
-      if (qg_arrive(a.cnt, j, nact, lane)) {
-        const double tw = qg_sum_parts(a.wpart, c, j, lo, RC, lane);
-        if (lane == 0) a.w[j] = tw;
-      }
     }
     grid.sync();
     // ---- phase 2: Y[s:, j] -= tau w_j v; exact masses of rows >= s+1 and >= s+2
@@ -241,7 +238,9 @@ __global__ void __launch_bounds__(QG_T, 4) qrcp_grid_kernel(QGArgs a) {
       const int ch = lo + q / na, j = alist[q % na];
       const int r0 = max(ch * CH, s + 1), r1 = min(m, (ch + 1) * CH);
       double* col = Y + (int64_t)j * ldy;
-      const double qj = t * a.w[j];
+      // w_j = sum of the chunk partials in chunk order (read by every chunk of column j: no
+      // atomics or fences in phase 1, the grid barrier orders the partials)
+      const double qj = t * qg_sum_parts(a.wpart, c, j, lo, RC, lane);
       const double qv = qj * scal;
       // row s+1 (first row of the chunk that holds it) peeled off: rows >= s+2 summed on their own
       int b = r0;
