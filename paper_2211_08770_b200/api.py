@@ -325,9 +325,10 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
                         floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0, chunks: int = 2,
                         out_host: Optional[torch.Tensor] = None, start_event=None):
     """End-to-end batched rounding from HOST inputs to HOST results, pipelined over `chunks`
-    contiguous slices of the batch: the host->device copy of slice c+1 and the device->host
-    copy of slice c-1's results run on a copy stream while slice c is rounded on the context's
-    stream (stream orchestration only; the rounding is tt_round_batch_strided).
+    contiguous slices of the batch: the host->device copy of slice c+1 (one copy stream) and
+    the device->host copy of slice c-1's results (another stream: the two directions use
+    different copy engines) run while slice c is rounded on the context's stream (stream
+    orchestration only; the rounding is tt_round_batch_strided).
     host_terms[l][k]: pinned CPU float64 tensors (B, r_{k-1}, n_k, r_k).  Results go to
     out_host (pinned float64, items in order, cores in order, each core C order; allocated if
     None).  Returns (out_host, ranks (B, d+1), norms (B,), doubles written)."""
@@ -336,9 +337,11 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
     coeffs = np.asarray(coeffs, dtype=np.float64).reshape(B, K)
     norms_a = None if norms is None else np.asarray(norms, dtype=np.float64).reshape(B, K)
     dev = f"cuda:{ctx.device}"
-    copy = torch.cuda.Stream(ctx.device)
+    copy = torch.cuda.Stream(ctx.device)   # host -> device (one copy engine)
+    back = torch.cuda.Stream(ctx.device)   # device -> host (the other direction's engine)
     if start_event is not None:
         copy.wait_event(start_event)
+        back.wait_event(start_event)
     bounds = [(B * c) // chunks for c in range(chunks + 1)]
     staged, events = [], []
 
@@ -379,8 +382,8 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
         # device -> host of this slice on the copy stream, overlapping the next slice's rounding
         done = torch.cuda.Event()
         done.record(ctx.stream)
-        copy.wait_event(done)
-        with torch.cuda.stream(copy):
+        back.wait_event(done)
+        with torch.cuda.stream(back):
             for w, (ptr, cnt) in enumerate(res.arenas()):
                 dst = out_host[offset:offset + cnt]
                 src = torch.as_tensor(_CoreArray(ptr, (cnt,), res), device=dev)
@@ -391,6 +394,7 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
         if dbg:
             print(f"[host_pipeline] slice {c} done at {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
     copy.synchronize()
+    back.synchronize()
     if dbg:
         print(f"[host_pipeline] copies done at {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
     del pending
