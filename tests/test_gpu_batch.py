@@ -245,3 +245,24 @@ def test_batch_exactly_rank_64_and_single_item():
     cores, coeffs = _stack(items)
     res = P.tt_round_batch_strided(ctx(), cores, coeffs, 1e-10)
     _check_item(res.item_numpy(0), list(res.ranks[0]), terms, [1.0, 2.0, -1.0], 1e-10, rounding.DEFAULT_FLOOR_C)
+
+
+def test_batch_c4_full_size_bench_config():
+    """BASELINE configs[3] at full size in the launch configuration bench.py times (4096 items,
+    tt_round_batch_strided, one call): closed-form ranks for every item, the distance to
+    y1 + [b even] y2 on a sample across waves, and oracle parity item by item on that sample."""
+    import torch
+    import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums_stacked
+    B = 4096
+    cores, coeffs = make_batch_sums_stacked(B)
+    dc = [[torch.from_numpy(c).cuda() for c in term] for term in cores]
+    res = P.tt_round_batch_strided(ctx(), dc, coeffs, 1e-6, norms=np.ones((B, 4)))
+    want = np.where(np.arange(B) % 2 == 0, 32, 16)
+    assert np.all(res.ranks[:, 1:-1] == want[:, None]) and np.all(res.ranks[:, [0, -1]] == 1)
+    for b in (0, 1, 1333, 2048, 2049, 4095):
+        terms = [[cores[s][k][b] for k in range(10)] for s in range(4)]
+        g = res.item_numpy(b)
+        refx = tt.tt_sum(terms[:2], [1.0, 1.0]) if b % 2 == 0 else terms[0]
+        assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
+        _check_item(g, list(res.ranks[b]), terms, list(coeffs[b]), 1e-6, rounding.DEFAULT_FLOOR_C, norms=[1.0] * 4)

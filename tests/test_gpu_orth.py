@@ -208,3 +208,22 @@ def test_orth_c5_shape_householder_teacher_forced():
     Q, R, rep = P.tt_orth(ctx(), "householder", [dev(a) for a in st.tensors], c.delta)
     assert rep["rounding_calls"] == 4 * 3 - 1
     assert rep["max_rank_per_call"] == [max(i.ranks) for i in ref.infos]
+
+
+def test_orth_c3_full_cgs2_closed_form():
+    """BASELINE configs[2] at full size (m = 50, d = 16, n = 64, r = 20, kappa = 1e6): CGS2 on the
+    GPU against the shared-tail closed form (R = R_M, q_i = B Q_M[:, i], LOO ~ u): the oracle
+    cannot run this size in test time, the construction fixes the exact answer."""
+    import paper_2211_08770_b200 as P
+    c = CONFIGS["C3"]
+    st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed)
+    A = [dev(a) for a in st.tensors]
+    Q, R, rep = P.tt_orth(ctx(), "cgs2", A, c.delta, want_loo=True)
+    assert rep["rounding_calls"] == 2 * c.m
+    qm, rm = st.qr_exact()
+    assert np.linalg.norm(R - rm) <= 1e-10 * np.linalg.norm(rm)
+    assert float(np.max(rep["loo_per_step"])) <= 1e-13
+    assert max(rep["max_rank_per_call"]) == c.r
+    for i in (0, 25, 49):  # forward error of the basis ~ u m kappa_i (kappa_49 = 1e6 here)
+        kap = np.linalg.cond(st.M[:, :i + 1]) if i > 0 else 1.0
+        assert diff_norm(Q[i].to_numpy(), st.q_exact(i)) <= max(1e-10, 16 * U_ROUND * c.m * kap), i
