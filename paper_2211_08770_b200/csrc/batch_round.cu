@@ -46,6 +46,7 @@ constexpr int BR_RPL = BR_CH / 32;     // chunk rows per lane
 constexpr int BR_CPW = BR_C / BR_W;    // columns per warp
 constexpr int BR_S0 = BR_C + BR_CH;    // rows of stack 0 (R block + first chunk)
 constexpr int BR_SL = 8;               // reflectors per staged slice of the applications
+constexpr int BR_APPLY_NS = 2;         // target columns per warp and pass of the applications
 constexpr int BR_MAXD = 64;
 constexpr int BR_MAXK = 16;
 constexpr int BR_JAC_SWEEPS = 60;
@@ -441,23 +442,24 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
 // out(row, col) = Q [T; 0] for the m-row factor whose stacks are at V (taus Tq, ncol reflectors
 // per stack); this warp's target columns col0 + 8 s + warp (s < 4, col < ntgt) with the R-block
 // rows of T in tr on entry.  Output address: out[row * rs + col * cs].
-__device__ __noinline__ void br_apply_q(double (&tr)[2][4], const double* V, const double* Tq, int64_t m, int ncol,
+template <int NS>
+__device__ __noinline__ void br_apply_q(double (&tr)[2][NS], const double* V, const double* Tq, int64_t m, int ncol,
                                         int col0, int ntgt, double* out, int64_t rs, int64_t cs, VStage& vs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nst = br_stacks(m);
   uint32_t ph[2] = {vs.phase[0], vs.phase[1]};
-  double tc[BR_RPL][4];
+  double tc[BR_RPL][NS];
 #pragma unroll 1
   for (int q = nst - 1; q >= 0; --q) {
 #pragma unroll
     for (int t = 0; t < BR_RPL; ++t)
 #pragma unroll
-      for (int s = 0; s < 4; ++s) tc[t][s] = 0.0;
-    if (q == 0) br_stack_apply<4, true>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
-    else br_stack_apply<4, false>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
+      for (int s = 0; s < NS; ++s) tc[t][s] = 0.0;
+    if (q == 0) br_stack_apply<NS, true>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
+    else br_stack_apply<NS, false>(tr, tc, V + br_stack_off(q, ncol), Tq + (int64_t)q * BR_C, q, ncol, ntgt - col0, vs, ph);
     const int64_t base = q == 0 ? BR_C : BR_S0 + (int64_t)BR_CH * (q - 1);
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int col = col0 + s * BR_W + warp;
       if (col < ntgt) {
 #pragma unroll
@@ -478,15 +480,16 @@ __device__ __noinline__ void br_apply_q(double (&tr)[2][4], const double* V, con
 }
 
 // Q [T; 0] for the rho target columns stored in src (column-major, ld 64, rows < cp), in passes
-// of 32 columns (4 per warp).
+// of 8 BR_APPLY_NS columns (BR_APPLY_NS per warp: 2 keeps the application within 80 registers
+// at 3 CTAs per SM without spilling; more passes re-stream the reflectors from L2).
 __device__ void br_apply_targets(const double* __restrict__ src, int rho, int cp, const double* V, const double* Tq,
                                  int64_t m, int ncol, double* out, int64_t rs, int64_t cs, VStage& vs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll 1
-  for (int col0 = 0; col0 < rho; col0 += 4 * BR_W) {
-    double tr[2][4];
+  for (int col0 = 0; col0 < rho; col0 += BR_APPLY_NS * BR_W) {
+    double tr[2][BR_APPLY_NS];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < BR_APPLY_NS; ++s) {
       const int col = col0 + s * BR_W + warp;
       const bool ok = col < rho;
       tr[0][s] = (ok && lane < cp) ? src[col * BR_C + lane] : 0.0;
