@@ -153,6 +153,7 @@ struct BRSmem {
   int cterm[BR_C], ca[BR_C];
   int flag;
   int rho;
+  double xst[BR_W][32];       // r2l panel assembly: the term-core values of one column, per warp
   VStage vst;
 };
 
@@ -535,6 +536,7 @@ struct PanelElem {
   const double* const* cores;  // this item's [l][kc]
   const BRShape* sh;
   const double* LT;
+  double* xst;                 // BR_W x 32 staging (shared memory)
   const int* cterm;
   const int* ca;
   int kc, d, n, Rpk, last;
@@ -569,6 +571,15 @@ struct PanelElem {
       const int64_t row = base + 32 * t + lane;
       ib[t] = row < m ? (int)((row / Rpk) << 8 | (row % Rpk)) : -1;
     }
+    // the chunk's rows cover mode indices i in [ilo, ilo + ni): per column the ni x rl term-core
+    // values X(a, i, beta) are loaded once, one per lane, into the warp's staging row, instead of
+    // one dependent L2 load per (row, beta) in the FMA loop (the term cores do not fit in L1)
+    const int64_t rlast = (base + BR_CH < m ? base + BR_CH : m) - 1;
+    const int ilo = (int)(base / Rpk), ni = rlast >= base ? (int)(rlast / Rpk) - ilo + 1 : 0;
+    int xi[BR_RPL];
+#pragma unroll
+    for (int t = 0; t < BR_RPL; ++t) xi[t] = ib[t] < 0 ? 0 : (ib[t] >> 8) - ilo;
+    double* xw = xst + warp * 32;
 #pragma unroll
     for (int s = 0; s < BR_CPW; ++s) {
       const int col = s * BR_W + warp;
@@ -590,13 +601,28 @@ struct PanelElem {
       double acc[BR_RPL];
 #pragma unroll
       for (int t = 0; t < BR_RPL; ++t) acc[t] = 0.0;
+      if (ni * rl <= 32) {
+        __syncwarp();
+        if (lane < ni * rl) xw[lane] = __ldg(xa + (int64_t)(ilo + lane / rl) * rl + lane % rl);
+        __syncwarp();
 #pragma unroll 2
-      for (int be = 0; be < rl; ++be) {
-        const double* lrow = LT + (int64_t)(o + be) * BR_C;
+        for (int be = 0; be < rl; ++be) {
+          const double* lrow = LT + (int64_t)(o + be) * BR_C;
 #pragma unroll
-        for (int t = 0; t < BR_RPL; ++t) {
-          const int q = ib[t] < 0 ? 0 : ib[t];
-          acc[t] += lrow[q & 255] * __ldg(xa + (int64_t)(q >> 8) * rl + be);
+          for (int t = 0; t < BR_RPL; ++t) {
+            const int q = ib[t] < 0 ? 0 : ib[t];
+            acc[t] += lrow[q & 255] * xw[xi[t] * rl + be];
+          }
+        }
+      } else {
+#pragma unroll 2
+        for (int be = 0; be < rl; ++be) {
+          const double* lrow = LT + (int64_t)(o + be) * BR_C;
+#pragma unroll
+          for (int t = 0; t < BR_RPL; ++t) {
+            const int q = ib[t] < 0 ? 0 : ib[t];
+            acc[t] += lrow[q & 255] * __ldg(xa + (int64_t)(q >> 8) * rl + be);
+          }
         }
       }
 #pragma unroll
@@ -690,7 +716,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
     br_load_lt(sm, A.L + (int64_t)b * 2 * BR_C * BR_C + ((k + 1) & 1) * BR_C * BR_C, Rpk, S->R[k]);
   }
   __syncthreads();
-  PanelElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, sm.cterm, sm.ca, kc, d, n, Rpk, last ? 1 : 0};
+  PanelElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, &sm.xst[0][0], sm.cterm, sm.ca, kc, d, n, Rpk, last ? 1 : 0};
   double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
   double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kc];
   br_qr(e, m, c, sm, V, Tq, (A.dbg && blockIdx.x == 0) ? A.dbg : nullptr);
