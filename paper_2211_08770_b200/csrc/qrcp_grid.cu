@@ -25,6 +25,7 @@
 // Panels up to ~80 MB stay in L2 across steps.  All reductions run in a fixed order
 // (deterministic, run to run).
 #include <cooperative_groups.h>
+#include <cuda/atomic>
 
 #include <algorithm>
 #include <cstdlib>
@@ -79,10 +80,10 @@ __device__ __forceinline__ double qg_sumsq(const double* col, int a, int r1, int
 // Called by the whole warp; lane 0 has written part[chunk * c + j] already.
 __device__ __forceinline__ bool qg_arrive(int* cnt, int j, int nact, int lane) {
   int last = 0;
-  if (lane == 0) {
-    __threadfence();
-    last = (atomicAdd(cnt + j, 1) == nact - 1);
-    if (last) { cnt[j] = 0; __threadfence(); }
+  if (lane == 0) {  // acq_rel RMW: releases this lane's partial, acquires the others' (no full fence)
+    cuda::atomic_ref<int, cuda::thread_scope_device> r(cnt[j]);
+    last = (r.fetch_add(1, cuda::memory_order_acq_rel) == nact - 1);
+    if (last) r.store(0, cuda::memory_order_relaxed);
   }
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
