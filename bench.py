@@ -310,7 +310,7 @@ def main():
     if not args.no_extras:
         from ttinputs import CONFIGS, make_shared_tail_set
         c3 = CONFIGS["C3"]
-        st3 = make_shared_tail_set(c3.d, c3.n, c3.r, c3.m, c3.kappa, c3.seed + rank)
+        st3 = make_shared_tail_set(c3.d, c3.n, c3.r, c3.m, c3.kappa, c3.seed)  # same set on every rank (sharded parts)
         A3 = [P.DeviceTT.from_numpy(a) for a in st3.tensors]
         G = P.tt_gram(ctx, A3)
         torch.cuda.synchronize()
@@ -346,6 +346,23 @@ def main():
                 sms.append(e0.elapsed_time(e1))
             tg = torch.tensor([statistics.median(sms)], device=dev, dtype=torch.float64)
             dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+            # CGS2 with the projection dots of every step split over the ranks (one NCCL
+            # all-gather per pass), C3 prefix m = 10; roundings replicated on every rank
+            A3p = A3[:10]
+            parallel.cgs_sharded(ctx, "cgs2", A3p[:2], c3.delta)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, Rsh, ncalls = parallel.cgs_sharded(ctx, "cgs2", A3p, c3.delta)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tc = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+            rm = st3.qr_exact()[1][:10, :10]
+            extras["cgs2_sharded"] = {"ranks": world, "m": 10, "roundings": ncalls, "ms": float(tc.item()),
+                                      "R_rel_err_vs_R_M": float(np.linalg.norm(Rsh - rm) / np.linalg.norm(rm)),
+                                      "collective": "NCCL all_gather_into_tensor of the projection dots, per pass"}
             extras["gram_sharded"] = {"ranks": world, "ms": float(tg.item()), "pairs_per_s": pairs / (float(tg.item()) * 1e-3),
                                       "rel_err_vs_MtM": float(np.linalg.norm(Gs - st3.gram_exact()) / np.linalg.norm(st3.gram_exact())),
                                       "collective": "NCCL all_gather_into_tensor of padded pair blocks"}

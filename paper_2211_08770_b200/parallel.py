@@ -117,3 +117,76 @@ def sharded_round_batch(items, round_fn: Callable, group=None):
     else:
         ranks = [list(o.ranks) for o in outs]
     return outs, ranks
+
+
+def dot_slice(P: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous slice [start, end) of a batch of P dot products for `rank`."""
+    return batch_slice(P, world, rank)
+
+
+def sharded_dots(P: int, dot_fn: Callable[[int, int], "object"], group=None) -> np.ndarray:
+    """A batch of P TT-dots split over the ranks of ``group``: rank r evaluates the contiguous
+    slice dot_slice(P, world, r) with dot_fn(start, end) (a 1-D float64 torch tensor on the
+    rank's device, e.g. ``tt_dot_batch`` of those pairs), ONE all-gather of equal-sized
+    (padded) buffers, every rank returns all P values in order (north star: "CGS projection
+    dot products are split ... and combined with NCCL all-gather")."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if P == 0:
+        return np.zeros(0)
+    s, e = dot_slice(P, world, rank)
+    mine = dot_fn(s, e) if e > s else None
+    cap = -(-P // world)
+    dev = mine.device if mine is not None else ("cuda" if dist.is_initialized() and dist.get_backend(group) == "nccl"
+                                                 else "cpu")
+    buf = torch.zeros(cap, dtype=torch.float64, device=dev)
+    if mine is not None:
+        buf[: e - s] = mine
+    if world > 1:
+        out = torch.empty(world * cap, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(out, buf, group=group)
+        allbuf = out.cpu().numpy().reshape(world, cap)
+    else:
+        allbuf = buf.cpu().numpy().reshape(1, cap)
+    vals = []
+    for r in range(world):
+        a, b = dot_slice(P, world, r)
+        vals.append(allbuf[r, : b - a])
+    return np.concatenate(vals)
+
+
+def cgs_sharded(ctx, kind: str, A, delta: float, floor_c: float = None, group=None):
+    """TT-CGS / TT-CGS2 (PAPER.md Algs. 1 and 3) with the projection dots of every step split
+    over the ranks (sharded_dots + one all-gather per pass); the roundings are replicated on
+    every rank (deterministic: identical results everywhere).  Same schedule as tt_orth's
+    lazy drivers: per pass the coefficients c_j = <p, q_j> (j < i), R(j, i) += c_j, then
+    p = round(p - sum_j c_j q_j); R(i, i) = ||p||, q_i = p / R(i, i).  Returns (Q, R, calls)."""
+    from . import api as P
+
+    if kind not in ("cgs", "cgs2"):
+        raise ValueError("cgs_sharded: kind must be 'cgs' or 'cgs2'")
+    fc = P.DEFAULT_FLOOR_C if floor_c is None else floor_c
+    passes = 2 if kind == "cgs2" else 1
+    m = len(A)
+    R = np.zeros((m, m))
+    Q = []
+    calls = 0
+    for i in range(m):
+        base = A[i]
+        for _ in range(passes):
+            if i > 0:
+                fn = lambda s, e: P.tt_dot_batch(ctx, [base] * (e - s), Q[s:e])  # noqa: E731
+                c = sharded_dots(i, fn, group)
+            else:
+                c = np.zeros(0)
+            R[:i, i] += c
+            base, _ = P.tt_round(ctx, [base] + Q, [1.0] + [-float(v) for v in c], delta, floor_c=fc)
+            calls += 1
+        nrm = P.tt_norm(ctx, base)
+        R[i, i] = nrm
+        q = P.tt_sum(ctx, [base], [1.0 / nrm])
+        Q.append(q)
+    return Q, R, calls

@@ -40,6 +40,12 @@ def test_lpt_balance():
     assert sorted(b for p in parts for b in p) == sorted(blocks)
 
 
+def test_dot_slices():
+    for P, W in [(49, 8), (1, 2), (0, 3), (5, 5)]:
+        sl = [parallel.dot_slice(P, W, r) for r in range(W)]
+        assert sl[0][0] == 0 and sl[-1][1] == P and sum(e - s for s, e in sl) == P
+
+
 def test_batch_slices():
     for B, W in [(4096, 8), (10, 3), (2, 4)]:
         sl = [parallel.batch_slice(B, W, r) for r in range(W)]
@@ -75,7 +81,14 @@ def _worker(rank, world, port, q):
                 self.ranks = ranks
         items = list(range(7))
         outs, ranks = parallel.sharded_round_batch(items, lambda xs: [R([1, x, 1]) for x in xs])
-        q.put((rank, ok_gram, ranks))
+        # CGS projection dots <a_8, a_j>, j < 8, split over the ranks and all-gathered
+        dots = parallel.sharded_dots(8, lambda s, e: torch.tensor([tt.tt_dot(A[8], A[j]) for j in range(s, e)],
+                                                                  dtype=torch.float64))
+        ok_dots = float(np.max(np.abs(dots - np.array([tt.tt_dot(A[8], A[j]) for j in range(8)]))))
+        # fewer dots than ranks (P = 1): the idle rank contributes an empty slice
+        one = parallel.sharded_dots(1, lambda s, e: torch.tensor([tt.tt_dot(A[1], A[0])], dtype=torch.float64))
+        ok_dots = max(ok_dots, float(abs(one[0] - tt.tt_dot(A[1], A[0]))) if len(one) == 1 else 1.0)
+        q.put((rank, max(ok_gram, ok_dots), ranks))
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, repr(e), None))
     finally:
