@@ -157,6 +157,30 @@ struct BRSmem {
   VStage vst;
 };
 
+// Sums over the 32 lanes of eight per-lane values v[0..7] (one total per column), returned in
+// every lane: a transposed butterfly halves the set per level (4 + 2 + 1 exchanges), two more
+// finish the sums, one broadcast per column -- 17 shuffles instead of 8 x 5.
+__device__ __forceinline__ void warp_sum8(double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0, b2 = (lane & 4) != 0;
+  double u4[4], u2[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double keep = b4 ? v[4 + k] : v[k], send = b4 ? v[k] : v[4 + k];
+    u4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);  // column 4 b4 + k
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double keep = b3 ? u4[2 + k] : u4[k], send = b3 ? u4[k] : u4[2 + k];
+    u2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);   // column 4 b4 + 2 b3 + k
+  }
+  double u1 = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4);  // column 4 b4 + 2 b3 + b2
+  u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+  u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = __shfl_sync(0xffffffffu, u1, ((c >> 2) & 1) * 16 + ((c >> 1) & 1) * 8 + (c & 1) * 4);
+}
+
 // Flat-tree Householder QR step over one stack: R block in sm.Rs (rows 0..63, column-major;
 // a full block for stack 0, upper triangular afterwards) stacked on the 128-row chunk in
 // registers a[t][s] (row 32t + lane, column 8s + warp).  LAPACK dlarfg arithmetic per column j;
@@ -233,10 +257,16 @@ __device__ void br_stack_qr_first(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int n
           for (int t = 2; t < BR_RPL; ++t) q += vc[t] * a[t][s];
           dt[s] = q;
         }
+        if (S < 5) {  // >= 4 live slots: transposed butterfly over all 8
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+          for (int s = 0; s < S; ++s) dt[s] = 0.0;
+          warp_sum8(dt);
+        } else {
 #pragma unroll
-          for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+        }
 #pragma unroll
         for (int s = S; s < BR_CPW; ++s) {
           const int col = s * BR_W + warp;
@@ -317,10 +347,16 @@ __device__ void br_stack_qr_later(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int n
           for (int t = 2; t < BR_RPL; ++t) q += vc[t] * a[t][s];
           dt[s] = q;
         }
+        if (S < 5) {  // >= 4 live slots: transposed butterfly over all 8
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+          for (int s = 0; s < S; ++s) dt[s] = 0.0;
+          warp_sum8(dt);
+        } else {
 #pragma unroll
-          for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+        }
 #pragma unroll
         for (int s = S; s < BR_CPW; ++s) {
           const int col = s * BR_W + warp;
