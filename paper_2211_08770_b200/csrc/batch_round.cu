@@ -181,6 +181,18 @@ __device__ __forceinline__ void warp_sum8(double (&v)[8]) {
   for (int c = 0; c < 8; ++c) v[c] = __shfl_sync(0xffffffffu, u1, ((c >> 2) & 1) * 16 + ((c >> 1) & 1) * 8 + (c & 1) * 4);
 }
 
+// Two per-lane values summed over the warp (one total each, in every lane): one exchange
+// halves the pair, four more finish, two broadcasts -- 7 shuffles instead of 2 x 5.
+__device__ __forceinline__ void warp_sum2(double (&v)[2]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = (lane & 16) != 0;
+  double u = (b4 ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, b4 ? v[0] : v[1], 16);  // column b4
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+  v[0] = __shfl_sync(0xffffffffu, u, 0);
+  v[1] = __shfl_sync(0xffffffffu, u, 16);
+}
+
 // Flat-tree Householder QR step over one stack: R block in sm.Rs (rows 0..63, column-major;
 // a full block for stack 0, upper triangular afterwards) stacked on the 128-row chunk in
 // registers a[t][s] (row 32t + lane, column 8s + warp).  LAPACK dlarfg arithmetic per column j;
@@ -456,10 +468,14 @@ __device__ void br_stack_apply(double (&tr)[2][NS], double (&tc)[BR_RPL][NS], co
         for (int t = 2; t < BR_RPL; ++t) q += vc[t] * tc[t][s];
         dt[s] = q;
       }
+      if constexpr (NS == 2) {
+        warp_sum2(dt);
+      } else {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int s = 0; s < NS; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+          for (int s = 0; s < NS; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+      }
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const double w = tau * dt[s];
