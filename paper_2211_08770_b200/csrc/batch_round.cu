@@ -153,6 +153,7 @@ struct BRSmem {
   int cterm[BR_C], ca[BR_C];
   int flag;
   int rho;
+  uint64_t qfull[2], qempty[2];  // split-phase reflector hand-off of the later stacks (br_stack_qr_later_async)
   double xst[BR_W][32];       // r2l panel assembly: the term-core values of one column, per warp
   VStage vst;
 };
@@ -390,6 +391,150 @@ __device__ void br_stack_qr_later(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int n
   __syncthreads();
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Later stacks (R block upper triangular, reflector R-block part e_j), split-phase version of
+// br_stack_qr_later: reflector j is handed over through buffer j & 1 guarded by two mbarriers
+// (qfull: the owner warp's 32 lanes arrive after writing it; qempty: every thread arrives once
+// it holds it in registers) instead of a __syncthreads per reflector.  The owner of column j+1
+// applies reflector j to that column first, forms reflector j+1 and publishes it, then updates
+// its other columns; every other warp updates its columns as soon as reflector j is out.  Every
+// column is touched by its owner warp only, so nothing else needs ordering.  Same arithmetic.
+template <int SL>
+__device__ __forceinline__ void br_gen_later(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int j, double* tau_out,
+                                             int lane) {
+  const int buf = j & 1;
+  double* Rc = sm.Rs + j * BR_C;
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < BR_RPL; ++t) ss += a[t][SL] * a[t][SL];
+  const double sigma = warp_sum(ss);
+  const double alpha = Rc[j];
+  double tau = 0.0, beta = alpha, scal = 0.0;
+  if (sigma != 0.0) {
+    const double nr = sqrt(alpha * alpha + sigma);
+    beta = alpha >= 0.0 ? -nr : nr;
+    const double am = alpha - beta;
+    const double inv = 1.0 / (beta * am);
+    tau = -am * am * inv;
+    scal = beta * inv;
+  }
+#pragma unroll
+  for (int t = 0; t < BR_RPL; ++t) {
+    a[t][SL] *= scal;
+    sm.vb[buf][BR_C + 32 * t + lane] = a[t][SL];
+  }
+  __syncwarp();
+  if (lane == 0) { Rc[j] = beta; sm.tb[buf] = tau; tau_out[j] = tau; }
+}
+
+template <int SL>
+__device__ __forceinline__ void br_upd_one_later(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int j, double tau,
+                                                 const double (&vc)[BR_RPL], int lane, int warp) {
+  const int col = SL * BR_W + warp;
+  const double rj = sm.Rs[col * BR_C + j];
+  double q = vc[0] * a[0][SL] + vc[1] * a[1][SL];
+#pragma unroll
+  for (int t = 2; t < BR_RPL; ++t) q += vc[t] * a[t][SL];
+  q = warp_sum(q);
+  const double w = tau * (rj + q);
+  __syncwarp();
+  if (lane == 0) sm.Rs[col * BR_C + j] = rj - w;
+#pragma unroll
+  for (int t = 0; t < BR_RPL; ++t) a[t][SL] -= w * vc[t];
+}
+
+template <int S>
+__device__ __forceinline__ void br_later_async_slot(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol,
+                                                    double* tau_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int ww = 0; ww < BR_W; ++ww) {
+    const int j = S * BR_W + ww;
+    if (j >= ncol) return;
+    const int buf = j & 1;
+    mbar_wait(&sm.qfull[buf], (uint32_t)((j >> 1) & 1));
+    const double tau = sm.tb[buf];
+    const double* v = sm.vb[buf];
+    double vc[BR_RPL];
+#pragma unroll
+    for (int t = 0; t < BR_RPL; ++t) vc[t] = v[BR_C + 32 * t + lane];
+    mbar_arrive(&sm.qempty[buf]);  // reflector j is in registers: its buffer may be reused
+    const int j1 = j + 1;
+    const bool own = j1 < ncol && warp == (j1 & (BR_W - 1));
+    if (own) {  // look-ahead: column j+1 first, reflector j+1 published, then the other columns
+      if (ww < BR_W - 1) {
+        if (tau != 0.0) br_upd_one_later<S>(a, sm, j, tau, vc, lane, warp);
+      } else {
+        if constexpr (S + 1 < BR_CPW)
+          if (tau != 0.0) br_upd_one_later<S + 1>(a, sm, j, tau, vc, lane, warp);
+      }
+      if (j1 >= 2) mbar_wait(&sm.qempty[j1 & 1], (uint32_t)(((j1 - 2) >> 1) & 1));
+      __syncwarp();
+      if (ww < BR_W - 1) {
+        br_gen_later<S>(a, sm, j1, tau_out, lane);
+      } else {
+        if constexpr (S + 1 < BR_CPW) br_gen_later<S + 1>(a, sm, j1, tau_out, lane);
+      }
+      __syncwarp();
+      mbar_arrive(&sm.qfull[j1 & 1]);
+    }
+    if (tau != 0.0) {
+      double dt[BR_CPW], rj[BR_CPW];
+#pragma unroll
+      for (int s = S; s < BR_CPW; ++s) {
+        const int col = min(s * BR_W + warp, BR_C - 1);
+        rj[s] = sm.Rs[col * BR_C + j];  // broadcast: row j of the R block
+        double q = vc[0] * a[0][s] + vc[1] * a[1][s];
+#pragma unroll
+        for (int t = 2; t < BR_RPL; ++t) q += vc[t] * a[t][s];
+        dt[s] = q;
+      }
+      if (S < 5) {  // >= 4 live slots: transposed butterfly over all 8
+#pragma unroll
+        for (int s = 0; s < S; ++s) dt[s] = 0.0;
+        warp_sum8(dt);
+      } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int s = S; s < BR_CPW; ++s) dt[s] += __shfl_xor_sync(0xffffffffu, dt[s], o);
+      }
+#pragma unroll
+      for (int s = S; s < BR_CPW; ++s) {
+        const int col = s * BR_W + warp;
+        const bool act = (s > S || warp > ww) && col < ncol && !(own && col == j1);
+        const double w = act ? tau * (rj[s] + dt[s]) : 0.0;
+        if (act && lane == 0) sm.Rs[col * BR_C + j] = rj[s] - w;
+#pragma unroll
+        for (int t = 0; t < BR_RPL; ++t) a[t][s] -= w * vc[t];
+      }
+    }
+  }
+  if constexpr (S + 1 < BR_CPW) br_later_async_slot<S + 1>(a, sm, ncol, tau_out);
+}
+
+__device__ void br_stack_qr_later_async(double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int ncol, double* tau_out) {
+  const int tid = threadIdx.x;
+  if (ncol <= 0) return;
+  if (tid == 0) {
+    mbar_init(&sm.qfull[0], 32);
+    mbar_init(&sm.qfull[1], 32);
+    mbar_init(&sm.qempty[0], BR_T);
+    mbar_init(&sm.qempty[1], BR_T);
+  }
+  __syncthreads();
+  if ((tid >> 5) == 0) {  // reflector 0: warp 0, slot 0
+    br_gen_later<0>(a, sm, 0, tau_out, tid & 31);
+    __syncwarp();
+    mbar_arrive(&sm.qfull[0]);
+  }
+  br_later_async_slot<0>(a, sm, ncol, tau_out);
+  __syncthreads();  // every warp done (every barrier phase consumed) before the stack is stored
+}
+
 // Store one stack's reflectors (column-major, ld = stack rows) and, for stack 0, move the
 // R-block reflector parts out of Rs (its strictly lower part is zeroed for the next stacks).
 __device__ void br_store_stack(const double (&a)[BR_RPL][BR_CPW], BRSmem& sm, int q, int ncol, double* Vq) {
@@ -574,7 +719,8 @@ __device__ __noinline__ void br_qr(const Elem& elem, int64_t m, int ncol, BRSmem
     __syncthreads();
     const long long c1 = clock64();
     if (q == 0) br_stack_qr_first(a, sm, ncol, Tq, dbg ? dbg + 16 : nullptr);
-    else br_stack_qr_later(a, sm, ncol, Tq + (int64_t)q * BR_C, dbg ? dbg + 16 : nullptr);
+    else if (dbg) br_stack_qr_later(a, sm, ncol, Tq + (int64_t)q * BR_C, dbg + 16);  // (debug counters)
+    else br_stack_qr_later_async(a, sm, ncol, Tq + (int64_t)q * BR_C);
     const long long c2 = clock64();
     br_store_stack(a, sm, q, ncol, V + br_stack_off(q, ncol));
     if (dbg && tid == 0) { dbg[0] += c1 - c0; dbg[1] += c2 - c1; dbg[2] += clock64() - c2; }
