@@ -28,6 +28,7 @@
 #include <cuda/atomic>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "qr.cuh"
@@ -331,7 +332,9 @@ bool qrcp_grid_run(tt_ctx ctx, double* Y, int64_t ldy, int64_t m, int64_t c, int
   const int G = ctx->num_sms * per_sm;
   const int64_t nwg = (int64_t)G * QG_W;
   // rows per chunk: about two (column, chunk) pairs per warp, 128-row multiples, 128..4096
-  int64_t CH = ceil_div(ceil_div(m * c, 2 * nwg), 128) * 128;
+  static const char* chm_env = std::getenv("TT_B200_QG_PAIRS");  // (column, chunk) pairs per warp
+  const double ppw = chm_env ? std::max(0.05, std::atof(chm_env)) : 1.0;
+  int64_t CH = ceil_div((int64_t)std::ceil((double)m * c / (ppw * (double)nwg)), 128) * 128;
   CH = std::max<int64_t>(128, std::min<int64_t>(CH, 4096));
   const int64_t RC = ceil_div(m, CH);
   DBuf parts(ctx, (size_t)(3 * RC * c + 2 * c + (size_t)m * c));
