@@ -83,6 +83,12 @@ tt_status tt_ctx_create(int device, void* stream, tt_ctx* out) {
 tt_status tt_ctx_destroy(tt_ctx ctx) {
   if (!ctx) return TT_EINVAL;
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->up_ring) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFreeHost(ctx->up_ring);
+    for (auto& pd : ctx->up_pending) cudaEventDestroy(pd.ev);
+    for (auto ev : ctx->up_events) cudaEventDestroy(ev);
+  }
   if (ctx->scratch) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->scratch); }
   delete ctx;
   return TT_OK;

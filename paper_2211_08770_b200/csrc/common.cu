@@ -63,6 +63,53 @@ void IBuf::release() {
   count = 0;
 }
 
+// Stage `bytes` of host data in the ctx's pinned ring (16 MiB) and return its address, or null
+// when it does not fit (then the caller copies from pageable memory).  A region is reused only
+// after the copy that last read it has completed (event per staged copy, waited on overlap).
+static const char* stage_pinned(tt_ctx c, const void* host, size_t bytes) {
+  constexpr size_t cap = (size_t)16 << 20;
+  if (bytes > cap / 4) return nullptr;
+  if (!c->up_ring) {
+    if (cudaMallocHost(reinterpret_cast<void**>(&c->up_ring), cap) != cudaSuccess) {
+      (void)cudaGetLastError();
+      c->up_ring = nullptr;
+      return nullptr;
+    }
+    c->up_cap = cap;
+    c->up_off = 0;
+  }
+  size_t off = (c->up_off + 255) & ~(size_t)255;
+  if (off + bytes > c->up_cap) off = 0;
+  // wait for pending copies that read [off, off + bytes)
+  for (size_t q = 0; q < c->up_pending.size();) {
+    const auto& pd = c->up_pending[q];
+    if (pd.start < off + bytes && off < pd.end) {
+      TTB_CUDA(cudaEventSynchronize(pd.ev));
+      c->up_events.push_back(pd.ev);
+      c->up_pending.erase(c->up_pending.begin() + (ptrdiff_t)q);
+    } else {
+      ++q;
+    }
+  }
+  std::memcpy(c->up_ring + off, host, bytes);
+  c->up_off = off + bytes;
+  return c->up_ring + off;
+}
+
+static void staged_done(tt_ctx c, const char* src, size_t bytes) {
+  cudaEvent_t ev;
+  if (!c->up_events.empty()) { ev = c->up_events.back(); c->up_events.pop_back(); }
+  else TTB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  TTB_CUDA(cudaEventRecord(ev, c->stream));
+  const size_t start = (size_t)(src - c->up_ring);
+  c->up_pending.push_back({start, start + bytes, ev});
+  if (c->up_pending.size() > 256) {  // bound the list: retire the oldest
+    TTB_CUDA(cudaEventSynchronize(c->up_pending.front().ev));
+    c->up_events.push_back(c->up_pending.front().ev);
+    c->up_pending.erase(c->up_pending.begin());
+  }
+}
+
 void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
   if (p && ctx) cudaFreeAsync(p, ctx->stream);
   ctx = c;
@@ -74,7 +121,13 @@ void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
     p = nullptr;
     fail(TT_ENOMEM, "descriptor allocation failed");
   }
-  TTB_CUDA(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, c->stream));
+  const char* src = stage_pinned(c, host, bytes);
+  if (src) {
+    TTB_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    staged_done(c, src, bytes);
+  } else {
+    TTB_CUDA(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, c->stream));
+  }
 }
 
 static cudaEvent_t pool_event(tt_ctx ctx) {

@@ -63,6 +63,13 @@ struct tt_ctx_s {
   size_t h_pinned_bytes = 0;
   void* scratch = nullptr;      // grow-only device workspace of the batched engine
   size_t scratch_bytes = 0;
+  // pinned ring for small host->device uploads (descriptor tables): a copy from pinned memory
+  // is truly asynchronous, a pageable one waits for the stream (BBuf::upload)
+  char* up_ring = nullptr;
+  size_t up_cap = 0, up_off = 0;
+  struct UpPending { size_t start, end; cudaEvent_t ev; };
+  std::vector<UpPending> up_pending;
+  std::vector<cudaEvent_t> up_events;  // free events
 };
 
 struct tt_tensor_s {
