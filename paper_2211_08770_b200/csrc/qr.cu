@@ -485,22 +485,23 @@ __global__ void __launch_bounds__(256) apply_reflectors_col_kernel(const double*
   for (int r = tid; r < m; r += 256) col[r] = xs[r];
 }
 
-// Same application with the column in registers: thread t owns rows t + 256 i (i < RPT), fixed
+// Same application with the column in registers: thread t owns rows t + T i (i < RPT), fixed
 // for all reflectors, so a reflector's dot and update touch only the thread's own rows (the
 // implicit 1 of v at row j is folded into the thread's v values); the one cross-thread step is
-// the dot's reduction (warp sums, one __syncthreads, every thread adds the 8 warp sums in the
+// the dot's reduction (warp sums, one __syncthreads, every thread adds the T/32 warp sums in the
 // same order; double-buffered).
-template <int RPT>
-__global__ void __launch_bounds__(256) apply_reflectors_reg_kernel(const double* __restrict__ Y, int64_t ldy,
-                                                                   const double* __restrict__ tau, int m, int k,
-                                                                   double* X, int64_t ldx) {
-  __shared__ double red[2][8];
+template <int T, int RPT>  // T threads, RPT rows per thread
+__global__ void __launch_bounds__(T) apply_reflectors_reg_kernel(const double* __restrict__ Y, int64_t ldy,
+                                                                 const double* __restrict__ tau, int m, int k,
+                                                                 double* X, int64_t ldx) {
+  constexpr int NW = T / 32;
+  __shared__ double red[2][NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* col = X + (int64_t)blockIdx.x * ldx;
   double x[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
-    const int r = tid + 256 * i;
+    const int r = tid + T * i;
     x[i] = r < m ? col[r] : 0.0;
   }
   int b = 0;
@@ -509,28 +510,37 @@ __global__ void __launch_bounds__(256) apply_reflectors_reg_kernel(const double*
     const double t = __ldg(tau + j);
     if (t == 0.0) continue;  // uniform
     const double* v = Y + (int64_t)j * ldy;
-    double vv[RPT];
+    constexpr bool KEEP = (T <= 256);  // v kept in registers (larger CTAs: read again from L2)
+    double vv[KEEP ? RPT : 1];
     double q0 = 0.0, q1 = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int r = tid + 256 * i;
-      vv[i] = (r > j && r < m) ? __ldg(v + r) : (r == j ? 1.0 : 0.0);
-      if (i & 1) q1 += vv[i] * x[i]; else q0 += vv[i] * x[i];
+      const int r = tid + T * i;
+      const double vi = (r > j && r < m) ? __ldg(v + r) : (r == j ? 1.0 : 0.0);
+      if constexpr (KEEP) vv[i] = vi;
+      if (i & 1) q1 += vi * x[i]; else q0 += vi * x[i];
     }
     const double ws = warp_sum(q0 + q1);
     if (lane == 0) red[b][warp] = ws;
     __syncthreads();
     double tot = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) tot += red[b][w];
+    for (int w = 0; w < NW; ++w) tot += red[b][w];
     const double q = t * tot;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) x[i] -= q * vv[i];
+    for (int i = 0; i < RPT; ++i) {
+      if constexpr (KEEP) {
+        x[i] -= q * vv[i];
+      } else {
+        const int r = tid + T * i;
+        x[i] -= q * ((r > j && r < m) ? __ldg(v + r) : (r == j ? 1.0 : 0.0));
+      }
+    }
     b ^= 1;
   }
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
-    const int r = tid + 256 * i;
+    const int r = tid + T * i;
     if (r < m) col[r] = x[i];
   }
 }
@@ -702,12 +712,15 @@ void qrcp_run(tt_ctx ctx, QRCPState& st, double* Y, int64_t ldy, double stop2, i
 void apply_reflectors_left(tt_ctx ctx, const double* Y, int64_t ldy, const double* tau, int64_t m, int k,
                            double* target, int64_t ldt, int64_t nc) {
   if (k <= 0 || nc <= 0) return;
-  if (m <= 4096) {  // one CTA per target column, the column in registers (<= 16 rows per thread)
-    const int rpt = (int)ceil_div(m, 256);
-    auto kern = rpt <= 2 ? apply_reflectors_reg_kernel<2> : rpt <= 4 ? apply_reflectors_reg_kernel<4>
-              : rpt <= 8 ? apply_reflectors_reg_kernel<8> : apply_reflectors_reg_kernel<16>;
+  if (m <= 16384) {  // one CTA per target column, the column in registers (<= 16 rows per thread)
+    const bool big = m > 4096;  // 1024 threads (measured faster than 512 with twice the rows)
+    const int T = big ? 1024 : 256;
+    const int rpt = (int)ceil_div(m, T);
+    auto kern = big ? (rpt <= 8 ? apply_reflectors_reg_kernel<1024, 8> : apply_reflectors_reg_kernel<1024, 16>)
+              : rpt <= 2 ? apply_reflectors_reg_kernel<256, 2> : rpt <= 4 ? apply_reflectors_reg_kernel<256, 4>
+              : rpt <= 8 ? apply_reflectors_reg_kernel<256, 8> : apply_reflectors_reg_kernel<256, 16>;
     TTB_RUN(ctx, "apply_reflectors", 4.0 * m * k * nc, 8.0 * (m * k + 2.0 * m * nc),
-            kern<<<(unsigned)nc, 256, 0, ctx->stream>>>(Y, ldy, tau, (int)m, k, target, ldt));
+            kern<<<(unsigned)nc, T, 0, ctx->stream>>>(Y, ldy, tau, (int)m, k, target, ldt));
     return;
   }
   const size_t smem = sizeof(double) * (size_t)m;
