@@ -9,6 +9,7 @@
 //  * qrcp_kernel        : unblocked Householder QR with column pivoting and a Frobenius
 //                         stopping test (truncated-SVD stage of the left-to-right sweep).
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "qr.cuh"
@@ -268,6 +269,31 @@ __global__ void copy_upper_kernel(const double* A, int64_t lda, int rows, int co
     const int r = (int)(idx % rows), c = (int)(idx / rows);
     R[r + (int64_t)c * ldr] = (r <= c) ? A[r + (int64_t)c * lda] : 0.0;
   }
+}
+
+// Merge two compact-WY blocks (dlarft's forward accumulation): with Q1 = I - Y1 T1 Y1^T and
+// Q2 = I - Y2 T2 Y2^T, Q1 Q2 = I - [Y1 Y2] T [Y1 Y2]^T, T = [[T1, -T1 G T2], [0, T2]], G = Y1^T Y2.
+// T points at the merged block (ld ldt): T1 in rows [0, w1) of columns [0, w1), T2 on entry in rows
+// [0, w2) of columns [w1, w1 + w2); on exit T2 sits in rows [w1, w1 + w2).  One CTA of 1024.
+__global__ void __launch_bounds__(1024) merge_t_kernel(double* T, int64_t ldt, const double* __restrict__ G,
+                                                       int64_t ldg, int w1, int w2) {
+  __shared__ double t1[32][33], t2[32][33], g[32][33], h[32][33];
+  const int tid = threadIdx.x, r = tid & 31, c = tid >> 5;
+  t1[r][c] = (r < w1 && c < w1) ? T[r + (int64_t)c * ldt] : 0.0;
+  t2[r][c] = (r < w2 && c < w2) ? T[r + (int64_t)(w1 + c) * ldt] : 0.0;
+  g[r][c] = (r < w1 && c < w2) ? G[r + (int64_t)c * ldg] : 0.0;
+  __syncthreads();
+  double acc = 0.0;  // H = G T2
+  for (int k = 0; k < w2; ++k) acc = fma(g[r][k], t2[k][c], acc);
+  h[r][c] = acc;
+  __syncthreads();
+  acc = 0.0;  // T12 = -T1 H
+  for (int k = 0; k < w1; ++k) acc = fma(t1[r][k], h[k][c], acc);
+  if (c < w2) {
+    if (r < w1) T[r + (int64_t)(w1 + c) * ldt] = -acc;
+    if (r < w2) T[w1 + r + (int64_t)(w1 + c) * ldt] = t2[r][c];
+  }
+  if (c < w1 && r < w2) T[w1 + r + (int64_t)c * ldt] = 0.0;
 }
 
 __global__ void set_identity_kernel(double* Q, int64_t ldq, int m, int k) {
@@ -566,11 +592,9 @@ void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& 
   TTB_CUDA(cudaMemsetAsync(f.Y.p, 0, sizeof(double) * (size_t)m * f.kmax, ctx->stream));
   f.pan_s.clear();
   f.pan_w.clear();
-  for (int64_t s = 0; s < f.kmax;) {
+  // One panel: Householder QR of the ms x w block at (s, s) into Y / T (ld QR_NB at column s).
+  auto factor = [&](int64_t s, int w) {
     const int64_t ms = m - s;
-    int w = (int)std::min<int64_t>(QR_NB, f.kmax - s);
-    // narrower panels when that lets one cluster hold the panel
-    if (ms > panel_cluster_max_rows(w) && ms <= panel_cluster_max_rows(16)) w = std::min(w, 16);
     double* P = A + s + s * lda;
     double* Yp = f.Y.p + s + s * m;
     double* Tp = f.T.p + s * QR_NB;
@@ -581,22 +605,56 @@ void geqrf(tt_ctx ctx, double* A, int64_t lda, int64_t m, int64_t c, QRFactors& 
               hr_kernel<<<grid_for(ms, 256, 1024), 256, 0, ctx->stream>>>(Qp.p, ms, (int)ms, w, Rp.p, w, Yp, m, Tp,
                                                                           QR_NB, P, lda));
     }
+  };
+  // C (rows [s, m), n2 columns starting at column c0) <- (I - Y T Y^T)^T C for the panel at s.
+  auto update = [&](int64_t s, int w, int64_t c0, int64_t n2) {
+    if (n2 <= 0) return;
+    const int64_t ms = m - s;
+    const double* Yp = f.Y.p + s + s * m;
+    const double* Tp = f.T.p + s * QR_NB;
+    double* C = A + s + c0 * lda;
+    GemmDesc g1;  // W = Y^T C
+    g1.M = w; g1.N = n2; g1.K = ms; g1.A = Yp; g1.lda = m; g1.ta = true; g1.B = C; g1.ldb = lda; g1.C = W.p; g1.ldc = w;
+    gemm(ctx, g1);
+    GemmDesc g2;  // W2 = T^T W
+    g2.M = w; g2.N = n2; g2.K = w; g2.A = Tp; g2.lda = QR_NB; g2.ta = true; g2.B = W.p; g2.ldb = w; g2.C = W2.p; g2.ldc = w;
+    gemm(ctx, g2);
+    GemmDesc g3;  // C -= Y W2
+    g3.M = ms; g3.N = n2; g3.K = w; g3.A = Yp; g3.lda = m; g3.B = W2.p; g3.ldb = w; g3.C = C; g3.ldc = lda;
+    g3.alpha = -1.0; g3.beta = 1.0;
+    gemm(ctx, g3);
+  };
+  static const bool merge_on = [] {
+    const char* e = std::getenv("TT_B200_QR_MERGE");
+    return !(e && e[0] == '0');
+  }();
+  for (int64_t s = 0; s < f.kmax;) {
+    const int64_t ms = m - s;
+    int w = (int)std::min<int64_t>(QR_NB, f.kmax - s);
+    // narrower panels when that lets one cluster hold the panel
+    if (ms > panel_cluster_max_rows(w) && ms <= panel_cluster_max_rows(16)) w = std::min(w, 16);
+    const int w2 = (int)std::min<int64_t>(QR_NB - w, f.kmax - s - w);
+    if (merge_on && w < QR_NB && w2 > 0 && c - s - w - w2 > 0) {
+      // Two narrow panels, one wide trailing update: the second panel is brought up to date
+      // alone, factored, and the two compact-WY blocks merged (T = [[T1, -T1 Y1^T Y2 T2], [0, T2]])
+      // so that the trailing matrix -- the HBM traffic of the factorization -- is read and
+      // written once per QR_NB columns instead of once per w.
+      factor(s, w);
+      update(s, w, s + w, w2);
+      factor(s + w, w2);
+      GemmDesc gg;  // G = Y1^T Y2 over rows [s, m) (Y2 is zero above row s + w)
+      gg.M = w; gg.N = w2; gg.K = ms; gg.A = f.Y.p + s + s * m; gg.lda = m; gg.ta = true;
+      gg.B = f.Y.p + s + (s + w) * m; gg.ldb = m; gg.C = W.p; gg.ldc = w;
+      gemm(ctx, gg);
+      TTB_RUN(ctx, "aux", 0, 8.0 * 3 * QR_NB * QR_NB,
+              merge_t_kernel<<<1, 1024, 0, ctx->stream>>>(f.T.p + s * QR_NB, QR_NB, W.p, w, w, w2));
+      w += w2;
+    } else {
+      factor(s, w);
+    }
     f.pan_s.push_back(s);
     f.pan_w.push_back(w);
-    const int64_t n2 = c - s - w;
-    if (n2 > 0) {
-      double* C = A + s + (s + w) * lda;
-      GemmDesc g1;  // W = Y^T C
-      g1.M = w; g1.N = n2; g1.K = ms; g1.A = Yp; g1.lda = m; g1.ta = true; g1.B = C; g1.ldb = lda; g1.C = W.p; g1.ldc = w;
-      gemm(ctx, g1);
-      GemmDesc g2;  // W2 = T^T W
-      g2.M = w; g2.N = n2; g2.K = w; g2.A = Tp; g2.lda = QR_NB; g2.ta = true; g2.B = W.p; g2.ldb = w; g2.C = W2.p; g2.ldc = w;
-      gemm(ctx, g2);
-      GemmDesc g3;  // C -= Y W2
-      g3.M = ms; g3.N = n2; g3.K = w; g3.A = Yp; g3.lda = m; g3.B = W2.p; g3.ldb = w; g3.C = C; g3.ldc = lda;
-      g3.alpha = -1.0; g3.beta = 1.0;
-      gemm(ctx, g3);
-    }
+    update(s, w, s + w, c - s - w);
     s += w;
   }
 }
