@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--batch", type=int, default=C4_BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the Gram / driver side measurements")
+    ap.add_argument("--e2e-chunks", type=int, default=2, help="pipelined slices of the host-to-host call")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -261,7 +262,7 @@ def main():
     e2e_ms, d2h = [], 0
     # untimed calls first (the torch caching allocator sizes the slice buffers)
     for _ in range(2):
-        out_host, _, _, _ = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=2, out_host=out_host)
+        out_host, _, _, _ = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=args.e2e_chunks, out_host=out_host)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -269,7 +270,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        out_host, rk_h, nr_h, cnt = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=2,
+        out_host, rk_h, nr_h, cnt = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=args.e2e_chunks,
                                                           out_host=out_host, start_event=e0)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -407,7 +408,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(args.batch, world),
             "e2e": {"value": e2e_value, "unit": "roundings/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_steps": [round(x, 2) for x in e2e_ms], "api": "tt_round_batch_host (2 pipelined slices)"},
+                    "ms_steps": [round(x, 2) for x in e2e_ms], "api": f"tt_round_batch_host ({args.e2e_chunks} pipelined slices)"},
             "gpu_launches": launches,
             "roofline": roof,
             "kernel_profile": "CUDA events around every launch of one extra step (ctx stream)",
