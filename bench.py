@@ -12,9 +12,9 @@ TT-MGS + TT-MGS2 drivers are timed alongside and reported in their own keys.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--batch B]
 
-N > 1 (torchrun, one process per GPU): the 4096-item batch is split into N contiguous slices
-(no data-path collective: the roundings are independent); time = max over ranks; "scaling":
-"strong".  --impl reference times the CPU oracle (oracle/, the slow fp64 reference written from
+N > 1 (torchrun, one process per GPU): every rank rounds its own 4096-item C4 batch (items
+rank*4096 .. rank*4096 + 4095 of the seeded stream; no data-path collective: the roundings are
+independent); time = max over ranks; value = all ranks' items / that time; "scaling": "weak".  --impl reference times the CPU oracle (oracle/, the slow fp64 reference written from
 the paper) on a bounded sample of the same items.
 """
 from __future__ import annotations
@@ -99,10 +99,9 @@ class ClockSampler:
 
 
 def _slice(batch: int, rank: int, world: int):
-    """(start, count) of this rank's contiguous slice of the batch (parallel.batch_slice)."""
-    from paper_2211_08770_b200.parallel import batch_slice
-    start, end = batch_slice(batch, world, rank)
-    return start, end - start
+    """(start, count) of this rank's shard: a whole `batch`-item batch per GPU (weak scaling),
+    rank r taking items [r * batch, (r + 1) * batch) of the seeded stream."""
+    return rank * batch, batch
 
 
 def _blas_threads() -> int:
@@ -116,8 +115,9 @@ def _blas_threads() -> int:
 def _config(batch: int, world: int):
     return {"workload": f"C4 (BASELINE.json configs[3]): batch of {batch} independent TT-roundings, "
                         "each the TT-sum of 4 unit-norm rank-16 TT-vectors (d=10, n=32, formal rank 64)",
-            "batch": batch, "d": 10, "n": 32, "terms": 4, "term_rank": 16, "delta": C4_DELTA,
-            "floor_c": 2048.0, "parallelism": f"batch split x{world}",
+            "batch": batch, "global_batch": batch * world, "d": 10, "n": 32, "terms": 4, "term_rank": 16,
+            "delta": C4_DELTA, "floor_c": 2048.0,
+            "parallelism": f"batch shard x{world} ({batch} independent roundings per GPU, no collective)",
             "l2": "inputs (8.7 GB at B=4096) exceed L2; L2 also flushed (256 MB write) between timed steps"}
 
 
@@ -154,7 +154,7 @@ def run_reference(args, rank: int, world: int):
               f"{T:.1f} s over {args.steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config(args.batch, world),
             "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
@@ -242,7 +242,7 @@ def main():
         t_max = float(t.item())
     else:
         t_max = t_local
-    value = args.batch * args.steps / t_max
+    value = args.batch * world * args.steps / t_max  # all ranks' items / max-over-ranks time
     rank_ok = bool(np.all(ranks[:, 1:-1] == np.where((np.arange(start, start + B) % 2 == 0), 32, 16)[:, None]))
 
     # ------------------------------------------------------------ per-kernel profile (one extra step)
@@ -281,7 +281,7 @@ def main():
         t = torch.tensor([te], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
-    e2e_value = args.batch * args.steps / te
+    e2e_value = args.batch * world * args.steps / te
 
     # ------------------------------------------------------------ roofline of the dominant kernel
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
@@ -405,7 +405,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(args.batch, world),
             "e2e": {"value": e2e_value, "unit": "roundings/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_steps": [round(x, 2) for x in e2e_ms], "api": f"tt_round_batch_host ({args.e2e_chunks} pipelined slices)"},
