@@ -337,18 +337,44 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
     coeffs = np.asarray(coeffs, dtype=np.float64).reshape(B, K)
     norms_a = None if norms is None else np.asarray(norms, dtype=np.float64).reshape(B, K)
     dev = f"cuda:{ctx.device}"
-    copy = torch.cuda.Stream(ctx.device)   # host -> device (one copy engine)
-    back = torch.cuda.Stream(ctx.device)   # device -> host (the other direction's engine)
+    bounds = [(B * c) // chunks for c in range(chunks + 1)]
+    per_item = [[int(np.prod(x.shape[1:])) for x in term] for term in host_terms]
+    item_doubles = sum(sum(t) for t in per_item)
+    need = max(bounds[c + 1] - bounds[c] for c in range(chunks)) * item_doubles
+    # Streams and two device staging buffers persist on the context: fresh streams would make
+    # the caching allocator hand out new blocks (cudaMalloc) every call, and per-tensor
+    # allocations cost more than the copies themselves.
+    pipe = getattr(ctx, "_host_pipe", None)
+    if pipe is None or pipe["cap"] < need:
+        if pipe is not None:
+            torch.cuda.synchronize(ctx.device)
+        pipe = {"copy": torch.cuda.Stream(ctx.device),   # host -> device (one copy engine)
+                "back": torch.cuda.Stream(ctx.device),   # device -> host (the other direction's)
+                "cap": need,
+                "stage": [torch.empty(need, dtype=torch.float64, device=dev) for _ in range(2)]}
+        torch.cuda.synchronize(ctx.device)
+        ctx._host_pipe = pipe
+    copy, back = pipe["copy"], pipe["back"]
     if start_event is not None:
         copy.wait_event(start_event)
         back.wait_event(start_event)
-    bounds = [(B * c) // chunks for c in range(chunks + 1)]
-    staged, events = [], []
+    staged, consumed = [], []
 
     def h2d(c):
         a, b = bounds[c], bounds[c + 1]
+        buf = pipe["stage"][c % 2]
+        if c >= 2:
+            copy.wait_event(consumed[c - 2])  # slice c-2's rounding has read this buffer
+        t, off = [], 0
         with torch.cuda.stream(copy):
-            t = [[x[a:b].to(dev, non_blocking=True) for x in term] for term in host_terms]
+            for term, sizes in zip(host_terms, per_item):
+                row = []
+                for x, sz in zip(term, sizes):
+                    v = buf[off:off + (b - a) * sz].view((b - a,) + tuple(x.shape[1:]))
+                    v.copy_(x[a:b], non_blocking=True)
+                    row.append(v)
+                    off += (b - a) * sz
+                t.append(row)
             ev = torch.cuda.Event()
             ev.record(copy)
         return t, ev
@@ -370,6 +396,9 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
             res = tt_round_batch_strided(ctx, t, coeffs[a:b], rel_tol,
                                          norms=None if norms_a is None else norms_a[a:b],
                                          floor_c=floor_c, max_rank=max_rank)
+        used = torch.cuda.Event()
+        used.record(ctx.stream)
+        consumed.append(used)
         ranks.append(res.ranks)
         nrm.append(res.norms)
         n = res.total_doubles()

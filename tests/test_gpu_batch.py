@@ -213,6 +213,28 @@ def test_batch_host_pipeline_matches_device_call():
     np.testing.assert_array_equal(norms, res.norms)
 
 
+def test_batch_host_pipeline_back_to_back_c4_shape():
+    """Two back-to-back host-to-host calls at the C4 item shape with 4 slices: the slices'
+    device inputs (allocated on the copy stream, read on the context stream) are not recycled
+    while still being read; both calls return the device call's bytes."""
+    import torch
+    import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums_stacked
+    B = 600
+    cores, coeffs = make_batch_sums_stacked(B, start=1000)
+    host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores]
+    res = P.tt_round_batch_strided(ctx(), [[c.cuda() for c in term] for term in host], coeffs, 1e-6,
+                                   norms=np.ones((B, 4)))
+    flat = np.concatenate([np.concatenate([c.ravel() for c in res.item_numpy(b)]) for b in range(B)])
+    outs = []
+    for _ in range(2):
+        out, ranks, _, cnt = P.tt_round_batch_host(ctx(), host, coeffs, 1e-6, norms=np.ones((B, 4)), chunks=4)
+        outs.append((out[:cnt].numpy().copy(), ranks))
+    for o, rk in outs:
+        assert np.array_equal(rk, res.ranks)
+        assert np.array_equal(o, flat)
+
+
 def test_batch_strided_unsupported_shape_and_serial_fallback():
     """Formal rank > 64 is outside the batched engine: tt_round_batch_strided reports
     TT_ENOTSUP, tt_round_batch falls back to the per-item rounding (still oracle-exact)."""
