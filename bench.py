@@ -171,7 +171,7 @@ def main():
     ap.add_argument("--batch", type=int, default=C4_BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the Gram / driver side measurements")
-    ap.add_argument("--e2e-chunks", type=int, default=2, help="pipelined slices of the host-to-host call")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="pipelined slices of the host-to-host call")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

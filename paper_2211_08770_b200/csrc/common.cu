@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstring>
 #include <sstream>
 
@@ -110,6 +111,18 @@ static void staged_done(tt_ctx c, const char* src, size_t bytes) {
   }
 }
 
+// Device-side copy out of the pinned ring (mapped host memory, same address under UVA): an SM
+// load over PCIe instead of a copy-engine transfer, so a small descriptor upload is never
+// queued behind a caller's multi-GB host-to-device copy on another stream (the copy engine
+// serves transfers in submission order).
+__global__ void upload_kernel(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src,
+                              size_t words, unsigned char* __restrict__ dtail, const unsigned char* __restrict__ stail,
+                              int tail) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && (int)threadIdx.x < tail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+
 void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
   if (p && ctx) cudaFreeAsync(p, ctx->stream);
   ctx = c;
@@ -123,7 +136,14 @@ void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
   }
   const char* src = stage_pinned(c, host, bytes);
   if (src) {
-    TTB_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    const size_t words = bytes / 8;
+    const int tail = (int)(bytes - words * 8);
+    const int blocks = (int)std::min<size_t>(std::max<size_t>((words + 255) / 256, 1), 64);
+    TTB_RUN(c, "aux", 0.0, 2.0 * bytes,
+            upload_kernel<<<blocks, 256, 0, c->stream>>>(
+                static_cast<unsigned long long*>(p), reinterpret_cast<const unsigned long long*>(src), words,
+                static_cast<unsigned char*>(p) + words * 8, reinterpret_cast<const unsigned char*>(src) + words * 8,
+                tail));
     staged_done(c, src, bytes);
   } else {
     TTB_CUDA(cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, c->stream));
