@@ -255,7 +255,7 @@ def main():
 
     # ------------------------------------------------------------ end to end (pinned host buffers)
     # the public host-to-host call: inputs copied from pinned memory and results copied back
-    # inside the timed region, pipelined over 2 slices (tt_round_batch_host)
+    # inside the timed region, pipelined over --e2e-chunks slices (tt_round_batch_host)
     host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores_h]
     h2d = sum(x.numel() * 8 for term in host for x in term)
     out_host = torch.empty(out_doubles + 4096, dtype=torch.float64).pin_memory()

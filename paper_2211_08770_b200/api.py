@@ -322,7 +322,7 @@ def tt_round_batch_strided(ctx: Context, terms, coeffs, rel_tol: float, norms=No
 
 
 def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=None,
-                        floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0, chunks: int = 2,
+                        floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0, chunks: int = 4,
                         out_host: Optional[torch.Tensor] = None, start_event=None):
     """End-to-end batched rounding from HOST inputs to HOST results, pipelined over `chunks`
     contiguous slices of the batch: the host->device copy of slice c+1 (one copy stream) and
