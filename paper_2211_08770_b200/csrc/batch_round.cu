@@ -1425,10 +1425,10 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   }
   // ---------------------------------------------------------------- device tables
   BBuf dsh, dtab, dcoef, dscale;
-  dsh.upload(ctx, &sh, sizeof(sh));
-  dtab.upload(ctx, in.tab.data(), in.tab.size() * sizeof(double*));
-  dcoef.upload(ctx, in.coef.data(), in.coef.size() * sizeof(double));
-  dscale.upload(ctx, scale.data(), scale.size() * sizeof(double));
+  dsh.upload(ctx, &sh, sizeof(sh), true);
+  dtab.upload(ctx, in.tab.data(), in.tab.size() * sizeof(double*), true);
+  dcoef.upload(ctx, in.coef.data(), in.coef.size() * sizeof(double), true);
+  dscale.upload(ctx, scale.data(), scale.size() * sizeof(double), true);
   // ---------------------------------------------------------------- waves
   stamp("tables uploaded");
   size_t free_b = 0, total_b = 0;
@@ -1588,9 +1588,9 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       res.arena_size.push_back(tot);
       res.wave_first.push_back(w0);
       BBuf ddst, dsz, dooff;
-      ddst.upload(ctx, dst.data(), dst.size() * sizeof(int64_t));
-      dsz.upload(ctx, sz.data(), sz.size() * sizeof(int64_t));
-      dooff.upload(ctx, sh.ooff, sizeof(int64_t) * d);
+      ddst.upload(ctx, dst.data(), dst.size() * sizeof(int64_t), true);
+      dsz.upload(ctx, sz.data(), sz.size() * sizeof(int64_t), true);
+      dooff.upload(ctx, sh.ooff, sizeof(int64_t) * d, true);
       stamp("arena allocated");
       TTB_RUN(ctx, "batch_compact", 0.0, 16.0 * (double)tot,
               br_compact_kernel<<<nb, 256, 0, ctx->stream>>>(O.p, sh.ostride, static_cast<const int64_t*>(dooff.p),

@@ -123,7 +123,7 @@ __global__ void upload_kernel(unsigned long long* __restrict__ dst, const unsign
   if (blockIdx.x == 0 && (int)threadIdx.x < tail) dtail[threadIdx.x] = stail[threadIdx.x];
 }
 
-void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
+void BBuf::upload(tt_ctx c, const void* host, size_t bytes, bool via_sm) {
   if (p && ctx) cudaFreeAsync(p, ctx->stream);
   ctx = c;
   p = nullptr;
@@ -135,7 +135,10 @@ void BBuf::upload(tt_ctx c, const void* host, size_t bytes) {
     fail(TT_ENOMEM, "descriptor allocation failed");
   }
   const char* src = stage_pinned(c, host, bytes);
-  if (src) {
+  if (src && !via_sm) {
+    TTB_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    staged_done(c, src, bytes);
+  } else if (src) {
     const size_t words = bytes / 8;
     const int tail = (int)(bytes - words * 8);
     const int blocks = (int)std::min<size_t>(std::max<size_t>((words + 255) / 256, 1), 64);

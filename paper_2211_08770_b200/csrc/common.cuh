@@ -128,7 +128,9 @@ struct BBuf {  // raw byte device buffer (descriptor tables)
   BBuf(const BBuf&) = delete;
   BBuf& operator=(const BBuf&) = delete;
   // allocate and copy `bytes` from host (pageable copy: the host buffer may be reused on return)
-  void upload(tt_ctx c, const void* host, size_t bytes);
+  // via_sm: copy out of the pinned ring with a kernel instead of the copy engine (for uploads
+  // that must not queue behind a caller's bulk transfer on another stream)
+  void upload(tt_ctx c, const void* host, size_t bytes, bool via_sm = false);
 };
 
 // ------------------------------------------------------------------ profiling
