@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -135,7 +136,11 @@ void BBuf::upload(tt_ctx c, const void* host, size_t bytes, bool via_sm) {
     fail(TT_ENOMEM, "descriptor allocation failed");
   }
   const char* src = stage_pinned(c, host, bytes);
-  if (src && !via_sm) {
+  static const bool sm_ok = [] {
+    const char* e = std::getenv("TT_B200_UPLOAD_SM");
+    return !(e && e[0] == '0');
+  }();
+  if (src && !(via_sm && sm_ok)) {
     TTB_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, c->stream));
     staged_done(c, src, bytes);
   } else if (src) {
