@@ -337,7 +337,13 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
     coeffs = np.asarray(coeffs, dtype=np.float64).reshape(B, K)
     norms_a = None if norms is None else np.asarray(norms, dtype=np.float64).reshape(B, K)
     dev = f"cuda:{ctx.device}"
-    bounds = [(B * c) // chunks for c in range(chunks + 1)]
+    # slice size: about B / chunks rounded to whole waves of the engine (one CTA per item, 2 per
+    # SM in the right-to-left kernel, 3 in the left-to-right ones: 6 x SMs items fill both), so
+    # the slices add no partial waves beyond the one of the whole batch
+    wave = 6 * torch.cuda.get_device_properties(ctx.device).multi_processor_count
+    step = max(wave, int(round(B / max(chunks, 1) / wave)) * wave) if B > wave * chunks else -(-B // max(chunks, 1))
+    bounds = list(range(0, B, max(step, 1))) + [B]
+    chunks = len(bounds) - 1
     per_item = [[int(np.prod(x.shape[1:])) for x in term] for term in host_terms]
     item_doubles = sum(sum(t) for t in per_item)
     need = max(bounds[c + 1] - bounds[c] for c in range(chunks)) * item_doubles
