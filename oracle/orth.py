@@ -28,6 +28,25 @@ from .rounding import DEFAULT_FLOOR_C, RoundInfo, tt_round_sum
 from .tt import TT, canonical_tt, element, modes, phi, tt_dot, tt_norm, tt_scale, tt_sum
 
 
+class NumericalDefect(Exception):
+    """TTH-vec with the literal beta (Alg. 6 line 10): ||a||^2 - s below
+    -1e-12 ||a||^2 (clamped to 0 when within that tolerance).  ``index`` is the
+    0-based step."""
+
+    def __init__(self, index: int):
+        super().__init__(f"||a||^2 - s < 0 in TTH-vec at step {index}")
+        self.index = index
+
+
+def _literal_beta(a_norm: float, s: float, i: int) -> float:
+    """beta = sqrt(||a||^2 - s) as Alg. 6 line 10 prints it, with SPEC.md:436's
+    defect rule; i is 1-based."""
+    d2 = a_norm * a_norm - s
+    if d2 < -1e-12 * a_norm * a_norm:
+        raise NumericalDefect(i - 1)
+    return float(np.sqrt(max(d2, 0.0)))
+
+
 class LinearDependence(Exception):
     def __init__(self, index: int):
         super().__init__(f"linear dependence at step {index}")
@@ -248,7 +267,7 @@ def tth_vec_literal(a: TT, i: int, delta: float, floor_c: float, hh_beta: str = 
     ei = canonical_tt(i, n)
     sg = _sign(tt_dot(a, ei))
     if hh_beta == "literal":                                 # line 10 as printed
-        beta = np.sqrt(max(an * an - s, 0.0))
+        beta = _literal_beta(an, s, i)
     else:                                                    # A9: beta = ||round(a - sum r_j e_j)||
         beta = _last_core_norm(w1)
     r[i - 1] = sg * beta
@@ -337,7 +356,7 @@ def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLO
         w1, info1 = tt_round_sum(terms, coefs, delta, floor_c=floor_c, term_norms=tn1)
         _record(res, terms, coefs, tn1, w1, info1)
         sg = _sign(ew[i - 1])
-        beta = np.sqrt(max(w_norm ** 2 - s, 0.0)) if hh_beta == "literal" else _last_core_norm(w1)
+        beta = _literal_beta(w_norm, s, i) if hh_beta == "literal" else _last_core_norm(w1)
         r[i - 1] = sg * beta
         w1n = _last_core_norm(w1)
         t2, c2 = [w1, canonical_tt(i, n)], [1.0, -r[i - 1]]

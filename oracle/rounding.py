@@ -47,7 +47,12 @@ def threshold(delta: float, norm: float, d: int, floor_c: float, scale: float) -
 
 
 def tt_round(x: TT, delta: float, floor_c: float = 0.0, scale: Optional[float] = None,
-             max_rank: Optional[int] = None) -> tuple[TT, RoundInfo]:
+             max_rank: Optional[int] = None,
+             force_ranks: Optional[Sequence[int]] = None) -> tuple[TT, RoundInfo]:
+    """force_ranks (test use only): force rho_k = min(ranks[k], #singular values) at every split
+    instead of the threshold rule -- the same truncation as another implementation that chose
+    those ranks, for comparing reconstructions where a decision sits inside the window of tau
+    (SURVEY.md §8(c) C6 item 1)."""
     check_tt(x)
     d = len(x)
     formal = [1] + [c.shape[2] for c in x]
@@ -82,6 +87,8 @@ def tt_round(x: TT, delta: float, floor_c: float = 0.0, scale: Optional[float] =
         Y = cores[k].reshape(r0 * n, r1)
         U, S, Vt = np.linalg.svd(Y, full_matrices=False)
         rho = truncation_rank(S, tau, keep_all=keep_all)
+        if force_ranks is not None:
+            rho = max(1, min(int(force_ranks[k + 1]), len(S)))
         if max_rank is not None:
             rho = max(1, min(rho, int(max_rank)))
         sigmas.append(S)
@@ -102,9 +109,10 @@ def sum_scale(terms: Sequence[TT], coeffs: Sequence[float],
 
 def tt_round_sum(terms: Sequence[TT], coeffs: Sequence[float], delta: float,
                  floor_c: float = 0.0, term_norms: Optional[Sequence[float]] = None,
-                 max_rank: Optional[int] = None) -> tuple[TT, RoundInfo]:
+                 max_rank: Optional[int] = None,
+                 force_ranks: Optional[Sequence[int]] = None) -> tuple[TT, RoundInfo]:
     """Round the TT-sum sum_l c_l y_l, materialised literally."""
     s = sum_scale(terms, coeffs, term_norms) if (floor_c > 0.0) else None
     x = tt_sum(terms, coeffs)
-    out, info = tt_round(x, delta, floor_c=floor_c, scale=s, max_rank=max_rank)
+    out, info = tt_round(x, delta, floor_c=floor_c, scale=s, max_rank=max_rank, force_ranks=force_ranks)
     return out, info

@@ -412,6 +412,7 @@ def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=
             out_host = torch.empty(0, dtype=torch.float64)
         if out_host.numel() < offset + n:
             grown = torch.empty(int((offset + n) * (chunks / (c + 1)) * 1.05) + 1024, dtype=torch.float64).pin_memory()
+            back.synchronize()  # earlier slices' device->host copies into out_host have landed
             grown[:offset].copy_(out_host[:offset])
             out_host = grown
         # device -> host of this slice on the copy stream, overlapping the next slice's rounding

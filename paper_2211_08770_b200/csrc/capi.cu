@@ -96,7 +96,18 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
 
 tt_status tt_ctx_set_stream(tt_ctx ctx, void* stream) {
   if (!ctx) return TT_EINVAL;
-  ctx->stream = static_cast<cudaStream_t>(stream);
+  cudaStream_t ns = static_cast<cudaStream_t>(stream);
+  if (ns == ctx->stream) return TT_OK;
+  // Work already queued on the old stream may still use the context's scratch, pooled blocks
+  // freed with cudaFreeAsync and descriptor uploads: the new stream waits for all of it.
+  cudaEvent_t ev;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(ev, ctx->stream) != cudaSuccess || cudaStreamWaitEvent(ns, ev, 0) != cudaSuccess) {
+    ctx->last_error = std::string("tt_ctx_set_stream: ") + cudaGetErrorString(cudaGetLastError());
+    return TT_ECUDA;
+  }
+  cudaEventDestroy(ev);
+  ctx->stream = ns;
   return TT_OK;
 }
 
@@ -354,6 +365,7 @@ tt_status tt_round_batch(tt_ctx ctx, int32_t B, const int32_t* K, const double* 
     const char* ser = std::getenv("TT_B200_BATCH_SERIAL");
     if (!(ser && ser[0] == '1') && batch_uniform_supported(B, items, nullptr)) {
       round_batch_uniform(ctx, items, o, out, ranks_out);
+      TTB_CUDA(cudaStreamSynchronize(ctx->stream));  // results valid for any stream (header)
       return;
     }
     int done = 0;
@@ -406,6 +418,9 @@ tt_status tt_round_batch_strided(tt_ctx ctx, int32_t B, int32_t K, int32_t d, co
     try {
       if (B > 0) run_batch(ctx, in, resolve(opts), bt->res);
       else { bt->res.d = d; bt->res.n = in.n; }
+      // the result arenas are filled by the compaction queued last: synchronise so the
+      // handle's pointers are valid for any stream (include/tt_b200.h)
+      TTB_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       delete bt;
       throw;

@@ -26,7 +26,7 @@ from oracle import metrics, orth, rounding, tt
 from oracle.dense import U_ROUND
 from ttinputs import CONFIGS, make_shared_tail_set
 
-from gpu_util import ctx, cuda_ok, dev, diff_norm, rank_window_ok
+from gpu_util import assert_round_parity, ctx, cuda_ok, dev, diff_norm
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
 
@@ -85,7 +85,7 @@ def _check(kind, st, delta, Q, R, rep, ref):
                 continue
             lo = min(ranks_g[t], max(info.ranks))
             gaps = [abs(np.sqrt(np.sum(S[lo:] ** 2)) - info.tau) / info.tau for S in info.sigmas if len(S) > lo]
-            assert gaps and min(gaps) <= max(1e-9, amp(m - 1)), (kind, t, ranks_g[t], max(info.ranks), min(gaps))
+            assert gaps and min(gaps) <= max(1e-12, amp(m - 1)), (kind, t, ranks_g[t], max(info.ranks), min(gaps))
     hh = (kind == "householder")
     sg, sc = _signs(R), _signs(ref.R)
     Rg = sg[:, None] * R if hh else R
@@ -110,9 +110,8 @@ def _teacher_forced(kind, st, delta, ref):
         info = ref.infos[t]
         out, ginfo = P.tt_round(ctx(), [dev(x, nr) for x, nr in zip(terms, norms)], list(coefs), delta)
         assert abs(ginfo["norm"] - info.norm) <= 1e-12 * info.scale, (kind, t)
-        assert rank_window_ok(out.ranks, info), (kind, t, out.ranks, info.ranks)
-        if out.ranks == info.ranks:
-            assert diff_norm(out.to_numpy(), ref.outputs[t]) <= 1e-10 * info.scale, (kind, t)
+        assert_round_parity(out.to_numpy(), out.ranks, terms, list(coefs), delta, FLOOR_C, norms, info=info,
+                            ref=ref.outputs[t], tag=f"{kind}#{t}")
 
 
 @pytest.mark.parametrize("kind", KINDS)
@@ -247,3 +246,52 @@ def test_cgs_sharded_driver_matches_tt_orth(kind):
     assert np.linalg.norm(Rs - R) <= max(1e-10, amp(len(A) - 1)) * np.linalg.norm(R)
     for i, (qs, q) in enumerate(zip(Qs, Q)):
         assert diff_norm(qs.to_numpy(), q.to_numpy()) <= max(1e-10, amp(i)), (kind, i)
+
+
+def test_orth_householder_beta_literal():
+    """hh_beta_literal = 1: beta = sqrt(||w||^2 - s) exactly as Alg. 6 line 10 prints it
+     against the oracle's literal branch (pinned in test_oracle_orth.py):
+    well-conditioned (kappa = 1e2, closed form R = R_M) and C1 (kappa = 1e8)."""
+    import paper_2211_08770_b200 as P
+    c1 = CONFIGS["C1"]
+    for st, delta in ((make_shared_tail_set(4, 8, 3, 10, 1e2, seed=991), 1e-12),
+                      (make_shared_tail_set(c1.d, c1.n, c1.r, c1.m, c1.kappa, c1.seed), c1.delta)):
+        ref = orth.orth("householder", st.tensors, delta, hh_beta="literal")
+        Q, R, rep = P.tt_orth(ctx(), "householder", [dev(a) for a in st.tensors], delta, hh_beta_literal=True,
+                              want_loo=True)
+        _check("householder", st, delta, Q, R, rep, ref)
+        if st.kappa <= 1e2:
+            qm, rm = st.qr_exact()
+            assert np.linalg.norm(_signs(R)[:, None] * R - rm) <= 1e-9 * np.linalg.norm(rm)
+
+
+def test_orth_c3_full_gram_closed_form():
+    """BASELINE configs[2] TT-Gram at full size (m = 50, d = 16, n = 64, r = 20, kappa = 1e6,
+    delta = 1e-5), against the shared-tail closed forms: the GPU Gram matrix equals M^T M
+    (north star 1e-10; here 1e-13), the GPU's R is the Cholesky factor of that Gram matrix
+    (oracle.dense.cholesky on the same bytes, 1e-13), R = R_M within the Cholesky perturbation of
+    kappa(G) = 1e12 (observed ~5 u kappa(M); bar 1e-9, as for the reduced-m C3 test), Table 1
+    count, and q_i = B Q_M[:, i] on the forward-stable prefix (u kappa_i^2 <= 1e-11)."""
+    import paper_2211_08770_b200 as P
+    from oracle import dense
+    c = CONFIGS["C3"]
+    st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed)
+    A = [dev(a) for a in st.tensors]
+    G = P.tt_gram(ctx(), A).cpu().numpy()
+    Gx = st.gram_exact()
+    assert np.linalg.norm(G - Gx) <= 1e-13 * np.linalg.norm(Gx)
+    Q, R, rep = P.tt_orth(ctx(), "gram", A, c.delta, want_loo=True)
+    assert rep["rounding_calls"] == c.m
+    Rc = dense.cholesky(G).T
+    assert np.linalg.norm(R - Rc) <= 1e-13 * np.linalg.norm(Rc)
+    qm, rm = st.qr_exact()
+    assert np.linalg.norm(R - rm) <= 1e-9 * np.linalg.norm(rm)
+    assert np.all(R[np.tril_indices(c.m, -1)] == 0.0)
+    kap = _kappas(st)
+    stable = [i for i in range(c.m) if U_ROUND * kap[i] ** 2 <= 1e-11]
+    assert len(stable) >= 15
+    for i in stable[::5]:
+        amp = FLOOR_C * U_ROUND * c.m * kap[i] ** 2
+        assert diff_norm(Q[i].to_numpy(), st.q_exact(i)) <= max(1e-10, amp), (i, amp)
+    loo = rep["loo_per_step"]
+    assert np.all(loo <= np.maximum(64 * c.m * U_ROUND * kap ** 2, 1e-14))

@@ -10,7 +10,7 @@ import pytest
 from oracle import rounding, tt
 from ttinputs import make_batch_sums, make_random_tt, make_shared_tail_set
 
-from gpu_util import ctx, cuda_ok, dev, diff_norm, rank_window_ok
+from gpu_util import assert_round_parity, ctx, cuda_ok, dev, diff_norm
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
 
@@ -46,11 +46,9 @@ def test_round_random_sums(seed, delta):
     out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, delta, floor_c=floor_c)
     g = out.to_numpy()
     assert abs(ginfo["norm"] - info.norm) <= 1e-13 * info.scale
-    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
+    assert_round_parity(g, out.ranks, terms, coeffs, delta, floor_c, norms, info=info, ref=ref, tag=f"round{seed}")
     x = tt.tt_sum(terms, coeffs)
     s = info.scale
-    if out.ranks == info.ranks:
-        assert diff_norm(g, ref) <= 1e-10 * s
     # the contract ||x - x~|| <= delta ||x|| (+ floor) on the GPU output itself
     d = len(terms[0])
     tol = max(delta * info.norm, np.sqrt(d - 1) * info.tau) * (1 + 1e-8) + 1e-13 * s
@@ -131,12 +129,11 @@ def test_round_tall_panels_qr_then_qrcp(distinct):
     ref, info = rounding.tt_round_sum(terms, coeffs, 1e-8, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
     out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-8)
     assert abs(ginfo["norm"] - info.norm) <= 1e-13 * info.scale
-    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
     if distinct == 5:
         assert out.ranks == [1, 64, 80, 64, 1]
     g = out.to_numpy()
-    if out.ranks == info.ranks:
-        assert diff_norm(g, ref) <= 1e-10 * info.scale
+    assert_round_parity(g, out.ranks, terms, coeffs, 1e-8, rounding.DEFAULT_FLOOR_C, norms, info=info, ref=ref,
+                        tag="tall")
     x = tt.tt_sum(terms, coeffs)
     assert diff_norm(x, g) <= 1e-8 * info.norm * (1 + 1e-8) + np.sqrt(d - 1) * info.tau
 
@@ -155,10 +152,9 @@ def test_round_wide_panel_grid_qrcp():
     ref, info = rounding.tt_round_sum(terms, coeffs, 1e-10, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
     out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-10)
     assert abs(ginfo["norm"] - info.norm) <= 1e-13 * info.scale
-    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
     g = out.to_numpy()
-    if out.ranks == info.ranks:
-        assert diff_norm(g, ref) <= 1e-10 * info.scale
+    assert_round_parity(g, out.ranks, terms, coeffs, 1e-10, rounding.DEFAULT_FLOOR_C, norms, info=info, ref=ref,
+                        tag="grid_qrcp")
     x = tt.tt_sum(terms, coeffs)
     assert diff_norm(x, g) <= 1e-10 * info.norm * (1 + 1e-8) + np.sqrt(d - 1) * info.tau
 
@@ -174,11 +170,10 @@ def test_round_large_rank_grid_jacobi():
     norms = [tt.tt_norm(t) for t in terms]
     ref, info = rounding.tt_round_sum(terms, coeffs, 1e-10, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=norms)
     out, ginfo = P.tt_round(ctx(), [dev(t, nr) for t, nr in zip(terms, norms)], coeffs, 1e-10)
-    assert rank_window_ok(out.ranks, info), (out.ranks, info.ranks)
     assert min(out.ranks[1:-1]) >= 128
     g = out.to_numpy()
-    if out.ranks == info.ranks:
-        assert diff_norm(g, ref) <= 1e-10 * info.scale
+    assert_round_parity(g, out.ranks, terms, coeffs, 1e-10, rounding.DEFAULT_FLOOR_C, norms, info=info, ref=ref,
+                        tag="grid_jacobi")
     for k in range(2):
         U = g[k].reshape(-1, g[k].shape[2])
         assert np.linalg.norm(U.T @ U - np.eye(U.shape[1])) <= 1e-12

@@ -213,3 +213,51 @@ def test_oracle_self_spread():
     noisy = (np.maximum(l1, l2) > 1e-14)
     assert np.any(ratio[noisy] > 2.0)
     assert np.all(np.maximum(l1, l2) <= np.maximum(64 * st.m * dense.U_ROUND * kap ** 2, 1e-14))
+
+
+# ---- hh_beta = "literal": Alg. 6 line 10 as printed, beta = sqrt(||a||^2 - s)
+def test_literal_beta_defect_rule_hand_values():
+    """||a||^2 - s < -1e-12 ||a||^2 -> NumericalDefect (0-based step); within the
+    tolerance it clamps to 0; otherwise the plain square root."""
+    assert orth._literal_beta(1.0, 1.0 + 1e-13, 1) == 0.0
+    with pytest.raises(orth.NumericalDefect) as ei:
+        orth._literal_beta(1.0, 1.0 + 1e-11, 3)
+    assert ei.value.index == 2
+    assert orth._literal_beta(5.0, 16.0, 2) == 3.0   # sqrt(25 - 16)
+
+
+def test_literal_beta_closed_form_and_dense_householder():
+    """Well-conditioned input (kappa = 1e2): the literal beta gives R = R_M up to D = diag(sign)
+    (closed form of the shared-tail construction) and the dense Householder R of the densified
+    vectors; literal == lazy."""
+    st = make_shared_tail_set(4, 8, 3, 10, 1e2, seed=991)
+    lit = orth.orth("householder", st.tensors, 1e-12, literal=True, hh_beta="literal")
+    laz = orth.orth("householder", st.tensors, 1e-12, hh_beta="literal")
+    qm, rm = st.qr_exact()
+    for res in (lit, laz):
+        R, s = _sign_fix(res.R)
+        assert np.linalg.norm(R - rm) <= 1e-9 * np.linalg.norm(rm)
+    assert np.linalg.norm(lit.R - laz.R) <= 1e-12 * np.linalg.norm(lit.R)
+    small = make_shared_tail_set(3, 4, 2, 5, 1e2, seed=17)
+    res = orth.orth("householder", small.tensors, 1e-14, hh_beta="literal")
+    Ad = np.stack([tt.densify(a) for a in small.tensors], axis=1)
+    _, Rd = np.linalg.qr(Ad)
+    Rd, _ = _sign_fix(Rd)
+    Rt, _ = _sign_fix(res.R)
+    assert np.linalg.norm(Rt - Rd) <= 1e-10 * np.linalg.norm(Rd)
+
+
+def test_literal_beta_cancels_at_high_kappa_reading_a9():
+    """Reading A9: the literal beta = sqrt(||a||^2 - s) cancels when a_i is nearly in
+    span(e_1..e_{i-1}); at kappa = 1e8 its R(i,i) carry ~1e-3 relative error where the
+    rounding-norm beta keeps ~2e-5 (both forms stay normwise backward stable: ||R - R_M||_F
+    at the rounding noise)."""
+    st = make_shared_tail_set(4, 8, 3, 10, 1e8, seed=991)
+    qm, rm = st.qr_exact()
+    err = {}
+    for hb in ("literal", "round_norm"):
+        R, _ = _sign_fix(orth.orth("householder", st.tensors, 1e-14, hh_beta=hb).R)
+        assert np.linalg.norm(R - rm) <= 1e-9 * np.linalg.norm(rm)
+        err[hb] = np.max(np.abs(np.diag(R) - np.diag(rm)) / np.abs(np.diag(rm)))
+    assert err["round_norm"] <= 1e-4
+    assert err["literal"] >= 1e-4 and err["literal"] >= 10 * err["round_norm"]
