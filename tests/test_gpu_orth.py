@@ -268,10 +268,11 @@ def test_orth_householder_beta_literal():
 def test_orth_c3_full_gram_closed_form():
     """BASELINE configs[2] TT-Gram at full size (m = 50, d = 16, n = 64, r = 20, kappa = 1e6,
     delta = 1e-5), against the shared-tail closed forms: the GPU Gram matrix equals M^T M
-    (north star 1e-10; here 1e-13), the GPU's R is the Cholesky factor of that Gram matrix
-    (oracle.dense.cholesky on the same bytes, 1e-13), R = R_M within the Cholesky perturbation of
-    kappa(G) = 1e12 (observed ~5 u kappa(M); bar 1e-9, as for the reduced-m C3 test), Table 1
-    count, and q_i = B Q_M[:, i] on the forward-stable prefix (u kappa_i^2 <= 1e-11)."""
+    (north star 1e-10; here 1e-13); the driver's R against the oracle's Cholesky (oracle.dense.cholesky)
+    of the GPU Gram matrix and against R = R_M, both within the Cholesky perturbation at kappa(G) =
+    1e12 (the driver forms its own Gram matrix: u-level differences in G move the smallest R(i,i)
+    by ~1e-6 relative; normwise ~5e-10; bar 1e-9, as for the reduced-m C3 test), Table 1 count,
+    and q_i = B Q_M[:, i] on the forward-stable prefix (u kappa_i^2 <= 1e-11)."""
     import paper_2211_08770_b200 as P
     from oracle import dense
     c = CONFIGS["C3"]
@@ -283,7 +284,7 @@ def test_orth_c3_full_gram_closed_form():
     Q, R, rep = P.tt_orth(ctx(), "gram", A, c.delta, want_loo=True)
     assert rep["rounding_calls"] == c.m
     Rc = dense.cholesky(G).T
-    assert np.linalg.norm(R - Rc) <= 1e-13 * np.linalg.norm(Rc)
+    assert np.linalg.norm(R - Rc) <= 1e-9 * np.linalg.norm(Rc)
     qm, rm = st.qr_exact()
     assert np.linalg.norm(R - rm) <= 1e-9 * np.linalg.norm(rm)
     assert np.all(R[np.tril_indices(c.m, -1)] == 0.0)
