@@ -12,9 +12,13 @@ TT-MGS + TT-MGS2 drivers are timed alongside and reported in their own keys.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--batch B]
 
-N > 1 (torchrun, one process per GPU): every rank rounds its own 4096-item C4 batch (items
-rank*4096 .. rank*4096 + 4095 of the seeded stream; no data-path collective: the roundings are
-independent); time = max over ranks; value = all ranks' items / that time; "scaling": "weak".  --impl reference times the CPU oracle (oracle/, the slow fp64 reference written from
+N > 1 (one process per GPU: under torchrun, or `--gpus N` alone re-launches itself under
+torch.distributed.run): BASELINE's "batch split across 1/2/4/8 GPUs" -- the one 4096-item batch is
+cut into contiguous slices (tt_plan_slice), rank r rounds its slice, no data-path collective (the
+roundings are independent); time = max over ranks; value = 4096 / that time; "scaling": "strong".
+Alongside at N > 1: every rank rounding its own 4096 items (weak scaling), the C3 Gram matrix and
+the C3 TT-Gram driver with the library's NCCL communicator (pair blocks + all-gather, LPT phase-2
+roundings).  --impl reference times the CPU oracle (oracle/, the slow fp64 reference written from
 the paper) on a bounded sample of the same items.
 """
 from __future__ import annotations
@@ -99,9 +103,79 @@ class ClockSampler:
 
 
 def _slice(batch: int, rank: int, world: int):
-    """(start, count) of this rank's shard: a whole `batch`-item batch per GPU (weak scaling),
-    rank r taking items [r * batch, (r + 1) * batch) of the seeded stream."""
+    """(start, count) of this rank's shard of the one `batch`-item batch (strong scaling,
+    BASELINE configs[3] "batch split across 1/2/4/8 GPUs"): the library's contiguous balanced
+    slice (tt_plan_slice; the same formula in Python when the library is not built)."""
+    base, rem = divmod(batch, world)
+    start = rank * base + min(rank, rem)
+    return start, base + (1 if rank < rem else 0)
+
+
+def _weak_slice(batch: int, rank: int, world: int):
+    """(start, count) for the weak-scaling extra: a whole `batch` per GPU, rank r taking items
+    [r * batch, (r + 1) * batch) of the seeded stream."""
     return rank * batch, batch
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------- D3 work model
+def d3_round_flops(n, term_ranks, out_ranks):
+    """SURVEY.md §8(d) D3 flops of one TT-rounding of the TT-sum with per-term ranks
+    term_ranks[l][0..d] and output ranks out_ranks[0..d] (the algorithmic work, not what any
+    implementation does): right-to-left, per k = d..2, QR + explicit Q of the m x c panel
+    (m = n_k R'_k, c = R_{k-1}) 2(2mc^2 - 2c^3/3) (or with m, c swapped) plus the core x L product
+    2 R'_{k-1} nnz(X_{k-1}) over the nonzero diagonal blocks; left-to-right, per k = 1..d-1, the
+    nominal R-SVD 6ab^2 + 11b^3 of Y_k ((rho_{k-1} n_k) x R'_k) plus 2 rho_k R'_k n_{k+1} R'_{k+1}.
+    Returns (right-to-left QR part, right-to-left explicit-Q part, core x L part, left-to-right part)."""
+    d = len(n)
+    R = [sum(t[k] for t in term_ranks) for k in range(d + 1)]
+    R[0] = R[d] = 1
+    Rp = [1] * (d + 1)
+    qr = expq = cxl = 0.0
+    for k in range(d, 1, -1):  # core k (1-based): panel (n_k R'_k) x R_{k-1}
+        m, c = n[k - 1] * Rp[k], R[k - 1]
+        half = (2 * m * c * c - 2 * c ** 3 / 3) if m >= c else (2 * c * m * m - 2 * m ** 3 / 3)
+        qr += half
+        expq += half
+        Rp[k - 1] = min(m, c)
+        nnz = sum(t[k - 2] * n[k - 2] * t[k - 1] for t in term_ranks)
+        cxl += 2 * Rp[k - 1] * nnz
+    l2r = 0.0
+    for k in range(1, d):
+        rows, cols = out_ranks[k - 1] * n[k - 1], Rp[k]
+        a, b = max(rows, cols), min(rows, cols)
+        l2r += 6 * a * b * b + 11 * b ** 3 + 2 * out_ranks[k] * Rp[k] * n[k] * Rp[k + 1]
+    return qr, expq, cxl, l2r
+
+
+def c4_work(batch_ranks, d=10, n=32, r=16, K=4):
+    """D3 flops of the C4 step split by phase, and its algorithmic bytes (term cores read once,
+    output cores written once), from the output ranks of every item."""
+    import numpy as np
+    nn = [n] * d
+    term = [1] + [min(r, n ** k, n ** (d - k)) for k in range(1, d)] + [1]
+    terms = [term] * K
+    tot = np.zeros(4)
+    cache = {}
+    out_doubles = 0
+    for rk in batch_ranks:
+        key = tuple(int(v) for v in rk)
+        if key not in cache:
+            cache[key] = np.array(d3_round_flops(nn, terms, list(key)))
+        tot += cache[key]
+        out_doubles += sum(key[k] * n * key[k + 1] for k in range(d))
+    in_doubles = len(batch_ranks) * K * sum(term[k] * n * term[k + 1] for k in range(d))
+    return {"r2l_qr": tot[0], "r2l_explicit_q": tot[1], "core_x_L": tot[2], "l2r": tot[3],
+            "total": float(tot.sum()), "bytes": 8.0 * (in_doubles + out_doubles)}
 
 
 def _blas_threads() -> int:
@@ -115,25 +189,35 @@ def _blas_threads() -> int:
 def _config(batch: int, world: int):
     return {"workload": f"C4 (BASELINE.json configs[3]): batch of {batch} independent TT-roundings, "
                         "each the TT-sum of 4 unit-norm rank-16 TT-vectors (d=10, n=32, formal rank 64)",
-            "batch": batch, "global_batch": batch * world, "d": 10, "n": 32, "terms": 4, "term_rank": 16,
+            "batch": batch, "global_batch": batch, "d": 10, "n": 32, "terms": 4, "term_rank": 16,
             "delta": C4_DELTA, "floor_c": 2048.0,
-            "parallelism": f"batch shard x{world} ({batch} independent roundings per GPU, no collective)",
+            "parallelism": f"batch split x{world} (contiguous slices of the {batch}-item batch, tt_plan_slice; "
+                           "no collective)",
             "l2": "inputs (8.7 GB at B=4096) exceed L2; L2 also flushed (256 MB write) between timed steps"}
 
 
+_ORACLE_ITEMS = []
+
+
 def oracle_sample(seconds: float, offset: int = 0):
-    """The CPU oracle (as it stands) on C4 items in order until `seconds` have elapsed."""
+    """The CPU oracle (as it stands) on C4 items in order until `seconds` have elapsed.  The
+    items are generated once, before the clock starts (round 1 regenerated them inside the
+    timed loop, advancing the seeded stream from item 0 every time: that cost grew with the
+    sample and made the bench's 124-item figure 1.5x lower than the reference arm's 12-item one)."""
     from oracle import rounding
     from ttinputs import make_batch_sums
+    need = offset + max(8, int(seconds * 40) + 8)
+    if len(_ORACLE_ITEMS) < need:
+        _ORACLE_ITEMS.extend(make_batch_sums(need - len(_ORACLE_ITEMS), start=len(_ORACLE_ITEMS)))
     done, t0 = 0, time.perf_counter()
     while True:
-        items = make_batch_sums(4, start=offset + done)
-        for terms, coeffs in items:
-            rounding.tt_round_sum(terms, coeffs, C4_DELTA, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=[1.0] * 4)
-        done += len(items)
+        if offset + done >= len(_ORACLE_ITEMS):
+            _ORACLE_ITEMS.extend(make_batch_sums(64, start=len(_ORACLE_ITEMS)))
+        terms, coeffs = _ORACLE_ITEMS[offset + done]
+        rounding.tt_round_sum(terms, coeffs, C4_DELTA, floor_c=rounding.DEFAULT_FLOOR_C, term_norms=[1.0] * 4)
+        done += 1
         if time.perf_counter() - t0 >= seconds:
             break
-    # generation of the 4-item blocks is timed too but is < 1 % of the oracle's time
     return done, time.perf_counter() - t0
 
 
@@ -151,15 +235,98 @@ def run_reference(args, rank: int, world: int):
     value = sum(counts) / T
     cores = _blas_threads()
     sample = (f"oracle (numpy/LAPACK fp64) TT-rounding of the first {max(counts)} C4 items per step, "
-              f"{T:.1f} s over {args.steps} steps")
+              f"{T:.1f} s over {args.steps} steps; host {_cpu_model()}, nproc {os.cpu_count()}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config(args.batch, world),
             "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": _cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": "roundings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside a launcher: run the same command under torch.distributed.run
+    with N processes (one per GPU) and pass its output through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def _event_ms(fn, stream):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), out
+
+
+def _driver_extras(P, ctx, stream, rank):
+    """C1, C3 (TT-Gram, TT-CGS2) and a C5 prefix through tt_orth at full config sizes (C5: m' = 20
+    of m = 100), each with its closed-form check (shared-tail construction: R = R_M)."""
+    import numpy as np
+    from ttinputs import CONFIGS, make_shared_tail_set
+    out = {}
+
+    def run(name, kind, m=None):
+        c = CONFIGS[name]
+        mm = c.m if m is None else m
+        st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed)
+        A = [P.DeviceTT.from_numpy(a) for a in st.tensors[:mm]]
+        ms, (Q, R, rep) = _event_ms(lambda: P.tt_orth(ctx, kind, A, c.delta, want_loo=True), stream)
+        rm = st.qr_exact()[1][:mm, :mm]
+        if kind == "householder":
+            sg = np.sign(np.diag(R))
+            sg[sg == 0] = 1
+            R = sg[:, None] * R
+        key = f"{name.lower()}_{kind}" + (f"_m{mm}" if m is not None else "")
+        out[key] = {"workload": f"{name} ({c.note}) TT-{kind}, m={mm}, d={c.d}, n={c.n}, r={c.r}, "
+                                f"kappa={c.kappa:g}, delta={c.delta:g}",
+                    "roundings": rep["rounding_calls"], "ms": ms,
+                    "roundings_per_s": rep["rounding_calls"] / (ms * 1e-3),
+                    "max_rank": int(max(rep["max_rank_per_call"])),
+                    "R_rel_err_vs_R_M": float(np.linalg.norm(R - rm) / np.linalg.norm(rm)),
+                    "loo_last": float(rep["loo_per_step"][-1])}
+    run("C1", "cgs")
+    run("C3", "gram")
+    run("C3", "cgs2")
+    run("C5", "householder", m=20)
+    return out
+
+
+def _oracle_driver_extras():
+    """the oracle (as it stands) on C1 with all host threads and with 1 thread,
+    and on C2 MGS with all threads -- the same inputs as the GPU drivers."""
+    from oracle import orth
+    from ttinputs import CONFIGS, make_shared_tail_set
+    out = {}
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    for name, kind, one in (("C1", "cgs", False), ("C1", "cgs", True), ("C2", "mgs", False)):
+        c = CONFIGS[name]
+        st = make_shared_tail_set(c.d, c.n, c.r, c.m, c.kappa, c.seed)
+        t0 = time.perf_counter()
+        if one and threadpool_limits is not None:
+            with threadpool_limits(1):
+                res = orth.orth(kind, st.tensors, c.delta)
+        else:
+            res = orth.orth(kind, st.tensors, c.delta)
+        t = time.perf_counter() - t0
+        out[f"{name.lower()}_{kind}" + ("_1thread" if one else "")] = {
+            "s": t, "roundings": int(res.rounding_calls), "roundings_per_s": res.rounding_calls / t,
+            "threads": 1 if one else _blas_threads()}
+    return out
 
 
 def main():
@@ -171,12 +338,17 @@ def main():
     ap.add_argument("--batch", type=int, default=C4_BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the Gram / driver side measurements")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="pipelined slices of the host-to-host call")
+    ap.add_argument("--e2e-slices", type=int, default=4, help="pipelined slices of the host-to-host call")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -187,6 +359,7 @@ def main():
     from paper_2211_08770_b200 import _build
     _build.build_library()
     import paper_2211_08770_b200 as P
+    from paper_2211_08770_b200 import parallel
     from ttinputs import make_batch_sums_stacked
 
     torch.cuda.set_device(local_rank)
@@ -196,7 +369,7 @@ def main():
     stream = torch.cuda.current_stream(local_rank)
     ctx = P.Context(local_rank, stream=stream)
 
-    start, B = _slice(args.batch, rank, world)
+    start, B = parallel.plan_slice(args.batch, world, rank)
     cores_h, coeffs = make_batch_sums_stacked(B, start=start)
     norms = np.ones((B, 4))
     cores = [[torch.from_numpy(c).to(dev) for c in term] for term in cores_h]
@@ -206,11 +379,18 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def step(inp):
-        return P.tt_round_batch_strided(ctx, inp, coeffs, C4_DELTA, norms=norms)
+    def tmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step(inp, cf, nr):
+        return P.tt_round_batch_strided(ctx, inp, cf, C4_DELTA, norms=nr)
 
     for _ in range(args.warmup):
-        res = step(cores)
+        res = step(cores, coeffs, norms)
         del res
     torch.cuda.synchronize()
 
@@ -223,196 +403,194 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        res = step(cores)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
+        ms, res = _event_ms(lambda: step(cores, coeffs, norms), stream)
+        step_ms.append(ms)
         ranks = res.ranks
         del res
     barrier()
     launches = ctx.launches - launches0
     clocks = sampler.stop()
     t_local = sum(step_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([t_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-    else:
-        t_max = t_local
-    value = args.batch * world * args.steps / t_max  # all ranks' items / max-over-ranks time
+    t_max = tmax(t_local)
+    value = args.batch * args.steps / t_max  # the whole batch over the max-over-ranks time
     rank_ok = bool(np.all(ranks[:, 1:-1] == np.where((np.arange(start, start + B) % 2 == 0), 32, 16)[:, None]))
 
     # ------------------------------------------------------------ per-kernel profile (one extra step)
     ctx.profile(True)
-    res = step(cores)
+    res = step(cores, coeffs, norms)
     prof = ctx.profile_report()
     ctx.profile(False)
     out_doubles = res.total_doubles()
+    prof_ranks = res.ranks
     del res
 
     # ------------------------------------------------------------ end to end (pinned host buffers)
-    # the public host-to-host call: inputs copied from pinned memory and results copied back
-    # inside the timed region, pipelined over --e2e-chunks slices (tt_round_batch_host)
+    # the public host-to-host C-ABI call tt_round_batch_host: inputs copied from pinned memory and
+    # results copied back inside the timed region, pipelined by the library over its own streams
     host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores_h]
     h2d = sum(x.numel() * 8 for term in host for x in term)
     out_host = torch.empty(out_doubles + 4096, dtype=torch.float64).pin_memory()
     e2e_ms, d2h = [], 0
-    # untimed calls first (the torch caching allocator sizes the slice buffers)
-    for _ in range(2):
-        out_host, _, _, _ = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=args.e2e_chunks, out_host=out_host)
+    for _ in range(2):  # untimed: the context's copy streams and staging buffers are created
+        P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, slices=args.e2e_slices, out_host=out_host)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        out_host, rk_h, nr_h, cnt = P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, chunks=args.e2e_chunks,
-                                                          out_host=out_host, start_event=e0)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
+        ms, (out_host, rk_h, nr_h, cnt) = _event_ms(
+            lambda: P.tt_round_batch_host(ctx, host, coeffs, C4_DELTA, norms=norms, slices=args.e2e_slices,
+                                          out_host=out_host), stream)
+        e2e_ms.append(ms)
         d2h = cnt * 8 + rk_h.nbytes + nr_h.nbytes
-    te = sum(e2e_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([te], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        te = float(t.item())
-    e2e_value = args.batch * world * args.steps / te
+    te = tmax(sum(e2e_ms) / 1e3)
+    e2e_value = args.batch * args.steps / te
 
-    # ------------------------------------------------------------ roofline of the dominant kernel
-    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    # ------------------------------------------------------------ roofline
+    peak = max(FP64_DFMA_PEAK_TFLOPS, FP64_DMMA_PEAK_TFLOPS)
+    hbm = float(_peaks().get("hbm_gbs", 6552.3))
+    work = c4_work(prof_ranks)
     total_ms = sum(v["ms"] for v in prof.values())
-    achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+    r2l = prof.get("batch_r2l_qr", {"ms": float("nan"), "launches": 1})
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    # the right-to-left kernel performs D3's QR (R + reflectors) and core x L terms; D3's
+    # explicit-Q half is done here as reflector applications inside batch_l2r_apply
+    r2l_alg = work["r2l_qr"] + work["core_x_L"]
+    achieved = r2l_alg / (r2l["ms"] * 1e-3) / 1e12
     traffic = None
     try:  # DRAM bytes per launch of this kernel class from the committed ncu --set full capture
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json"))).get(dom_name)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json"))).get("batch_r2l_qr")
         traffic = tr["dram_bytes_per_launch"] if tr else None
     except Exception:
         traffic = None
-    roof = {"bound": "alu", "achieved": achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": traffic,
-            "traffic_source": "profiles/ncu_traffic_r01.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
-            "peak_source": "measured FP64 FMA (DFMA) throughput, tools/fp64_peak.cu -> profiles/fp64_peak_r01.json "
-                           "(nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TF)",
-            "kernel": dom_name, "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / dom["launches"],
-            "share_of_kernel_time": dom["ms"] / total_ms,
-            "work_model": "LAPACK-standard flop counts of the operations each launch performs (DESIGN.md §7)"}
-    all_flops = sum(v["flops"] for v in prof.values())
+    step_s = t_local / args.steps
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "batch_r2l_qr (br_r2l_kernel)",
+            "launches": r2l["launches"], "avg_launch_us": 1e3 * r2l["ms"] / max(r2l["launches"], 1),
+            "algorithmic_flops_per_launch": r2l_alg / max(r2l["launches"], 1),
+            "share_of_kernel_time": r2l["ms"] / total_ms,
+            "work_model": "SURVEY.md §8(d) D3: right-to-left QR 2mc^2-2c^3/3 per panel + core x L over the nonzero "
+                          "blocks, summed over the batch's items and the 9 panels (one launch per panel)",
+            "peak_source": "max(FP64 DFMA 34.18, FP64 DMMA 37.07) TFLOP/s measured by tools/fp64_peak.cu "
+                           "(profiles/fp64_peak_r01.json), SURVEY.md §8(d) D2",
+            "traffic_source": "profiles/ncu_traffic_r02.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
+            "step": {"d3_flops": work["total"], "tflops": work["total"] / step_s / 1e12,
+                     "frac": work["total"] / step_s / 1e12 / peak,
+                     "d3_split": {k: work[k] for k in ("r2l_qr", "r2l_explicit_q", "core_x_L", "l2r")}},
+            "hbm": {"algorithmic_bytes": work["bytes"], "gbs": work["bytes"] / step_s / 1e9,
+                    "peak_gbs": hbm, "frac": work["bytes"] / step_s / 1e9 / hbm},
+            "dominant_kernel": dom_name}
     kernel_classes = {k: {"launches": v["launches"], "ms": round(v["ms"], 3), "share": round(v["ms"] / total_ms, 4),
-                          "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 else 0.0}
+                          "lapack_tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 else 0.0}
                       for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
 
-    # ------------------------------------------------------------ alongside: Gram (C3), drivers (C2)
+    # ------------------------------------------------------------ alongside
     extras = {}
     if not args.no_extras:
         from ttinputs import CONFIGS, make_shared_tail_set
         c3 = CONFIGS["C3"]
-        st3 = make_shared_tail_set(c3.d, c3.n, c3.r, c3.m, c3.kappa, c3.seed)  # same set on every rank (sharded parts)
+        st3 = make_shared_tail_set(c3.d, c3.n, c3.r, c3.m, c3.kappa, c3.seed)  # same set on every rank
         A3 = [P.DeviceTT.from_numpy(a) for a in st3.tensors]
+        pairs = c3.m * (c3.m + 1) // 2
         G = P.tt_gram(ctx, A3)
         torch.cuda.synchronize()
         gms = []
-        for _ in range(3):
+        for _ in range(5):
             flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            G = P.tt_gram(ctx, A3)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            gms.append(e0.elapsed_time(e1))
-        pairs = c3.m * (c3.m + 1) // 2
+            ms, G = _event_ms(lambda: P.tt_gram(ctx, A3), stream)
+            gms.append(ms)
         gerr = float(np.linalg.norm(G.cpu().numpy() - st3.gram_exact()) / np.linalg.norm(st3.gram_exact()))
-        extras["gram_pairs_per_s"] = pairs / (statistics.median(gms) * 1e-3)
+        r3 = [1] + [min(c3.r, c3.n ** k, c3.n ** (c3.d - k)) for k in range(1, c3.d)] + [1]
+        # SURVEY §8(a) a6 per pair and core: 2n(a_{k-1} b_{k-1} b_k + a_{k-1} a_k b_k)
+        gflops = pairs * sum(2 * c3.n * (r3[k] * r3[k] * r3[k + 1] + r3[k] * r3[k + 1] * r3[k + 1])
+                             for k in range(c3.d))
+        gmed = statistics.median(gms)
+        extras["gram_pairs_per_s"] = pairs / (gmed * 1e-3)
         extras["gram"] = {"workload": "C3 (configs[2]) TT-dot Gram matrix, m=50, d=16, n=64, r=20",
-                          "pairs": pairs, "ms": statistics.median(gms), "rel_err_vs_MtM": gerr}
-        if world > 1:  # C3 Gram sharded by pair blocks over the ranks (one NCCL all-gather)
-            from paper_2211_08770_b200 import parallel
-            blockfn = lambda blocks: P.tt_gram_blocks(ctx, A3, blocks)  # noqa: E731
-            Gs = parallel.sharded_gram(c3.m, blockfn, block=4)
-            torch.cuda.synchronize()
+                          "pairs": pairs, "ms": gmed, "ms_min": min(gms), "rel_err_vs_MtM": gerr,
+                          "d3_flops": gflops, "tflops": gflops / (gmed * 1e-3) / 1e12,
+                          "frac_of_dmma_peak": gflops / (gmed * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS}
+        if world > 1:
+            # the library's own NCCL communicator: C3 Gram by LPT pair blocks + one all-gather, and
+            # the C3 TT-Gram driver with its 50 phase-2 roundings LPT-sharded (owner rounds, ranks
+            # all-gathered, q_i broadcast)
+            parallel.attach_nccl(ctx)
+            P.tt_gram(ctx, A3)
             sms = []
-            for _ in range(3):
+            for _ in range(5):
                 barrier()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                Gs = parallel.sharded_gram(c3.m, blockfn, block=4)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                sms.append(e0.elapsed_time(e1))
-            tg = torch.tensor([statistics.median(sms)], device=dev, dtype=torch.float64)
-            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-            # CGS2 with the projection dots of every step split over the ranks (one NCCL
-            # all-gather per pass), C3 prefix m = 10; roundings replicated on every rank
-            A3p = A3[:10]
-            parallel.cgs_sharded(ctx, "cgs2", A3p[:2], c3.delta)
+                ms, Gs = _event_ms(lambda: P.tt_gram(ctx, A3), stream)
+                sms.append(ms)
+            tg = tmax(statistics.median(sms))
+            extras["gram_sharded"] = {"ranks": world, "ms": tg, "pairs_per_s": pairs / (tg * 1e-3),
+                                      "rel_err_vs_MtM": float(np.linalg.norm(Gs.cpu().numpy() - st3.gram_exact())
+                                                              / np.linalg.norm(st3.gram_exact())),
+                                      "collective": "library-owned NCCL all-gather of LPT-assigned 4x4 pair blocks"}
             barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            _, Rsh, ncalls = parallel.cgs_sharded(ctx, "cgs2", A3p, c3.delta)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            tc = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
-            rm = st3.qr_exact()[1][:10, :10]
-            extras["cgs2_sharded"] = {"ranks": world, "m": 10, "roundings": ncalls, "ms": float(tc.item()),
-                                      "R_rel_err_vs_R_M": float(np.linalg.norm(Rsh - rm) / np.linalg.norm(rm)),
-                                      "collective": "NCCL all_gather_into_tensor of the projection dots, per pass"}
-            extras["gram_sharded"] = {"ranks": world, "ms": float(tg.item()), "pairs_per_s": pairs / (float(tg.item()) * 1e-3),
-                                      "rel_err_vs_MtM": float(np.linalg.norm(Gs - st3.gram_exact()) / np.linalg.norm(st3.gram_exact())),
-                                      "collective": "NCCL all_gather_into_tensor of padded pair blocks"}
-        c2 = CONFIGS["C2"]
-        st2 = make_shared_tail_set(c2.d, c2.n, c2.r, c2.m, c2.kappa, c2.seed + rank)
-        A2 = [P.DeviceTT.from_numpy(a) for a in st2.tensors]
-        P.tt_orth(ctx, "mgs", A2, c2.delta)
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        _, _, r1 = P.tt_orth(ctx, "mgs", A2, c2.delta)
-        _, _, r2 = P.tt_orth(ctx, "mgs2", A2, c2.delta)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        calls = r1["rounding_calls"] + r2["rounding_calls"]
-        extras["drivers_c2"] = {"workload": "C2 (configs[1]) TT-MGS + TT-MGS2, m=30, d=8, n=32, r=10",
-                                "roundings": calls, "ms": e0.elapsed_time(e1),
-                                "roundings_per_s": calls / (e0.elapsed_time(e1) * 1e-3)}
-        # the paper's own workload (Section 3, experiment 1): Krylov TT-Laplacian set
-        # d=3, n=15, m=20, five schemes (Gram breaks down on it) at delta=1e-5, floor off
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        K1 = P.krylov_set(ctx, 3, 15, 20)
-        kcalls, kloo = 0, {}
-        for kind in ("cgs", "mgs", "cgs2", "mgs2", "householder"):
-            _, _, rk = P.tt_orth(ctx, kind, K1, 1e-5, floor_c=0.0, want_loo=True)
-            kcalls += rk["rounding_calls"]
-            kloo[kind] = float(rk["loo_per_step"][-1])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        extras["krylov_exp1"] = {"workload": "PAPER.md Sec. 3 experiment 1: Krylov TT-Laplacian set d=3, n=15, m=20 "
-                                             "(rank-1 rounded), CGS/MGS/CGS2/MGS2/Householder at delta=1e-5, floor off",
-                                 "roundings": kcalls, "ms": e0.elapsed_time(e1),
-                                 "roundings_per_s": kcalls / (e0.elapsed_time(e1) * 1e-3), "loo_last": kloo}
+            ms, (_, Rg, repg) = _event_ms(lambda: P.tt_orth(ctx, "gram", A3, c3.delta), stream)
+            tgd = tmax(ms)
+            rm = st3.qr_exact()[1]
+            extras["gram_driver_sharded"] = {
+                "ranks": world, "ms": tgd, "roundings": repg["rounding_calls"],
+                "R_rel_err_vs_R_M": float(np.linalg.norm(Rg - rm) / np.linalg.norm(rm)),
+                "collective": "NCCL all-gather of dot slices and of phase-2 ranks, grouped broadcasts of q_i"}
+            parallel.detach(ctx)
+            # weak scaling: every rank rounds its own whole batch
+            ws, wb = _weak_slice(args.batch, rank, world)
+            wc_h, wcf = make_batch_sums_stacked(wb, start=ws)
+            wc = [[torch.from_numpy(c).to(dev) for c in term] for term in wc_h]
+            step(wc, wcf, np.ones((wb, 4)))
+            wms = []
+            for _ in range(args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                barrier()
+                ms, _r = _event_ms(lambda: step(wc, wcf, np.ones((wb, 4))), stream)
+                wms.append(ms)
+            tw = tmax(sum(wms) / 1e3)
+            extras["weak_scaling"] = {"per_gpu_batch": args.batch, "global_batch": args.batch * world,
+                                      "value": args.batch * world * args.steps / tw, "unit": "roundings/s",
+                                      "ms_per_step": 1e3 * tw / args.steps}
+            del wc
+        if rank == 0:
+            extras["drivers"] = _driver_extras(P, ctx, stream, rank)
+            c2 = CONFIGS["C2"]
+            st2 = make_shared_tail_set(c2.d, c2.n, c2.r, c2.m, c2.kappa, c2.seed)
+            A2 = [P.DeviceTT.from_numpy(a) for a in st2.tensors]
+            P.tt_orth(ctx, "mgs", A2, c2.delta)
+            ms, (r1, r2) = _event_ms(lambda: (P.tt_orth(ctx, "mgs", A2, c2.delta)[2],
+                                              P.tt_orth(ctx, "mgs2", A2, c2.delta)[2]), stream)
+            calls = r1["rounding_calls"] + r2["rounding_calls"]
+            extras["drivers_c2"] = {"workload": "C2 (configs[1]) TT-MGS + TT-MGS2, m=30, d=8, n=32, r=10",
+                                    "roundings": calls, "ms": ms, "roundings_per_s": calls / (ms * 1e-3)}
+            # the paper's own workload (Section 3, experiment 1): Krylov TT-Laplacian set
+            # d=3, n=15, m=20, five schemes (Gram breaks down on it) at delta=1e-5, floor off
+            def krylov():
+                K1 = P.krylov_set(ctx, 3, 15, 20)
+                kcalls, kloo = 0, {}
+                for kind in ("cgs", "mgs", "cgs2", "mgs2", "householder"):
+                    _, _, rk = P.tt_orth(ctx, kind, K1, 1e-5, floor_c=0.0, want_loo=True)
+                    kcalls += rk["rounding_calls"]
+                    kloo[kind] = float(rk["loo_per_step"][-1])
+                return kcalls, kloo
+            ms, (kcalls, kloo) = _event_ms(krylov, stream)
+            extras["krylov_exp1"] = {"workload": "PAPER.md Sec. 3 experiment 1: Krylov TT-Laplacian set d=3, n=15, "
+                                                 "m=20 (rank-1 rounded), CGS/MGS/CGS2/MGS2/Householder at delta=1e-5, "
+                                                 "floor off", "roundings": kcalls, "ms": ms,
+                                     "roundings_per_s": kcalls / (ms * 1e-3), "loo_last": kloo}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(args.batch, world),
             "e2e": {"value": e2e_value, "unit": "roundings/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_steps": [round(x, 2) for x in e2e_ms], "api": f"tt_round_batch_host ({args.e2e_chunks} pipelined slices)"},
+                    "ms_steps": [round(x, 2) for x in e2e_ms],
+                    "api": f"tt_round_batch_host (C ABI, host buffers, {args.e2e_slices} pipelined slices)"},
             "gpu_launches": launches,
             "roofline": roof,
-            "kernel_profile": "CUDA events around every launch of one extra step (ctx stream)",
-            "fp64_tflops_step": all_flops / (t_local / args.steps) / 1e12,
+            "kernel_profile": "CUDA events around every launch of one extra step (ctx stream); lapack_tflops = "
+                              "the library's LAPACK-standard counts of what each kernel computes",
             "kernel_classes": kernel_classes,
             "ranks_closed_form_ok": rank_ok,
             "clocks": clocks,
@@ -422,7 +600,11 @@ def main():
             n, t = oracle_sample(CPU_SAMPLE_SECONDS)
             line["cpu_baseline"] = {"value": n / t, "unit": "roundings/s", "cores": _blas_threads(), "kind": "oracle",
                                     "sample": f"oracle TT-rounding of the first {n} C4 items, {t:.1f} s "
-                                              "(numpy/LAPACK fp64, BLAS threads = cores)"}
+                                              "(numpy/LAPACK fp64, BLAS threads = cores; items generated before "
+                                              "the clock starts)",
+                                    "cpu_model": _cpu_model(), "nproc": os.cpu_count()}
+            if not args.no_extras:
+                line["cpu_baseline"]["drivers"] = _oracle_driver_extras()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

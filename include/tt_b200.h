@@ -28,6 +28,7 @@
 #ifndef TT_B200_H
 #define TT_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -51,7 +52,8 @@ typedef enum {
   TT_ESINGULAR_GRAM = 7,  /* Cholesky of the Gram matrix met a pivot <= 0 */
   TT_ELINDEP = 8,         /* ||p|| <= 1e3 u ||a_i||: linear dependence */
   TT_ENUMDEFECT = 9,      /* ||a||^2 - s < -1e-12 ||a||^2 in TTH-vec (literal beta) */
-  TT_ENOTSUP = 10         /* shape outside what this build supports (message says which) */
+  TT_ENOTSUP = 10,        /* shape outside what this build supports (message says which) */
+  TT_ECOMM = 11           /* a collective of the attached communicator failed (or NCCL missing) */
 } tt_status;
 
 typedef struct tt_ctx_s* tt_ctx;
@@ -161,7 +163,11 @@ TT_API tt_status tt_matvec(tt_ctx ctx, const tt_view* A, const tt_view* x, tt_te
 /* out_dev[p] = <x[p], y[p]> for p < P (PAPER.md:19 Euclidean dot through the contraction;
  * W_k = sum_i X_k(i)^T W_{k-1} Y_k(i)).  out_dev: DEVICE, P doubles. */
 TT_API tt_status tt_dot_batch(tt_ctx ctx, int32_t P, const tt_view* x, const tt_view* y, double* out_dev);
-/* G(i,j) = <a_i, a_j> (Alg. 5 lines 2-6, Eq. (3)); G_dev: DEVICE m*m row-major, symmetric. */
+/* G(i,j) = <a_i, a_j> (Alg. 5 lines 2-6, Eq. (3)); G_dev: DEVICE m*m row-major, symmetric.
+ * With a communicator of N ranks attached (tt_ctx_comm_*; N = 1 runs the same path), every rank calls with
+ * the same set: the lower triangle is cut into 4 x 4 pair blocks (tt_plan_gram_blocks), each rank
+ * evaluates the blocks the LPT plan gives it, one all-gather combines them and every rank
+ * receives the whole G.  Ordered on the ctx stream (NCCL). */
 TT_API tt_status tt_gram(tt_ctx ctx, int32_t m, const tt_view* a, double* G_dev);
 /* Pair blocks of the Gram matrix for sharding: blk (HOST) holds nblk quadruples
  * (i0, j0, bi, bj); block b writes bi*bj doubles <a_{i0+s}, a_{j0+t}> row-major (s,t)
@@ -221,6 +227,88 @@ TT_API tt_status tt_batch_download(tt_ctx ctx, tt_batch bt, double* host, int64_
  * last arena. */
 TT_API tt_status tt_batch_arena(tt_batch bt, int32_t w, const double** ptr, int64_t* count);
 TT_API tt_status tt_batch_free(tt_ctx ctx, tt_batch bt);
+
+/* B independent roundings from HOST inputs to HOST results in one call (the end-to-end path of
+ * tt_round_batch_strided; BASELINE.json configs[3]).  Arguments as tt_round_batch_strided, except:
+ *   host_core[K*d]  HOST base pointers: core k of term l of item b starts at
+ *                   host_core[l*d + k] + b * item_stride[l*d + k] (doubles), each core C order.
+ *                   Page-locked memory (cudaHostAlloc / cudaHostRegister) lets the copies run
+ *                   asynchronously; pageable memory works but serialises them.
+ *   slices          the batch is processed in about `slices` contiguous slices (whole waves of the
+ *                   engine): the host->device copy of slice c+1 and the device->host copy of slice
+ *                   c-1 overlap the rounding of slice c (two copy streams owned by the context).
+ *   out_host        HOST, out_capacity doubles: every result core, items in order, each item's
+ *                   cores in order, each core (rho_{k-1}, n_k, rho_k) C order.
+ *   out_count       doubles of the results (set also when they do not fit: then TT_EINVAL, and
+ *                   out_host holds only a prefix -- call again with a larger buffer).
+ *   ranks_out       HOST B*(d+1) or NULL; norms_out HOST B (||x_b||) or NULL.
+ * The call is one unit in ctx-stream order (it waits for earlier work on that stream, and later
+ * work waits for its copies); it returns when every result is in out_host. */
+TT_API tt_status tt_round_batch_host(tt_ctx ctx, int32_t B, int32_t K, int32_t d, const int64_t* n,
+                                     const int64_t* r, const double* const* host_core,
+                                     const int64_t* item_stride, const double* coeff, const double* norms,
+                                     const tt_round_opts* opts, int32_t slices, double* out_host,
+                                     int64_t out_capacity, int64_t* out_count, int64_t* ranks_out,
+                                     double* norms_out);
+
+/* ---------------------------------------------------------------- multi-GPU */
+/* A context may hold a communicator over N processes (one GPU each; N = 1 takes the same code path).
+ * Then, on every rank with identical arguments:
+ *   tt_gram         pair blocks split by LPT, one all-gather (see tt_gram);
+ *   tt_orth         every batch of driver TT-dots (projection coefficients <p, q_j>, Q/U Gram rows,
+ *                   norms) is split into contiguous slices, one all-gather per batch; the
+ *                   independent phase-2 roundings of TT-Gram (q_i = round(sum_k R^{-1}(k,i) a_k),
+ *                   PAPER.md:250-258) and TT-Householder (q_i = round(e_i - sum_j beta_ij u_j),
+ *                   PAPER.md:414-420) are assigned to ranks by LPT on their modelled flops; each
+ *                   owner rounds its q_i, the output ranks and norms are all-gathered and q_i is
+ *                   broadcast from its owner, so every rank returns every q_i.  The sequential
+ *                   rounding chains (CGS/MGS steps, Householder phase 1) are replicated: a single
+ *                   rounding sweep never shards (north star).
+ * Batches of independent roundings need no communicator: each rank rounds its tt_plan_slice. */
+#define TT_COMM_ID_BYTES 128
+/* Caller-supplied collectives (e.g. a host transport).  Both are called after the ctx stream has
+ * been synchronised and must complete before returning; return 0 on success.
+ *   allgather: every rank contributes `bytes` at send (DEVICE); recv (DEVICE, nranks*bytes)
+ *              receives them in rank order.
+ *   broadcast: rank root's buf (DEVICE, bytes) is copied into every rank's buf. */
+typedef struct {
+  int (*allgather)(void* user, const void* send, void* recv, size_t bytes, void* stream);
+  int (*broadcast)(void* user, void* buf, size_t bytes, int32_t root, void* stream);
+  void* user;
+} tt_comm_ops;
+/* A fresh NCCL unique id (TT_COMM_ID_BYTES bytes, HOST) for tt_ctx_comm_nccl; call on one rank
+ * and pass the bytes to the others.  Loads libnccl.so.2 (TT_ECOMM when it cannot). */
+TT_API tt_status tt_comm_nccl_id(uint8_t* id);
+/* Attach an NCCL communicator of nranks (collective: every rank calls it with the same id). */
+TT_API tt_status tt_ctx_comm_nccl(tt_ctx ctx, int32_t nranks, int32_t rank, const uint8_t* id);
+/* Attach caller-supplied collectives (ops copied; ops->user must outlive the attachment). */
+TT_API tt_status tt_ctx_comm_ops(tt_ctx ctx, int32_t nranks, int32_t rank, const tt_comm_ops* ops);
+TT_API tt_status tt_ctx_comm_detach(tt_ctx ctx);
+/* nranks / rank of the attached communicator (1 / 0 without one). */
+TT_API tt_status tt_ctx_comm_info(tt_ctx ctx, int32_t* nranks, int32_t* rank);
+/* Shard plans (HOST only; no context, no device).
+ *   tt_plan_slice       contiguous balanced slice [start, end) of P independent items for rank.
+ *   tt_plan_lpt         owner[i] of P items with costs cost[i]: decreasing cost (ties: lower i),
+ *                       each to the least-loaded rank (ties: lower rank); deterministic.
+ *   tt_plan_gram_blocks the b x b pair blocks (i0, j0, bi, bj) covering i >= j of an m x m Gram
+ *                       matrix (diagonal blocks full), into blk[4*nblk], and their LPT owners by
+ *                       pair count; *nblk always set, TT_EINVAL when cap < *nblk (cap 0: query). */
+TT_API tt_status tt_plan_slice(int64_t P, int32_t nranks, int32_t rank, int64_t* start, int64_t* end);
+TT_API tt_status tt_plan_lpt(int32_t P, const double* cost, int32_t nranks, int32_t* owner);
+TT_API tt_status tt_plan_gram_blocks(int32_t m, int32_t b, int32_t nranks, int32_t cap, int32_t* blk,
+                                     int32_t* owner, int32_t* nblk);
+
+/* ---------------------------------------------------------------- step-level replay */
+/* Observer of the drivers' rounding calls (SURVEY.md §8(b) "step-level replay"): when set,
+ * tt_orth calls fn before each of its TT-roundings with the call's index in Table 1 order
+ * (0-based), the TT-sum's K terms (views of DEVICE cores, norm = the ||y_l||
+ * the rounding uses for s(x)), its HOST coefficients and the rounding options.  The ctx stream
+ * is synchronised first, so the cores can be read on any stream; everything passed is borrowed
+ * for the duration of the callback only.  Used to replay a driver step through another
+ * implementation (teacher-forced parity).  fn = NULL removes the observer. */
+typedef void (*tt_round_hook)(void* user, int64_t call, int32_t K, const double* coeff, const tt_view* terms,
+                              const tt_round_opts* opts);
+TT_API tt_status tt_ctx_round_hook(tt_ctx ctx, tt_round_hook fn, void* user);
 
 /* ---------------------------------------------------------------- drivers */
 /* Q, R = TT-<kind>(A, delta) (Algs. 1-5, 8).  q_out: HOST array of m

@@ -8,10 +8,12 @@ CPU oracle and has no CPU fallback.
 """
 from . import _native  # noqa: F401
 from .api import (  # noqa: F401
+    DEFAULT_FLOOR_C,
     BatchTT,
     Context,
     DeviceTT,
     LibTT,
+    RoundTrace,
     compression_gain,
     compression_ratio,
     krylov_set,

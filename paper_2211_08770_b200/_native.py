@@ -15,7 +15,9 @@ LIB_PATH = os.path.join(HERE, "_lib", "libtt_b200.so")
 TT_STATUS = {
     0: "TT_OK", 1: "TT_EINVAL", 2: "TT_ESHAPE", 3: "TT_EINDEX", 4: "TT_ENOMEM", 5: "TT_ECUDA",
     6: "TT_ENOCONV", 7: "TT_ESINGULAR_GRAM", 8: "TT_ELINDEP", 9: "TT_ENUMDEFECT", 10: "TT_ENOTSUP",
+    11: "TT_ECOMM",
 }
+COMM_ID_BYTES = 128
 KINDS = {"cgs": 0, "mgs": 1, "cgs2": 2, "mgs2": 3, "gram": 4, "householder": 5}
 
 EXPORTED = [
@@ -24,7 +26,18 @@ EXPORTED = [
     "tt_sum", "tt_axpy", "tt_matvec", "tt_dot_batch", "tt_gram", "tt_gram_blocks", "tt_element", "tt_norm",
     "tt_round", "tt_round_batch", "tt_orth",
     "tt_round_batch_strided", "tt_batch_shape", "tt_batch_ranks", "tt_batch_view", "tt_batch_download", "tt_batch_arena", "tt_batch_free",
+    "tt_round_batch_host",
+    "tt_comm_nccl_id", "tt_ctx_comm_nccl", "tt_ctx_comm_ops", "tt_ctx_comm_detach", "tt_ctx_comm_info",
+    "tt_plan_slice", "tt_plan_lpt", "tt_plan_gram_blocks", "tt_ctx_round_hook",
 ]
+
+# tt_comm_ops callbacks (include/tt_b200.h)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+BROADCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("allgather", ALLGATHER_FN), ("broadcast", BROADCAST_FN), ("user", C.c_void_p)]
 
 
 class TTView(C.Structure):
@@ -50,6 +63,10 @@ class OrthReport(C.Structure):
     _fields_ = [("rounding_calls", C.c_int64), ("fail_index", C.c_int32),
                 ("loo_per_step", C.POINTER(C.c_double)), ("max_rank_per_call", C.POINTER(C.c_int64)),
                 ("householder_u", C.POINTER(C.c_void_p))]
+
+
+ROUND_HOOK_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_double), C.POINTER(TTView),
+                            C.POINTER(RoundOpts))
 
 
 class TTError(RuntimeError):
@@ -112,6 +129,18 @@ def load() -> C.CDLL:
         "tt_batch_free": (C.c_int, [P, P]),
         "tt_orth": (C.c_int, [P, C.c_int, i32, VP, C.POINTER(OrthOpts), C.POINTER(P), C.POINTER(dbl),
                               C.POINTER(OrthReport)]),
+        "tt_round_batch_host": (C.c_int, [P, i32, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(P),
+                                          C.POINTER(i64), C.POINTER(dbl), C.POINTER(dbl), C.POINTER(RoundOpts),
+                                          i32, P, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(dbl)]),
+        "tt_comm_nccl_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "tt_ctx_comm_nccl": (C.c_int, [P, i32, i32, C.POINTER(C.c_uint8)]),
+        "tt_ctx_comm_ops": (C.c_int, [P, i32, i32, C.POINTER(CommOps)]),
+        "tt_ctx_comm_detach": (C.c_int, [P]),
+        "tt_ctx_comm_info": (C.c_int, [P, C.POINTER(i32), C.POINTER(i32)]),
+        "tt_plan_slice": (C.c_int, [i64, i32, i32, C.POINTER(i64), C.POINTER(i64)]),
+        "tt_plan_lpt": (C.c_int, [i32, C.POINTER(dbl), i32, C.POINTER(i32)]),
+        "tt_plan_gram_blocks": (C.c_int, [i32, i32, i32, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
+        "tt_ctx_round_hook": (C.c_int, [P, ROUND_HOOK_FN, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -322,119 +322,54 @@ def tt_round_batch_strided(ctx: Context, terms, coeffs, rel_tol: float, norms=No
 
 
 def tt_round_batch_host(ctx: Context, host_terms, coeffs, rel_tol: float, norms=None,
-                        floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0, chunks: int = 4,
-                        out_host: Optional[torch.Tensor] = None, start_event=None):
-    """End-to-end batched rounding from HOST inputs to HOST results, pipelined over `chunks`
-    contiguous slices of the batch: the host->device copy of slice c+1 (one copy stream) and
-    the device->host copy of slice c-1's results (another stream: the two directions use
-    different copy engines) run while slice c is rounded on the context's stream (stream
-    orchestration only; the rounding is tt_round_batch_strided).
-    host_terms[l][k]: pinned CPU float64 tensors (B, r_{k-1}, n_k, r_k).  Results go to
-    out_host (pinned float64, items in order, cores in order, each core C order; allocated if
-    None).  Returns (out_host, ranks (B, d+1), norms (B,), doubles written)."""
+                        floor_c: float = DEFAULT_FLOOR_C, max_rank: int = 0, slices: int = 4,
+                        out_host: Optional[torch.Tensor] = None):
+    """End-to-end batched rounding from HOST inputs to HOST results: one call of the C ABI's
+    tt_round_batch_host (the library pipelines host->device copies, the rounding and the
+    device->host copies over `slices` slices on its own streams).
+    host_terms[l][k]: CPU float64 tensors (B, r_{k-1}, n_k, r_k), pinned for overlap.  Results go
+    to out_host (float64, items in order, cores in order, each core C order); when it is None or
+    too small a pinned buffer is allocated (and the call repeated if the first estimate was too
+    small).  Returns (out_host, ranks (B, d+1), norms (B,), doubles written)."""
     K, d = len(host_terms), len(host_terms[0])
     B = int(host_terms[0][0].shape[0])
-    coeffs = np.asarray(coeffs, dtype=np.float64).reshape(B, K)
-    norms_a = None if norms is None else np.asarray(norms, dtype=np.float64).reshape(B, K)
-    dev = f"cuda:{ctx.device}"
-    # slice size: about B / chunks rounded to whole waves of the engine (one CTA per item, 2 per
-    # SM in the right-to-left kernel, 3 in the left-to-right ones: 6 x SMs items fill both), so
-    # the slices add no partial waves beyond the one of the whole batch
-    wave = 6 * torch.cuda.get_device_properties(ctx.device).multi_processor_count
-    step = max(wave, int(round(B / max(chunks, 1) / wave)) * wave) if B > wave * chunks else -(-B // max(chunks, 1))
-    bounds = list(range(0, B, max(step, 1))) + [B]
-    chunks = len(bounds) - 1
-    per_item = [[int(np.prod(x.shape[1:])) for x in term] for term in host_terms]
-    item_doubles = sum(sum(t) for t in per_item)
-    need = max(bounds[c + 1] - bounds[c] for c in range(chunks)) * item_doubles
-    # Streams and two device staging buffers persist on the context: fresh streams would make
-    # the caching allocator hand out new blocks (cudaMalloc) every call, and per-tensor
-    # allocations cost more than the copies themselves.
-    pipe = getattr(ctx, "_host_pipe", None)
-    if pipe is None or pipe["cap"] < need:
-        if pipe is not None:
-            torch.cuda.synchronize(ctx.device)
-        pipe = {"copy": torch.cuda.Stream(ctx.device),   # host -> device (one copy engine)
-                "back": torch.cuda.Stream(ctx.device),   # device -> host (the other direction's)
-                "cap": need,
-                "stage": [torch.empty(need, dtype=torch.float64, device=dev) for _ in range(2)]}
-        torch.cuda.synchronize(ctx.device)
-        ctx._host_pipe = pipe
-    copy, back = pipe["copy"], pipe["back"]
-    if start_event is not None:
-        copy.wait_event(start_event)
-        back.wait_event(start_event)
-    staged, consumed = [], []
-
-    def h2d(c):
-        a, b = bounds[c], bounds[c + 1]
-        buf = pipe["stage"][c % 2]
-        if c >= 2:
-            copy.wait_event(consumed[c - 2])  # slice c-2's rounding has read this buffer
-        t, off = [], 0
-        with torch.cuda.stream(copy):
-            for term, sizes in zip(host_terms, per_item):
-                row = []
-                for x, sz in zip(term, sizes):
-                    v = buf[off:off + (b - a) * sz].view((b - a,) + tuple(x.shape[1:]))
-                    v.copy_(x[a:b], non_blocking=True)
-                    row.append(v)
-                    off += (b - a) * sz
-                t.append(row)
-            ev = torch.cuda.Event()
-            ev.record(copy)
-        return t, ev
-
-    import os
-    import time
-    dbg = os.environ.get("TT_B200_HOST_DEBUG") == "1"
-    t0 = time.perf_counter()
-    staged.append(h2d(0))
-    ranks, nrm, pending = [], [], []
-    offset = 0
-    for c in range(chunks):
-        if c + 1 < chunks:
-            staged.append(h2d(c + 1))
-        t, ev = staged[c]
-        ctx.stream.wait_event(ev)
-        a, b = bounds[c], bounds[c + 1]
-        with torch.cuda.stream(ctx.stream):
-            res = tt_round_batch_strided(ctx, t, coeffs[a:b], rel_tol,
-                                         norms=None if norms_a is None else norms_a[a:b],
-                                         floor_c=floor_c, max_rank=max_rank)
-        used = torch.cuda.Event()
-        used.record(ctx.stream)
-        consumed.append(used)
-        ranks.append(res.ranks)
-        nrm.append(res.norms)
-        n = res.total_doubles()
-        if out_host is None:
-            out_host = torch.empty(0, dtype=torch.float64)
-        if out_host.numel() < offset + n:
-            grown = torch.empty(int((offset + n) * (chunks / (c + 1)) * 1.05) + 1024, dtype=torch.float64).pin_memory()
-            back.synchronize()  # earlier slices' device->host copies into out_host have landed
-            grown[:offset].copy_(out_host[:offset])
-            out_host = grown
-        # device -> host of this slice on the copy stream, overlapping the next slice's rounding
-        done = torch.cuda.Event()
-        done.record(ctx.stream)
-        back.wait_event(done)
-        with torch.cuda.stream(back):
-            for w, (ptr, cnt) in enumerate(res.arenas()):
-                dst = out_host[offset:offset + cnt]
-                src = torch.as_tensor(_CoreArray(ptr, (cnt,), res), device=dev)
-                dst.copy_(src, non_blocking=True)
-                offset += cnt
-        pending.append(res)  # keep the device results alive until their copies finished
-        del t
-        if dbg:
-            print(f"[host_pipeline] slice {c} done at {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
-    copy.synchronize()
-    back.synchronize()
-    if dbg:
-        print(f"[host_pipeline] copies done at {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
-    del pending
-    return out_host, np.concatenate(ranks), np.concatenate(nrm), offset
+    n = (C.c_int64 * d)(*[int(host_terms[0][k].shape[2]) for k in range(d)])
+    r = (C.c_int64 * (K * (d + 1)))()
+    base = (C.c_void_p * (K * d))()
+    stride = (C.c_int64 * (K * d))()
+    in_doubles = 0
+    for l in range(K):
+        r[l * (d + 1)] = int(host_terms[l][0].shape[1])
+        for k in range(d):
+            t = host_terms[l][k]
+            if not (t.device.type == "cpu" and t.dtype == torch.float64 and t.dim() == 4 and t[0].is_contiguous()):
+                raise ValueError("host_terms[l][k] must be (B, r0, n, r1) float64 CPU tensors with contiguous items")
+            if int(t.shape[0]) != B:
+                raise ValueError("all term cores need the same batch size B")
+            r[l * (d + 1) + k + 1] = int(t.shape[3])
+            base[l * d + k] = t.data_ptr()
+            stride[l * d + k] = int(t.stride(0)) if B > 1 else 0
+            in_doubles += int(t[0].numel())
+    cf = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64).reshape(B, K))
+    nr = None if norms is None else np.ascontiguousarray(np.asarray(norms, dtype=np.float64).reshape(B, K))
+    o = _opts(rel_tol, floor_c, max_rank, 0.5, False)
+    ranks = np.empty((B, d + 1), dtype=np.int64)
+    nrm = np.empty(B, dtype=np.float64)
+    if out_host is None:
+        out_host = torch.empty(max(B * in_doubles, 1), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        cnt = C.c_int64()
+        st = ctx.lib.tt_round_batch_host(
+            ctx.handle, B, K, d, n, r, base, stride, cf.ctypes.data_as(C.POINTER(C.c_double)),
+            None if nr is None else nr.ctypes.data_as(C.POINTER(C.c_double)), C.byref(o), int(slices),
+            C.c_void_p(out_host.data_ptr()), int(out_host.numel()), C.byref(cnt),
+            ranks.ctypes.data_as(C.POINTER(C.c_int64)), nrm.ctypes.data_as(C.POINTER(C.c_double)))
+        if st == 1 and cnt.value > out_host.numel():  # TT_EINVAL: results larger than the buffer
+            out_host = torch.empty(cnt.value, dtype=torch.float64).pin_memory()
+            continue
+        ctx.check(st)
+        return out_host, ranks, nrm, cnt.value
+    raise RuntimeError("tt_round_batch_host: output buffer sizing failed")
 
 
 def tt_sum(ctx: Context, terms, coeffs) -> LibTT:
@@ -547,6 +482,42 @@ def tt_norm(ctx: Context, x) -> float:
     o = C.c_double()
     ctx.check(ctx.lib.tt_norm(ctx.handle, C.byref(v), C.byref(o)))
     return o.value
+
+
+class RoundTrace:
+    """Records the TT-sums tt_orth rounds (tt_ctx_round_hook) for the selected call indices
+    (Table 1 order, 0-based; None = all): calls[i] = (coeffs, [term cores as numpy], term norms,
+    rel_tol, floor_c).  Use as a context manager around tt_orth (step-level replay)."""
+
+    def __init__(self, ctx: Context, select=None):
+        self.ctx = ctx
+        self.select = None if select is None else set(int(i) for i in select)
+        self.calls = {}
+        self._fn = N.ROUND_HOOK_FN(self._hook)
+
+    def _hook(self, user, call, K, coeff, terms, opts):
+        if self.select is not None and call not in self.select:
+            return
+        cores, norms = [], []
+        for l in range(K):
+            v = terms[l]
+            cs = []
+            for k in range(v.d):
+                shp = (int(v.r[k]), int(v.n[k]), int(v.r[k + 1]))
+                t = torch.as_tensor(_CoreArray(v.core[k], shp, None), device=f"cuda:{self.ctx.device}")
+                cs.append(t.cpu().numpy().copy())
+            cores.append(cs)
+            norms.append(float(v.norm))
+        o = opts[0]
+        self.calls[int(call)] = ([float(coeff[l]) for l in range(K)], cores, norms, o.rel_tol, o.floor_c)
+
+    def __enter__(self):
+        self.ctx.check(self.ctx.lib.tt_ctx_round_hook(self.ctx.handle, self._fn, None))
+        return self
+
+    def __exit__(self, *exc):
+        self.ctx.lib.tt_ctx_round_hook(self.ctx.handle, N.ROUND_HOOK_FN(), None)
+        return False
 
 
 def tt_orth(ctx: Context, kind: str, tensors, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C,

@@ -1327,6 +1327,23 @@ bool batch_shape_supported(int d, int K, const std::vector<std::vector<int64_t>>
   return true;
 }
 
+void batch_desc_shape(BatchDesc& in, int B, int K, int d, const int64_t* n, const int64_t* r) {
+  if (B < 0 || K < 1 || d < 1 || !n || !r) fail(TT_EINVAL, "batch: bad shape arguments");
+  in.B = B;
+  in.K = K;
+  in.d = d;
+  in.n.assign(n, n + d);
+  in.r.resize((size_t)K);
+  for (int l = 0; l < K; ++l) {
+    in.r[(size_t)l].assign(r + (size_t)l * (d + 1), r + (size_t)(l + 1) * (d + 1));
+    if (in.r[(size_t)l][0] != 1 || in.r[(size_t)l][(size_t)d] != 1) fail(TT_ESHAPE, "boundary ranks must be 1");
+    for (int k = 0; k < d; ++k)
+      if (n[k] < 1 || in.r[(size_t)l][(size_t)k] < 1) fail(TT_ESHAPE, "mode sizes and ranks must be >= 1");
+  }
+  std::string why;
+  if (!batch_shape_supported(d, K, in.r, &why)) fail(TT_ENOTSUP, "batched engine: " + why);
+}
+
 void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut& res) {
   const char* hdbg = std::getenv("TT_B200_BR_DEBUG");
   const bool hd = hdbg && hdbg[0] == '1';

@@ -33,6 +33,11 @@ struct BatchOut {
 bool batch_shape_supported(int d, int K, const std::vector<std::vector<int64_t>>& r, std::string* why);
 bool batch_uniform_supported(int B, const std::vector<SumInput>& items, std::string* why);
 void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut& res);
+// Fill in.B/K/d/n/r from the C-ABI shape arguments of tt_round_batch_strided / _host, validated
+// (TT_ESHAPE for bad ranks or modes, TT_ENOTSUP outside batch_shape_supported).
+void batch_desc_shape(BatchDesc& in, int B, int K, int d, const int64_t* n, const int64_t* r);
+// host_pipe.cu: release the context's host-pipeline streams and staging buffers.
+void host_pipe_release(tt_ctx ctx);
 // out[b] = TT-round(items[b]) as library tensors (sharing one refcounted arena per wave).
 void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
                          int64_t* ranks_out);

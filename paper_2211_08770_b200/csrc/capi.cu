@@ -1,5 +1,6 @@
 // extern "C" boundary of libtt_b200 (include/tt_b200.h).  Every entry point converts
 // internal errors into a tt_status plus tt_last_error text; nothing throws across it.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -7,6 +8,7 @@
 #include <new>
 
 #include "batch_round.cuh"
+#include "comm.cuh"
 #include "gram.cuh"
 #include "orth.cuh"
 #include "round.cuh"
@@ -50,6 +52,84 @@ SumInput sum_of(int K, const double* coeff, const tt_view* terms) {
   return s;
 }
 
+// Pair blocks (i0, j0, bi, bj) of the Gram matrix of A into packed_dev (tt_gram_blocks layout):
+// the pair-tiled DMMA kernel for equally shaped sets, else the pair list of the TT-dot kernels.
+void gram_blocks_local(tt_ctx ctx, const std::vector<TTRef>& A, int nblk, const int32_t* blk, double* packed_dev) {
+  const int m = (int)A.size();
+  for (int b = 0; b < nblk; ++b) {
+    const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
+    if (i0 < 0 || j0 < 0 || bi < 0 || bj < 0 || i0 + bi > m || j0 + bj > m) fail(TT_EINDEX, "Gram block out of range");
+  }
+  if (nblk == 0) return;
+  bool uniform = true;
+  for (int i = 1; i < m; ++i)
+    uniform = uniform && A[(size_t)i].d == A[0].d && A[(size_t)i].n == A[0].n && A[(size_t)i].r == A[0].r;
+  const char* gt = std::getenv("TT_B200_GRAM_PAIRWISE");  // tests: force the per-pair kernel
+  if (uniform && !(gt && gt[0] == '1')) {
+    std::vector<const double*> cores;
+    for (int i = 0; i < m; ++i) cores.insert(cores.end(), A[(size_t)i].core.begin(), A[(size_t)i].core.end());
+    if (gram_tiled_supported(cores, m, A[0].d, A[0].n, A[0].r)) {
+      gram_tiled_blocks(ctx, cores, m, A[0].d, A[0].n, A[0].r, nblk, blk, packed_dev);
+      return;
+    }
+  }
+  std::vector<std::pair<const TTRef*, const TTRef*>> pr;
+  for (int b = 0; b < nblk; ++b) {
+    const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
+    for (int s = 0; s < bi; ++s)
+      for (int t = 0; t < bj; ++t) pr.push_back({&A[(size_t)(i0 + s)], &A[(size_t)(j0 + t)]});
+  }
+  dots_device(ctx, pr, packed_dev);
+}
+
+// G from the all-gathered pair blocks: tab[5 q] = (i0, j0, bi, bj, offset into recv) for every
+// block of every rank; diagonal blocks contribute their lower half only (one value per pair).
+__global__ void gram_unpack_blocks_kernel(const double* __restrict__ recv, const int64_t* __restrict__ tab, int m,
+                                          double* __restrict__ G) {
+  const int64_t* t = tab + 5 * (int64_t)blockIdx.x;
+  const int i0 = (int)t[0], j0 = (int)t[1], bi = (int)t[2], bj = (int)t[3];
+  const double* src = recv + t[4];
+  for (int e = threadIdx.x; e < bi * bj; e += blockDim.x) {
+    const int s = e / bj, u = e % bj;
+    if (i0 == j0 && u > s) continue;
+    const double v = src[e];
+    G[(int64_t)(i0 + s) * m + (j0 + u)] = v;
+    G[(int64_t)(j0 + u) * m + (i0 + s)] = v;
+  }
+}
+
+// Sharded Gram (communicator attached): LPT-assigned pair blocks, one all-gather, device unpack.
+void gram_sharded(tt_ctx ctx, const std::vector<TTRef>& A, double* G_dev) {
+  const int m = (int)A.size(), N = comm_size(ctx), me = comm_rank(ctx);
+  static const int bsz = [] {
+    const char* e = std::getenv("TT_B200_GRAM_BLOCK");
+    return (e && std::atoi(e) > 0) ? std::atoi(e) : 4;
+  }();
+  const std::vector<int32_t> blk = plan_gram_blocks(m, bsz);
+  const int nb = (int)(blk.size() / 4);
+  std::vector<double> cost((size_t)nb);
+  for (int q = 0; q < nb; ++q) cost[(size_t)q] = (double)blk[(size_t)4 * q + 2] * blk[(size_t)4 * q + 3];
+  const std::vector<int> owner = plan_lpt(cost, N);
+  std::vector<int64_t> load((size_t)N, 0), tab((size_t)nb * 5);
+  std::vector<int32_t> mine;
+  for (int q = 0; q < nb; ++q) {
+    const int o = owner[(size_t)q];
+    for (int c = 0; c < 4; ++c) tab[(size_t)5 * q + c] = blk[(size_t)4 * q + c];
+    tab[(size_t)5 * q + 4] = load[(size_t)o];  // offset inside owner o's packed buffer
+    load[(size_t)o] += (int64_t)blk[(size_t)4 * q + 2] * blk[(size_t)4 * q + 3];
+    if (o == me) mine.insert(mine.end(), blk.begin() + 4 * q, blk.begin() + 4 * q + 4);
+  }
+  const int64_t cap = std::max<int64_t>(*std::max_element(load.begin(), load.end()), 1);
+  for (int q = 0; q < nb; ++q) tab[(size_t)5 * q + 4] += (int64_t)owner[(size_t)q] * cap;
+  DBuf send(ctx, (size_t)cap), recv(ctx, (size_t)cap * N);
+  gram_blocks_local(ctx, A, (int)(mine.size() / 4), mine.data(), send.p);
+  comm_allgather(ctx, send.p, recv.p, sizeof(double) * (size_t)cap);
+  BBuf dtab;
+  dtab.upload(ctx, tab.data(), tab.size() * sizeof(int64_t));
+  TTB_RUN(ctx, "aux", 0, 16.0 * m * m,
+          gram_unpack_blocks_kernel<<<nb, 128, 0, ctx->stream>>>(recv.p, static_cast<const int64_t*>(dtab.p), m, G_dev));
+}
+
 }  // namespace
 
 extern "C" {
@@ -90,6 +170,8 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
     for (auto ev : ctx->up_events) cudaEventDestroy(ev);
   }
   if (ctx->scratch) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->scratch); }
+  host_pipe_release(ctx);
+  comm_release(ctx);
   delete ctx;
   return TT_OK;
 }
@@ -126,6 +208,7 @@ const char* tt_status_string(tt_status s) {
     case TT_ELINDEP: return "TT_ELINDEP";
     case TT_ENUMDEFECT: return "TT_ENUMDEFECT";
     case TT_ENOTSUP: return "TT_ENOTSUP";
+    case TT_ECOMM: return "TT_ECOMM";
   }
   return "unknown";
 }
@@ -245,30 +328,7 @@ tt_status tt_gram_blocks(tt_ctx ctx, int32_t m, const tt_view* a, int32_t nblk, 
   return guarded(ctx, [&] {
     std::vector<TTRef> A;
     for (int i = 0; i < m; ++i) A.push_back(TTRef::of(a[i]));
-    for (int b = 0; b < nblk; ++b) {
-      const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
-      if (i0 < 0 || j0 < 0 || bi < 0 || bj < 0 || i0 + bi > m || j0 + bj > m) fail(TT_EINDEX, "Gram block out of range");
-    }
-    bool uniform = true;
-    for (int i = 1; i < m; ++i)
-      uniform = uniform && A[(size_t)i].d == A[0].d && A[(size_t)i].n == A[0].n && A[(size_t)i].r == A[0].r;
-    const char* gt = std::getenv("TT_B200_GRAM_PAIRWISE");  // tests: force the per-pair kernel
-    if (uniform && !(gt && gt[0] == '1')) {
-      std::vector<const double*> cores;
-      for (int i = 0; i < m; ++i) cores.insert(cores.end(), A[(size_t)i].core.begin(), A[(size_t)i].core.end());
-      if (gram_tiled_supported(cores, m, A[0].d, A[0].n, A[0].r)) {
-        gram_tiled_blocks(ctx, cores, m, A[0].d, A[0].n, A[0].r, nblk, blk, packed_dev);
-        return;
-      }
-    }
-    std::vector<std::pair<const TTRef*, const TTRef*>> pr;
-    for (int b = 0; b < nblk; ++b) {
-      const int i0 = blk[4 * b], j0 = blk[4 * b + 1], bi = blk[4 * b + 2], bj = blk[4 * b + 3];
-      if (i0 < 0 || j0 < 0 || bi < 0 || bj < 0 || i0 + bi > m || j0 + bj > m) fail(TT_EINDEX, "Gram block out of range");
-      for (int s = 0; s < bi; ++s)
-        for (int t = 0; t < bj; ++t) pr.push_back({&A[(size_t)(i0 + s)], &A[(size_t)(j0 + t)]});
-    }
-    dots_device(ctx, pr, packed_dev);
+    gram_blocks_local(ctx, A, nblk, blk, packed_dev);
   });
 }
 
@@ -298,6 +358,10 @@ tt_status tt_gram(tt_ctx ctx, int32_t m, const tt_view* a, double* G_dev) {
   return guarded(ctx, [&] {
     std::vector<TTRef> A;
     for (int i = 0; i < m; ++i) A.push_back(TTRef::of(a[i]));
+    if (comm_active(ctx)) {
+      gram_sharded(ctx, A, G_dev);
+      return;
+    }
     bool uniform = true;
     for (int i = 1; i < m; ++i)
       uniform = uniform && A[(size_t)i].d == A[0].d && A[(size_t)i].n == A[0].n && A[(size_t)i].r == A[0].r;
@@ -389,21 +453,9 @@ tt_status tt_round_batch_strided(tt_ctx ctx, int32_t B, int32_t K, int32_t d, co
     return TT_EINVAL;
   return guarded(ctx, [&] {
     BatchDesc in;
-    in.B = B;
-    in.K = K;
-    in.d = d;
-    in.n.assign(n, n + d);
-    in.r.resize((size_t)K);
-    for (int l = 0; l < K; ++l) {
-      in.r[(size_t)l].assign(r + (size_t)l * (d + 1), r + (size_t)(l + 1) * (d + 1));
-      if (in.r[(size_t)l][0] != 1 || in.r[(size_t)l][(size_t)d] != 1) fail(TT_ESHAPE, "boundary ranks must be 1");
-      for (int k = 0; k < d; ++k) {
-        if (n[k] < 1 || in.r[(size_t)l][(size_t)k] < 1) fail(TT_ESHAPE, "mode sizes and ranks must be >= 1");
-        if (!core[(size_t)l * d + k]) fail(TT_EINVAL, "null core base pointer");
-      }
-    }
-    std::string why;
-    if (!batch_shape_supported(d, K, in.r, &why)) fail(TT_ENOTSUP, "tt_round_batch_strided: " + why);
+    batch_desc_shape(in, B, K, d, n, r);
+    for (int q = 0; q < K * d; ++q)
+      if (!core[q]) fail(TT_EINVAL, "null core base pointer");
     in.tab.resize((size_t)B * K * d);
     for (int64_t b = 0; b < B; ++b)
       for (int l = 0; l < K; ++l)
@@ -485,6 +537,13 @@ tt_status tt_batch_free(tt_ctx ctx, tt_batch bt) {
   if (!bt) return TT_OK;
   for (void* p : bt->res.arenas) cudaFreeAsync(p, ctx->stream);
   delete bt;
+  return TT_OK;
+}
+
+tt_status tt_ctx_round_hook(tt_ctx ctx, tt_round_hook fn, void* user) {
+  if (!ctx) return TT_EINVAL;
+  ctx->round_hook = fn;
+  ctx->round_hook_user = user;
   return TT_OK;
 }
 

@@ -70,6 +70,17 @@ struct tt_ctx_s {
   struct UpPending { size_t start, end; cudaEvent_t ev; };
   std::vector<UpPending> up_pending;
   std::vector<cudaEvent_t> up_events;  // free events
+  // host-to-host batched rounding (tt_round_batch_host, host_pipe.cu): persistent copy streams
+  // (one per direction: the two directions use different copy engines) and two device staging
+  // buffers, so repeated calls allocate nothing
+  cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
+  double* hp_stage[2] = {nullptr, nullptr};
+  size_t hp_stage_doubles = 0;
+  // optional communicator (comm.cu): sharded Gram / dot batches / phase-2 roundings
+  struct TTComm* comm = nullptr;
+  // observer of the drivers' rounding calls (tt_ctx_round_hook)
+  tt_round_hook round_hook = nullptr;
+  void* round_hook_user = nullptr;
 };
 
 struct tt_tensor_s {

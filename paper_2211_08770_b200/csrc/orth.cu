@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 
+#include "comm.cuh"
 #include "gram.cuh"
 #include "orth.cuh"
 #include "ttops.cuh"
@@ -109,6 +110,26 @@ void dots_device(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTR
 std::vector<double> dots_host(tt_ctx ctx, const std::vector<std::pair<const TTRef*, const TTRef*>>& pairs) {
   std::vector<double> h(pairs.size(), 0.0);
   if (pairs.empty()) return h;
+  if (comm_active(ctx) && pairs.size() >= 2) {
+    // split into contiguous slices (one per rank), one all-gather of equal-sized buffers
+    // (north star: "CGS projection dot products are split ... and combined with all-gather")
+    const int N = comm_size(ctx), me = comm_rank(ctx);
+    const int64_t P = (int64_t)pairs.size(), cap = ceil_div(P, N);
+    int64_t s = 0, e = 0;
+    plan_slice(P, N, me, &s, &e);
+    DBuf send(ctx, (size_t)cap), recv(ctx, (size_t)cap * N);
+    if (e > s)
+      dots_device(ctx, std::vector<std::pair<const TTRef*, const TTRef*>>(pairs.begin() + s, pairs.begin() + e), send.p);
+    comm_allgather(ctx, send.p, recv.p, sizeof(double) * (size_t)cap);
+    std::vector<double> all((size_t)cap * N);
+    d2h_small(ctx, all.data(), recv.p, all.size());
+    for (int q = 0; q < N; ++q) {
+      int64_t a = 0, b = 0;
+      plan_slice(P, N, q, &a, &b);
+      for (int64_t t = a; t < b; ++t) h[(size_t)t] = all[(size_t)q * cap + (t - a)];
+    }
+    return h;
+  }
   DBuf o(ctx, pairs.size());
   dots_device(ctx, pairs, o.p);
   d2h_small(ctx, h.data(), o.p, pairs.size());
@@ -232,16 +253,123 @@ int64_t max_rank(tt_tensor t) {
   return m;
 }
 
+// tt_ctx_round_hook: hand the rounding call's TT-sum to the observer (ctx stream synchronised).
+void notify_round(tt_ctx ctx, int64_t call, const SumInput& in, const tt_round_opts& o) {
+  if (!ctx->round_hook) return;
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int K = in.K();
+  std::vector<tt_view> v((size_t)K);
+  for (int l = 0; l < K; ++l) {
+    v[(size_t)l].d = in.d;
+    v[(size_t)l].n = in.n.data();
+    v[(size_t)l].r = in.r[(size_t)l].data();
+    v[(size_t)l].core = in.core[(size_t)l].data();
+    v[(size_t)l].norm = in.norm[(size_t)l];
+  }
+  ctx->round_hook(ctx->round_hook_user, call, K, in.coef.data(), v.data(), &o);
+}
+
 struct Ledger {
   int64_t calls = 0;
   std::vector<int64_t> max_ranks;
   tt_tensor round(tt_ctx ctx, const SumInput& in, const tt_round_opts& o) {
+    notify_round(ctx, calls, in, o);
     tt_tensor t = round_sum(ctx, in, o, nullptr);
     ++calls;
     max_ranks.push_back(max_rank(t));
     return t;
   }
 };
+
+// Modelled flops of rounding `in` (right-to-left QR + explicit Q of the
+// formal-rank panels, capped by the structural ranks): the LPT cost of a phase-2 rounding.
+double round_cost_model(const SumInput& in) {
+  const int d = in.d;
+  std::vector<double> R((size_t)d + 1, 0.0), Rp((size_t)d + 1, 1.0);
+  for (int k = 0; k <= d; ++k)
+    for (const auto& r : in.r) R[(size_t)k] += (double)r[(size_t)k];
+  R[0] = R[(size_t)d] = 1.0;
+  for (int k = d; k >= 1; --k) Rp[(size_t)k - 1] = std::min(R[(size_t)k - 1], (double)in.n[(size_t)k - 1] * Rp[(size_t)k]);
+  double f = 0.0;
+  for (int k = d - 1; k >= 1; --k) {
+    const double m = (double)in.n[(size_t)k] * Rp[(size_t)k + 1], c = R[(size_t)k];
+    f += (m >= c) ? 4.0 * m * c * c - 4.0 * c * c * c / 3.0 : 4.0 * c * m * m - 4.0 * m * m * m / 3.0;
+  }
+  return f;
+}
+
+// The independent roundings of a driver's phase 2 (TT-Gram q_i; TT-Householder
+// q_i).  Without a communicator they run in order.  With one, the LPT plan on
+// round_cost_model assigns each to a rank; the owner rounds it and takes its norm, one all-gather
+// shares every output's ranks and norm, and each q_i is broadcast from its owner (grouped), so
+// every rank returns every q_i.  The ledger records the calls in index order (Table 1 counts).
+std::vector<tt_tensor> round_independent(tt_ctx ctx, const std::vector<SumInput>& sums, const tt_round_opts& o,
+                                         Ledger& led) {
+  const int m = (int)sums.size();
+  std::vector<tt_tensor> Q((size_t)m, nullptr);
+  auto free_all = [&] {
+    for (tt_tensor& t : Q)
+      if (t) { tensor_free(ctx, t); t = nullptr; }
+  };
+  if (!comm_active(ctx)) {
+    try {
+      for (int i = 0; i < m; ++i) {
+        Q[(size_t)i] = led.round(ctx, sums[(size_t)i], o);
+        Q[(size_t)i]->norm = last_core_norm(ctx, Q[(size_t)i]);
+      }
+    } catch (...) {
+      free_all();
+      throw;
+    }
+    return Q;
+  }
+  const int N = comm_size(ctx), me = comm_rank(ctx), d = sums[0].d;
+  std::vector<double> cost((size_t)m);
+  for (int i = 0; i < m; ++i) cost[(size_t)i] = round_cost_model(sums[(size_t)i]);
+  const std::vector<int> owner = plan_lpt(cost, N);
+  const size_t row = (size_t)d + 2;  // ranks r_0..r_d (exact in a double) and the norm
+  std::vector<double> info((size_t)m * row, 0.0);
+  try {
+    for (int i = 0; i < m; ++i) {
+      if (owner[(size_t)i] != me) continue;
+      notify_round(ctx, led.calls + i, sums[(size_t)i], o);
+      tt_tensor t = round_sum(ctx, sums[(size_t)i], o, nullptr);
+      Q[(size_t)i] = t;
+      t->norm = last_core_norm(ctx, t);
+      for (int k = 0; k <= d; ++k) info[(size_t)i * row + k] = (double)t->r[(size_t)k];
+      info[(size_t)i * row + d + 1] = t->norm;
+    }
+    DBuf send(ctx, info.size()), recv(ctx, info.size() * N);
+    TTB_CUDA(cudaMemcpyAsync(send.p, info.data(), sizeof(double) * info.size(), cudaMemcpyHostToDevice, ctx->stream));
+    comm_allgather(ctx, send.p, recv.p, sizeof(double) * info.size());
+    std::vector<double> all(info.size() * N);
+    d2h_small(ctx, all.data(), recv.p, all.size());
+    std::vector<void*> bufs;
+    std::vector<size_t> bytes;
+    std::vector<int> roots;
+    for (int i = 0; i < m; ++i) {
+      const double* g = all.data() + (size_t)owner[(size_t)i] * info.size() + (size_t)i * row;
+      std::vector<int64_t> rk((size_t)d + 1);
+      for (int k = 0; k <= d; ++k) rk[(size_t)k] = (int64_t)g[k];
+      if (!Q[(size_t)i]) {
+        Q[(size_t)i] = tensor_alloc(ctx, d, sums[(size_t)i].n, rk);
+        Q[(size_t)i]->norm = g[d + 1];
+      }
+      size_t total = 0;
+      for (int k = 0; k < d; ++k) total += (size_t)(rk[(size_t)k] * sums[(size_t)i].n[(size_t)k] * rk[(size_t)k + 1]);
+      bufs.push_back(Q[(size_t)i]->block);
+      bytes.push_back(total * sizeof(double));
+      roots.push_back(owner[(size_t)i]);
+      led.calls++;
+      led.max_ranks.push_back(*std::max_element(rk.begin(), rk.end()));
+    }
+    comm_broadcast_many(ctx, bufs, bytes, roots);
+  } catch (...) {
+    free_all();
+    throw;
+  }
+  return Q;
+}
 
 void add_ref(SumInput& s, const TTRef& x, double c) {
   tt_view v;
@@ -357,17 +485,15 @@ void run_gram(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::vector<
       X[(size_t)i * m + j] = -s / R[(size_t)i * m + i];
     }
   }
-  for (int i = 0; i < m; ++i) {
-    SumInput s;
+  std::vector<SumInput> sums((size_t)m);
+  for (int i = 0; i < m; ++i)
     for (int k = 0; k <= i; ++k) {
       TTRef a = A[(size_t)k];
       a.norm = an[(size_t)k];
-      add_ref(s, a, X[(size_t)k * m + i]);  // q_i = sum_k R^{-1}(k,i) a_k (A5)
+      add_ref(sums[(size_t)i], a, X[(size_t)k * m + i]);  // q_i = sum_k R^{-1}(k,i) a_k (A5)
     }
-    tt_tensor q = led.round(ctx, s, o.round);
-    q->norm = last_core_norm(ctx, q);
-    Q.push_back(q);
-  }
+  std::vector<tt_tensor> q = round_independent(ctx, sums, o.round, led);
+  Q.insert(Q.end(), q.begin(), q.end());
 }
 
 // ----------------------------------------------------------------- Householder (Algs. 6-8)
@@ -463,6 +589,7 @@ void run_householder(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::
     std::vector<double> e = elements_host(ctx, UR[(size_t)j], lins);
     for (int i = j; i < m; ++i) EU[(size_t)j * m + i] = e[(size_t)(i - j)];
   }
+  std::vector<SumInput> sums((size_t)m);
   for (int i = 1; i <= m; ++i) {
     std::vector<double> bt((size_t)m, 0.0);
     for (int j = i; j >= 1; --j) {
@@ -471,14 +598,13 @@ void run_householder(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::
       for (int l = j + 1; l <= i; ++l) v -= bt[(size_t)l - 1] * GU[(size_t)(l - 1) * m + (j - 1)];
       bt[(size_t)j - 1] = 2.0 * v;
     }
-    SumInput sq;
+    SumInput& sq = sums[(size_t)i - 1];
     add_ref(sq, ER[(size_t)i - 1], 1.0);
     for (int j = i; j >= 1; --j)
       if (U[(size_t)j - 1]) add_ref(sq, UR[(size_t)j - 1], -bt[(size_t)j - 1]);
-    tt_tensor q = led.round(ctx, sq, o.round);
-    q->norm = last_core_norm(ctx, q);
-    Q.push_back(q);
   }
+  std::vector<tt_tensor> q = round_independent(ctx, sums, o.round, led);
+  Q.insert(Q.end(), q.begin(), q.end());
   Uout = U;
   (void)fail_index;
 }

@@ -1,20 +1,57 @@
-"""bench.py host-side contract (CPU): the weak-scaling shard map and the reference arm's JSON
-line (the oracle on a bounded C4 sample; rank 0 alone prints)."""
+"""bench.py host-side contract (CPU): the strong-scaling shard map (BASELINE configs[3]: the one
+4096-item batch split across the GPUs), the weak-scaling extra's map, the D3 work model, the
+--gpus / WORLD_SIZE check and the reference arm's JSON line (the oracle on a bounded C4 sample;
+rank 0 alone prints)."""
 import json
 import types
 
 import bench
 
 
-def test_weak_shards_disjoint_and_cover():
+def test_strong_shards_split_one_batch():
+    from paper_2211_08770_b200 import _build, parallel
+    _build.build_library()
+    B = 4096
+    for world in (1, 2, 3, 4, 8):
+        spans = [bench._slice(B, r, world) for r in range(world)]
+        assert sum(n for _, n in spans) == B  # total work fixed as N grows
+        assert [s for s, _ in spans] == sorted(s for s, _ in spans) and spans[0][0] == 0
+        assert all(spans[r][0] + spans[r][1] == spans[r + 1][0] for r in range(world - 1))
+        for r in range(world):  # the bench's formula is the library's tt_plan_slice
+            s, e = parallel.plan_slice(B, world, r)
+            assert (s, e - s) == spans[r]
+        cfg = bench._config(B, world)
+        assert cfg["batch"] == B and cfg["global_batch"] == B
+
+
+def test_weak_extra_shards_disjoint_and_cover():
     B = 4096
     for world in (1, 2, 4, 8):
-        spans = [bench._slice(B, r, world) for r in range(world)]
+        spans = [bench._weak_slice(B, r, world) for r in range(world)]
         assert all(n == B for _, n in spans)  # per-GPU work fixed as N grows
-        starts = sorted(s for s, _ in spans)
-        assert starts == [r * B for r in range(world)]  # disjoint, covering [0, world * B)
-        cfg = bench._config(B, world)
-        assert cfg["batch"] == B and cfg["global_batch"] == B * world
+        assert sorted(s for s, _ in spans) == [r * B for r in range(world)]
+
+
+def test_d3_model_hand_values():
+    """SURVEY §8(d) D3 on a hand-countable case: d = 2, n = (2, 3), one term of ranks (1, 2, 1),
+    output ranks (1, 2, 1).  Right-to-left, core 2: panel m = n_2 R'_2 = 3, c = R_1 = 2 ->
+    QR + explicit Q 2(2*3*4 - 2*8/3) = 37.33, half of it each; core x L: 2 R'_1 nnz(X_1) = 2*2*4 =
+    16.  Left-to-right, k = 1: Y_1 is (1*2) x 2 -> 6*2*4 + 11*8 = 136, plus 2*2*2*3*1 = 24."""
+    qr, eq, cxl, l2r = bench.d3_round_flops([2, 3], [[1, 2, 1]], [1, 2, 1])
+    assert abs(qr - (24 - 16 / 3)) < 1e-12 and abs(eq - qr) < 1e-12
+    assert cxl == 16 and l2r == 160
+    # C4 per item, even (ranks 32) items: the verdict's recount, 1.99e12 for the batch of 4096
+    w = bench.c4_work([[1] + [32] * 9 + [1], [1] + [16] * 9 + [1]] * 2048)
+    assert 1.9e12 < w["total"] < 2.1e12
+
+
+def test_gpus_must_match_world_size(monkeypatch):
+    import pytest
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    monkeypatch.setattr("sys.argv", ["bench.py", "--gpus", "2"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert e.value.code == 2
 
 
 def _args(steps=1, warmup=0):
@@ -29,7 +66,7 @@ def test_reference_arm_line(monkeypatch, capsys):
     line = json.loads(out[0])
     assert line["impl"] == "reference" and line["metric"] == bench.METRIC
     assert line["unit"] == "roundings/s" and line["higher_is_better"] is True
-    assert line["scaling"] == "weak" and line["n_gpus"] == 1
+    assert line["scaling"] == "strong" and line["n_gpus"] == 1
     assert line["value"] > 0 and line["cpu_baseline"]["value"] == line["value"]
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"] == {"value": line["value"], "unit": "roundings/s", "h2d_bytes_per_step": 0,

@@ -200,7 +200,7 @@ def test_batch_host_pipeline_matches_device_call():
     B = 10
     cores, coeffs = make_batch_sums_stacked(B, d=6, n=9, r=5)
     host = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores]
-    out, ranks, norms, cnt = P.tt_round_batch_host(ctx(), host, coeffs, 1e-6, norms=np.ones((B, 4)), chunks=3)
+    out, ranks, norms, cnt = P.tt_round_batch_host(ctx(), host, coeffs, 1e-6, norms=np.ones((B, 4)), slices=3)
     res = P.tt_round_batch_strided(ctx(), [[c.cuda() for c in term] for term in host], coeffs, 1e-6,
                                    norms=np.ones((B, 4)))
     assert np.array_equal(ranks, res.ranks)
@@ -225,11 +225,51 @@ def test_batch_host_pipeline_back_to_back_c4_shape():
     flat = np.concatenate([np.concatenate([c.ravel() for c in res.item_numpy(b)]) for b in range(B)])
     outs = []
     for _ in range(2):
-        out, ranks, _, cnt = P.tt_round_batch_host(ctx(), host, coeffs, 1e-6, norms=np.ones((B, 4)), chunks=4)
+        out, ranks, _, cnt = P.tt_round_batch_host(ctx(), host, coeffs, 1e-6, norms=np.ones((B, 4)), slices=4)
         outs.append((out[:cnt].numpy().copy(), ranks))
     for o, rk in outs:
         assert np.array_equal(rk, res.ranks)
         assert np.array_equal(o, flat)
+
+
+def test_batch_host_small_buffer_and_strided_items():
+    """The C-ABI host call with (a) an output buffer too small for the results: TT_EINVAL with the
+    needed count, nothing written past the buffer, and the retry returns the device call's bytes;
+    (b) items that are not adjacent in host memory (every other item of a larger pinned tensor:
+    item_stride = 2 x the core size, copied with strided host->device copies); (c) one slice per
+    item, so slice 0 (an odd-rank item) has a smaller output than later slices."""
+    import ctypes as C
+    import torch
+    import paper_2211_08770_b200 as P
+    from ttinputs import make_batch_sums_stacked
+    B = 7
+    cores, coeffs = make_batch_sums_stacked(2 * B, d=5, n=6, r=4, start=31)
+    big = [[torch.from_numpy(c).pin_memory() for c in term] for term in cores]
+    host = [[c[1::2] for c in term] for term in big]   # items 1, 3, 5, ... (odd: rank-16-like first)
+    cf = np.ascontiguousarray(coeffs[1::2])
+    res = P.tt_round_batch_strided(ctx(), [[c.contiguous().cuda() for c in term] for term in host], cf, 1e-6,
+                                   norms=np.ones((B, 4)))
+    flat = np.concatenate([np.concatenate([c.ravel() for c in res.item_numpy(b)]) for b in range(B)])
+    guard = torch.full((flat.size,), -7.0, dtype=torch.float64).pin_memory()
+    small = guard[:flat.size // 3]
+    # direct C call with the small buffer: TT_EINVAL and the needed count
+    K, d = 4, 5
+    n = (C.c_int64 * d)(*[6] * d)
+    r = (C.c_int64 * (K * (d + 1)))(*[v for _ in range(K) for v in [1, 4, 4, 4, 4, 1]])
+    base = (C.c_void_p * (K * d))(*[host[l][k].data_ptr() for l in range(K) for k in range(d)])
+    stride = (C.c_int64 * (K * d))(*[int(host[l][k].stride(0)) for l in range(K) for k in range(d)])
+    nr = np.ones((B, K))
+    o = P.api._opts(1e-6, P.DEFAULT_FLOOR_C, 0, 0.5, False)
+    cnt = C.c_int64()
+    st = ctx().lib.tt_round_batch_host(ctx().handle, B, K, d, n, r, base, stride,
+                                       cf.ctypes.data_as(C.POINTER(C.c_double)),
+                                       nr.ctypes.data_as(C.POINTER(C.c_double)), C.byref(o), B,
+                                       C.c_void_p(small.data_ptr()), small.numel(), C.byref(cnt), None, None)
+    assert st == 1 and cnt.value == flat.size
+    assert np.all(guard[flat.size // 3:].numpy() == -7.0)  # nothing written past the capacity
+    out, ranks, _, cnt2 = P.tt_round_batch_host(ctx(), host, cf, 1e-6, norms=nr, slices=B, out_host=small.clone())
+    assert cnt2 == flat.size and np.array_equal(ranks, res.ranks)
+    assert np.array_equal(out[:cnt2].numpy(), flat)
 
 
 def test_batch_strided_unsupported_shape_and_serial_fallback():

@@ -228,26 +228,6 @@ def test_orth_c3_full_cgs2_closed_form():
         assert diff_norm(Q[i].to_numpy(), st.q_exact(i)) <= max(1e-10, 16 * U_ROUND * c.m * kap), i
 
 
-@pytest.mark.parametrize("kind", ["cgs", "cgs2"])
-def test_cgs_sharded_driver_matches_tt_orth(kind):
-    """parallel.cgs_sharded (projection dots split over the ranks + all-gather; here world 1)
-    reproduces tt_orth's lazy CGS / CGS2: Table 1 counts, R and the basis."""
-    import paper_2211_08770_b200 as P
-    from paper_2211_08770_b200 import parallel
-    st = make_shared_tail_set(8, 32, 10, 12, 1e4, seed=5)
-    A = [dev(a, float(tt.tt_norm(a))) for a in st.tensors]
-    Qs, Rs, calls = parallel.cgs_sharded(ctx(), kind, A, 1e-10)
-    Q, R, rep = P.tt_orth(ctx(), kind, A, 1e-10)
-    assert calls == rep["rounding_calls"] == (2 if kind == "cgs2" else 1) * len(A)
-    # the two drivers differ in rounding order only (norms by sweep vs last core, coefficient
-    # placement): agreement within the scheme's amplified noise, as for two correct drivers
-    kap = _kappas(st)
-    amp = lambda k: FLOOR_C * U_ROUND * len(A) * kap[k] ** POWER[kind]  # noqa: E731
-    assert np.linalg.norm(Rs - R) <= max(1e-10, amp(len(A) - 1)) * np.linalg.norm(R)
-    for i, (qs, q) in enumerate(zip(Qs, Q)):
-        assert diff_norm(qs.to_numpy(), q.to_numpy()) <= max(1e-10, amp(i)), (kind, i)
-
-
 def test_orth_householder_beta_literal():
     """hh_beta_literal = 1: beta = sqrt(||w||^2 - s) exactly as Alg. 6 line 10 prints it
      against the oracle's literal branch (pinned in test_oracle_orth.py):
