@@ -48,7 +48,7 @@ def threshold(delta: float, norm: float, d: int, floor_c: float, scale: float) -
 
 def tt_round(x: TT, delta: float, floor_c: float = 0.0, scale: Optional[float] = None,
              max_rank: Optional[int] = None,
-             force_ranks: Optional[Sequence[int]] = None) -> tuple[TT, RoundInfo]:
+             force_ranks: Optional[Sequence[int]] = None, _owned: bool = False) -> tuple[TT, RoundInfo]:
     """force_ranks (test use only): force rho_k = min(ranks[k], #singular values) at every split
     instead of the threshold rule -- the same truncation as another implementation that chose
     those ranks, for comparing reconstructions where a decision sits inside the window of tau
@@ -56,7 +56,9 @@ def tt_round(x: TT, delta: float, floor_c: float = 0.0, scale: Optional[float] =
     check_tt(x)
     d = len(x)
     formal = [1] + [c.shape[2] for c in x]
-    cores = [np.array(c, dtype=np.float64, copy=True) for c in x]
+    # _owned: x is a fresh array list nobody else holds (tt_round_sum's materialised sum), so the
+    # sweep may overwrite it instead of copying (memory only: at C5 size the sum is ~60 GB)
+    cores = x if _owned else [np.array(c, dtype=np.float64, copy=True) for c in x]
     if d == 1:
         nrm = float(np.linalg.norm(cores[0]))
         return cores, RoundInfo([1, 1], nrm, 0.0, nrm if scale is None else scale, formal, [1, 1])
@@ -114,5 +116,5 @@ def tt_round_sum(terms: Sequence[TT], coeffs: Sequence[float], delta: float,
     """Round the TT-sum sum_l c_l y_l, materialised literally."""
     s = sum_scale(terms, coeffs, term_norms) if (floor_c > 0.0) else None
     x = tt_sum(terms, coeffs)
-    out, info = tt_round(x, delta, floor_c=floor_c, scale=s, max_rank=max_rank, force_ranks=force_ranks)
+    out, info = tt_round(x, delta, floor_c=floor_c, scale=s, max_rank=max_rank, force_ranks=force_ranks, _owned=True)
     return out, info

@@ -32,6 +32,7 @@
 #include <cstring>
 
 #include "batch_round.cuh"
+#include "batch_wy.cuh"
 #include "ttops.cuh"
 
 namespace ttb {
@@ -62,6 +63,7 @@ struct BRShape {
   int64_t toff[BR_MAXD];          // core index kc: offset of its taus (per item)
   int64_t ooff[BR_MAXD];          // core index kc: worst-case output core offset (per item)
   int64_t vstride, tstride, ystride, ytstride, zstride, ostride;
+  int wyni[BR_MAXD];              // WY engine: mode indices per chunk of panel kc (chunk rows wyni * Rp[kc+1])
 };
 
 struct LBuf {  // long long device buffer (debug counters)
@@ -1290,6 +1292,239 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_apply_kernel(BRArgs A, int k) 
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[10] += clock64() - cz0;
 }
 
+
+// ================================================================ compact-WY engine (batch_wy.cuh)
+// The same three phases as above with the blocked, tensor-core QR and applications.
+
+// r2l chunk of panel kc (core k = kc + 1 < d), mode indices [i0, i0 + ni): rows (i - i0) Rpk + b',
+// column off_{k-1,l} + a:  sum_beta L_{k+1}[b'][off_{k,l} + beta] X_k^(l)[a, i, beta] as DMMA tiles
+// (M = b', N = a, K = beta), L read from the item's L slot (row-major ld 64, L2-resident).
+__device__ void wy_panel_chunk(wy::Smem& sm, const BRShape* S, const double* const* cores, const double* L, int kc,
+                               int i0, int ni) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q4 = lane & 3, r8 = lane >> 2;
+  const int K = S->K, d = S->d, n = S->n[kc], Rpk = S->Rp[kc + 1];
+  const int mtiles = (Rpk + 7) >> 3;
+  // units (i, l, m-tile, n-tile)
+  int units = 0;
+  int nt_l[BR_MAXK];
+  for (int l = 0; l < K; ++l) { nt_l[l] = (S->r[l][kc] + 7) >> 3; units += nt_l[l]; }
+  const int per_i = units * mtiles;
+#pragma unroll 1
+  for (int u = w; u < ni * per_i; u += wy::W) {
+    const int ii = u / per_i, rem = u % per_i;
+    const int mt = rem % mtiles;
+    int nl = rem / mtiles, l = 0;
+    while (nl >= nt_l[l]) { nl -= nt_l[l]; ++l; }
+    const int i = i0 + ii;
+    const int ra = S->r[l][kc], rb = S->r[l][kc + 1];
+    const int ob = S->off[kc + 1][l], oa = S->off[kc][l];
+    const double* X = cores[l * d + kc];
+    const int bp = 8 * mt + r8, a_b = 8 * nl + r8;  // A row (b'), B column (a)
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    const double* lrow = L + (int64_t)bp * BR_C + ob;
+    const double* xrow = X + ((int64_t)a_b * n + i) * rb;
+    const bool aok = bp < Rpk, bok = a_b < ra;
+    int be = 0;
+    for (; be + 8 <= rb; be += 8) {
+      const double a0 = aok ? __ldg(lrow + be + q4) : 0.0, x0 = bok ? __ldg(xrow + be + q4) : 0.0;
+      const double a1 = aok ? __ldg(lrow + be + 4 + q4) : 0.0, x1 = bok ? __ldg(xrow + be + 4 + q4) : 0.0;
+      wy::dmma(c0, c1, a0, x0);
+      wy::dmma(e0, e1, a1, x1);
+    }
+    for (; be < rb; be += 4) {
+      const bool kok = be + q4 < rb;
+      const double a0 = (aok && kok) ? __ldg(lrow + be + q4) : 0.0, x0 = (bok && kok) ? __ldg(xrow + be + q4) : 0.0;
+      wy::dmma(c0, c1, a0, x0);
+    }
+    c0 += e0;
+    c1 += e1;
+    const int row = (i - i0) * Rpk + 8 * mt + r8, col = oa + 8 * nl + 2 * q4;
+    if (8 * mt + r8 < Rpk) {
+      if (8 * nl + 2 * q4 < ra) sm.st[col * wy::LD + wy::RR + row] = c0;
+      if (8 * nl + 2 * q4 + 1 < ra) sm.st[(col + 1) * wy::LD + wy::RR + row] = c1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  wy::Smem& sm = *reinterpret_cast<wy::Smem*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x, gb = A.item0 + b;
+  const int d = S->d, K = S->K;
+  const int k = kc + 1;                 // 1-based core index, 2..d
+  const int n = S->n[kc], Rpk = S->Rp[k], c = S->R[k - 1];
+  const int64_t m = (int64_t)n * Rpk;
+  const bool last = (k == d);
+  const int tid = threadIdx.x;
+  const int ni = S->wyni[kc], cr = ni * Rpk;
+  const int nst = (n + ni - 1) / ni;
+  const int nrefl = (int)(m < c ? m : (int64_t)c);
+  const double* const* cores = A.cores + (int64_t)gb * K * d;
+  const double* Lin = A.L + (int64_t)b * 2 * BR_C * BR_C + ((k + 1) & 1) * BR_C * BR_C;
+  double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
+  const int64_t sd = wy::stack_doubles(c);
+  wy::init(sm);
+#pragma unroll 1
+  for (int q = 0; q < nst; ++q) {
+    const int i0 = q * ni, nq = min(ni, n - i0);
+    wy::zero_chunk(sm);
+    __syncthreads();
+    if (last) {  // A[i, off_l + a] = c_l X_d^(l)[a, i, 0]
+      for (int idx = tid; idx < nq * c; idx += wy::T) {
+        const int ii = idx / c, col = idx % c;
+        int l = 0;
+        while (l + 1 < K && col >= S->off[k - 1][l + 1]) ++l;
+        const int a = col - S->off[k - 1][l];
+        sm.st[col * wy::LD + wy::RR + ii] = A.coef[(int64_t)gb * K + l] * __ldg(cores[l * d + kc] + (int64_t)a * n + i0 + ii);
+      }
+    } else {
+      wy_panel_chunk(sm, S, cores, Lin, kc, i0, nq);
+    }
+    __syncthreads();
+    wy::factor_stack(sm, c, nrefl, nq * Rpk, q, V + (int64_t)q * sd);
+    __syncthreads();
+  }
+  (void)cr;
+  // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
+  double* Lout = A.L + (int64_t)b * 2 * BR_C * BR_C + (k & 1) * BR_C * BR_C;
+  const int rows = S->Rp[k - 1];
+  for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
+    const int row = idx / BR_C, col = idx % BR_C;
+    Lout[idx] = (row < rows && col < c && row <= col) ? sm.st[col * wy::LD + row] : 0.0;
+  }
+}
+
+// Left-to-right QR of a tall Y_k (p > 64 rows, cp columns) with the WY engine; R -> JM.
+__global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  wy::Smem& sm = *reinterpret_cast<wy::Smem*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x, gb = A.item0 + b;
+  const int d = S->d, K = S->K;
+  const int kc = k - 1;
+  const int tid = threadIdx.x;
+  int* rk = A.ranks + (int64_t)b * (d + 1);
+  double* sc = A.scal + (int64_t)b * 4;
+  double* out = A.out + (int64_t)b * S->ostride;
+  const int n = S->n[kc], cp = S->Rp[k];
+  if (k > 1 && sc[3] != 0.0) {  // ||x|| = 0: rank-1 zero tensor
+    for (int i = tid; i < n; i += wy::T) out[S->ooff[kc] + i] = 0.0;
+    if (k + 1 == d)
+      for (int i = tid; i < S->n[d - 1]; i += wy::T) out[S->ooff[d - 1] + i] = 0.0;
+    if (tid == 0) { rk[k] = 1; if (k + 1 == d) rk[d] = 1; }
+    return;
+  }
+  const int64_t p = (k == 1) ? (int64_t)n : (int64_t)rk[k - 1] * n;
+  const bool tall = p > BR_C;
+  const double* Lin = A.L;  // k == 1: L_2 in slot 0
+  const double* Z = A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride;
+  const double* const* cores = A.cores + (int64_t)gb * K * d;
+  // element (row, col) of Y_k
+  auto yel = [&](int64_t row, int col) -> double {
+    if (k > 1) return Z[row * cp + col];
+    double s = 0.0;  // Y_1[i, b'] = sum_l sum_beta X_1^(l)[0, i, beta] L_2[b'][off_{1,l} + beta]
+    const double* Lr = Lin + (int64_t)b * 2 * BR_C * BR_C + (int64_t)col * BR_C;
+    for (int l = 0; l < K; ++l) {
+      const int rl = S->r[l][1], o = S->off[1][l];
+      const double* xp = cores[l * d] + row * rl;
+      for (int be = 0; be < rl; ++be) s += Lr[o + be] * __ldg(xp + be);
+    }
+    return s;
+  };
+  wy::init(sm);
+  if (tall) {
+    double* YV = A.YV + (int64_t)b * S->ystride;
+    const int64_t sd = wy::stack_doubles(cp);
+    const int nst = (int)((p + wy::CH - 1) / wy::CH);
+#pragma unroll 1
+    for (int q = 0; q < nst; ++q) {
+      const int64_t r0 = (int64_t)q * wy::CH;
+      const int crow = (int)(p - r0 < wy::CH ? p - r0 : (int64_t)wy::CH);
+      wy::zero_chunk(sm);
+      __syncthreads();
+      for (int idx = tid; idx < crow * cp; idx += wy::T) {
+        const int r = idx / cp, col = idx % cp;
+        sm.st[col * wy::LD + wy::RR + r] = yel(r0 + r, col);
+      }
+      __syncthreads();
+      wy::factor_stack(sm, cp, cp, crow, q, YV + (int64_t)q * sd);
+      __syncthreads();
+    }
+  } else {
+    for (int idx = tid; idx < p * cp; idx += wy::T) {
+      const int r = idx / cp, col = idx % cp;
+      sm.st[col * wy::LD + r] = yel(r, col);  // short Y_k: the Jacobi input is Y itself
+    }
+    __syncthreads();
+  }
+  if (k == 1) {
+    double q = 0.0;
+    for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
+      const double v = sm.st[(idx / BR_C) * wy::LD + idx % BR_C];
+      q += v * v;
+    }
+    const double nrm = sqrt(block_sum(q, sm.red));
+    if (tid == 0) {
+      const double s = A.scale[gb];
+      double tau = 0.0;
+      if (!A.keep_all) tau = fmax(A.rel_tol * nrm / sqrt((double)(d - 1)), A.floor_c * U_ROUND * s);
+      sc[0] = nrm;
+      sc[1] = tau;
+      sc[2] = s;
+      sc[3] = nrm == 0.0 ? 1.0 : 0.0;
+      rk[0] = 1;
+      rk[d] = 1;
+    }
+    if (nrm == 0.0) {
+      for (int i = tid; i < n; i += wy::T) out[S->ooff[0] + i] = 0.0;
+      if (d == 2)
+        for (int i = tid; i < S->n[1]; i += wy::T) out[S->ooff[1] + i] = 0.0;
+      if (tid == 0) { rk[1] = 1; rk[d] = 1; }
+      return;
+    }
+  }
+  double* jm = A.JM + (int64_t)b * BR_C * BR_C;  // column-major ld 64, zero outside
+  for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
+    const int col = idx / BR_C, row = idx % BR_C;
+    jm[idx] = (col < cp && row <= (tall ? col : BR_C)) ? sm.st[col * wy::LD + row] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(wy::T, 2) br_l2r_apply_wy_kernel(BRArgs A, int k) {
+  extern __shared__ __align__(16) unsigned char br_smem_raw[];
+  wy::ASmem& sm = *reinterpret_cast<wy::ASmem*>(br_smem_raw);
+  const BRShape* S = A.sh;
+  const int b = blockIdx.x;
+  const int d = S->d;
+  const int kc = k - 1;
+  const int* rk = A.ranks + (int64_t)b * (d + 1);
+  const double* sc = A.scal + (int64_t)b * 4;
+  if (sc[3] != 0.0) return;
+  wy::apply_init(sm);
+  uint32_t ph[2] = {0u, 0u};
+  double* out = A.out + (int64_t)b * S->ostride;
+  const int n = S->n[kc], cp = S->Rp[k];
+  const int64_t p = (k == 1) ? (int64_t)n : (int64_t)rk[k - 1] * n;
+  const bool tall = p > BR_C;
+  const int rho = rk[k];
+  const double* tt = A.TT + (int64_t)b * 2 * BR_C * BR_C;
+  if (tall && A.gemm[b]) {
+    br_gemm_yw(A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride, (int)p, cp, tt, rho, out + S->ooff[kc]);
+    __syncthreads();
+  } else if (tall) {  // output core k = Q_Y [U_rho; 0]  ((rho_{k-1} n_k) x rho, row-major)
+    wy::apply(sm, ph, tt, cp, rho, A.YV + (int64_t)b * S->ystride, p, wy::CH, cp, cp, out + S->ooff[kc], rho, 1);
+  }
+  // Z_{k+1} = Q_{k+1} [(S V^T)^T; 0] (panel rows (i, b') of core k+1 -> core layout (a, i, b'))
+  const int kn = kc + 1;
+  const int64_t m1 = (int64_t)S->n[kn] * S->Rp[k + 1];
+  const int c1 = S->R[k];
+  double* dst = (k + 1 == d) ? out + S->ooff[kn] : A.Z + (int64_t)b * 2 * S->zstride + ((k + 1) & 1) * S->zstride;
+  const double* V = A.V + (int64_t)b * S->vstride + S->voff[kn];
+  const int cr = S->wyni[kn] * S->Rp[k + 1];
+  wy::apply(sm, ph, tt + BR_C * BR_C, cp, rho, V, m1, cr, c1, (int)(m1 < c1 ? m1 : (int64_t)c1), dst, 1, m1);
+}
+
 // Copy item b's cores from the worst-case workspace to the exact-size arena.
 __global__ void br_compact_kernel(const double* __restrict__ work, int64_t ostride, const int64_t* __restrict__ ooff,
                                   const int64_t* __restrict__ dst_off, const int64_t* __restrict__ sizes, int d,
@@ -1396,6 +1631,27 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
     }
     if (k + 1 < d) zmax = std::max<int64_t>(zmax, (int64_t)sh.n[k] * sh.Rp[k + 1] * sh.Rp[k]);
   }
+  static const bool use_wy = [] {
+    const char* e = std::getenv("TT_B200_BR_WY");
+    return !(e && e[0] == '0');
+  }();
+  if (use_wy) {  // compact-WY engine: stacks of whole mode indices (<= 128 rows), V + T per stack
+    v = 0;
+    yv = 0;
+    for (int kc = 1; kc < d; ++kc) {
+      const int Rpk = sh.Rp[kc + 1];
+      const int ni = std::max(1, std::min(sh.n[kc], wy::CH / Rpk));
+      sh.wyni[kc] = ni;
+      sh.voff[kc] = v;
+      v += (int64_t)((sh.n[kc] + ni - 1) / ni) * wy::stack_doubles(sh.R[kc]);
+    }
+    for (int k = 1; k < d; ++k) {
+      const int64_t p = (int64_t)sh.Rp[k - 1] * sh.n[k - 1];
+      if (p > BR_C) yv = std::max<int64_t>(yv, ((p + wy::CH - 1) / wy::CH) * wy::stack_doubles(sh.Rp[k]));
+    }
+    t = 2;
+    yt = 2;
+  }
   sh.vstride = (std::max<int64_t>(v, 2) + 1) & ~(int64_t)1;
   sh.tstride = (std::max<int64_t>(t, 2) + 1) & ~(int64_t)1;
   sh.ystride = (std::max<int64_t>(yv, 2) + 1) & ~(int64_t)1;
@@ -1465,6 +1721,12 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   TTB_CUDA(cudaFuncSetAttribute(br_l2r_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
   TTB_CUDA(cudaFuncSetAttribute(br_l2r_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
   TTB_CUDA(cudaFuncSetAttribute(br_l2r_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
+  const size_t smem_wy = sizeof(wy::Smem), smem_wya = sizeof(wy::ASmem);
+  if (use_wy) {
+    TTB_CUDA(cudaFuncSetAttribute(br_r2l_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wy));
+    TTB_CUDA(cudaFuncSetAttribute(br_l2r_qr_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wy));
+    TTB_CUDA(cudaFuncSetAttribute(br_l2r_apply_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wya));
+  }
   res.B = B;
   res.d = d;
   res.n = in.n;
@@ -1530,13 +1792,23 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         const double mm = (double)m;
         const double fl = nb * (2.0 * mm * rl + (mm >= c ? 2.0 * mm * c * c - 2.0 * c * c * c / 3.0
                                                          : 2.0 * c * mm * mm - 2.0 * mm * mm * mm / 3.0));
-        TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
-                br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
+        if (use_wy)
+          TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
+                  br_r2l_wy_kernel<<<nb, wy::T, smem_wy, ctx->stream>>>(a, kc));
+        else
+          TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
+                  br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
       }
       for (int k = 1; k < d; ++k) {
-        TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
+        if (use_wy)
+          TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_wy_kernel<<<nb, wy::T, smem_wy, ctx->stream>>>(a, k));
+        else
+          TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
         TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_svd_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
-        TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
+        if (use_wy)
+          TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_wy_kernel<<<nb, wy::T, smem_wya, ctx->stream>>>(a, k));
+        else
+          TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
       }
       if (dbg.p) {
         long long h[32];

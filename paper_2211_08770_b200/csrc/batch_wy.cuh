@@ -1,0 +1,459 @@
+// Blocked (compact-WY) Householder QR of tall panels on the FP64 tensor cores, one CTA per item
+// (the batched engine, batch_round.cu).  PAPER.md:69 (rounding = QR sweeps of the core
+// unfoldings), north star "core x R ... as FP64 DMMA tensor-core tiles".
+//
+// Flat tree over row chunks ("stacks"): the CTA keeps a 64-row R block plus one chunk of up to
+// 128 panel rows in shared memory, column-major with ld WY_LD, and factors
+//      [R; chunk]  ->  [R'; 0]
+// with reflectors v = [e_j; v_chunk] (the R block is upper triangular, so a reflector's R part is
+// the unit vector of its own row).  Stack 0 starts from R = 0: the panel is factored as [0; A]
+// (an augmented panel with 64 virtual zero rows on top), so every stack has the same structure;
+// A = Q R with Q = rows 64.. of the product of all reflectors applied to [I; 0] (the virtual rows
+// of that product vanish wherever R has full row rank).
+//
+// Columns come in blocks of 8; warp w owns column block w.  Per stack, warp w applies the
+// published reflector blocks jb < w to its columns -- W = R[8jb.., blk w] + V_jb^T A_w,
+// W' = T_jb^T W, A_w -= V_jb W', R rows -= W' -- as mma.sync.m8n8k4.f64 tiles (DMMA), then
+// factors its own block (8 reflectors, LAPACK dlarfg arithmetic, the block's 128 x 8 chunk in
+// registers), forms T_w (compact WY: H_1..H_8 = I - V T V^T, T from the DMMA Gram V^T V) and
+// publishes the block through an mbarrier.  So block w+1's factorisation starts as soon as warp
+// w+1 has applied block w, while the other warps still update their columns (look-ahead by
+// construction); there is no CTA-wide barrier inside a stack.
+//
+// Stored per stack: V_chunk (WY_CH x ncol, column-major ld WY_CH, rows beyond the chunk zero) and
+// T (ncol/8 blocks of 8 x 8, row-major) -- wy_apply applies them to thin targets.
+#pragma once
+
+#include "common.cuh"
+
+namespace ttb {
+namespace wy {
+
+constexpr int T = 256;        // threads per CTA
+constexpr int W = T / 32;     // warps
+constexpr int C = 64;         // max columns
+constexpr int NB = 8;         // columns per reflector block
+constexpr int CH = 128;       // max chunk rows per stack
+constexpr int RR = 64;        // R-block rows at the top of the stack
+constexpr int LD = RR + CH + 4;  // smem ld: 196 = 4 (mod 16) spreads the fragment loads over all banks
+
+// doubles of one stack's stored factor: V (CH x ncol) + T (ceil(ncol/8) blocks x 64)
+__host__ __device__ inline int64_t stack_doubles(int ncol) {
+  return (int64_t)CH * ncol + 64 * ((ncol + NB - 1) / NB);
+}
+
+struct Smem {
+  double st[C * LD];      // the stack: column-major, rows 0..63 R block, 64..191 chunk
+  double Tm[C / NB][64];  // T of each block (row-major 8 x 8)
+  double ws[W][64];       // per-warp 8 x 8 scratch (fragment layout changes)
+  double red[32];
+  uint64_t ready[C / NB]; // block published (32 arrivals: the owner warp's lanes)
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done)
+                 : "r"(su32(b)), "r"(parity)
+                 : "memory");
+  }
+}
+
+// Sum of eight per-lane values over the warp, every lane gets all eight (transposed butterfly).
+__device__ __forceinline__ void warp_sum8v(double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0, b2 = (lane & 4) != 0;
+  double u4[4], u2[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double keep = b4 ? v[4 + k] : v[k], send = b4 ? v[k] : v[4 + k];
+    u4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double keep = b3 ? u4[2 + k] : u4[k], send = b3 ? u4[k] : u4[2 + k];
+    u2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double u1 = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4);
+  u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+  u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = __shfl_sync(0xffffffffu, u1, ((c >> 2) & 1) * 16 + ((c >> 1) & 1) * 8 + (c & 1) * 4);
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Warp w applies published reflector block jb to its column block w (chunk rows < crow).
+__device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) {
+  const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
+  double* st = sm.st;
+  // W = R[8jb + i][8w + c] + sum_rows V[row][8jb + i] A[row][8w + c]   (C fragment: i = r8, c = 2 q4 + e)
+  double c0 = st[(8 * w + 2 * q4) * LD + 8 * jb + r8];
+  double c1 = st[(8 * w + 2 * q4 + 1) * LD + 8 * jb + r8];
+  double e0 = 0.0, e1 = 0.0;
+  const double* vp = st + (8 * jb + r8) * LD + RR + q4;  // V^T fragment: V[4kk + q4][8jb + r8]
+  const double* ap = st + (8 * w + r8) * LD + RR + q4;   // A fragment:   A[4kk + q4][8w + r8]
+  const int nk = (crow + 3) >> 2;
+  int kk = 0;
+#pragma unroll 4
+  for (; kk + 1 < nk; kk += 2) {
+    dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
+    dmma(e0, e1, vp[4 * kk + 4], ap[4 * kk + 4]);
+  }
+  if (kk < nk) dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
+  c0 += e0;
+  c1 += e1;
+  // W' = T^T W (through the warp scratch: C fragment -> B fragment)
+  double* ws = sm.ws[w];
+  ws[r8 * 8 + 2 * q4] = c0;
+  ws[r8 * 8 + 2 * q4 + 1] = c1;
+  __syncwarp();
+  const double* Tj = sm.Tm[jb];
+  double d0 = 0.0, d1 = 0.0;
+  dmma(d0, d1, Tj[q4 * 8 + r8], ws[q4 * 8 + r8]);
+  dmma(d0, d1, Tj[(4 + q4) * 8 + r8], ws[(4 + q4) * 8 + r8]);
+  __syncwarp();
+  st[(8 * w + 2 * q4) * LD + 8 * jb + r8] -= d0;
+  st[(8 * w + 2 * q4 + 1) * LD + 8 * jb + r8] -= d1;
+  ws[r8 * 8 + 2 * q4] = d0;
+  ws[r8 * 8 + 2 * q4 + 1] = d1;
+  __syncwarp();
+  const double b0 = ws[q4 * 8 + r8], b1 = ws[(4 + q4) * 8 + r8];  // W' as B fragments (k = i)
+  // A_w[chunk] -= V W'   (A fragment: -V[8mt + r8][8jb + q4 (+4)])
+  const int nm = (crow + 7) >> 3;
+#pragma unroll 2
+  for (int mt = 0; mt < nm; ++mt) {
+    double* cp = st + (8 * w + 2 * q4) * LD + RR + 8 * mt + r8;
+    double x0 = cp[0], x1 = cp[LD];
+    const double va = -st[(8 * jb + q4) * LD + RR + 8 * mt + r8];
+    const double vb = -st[(8 * jb + 4 + q4) * LD + RR + 8 * mt + r8];
+    dmma(x0, x1, va, b0);
+    dmma(x0, x1, vb, b1);
+    cp[0] = x0;
+    cp[LD] = x1;
+  }
+  __syncwarp();
+}
+
+// Warp w factors its column block (reflectors j = 8w + jj, jj < nr), forms T_w, stores V into
+// the chunk rows of its columns; taus on the diagonal of T.
+__device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) {
+  const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
+  double* st = sm.st;
+  double x[4][NB];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) x[t][c] = st[(8 * w + c) * LD + RR + 32 * t + lane];  // rows >= crow are 0
+  double tau[NB];
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) {
+    tau[jj] = 0.0;
+    if (jj < nr) {
+      const int j = 8 * w + jj;
+      double ss = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ss += x[t][jj] * x[t][jj];
+      const double sigma = wsum(ss);
+      const double alpha = st[j * LD + j];
+      double beta = alpha, scal = 0.0, tj = 0.0;
+      if (sigma != 0.0) {  // dlarfg with one reciprocal
+        const double nrm = sqrt(alpha * alpha + sigma);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        const double am = alpha - beta;
+        const double inv = 1.0 / (beta * am);
+        tj = -am * am * inv;
+        scal = beta * inv;
+      }
+      tau[jj] = tj;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
+      if (tj != 0.0) {
+        double dt[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          double q = 0.0;
+          if (c > jj) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) q += x[t][jj] * x[t][c];
+          }
+          dt[c] = q;
+        }
+        warp_sum8v(dt);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          if (c > jj) {
+            const double rj = st[(8 * w + c) * LD + j];
+            const double wv = tj * (rj + dt[c]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) x[t][c] -= wv * x[t][jj];
+            __syncwarp();
+            if (lane == 0) st[(8 * w + c) * LD + j] = rj - wv;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) st[j * LD + j] = beta;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) st[(8 * w + c) * LD + RR + 32 * t + lane] = x[t][c];
+  __syncwarp();
+  // G = V^T V over the chunk rows (DMMA), then T: T(i,i) = tau_i, T(0:i, i) = -tau_i T(0:i,0:i) G(0:i, i)
+  double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
+  const double* vp = st + (8 * w + r8) * LD + RR + q4;
+  const int nk = (crow + 3) >> 2;
+  int kk = 0;
+  for (; kk + 1 < nk; kk += 2) {
+    const double a = vp[4 * kk], b = vp[4 * kk + 4];
+    dmma(g0, g1, a, a);
+    dmma(h0, h1, b, b);
+  }
+  if (kk < nk) { const double a = vp[4 * kk]; dmma(g0, g1, a, a); }
+  double* ws = sm.ws[w];
+  ws[r8 * 8 + 2 * q4] = g0 + h0;
+  ws[r8 * 8 + 2 * q4 + 1] = g1 + h1;
+  __syncwarp();
+  if (lane < NB) {  // lane r builds row r of T
+    double trow[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      double v = 0.0;
+      if (lane == i) v = tau[i];
+      else if (lane < i) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q >= lane && q < i) s += trow[q] * ws[q * 8 + i];
+        v = -tau[i] * s;
+      }
+      trow[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) sm.Tm[w][lane * 8 + i] = trow[i];
+  }
+  __syncwarp();
+}
+
+// Factor the current stack (R block + chunk of crow rows in sm.st): ncol columns, nrefl
+// reflectors (< ncol only for a single-stack panel with fewer rows than columns).  q = stack
+// index (mbarrier parity).  On return (after a CTA barrier) V and T are stored at out.
+__device__ __forceinline__ void factor_stack(Smem& sm, int ncol, int nrefl, int crow, int q, double* __restrict__ out) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nbr = (nrefl + NB - 1) / NB;
+  const uint32_t par = (uint32_t)(q & 1);
+  if (8 * w < ncol) {
+    const int lim = w < nbr ? w : nbr;
+#pragma unroll 1
+    for (int jb = 0; jb < lim; ++jb) {
+      bar_wait(&sm.ready[jb], par);
+      update_block(sm, jb, w, crow);
+    }
+    if (w < nbr) {
+      factor_block(sm, w, min(NB, nrefl - 8 * w), crow);
+      bar_arrive(&sm.ready[w]);  // release: V, T, R rows of block w
+    }
+  }
+  __syncthreads();
+  // store V (CH x min(ncol, 8 nbr), column-major ld CH: whole blocks, so every staged column of a
+  // partial block is finite) and T
+  const int nvc = min(ncol, NB * nbr);
+  for (int idx = tid; idx < CH * nvc; idx += T) {
+    const int c = idx / CH, r = idx % CH;
+    out[idx] = sm.st[c * LD + RR + r];
+  }
+  double* tout = out + (int64_t)CH * ncol;
+  for (int idx = tid; idx < 64 * nbr; idx += T) tout[idx] = (&sm.Tm[0][0])[idx];
+  (void)lane;
+}
+
+// Initialise the mbarriers (once per launch, before the first stack) and zero the R block.
+__device__ __forceinline__ void init(Smem& sm) {
+  const int tid = threadIdx.x;
+  if (tid < C / NB) bar_init(&sm.ready[tid], 32);
+  for (int idx = tid; idx < C * LD; idx += T) sm.st[idx] = 0.0;
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+}
+
+// Zero the chunk rows (64 .. 191) of every column (before a loader fills them).
+__device__ __forceinline__ void zero_chunk(Smem& sm) {
+  for (int idx = threadIdx.x; idx < C * CH; idx += T) {
+    const int c = idx / CH, r = idx % CH;
+    sm.st[c * LD + RR + r] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- applications
+// Q [X; 0] for a factored panel: Q = (stack 0 blocks)(stack 1 blocks)..., each block
+// I - V T V^T, so the last stack's last block is applied first; the target's R-block rows start
+// as X and its chunk rows as 0 per stack (each chunk's rows are touched by its own stack only and
+// are final once that stack is applied).  Target columns in passes of AN; 3 CTAs per SM.
+constexpr int AN = 32;           // target columns per pass
+constexpr int ALD = CH + 4;      // ld of the chunk target (132 = 4 mod 16)
+constexpr int RLD = RR;          // ld of the R-block target (few accesses: no padding)
+constexpr int VLD = CH + 4;      // ld of a staged V block
+constexpr int WLD = AN + 4;      // row stride of W (8 x AN)
+struct ASmem {
+  double Ct[AN * ALD];           // chunk rows of the target (column-major)
+  double Rt[AN * RLD];           // R-block rows of the target (column-major)
+  double Vs[2][NB * VLD];        // staged V block (column-major), double-buffered
+  double Ts[2][64];
+  double Wp[W][8 * 12];          // partial W tiles (8 x 8, row stride 12) per (column tile, k-split)
+  double Wf[8 * WLD];            // W' = T W
+  uint64_t bar[2];
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void apply_init(ASmem& sm) {
+  for (int idx = threadIdx.x; idx < 2 * NB * VLD; idx += T) (&sm.Vs[0][0])[idx] = 0.0;  // never-staged columns
+  if (threadIdx.x == 0) {
+    bar_init(&sm.bar[0], 1);
+    bar_init(&sm.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// Stage V block jb of the stack factor F (and its T) into buffer b (thread 0).
+__device__ __forceinline__ void stage_block(ASmem& sm, const double* F, int ncol, int jb, int b) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const int nc = min(NB, ncol - NB * jb);
+  bar_expect(&sm.bar[b], (uint32_t)((nc * CH + 64) * sizeof(double)));
+  for (int c = 0; c < nc; ++c)
+    bulk_g2s(sm.Vs[b] + c * VLD, F + (int64_t)(NB * jb + c) * CH, CH * sizeof(double), &sm.bar[b]);
+  bulk_g2s(sm.Ts[b], F + (int64_t)CH * ncol + 64 * jb, 64 * sizeof(double), &sm.bar[b]);
+}
+
+// out[row * rs + col * cs] = (Q [X; 0])[row][col] for the m panel rows, X = src (ncx x nt,
+// column-major ld 64, global).  Stack q holds panel rows [q cr, min(m, (q+1) cr)), factor at
+// F + q * stack_doubles(ncol).  ph[]: the staging barriers' phase bits (kept across calls).
+__device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ src, int ncx, int nt,
+                      const double* __restrict__ F0, int64_t m, int cr, int ncol, int nrefl, double* __restrict__ out,
+                      int64_t rs, int64_t cs) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q4 = lane & 3, r8 = lane >> 2;
+  const int S = (int)((m + cr - 1) / cr);
+  const int nbr = (nrefl + NB - 1) / NB;
+  const int64_t sd = stack_doubles(ncol);
+#pragma unroll 1
+  for (int t0 = 0; t0 < nt; t0 += AN) {
+    const int ntp = min(AN, nt - t0), ntl = (ntp + 7) >> 3;
+    const int ksp = ntl == 1 ? 8 : ntl == 2 ? 4 : 2;  // k-splits of the W phase (ntl * ksp <= 8 units)
+    __syncthreads();
+    for (int idx = tid; idx < AN * RR; idx += T) {
+      const int c = idx / RR, r = idx % RR;
+      sm.Rt[c * RLD + r] = (c < ntp && r < ncx) ? src[(int64_t)(t0 + c) * 64 + r] : 0.0;
+    }
+#pragma unroll 1
+    for (int q = S - 1; q >= 0; --q) {
+      const double* F = F0 + (int64_t)q * sd;
+      const int64_t row0 = (int64_t)q * cr;
+      const int crow = (int)(m - row0 < cr ? m - row0 : cr);
+      const int nk = (crow + 3) >> 2, nm = (crow + 7) >> 3;
+      for (int idx = tid; idx < AN * CH; idx += T) sm.Ct[(idx / CH) * ALD + idx % CH] = 0.0;
+      __syncthreads();
+      int b = 0;
+      if (tid == 0) stage_block(sm, F, ncol, nbr - 1, 0);
+#pragma unroll 1
+      for (int jb = nbr - 1; jb >= 0; --jb, b ^= 1) {
+        if (jb > 0 && tid == 0) stage_block(sm, F, ncol, jb - 1, b ^ 1);
+        bar_wait(&sm.bar[b], ph[b]);
+        ph[b] ^= 1u;
+        const double* Vs = sm.Vs[b];
+        const bool first = (jb == nbr - 1);
+        // ---- W = Rt[8jb + i][:] + V^T Ct (8 x ntp), split over (column tile, k range)
+        {
+          const int nti = w / ksp, ks = w % ksp;
+          if (nti < ntl) {
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+            if (ks == 0) {
+              c0 = sm.Rt[(8 * nti + 2 * q4) * RLD + 8 * jb + r8];
+              c1 = sm.Rt[(8 * nti + 2 * q4 + 1) * RLD + 8 * jb + r8];
+            }
+            if (!first) {
+              const int k0 = (nk * ks) / ksp, k1 = (nk * (ks + 1)) / ksp;
+              const double* vp = Vs + r8 * VLD + q4;
+              const double* cp = sm.Ct + (8 * nti + r8) * ALD + q4;
+              int kk = k0;
+              for (; kk + 1 < k1; kk += 2) {
+                dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
+                dmma(e0, e1, vp[4 * kk + 4], cp[4 * kk + 4]);
+              }
+              if (kk < k1) dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
+            }
+            double* wp = sm.Wp[w];
+            wp[r8 * 12 + 2 * q4] = c0 + e0;
+            wp[r8 * 12 + 2 * q4 + 1] = c1 + e1;
+          }
+        }
+        __syncthreads();
+        // ---- W' = T W, R-block rows -= W'
+        if (w < ntl) {
+          double b0 = 0.0, b1 = 0.0;
+          for (int ks = 0; ks < ksp; ++ks) {
+            b0 += sm.Wp[w * ksp + ks][q4 * 12 + r8];
+            b1 += sm.Wp[w * ksp + ks][(4 + q4) * 12 + r8];
+          }
+          const double* Tj = sm.Ts[b];
+          double d0 = 0.0, d1 = 0.0;
+          dmma(d0, d1, Tj[r8 * 8 + q4], b0);
+          dmma(d0, d1, Tj[r8 * 8 + 4 + q4], b1);
+          sm.Wf[r8 * WLD + 8 * w + 2 * q4] = d0;
+          sm.Wf[r8 * WLD + 8 * w + 2 * q4 + 1] = d1;
+          sm.Rt[(8 * w + 2 * q4) * RLD + 8 * jb + r8] -= d0;
+          sm.Rt[(8 * w + 2 * q4 + 1) * RLD + 8 * jb + r8] -= d1;
+        }
+        __syncthreads();
+        // ---- Ct -= V W'
+        for (int u = w; u < nm * ntl; u += W) {
+          const int mt = u / ntl, nti = u % ntl;
+          double* cp = sm.Ct + (8 * nti + 2 * q4) * ALD + 8 * mt + r8;
+          double x0 = cp[0], x1 = cp[ALD];
+          dmma(x0, x1, -Vs[q4 * VLD + 8 * mt + r8], sm.Wf[q4 * WLD + 8 * nti + r8]);
+          dmma(x0, x1, -Vs[(4 + q4) * VLD + 8 * mt + r8], sm.Wf[(4 + q4) * WLD + 8 * nti + r8]);
+          cp[0] = x0;
+          cp[ALD] = x1;
+        }
+        __syncthreads();
+      }
+      for (int idx = tid; idx < ntp * crow; idx += T) {
+        const int c = idx / crow, r = idx % crow;
+        out[(row0 + r) * rs + (int64_t)(t0 + c) * cs] = sm.Ct[c * ALD + r];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace wy
+}  // namespace ttb
