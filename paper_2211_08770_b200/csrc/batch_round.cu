@@ -1303,45 +1303,58 @@ __device__ void wy_panel_chunk(wy::Smem& sm, const BRShape* S, const double* con
                                int i0, int ni) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q4 = lane & 3, r8 = lane >> 2;
   const int K = S->K, d = S->d, n = S->n[kc], Rpk = S->Rp[kc + 1];
-  const int mtiles = (Rpk + 7) >> 3;
-  // units (i, l, m-tile, n-tile)
-  int units = 0;
-  int nt_l[BR_MAXK];
-  for (int l = 0; l < K; ++l) { nt_l[l] = (S->r[l][kc] + 7) >> 3; units += nt_l[l]; }
-  const int per_i = units * mtiles;
+  const int mtiles = (Rpk + 7) >> 3;  // <= 8: one b' tile per warp
+  // Warp w owns b' tile w.  Per (i, term l, pair of a tiles) it issues every L and X fragment load
+  // of a 16-wide beta slab before its DMMAs, so a batch waits for the memory system once instead of
+  // once per k-step (the assembly is bound by the latency of these L2/HBM loads).
 #pragma unroll 1
-  for (int u = w; u < ni * per_i; u += wy::W) {
-    const int ii = u / per_i, rem = u % per_i;
-    const int mt = rem % mtiles;
-    int nl = rem / mtiles, l = 0;
-    while (nl >= nt_l[l]) { nl -= nt_l[l]; ++l; }
-    const int i = i0 + ii;
-    const int ra = S->r[l][kc], rb = S->r[l][kc + 1];
-    const int ob = S->off[kc + 1][l], oa = S->off[kc][l];
-    const double* X = cores[l * d + kc];
-    const int bp = 8 * mt + r8, a_b = 8 * nl + r8;  // A row (b'), B column (a)
-    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-    const double* lrow = L + (int64_t)bp * BR_C + ob;
-    const double* xrow = X + ((int64_t)a_b * n + i) * rb;
-    const bool aok = bp < Rpk, bok = a_b < ra;
-    int be = 0;
-    for (; be + 8 <= rb; be += 8) {
-      const double a0 = aok ? __ldg(lrow + be + q4) : 0.0, x0 = bok ? __ldg(xrow + be + q4) : 0.0;
-      const double a1 = aok ? __ldg(lrow + be + 4 + q4) : 0.0, x1 = bok ? __ldg(xrow + be + 4 + q4) : 0.0;
-      wy::dmma(c0, c1, a0, x0);
-      wy::dmma(e0, e1, a1, x1);
-    }
-    for (; be < rb; be += 4) {
-      const bool kok = be + q4 < rb;
-      const double a0 = (aok && kok) ? __ldg(lrow + be + q4) : 0.0, x0 = (bok && kok) ? __ldg(xrow + be + q4) : 0.0;
-      wy::dmma(c0, c1, a0, x0);
-    }
-    c0 += e0;
-    c1 += e1;
-    const int row = (i - i0) * Rpk + 8 * mt + r8, col = oa + 8 * nl + 2 * q4;
-    if (8 * mt + r8 < Rpk) {
-      if (8 * nl + 2 * q4 < ra) sm.st[col * wy::LD + wy::RR + row] = c0;
-      if (8 * nl + 2 * q4 + 1 < ra) sm.st[(col + 1) * wy::LD + wy::RR + row] = c1;
+  for (int mt = w; mt < mtiles; mt += wy::W) {
+    const int bp = 8 * mt + r8;
+    const bool aok = bp < Rpk;
+#pragma unroll 1
+    for (int ii = 0; ii < ni; ++ii) {
+      const int i = i0 + ii;
+      const int rowb = ii * Rpk + 8 * mt + r8;
+#pragma unroll 1
+      for (int l = 0; l < K; ++l) {
+        const int ra = S->r[l][kc], rb = S->r[l][kc + 1];
+        const int ob = S->off[kc + 1][l], oa = S->off[kc][l];
+        const double* X = cores[l * d + kc];
+        const double* lrow = L + (int64_t)bp * BR_C + ob;
+#pragma unroll 1
+        for (int n0 = 0; n0 < ra; n0 += 16) {
+          const int a0 = n0 + r8, a1 = n0 + 8 + r8;
+          const double* x0 = X + ((int64_t)a0 * n + i) * rb;
+          const double* x1 = X + ((int64_t)a1 * n + i) * rb;
+          const bool b0ok = a0 < ra, b1ok = a1 < ra;
+          double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll 1
+          for (int be = 0; be < rb; be += 16) {
+            double af[4], bf0[4], bf1[4];
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) {
+              const int beta = be + 4 * s4 + q4;
+              const bool kok = beta < rb;
+              af[s4] = (aok && kok) ? __ldg(lrow + beta) : 0.0;
+              bf0[s4] = (b0ok && kok) ? __ldg(x0 + beta) : 0.0;
+              bf1[s4] = (b1ok && kok) ? __ldg(x1 + beta) : 0.0;
+            }
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) {
+              wy::dmma(c00, c01, af[s4], bf0[s4]);
+              wy::dmma(c10, c11, af[s4], bf1[s4]);
+            }
+          }
+          if (aok) {
+            const int ca = n0 + 2 * q4;
+            double* dst = sm.st + (int64_t)(oa + ca) * wy::LD + wy::RR + rowb;
+            if (ca < ra) dst[0] = c00;
+            if (ca + 1 < ra) dst[wy::LD] = c01;
+            if (ca + 8 < ra) dst[8 * wy::LD] = c10;
+            if (ca + 9 < ra) dst[9 * wy::LD] = c11;
+          }
+        }
+      }
     }
   }
 }
@@ -1359,7 +1372,7 @@ __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
   const int tid = threadIdx.x;
   const int ni = S->wyni[kc], cr = ni * Rpk;
   const int nst = (n + ni - 1) / ni;
-  const int nrefl = (int)(m < c ? m : (int64_t)c);
+  const int nrefl = c;  // m >= c here (m < c panels take Q = I)
   const double* const* cores = A.cores + (int64_t)gb * K * d;
   const double* Lin = A.L + (int64_t)b * 2 * BR_C * BR_C + ((k + 1) & 1) * BR_C * BR_C;
   double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
@@ -1382,13 +1395,24 @@ __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
       wy_panel_chunk(sm, S, cores, Lin, kc, i0, nq);
     }
     __syncthreads();
+    if (m < c) break;  // fewer rows than columns (one stack): Q = I, R = A (below)
     wy::factor_stack(sm, c, nrefl, nq * Rpk, q, V + (int64_t)q * sd);
     __syncthreads();
   }
   (void)cr;
-  // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
   double* Lout = A.L + (int64_t)b * 2 * BR_C * BR_C + (k & 1) * BR_C * BR_C;
   const int rows = S->Rp[k - 1];
+  if (m < c) {
+    // A_k = I_m A_k: the identity is a valid (m x m orthogonal) Q and R = A_k itself, exactly.  The
+    // augmented factorisation cannot be used here: with m reflectors for c > m columns, columns
+    // whose leading block is rank deficient would keep part of their chunk.
+    for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
+      const int row = idx / BR_C, col = idx % BR_C;
+      Lout[idx] = (row < rows && col < c) ? sm.st[col * wy::LD + wy::RR + row] : 0.0;
+    }
+    return;
+  }
+  // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
   for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
     const int row = idx / BR_C, col = idx % BR_C;
     Lout[idx] = (row < rows && col < c && row <= col) ? sm.st[col * wy::LD + row] : 0.0;
@@ -1522,7 +1546,15 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_apply_wy_kernel(BRArgs A, int
   double* dst = (k + 1 == d) ? out + S->ooff[kn] : A.Z + (int64_t)b * 2 * S->zstride + ((k + 1) & 1) * S->zstride;
   const double* V = A.V + (int64_t)b * S->vstride + S->voff[kn];
   const int cr = S->wyni[kn] * S->Rp[k + 1];
-  wy::apply(sm, ph, tt + BR_C * BR_C, cp, rho, V, m1, cr, c1, (int)(m1 < c1 ? m1 : (int64_t)c1), dst, 1, m1);
+  if (m1 < c1) {  // Q_{k+1} = I (br_r2l_wy_kernel): the panel rows are the target rows (cp = m1)
+    const double* src = tt + BR_C * BR_C;
+    for (int idx = threadIdx.x; idx < rho * m1; idx += wy::T) {
+      const int col = idx / (int)m1, row = idx % (int)m1;
+      dst[row + (int64_t)col * m1] = src[col * BR_C + row];
+    }
+    return;
+  }
+  wy::apply(sm, ph, tt + BR_C * BR_C, cp, rho, V, m1, cr, c1, c1, dst, 1, m1);
 }
 
 // Copy item b's cores from the worst-case workspace to the exact-size arena.
@@ -1798,6 +1830,15 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         else
           TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
                   br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
+        static const char* dump = std::getenv("TT_B200_BR_DUMP");  // debugging: item 0's R factors
+        if (dump && w0 == 0) {
+          std::vector<double> h(BR_C * BR_C);
+          TTB_CUDA(cudaMemcpyAsync(h.data(), L.p + ((kc + 1) & 1) * BR_C * BR_C, sizeof(double) * h.size(),
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+          TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+          FILE* f = std::fopen(dump, kc == d - 1 ? "wb" : "ab");
+          if (f) { std::fwrite(h.data(), sizeof(double), h.size(), f); std::fclose(f); }
+        }
       }
       for (int k = 1; k < d; ++k) {
         if (use_wy)

@@ -187,9 +187,10 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
 #pragma unroll
       for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
       if (tj != 0.0) {
-        double dt[NB];
+        double dt[NB], rj[NB];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) {
+        for (int c = 0; c < NB; ++c) {  // R row j of the block's later columns: independent loads
+          rj[c] = c > jj ? st[(8 * w + c) * LD + j] : 0.0;
           double q = 0.0;
           if (c > jj) {
 #pragma unroll
@@ -201,13 +202,17 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
           if (c > jj) {
-            const double rj = st[(8 * w + c) * LD + j];
-            const double wv = tj * (rj + dt[c]);
+            const double wv = tj * (rj[c] + dt[c]);
 #pragma unroll
             for (int t = 0; t < 4; ++t) x[t][c] -= wv * x[t][jj];
-            __syncwarp();
-            if (lane == 0) st[(8 * w + c) * LD + j] = rj - wv;
+            rj[c] -= wv;
           }
+        }
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            if (c > jj) st[(8 * w + c) * LD + j] = rj[c];
         }
       }
       __syncwarp();
@@ -450,6 +455,7 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ s
         const int c = idx / crow, r = idx % crow;
         out[(row0 + r) * rs + (int64_t)(t0 + c) * cs] = sm.Ct[c * ALD + r];
       }
+      __syncthreads();  // every thread is done reading Ct before the next stack zeroes it
     }
   }
   __syncthreads();
