@@ -1299,65 +1299,108 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_apply_kernel(BRArgs A, int k) 
 // r2l chunk of panel kc (core k = kc + 1 < d), mode indices [i0, i0 + ni): rows (i - i0) Rpk + b',
 // column off_{k-1,l} + a:  sum_beta L_{k+1}[b'][off_{k,l} + beta] X_k^(l)[a, i, beta] as DMMA tiles
 // (M = b', N = a, K = beta), L read from the item's L slot (row-major ld 64, L2-resident).
-__device__ void wy_panel_chunk(wy::Smem& sm, const BRShape* S, const double* const* cores, const double* L, int kc,
-                               int i0, int ni) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, q4 = lane & 3, r8 = lane >> 2;
-  const int K = S->K, d = S->d, n = S->n[kc], Rpk = S->Rp[kc + 1];
-  const int mtiles = (Rpk + 7) >> 3;  // <= 8: one b' tile per warp
-  // Warp w owns b' tile w.  Per (i, term l, pair of a tiles) it issues every L and X fragment load
-  // of a 16-wide beta slab before its DMMAs, so a batch waits for the memory system once instead of
-  // once per k-step (the assembly is bound by the latency of these L2/HBM loads).
+// Loader of the right-to-left panel of core k = kc + 1 (wy::factor_panel): stack q holds mode
+// indices [q ni, q ni + nq), rows (i - i0) Rpk + b'; column off_{k-1,l} + a of term l is
+//   A[(i, b'), col] = sum_beta L_{k+1}[b'][off_{k,l} + beta] X_k^(l)[a, i, beta]   (k < d)
+//   A[i, col]      = c_l X_d^(l)[a, i, 0]                                         (k = d)
+// (the TT-sum's block-diagonal cores read in place).  A warp fills its own 8 columns: as DMMA tiles
+// (M = b', N = a, K = beta; L from the item's L slot, row-major ld 64, L2-resident) when they belong
+// to one term, else element by element.
+struct R2LLoader {
+  const BRShape* S;
+  const double* const* cores;
+  const double* L;
+  const double* coef;
+  int kc, n, Rpk, c, ni, last, K, d;
+  __device__ int stacks() const { return (n + ni - 1) / ni; }
+  __device__ int crow(int q) const { return min(ni, n - q * ni) * Rpk; }
+  __device__ int term(int col) const {
+    int l = 0;
+    while (l + 1 < K && col >= S->off[kc][l + 1]) ++l;
+    return l;
+  }
+  __device__ void load(wy::Smem& sm, int q, int w) const {
+    const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
+    const int i0 = q * ni, nq = min(ni, n - i0);
+    const int c0 = wy::NB * w, c1 = min(c0 + wy::NB, c);
+    wy::zero_cols(sm, w);
+    if (last) {
+      for (int idx = lane; idx < nq * wy::NB; idx += 32) {
+        const int ii = idx / wy::NB, col = c0 + idx % wy::NB;
+        if (col < c1) {
+          const int l = term(col), a = col - S->off[kc][l];
+          sm.st[col * wy::LD + wy::RR + ii] = coef[l] * __ldg(cores[l * d + kc] + (int64_t)a * n + i0 + ii);
+        }
+      }
+      __syncwarp();
+      return;
+    }
+    const int l0 = term(c0), l1 = term(c1 - 1);
+    if (l0 == l1) {  // one term: D (b' x 8) = L[:, ob + beta] X[a0 + (0..7)][i][beta]^T
+      const int ra = S->r[l0][kc], rb = S->r[l0][kc + 1], ob = S->off[kc + 1][l0];
+      const int a0 = c0 - S->off[kc][l0];
+      const double* X = cores[l0 * d + kc];
+      const int mtiles = (Rpk + 7) >> 3;
+      const bool bok = a0 + r8 < ra && c0 + r8 < c1;
 #pragma unroll 1
-  for (int mt = w; mt < mtiles; mt += wy::W) {
-    const int bp = 8 * mt + r8;
-    const bool aok = bp < Rpk;
+      for (int ii = 0; ii < nq; ++ii) {
+        const double* xr = X + ((int64_t)(a0 + r8) * n + i0 + ii) * rb;
 #pragma unroll 1
-    for (int ii = 0; ii < ni; ++ii) {
-      const int i = i0 + ii;
-      const int rowb = ii * Rpk + 8 * mt + r8;
-#pragma unroll 1
-      for (int l = 0; l < K; ++l) {
-        const int ra = S->r[l][kc], rb = S->r[l][kc + 1];
-        const int ob = S->off[kc + 1][l], oa = S->off[kc][l];
-        const double* X = cores[l * d + kc];
-        const double* lrow = L + (int64_t)bp * BR_C + ob;
-#pragma unroll 1
-        for (int n0 = 0; n0 < ra; n0 += 16) {
-          const int a0 = n0 + r8, a1 = n0 + 8 + r8;
-          const double* x0 = X + ((int64_t)a0 * n + i) * rb;
-          const double* x1 = X + ((int64_t)a1 * n + i) * rb;
-          const bool b0ok = a0 < ra, b1ok = a1 < ra;
-          double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+        for (int mg = 0; mg < mtiles; mg += 4) {
+          double acc[4][2];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll 1
           for (int be = 0; be < rb; be += 16) {
-            double af[4], bf0[4], bf1[4];
+            double af[4][4], bf[4];
 #pragma unroll
             for (int s4 = 0; s4 < 4; ++s4) {
               const int beta = be + 4 * s4 + q4;
               const bool kok = beta < rb;
-              af[s4] = (aok && kok) ? __ldg(lrow + beta) : 0.0;
-              bf0[s4] = (b0ok && kok) ? __ldg(x0 + beta) : 0.0;
-              bf1[s4] = (b1ok && kok) ? __ldg(x1 + beta) : 0.0;
+              bf[s4] = (bok && kok) ? __ldg(xr + beta) : 0.0;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int bp = 8 * (mg + t) + r8;
+                af[t][s4] = (kok && bp < Rpk) ? __ldg(L + (int64_t)bp * BR_C + ob + beta) : 0.0;
+              }
             }
 #pragma unroll
-            for (int s4 = 0; s4 < 4; ++s4) {
-              wy::dmma(c00, c01, af[s4], bf0[s4]);
-              wy::dmma(c10, c11, af[s4], bf1[s4]);
-            }
+            for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) wy::dmma(acc[t][0], acc[t][1], af[t][s4], bf[s4]);
           }
-          if (aok) {
-            const int ca = n0 + 2 * q4;
-            double* dst = sm.st + (int64_t)(oa + ca) * wy::LD + wy::RR + rowb;
-            if (ca < ra) dst[0] = c00;
-            if (ca + 1 < ra) dst[wy::LD] = c01;
-            if (ca + 8 < ra) dst[8 * wy::LD] = c10;
-            if (ca + 9 < ra) dst[9 * wy::LD] = c11;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int bp = 8 * (mg + t) + r8;
+            if (bp < Rpk) {
+              const int ca = 2 * q4;
+              double* dst = sm.st + (int64_t)(c0 + ca) * wy::LD + wy::RR + ii * Rpk + bp;
+              if (c0 + ca < c1 && a0 + ca < ra) dst[0] = acc[t][0];
+              if (c0 + ca + 1 < c1 && a0 + ca + 1 < ra) dst[wy::LD] = acc[t][1];
+            }
           }
         }
       }
+    } else {  // columns of several terms: element by element, lane = row
+      const int rows = nq * Rpk;
+#pragma unroll 1
+      for (int col = c0; col < c1; ++col) {
+        const int l = term(col), a = col - S->off[kc][l];
+        const int rb = S->r[l][kc + 1], ob = S->off[kc + 1][l];
+        const double* X = cores[l * d + kc];
+        for (int r = lane; r < rows; r += 32) {
+          const int ii = r / Rpk, bp = r % Rpk;
+          const double* xp = X + ((int64_t)a * n + i0 + ii) * rb;
+          const double* lp = L + (int64_t)bp * BR_C + ob;
+          double acc = 0.0;
+          for (int be = 0; be < rb; ++be) acc += __ldg(lp + be) * __ldg(xp + be);
+          sm.st[col * wy::LD + wy::RR + r] = acc;
+        }
+      }
     }
+    __syncwarp();
   }
-}
+};
 
 __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
@@ -1368,56 +1411,61 @@ __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
   const int k = kc + 1;                 // 1-based core index, 2..d
   const int n = S->n[kc], Rpk = S->Rp[k], c = S->R[k - 1];
   const int64_t m = (int64_t)n * Rpk;
-  const bool last = (k == d);
   const int tid = threadIdx.x;
-  const int ni = S->wyni[kc], cr = ni * Rpk;
-  const int nst = (n + ni - 1) / ni;
-  const int nrefl = c;  // m >= c here (m < c panels take Q = I)
-  const double* const* cores = A.cores + (int64_t)gb * K * d;
-  const double* Lin = A.L + (int64_t)b * 2 * BR_C * BR_C + ((k + 1) & 1) * BR_C * BR_C;
-  double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
-  const int64_t sd = wy::stack_doubles(c);
-  wy::init(sm);
-#pragma unroll 1
-  for (int q = 0; q < nst; ++q) {
-    const int i0 = q * ni, nq = min(ni, n - i0);
-    wy::zero_chunk(sm);
-    __syncthreads();
-    if (last) {  // A[i, off_l + a] = c_l X_d^(l)[a, i, 0]
-      for (int idx = tid; idx < nq * c; idx += wy::T) {
-        const int ii = idx / c, col = idx % c;
-        int l = 0;
-        while (l + 1 < K && col >= S->off[k - 1][l + 1]) ++l;
-        const int a = col - S->off[k - 1][l];
-        sm.st[col * wy::LD + wy::RR + ii] = A.coef[(int64_t)gb * K + l] * __ldg(cores[l * d + kc] + (int64_t)a * n + i0 + ii);
-      }
-    } else {
-      wy_panel_chunk(sm, S, cores, Lin, kc, i0, nq);
-    }
-    __syncthreads();
-    if (m < c) break;  // fewer rows than columns (one stack): Q = I, R = A (below)
-    wy::factor_stack(sm, c, nrefl, nq * Rpk, q, V + (int64_t)q * sd);
-    __syncthreads();
-  }
-  (void)cr;
+  R2LLoader ld{S, A.cores + (int64_t)gb * K * d, A.L + (int64_t)b * 2 * BR_C * BR_C + ((k + 1) & 1) * BR_C * BR_C,
+               A.coef + (int64_t)gb * K, kc, n, Rpk, c, S->wyni[kc], k == d ? 1 : 0, K, d};
   double* Lout = A.L + (int64_t)b * 2 * BR_C * BR_C + (k & 1) * BR_C * BR_C;
   const int rows = S->Rp[k - 1];
   if (m < c) {
-    // A_k = I_m A_k: the identity is a valid (m x m orthogonal) Q and R = A_k itself, exactly.  The
-    // augmented factorisation cannot be used here: with m reflectors for c > m columns, columns
-    // whose leading block is rank deficient would keep part of their chunk.
+    // fewer rows than columns (one stack): A_k = I_m A_k -- the identity is a valid orthogonal Q and
+    // R = A_k exactly (an augmented factorisation with m reflectors for c > m columns would lose
+    // the columns whose leading block is rank deficient)
+    const int w = tid >> 5;
+    if (8 * w < c) ld.load(sm, 0, w);
+    __syncthreads();
     for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
       const int row = idx / BR_C, col = idx % BR_C;
       Lout[idx] = (row < rows && col < c) ? sm.st[col * wy::LD + wy::RR + row] : 0.0;
     }
     return;
   }
+  wy::factor_panel(sm, ld, c, A.V + (int64_t)b * S->vstride + S->voff[kc]);
   // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
   for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
     const int row = idx / BR_C, col = idx % BR_C;
     Lout[idx] = (row < rows && col < c && row <= col) ? sm.st[col * wy::LD + row] : 0.0;
   }
 }
+
+// Loader of a tall left-to-right Y_k (p rows, cp columns) in stacks of 128 rows.
+struct YLoader {
+  const BRShape* S;
+  const double* Z;       // k > 1: Y_k row-major ld cp
+  const double* L2;      // k = 1: L_2 (row-major ld 64)
+  const double* const* cores;
+  int k, p, cp, K, d;
+  __device__ int stacks() const { return (p + wy::CH - 1) / wy::CH; }
+  __device__ int crow(int q) const { return min(wy::CH, p - q * wy::CH); }
+  __device__ double el(int64_t row, int col) const {
+    if (k > 1) return Z[row * cp + col];
+    double s = 0.0;  // Y_1[i, b'] = sum_l sum_beta X_1^(l)[0, i, beta] L_2[b'][off_{1,l} + beta]
+    const double* Lr = L2 + (int64_t)col * BR_C;
+    for (int l = 0; l < K; ++l) {
+      const int rl = S->r[l][1], o = S->off[1][l];
+      const double* xp = cores[l * d] + row * rl;
+      for (int be = 0; be < rl; ++be) s += Lr[o + be] * __ldg(xp + be);
+    }
+    return s;
+  }
+  __device__ void load(wy::Smem& sm, int q, int w) const {
+    const int lane = threadIdx.x & 31;
+    const int rows = crow(q), c0 = wy::NB * w, c1 = min(c0 + wy::NB, cp);
+    wy::zero_cols(sm, w);
+    for (int r = lane; r < rows; r += 32)
+      for (int col = c0; col < c1; ++col) sm.st[col * wy::LD + wy::RR + r] = el((int64_t)q * wy::CH + r, col);
+    __syncwarp();
+  }
+};
 
 // Left-to-right QR of a tall Y_k (p > 64 rows, cp columns) with the WY engine; R -> JM.
 __global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k) {
@@ -1444,41 +1492,14 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k)
   const double* Lin = A.L;  // k == 1: L_2 in slot 0
   const double* Z = A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride;
   const double* const* cores = A.cores + (int64_t)gb * K * d;
-  // element (row, col) of Y_k
-  auto yel = [&](int64_t row, int col) -> double {
-    if (k > 1) return Z[row * cp + col];
-    double s = 0.0;  // Y_1[i, b'] = sum_l sum_beta X_1^(l)[0, i, beta] L_2[b'][off_{1,l} + beta]
-    const double* Lr = Lin + (int64_t)b * 2 * BR_C * BR_C + (int64_t)col * BR_C;
-    for (int l = 0; l < K; ++l) {
-      const int rl = S->r[l][1], o = S->off[1][l];
-      const double* xp = cores[l * d] + row * rl;
-      for (int be = 0; be < rl; ++be) s += Lr[o + be] * __ldg(xp + be);
-    }
-    return s;
-  };
-  wy::init(sm);
+  YLoader ld{S, Z, Lin + (int64_t)b * 2 * BR_C * BR_C, cores, k, (int)p, cp, K, d};
   if (tall) {
-    double* YV = A.YV + (int64_t)b * S->ystride;
-    const int64_t sd = wy::stack_doubles(cp);
-    const int nst = (int)((p + wy::CH - 1) / wy::CH);
-#pragma unroll 1
-    for (int q = 0; q < nst; ++q) {
-      const int64_t r0 = (int64_t)q * wy::CH;
-      const int crow = (int)(p - r0 < wy::CH ? p - r0 : (int64_t)wy::CH);
-      wy::zero_chunk(sm);
-      __syncthreads();
-      for (int idx = tid; idx < crow * cp; idx += wy::T) {
-        const int r = idx / cp, col = idx % cp;
-        sm.st[col * wy::LD + wy::RR + r] = yel(r0 + r, col);
-      }
-      __syncthreads();
-      wy::factor_stack(sm, cp, cp, crow, q, YV + (int64_t)q * sd);
-      __syncthreads();
-    }
+    wy::factor_panel(sm, ld, cp, A.YV + (int64_t)b * S->ystride);
   } else {
+    wy::init(sm);
     for (int idx = tid; idx < p * cp; idx += wy::T) {
       const int r = idx / cp, col = idx % cp;
-      sm.st[col * wy::LD + r] = yel(r, col);  // short Y_k: the Jacobi input is Y itself
+      sm.st[col * wy::LD + r] = ld.el(r, col);  // short Y_k: the Jacobi input is Y itself
     }
     __syncthreads();
   }

@@ -48,6 +48,7 @@ struct Smem {
   double ws[W][64];       // per-warp 8 x 8 scratch (fragment layout changes)
   double red[32];
   uint64_t ready[C / NB]; // block published (32 arrivals: the owner warp's lanes)
+  uint64_t used[C / NB];  // block applied by every later warp (32 arrivals per consumer warp)
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -308,6 +309,73 @@ __device__ __forceinline__ void zero_chunk(Smem& sm) {
     const int c = idx / CH, r = idx % CH;
     sm.st[c * LD + RR + r] = 0.0;
   }
+}
+
+// ---------------------------------------------------------------- pipelined panel
+// The whole flat tree of a panel with no CTA barrier between stacks: warp w owns column block w
+// and loops over the stacks on its own -- apply the published blocks jb < w of stack q (consumer
+// arrival on used[jb] after each), factor its block, publish it, store its V and T, then (once
+// every later warp has applied its block: used[w]) load its columns of stack q+1 into the chunk
+// rows.  Warp 0 can thus start stack q+1 while the last warps still work on stack q: the stacks
+// flow through the warps as a wavefront (the data a warp reads from others are only the V / T of
+// published blocks; its own columns and their R rows are private to it).
+//   L.stacks(), L.crow(q) (rows of stack q), L.load(sm, q, w) (warp w fills rows 64.. of its
+//   columns for stack q, rows >= crow zero; warp-synchronous), out + q * stack_doubles(ncol).
+template <class Loader>
+__device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __restrict__ out) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nact = (ncol + NB - 1) / NB;  // active column blocks (all factored: nrefl = ncol)
+  const int S = L.stacks();
+  const int64_t sd = stack_doubles(ncol);
+  if (tid < C / NB) {
+    bar_init(&sm.ready[tid], 32);
+    bar_init(&sm.used[tid], (uint32_t)(32 * max(1, nact - 1 - tid)));  // every lane of every consumer
+  }
+  for (int idx = tid; idx < C * RR; idx += T) sm.st[(idx / RR) * LD + idx % RR] = 0.0;  // R block = 0
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (w < nact) {
+    L.load(sm, 0, w);
+#pragma unroll 1
+    for (int q = 0; q < S; ++q) {
+      const int crow = L.crow(q);
+      const uint32_t par = (uint32_t)(q & 1);
+#pragma unroll 1
+      for (int jb = 0; jb < w; ++jb) {
+        bar_wait(&sm.ready[jb], par);
+        update_block(sm, jb, w, crow);
+        bar_arrive(&sm.used[jb]);
+      }
+      factor_block(sm, w, min(NB, ncol - NB * w), crow);
+      bar_arrive(&sm.ready[w]);
+      // V (CH x 8 of this block, column-major ld CH) and T_w
+      double* o = out + (int64_t)q * sd;
+      const int nc = min(NB, ncol - NB * w);
+#pragma unroll 4
+      for (int idx = lane; idx < CH * nc; idx += 32) {
+        const int c = idx / CH, r = idx % CH;
+        o[(int64_t)(NB * w + c) * CH + r] = sm.st[(NB * w + c) * LD + RR + r];
+      }
+      o[(int64_t)CH * ncol + 64 * w + lane] = sm.Tm[w][lane];
+      o[(int64_t)CH * ncol + 64 * w + 32 + lane] = sm.Tm[w][32 + lane];
+      if (q + 1 < S) {
+        if (w < nact - 1) bar_wait(&sm.used[w], par);  // every later warp is done with V_w, T_w
+        __syncwarp();
+        L.load(sm, q + 1, w);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Zero rows 64.. of warp w's columns (before a loader fills them).
+__device__ __forceinline__ void zero_cols(Smem& sm, int w) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+#pragma unroll
+    for (int t = 0; t < CH / 32; ++t) sm.st[(NB * w + c) * LD + RR + 32 * t + lane] = 0.0;
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- applications
