@@ -86,6 +86,7 @@ struct BRArgs {
   double* Z;                   // Y_{k+1} staging, 2 slots   [item][2][zstride]
   double* out;                 // worst-case output cores    [item][ostride]
   double* JM;                  // l2r: Jacobi input (R_Y or Y), 64 x 64 per item
+  double* QX;                  // l2r: QRCP of R_Y^T (factors 64 x 64 + 64 taus) per item
   double* TT;                  // l2r: apply targets U_rho and V_rho S, 2 x 64 x 64 per item
   int* ranks;                  // [item][d+1]
   double* scal;                // [item][4]: ||x||, tau, s, zero flag
@@ -95,6 +96,7 @@ struct BRArgs {
   int64_t max_rank;
   int keep_all;
   int jac_t;                   // tall splits: one-sided Jacobi on R_Y^T (rows of R) instead of R_Y
+  int qrcp_svd;                // tall splits: rank-revealing QR of R_Y^T before the Jacobi (truncated)
   int item0;                   // global index of this wave's first item
   long long* dbg;              // TT_B200_BR_DEBUG: CTA 0 phase cycle counters (else null)
 };
@@ -1036,6 +1038,117 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
   return conv;
 }
 
+// Column-pivoted Householder QR of the rows x nc matrix X in sm.Rs (column-major, ld 64), stopped
+// at the first step s whose remaining columns carry squared mass <= stop2 (LAPACK dlaqp2
+// arithmetic; masses recomputed exactly after every step, no downdating).  Reflectors below the
+// diagonal, taus in tau_s[], pivot order in piv[] (pivoted column j = original column piv[j]);
+// returns the number of steps k, the remaining mass in *e2.  Warp w owns the columns j = w mod 8.
+__device__ int br_qrcp(BRSmem& sm, int rows, int nc, double stop2, double* tau_s, int* piv, double* nrm2,
+                       double* e2) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = warp; j < nc; j += BR_W) {
+    const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
+    const double q = warp_sum(x0 * x0 + x1 * x1);
+    if (lane == 0) { nrm2[j] = q; piv[j] = j; }
+  }
+  __syncthreads();
+  int s = 0;
+#pragma unroll 1
+  for (; s < nc && s < rows; ++s) {
+    if (warp == 0) {  // remaining mass and the pivot (largest mass, lowest index on ties)
+      const int j0 = s + lane, j1 = s + lane + 32;
+      const double v0 = j0 < nc ? nrm2[j0] : -1.0, v1 = j1 < nc ? nrm2[j1] : -1.0;
+      double tot = (v0 > 0.0 ? v0 : 0.0) + (v1 > 0.0 ? v1 : 0.0);
+      double bv = v1 > v0 ? v1 : v0;
+      int bj = v1 > v0 ? j1 : j0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+      }
+      if (lane == 0) { sm.red[0] = tot; sm.flag = bj; }
+    }
+    __syncthreads();
+    const double tot = sm.red[0];
+    const int p = sm.flag;
+    if (tot <= stop2) break;
+    if (p != s) {  // swap columns s and p
+      for (int r = tid; r < BR_C; r += BR_T) {
+        const double t = sm.Rs[s * BR_C + r];
+        sm.Rs[s * BR_C + r] = sm.Rs[p * BR_C + r];
+        sm.Rs[p * BR_C + r] = t;
+      }
+      if (tid == 0) {
+        const double t = nrm2[s]; nrm2[s] = nrm2[p]; nrm2[p] = t;
+        const int ti = piv[s]; piv[s] = piv[p]; piv[p] = ti;
+      }
+      __syncthreads();
+    }
+    if (warp == (s & (BR_W - 1))) {  // reflector of column s, rows s..63 (dlarfg)
+      double* cs = sm.Rs + s * BR_C;
+      const double x0 = cs[lane], x1 = cs[lane + 32];
+      const double sig = warp_sum((lane > s ? x0 * x0 : 0.0) + (lane + 32 > s ? x1 * x1 : 0.0));
+      const double alpha = cs[s];
+      double beta = alpha, tau = 0.0, scal = 0.0;
+      if (sig != 0.0) {
+        const double nr = sqrt(alpha * alpha + sig);
+        beta = alpha >= 0.0 ? -nr : nr;
+        const double am = alpha - beta;
+        const double inv = 1.0 / (beta * am);
+        tau = -am * am * inv;
+        scal = beta * inv;
+      }
+      __syncwarp();
+      if (lane > s) cs[lane] = x0 * scal;
+      if (lane + 32 > s) cs[lane + 32] = x1 * scal;
+      if (lane == 0) { cs[s] = beta; tau_s[s] = tau; }
+    }
+    __syncthreads();
+    const double tau = tau_s[s];
+    const double* v = sm.Rs + s * BR_C;
+    const double v0 = lane > s ? v[lane] : (lane == s ? 1.0 : 0.0);
+    const double v1 = lane + 32 > s ? v[lane + 32] : (lane + 32 == s ? 1.0 : 0.0);
+    for (int j = s + 1 + ((warp - s - 1) & (BR_W - 1)); j < nc; j += BR_W) {  // this warp's columns > s
+      double* cj = sm.Rs + j * BR_C;
+      double x0 = cj[lane], x1 = cj[lane + 32];
+      if (tau != 0.0) {
+        const double w = tau * warp_sum(v0 * x0 + v1 * x1);
+        x0 -= w * v0;
+        x1 -= w * v1;
+        cj[lane] = x0;
+        cj[lane + 32] = x1;
+      }
+      const double q = warp_sum((lane > s ? x0 * x0 : 0.0) + (lane + 32 > s ? x1 * x1 : 0.0));
+      if (lane == 0) nrm2[j] = q;
+    }
+    __syncthreads();
+  }
+  double rest = 0.0;
+  for (int j = s; j < nc; ++j) rest += nrm2[j];
+  *e2 = rest;
+  return s;
+}
+
+// y (64-vector in shared or global memory, per warp) <- Q [y] with Q = H_0 .. H_{k-1} the
+// reflectors stored below the diagonal of F (column-major ld 64) and taus t (H_{k-1} applied first).
+__device__ __forceinline__ void br_apply_qx(double& y0, double& y1, const double* __restrict__ F,
+                                            const double* __restrict__ t, int k) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int i = k - 1; i >= 0; --i) {
+    const double tau = t[i];
+    if (tau == 0.0) continue;
+    const double* v = F + i * BR_C;
+    const double v0 = lane > i ? v[lane] : (lane == i ? 1.0 : 0.0);
+    const double v1 = lane + 32 > i ? v[lane + 32] : (lane + 32 == i ? 1.0 : 0.0);
+    const double w = tau * warp_sum(v0 * y0 + v1 * y1);
+    y0 -= w * v0;
+    y1 -= w * v1;
+  }
+}
+
 // ---- left-to-right step at split k, in three launches over the batch:
 //   br_l2r_qr_kernel     Y_k -> (tall: flat-tree QR, reflectors to YV/YT) -> Jacobi input JM;
 //                        split 1 also computes ||x|| and tau
@@ -1140,6 +1253,85 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T)
     sm.Rs[idx] = jt ? jm[(idx % BR_C) * BR_C + idx / BR_C] : jm[idx];
   __syncthreads();
+  static_assert(BR_C == 64, "QRCP path assumes 64-row columns");
+  if (jt && !A.keep_all && A.max_rank <= 0 && A.qrcp_svd) {
+    // Truncated SVD through a rank-revealing QR of X = R_Y^T: X P = Q_X [T; E]
+    // with ||E||_F^2 = e2 <= (theta tau)^2, theta = 1e-3, then one-sided Jacobi on T^T (cp x kq,
+    // kq ~ the kept rank instead of 64).  Ky Fan: tail(rho)^2 lies in [sum_{j>=rho} sigma_j(T)^2,
+    // that + e2], so the decision equals the exact-SVD decision unless tau^2 falls inside the
+    // interval for rho - 1 (then the full Jacobi below decides).  U_rho (R_Y's left vectors) =
+    // P (T^T J) / sigma, V_rho S = Q_X [J Sigma; 0] (or Q_X [J Sigma^-1; 0] for U = Y W).
+    const double tau = sc[1];
+    double* qx = A.QX + (int64_t)b * (BR_C * BR_C + BR_C);
+    double* taus = sm.vb[1];
+    double* nrm2 = sm.vb[0];
+    double e2 = 0.0;
+    const int kq = br_qrcp(sm, cp, cp, 1e-6 * tau * tau, taus, sm.cterm, nrm2, &e2);
+    for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) qx[idx] = sm.Rs[idx];
+    if (tid < BR_C) qx[BR_C * BR_C + tid] = tid < kq ? taus[tid] : 0.0;
+    __syncthreads();
+    for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) {  // C = T^T: column i = row i of T (j >= i)
+      const int i = idx / BR_C, j = idx % BR_C;
+      sm.Rs[idx] = (i < kq && j < cp && j >= i) ? qx[j * BR_C + i] : 0.0;
+    }
+    __syncthreads();
+    const bool conv = kq < 1 || br_jacobi(sm, cp, kq, tau * tau / (double)(kq > 0 ? kq : 1),
+                                          (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
+    if (tid == 0) {
+      int rho = kq;
+      double t2 = e2;
+      for (int r = kq - 1; r >= 1; --r) {
+        t2 += sm.sig[r] * sm.sig[r];
+        if (t2 <= tau * tau) rho = r; else break;
+      }
+      rho = rho < 1 ? 1 : rho;
+      double lo = 0.0;  // lower bound of the exact tail at rho - 1
+      for (int r = rho - 1; r < kq; ++r) lo += sm.sig[r] * sm.sig[r];
+      const bool amb = kq < 1 || (rho > 1 && lo <= tau * tau);
+      if (!conv && !amb) A.info[b] = 1;
+      sm.flag = amb ? 1 : 0;
+      sm.rho = rho;
+    }
+    __syncthreads();
+    if (!sm.flag) {
+      const int rho = sm.rho;
+      if (tid == 0) rk[k] = rho;
+      const bool use_gemm = sm.sig[rho - 1] >= 1e-3 * sm.sig[0];
+      if (tid == 0) A.gemm[b] = use_gemm ? 1 : 0;
+      double* tt = A.TT + (int64_t)b * 2 * BR_C * BR_C;
+      if (!use_gemm)  // U_rho = P (C J)[:, perm] / sigma  (C J = the rotated columns in Rs)
+        for (int idx = tid; idx < BR_C * rho; idx += BR_T) {
+          const int col = idx / BR_C, j = idx % BR_C;
+          const double sg = sm.sig[col];
+          if (j < cp) tt[col * BR_C + sm.cterm[j]] = sg > 0.0 ? sm.Rs[sm.perm[col] * BR_C + j] / sg : 0.0;
+          else tt[col * BR_C + j] = 0.0;
+        }
+      // V_rho S = Q_X [J Sigma; 0] (second slot) and, for U = Y W, W = Q_X [J Sigma^-1; 0] (first)
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int col = warp; col < rho; col += BR_W) {
+        const double sg = sm.sig[col];
+        const int pc = sm.perm[col];
+        const double j0 = lane < kq ? sm.Aux[pc * BR_C + lane] : 0.0;
+        const double j1 = lane + 32 < kq ? sm.Aux[pc * BR_C + lane + 32] : 0.0;
+        double y0 = j0 * sg, y1 = j1 * sg;
+        br_apply_qx(y0, y1, qx, qx + BR_C * BR_C, kq);
+        tt[BR_C * BR_C + col * BR_C + lane] = lane < cp ? y0 : 0.0;
+        tt[BR_C * BR_C + col * BR_C + lane + 32] = lane + 32 < cp ? y1 : 0.0;
+        if (use_gemm) {
+          const double is = sg > 0.0 ? 1.0 / sg : 0.0;
+          y0 = j0 * is;
+          y1 = j1 * is;
+          br_apply_qx(y0, y1, qx, qx + BR_C * BR_C, kq);
+          tt[col * BR_C + lane] = lane < cp ? y0 : 0.0;
+          tt[col * BR_C + lane + 32] = lane + 32 < cp ? y1 : 0.0;
+        }
+      }
+      return;
+    }
+    // ambiguous decision: the full Jacobi on X decides (reload R_Y^T)
+    for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Rs[idx] = jm[(idx % BR_C) * BR_C + idx / BR_C];
+    __syncthreads();
+  }
   const long long cj0 = clock64();
   static_assert(BR_C == 64, "tail2 below assumes nc <= 64");
   const double tail2 = (A.keep_all || A.max_rank > 0) ? 0.0 : sc[1] * sc[1] / (double)(cp > 0 ? cp : 1);
@@ -1711,7 +1903,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   sh.ytstride = (std::max<int64_t>(yt, 2) + 1) & ~(int64_t)1;
   sh.zstride = (std::max<int64_t>(zmax, 2) + 1) & ~(int64_t)1;
   sh.ostride = omax;
-  const int64_t per_item = sh.vstride + sh.tstride + 2 * BR_C * BR_C + sh.ystride + sh.ytstride + 2 * sh.zstride +
+  const int64_t per_item = sh.vstride + sh.tstride + 6 * BR_C * BR_C + BR_C + sh.ystride + sh.ytstride + 2 * sh.zstride +
                            sh.ostride + 8;
   // ---------------------------------------------------------------- s(x) per item
   const bool keep_all = (o.rel_tol == 0.0);
@@ -1764,7 +1956,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   const double budget = std::min<double>(0.6 * ((double)free_b + (double)ctx->scratch_bytes), 100e9);
   const int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
   const int nb_max = std::min(W, B);
-  const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 5 * BR_C * BR_C + sh.ystride +
+  const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 6 * BR_C * BR_C + BR_C + sh.ystride +
                                               sh.ytstride + 2 * sh.zstride + std::max<int64_t>(sh.ostride, 1) + 4) +
                             (size_t)nb_max * (d + 3) + 64;
   double* ws = static_cast<double*>(ctx_scratch(ctx, ws_doubles * sizeof(double)));
@@ -1794,7 +1986,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
     for (int w0 = 0; w0 < B; w0 += W) {
       const int nb = std::min(W, B - w0);
       stamp("wave start");
-      struct { double* p; } V, T, L, YV, YT, Z, O, SC, JM, TT;
+      struct { double* p; } V, T, L, YV, YT, Z, O, SC, JM, TT, QX;
       struct { int* p; } RK, INF, GM;
       {
         double* w = ws;  // carve the scratch (every piece a multiple of 2 doubles: 16-B aligned)
@@ -1808,6 +2000,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         O.p = take((size_t)nb * std::max<int64_t>(sh.ostride, 1));
         JM.p = take((size_t)nb * BR_C * BR_C);
         TT.p = take((size_t)nb * 2 * BR_C * BR_C);
+        QX.p = take((size_t)nb * (BR_C * BR_C + BR_C));
         SC.p = take((size_t)nb * 4);
         RK.p = reinterpret_cast<int*>(take(((size_t)nb * (d + 1) + 1) / 2));
         INF.p = reinterpret_cast<int*>(take(((size_t)nb + 1) / 2));
@@ -1819,7 +2012,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       a.cores = static_cast<const double* const*>(dtab.p);
       a.coef = static_cast<const double*>(dcoef.p);
       a.scale = static_cast<const double*>(dscale.p);
-      a.V = V.p; a.T = T.p; a.L = L.p; a.YV = YV.p; a.YT = YT.p; a.Z = Z.p; a.out = O.p; a.JM = JM.p; a.TT = TT.p;
+      a.V = V.p; a.T = T.p; a.L = L.p; a.YV = YV.p; a.YT = YT.p; a.Z = Z.p; a.out = O.p; a.JM = JM.p; a.TT = TT.p; a.QX = QX.p;
       a.ranks = RK.p; a.scal = SC.p; a.info = INF.p; a.gemm = GM.p;
       a.rel_tol = o.rel_tol;
       a.floor_c = o.floor_c;
@@ -1828,6 +2021,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       {
         static const char* jt = std::getenv("TT_B200_BR_JACT");
         a.jac_t = (jt && jt[0] == '0') ? 0 : 1;
+        static const char* qs = std::getenv("TT_B200_BR_QRCP");
+        a.qrcp_svd = (qs && qs[0] == '0') ? 0 : 1;
       }
       a.item0 = w0;
       const char* dbe = std::getenv("TT_B200_BR_DEBUG");
