@@ -940,52 +940,48 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
 // used.  The big-small pairs still converge, so the small columns span the orthogonal
 // complement of the kept subspace and their squared norms sum to the exact tail mass: the rank
 // decision, U_rho and S V^T are those of the full Jacobi.
-__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail2, long long* nsweeps = nullptr) {
+// LPP lanes per column pair (8, 16 or 32: 4, 2 or 1 pairs per warp), each lane holding 64 / LPP
+// rows -- the caller picks LPP so that a round's kk / 2 pairs fill the 8 warps.
+template <int LPP>
+__device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol, double negl, double tail2,
+                                                 long long* nsweeps) {
+  constexpr int RPL = BR_C / LPP, NPW = 32 / LPP;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
-  const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
   const int kk = nc + (nc & 1);
   bool conv = nc < 2;
-  // Columns with ||c||_2 <= u ||A||_F are numerically zero: rotating them against the others
-  // only shrinks them geometrically (each projection leaves rounding residue) and the
-  // relative test never settles, so they are left alone (their sigma stays <= u ||A||_F).
-  double fro = 0.0;
-  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; fro += v * v; }
-  const double negl = block_sum(fro, sm.red) * U_ROUND * U_ROUND;
-  __syncthreads();
 #pragma unroll 1
   for (int sweep = 0; sweep < BR_JAC_SWEEPS && !conv; ++sweep) {
     if (tid == 0) sm.flag = 0;
     __syncthreads();
 #pragma unroll 1
     for (int r = 0; r < kk - 1; ++r) {
-      // 4 pairs per warp, 8 lanes per pair: lane = 8 pp + r8 holds rows 8 ((k + pp) & 7) + r8,
-      // k = 0..7 (the row-block stagger keeps the two pairs of a half-warp on different banks)
-      const int pp = lane >> 3, r8 = lane & 7;
+      // lane = LPP pp + rl holds rows LPP ((t + pp) mod RPL) + rl (the stagger keeps the pairs of
+      // a warp on different banks)
+      const int pp = lane / LPP, rl = lane % LPP;
       const int q = warp + pp * BR_W;
       int p0, p1;
       if (q == 0) { p0 = kk - 1; p1 = r; }
       else { p0 = (r + q) % (kk - 1); p1 = (r + kk - 1 - q) % (kk - 1); }
       if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
-      const bool act = q < kk / 2 && p1 < nc;
+      const bool act = q < kk / 2 && p1 < nc && pp < NPW;
       double* ca = sm.Rs + (act ? p0 : 0) * BR_C;
       double* cb = sm.Rs + (act ? p1 : 0) * BR_C;
-      double x[8], y[8];
+      double x[RPL], y[RPL];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int row = 8 * ((k + pp) & 7) + r8;
-        x[k] = act ? ca[row] : 0.0;
-        y[k] = act ? cb[row] : 0.0;
+      for (int t = 0; t < RPL; ++t) {
+        const int row = LPP * ((t + pp) % RPL) + rl;
+        x[t] = act ? ca[row] : 0.0;
+        y[t] = act ? cb[row] : 0.0;
       }
-      // pairwise (depth-3) sums: shorter dependency chains than sequential accumulation
-      double al = ((x[0] * x[0] + x[1] * x[1]) + (x[2] * x[2] + x[3] * x[3])) +
-                  ((x[4] * x[4] + x[5] * x[5]) + (x[6] * x[6] + x[7] * x[7]));
-      double be = ((y[0] * y[0] + y[1] * y[1]) + (y[2] * y[2] + y[3] * y[3])) +
-                  ((y[4] * y[4] + y[5] * y[5]) + (y[6] * y[6] + y[7] * y[7]));
-      double ga = ((x[0] * y[0] + x[1] * y[1]) + (x[2] * y[2] + x[3] * y[3])) +
-                  ((x[4] * y[4] + x[5] * y[5]) + (x[6] * y[6] + x[7] * y[7]));
+      double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
+      for (int t = 0; t < RPL; ++t) {
+        al += x[t] * x[t];
+        be += y[t] * y[t];
+        ga += x[t] * y[t];
+      }
+#pragma unroll
+      for (int o = LPP / 2; o > 0; o >>= 1) {
         al += __shfl_xor_sync(0xffffffffu, al, o);
         be += __shfl_xor_sync(0xffffffffu, be, o);
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
@@ -993,18 +989,16 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
       const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tail2 || be > tail2) &&
                        fabs(ga) > tol * sqrt(al * be);
       if (rot) {
-        // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga), with one
-        // division: t = 2 ga sign(be - al) / (|be - al| + sqrt((be - al)^2 + 4 ga^2))
         const double dd = be - al;
         const double t = (dd >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(dd) + sqrt(dd * dd + 4.0 * ga * ga));
         const double cs = rsqrt(1.0 + t * t), sn = cs * t;
         double* va = sm.Aux + p0 * BR_C;
         double* vbp = sm.Aux + p1 * BR_C;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int row = 8 * ((k + pp) & 7) + r8;
-          ca[row] = cs * x[k] - sn * y[k];
-          cb[row] = sn * x[k] + cs * y[k];
+        for (int u = 0; u < RPL; ++u) {
+          const int row = LPP * ((u + pp) % RPL) + rl;
+          ca[row] = cs * x[u] - sn * y[u];
+          cb[row] = sn * x[u] + cs * y[u];
           const double a0 = va[row], b0 = vbp[row];
           va[row] = cs * a0 - sn * b0;
           vbp[row] = sn * a0 + cs * b0;
@@ -1017,6 +1011,25 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
     if (nsweeps && tid == 0) *nsweeps += 1;
     __syncthreads();
   }
+  return conv;
+}
+
+__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail2, long long* nsweeps = nullptr) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
+  const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
+  // Columns with ||c||_2 <= u ||A||_F are numerically zero: rotating them against the others
+  // only shrinks them geometrically (each projection leaves rounding residue) and the
+  // relative test never settles, so they are left alone (their sigma stays <= u ||A||_F).
+  double fro = 0.0;
+  for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; fro += v * v; }
+  const double negl = block_sum(fro, sm.red) * U_ROUND * U_ROUND;
+  __syncthreads();
+  const int pairs = (nc + (nc & 1)) / 2;
+  bool conv;
+  if (pairs <= BR_W) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, nsweeps);
+  else if (pairs <= 2 * BR_W) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, nsweeps);
+  else conv = br_jacobi_rounds<8>(sm, nc, tol, negl, tail2, nsweeps);
   // singular values = column norms, sorted descending (ties: lower column first)
   for (int j = warp; j < nc; j += BR_W) {
     const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];

@@ -109,19 +109,21 @@ __device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) 
   // W = R[8jb + i][8w + c] + sum_rows V[row][8jb + i] A[row][8w + c]   (C fragment: i = r8, c = 2 q4 + e)
   double c0 = st[(8 * w + 2 * q4) * LD + 8 * jb + r8];
   double c1 = st[(8 * w + 2 * q4 + 1) * LD + 8 * jb + r8];
-  double e0 = 0.0, e1 = 0.0;
+  double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;  // four independent chains
   const double* vp = st + (8 * jb + r8) * LD + RR + q4;  // V^T fragment: V[4kk + q4][8jb + r8]
   const double* ap = st + (8 * w + r8) * LD + RR + q4;   // A fragment:   A[4kk + q4][8w + r8]
   const int nk = (crow + 3) >> 2;
   int kk = 0;
-#pragma unroll 4
-  for (; kk + 1 < nk; kk += 2) {
+#pragma unroll 2
+  for (; kk + 3 < nk; kk += 4) {
     dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
     dmma(e0, e1, vp[4 * kk + 4], ap[4 * kk + 4]);
+    dmma(f0, f1, vp[4 * kk + 8], ap[4 * kk + 8]);
+    dmma(g0, g1, vp[4 * kk + 12], ap[4 * kk + 12]);
   }
-  if (kk < nk) dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
-  c0 += e0;
-  c1 += e1;
+  for (; kk < nk; ++kk) dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
+  c0 += e0 + (f0 + g0);
+  c1 += e1 + (f1 + g1);
   // W' = T^T W (through the warp scratch: C fragment -> B fragment)
   double* ws = sm.ws[w];
   ws[r8 * 8 + 2 * q4] = c0;
@@ -140,7 +142,7 @@ __device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) 
   const double b0 = ws[q4 * 8 + r8], b1 = ws[(4 + q4) * 8 + r8];  // W' as B fragments (k = i)
   // A_w[chunk] -= V W'   (A fragment: -V[8mt + r8][8jb + q4 (+4)])
   const int nm = (crow + 7) >> 3;
-#pragma unroll 2
+#pragma unroll 4
   for (int mt = 0; mt < nm; ++mt) {
     double* cp = st + (8 * w + 2 * q4) * LD + RR + 8 * mt + r8;
     double x0 = cp[0], x1 = cp[LD];
@@ -394,7 +396,7 @@ struct ASmem {
   double Vs[2][NB * VLD];        // staged V block (column-major), double-buffered
   double Ts[2][64];
   double Wp[W][8 * 12];          // partial W tiles (8 x 8, row stride 12) per (column tile, k-split)
-  double Wf[8 * WLD];            // W' = T W
+  double Wf[W * 64];             // per-warp 8 x 8 scratch: W' = T W as B fragments
   uint64_t bar[2];
 };
 
@@ -441,7 +443,8 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ s
 #pragma unroll 1
   for (int t0 = 0; t0 < nt; t0 += AN) {
     const int ntp = min(AN, nt - t0), ntl = (ntp + 7) >> 3;
-    const int ksp = ntl == 1 ? 8 : ntl == 2 ? 4 : 2;  // k-splits of the W phase (ntl * ksp <= 8 units)
+    const int ntl4 = ntl == 3 ? 4 : ntl;               // a divisor of 8: each warp keeps one tile
+    const int ksp = 8 / ntl4;                          // k-splits of the W phase
     __syncthreads();
     for (int idx = tid; idx < AN * RR; idx += T) {
       const int c = idx / RR, r = idx % RR;
@@ -478,11 +481,16 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ s
               const double* vp = Vs + r8 * VLD + q4;
               const double* cp = sm.Ct + (8 * nti + r8) * ALD + q4;
               int kk = k0;
-              for (; kk + 1 < k1; kk += 2) {
+              double f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
+              for (; kk + 3 < k1; kk += 4) {
                 dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
                 dmma(e0, e1, vp[4 * kk + 4], cp[4 * kk + 4]);
+                dmma(f0, f1, vp[4 * kk + 8], cp[4 * kk + 8]);
+                dmma(g0, g1, vp[4 * kk + 12], cp[4 * kk + 12]);
               }
-              if (kk < k1) dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
+              for (; kk < k1; ++kk) dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
+              e0 += f0 + g0;
+              e1 += f1 + g1;
             }
             double* wp = sm.Wp[w];
             wp[r8 * 12 + 2 * q4] = c0 + e0;
@@ -490,32 +498,39 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ s
           }
         }
         __syncthreads();
-        // ---- W' = T W, R-block rows -= W'
-        if (w < ntl) {
-          double b0 = 0.0, b1 = 0.0;
-          for (int ks = 0; ks < ksp; ++ks) {
-            b0 += sm.Wp[w * ksp + ks][q4 * 12 + r8];
-            b1 += sm.Wp[w * ksp + ks][(4 + q4) * 12 + r8];
+        // ---- per warp: W' = T W of its column tile (nti = w mod ntl4: the same for every unit of
+        // this warp), R-block rows -= W' (one warp per tile), then C -= V W' over its units
+        {
+          const int nti = w % ntl4;
+          if (nti < ntl) {
+            double b0 = 0.0, b1 = 0.0;
+            for (int ks = 0; ks < ksp; ++ks) {
+              b0 += sm.Wp[nti * ksp + ks][q4 * 12 + r8];
+              b1 += sm.Wp[nti * ksp + ks][(4 + q4) * 12 + r8];
+            }
+            const double* Tj = sm.Ts[b];
+            double d0 = 0.0, d1 = 0.0;
+            dmma(d0, d1, Tj[r8 * 8 + q4], b0);
+            dmma(d0, d1, Tj[r8 * 8 + 4 + q4], b1);
+            if (w == nti) {
+              sm.Rt[(8 * nti + 2 * q4) * RLD + 8 * jb + r8] -= d0;
+              sm.Rt[(8 * nti + 2 * q4 + 1) * RLD + 8 * jb + r8] -= d1;
+            }
+            double* ws = sm.Wf + w * 64;  // warp-private C -> B fragment exchange
+            ws[r8 * 8 + 2 * q4] = d0;
+            ws[r8 * 8 + 2 * q4 + 1] = d1;
+            __syncwarp();
+            const double f0 = ws[q4 * 8 + r8], f1 = ws[(4 + q4) * 8 + r8];
+            for (int u = w; u < nm * ntl4; u += W) {
+              const int mt = u / ntl4;
+              double* cp = sm.Ct + (8 * nti + 2 * q4) * ALD + 8 * mt + r8;
+              double x0 = cp[0], x1 = cp[ALD];
+              dmma(x0, x1, -Vs[q4 * VLD + 8 * mt + r8], f0);
+              dmma(x0, x1, -Vs[(4 + q4) * VLD + 8 * mt + r8], f1);
+              cp[0] = x0;
+              cp[ALD] = x1;
+            }
           }
-          const double* Tj = sm.Ts[b];
-          double d0 = 0.0, d1 = 0.0;
-          dmma(d0, d1, Tj[r8 * 8 + q4], b0);
-          dmma(d0, d1, Tj[r8 * 8 + 4 + q4], b1);
-          sm.Wf[r8 * WLD + 8 * w + 2 * q4] = d0;
-          sm.Wf[r8 * WLD + 8 * w + 2 * q4 + 1] = d1;
-          sm.Rt[(8 * w + 2 * q4) * RLD + 8 * jb + r8] -= d0;
-          sm.Rt[(8 * w + 2 * q4 + 1) * RLD + 8 * jb + r8] -= d1;
-        }
-        __syncthreads();
-        // ---- Ct -= V W'
-        for (int u = w; u < nm * ntl; u += W) {
-          const int mt = u / ntl, nti = u % ntl;
-          double* cp = sm.Ct + (8 * nti + 2 * q4) * ALD + 8 * mt + r8;
-          double x0 = cp[0], x1 = cp[ALD];
-          dmma(x0, x1, -Vs[q4 * VLD + 8 * mt + r8], sm.Wf[q4 * WLD + 8 * nti + r8]);
-          dmma(x0, x1, -Vs[(4 + q4) * VLD + 8 * mt + r8], sm.Wf[(4 + q4) * WLD + 8 * nti + r8]);
-          cp[0] = x0;
-          cp[ALD] = x1;
         }
         __syncthreads();
       }
