@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
   PanelElem e{A.cores + (int64_t)gb * K * d, S, sm.Aux, &sm.xst[0][0], sm.cterm, sm.ca, kc, d, n, Rpk, last ? 1 : 0};
   double* V = A.V + (int64_t)b * S->vstride + S->voff[kc];
   double* Tq = A.T + (int64_t)b * S->tstride + S->toff[kc];
-  br_qr(e, m, c, sm, V, Tq, (A.dbg && blockIdx.x == 0) ? A.dbg : nullptr);
+  br_qr(e, m, c, sm, V, Tq, (A.dbg && blockIdx.x == 0) ? A.dbg + 32 : nullptr);
   // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
   double* Lout = A.L + (int64_t)b * 2 * BR_C * BR_C + (k & 1) * BR_C * BR_C;
   const int rows = S->Rp[k - 1];
@@ -1634,7 +1634,8 @@ __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
     }
     return;
   }
-  wy::factor_panel(sm, ld, c, A.V + (int64_t)b * S->vstride + S->voff[kc]);
+  wy::factor_panel(sm, ld, c, A.V + (int64_t)b * S->vstride + S->voff[kc],
+                   (A.dbg && blockIdx.x == 0) ? A.dbg + 32 : nullptr);
   // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
   for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
     const int row = idx / BR_C, col = idx % BR_C;
@@ -2041,8 +2042,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       const char* dbe = std::getenv("TT_B200_BR_DEBUG");
       LBuf dbg;
       if (dbe && dbe[0] == '1') {
-        dbg.alloc(ctx, 32);
-        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 32 * sizeof(long long), ctx->stream));
+        dbg.alloc(ctx, 64);
+        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 64 * sizeof(long long), ctx->stream));
       }
       a.dbg = dbg.p;
       for (int kc = d - 1; kc >= 1; --kc) {
@@ -2081,11 +2082,19 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
           TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
       }
       if (dbg.p) {
-        long long h[32];
+        long long h[64];
         TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (use_wy) {
+          std::fprintf(stderr, "[br_debug] WY r2l, CTA 0, per warp (wait / update / factor / store+release+load, Mcycles):");
+          for (int w = 0; w < 8; ++w)
+            std::fprintf(stderr, " w%d %.2f/%.2f/%.2f/%.2f", w, 1e-6 * h[32 + 4 * w], 1e-6 * h[33 + 4 * w],
+                         1e-6 * h[34 + 4 * w], 1e-6 * h[35 + 4 * w]);
+          std::fprintf(stderr, "\n");
+        } else {
         std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld (%lld sweeps) outcore %lld nextcore %lld (cycles, CTA 0) | qr steps: owner(w0) %lld x%lld, pre-barrier(w0 not owner) %lld, barrier %lld, update %lld\n",
                      h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[11], h[9], h[10], h[16], h[19], h[20], h[17], h[18]);
+        }
       }
       // ranks (the one host synchronisation of the wave), then compaction
       std::vector<int> hr((size_t)nb * (d + 1)), hinf((size_t)nb);

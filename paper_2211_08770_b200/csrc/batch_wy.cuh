@@ -324,7 +324,8 @@ __device__ __forceinline__ void zero_chunk(Smem& sm) {
 //   L.stacks(), L.crow(q) (rows of stack q), L.load(sm, q, w) (warp w fills rows 64.. of its
 //   columns for stack q, rows >= crow zero; warp-synchronous), out + q * stack_doubles(ncol).
 template <class Loader>
-__device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __restrict__ out) {
+__device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __restrict__ out,
+                             long long* __restrict__ prof = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int nact = (ncol + NB - 1) / NB;  // active column blocks (all factored: nrefl = ncol)
   const int S = L.stacks();
@@ -337,7 +338,11 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   if (w < nact) {
+    // prof (debugging, CTA 0): per warp cycles waiting for blocks, applying them, factoring, and
+    // storing + waiting for the release + loading the next stack
+    long long t0 = prof ? clock64() : 0, tw = 0, tu = 0, tf = 0, tl = 0;
     L.load(sm, 0, w);
+    if (prof) { tl += clock64() - t0; t0 = clock64(); }
 #pragma unroll 1
     for (int q = 0; q < S; ++q) {
       const int crow = L.crow(q);
@@ -345,11 +350,14 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
 #pragma unroll 1
       for (int jb = 0; jb < w; ++jb) {
         bar_wait(&sm.ready[jb], par);
+        if (prof) { const long long t = clock64(); tw += t - t0; t0 = t; }
         update_block(sm, jb, w, crow);
         bar_arrive(&sm.used[jb]);
+        if (prof) { const long long t = clock64(); tu += t - t0; t0 = t; }
       }
       factor_block(sm, w, min(NB, ncol - NB * w), crow);
       bar_arrive(&sm.ready[w]);
+      if (prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
       // V (CH x 8 of this block, column-major ld CH) and T_w
       double* o = out + (int64_t)q * sd;
       const int nc = min(NB, ncol - NB * w);
@@ -365,6 +373,13 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
         __syncwarp();
         L.load(sm, q + 1, w);
       }
+      if (prof) { const long long t = clock64(); tl += t - t0; t0 = t; }
+    }
+    if (prof && lane == 0) {
+      prof[4 * w + 0] += tw;
+      prof[4 * w + 1] += tu;
+      prof[4 * w + 2] += tf;
+      prof[4 * w + 3] += tl;
     }
   }
   __syncthreads();
