@@ -1753,7 +1753,7 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_apply_wy_kernel(BRArgs A, int
   const double* sc = A.scal + (int64_t)b * 4;
   if (sc[3] != 0.0) return;
   wy::apply_init(sm);
-  uint32_t ph[2] = {0u, 0u};
+  uint32_t ph[wy::NBUF] = {};
   double* out = A.out + (int64_t)b * S->ostride;
   const int n = S->n[kc], cp = S->Rp[k];
   const int64_t p = (k == 1) ? (int64_t)n : (int64_t)rk[k - 1] * n;

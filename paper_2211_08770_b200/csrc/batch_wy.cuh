@@ -157,19 +157,23 @@ __device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) 
 }
 
 // Warp w factors its column block (reflectors j = 8w + jj, jj < nr), forms T_w, stores V into
-// the chunk rows of its columns; taus on the diagonal of T.
+// the chunk rows of its columns; taus on the diagonal of T.  T is built column by column as the
+// reflectors appear (T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) V(:, 0:jj)^T v_jj, lane r keeping row r):
+// the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots v_jj^T a_c (c > jj).
 __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) {
-  const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
+  const int lane = threadIdx.x & 31;
   double* st = sm.st;
+  (void)crow;
   double x[4][NB];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
 #pragma unroll
     for (int c = 0; c < NB; ++c) x[t][c] = st[(8 * w + c) * LD + RR + 32 * t + lane];  // rows >= crow are 0
-  double tau[NB];
+  double trow[NB];  // row `lane` of T (lanes 0..7)
+#pragma unroll
+  for (int c = 0; c < NB; ++c) trow[c] = 0.0;
 #pragma unroll
   for (int jj = 0; jj < NB; ++jj) {
-    tau[jj] = 0.0;
     if (jj < nr) {
       const int j = 8 * w + jj;
       double ss = 0.0;
@@ -186,22 +190,28 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
         tj = -am * am * inv;
         scal = beta * inv;
       }
-      tau[jj] = tj;
 #pragma unroll
       for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
       if (tj != 0.0) {
         double dt[NB], rj[NB];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) {  // R row j of the block's later columns: independent loads
+        for (int c = 0; c < NB; ++c) {  // c > jj: v_jj^T a_c (update); c < jj: v_c^T v_jj (for T)
           rj[c] = c > jj ? st[(8 * w + c) * LD + j] : 0.0;
           double q = 0.0;
-          if (c > jj) {
+          if (c != jj) {
 #pragma unroll
             for (int t = 0; t < 4; ++t) q += x[t][jj] * x[t][c];
           }
           dt[c] = q;
         }
         warp_sum8v(dt);
+        {  // T(lane, jj) for lane < jj, T(jj, jj) = tau
+          double tv = 0.0;
+#pragma unroll
+          for (int q = 0; q < NB; ++q)
+            if (q < jj && q >= lane) tv += trow[q] * dt[q];
+          trow[jj] = lane < jj ? -tj * tv : (lane == jj ? tj : 0.0);
+        }
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
           if (c > jj) {
@@ -227,37 +237,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
   for (int t = 0; t < 4; ++t)
 #pragma unroll
     for (int c = 0; c < NB; ++c) st[(8 * w + c) * LD + RR + 32 * t + lane] = x[t][c];
-  __syncwarp();
-  // G = V^T V over the chunk rows (DMMA), then T: T(i,i) = tau_i, T(0:i, i) = -tau_i T(0:i,0:i) G(0:i, i)
-  double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
-  const double* vp = st + (8 * w + r8) * LD + RR + q4;
-  const int nk = (crow + 3) >> 2;
-  int kk = 0;
-  for (; kk + 1 < nk; kk += 2) {
-    const double a = vp[4 * kk], b = vp[4 * kk + 4];
-    dmma(g0, g1, a, a);
-    dmma(h0, h1, b, b);
-  }
-  if (kk < nk) { const double a = vp[4 * kk]; dmma(g0, g1, a, a); }
-  double* ws = sm.ws[w];
-  ws[r8 * 8 + 2 * q4] = g0 + h0;
-  ws[r8 * 8 + 2 * q4 + 1] = g1 + h1;
-  __syncwarp();
-  if (lane < NB) {  // lane r builds row r of T
-    double trow[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      double v = 0.0;
-      if (lane == i) v = tau[i];
-      else if (lane < i) {
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < NB; ++q)
-          if (q >= lane && q < i) s += trow[q] * ws[q * 8 + i];
-        v = -tau[i] * s;
-      }
-      trow[i] = v;
-    }
+  if (lane < NB) {
 #pragma unroll
     for (int i = 0; i < NB; ++i) sm.Tm[w][lane * 8 + i] = trow[i];
   }
@@ -405,14 +385,15 @@ constexpr int ALD = CH + 4;      // ld of the chunk target (132 = 4 mod 16)
 constexpr int RLD = RR;          // ld of the R-block target (few accesses: no padding)
 constexpr int VLD = CH + 4;      // ld of a staged V block
 constexpr int WLD = AN + 4;      // row stride of W (8 x AN)
+constexpr int NBUF = 2;          // staging ring depth (4 measured no faster on C4: the blocks are L2-resident)
 struct ASmem {
   double Ct[AN * ALD];           // chunk rows of the target (column-major)
   double Rt[AN * RLD];           // R-block rows of the target (column-major)
-  double Vs[2][NB * VLD];        // staged V block (column-major), double-buffered
-  double Ts[2][64];
+  double Vs[NBUF][NB * VLD];     // staged V blocks (column-major), a ring NBUF deep
+  double Ts[NBUF][64];
   double Wp[W][8 * 12];          // partial W tiles (8 x 8, row stride 12) per (column tile, k-split)
   double Wf[W * 64];             // per-warp 8 x 8 scratch: W' = T W as B fragments
-  uint64_t bar[2];
+  uint64_t bar[NBUF];
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -426,10 +407,9 @@ __device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
 }
 
 __device__ __forceinline__ void apply_init(ASmem& sm) {
-  for (int idx = threadIdx.x; idx < 2 * NB * VLD; idx += T) (&sm.Vs[0][0])[idx] = 0.0;  // never-staged columns
+  for (int idx = threadIdx.x; idx < NBUF * NB * VLD; idx += T) (&sm.Vs[0][0])[idx] = 0.0;  // never-staged columns
   if (threadIdx.x == 0) {
-    bar_init(&sm.bar[0], 1);
-    bar_init(&sm.bar[1], 1);
+    for (int b = 0; b < NBUF; ++b) bar_init(&sm.bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -448,7 +428,7 @@ __device__ __forceinline__ void stage_block(ASmem& sm, const double* F, int ncol
 // out[row * rs + col * cs] = (Q [X; 0])[row][col] for the m panel rows, X = src (ncx x nt,
 // column-major ld 64, global).  Stack q holds panel rows [q cr, min(m, (q+1) cr)), factor at
 // F + q * stack_doubles(ncol).  ph[]: the staging barriers' phase bits (kept across calls).
-__device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ src, int ncx, int nt,
+__device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict__ src, int ncx, int nt,
                       const double* __restrict__ F0, int64_t m, int cr, int ncol, int nrefl, double* __restrict__ out,
                       int64_t rs, int64_t cs) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q4 = lane & 3, r8 = lane >> 2;
@@ -473,11 +453,18 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[2], const double* __restrict__ s
       const int nk = (crow + 3) >> 2, nm = (crow + 7) >> 3;
       for (int idx = tid; idx < AN * CH; idx += T) sm.Ct[(idx / CH) * ALD + idx % CH] = 0.0;
       __syncthreads();
-      int b = 0;
-      if (tid == 0) stage_block(sm, F, ncol, nbr - 1, 0);
 #pragma unroll 1
-      for (int jb = nbr - 1; jb >= 0; --jb, b ^= 1) {
-        if (jb > 0 && tid == 0) stage_block(sm, F, ncol, jb - 1, b ^ 1);
+      for (int jb = nbr - 1; jb >= 0; --jb) {
+        // block sequence index over the whole pass (stacks descending, blocks descending): the
+        // ring is filled NBUF - 1 blocks ahead, across stack boundaries
+        const int tq = (S - 1 - q) * nbr + (nbr - 1 - jb), tot = S * nbr;
+        if (tid == 0) {
+          for (int u = (tq == 0 ? 0 : tq + NBUF - 1); u <= tq + NBUF - 1 && u < tot; ++u) {
+            const int uq = S - 1 - u / nbr, ujb = nbr - 1 - u % nbr;
+            stage_block(sm, F0 + (int64_t)uq * sd, ncol, ujb, u % NBUF);
+          }
+        }
+        const int b = tq % NBUF;
         bar_wait(&sm.bar[b], ph[b]);
         ph[b] ^= 1u;
         const double* Vs = sm.Vs[b];

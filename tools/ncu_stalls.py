@@ -56,7 +56,7 @@ if __name__ == "__main__":
         print(f"{kk}: {vv}")
     r = raw(rep, ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                   "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-                  "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "SM_C.TriageCompute.smsp__pipe_tensor_subpipe_dmma_cycles_active.avg", "sm__cycles_elapsed.avg",
                   "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__warps_issue_stalled_barrier_per_warp_active.pct"])
     for kk, vv in r.items():
         print(f"{kk}: {vv}")

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(wy::T, 1) apply_kernel(const double* X, int nc
   extern __shared__ __align__(16) unsigned char raw[];
   wy::ASmem& sm = *reinterpret_cast<wy::ASmem*>(raw);
   wy::apply_init(sm);
-  uint32_t ph[2] = {0u, 0u};
+  uint32_t ph[wy::NBUF] = {};
   wy::apply(sm, ph, X, ncx, nt, F, m, cr, c, (int)(m < c ? m : c), out, nt, 1);
 }
 
