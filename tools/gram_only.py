@@ -23,7 +23,11 @@ def main():
         G = P.tt_gram(ctx, A)
     e1.record()
     torch.cuda.synchronize()
-    print(f"gram {e0.elapsed_time(e1) / 3:.3f} ms")
+    import numpy as np
+    Gx = st.gram_exact()
+    err = float(np.linalg.norm(G.cpu().numpy() - Gx) / np.linalg.norm(Gx))
+    print(f"gram {e0.elapsed_time(e1) / 3:.3f} ms  rel err vs M^T M {err:.2e}  "
+          f"(v1={os.environ.get('TT_B200_GRAM_V1', '0')}, CS={os.environ.get('TT_B200_GRAM_CS', 'auto')})")
 
 
 if __name__ == "__main__":
