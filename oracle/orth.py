@@ -25,7 +25,7 @@ import numpy as np
 
 from .dense import cholesky, invert_upper, loo
 from .rounding import DEFAULT_FLOOR_C, RoundInfo, tt_round_sum
-from .tt import TT, canonical_tt, element, modes, phi, tt_dot, tt_norm, tt_scale, tt_sum
+from .tt import TT, canonical_tt, element, mask_geq, modes, phi, tt_dot, tt_hadamard, tt_norm, tt_scale, tt_sum
 
 
 class NumericalDefect(Exception):
@@ -329,11 +329,15 @@ def householder_literal(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_
 
 
 def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLOOR_C,
-                     hh_beta: str = "round_norm") -> OrthResult:
+                     hh_beta: str = "round_norm", hh_mask: bool = False) -> OrthResult:
     """Alg. 8 with a~_j = a_j - sum_l gamma_{jl} u_l kept as coefficients:
     gamma_{jl} = 2(<a_j,u_l> - sum_{p<l} gamma_{jp} <u_p,u_l>), and
     q_i = e_i - sum_{j<=i} beta_{ij} u_j with beta_{ij} = 2(<e_i,u_j> - sum_{j<l<=i} beta_{il}<u_l,u_j>)
-    (SURVEY.md §8(c) C3).  <x, e_j> is the element x(phi(j))."""
+    (SURVEY.md §8(c) C3).  <x, e_j> is the element x(phi(j)).
+    hh_mask (a DEPARTURE from Alg. 6's listing): the first TTH-vec rounding
+    takes w with its entries at phi(1..i-1) set to zero exactly -- the Hadamard product with
+    the rank-2 mask of the canonical indices >= i (mask_geq) -- instead of the TT-sum
+    w - sum_{j<i} r(j) e_j, which equals it in exact arithmetic but cancels in floating point."""
     m = len(A)
     n = modes(A[0])
     a_norms = [tt_norm(a) for a in A]
@@ -350,9 +354,14 @@ def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLO
         r = np.zeros(i)
         r[:i - 1] = ew[:i - 1]
         s = float(np.sum(r[:i - 1] ** 2))
-        terms = [w] + [canonical_tt(j, n) for j in range(1, i)]
-        coefs = [1.0] + list(-r[:i - 1])
-        tn1 = [w_norm] + [1.0] * (i - 1)
+        if hh_mask and i > 1:
+            terms = [tt_hadamard(w, mask_geq(n, i - 1))]
+            coefs = [1.0]
+            tn1 = [tt_norm(terms[0])]
+        else:
+            terms = [w] + [canonical_tt(j, n) for j in range(1, i)]
+            coefs = [1.0] + list(-r[:i - 1])
+            tn1 = [w_norm] + [1.0] * (i - 1)
         w1, info1 = tt_round_sum(terms, coefs, delta, floor_c=floor_c, term_norms=tn1)
         _record(res, terms, coefs, tn1, w1, info1)
         sg = _sign(ew[i - 1])
@@ -407,12 +416,14 @@ def householder_lazy(A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLO
 # dispatcher
 # ========================================================================================
 def orth(kind: str, A: Sequence[TT], delta: float, floor_c: float = DEFAULT_FLOOR_C,
-         literal: bool = False, hh_beta: str = "round_norm") -> OrthResult:
+         literal: bool = False, hh_beta: str = "round_norm", hh_mask: bool = False) -> OrthResult:
     kind = kind.lower()
     if kind in ("cgs", "mgs", "cgs2", "mgs2"):
         return (gs_literal if literal else gs_lazy)(A, delta, kind, floor_c)
     if kind == "gram":
         return gram_orth(A, delta, floor_c, literal=literal)
     if kind in ("householder", "hh"):
+        if hh_mask:
+            return householder_lazy(A, delta, floor_c, hh_beta, hh_mask=True)
         return (householder_literal if literal else householder_lazy)(A, delta, floor_c, hh_beta)
     raise ValueError(kind)

@@ -179,3 +179,56 @@ def compression_gain(before: TT, after: TT) -> float:
     if modes(before) != modes(after):
         raise ValueError("shape mismatch")
     return storage_count(before) / float(storage_count(after))
+
+
+def tt_hadamard(x: TT, y: TT) -> TT:
+    """Elementwise product z(i) = x(i) y(i): core k is the Kronecker product of the slices,
+    Z_k(i) = X_k(i) (x) Y_k(i), ranks multiply (SPEC.md:177-185 Hadamard; used only by the
+    TTH-vec masking variant)."""
+    if modes(x) != modes(y):
+        raise ValueError("shape mismatch in TT-Hadamard")
+    out = []
+    for X, Y in zip(x, y):
+        a0, n, a1 = X.shape
+        b0, _, b1 = Y.shape
+        Z = np.einsum("aib,cid->acibd", X, Y).reshape(a0 * b0, n, a1 * b1)
+        out.append(np.ascontiguousarray(Z))
+    return out
+
+
+def mask_geq(n: Sequence[int], L: int) -> TT:
+    """Indicator of the canonical indices j >= L + 1, i.e. of the multi-indices whose psi-order
+    linear index (mode 1 fastest) is >= L, as a TT of ranks <= 2: a comparison of the
+    mixed-radix digits from the most significant (mode d) down, state 0 = equal so far, 1 =
+    already greater; core k maps the state before digit k (right index) to the state after it
+    (left index); core 1 accepts states 'equal' (digit >= l_1) and 'greater'.  L = 0 gives ones."""
+    d = len(n)
+    digits, rem = [], int(L)
+    for k in range(d):
+        digits.append(rem % n[k])
+        rem //= n[k]
+    if rem:
+        raise ValueError("L beyond prod(n)")
+    cores = []
+    for k in range(d):
+        lk = digits[k]
+        left = 1 if k == 0 else 2
+        right = 1 if k == d - 1 else 2
+        C = np.zeros((left, n[k], right))
+        for s_in in range(right):          # state from the digits above k (mode d: start 'equal')
+            state_in = 0 if k == d - 1 else s_in
+            for x in range(n[k]):
+                if state_in == 1:
+                    s_out = 1
+                elif x > lk:
+                    s_out = 1
+                elif x == lk:
+                    s_out = 0
+                else:
+                    continue               # smaller at the first differing digit: rejected
+                if k == 0:
+                    C[0, x, s_in] = 1.0    # accept 'equal' (lin == L) and 'greater'
+                else:
+                    C[s_out, x, s_in] = 1.0
+        cores.append(C)
+    return cores

@@ -261,3 +261,64 @@ def test_literal_beta_cancels_at_high_kappa_reading_a9():
         err[hb] = np.max(np.abs(np.diag(R) - np.diag(rm)) / np.abs(np.diag(rm)))
     assert err["round_norm"] <= 1e-4
     assert err["literal"] >= 1e-4 and err["literal"] >= 10 * err["round_norm"]
+
+
+# ---------------------------------------------------------------- TTH-vec masking variant (§8(f) 3)
+def test_mask_geq_brute_force():
+    """mask_geq(n, L) densified is the indicator of psi-order linear index >= L,
+    for every L on small mixed-radix shapes (brute force over all multi-indices)."""
+    from oracle.tt import densify, mask_geq, psi
+    import itertools
+    for n in ([3], [2, 3], [3, 2, 4], [2, 2, 2, 3]):
+        total = int(np.prod(n))
+        for L in range(total + 1 if total < 30 else 30):
+            if L == total:
+                continue
+            D = densify(mask_geq(n, L))  # psi order: entry lin = psi(i) - 1
+            for idx in itertools.product(*[range(v) for v in n]):
+                lin = psi([i + 1 for i in idx], n) - 1
+                assert D[lin] == (1.0 if lin >= L else 0.0), (n, L, idx)
+            ranks = [c.shape[0] for c in mask_geq(n, L)] + [1]
+            assert max(ranks) <= 2
+
+
+def test_hadamard_dense():
+    from oracle.tt import densify, tt_hadamard
+    rng = np.random.Generator(np.random.PCG64(71))
+    n = [3, 4, 2]
+    x = [rng.standard_normal((1, 3, 2)), rng.standard_normal((2, 4, 3)), rng.standard_normal((3, 2, 1))]
+    y = [rng.standard_normal((1, 3, 3)), rng.standard_normal((3, 4, 2)), rng.standard_normal((2, 2, 1))]
+    z = tt_hadamard(x, y)
+    assert np.allclose(densify(z), densify(x) * densify(y), rtol=1e-13, atol=1e-13)
+    assert [c.shape[2] for c in z] == [6, 6, 1]
+
+
+def test_masked_first_rounding_input_equals_subtraction():
+    """w (x) mask_geq(n, i-1) equals w - sum_{j<i} w(phi(j)) e_j (Alg. 6 lines 4-9) entry by entry
+    on a densified tensor; the masked form has no cancellation: the zeroed entries are exactly 0."""
+    from oracle.tt import canonical_tt, densify, element, mask_geq, phi, tt_hadamard, tt_sum
+    from ttinputs import make_random_tt
+    rng = np.random.Generator(np.random.PCG64(72))
+    n = [4, 3, 3]
+    w = make_random_tt(3, n, [1, 3, 2, 1], rng)
+    for i in (1, 2, 5, 13, 36):
+        masked = densify(tt_hadamard(w, mask_geq(n, i - 1)))
+        terms = [w] + [canonical_tt(j, n) for j in range(1, i)]
+        coefs = [1.0] + [-element(w, [t - 1 for t in phi(j, n)]) for j in range(1, i)]
+        sub = densify(tt_sum(terms, coefs))
+        assert np.max(np.abs(masked - sub)) <= 1e-14 * np.max(np.abs(densify(w)))
+        for j in range(1, i):
+            assert masked[j - 1] == 0.0  # densify is in psi order: entry j - 1 is phi(j)
+
+
+def test_householder_masked_closed_form():
+    """The masked variant (hh_mask) keeps Alg. 8's Table 1 count (4m-1) and the shared-tail
+    closed form R = R_M (up to the signs D) on a well-conditioned set."""
+    from oracle import orth
+    st = make_shared_tail_set(4, 6, 3, 8, 1e2, seed=991)
+    res = orth.orth("householder", st.tensors, 1e-12, hh_mask=True)
+    assert res.rounding_calls == 4 * 8 - 1
+    rm = st.qr_exact()[1]
+    sg = np.sign(np.diag(res.R))
+    sg[sg == 0] = 1
+    assert np.linalg.norm(sg[:, None] * res.R - rm) <= 1e-10 * np.linalg.norm(rm)
