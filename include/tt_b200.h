@@ -107,6 +107,10 @@ typedef struct {
   int32_t hh_beta_literal;  /* 0: R(i,i) = sign * ||round(w - sum_{j<i} r_j e_j)||;
                                1: literal sqrt(||w||^2 - s) of Alg. 6 line 10 */
   int32_t want_loo;         /* fill report->loo_per_step (costs the Q Gram) */
+  int32_t hh_mask;          /* Householder only, a DEPARTURE from Alg. 6 lines 4-9:
+                               the first TTH-vec rounding takes w with its entries phi(1..i-1) zeroed
+                               exactly (Hadamard product with a rank-2 comparison mask) instead of
+                               the cancelling TT-sum w - sum_{j<i} r(j) e_j.  0 = Alg. 6 as listed. */
 } tt_orth_opts;
 
 typedef struct {

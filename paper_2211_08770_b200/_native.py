@@ -56,7 +56,8 @@ class RoundInfo(C.Structure):
 
 
 class OrthOpts(C.Structure):
-    _fields_ = [("round", RoundOpts), ("hh_beta_literal", C.c_int32), ("want_loo", C.c_int32)]
+    _fields_ = [("round", RoundOpts), ("hh_beta_literal", C.c_int32), ("want_loo", C.c_int32),
+                ("hh_mask", C.c_int32)]
 
 
 class OrthReport(C.Structure):

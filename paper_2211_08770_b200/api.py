@@ -522,10 +522,11 @@ class RoundTrace:
 
 def tt_orth(ctx: Context, kind: str, tensors, rel_tol: float, floor_c: float = DEFAULT_FLOOR_C,
             theta: float = 0.5, hh_beta_literal: bool = False, want_loo: bool = False,
-            keep_u: bool = False, rank_revealing: bool = True):
+            keep_u: bool = False, rank_revealing: bool = True, hh_mask: bool = False):
     m = len(tensors)
     arr, keep = _views(tensors)
-    o = N.OrthOpts(_opts(rel_tol, floor_c, 0, theta, rank_revealing), int(hh_beta_literal), int(want_loo))
+    o = N.OrthOpts(_opts(rel_tol, floor_c, 0, theta, rank_revealing), int(hh_beta_literal), int(want_loo),
+                   int(hh_mask))
     qs = (C.c_void_p * m)()
     R = np.zeros((m, m), dtype=np.float64)
     ncalls = {"cgs": m, "mgs": m, "cgs2": 2 * m, "mgs2": 2 * m, "gram": m, "householder": 4 * m - 1}[kind]

@@ -552,7 +552,7 @@ tt_status tt_orth(tt_ctx ctx, tt_orth_kind kind, int32_t m, const tt_view* a, co
   if (!ctx) return TT_EINVAL;
   tt_orth_opts o;
   if (opts) o = *opts;
-  else { o.round = default_round_opts(); o.hh_beta_literal = 0; o.want_loo = 0; }
+  else { o.round = default_round_opts(); o.hh_beta_literal = 0; o.want_loo = 0; o.hh_mask = 0; }
   return guarded(ctx, [&] { orth_run(ctx, kind, m, a, o, q_out, R_host, report); });
 }
 

@@ -381,6 +381,38 @@ void add_ref(SumInput& s, const TTRef& x, double c) {
   s.add(v, c);
 }
 
+// TT of the indicator "psi-order linear index >= L" (0-based index, mode 1 fastest): ranks <= 2,
+// states 0 = digits equal so far (from mode d down), 1 = already greater; core k's right index is
+// the state before its digit, its left index the state after; core 1 accepts both states.
+tt_tensor mask_geq_tt(tt_ctx ctx, const std::vector<int64_t>& n, int64_t L) {
+  const int d = (int)n.size();
+  std::vector<int64_t> dig((size_t)d), r((size_t)d + 1, 2);
+  int64_t rem = L;
+  for (int k = 0; k < d; ++k) { dig[(size_t)k] = rem % n[(size_t)k]; rem /= n[(size_t)k]; }
+  r[0] = r[(size_t)d] = 1;
+  tt_tensor t = tensor_alloc(ctx, d, n, r);
+  std::vector<double> h;
+  for (int k = 0; k < d; ++k) {
+    const int64_t left = r[(size_t)k], right = r[(size_t)k + 1], nk = n[(size_t)k];
+    std::vector<double> c((size_t)(left * nk * right), 0.0);
+    for (int64_t sin = 0; sin < right; ++sin) {
+      const int64_t state = (k == d - 1) ? 0 : sin;  // mode d starts "equal"
+      for (int64_t x = 0; x < nk; ++x) {
+        int64_t sout;
+        if (state == 1 || x > dig[(size_t)k]) sout = 1;
+        else if (x == dig[(size_t)k]) sout = 0;
+        else continue;  // smaller at the most significant differing digit
+        const int64_t row = (k == 0) ? 0 : sout;
+        c[(size_t)((row * nk + x) * right + sin)] = 1.0;
+      }
+    }
+    h.insert(h.end(), c.begin(), c.end());
+  }
+  TTB_CUDA(cudaMemcpyAsync(t->block, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+  TTB_CUDA(cudaStreamSynchronize(ctx->stream));  // h is a host temporary
+  return t;
+}
+
 std::vector<int64_t> phi0(const std::vector<int64_t>& n, int64_t lin1) {
   std::vector<int64_t> idx(n.size());
   int64_t rem = lin1 - 1;
@@ -522,8 +554,18 @@ void run_householder(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::
     double s = 0.0;
     for (int j = 0; j < i - 1; ++j) { r[(size_t)j] = ew[(size_t)j]; s += r[(size_t)j] * r[(size_t)j]; }
     SumInput s1;
-    add_ref(s1, w, 1.0);
-    for (int j = 0; j < i - 1; ++j) add_ref(s1, ER[(size_t)j], -r[(size_t)j]);
+    Owned masked(ctx);
+    if (o.hh_mask && i > 1) {
+      // SURVEY.md §8(f) 3 (departure from Alg. 6 lines 4-9): w with the entries phi(1..i-1) set to
+      // zero exactly, as w (.) mask(lin >= i-1), instead of the cancelling w - sum_{j<i} r(j) e_j
+      Owned mk(ctx, mask_geq_tt(ctx, n, i - 1));
+      masked.reset(hadamard(ctx, w.d, w.n, w.r, w.core, mk.t->r, mk.t->core_c));
+      TTRef mr = TTRef::of(masked.t);
+      add_ref(s1, mr, 1.0);  // norm NaN: s(x) = its own norm, computed (no cancellation)
+    } else {
+      add_ref(s1, w, 1.0);
+      for (int j = 0; j < i - 1; ++j) add_ref(s1, ER[(size_t)j], -r[(size_t)j]);
+    }
     Owned w1(ctx, led.round(ctx, s1, o.round));                 // Alg. 6 line 9
     const double w1n = last_core_norm(ctx, w1.t);
     w1.t->norm = w1n;

@@ -325,6 +325,43 @@ tt_tensor matvec(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::ve
 
 namespace {
 
+// Z_k((a, c), i, (b, e)) = X_k(a, i, b) Y_k(c, i, e): the slices' Kronecker product (elementwise
+// product of the two tensors), one thread per output element.
+__global__ void hadamard_core_kernel(const double* __restrict__ Xk, const double* __restrict__ Yk, int rx0, int rx1,
+                                     int ry0, int ry1, int n, double* __restrict__ Zk) {
+  const int64_t r1 = (int64_t)rx1 * ry1;
+  const int64_t total = (int64_t)rx0 * ry0 * n * r1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c1 = idx % r1, t = idx / r1;
+    const int i = (int)(t % n);
+    const int64_t c0 = t / n;
+    const int a = (int)(c0 / ry0), c = (int)(c0 % ry0), b = (int)(c1 / ry1), e = (int)(c1 % ry1);
+    Zk[idx] = Xk[((int64_t)a * n + i) * rx1 + b] * Yk[((int64_t)c * n + i) * ry1 + e];
+  }
+}
+
+}  // namespace
+
+tt_tensor hadamard(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& rx,
+                   const std::vector<const double*>& xc, const std::vector<int64_t>& ry,
+                   const std::vector<const double*>& yc) {
+  std::vector<int64_t> rz((size_t)d + 1);
+  for (int k = 0; k <= d; ++k) rz[(size_t)k] = rx[(size_t)k] * ry[(size_t)k];
+  tt_tensor z = tensor_alloc(ctx, d, n, rz);
+  for (int k = 0; k < d; ++k) {
+    const int64_t total = rz[(size_t)k] * n[(size_t)k] * rz[(size_t)k + 1];
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 4096));
+    TTB_RUN(ctx, "tt_hadamard", (double)total, 24.0 * total,
+            hadamard_core_kernel<<<blocks, 256, 0, ctx->stream>>>(
+                xc[(size_t)k], yc[(size_t)k], (int)rx[(size_t)k], (int)rx[(size_t)k + 1], (int)ry[(size_t)k],
+                (int)ry[(size_t)k + 1], (int)n[(size_t)k], z->core[(size_t)k]));
+  }
+  return z;
+}
+
+namespace {
+
 __global__ void dot_init_kernel(double* W, const int64_t* __restrict__ wo, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < P) W[wo[p]] = 1.0;

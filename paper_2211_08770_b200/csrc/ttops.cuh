@@ -45,6 +45,10 @@ struct DotBatch {
 void dot_batch(tt_ctx ctx, const DotBatch& b, double* out_dev, double* traces_dev = nullptr);
 // y = A x for a TT-matrix A (cores (ra_k, n_k, n_k, ra_{k+1}), row index then column index) and
 // a TT-vector x: a new tensor with ranks ra_k rx_k (the Krylov workload).
+// z = x (.) y elementwise (cores: Kronecker products of the slices, ranks multiply).
+tt_tensor hadamard(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& rx,
+                   const std::vector<const double*>& xc, const std::vector<int64_t>& ry,
+                   const std::vector<const double*>& yc);
 tt_tensor matvec(tt_ctx ctx, int d, const std::vector<int64_t>& n, const std::vector<int64_t>& ra,
                  const std::vector<const double*>& acore, const std::vector<int64_t>& rx,
                  const std::vector<const double*>& xcore);

@@ -276,3 +276,21 @@ def test_orth_c3_full_gram_closed_form():
         assert diff_norm(Q[i].to_numpy(), st.q_exact(i)) <= max(1e-10, amp), (i, amp)
     loo = rep["loo_per_step"]
     assert np.all(loo <= np.maximum(64 * c.m * U_ROUND * kap ** 2, 1e-14))
+
+
+def test_orth_householder_masked_variant():
+    """hh_mask = 1 (a flagged departure from Alg. 6 lines 4-9): the first TTH-vec
+    rounding takes w (.) mask(lin >= i-1) instead of w - sum_{j<i} r(j) e_j.  Against the oracle's
+    masked variant (pinned in test_oracle_orth.py: brute-force mask, dense equality with the
+    subtraction form, closed form), well-conditioned (R = R_M) and C1 (kappa = 1e8)."""
+    import paper_2211_08770_b200 as P
+    c1 = CONFIGS["C1"]
+    for st, delta in ((make_shared_tail_set(4, 8, 3, 10, 1e2, seed=991), 1e-12),
+                      (make_shared_tail_set(c1.d, c1.n, c1.r, c1.m, c1.kappa, c1.seed), c1.delta)):
+        ref = orth.orth("householder", st.tensors, delta, hh_mask=True)
+        Q, R, rep = P.tt_orth(ctx(), "householder", [dev(a) for a in st.tensors], delta, hh_mask=True,
+                              want_loo=True)
+        _check("householder", st, delta, Q, R, rep, ref)
+        if st.kappa <= 1e2:
+            qm, rm = st.qr_exact()
+            assert np.linalg.norm(_signs(R)[:, None] * R - rm) <= 1e-9 * np.linalg.norm(rm)
