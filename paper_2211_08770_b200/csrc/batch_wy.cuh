@@ -160,8 +160,16 @@ __device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) 
 // the chunk rows of its columns; taus on the diagonal of T.  T is built column by column as the
 // reflectors appear (T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) V(:, 0:jj)^T v_jj, lane r keeping row r):
 // the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots v_jj^T a_c (c > jj).
-__device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) {
+__device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, long long* fp = nullptr) {
   const int lane = threadIdx.x & 31;
+  long long f0 = fp ? clock64() : 0;
+  auto tick = [&](int slot) {
+    if (fp) {
+      const long long t = clock64();
+      if (lane == 0) fp[slot] += t - f0;
+      f0 = t;
+    }
+  };
   double* st = sm.st;
   (void)crow;
   double x[4][NB];
@@ -180,6 +188,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
 #pragma unroll
       for (int t = 0; t < 4; ++t) ss += x[t][jj] * x[t][jj];
       const double sigma = wsum(ss);
+      tick(0);
       const double alpha = st[j * LD + j];
       double beta = alpha, scal = 0.0, tj = 0.0;
       if (sigma != 0.0) {  // dlarfg with one reciprocal
@@ -192,6 +201,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
       }
 #pragma unroll
       for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
+      tick(1);
       if (tj != 0.0) {
         double dt[NB], rj[NB];
 #pragma unroll
@@ -205,6 +215,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
           dt[c] = q;
         }
         warp_sum8v(dt);
+        tick(2);
         {  // T(lane, jj) for lane < jj, T(jj, jj) = tau
           double tv = 0.0;
 #pragma unroll
@@ -230,6 +241,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
       }
       __syncwarp();
       if (lane == 0) st[j * LD + j] = beta;
+      tick(3);
     }
   }
   __syncwarp();
@@ -242,6 +254,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow) 
     for (int i = 0; i < NB; ++i) sm.Tm[w][lane * 8 + i] = trow[i];
   }
   __syncwarp();
+  tick(4);
 }
 
 // Factor the current stack (R block + chunk of crow rows in sm.st): ncol columns, nrefl
@@ -335,7 +348,7 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
         bar_arrive(&sm.used[jb]);
         if (prof) { const long long t = clock64(); tu += t - t0; t0 = t; }
       }
-      factor_block(sm, w, min(NB, ncol - NB * w), crow);
+      factor_block(sm, w, min(NB, ncol - NB * w), crow, (prof && w == 3) ? prof + 32 : nullptr);
       bar_arrive(&sm.ready[w]);
       if (prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
       // V (CH x 8 of this block, column-major ld CH) and T_w
