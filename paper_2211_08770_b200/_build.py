@@ -50,7 +50,10 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(LIBDIR, "obj", os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            jobs.append([nvcc] + NVCC_FLAGS + ["-I", INCLUDE, "-c", src, "-o", obj])
+            # TT_B200_NVCC_EXTRA: extra flags for debugging builds (e.g. "-DWY_PROF=1": the batched
+            # engine's cycle counters); a changed value needs force=True
+            extra = os.environ.get("TT_B200_NVCC_EXTRA", "").split()
+            jobs.append([nvcc] + NVCC_FLAGS + extra + ["-I", INCLUDE, "-c", src, "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

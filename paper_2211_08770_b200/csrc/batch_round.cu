@@ -1781,7 +1781,8 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_apply_wy_kernel(BRArgs A, int
     }
     return;
   }
-  wy::apply(sm, ph, tt + BR_C * BR_C, cp, rho, V, m1, cr, c1, c1, dst, 1, m1);
+  wy::apply(sm, ph, tt + BR_C * BR_C, cp, rho, V, m1, cr, c1, c1, dst, 1, m1,
+            (A.dbg && blockIdx.x == 0) ? A.dbg + 72 : nullptr);
 }
 
 // Copy item b's cores from the worst-case workspace to the exact-size arena.
@@ -2042,8 +2043,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       const char* dbe = std::getenv("TT_B200_BR_DEBUG");
       LBuf dbg;
       if (dbe && dbe[0] == '1') {
-        dbg.alloc(ctx, 80);
-        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 80 * sizeof(long long), ctx->stream));
+        dbg.alloc(ctx, 96);
+        TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 96 * sizeof(long long), ctx->stream));
       }
       a.dbg = dbg.p;
       for (int kc = d - 1; kc >= 1; --kc) {
@@ -2082,16 +2083,21 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
           TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
       }
       if (dbg.p) {
-        long long h[80];
+        long long h[96];
         TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         TTB_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (use_wy) {
+        if (use_wy && !WY_PROF) {
+          std::fprintf(stderr, "[br_debug] WY cycle counters: rebuild with TT_B200_NVCC_EXTRA=-DWY_PROF=1\n");
+        } else if (use_wy) {
           std::fprintf(stderr, "[br_debug] WY r2l, CTA 0, per warp (wait / update / factor / store+release+load, Mcycles):");
           for (int w = 0; w < 8; ++w)
             std::fprintf(stderr, " w%d %.2f/%.2f/%.2f/%.2f", w, 1e-6 * h[32 + 4 * w], 1e-6 * h[33 + 4 * w],
                          1e-6 * h[34 + 4 * w], 1e-6 * h[35 + 4 * w]);
-          std::fprintf(stderr, "\n[br_debug] warp 3 block factorisation (Mcycles): norm %.2f dlarfg %.2f dots %.2f T+update %.2f writeback %.2f\n",
+          std::fprintf(stderr, "\n[br_debug] warp 3 block factorisation (Mcycles): dots + reduction %.2f dlarfg %.2f update %.2f T + R row %.2f writeback %.2f\n",
                        1e-6 * h[64], 1e-6 * h[65], 1e-6 * h[66], 1e-6 * h[67], 1e-6 * h[68]);
+          std::fprintf(stderr, "[br_debug] Z application, CTA 0 thread 0 (Mcycles): staging wait %.2f, W %.2f, barrier %.2f, "
+                       "W' + update %.2f, end barrier + issue %.2f\n",
+                       1e-6 * h[72], 1e-6 * h[73], 1e-6 * h[74], 1e-6 * h[75], 1e-6 * h[76]);
         } else {
         std::fprintf(stderr, "[br_debug] r2l: assemble %lld qr %lld store %lld | l2r: assemble %lld qr %lld store %lld | jacobi %lld (%lld sweeps) outcore %lld nextcore %lld (cycles, CTA 0) | qr steps: owner(w0) %lld x%lld, pre-barrier(w0 not owner) %lld, barrier %lld, update %lld\n",
                      h[0], h[1], h[2], h[4], h[5], h[6], h[8], h[11], h[9], h[10], h[16], h[19], h[20], h[17], h[18]);

@@ -26,6 +26,12 @@
 
 #include "common.cuh"
 
+// Cycle counters of factor_panel / factor_block / apply (CTA 0, TT_B200_BR_DEBUG): compiled in only
+// with -DWY_PROF=1 (tools/wy_check time builds), so the production kernels carry no counters.
+#ifndef WY_PROF
+#define WY_PROF 0
+#endif
+
 namespace ttb {
 namespace wy {
 
@@ -159,19 +165,24 @@ __device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) 
 // Warp w factors its column block (reflectors j = 8w + jj, jj < nr), forms T_w, stores V into
 // the chunk rows of its columns; taus on the diagonal of T.  T is built column by column as the
 // reflectors appear (T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) V(:, 0:jj)^T v_jj, lane r keeping row r):
-// the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots v_jj^T a_c (c > jj).
-__device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, long long* fp = nullptr) {
+// the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots v_jj^T a_c (c > jj)
+// and the column mass sigma: one warp reduction per reflector.
+template <bool PROF>
+__device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, long long* fp) {
+  // Columns jj >= nr of a partial block are zero (chunk and R rows), so their steps below are
+  // exact no-ops (sigma = alpha = 0: tau = 0, beta = 0): the loop runs all NB steps branch-free.
+  (void)nr;
+  (void)crow;
   const int lane = threadIdx.x & 31;
-  long long f0 = fp ? clock64() : 0;
+  long long f0 = PROF ? clock64() : 0, facc[5] = {0, 0, 0, 0, 0};  // phase cycles (flushed at the end)
   auto tick = [&](int slot) {
-    if (fp) {
+    if (PROF) {
       const long long t = clock64();
-      if (lane == 0) fp[slot] += t - f0;
+      facc[slot] += t - f0;
       f0 = t;
     }
   };
   double* st = sm.st;
-  (void)crow;
   double x[4][NB];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
@@ -182,67 +193,63 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, 
   for (int c = 0; c < NB; ++c) trow[c] = 0.0;
 #pragma unroll
   for (int jj = 0; jj < NB; ++jj) {
-    if (jj < nr) {
-      const int j = 8 * w + jj;
-      double ss = 0.0;
+    const int j = 8 * w + jj;
+    // R row j of this block (only reflector jj touches it: loads off the dependency chain)
+    const double alpha = st[j * LD + j];
+    double rj[NB];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) ss += x[t][jj] * x[t][jj];
-      const double sigma = wsum(ss);
-      tick(0);
-      const double alpha = st[j * LD + j];
-      double beta = alpha, scal = 0.0, tj = 0.0;
-      if (sigma != 0.0) {  // dlarfg with one reciprocal
-        const double nrm = sqrt(alpha * alpha + sigma);
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        const double am = alpha - beta;
-        const double inv = 1.0 / (beta * am);
-        tj = -am * am * inv;
-        scal = beta * inv;
-      }
+    for (int c = 0; c < NB; ++c) rj[c] = c > jj ? st[(8 * w + c) * LD + j] : 0.0;
+    // one reduction for sigma = ||x_jj||^2 (slot jj), the dots x_jj^T a_c (c > jj: the update)
+    // and x_jj^T v_c (c < jj: for T), all with the unscaled x_jj
+    double dt[NB];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
-      tick(1);
-      if (tj != 0.0) {
-        double dt[NB], rj[NB];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {  // c > jj: v_jj^T a_c (update); c < jj: v_c^T v_jj (for T)
-          rj[c] = c > jj ? st[(8 * w + c) * LD + j] : 0.0;
-          double q = 0.0;
-          if (c != jj) {
-#pragma unroll
-            for (int t = 0; t < 4; ++t) q += x[t][jj] * x[t][c];
-          }
-          dt[c] = q;
-        }
-        warp_sum8v(dt);
-        tick(2);
-        {  // T(lane, jj) for lane < jj, T(jj, jj) = tau
-          double tv = 0.0;
-#pragma unroll
-          for (int q = 0; q < NB; ++q)
-            if (q < jj && q >= lane) tv += trow[q] * dt[q];
-          trow[jj] = lane < jj ? -tj * tv : (lane == jj ? tj : 0.0);
-        }
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          if (c > jj) {
-            const double wv = tj * (rj[c] + dt[c]);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) x[t][c] -= wv * x[t][jj];
-            rj[c] -= wv;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll
-          for (int c = 0; c < NB; ++c)
-            if (c > jj) st[(8 * w + c) * LD + j] = rj[c];
-        }
-      }
-      __syncwarp();
-      if (lane == 0) st[j * LD + j] = beta;
-      tick(3);
+    for (int c = 0; c < NB; ++c) {
+      const double p0 = x[0][jj] * x[0][c] + x[1][jj] * x[1][c];
+      const double p1 = x[2][jj] * x[2][c] + x[3][jj] * x[3][c];
+      dt[c] = p0 + p1;
     }
+    warp_sum8v(dt);
+    tick(0);
+    const double sigma = dt[jj];
+    // dlarfg with one reciprocal, branch-free (sigma = 0: H = I, beta = alpha)
+    const double nrm = sqrt(fma(alpha, alpha, sigma));
+    const double beta0 = alpha >= 0.0 ? -nrm : nrm;
+    const double am = alpha - beta0;
+    const double inv = 1.0 / (beta0 * am);
+    const bool live = sigma != 0.0;
+    const double tj = live ? -am * am * inv : 0.0;
+    const double scal = live ? beta0 * inv : 0.0;
+    const double beta = live ? beta0 : alpha;
+    tick(1);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) dt[c] *= scal;  // v_jj^T a_c (c > jj), v_c^T v_jj (c < jj)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      if (c > jj) {
+        const double wv = tj * (rj[c] + dt[c]);
+        const double wsc = wv * scal;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) x[t][c] -= wsc * x[t][jj];
+        rj[c] -= wv;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
+    tick(2);
+    {  // T(lane, jj) for lane < jj, T(jj, jj) = tau
+      double tv = 0.0;
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+        if (q < jj && q >= lane) tv += trow[q] * dt[q];
+      trow[jj] = lane < jj ? -tj * tv : (lane == jj ? tj : 0.0);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c > jj) st[(8 * w + c) * LD + j] = rj[c];
+      st[j * LD + j] = beta;
+    }
+    tick(3);
   }
   __syncwarp();
 #pragma unroll
@@ -255,38 +262,9 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, 
   }
   __syncwarp();
   tick(4);
-}
-
-// Factor the current stack (R block + chunk of crow rows in sm.st): ncol columns, nrefl
-// reflectors (< ncol only for a single-stack panel with fewer rows than columns).  q = stack
-// index (mbarrier parity).  On return (after a CTA barrier) V and T are stored at out.
-__device__ __forceinline__ void factor_stack(Smem& sm, int ncol, int nrefl, int crow, int q, double* __restrict__ out) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int nbr = (nrefl + NB - 1) / NB;
-  const uint32_t par = (uint32_t)(q & 1);
-  if (8 * w < ncol) {
-    const int lim = w < nbr ? w : nbr;
-#pragma unroll 1
-    for (int jb = 0; jb < lim; ++jb) {
-      bar_wait(&sm.ready[jb], par);
-      update_block(sm, jb, w, crow);
-    }
-    if (w < nbr) {
-      factor_block(sm, w, min(NB, nrefl - 8 * w), crow);
-      bar_arrive(&sm.ready[w]);  // release: V, T, R rows of block w
-    }
-  }
-  __syncthreads();
-  // store V (CH x min(ncol, 8 nbr), column-major ld CH: whole blocks, so every staged column of a
-  // partial block is finite) and T
-  const int nvc = min(ncol, NB * nbr);
-  for (int idx = tid; idx < CH * nvc; idx += T) {
-    const int c = idx / CH, r = idx % CH;
-    out[idx] = sm.st[c * LD + RR + r];
-  }
-  double* tout = out + (int64_t)CH * ncol;
-  for (int idx = tid; idx < 64 * nbr; idx += T) tout[idx] = (&sm.Tm[0][0])[idx];
-  (void)lane;
+  if (PROF && lane == 0)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) fp[i] += facc[i];
 }
 
 // Initialise the mbarriers (once per launch, before the first stack) and zero the R block.
@@ -333,9 +311,9 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
   if (w < nact) {
     // prof (debugging, CTA 0): per warp cycles waiting for blocks, applying them, factoring, and
     // storing + waiting for the release + loading the next stack
-    long long t0 = prof ? clock64() : 0, tw = 0, tu = 0, tf = 0, tl = 0;
+    long long t0 = (WY_PROF && prof) ? clock64() : 0, tw = 0, tu = 0, tf = 0, tl = 0;
     L.load(sm, 0, w);
-    if (prof) { tl += clock64() - t0; t0 = clock64(); }
+    if (WY_PROF && prof) { tl += clock64() - t0; t0 = clock64(); }
 #pragma unroll 1
     for (int q = 0; q < S; ++q) {
       const int crow = L.crow(q);
@@ -343,14 +321,17 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
 #pragma unroll 1
       for (int jb = 0; jb < w; ++jb) {
         bar_wait(&sm.ready[jb], par);
-        if (prof) { const long long t = clock64(); tw += t - t0; t0 = t; }
+        if (WY_PROF && prof) { const long long t = clock64(); tw += t - t0; t0 = t; }
         update_block(sm, jb, w, crow);
         bar_arrive(&sm.used[jb]);
-        if (prof) { const long long t = clock64(); tu += t - t0; t0 = t; }
+        if (WY_PROF && prof) { const long long t = clock64(); tu += t - t0; t0 = t; }
       }
-      factor_block(sm, w, min(NB, ncol - NB * w), crow, (prof && w == 3) ? prof + 32 : nullptr);
+      if (WY_PROF && prof && w == 3)
+        factor_block<true>(sm, w, min(NB, ncol - NB * w), crow, prof + 32);
+      else
+        factor_block<false>(sm, w, min(NB, ncol - NB * w), crow, nullptr);
       bar_arrive(&sm.ready[w]);
-      if (prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
+      if (WY_PROF && prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
       // V (CH x 8 of this block, column-major ld CH) and T_w
       double* o = out + (int64_t)q * sd;
       const int nc = min(NB, ncol - NB * w);
@@ -366,9 +347,9 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
         __syncwarp();
         L.load(sm, q + 1, w);
       }
-      if (prof) { const long long t = clock64(); tl += t - t0; t0 = t; }
+      if (WY_PROF && prof) { const long long t = clock64(); tl += t - t0; t0 = t; }
     }
-    if (prof && lane == 0) {
+    if (WY_PROF && prof && lane == 0) {
       prof[4 * w + 0] += tw;
       prof[4 * w + 1] += tu;
       prof[4 * w + 2] += tf;
@@ -443,8 +424,16 @@ __device__ __forceinline__ void stage_block(ASmem& sm, const double* F, int ncol
 // F + q * stack_doubles(ncol).  ph[]: the staging barriers' phase bits (kept across calls).
 __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict__ src, int ncx, int nt,
                       const double* __restrict__ F0, int64_t m, int cr, int ncol, int nrefl, double* __restrict__ out,
-                      int64_t rs, int64_t cs) {
+                      int64_t rs, int64_t cs, long long* ap = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q4 = lane & 3, r8 = lane >> 2;
+  long long a0 = (WY_PROF && ap && tid == 0) ? clock64() : 0, aacc[5] = {0, 0, 0, 0, 0};
+  auto tk = [&](int slot) {
+    if (WY_PROF && ap && tid == 0) {
+      const long long t = clock64();
+      aacc[slot] += t - a0;
+      a0 = t;
+    }
+  };
   const int S = (int)((m + cr - 1) / cr);
   const int nbr = (nrefl + NB - 1) / NB;
   const int64_t sd = stack_doubles(ncol);
@@ -478,8 +467,10 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
           }
         }
         const int b = tq % NBUF;
+        tk(4);
         bar_wait(&sm.bar[b], ph[b]);
         ph[b] ^= 1u;
+        tk(0);
         const double* Vs = sm.Vs[b];
         const bool first = (jb == nbr - 1);
         // ---- W = Rt[8jb + i][:] + V^T Ct (8 x ntp), split over (column tile, k range)
@@ -512,7 +503,9 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
             wp[r8 * 12 + 2 * q4 + 1] = c1 + e1;
           }
         }
+        tk(1);
         __syncthreads();
+        tk(2);
         // ---- per warp: W' = T W of its column tile (nti = w mod ntl4: the same for every unit of
         // this warp), R-block rows -= W' (one warp per tile), then C -= V W' over its units
         {
@@ -536,6 +529,7 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
             ws[r8 * 8 + 2 * q4 + 1] = d1;
             __syncwarp();
             const double f0 = ws[q4 * 8 + r8], f1 = ws[(4 + q4) * 8 + r8];
+#pragma unroll 4
             for (int u = w; u < nm * ntl4; u += W) {
               const int mt = u / ntl4;
               double* cp = sm.Ct + (8 * nti + 2 * q4) * ALD + 8 * mt + r8;
@@ -547,6 +541,7 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
             }
           }
         }
+        tk(3);
         __syncthreads();
       }
       for (int idx = tid; idx < ntp * crow; idx += T) {
@@ -557,6 +552,9 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
     }
   }
   __syncthreads();
+  if (WY_PROF && ap && tid == 0)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) ap[i] += aacc[i];
 }
 
 }  // namespace wy

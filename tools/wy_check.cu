@@ -1,11 +1,15 @@
 // Standalone check of the compact-WY flat-tree QR and its application (csrc/batch_wy.cuh):
 // factor a random m x c matrix in stacks of cr rows, apply Q to [I; 0], and compare on the host:
 // ||A - Q R|| / ||A|| and ||Q^T Q - I||.
+// Cases include nearly dependent, rank-deficient and graded columns.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -o tools/wy_check tools/wy_check.cu
+// Timing of the pipelined panel (2048 x 64, one matrix per CTA; per-warp cycle counters of CTA 0
+// when built with -DWY_PROF=1):  tools/wy_check time GRID
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "../paper_2211_08770_b200/csrc/batch_wy.cuh"
@@ -39,6 +43,55 @@ __global__ void __launch_bounds__(wy::T, 1) factor_kernel(const double* A, int64
   }
 }
 
+// timing: CTA b factors its own m x c matrix (A + b m c); CTA 0 records the per-warp counters
+__global__ void __launch_bounds__(wy::T, 2) time_kernel(const double* A, int64_t m, int c, int cr, double* F,
+                                                        long long* prof) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  wy::Smem& sm = *reinterpret_cast<wy::Smem*>(raw);
+  RowLoader ld{A + (int64_t)blockIdx.x * m * c, m, c, cr};
+  wy::factor_panel(sm, ld, c, F + (int64_t)blockIdx.x * ((m + cr - 1) / cr) * wy::stack_doubles(c),
+                   blockIdx.x == 0 ? prof : nullptr);
+}
+
+static int time_main(int grid) {
+  const int64_t m = 2048;
+  const int c = 64, cr = 128, S = (int)(m / cr);
+  double *dA, *dF;
+  long long* dp;
+  cudaMalloc(&dA, sizeof(double) * grid * m * c);
+  cudaMalloc(&dF, sizeof(double) * grid * S * wy::stack_doubles(c));
+  cudaMalloc(&dp, sizeof(long long) * 64);
+  std::vector<double> A((size_t)grid * m * c);
+  std::mt19937_64 rng(11);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (auto& v : A) v = nd(rng);
+  cudaMemcpy(dA, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice);
+  cudaFuncSetAttribute(time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(wy::Smem));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int it = 0; it < 3; ++it) {
+    cudaMemset(dp, 0, sizeof(long long) * 64);
+    cudaEventRecord(e0);
+    time_kernel<<<grid, wy::T, sizeof(wy::Smem)>>>(dA, m, c, cr, dF, dp);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long h[64];
+  cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost);
+  std::printf("grid %d: %.3f ms, %d stacks of %d x %d per CTA (%s)\n", grid, ms, S, cr, c,
+              cudaGetErrorString(cudaGetLastError()));
+  for (int w = 0; w < 8; ++w)
+    std::printf("  w%d wait %.0f update %.0f factor %.0f store+load %.0f (cycles per stack)\n", w, (double)h[4 * w] / S,
+                (double)h[4 * w + 1] / S, (double)h[4 * w + 2] / S, (double)h[4 * w + 3] / S);
+  std::printf("  w3 factor phases per block: dots+reduce %.0f dlarfg %.0f update %.0f T+store %.0f writeback %.0f\n",
+              (double)h[32] / S, (double)h[33] / S, (double)h[34] / S, (double)h[35] / S, (double)h[36] / S);
+  cudaFree(dA); cudaFree(dF); cudaFree(dp);
+  return 0;
+}
+
 __global__ void __launch_bounds__(wy::T, 1) apply_kernel(const double* X, int ncx, int nt, const double* F, int64_t m,
                                                          int cr, int c, double* out) {
   extern __shared__ __align__(16) unsigned char raw[];
@@ -49,10 +102,13 @@ __global__ void __launch_bounds__(wy::T, 1) apply_kernel(const double* X, int nc
 }
 
 int main(int argc, char** argv) {
-  struct Case { int64_t m; int c, cr; };
+  if (argc > 2 && std::string(argv[1]) == "time") return time_main(std::atoi(argv[2]));
+  struct Case { int64_t m; int c, cr, kind = 0; };
   std::vector<Case> cases = {{50, 8, 128}, {100, 12, 128}, {300, 24, 120}, {720, 24, 120}, {2500, 64, 100},
                              {2500, 50, 128}, {2048, 64, 128},  {825, 12, 128},
-                             {480, 16, 128}, {396, 25, 120}, {270, 3, 126}, {90, 9, 128}, {270, 3, 128}, {64, 3, 64}};
+                             {480, 16, 128}, {396, 25, 120}, {270, 3, 126}, {90, 9, 128}, {270, 3, 128}, {64, 3, 64},
+                             {2048, 64, 128, 1}, {300, 24, 120, 1}, {2048, 64, 128, 2}, {396, 25, 120, 2},
+                             {2048, 64, 128, 3}, {720, 24, 120, 3}};
   std::mt19937_64 rng(7);
   std::normal_distribution<double> nd(0.0, 1.0);
   cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(wy::Smem));
@@ -64,6 +120,15 @@ int main(int argc, char** argv) {
     const int k = (int)(m < c ? m : c);
     std::vector<double> A((size_t)m * c);
     for (auto& v : A) v = nd(rng);
+    if (cs.kind == 1)  // nearly dependent column pairs: a_{2i+1} = a_{2i} + 1e-9 noise
+      for (int64_t i = 0; i < m; ++i)
+        for (int j = 1; j < c; j += 2) A[i * c + j] = A[i * c + j - 1] + 1e-9 * A[i * c + j];
+    if (cs.kind == 2)  // exactly repeated columns and a zero column: rank deficient
+      for (int64_t i = 0; i < m; ++i)
+        for (int j = 0; j < c; ++j) A[i * c + j] = j % 3 == 2 ? A[i * c + j - 1] : (j == 7 ? 0.0 : A[i * c + j]);
+    if (cs.kind == 3)  // graded columns: scale 10^(-j / 4)
+      for (int64_t i = 0; i < m; ++i)
+        for (int j = 0; j < c; ++j) A[i * c + j] *= std::pow(10.0, -0.25 * j);
     const int S = (int)((m + cr - 1) / cr);
     double *dA, *dF, *dR, *dX, *dQ;
     cudaMalloc(&dA, sizeof(double) * A.size());
@@ -97,8 +162,25 @@ int main(int argc, char** argv) {
         const double d = s - (a == b ? 1.0 : 0.0);
         north += d * d;
       }
+    if (cs.kind == 2) {  // rank-deficient A: the augmented factorisation gives Q^T Q R = R (the
+      // virtual rows of Q vanish only on range(R)), so check ||(Q^T Q - I) R|| / ||R|| instead
+      north = 0.0;
+      double nr = 0.0;
+      for (int a = 0; a < k; ++a)
+        for (int j = 0; j < c; ++j) {
+          double s = 0;
+          for (int b = 0; b < k; ++b) {
+            double g = 0;
+            for (int64_t i = 0; i < m; ++i) g += Q[i * k + a] * Q[i * k + b];
+            s += (g - (a == b ? 1.0 : 0.0)) * R[b * c + j];
+          }
+          north += s * s;
+          nr += R[a * c + j] * R[a * c + j];
+        }
+      north /= nr;
+    }
     const double rel = std::sqrt(nres / na), orth = std::sqrt(north);
-    const bool ok = e == cudaSuccess && rel < 1e-13 && orth < 1e-13;
+    const bool ok = e == cudaSuccess && rel < 1e-13 && orth < 1e-13;  // kind 2: Q spans a rank-deficient A
     if (argc > 1 && m == 300) {  // dump A, R, F, Q for host-side analysis
       std::vector<double> Fh((size_t)S * wy::stack_doubles(c));
       cudaMemcpy(Fh.data(), dF, sizeof(double) * Fh.size(), cudaMemcpyDeviceToHost);
@@ -110,7 +192,8 @@ int main(int argc, char** argv) {
       std::fclose(f);
     }
     bad += !ok;
-    std::printf("m %5lld c %2d cr %3d: ||A-QR||/||A|| %.2e  ||Q^TQ-I|| %.2e  %s %s\n", (long long)m, c, cr, rel, orth,
+    std::printf("m %5lld c %2d cr %3d kind %d: ||A-QR||/||A|| %.2e  ||Q^TQ-I|| %.2e  %s %s\n", (long long)m, c, cr,
+                cs.kind, rel, orth,
                 ok ? "OK" : "BAD", cudaGetErrorString(e));
     cudaFree(dA); cudaFree(dF); cudaFree(dR); cudaFree(dX); cudaFree(dQ);
   }
