@@ -999,9 +999,11 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
           const int row = LPP * ((u + pp) % RPL) + rl;
           ca[row] = cs * x[u] - sn * y[u];
           cb[row] = sn * x[u] + cs * y[u];
-          const double a0 = va[row], b0 = vbp[row];
-          va[row] = cs * a0 - sn * b0;
-          vbp[row] = sn * a0 + cs * b0;
+          if (row < nc) {  // V = Aux starts as I: rows >= nc of its first nc columns stay zero
+            const double a0 = va[row], b0 = vbp[row];
+            va[row] = cs * a0 - sn * b0;
+            vbp[row] = sn * a0 + cs * b0;
+          }
         }
       }
       if (__any_sync(0xffffffffu, rot) && lane == 0) sm.flag = 1;
@@ -1123,18 +1125,42 @@ __device__ int br_qrcp(BRSmem& sm, int rows, int nc, double stop2, double* tau_s
     const double* v = sm.Rs + s * BR_C;
     const double v0 = lane > s ? v[lane] : (lane == s ? 1.0 : 0.0);
     const double v1 = lane + 32 > s ? v[lane + 32] : (lane + 32 == s ? 1.0 : 0.0);
-    for (int j = s + 1 + ((warp - s - 1) & (BR_W - 1)); j < nc; j += BR_W) {  // this warp's columns > s
-      double* cj = sm.Rs + j * BR_C;
-      double x0 = cj[lane], x1 = cj[lane + 32];
-      if (tau != 0.0) {
-        const double w = tau * warp_sum(v0 * x0 + v1 * x1);
-        x0 -= w * v0;
-        x1 -= w * v1;
-        cj[lane] = x0;
-        cj[lane + 32] = x1;
+    {  // this warp's columns j > s (j = j0 + 8 t, at most 8): dots and masses through one
+       // transposed butterfly each instead of two warp reductions per column
+      const int j0 = s + 1 + ((warp - s - 1) & (BR_W - 1));
+      const int ncj = j0 < nc ? (nc - j0 + BR_W - 1) / BR_W : 0;
+      double x0[8], x1[8], dq[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double* cj = sm.Rs + (t < ncj ? j0 + BR_W * t : 0) * BR_C;
+        x0[t] = t < ncj ? cj[lane] : 0.0;
+        x1[t] = t < ncj ? cj[lane + 32] : 0.0;
       }
-      const double q = warp_sum((lane > s ? x0 * x0 : 0.0) + (lane + 32 > s ? x1 * x1 : 0.0));
-      if (lane == 0) nrm2[j] = q;
+      if (tau != 0.0 && ncj > 0) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dq[t] = v0 * x0[t] + v1 * x1[t];
+        wy::warp_sum8v(dq);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const double w = tau * dq[t];
+          x0[t] -= w * v0;
+          x1[t] -= w * v1;
+          if (t < ncj) {
+            double* cj = sm.Rs + (j0 + BR_W * t) * BR_C;
+            cj[lane] = x0[t];
+            cj[lane + 32] = x1[t];
+          }
+        }
+      }
+      if (ncj > 0) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dq[t] = (lane > s ? x0[t] * x0[t] : 0.0) + (lane + 32 > s ? x1[t] * x1[t] : 0.0);
+        wy::warp_sum8v(dq);
+        if (lane == 0)
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t < ncj) nrm2[j0 + BR_W * t] = dq[t];
+      }
     }
     __syncthreads();
   }
@@ -1279,7 +1305,10 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
     double* taus = sm.vb[1];
     double* nrm2 = sm.vb[0];
     double e2 = 0.0;
+    const bool prof = A.dbg && blockIdx.x == 0 && tid == 0;  // CTA 0 phase cycles (TT_B200_BR_DEBUG)
+    long long pt = prof ? clock64() : 0;
     const int kq = br_qrcp(sm, cp, cp, 1e-6 * tau * tau, taus, sm.cterm, nrm2, &e2);
+    if (prof) { const long long t = clock64(); A.dbg[80] += t - pt; A.dbg[84] += kq; A.dbg[85] += 1; pt = t; }
     for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) qx[idx] = sm.Rs[idx];
     if (tid < BR_C) qx[BR_C * BR_C + tid] = tid < kq ? taus[tid] : 0.0;
     __syncthreads();
@@ -1290,6 +1319,7 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
     __syncthreads();
     const bool conv = kq < 1 || br_jacobi(sm, cp, kq, tau * tau / (double)(kq > 0 ? kq : 1),
                                           (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
+    if (prof) { const long long t = clock64(); A.dbg[81] += t - pt; pt = t; }
     if (tid == 0) {
       int rho = kq;
       double t2 = e2;
@@ -1320,27 +1350,59 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
           else tt[col * BR_C + j] = 0.0;
         }
       // V_rho S = Q_X [J Sigma; 0] (second slot) and, for U = Y W, W = Q_X [J Sigma^-1; 0] (first)
+      // Targets of this warp: its columns col = warp + 8 i, each as J Sigma (second slot) and, for
+      // U = Y W, J Sigma^-1 (first slot); up to 8 targets at a time take each reflector together
+      // (one transposed butterfly per reflector for all of them).
       const int lane = tid & 31, warp = tid >> 5;
-      for (int col = warp; col < rho; col += BR_W) {
-        const double sg = sm.sig[col];
-        const int pc = sm.perm[col];
-        const double j0 = lane < kq ? sm.Aux[pc * BR_C + lane] : 0.0;
-        const double j1 = lane + 32 < kq ? sm.Aux[pc * BR_C + lane + 32] : 0.0;
-        double y0 = j0 * sg, y1 = j1 * sg;
-        br_apply_qx(y0, y1, qx, qx + BR_C * BR_C, kq);
-        tt[BR_C * BR_C + col * BR_C + lane] = lane < cp ? y0 : 0.0;
-        tt[BR_C * BR_C + col * BR_C + lane + 32] = lane + 32 < cp ? y1 : 0.0;
-        if (use_gemm) {
-          const double is = sg > 0.0 ? 1.0 / sg : 0.0;
-          y0 = j0 * is;
-          y1 = j1 * is;
-          br_apply_qx(y0, y1, qx, qx + BR_C * BR_C, kq);
-          tt[col * BR_C + lane] = lane < cp ? y0 : 0.0;
-          tt[col * BR_C + lane + 32] = lane + 32 < cp ? y1 : 0.0;
+      const int ncw = rho > warp ? (rho - warp + BR_W - 1) / BR_W : 0;
+      const int ntg = ncw * (use_gemm ? 2 : 1);
+      const double* taus_x = qx + BR_C * BR_C;
+#pragma unroll 1
+      for (int g0 = 0; g0 < ntg; g0 += 8) {
+        double y0[8], y1[8], dq[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int tg = g0 + t;
+          const int col = warp + BR_W * (use_gemm ? tg >> 1 : tg);
+          const bool live = tg < ntg;
+          const double sg = live ? sm.sig[col] : 0.0;
+          const double f = (use_gemm && (tg & 1)) ? (sg > 0.0 ? 1.0 / sg : 0.0) : sg;
+          const int pc = live ? sm.perm[col] : 0;
+          y0[t] = live && lane < kq ? sm.Aux[pc * BR_C + lane] * f : 0.0;
+          y1[t] = live && lane + 32 < kq ? sm.Aux[pc * BR_C + lane + 32] * f : 0.0;
+        }
+#pragma unroll 1
+        for (int i = kq - 1; i >= 0; --i) {  // Q_X = H_0 .. H_{kq-1}: H_{kq-1} first
+          const double tau = taus_x[i];
+          if (tau == 0.0) continue;
+          const double* vq = qx + i * BR_C;
+          const double v0 = lane > i ? vq[lane] : (lane == i ? 1.0 : 0.0);
+          const double v1 = lane + 32 > i ? vq[lane + 32] : (lane + 32 == i ? 1.0 : 0.0);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) dq[t] = v0 * y0[t] + v1 * y1[t];
+          wy::warp_sum8v(dq);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const double w = tau * dq[t];
+            y0[t] -= w * v0;
+            y1[t] -= w * v1;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int tg = g0 + t;
+          if (tg < ntg) {
+            const int col = warp + BR_W * (use_gemm ? tg >> 1 : tg);
+            double* dst = tt + ((use_gemm && (tg & 1)) ? 0 : BR_C * BR_C) + col * BR_C;
+            dst[lane] = lane < cp ? y0[t] : 0.0;
+            dst[lane + 32] = lane + 32 < cp ? y1[t] : 0.0;
+          }
         }
       }
+      if (prof) A.dbg[82] += clock64() - pt;
       return;
     }
+    if (prof) A.dbg[83] += 1;
     // ambiguous decision: the full Jacobi on X decides (reload R_Y^T)
     for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Rs[idx] = jm[(idx % BR_C) * BR_C + idx / BR_C];
     __syncthreads();
@@ -2086,6 +2148,10 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         long long h[96];
         TTB_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (use_wy)
+          std::fprintf(stderr, "[br_debug] l2r SVD, CTA 0 (%lld tall splits, kq sum %lld, %lld ambiguous): QRCP %.2f Mcycles, "
+                       "Jacobi %.2f (%lld sweeps), Q_X applications %.2f\n", h[85], h[84], h[83], 1e-6 * h[80],
+                       1e-6 * h[81], h[11], 1e-6 * h[82]);
         if (use_wy && !WY_PROF) {
           std::fprintf(stderr, "[br_debug] WY cycle counters: rebuild with TT_B200_NVCC_EXTRA=-DWY_PROF=1\n");
         } else if (use_wy) {
