@@ -2026,25 +2026,35 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   dscale.upload(ctx, scale.data(), scale.size() * sizeof(double), true);
   // ---------------------------------------------------------------- waves
   stamp("tables uploaded");
-  size_t free_b = 0, total_b = 0;
-  TTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  auto ws_for = [&](int nbm) {
+    return (size_t)nbm * ((size_t)sh.vstride + sh.tstride + 6 * BR_C * BR_C + BR_C + sh.ystride + sh.ytstride +
+                          2 * sh.zstride + std::max<int64_t>(sh.ostride, 1) + 4) +
+           (size_t)nbm * (d + 3) + 64;
+  };
   // one wave when the whole batch fits in ~60 % of the device (the workspace is the context's
-  // grow-only scratch: no allocation churn between calls)
-  const double budget = std::min<double>(0.6 * ((double)free_b + (double)ctx->scratch_bytes), 100e9);
-  const int W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
+  // grow-only scratch: no allocation churn between calls).  A batch the scratch already holds
+  // skips the free-memory query (cudaMemGetInfo costs 0.2-2 ms: the serial drivers' one-item
+  // batches would pay it on every rounding).
+  size_t free_b = 0, total_b = 0;
+  int W = B;
+  if (ws_for(B) * sizeof(double) > ctx->scratch_bytes) {
+    TTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double budget = std::min<double>(0.6 * ((double)free_b + (double)ctx->scratch_bytes), 100e9);
+    W = (int)std::max<int64_t>(1, std::min<int64_t>(B, (int64_t)(budget / (8.0 * (double)per_item))));
+  }
   const int nb_max = std::min(W, B);
-  const size_t ws_doubles = (size_t)nb_max * ((size_t)sh.vstride + sh.tstride + 6 * BR_C * BR_C + BR_C + sh.ystride +
-                                              sh.ytstride + 2 * sh.zstride + std::max<int64_t>(sh.ostride, 1) + 4) +
-                            (size_t)nb_max * (d + 3) + 64;
+  const size_t ws_doubles = ws_for(nb_max);
   double* ws = static_cast<double*>(ctx_scratch(ctx, ws_doubles * sizeof(double)));
   // kernels that do not stage reflector slices leave out the VStage buffers
   const size_t smem = offsetof(BRSmem, vst), smem_q = offsetof(BRSmem, vst), smem_a = sizeof(BRSmemA);
-  TTB_CUDA(cudaFuncSetAttribute(br_r2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  TTB_CUDA(cudaFuncSetAttribute(br_l2r_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
-  TTB_CUDA(cudaFuncSetAttribute(br_l2r_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
-  TTB_CUDA(cudaFuncSetAttribute(br_l2r_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
   const size_t smem_wy = sizeof(wy::Smem), smem_wya = sizeof(wy::ASmem);
-  if (use_wy) {
+  static uint64_t attr_set = 0;  // devices whose kernel attributes are set (once per process)
+  if (!(attr_set >> (ctx->device & 63) & 1)) {
+    attr_set |= (uint64_t)1 << (ctx->device & 63);
+    TTB_CUDA(cudaFuncSetAttribute(br_r2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TTB_CUDA(cudaFuncSetAttribute(br_l2r_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
+    TTB_CUDA(cudaFuncSetAttribute(br_l2r_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q));
+    TTB_CUDA(cudaFuncSetAttribute(br_l2r_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
     TTB_CUDA(cudaFuncSetAttribute(br_r2l_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wy));
     TTB_CUDA(cudaFuncSetAttribute(br_l2r_qr_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wy));
     TTB_CUDA(cudaFuncSetAttribute(br_l2r_apply_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wya));
@@ -2054,6 +2064,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
   res.n = in.n;
   res.ranks.assign((size_t)B * (d + 1), 1);
   res.norm.assign((size_t)B, 0.0);
+  res.tau.assign((size_t)B, 0.0);
+  res.scale.assign((size_t)B, 0.0);
   res.core.assign((size_t)B * d, nullptr);
   res.wave_first.clear();
   res.arenas.clear();
@@ -2172,15 +2184,19 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       // ranks (the one host synchronisation of the wave), then compaction
       std::vector<int> hr((size_t)nb * (d + 1)), hinf((size_t)nb);
       stamp("launched");
-      d2h_small_int(ctx, hr.data(), RK.p, hr.size());
+      // SC, RK, INF and GM are consecutive pieces of the scratch: one read-back
+      std::vector<double> hblk((size_t)((reinterpret_cast<double*>(GM.p) - SC.p) + (nb + 1) / 2));
+      d2h_small(ctx, hblk.data(), SC.p, hblk.size());
       stamp("synced (ranks)");
-      d2h_small_int(ctx, hinf.data(), INF.p, hinf.size());
+      auto piece = [&](const void* dp) { return reinterpret_cast<const char*>(hblk.data()) + (reinterpret_cast<const char*>(dp) - reinterpret_cast<const char*>(SC.p)); };
+      std::memcpy(hr.data(), piece(RK.p), sizeof(int) * hr.size());
+      std::memcpy(hinf.data(), piece(INF.p), sizeof(int) * hinf.size());
       for (int b = 0; b < nb; ++b)
         if (hinf[(size_t)b]) fail(TT_ENOCONV, "Jacobi SVD did not converge (batch item " + std::to_string(w0 + b) + ")");
       std::vector<double> hsc((size_t)nb * 4);
-      d2h_small(ctx, hsc.data(), SC.p, hsc.size());
+      std::memcpy(hsc.data(), piece(SC.p), sizeof(double) * hsc.size());
       std::vector<int> hgm((size_t)nb);
-      d2h_small_int(ctx, hgm.data(), GM.p, hgm.size());
+      std::memcpy(hgm.data(), piece(GM.p), sizeof(int) * hgm.size());
       std::vector<int64_t> dst((size_t)nb * d), sz((size_t)nb * d);
       int64_t tot = 0;
       double l2r_svd_fl = 0.0, l2r_qr_fl = 0.0, l2r_ap_fl = 0.0;
@@ -2243,6 +2259,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         for (int kc = 0; kc < d; ++kc)
           res.core[(size_t)(w0 + b) * d + kc] = static_cast<double*>(arena) + dst[(size_t)b * d + kc];
         res.norm[(size_t)(w0 + b)] = hsc[(size_t)b * 4 + 0];
+        res.tau[(size_t)(w0 + b)] = hsc[(size_t)b * 4 + 1];
+        res.scale[(size_t)(w0 + b)] = hsc[(size_t)b * 4 + 2];
       }
       stamp("wave done (host)");
     }
@@ -2254,7 +2272,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
 }
 
 void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
-                         int64_t* ranks_out) {
+                         int64_t* ranks_out, tt_round_info* info) {
   BatchDesc in;
   const SumInput& f = items[0];
   in.B = (int)items.size();
@@ -2290,6 +2308,12 @@ void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const t
       tt->arena = res.arenas[w];
       tt->arena_refs = refs;
       out[b] = tt;
+      if (info) {
+        info[b] = tt_round_info{};
+        info[b].norm = res.norm[(size_t)b];
+        info[b].scale = res.scale[(size_t)b];
+        info[b].tau = res.tau[(size_t)b];
+      }
       if (ranks_out)
         for (int k = 0; k <= d; ++k) ranks_out[(size_t)b * (d + 1) + k] = tt->r[(size_t)k];
     }

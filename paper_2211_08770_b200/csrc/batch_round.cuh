@@ -23,7 +23,7 @@ struct BatchOut {
   std::vector<int64_t> n;
   std::vector<int64_t> ranks;
   std::vector<double*> core;
-  std::vector<double> norm;
+  std::vector<double> norm, tau, scale;  // ||x||, the truncation threshold and s(x) per item
   std::vector<void*> arenas;   // one exact-size allocation per wave (caller frees)
   std::vector<int64_t> arena_size;  // doubles in each arena (items in order, cores in order)
   std::vector<int> wave_first; // first item of each wave
@@ -39,7 +39,8 @@ void batch_desc_shape(BatchDesc& in, int B, int K, int d, const int64_t* n, cons
 // host_pipe.cu: release the context's host-pipeline streams and staging buffers.
 void host_pipe_release(tt_ctx ctx);
 // out[b] = TT-round(items[b]) as library tensors (sharing one refcounted arena per wave).
+// info (optional, B entries): ||x||, s(x) and tau of each item.
 void round_batch_uniform(tt_ctx ctx, const std::vector<SumInput>& items, const tt_round_opts& o, tt_tensor* out,
-                         int64_t* ranks_out);
+                         int64_t* ranks_out, tt_round_info* info = nullptr);
 
 }  // namespace ttb

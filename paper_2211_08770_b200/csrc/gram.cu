@@ -41,17 +41,17 @@ struct GramShape {  // modes and the rank profiles of the I-side (r) and J-side 
 };
 
 
-// ---- FP64 tensor-core (DMMA, mma.sync m8n8k4) version: one warp per pair of the 2 x 2 tile.
-// Warp p = 2 i + j keeps W's A fragments in registers for the whole core and V in DMMA
-// accumulators; per mode slice s it forms U = W X^(j)(s) (NT x NT 8x8 tiles, K = R0) into its own
-// shared block and then V += X^(i)(s)^T U -- no cross-warp dependency inside a slice, one
-// __syncthreads per slice for the staged slices (cp.async from a per-core copy list in shared
-// memory: one 16-byte copy per list entry and thread, no per-copy index arithmetic; double
-// buffered, the next core's first slice prefetched during the last slice of the current one).  One warp per SM
-// sub-partition with >= 2 independent accumulators saturates the DMMA pipe (tools/dmma_bench:
-// latency 26 cycles, 16 cycles per DMMA per sub-partition), so 9 accumulators per warp leave the
-// pipe the only limit.  Ranks are padded to 8 NT with zeros; the row stride L = 4 or 12 (mod 16)
-// keeps the fragment loads free of bank conflicts.
+// ---- FP64 tensor-core (DMMA, mma.sync m8n8k4) kernel: one warp per pair of the 2 x 2 tile.
+// Warp p = 2 i + j keeps W and V in DMMA fragments (registers) for the whole core; per mode
+// slice s it forms U^T = X^(j)(s)^T W^T and then V += X^(i)(s)^T U -- no cross-warp dependency
+// inside a slice, one __syncthreads per slice for the staged slices (cp.async from a per-core copy
+// list in shared memory: one 16-byte copy per list entry and thread, no per-copy index
+// arithmetic; double buffered, the next core's first slice prefetched during the last slice of
+// the current one).  One warp per SM sub-partition with >= 2 independent accumulators saturates
+// the DMMA pipe (tools/dmma_bench: latency 26 cycles, 16 cycles per DMMA per sub-partition).
+// Ranks are padded to 8 NT with zeros; the row stride L = 4 or 12 (mod 16) keeps the fragment
+// loads free of bank conflicts.  C3 Gram (profiles/ncu_r02_v2.md): DMMA sub-pipe 62 % busy;
+// the padding 20 -> 24 on M and N costs the rest.
 __device__ __forceinline__ void gmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -60,14 +60,28 @@ __device__ __forceinline__ void gmma(double& c0, double& c1, double a, double b)
 
 constexpr int GM_T = 128;  // threads per CTA: one warp per pair
 
+// ---- register-chained version: the two GEMMs of a slice pass U through registers.  U^T =
+// X_j(s)^T W^T leaves U^T in C fragments (thread (g, tg) holds U^T[8x + g][8y + 2tg + e]); read
+// as B[k][n] of V += X_i(s)^T U with the k positions of a k-step taken as 8z + 2tg + e (e fixed)
+// -- a relabelling of the contraction index, matched by the A fragments' row offsets -- they are
+// exactly the B fragments, and likewise V's C fragments are next core's W^T B fragments.  No
+// shared-memory round trip of U, no fragment shuffles.  A rank whose last 8-block is at most half
+// full places that block's entries on the even positions (rc_pos), so the odd k-step of the
+// block is all padding and skipped: K steps = ceil(r / 4), as with natural k-steps of 4.
+__device__ __forceinline__ int rc_pos(int p, int nt, bool half) {
+  const int b = 8 * (nt - 1);
+  if (!half || p < b || p >= b + 8) return p;
+  const int l = p - b;
+  return b + ((l & 1) ? 4 + (l >> 1) : (l >> 1));
+}
+
 template <int NT>
-__global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const double* const* __restrict__ cores,
+__global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_rc_kernel(const double* const* __restrict__ cores,
                                                                       GramShape sh, int m,
                                                                       const GramTile* __restrict__ tiles, int L,
                                                                       double* __restrict__ G) {
   extern __shared__ __align__(16) double gsm[];
   constexpr int RP = 8 * NT;
-  constexpr int KT = 2 * NT;                // k-steps of 4 over RP
   const int MB = RP * L;                    // one matrix block
   double* U = gsm;                          // [pair][a][c'] row-major, stride L (also W at core ends)
   double* XB = U + GT_P * MB;               // 2 buffers x [I0, I1, J0, J1][a][a']
@@ -82,12 +96,13 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   const GramTile tl = tiles[blockIdx.x / CS];
   const int i0 = tl.i0, j0 = tl.j0, d = sh.d;
   double* Up = U + p * MB;
-  // W's A fragments (W[8x + g][4q + tg]) for the whole core, in registers; W_0 = 1 (1 x 1)
-  double wf[NT][KT];
+  // W as the C fragments of the previous core's V (W[8x + g][8y + 2tg + e]); W_0 = 1 (1 x 1)
+  double wf[NT][NT][2];
 #pragma unroll
   for (int x = 0; x < NT; ++x)
 #pragma unroll
-    for (int q = 0; q < KT; ++q) wf[x][q] = (x == 0 && q == 0 && g == 0 && tg == 0) ? 1.0 : 0.0;
+    for (int y = 0; y < NT; ++y) wf[x][y][0] = wf[x][y][1] = 0.0;
+  wf[0][0][0] = (g == 0 && tg == 0) ? 1.0 : 0.0;
   double gv = 0.0;
   // Staged rows of core kk: the tile's I tensors (R0i rows of R1i doubles) then its J tensors
   // (R0j rows of R1j), clamped into the tile's block, so a padding tensor has its side's shape
@@ -144,7 +159,6 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
   bool staged = false;    // core k's first slice already in flight (prefetched by core k-1)
 #pragma unroll 1
   for (int k = 0; k < d; ++k) {
-    const int K4i = (sh.r[k] + 3) >> 2, K4j = (sh.q[k] + 3) >> 2;  // k-steps of the V / U GEMMs
     int sb, se;
     srange(k, sb, se);
     // the next core can be prefetched when its staged slices have the same shape (same copy
@@ -161,6 +175,24 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
     }
     if (pre_next) set_bases(k + 1);  // read after the slice loop's first barrier
     staged = false;
+    // rank spaces of this core: a = r_{k-1} (rows of the slices), a' = r_k (columns), per side
+    const int nti0 = (sh.r[k] + 7) >> 3, nti1 = (sh.r[k + 1] + 7) >> 3;
+    const int ntj0 = (sh.q[k] + 7) >> 3, ntj1 = (sh.q[k + 1] + 7) >> 3;
+    const bool pi0 = sh.r[k] - 8 * (nti0 - 1) <= 4, pi1 = sh.r[k + 1] - 8 * (nti1 - 1) <= 4;
+    const bool pj0 = sh.q[k] - 8 * (ntj0 - 1) <= 4, pj1 = sh.q[k + 1] - 8 * (ntj1 - 1) <= 4;
+    // fragment offsets inside a staged slice: rows at the k-step positions 8z + 2tg + e, columns
+    // at the M positions 8x + g (rc_pos: the half-full last block on the even positions)
+    int ci[NT], cj[NT], ri[NT][2], rj[NT][2];
+#pragma unroll
+    for (int x = 0; x < NT; ++x) {
+      ci[x] = rc_pos(8 * x + g, nti1, pi1);
+      cj[x] = rc_pos(8 * x + g, ntj1, pj1);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ri[x][e] = rc_pos(8 * x + 2 * tg + e, nti0, pi0) * L;
+        rj[x][e] = rc_pos(8 * x + 2 * tg + e, ntj0, pj0) * L;
+      }
+    }
     double v[NT][NT][2];
 #pragma unroll
     for (int x = 0; x < NT; ++x)
@@ -182,78 +214,79 @@ __global__ void __launch_bounds__(GM_T, NT >= 4 ? 1 : 3) gram_mma_kernel(const d
       bufc ^= 1;
       const double* Xi = XS + pi * MB;
       const double* Xj = XS + (GT_I + pj) * MB;
-      // U = W X_j(s): A[a][c] = W[a][c] (registers), B[c][c'] = X_j[c][c']
+      // U^T = X_j(s)^T W^T: A[c'][c] = X_j[c][c'] (smem), B[c][a] = W[a][c] (registers, the C
+      // fragments of the previous core's V: k positions 8z + 2tg + e)
       double u[NT][NT][2];
 #pragma unroll
       for (int x = 0; x < NT; ++x)
 #pragma unroll
         for (int y = 0; y < NT; ++y) u[x][y][0] = u[x][y][1] = 0.0;
 #pragma unroll
-      for (int q = 0; q < KT; ++q) {
-        if (q < K4j) {
-          double bf[NT];
+      for (int z = 0; z < NT; ++z) {
 #pragma unroll
-          for (int y = 0; y < NT; ++y) bf[y] = Xj[(4 * q + tg) * L + 8 * y + g];
+        for (int e = 0; e < 2; ++e) {
+          if (z < ntj0 && !(e == 1 && z == ntj0 - 1 && pj0)) {
+            double af[NT];
 #pragma unroll
-          for (int x = 0; x < NT; ++x)
+            for (int x = 0; x < NT; ++x) af[x] = Xj[rj[z][e] + cj[x]];
 #pragma unroll
-            for (int y = 0; y < NT; ++y) gmma(u[x][y][0], u[x][y][1], wf[x][q], bf[y]);
+            for (int x = 0; x < NT; ++x)
+#pragma unroll
+              for (int y = 0; y < NT; ++y)
+                gmma(u[x][y][0], u[x][y][1], af[x], wf[y][z][e]);  // pad tiles: zero operands
+          }
         }
       }
+      // V += X_i(s)^T U: A[a'][a] = X_i[a][a'] (smem), B[a][c'] = U^T[c'][a] (the C fragments of u)
+#pragma unroll
+      for (int z = 0; z < NT; ++z) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (z < nti0 && !(e == 1 && z == nti0 - 1 && pi0)) {
+            double af[NT];
+#pragma unroll
+            for (int x = 0; x < NT; ++x) af[x] = Xi[ri[z][e] + ci[x]];
+#pragma unroll
+            for (int x = 0; x < NT; ++x)
+#pragma unroll
+              for (int y = 0; y < NT; ++y)
+                gmma(v[x][y][0], v[x][y][1], af[x], u[y][z][e]);
+          }
+        }
+      }
+    }
+    // W_k = V (summed over the cluster's slice ranges, cluster-rank order): C fragments in place
+    if (CS > 1) {
 #pragma unroll
       for (int x = 0; x < NT; ++x)
 #pragma unroll
         for (int y = 0; y < NT; ++y)
-          *reinterpret_cast<double2*>(Up + (8 * x + g) * L + 8 * y + 2 * tg) = make_double2(u[x][y][0], u[x][y][1]);
-      __syncwarp();
-      // V += X_i(s)^T U: A[a'][a] = X_i[a][a'], B[a][c'] = U[a][c']
-#pragma unroll
-      for (int q = 0; q < KT; ++q) {
-        if (q < K4i) {
-          double af[NT], bf[NT];
-#pragma unroll
-          for (int x = 0; x < NT; ++x) af[x] = Xi[(4 * q + tg) * L + 8 * x + g];
-#pragma unroll
-          for (int y = 0; y < NT; ++y) bf[y] = Up[(4 * q + tg) * L + 8 * y + g];
-#pragma unroll
-          for (int x = 0; x < NT; ++x)
-#pragma unroll
-            for (int y = 0; y < NT; ++y) gmma(v[x][y][0], v[x][y][1], af[x], bf[y]);
-        }
-      }
-      __syncwarp();  // U reads done before the next slice overwrites it
-    }
-    // W_k = V (summed over the cluster's slice ranges, cluster-rank order) -> A fragments
-#pragma unroll
-    for (int x = 0; x < NT; ++x)
-#pragma unroll
-      for (int y = 0; y < NT; ++y)
-        *reinterpret_cast<double2*>(Up + (8 * x + g) * L + 8 * y + 2 * tg) = make_double2(v[x][y][0], v[x][y][1]);
-    if (CS > 1) {
+          *reinterpret_cast<double2*>(Up + (8 * x + g) * L + 8 * y + 2 * tg) = make_double2(v[x][y][0], v[x][y][1]);
       cl.sync();  // every CTA's partial is complete
 #pragma unroll
       for (int x = 0; x < NT; ++x)
 #pragma unroll
-        for (int q = 0; q < KT; ++q) {
-          double w = 0.0;
-          for (int c = 0; c < CS; ++c) w += cl.map_shared_rank(Up, c)[(8 * x + g) * L + 4 * q + tg];
-          wf[x][q] = w;
+        for (int y = 0; y < NT; ++y) {
+          double w0 = 0.0, w1 = 0.0;
+          for (int c = 0; c < CS; ++c) {
+            const double2 t = *reinterpret_cast<const double2*>(cl.map_shared_rank(Up, c) + (8 * x + g) * L + 8 * y + 2 * tg);
+            w0 += t.x;
+            w1 += t.y;
+          }
+          wf[x][y][0] = w0;
+          wf[x][y][1] = w1;
         }
-      if (k == d - 1) {
-        double w = 0.0;
-        for (int c = 0; c < CS; ++c) w += cl.map_shared_rank(Up, c)[0];
-        gv = w;
-      }
-      cl.sync();  // partials read everywhere before U is reused
+      cl.sync();  // partials read everywhere before they are rewritten
     } else {
-      __syncwarp();
 #pragma unroll
       for (int x = 0; x < NT; ++x)
 #pragma unroll
-        for (int q = 0; q < KT; ++q) wf[x][q] = Up[(8 * x + g) * L + 4 * q + tg];
-      if (k == d - 1) gv = Up[0];
-      __syncwarp();
+        for (int y = 0; y < NT; ++y) {
+          wf[x][y][0] = v[x][y][0];
+          wf[x][y][1] = v[x][y][1];
+        }
     }
+    if (k == d - 1) gv = wf[0][0][0];
   }
   if (lane == 0 && crank == 0) {
     const int i = i0 + pi, j = j0 + pj;
@@ -314,8 +347,8 @@ static void gram_launch(tt_ctx ctx, const std::vector<const double*>& cores, int
   while (L % 16 != 4 && L % 16 != 12) ++L;
   const size_t smem_m = sizeof(double) * (size_t)(GT_P + 2 * (GT_I + GT_J)) * (8 * NT) * L +
                         sizeof(int2) * (size_t)(GT_I + GT_J) * (8 * NT) * (4 * NT);  // copy list
-  auto kern = NT == 1 ? gram_mma_kernel<1> : NT == 2 ? gram_mma_kernel<2> : NT == 3 ? gram_mma_kernel<3>
-                                                                                  : gram_mma_kernel<4>;
+  auto kern = NT == 1 ? gram_rc_kernel<1> : NT == 2 ? gram_rc_kernel<2> : NT == 3 ? gram_rc_kernel<3>
+                                                                                 : gram_rc_kernel<4>;
   const int T = GM_T;
   TTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m));
   TTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

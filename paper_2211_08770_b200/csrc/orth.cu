@@ -357,7 +357,7 @@ std::vector<tt_tensor> round_independent(tt_ctx ctx, const std::vector<SumInput>
       }
       size_t total = 0;
       for (int k = 0; k < d; ++k) total += (size_t)(rk[(size_t)k] * sums[(size_t)i].n[(size_t)k] * rk[(size_t)k + 1]);
-      bufs.push_back(Q[(size_t)i]->block);
+      bufs.push_back(Q[(size_t)i]->block ? Q[(size_t)i]->block : Q[(size_t)i]->core[0]);  // arena items: cores contiguous
       bytes.push_back(total * sizeof(double));
       roots.push_back(owner[(size_t)i]);
       led.calls++;

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <numeric>
 
+#include "batch_round.cuh"
 #include "gemm.cuh"
 #include "qr.cuh"
 #include "round.cuh"
@@ -355,6 +356,21 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
     inf.norm = norm_of(ctx, t->core[0], in.n[0]);
     inf.scale = inf.norm;
     t->norm = inf.norm;
+    if (info) *info = inf;
+    return t;
+  }
+  // Sums inside the batched engine's shapes (d <= 64, K <= 16, formal ranks <= 64: C1, the Krylov
+  // sets, short Householder sums) run as a one-item batch: the whole rounding is a handful of
+  // one-CTA launches with on-device decisions and a single ranks read-back, where this sweep pays
+  // several launches and host round trips per core.  Same rounding (SURVEY A2/A12
+  // threshold), parity-tested against the oracle like the sweep.  TT_B200_SERIAL_BATCH=0 keeps the
+  // sweep.  Exact rounding (rel_tol = 0) stays on the sweep: the batched engine forms the output
+  // cores as Y V S^-1, which leaves a zero column (not an orthonormal completion) for an exactly
+  // zero singular value that keep_all retains.
+  static const char* sb_env = std::getenv("TT_B200_SERIAL_BATCH");
+  if (!(sb_env && sb_env[0] == '0') && !keep_all && batch_shape_supported(d, K, in.r, nullptr)) {
+    tt_tensor t = nullptr;
+    round_batch_uniform(ctx, std::vector<SumInput>{in}, o, &t, nullptr, &inf);
     if (info) *info = inf;
     return t;
   }
