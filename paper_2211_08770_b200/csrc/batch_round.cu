@@ -1586,17 +1586,17 @@ struct R2LLoader {
     while (l + 1 < K && col >= S->off[kc][l + 1]) ++l;
     return l;
   }
-  __device__ void load(wy::Smem& sm, int q, int w) const {
+  __device__ void load(double* __restrict__ buf, int q, int jb) const {
     const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
     const int i0 = q * ni, nq = min(ni, n - i0);
-    const int c0 = wy::NB * w, c1 = min(c0 + wy::NB, c);
-    wy::zero_cols(sm, w);
+    const int c0 = wy::NB * jb, c1 = min(c0 + wy::NB, c);
+    wy::zero_buf(buf);
     if (last) {
       for (int idx = lane; idx < nq * wy::NB; idx += 32) {
         const int ii = idx / wy::NB, col = c0 + idx % wy::NB;
         if (col < c1) {
           const int l = term(col), a = col - S->off[kc][l];
-          sm.st[col * wy::LD + wy::RR + ii] = coef[l] * __ldg(cores[l * d + kc] + (int64_t)a * n + i0 + ii);
+          buf[(col - c0) * wy::VLD + ii] = coef[l] * __ldg(cores[l * d + kc] + (int64_t)a * n + i0 + ii);
         }
       }
       __syncwarp();
@@ -1641,9 +1641,9 @@ struct R2LLoader {
             const int bp = 8 * (mg + t) + r8;
             if (bp < Rpk) {
               const int ca = 2 * q4;
-              double* dst = sm.st + (int64_t)(c0 + ca) * wy::LD + wy::RR + ii * Rpk + bp;
+              double* dst = buf + ca * wy::VLD + ii * Rpk + bp;
               if (c0 + ca < c1 && a0 + ca < ra) dst[0] = acc[t][0];
-              if (c0 + ca + 1 < c1 && a0 + ca + 1 < ra) dst[wy::LD] = acc[t][1];
+              if (c0 + ca + 1 < c1 && a0 + ca + 1 < ra) dst[wy::VLD] = acc[t][1];
             }
           }
         }
@@ -1661,7 +1661,7 @@ struct R2LLoader {
           const double* lp = L + (int64_t)bp * BR_C + ob;
           double acc = 0.0;
           for (int be = 0; be < rb; ++be) acc += __ldg(lp + be) * __ldg(xp + be);
-          sm.st[col * wy::LD + wy::RR + r] = acc;
+          buf[(col - c0) * wy::VLD + r] = acc;
         }
       }
     }
@@ -1688,11 +1688,11 @@ __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
     // R = A_k exactly (an augmented factorisation with m reflectors for c > m columns would lose
     // the columns whose leading block is rank deficient)
     const int w = tid >> 5;
-    if (8 * w < c) ld.load(sm, 0, w);
+    if (8 * w < c) ld.load(sm.Vb[w], 0, w);
     __syncthreads();
     for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
       const int row = idx / BR_C, col = idx % BR_C;
-      Lout[idx] = (row < rows && col < c) ? sm.st[col * wy::LD + wy::RR + row] : 0.0;
+      Lout[idx] = (row < rows && col < c) ? sm.Vb[col >> 3][(col & 7) * wy::VLD + row] : 0.0;
     }
     return;
   }
@@ -1725,12 +1725,12 @@ struct YLoader {
     }
     return s;
   }
-  __device__ void load(wy::Smem& sm, int q, int w) const {
+  __device__ void load(double* __restrict__ buf, int q, int jb) const {
     const int lane = threadIdx.x & 31;
-    const int rows = crow(q), c0 = wy::NB * w, c1 = min(c0 + wy::NB, cp);
-    wy::zero_cols(sm, w);
+    const int rows = crow(q), c0 = wy::NB * jb, c1 = min(c0 + wy::NB, cp);
+    wy::zero_buf(buf);
     for (int r = lane; r < rows; r += 32)
-      for (int col = c0; col < c1; ++col) sm.st[col * wy::LD + wy::RR + r] = el((int64_t)q * wy::CH + r, col);
+      for (int col = c0; col < c1; ++col) buf[(col - c0) * wy::VLD + r] = el((int64_t)q * wy::CH + r, col);
     __syncwarp();
   }
 };

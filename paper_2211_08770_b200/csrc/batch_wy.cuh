@@ -2,23 +2,29 @@
 // (the batched engine, batch_round.cu).  PAPER.md:69 (rounding = QR sweeps of the core
 // unfoldings), north star "core x R ... as FP64 DMMA tensor-core tiles".
 //
-// Flat tree over row chunks ("stacks"): the CTA keeps a 64-row R block plus one chunk of up to
-// 128 panel rows in shared memory, column-major with ld WY_LD, and factors
+// Flat tree over row chunks ("stacks"): the panel is cut into chunks of up to 128 rows and
 //      [R; chunk]  ->  [R'; 0]
-// with reflectors v = [e_j; v_chunk] (the R block is upper triangular, so a reflector's R part is
-// the unit vector of its own row).  Stack 0 starts from R = 0: the panel is factored as [0; A]
-// (an augmented panel with 64 virtual zero rows on top), so every stack has the same structure;
-// A = Q R with Q = rows 64.. of the product of all reflectors applied to [I; 0] (the virtual rows
-// of that product vanish wherever R has full row rank).
+// is factored per stack with reflectors v = [e_j; v_chunk] (the 64-row R block is upper
+// triangular, so a reflector's R part is the unit vector of its own row).  Stack 0 starts from
+// R = 0: the panel is factored as [0; A] (an augmented panel with 64 virtual zero rows on top), so
+// every stack has the same structure; A = Q R with Q = rows 64.. of the product of all reflectors
+// applied to [I; 0] (the virtual rows of that product vanish wherever R has full row rank).
 //
-// Columns come in blocks of 8; warp w owns column block w.  Per stack, warp w applies the
-// published reflector blocks jb < w to its columns -- W = R[8jb.., blk w] + V_jb^T A_w,
-// W' = T_jb^T W, A_w -= V_jb W', R rows -= W' -- as mma.sync.m8n8k4.f64 tiles (DMMA), then
-// factors its own block (8 reflectors, LAPACK dlarfg arithmetic, the block's 128 x 8 chunk in
-// registers), forms T_w (compact WY: H_1..H_8 = I - V T V^T, T from the DMMA Gram V^T V) and
-// publishes the block through an mbarrier.  So block w+1's factorisation starts as soon as warp
-// w+1 has applied block w, while the other warps still update their columns (look-ahead by
-// construction); there is no CTA-wide barrier inside a stack.
+// Columns come in blocks of 8.  A *cell* (q, jb) -- column block jb of stack q -- is the work of
+// one warp: load the 128 x 8 chunk, apply the published reflector blocks jb' < jb of the stack to
+// it (W = R[8jb'.., blk jb] + V^T A, W' = T^T W, A -= V W', R rows -= W': mma.sync.m8n8k4.f64),
+// factor it (8 reflectors, LAPACK dlarfg arithmetic) with its T (compact WY: H_1..H_8 = I - V T V^T),
+// store V / T into the stack's factor in global memory and publish the cell.  Cell (q, jb) depends
+// on (q, jb' < jb) (their V / T) and on (q - 1, jb) (the R rows of the block): a 2-D wavefront.
+//
+// Decoupled wavefront: the chunk of a cell lives in its warp's REGISTERS as transposed DMMA
+// accumulator fragments (A^T tiles, 8 columns x 8 rows; a C fragment doubles as the A operand of
+// the next product, contracting over its column index, so W^T = A^T V, W'^T = W^T T and
+// A^T -= W'^T V^T chain through registers), shared memory holds only the R block and one staging
+// buffer per warp, and a published block's V / T are read back from global memory (L2) by TMA bulk
+// copies into the consumer's staging buffer.  So nothing ever waits for a consumer: warp w runs its
+// own loop over the stacks, cell (q, (w + q) mod nblk) -- the rotation balances the cells' cost
+// (jb updates + one factorisation) over the warps -- and waits only for pub[jb'] > q.
 //
 // Stored per stack: V_chunk (WY_CH x ncol, column-major ld WY_CH, rows beyond the chunk zero) and
 // T (ncol/8 blocks of 8 x 8, row-major) -- wy_apply applies them to thin targets.
@@ -40,8 +46,10 @@ constexpr int W = T / 32;     // warps
 constexpr int C = 64;         // max columns
 constexpr int NB = 8;         // columns per reflector block
 constexpr int CH = 128;       // max chunk rows per stack
-constexpr int RR = 64;        // R-block rows at the top of the stack
-constexpr int LD = RR + CH + 4;  // smem ld: 196 = 4 (mod 16) spreads the fragment loads over all banks
+constexpr int RR = 64;        // rows of the R block
+constexpr int LD = RR + 4;    // ld of the R block (68 = 4 mod 16)
+constexpr int VLD = CH + 4;   // ld of a staged V block / chunk buffer (132 = 4 mod 16)
+constexpr int VBUF = NB * VLD + 64;  // staging buffer: V block (column-major ld VLD) + T (8 x 8 row-major)
 
 // doubles of one stack's stored factor: V (CH x ncol) + T (ceil(ncol/8) blocks x 64)
 __host__ __device__ inline int64_t stack_doubles(int ncol) {
@@ -49,12 +57,11 @@ __host__ __device__ inline int64_t stack_doubles(int ncol) {
 }
 
 struct Smem {
-  double st[C * LD];      // the stack: column-major, rows 0..63 R block, 64..191 chunk
-  double Tm[C / NB][64];  // T of each block (row-major 8 x 8)
-  double ws[W][64];       // per-warp 8 x 8 scratch (fragment layout changes)
+  double st[C * LD];      // the R block: column-major ld LD, upper triangular (the rest stays zero)
+  double Vb[W][VBUF];     // per-warp staging: the cell's chunk (loader / factorisation) or a staged V + T
   double red[32];
-  uint64_t ready[C / NB]; // block published (32 arrivals: the owner warp's lanes)
-  uint64_t used[C / NB];  // block applied by every later warp (32 arrivals per consumer warp)
+  uint64_t bar[W];        // per-warp TMA completion barrier
+  int pub[C / NB];        // stacks of block jb whose V / T are in global memory (monotone)
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -78,6 +85,26 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
                  : "r"(su32(b)), "r"(parity)
                  : "memory");
   }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pub_store(int* p, int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(su32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int pub_load(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(su32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void pub_wait(const int* p, int need) {
+  while (pub_load(p) < need) __nanosleep(64);
 }
 
 // Sum of eight per-lane values over the warp, every lane gets all eight (transposed butterfly).
@@ -108,71 +135,84 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// Warp w applies published reflector block jb to its column block w (chunk rows < crow).
-__device__ __forceinline__ void update_block(Smem& sm, int jb, int w, int crow) {
+// ---- the cell's chunk as transposed accumulator fragments
+// Lane (r8 = lane >> 2, q4 = lane & 3) keeps a[mt][e] = A[8 mt + P(2 q4 + e)][column r8 of the
+// block], P(s) = s ^ (s >> 2) (slots 4..7 hold rows 5, 4, 7, 6): tile mt is the C fragment of the
+// 8 x 8 tile A^T[column][slot].  The slot permutation makes every staged-V access below hit 16
+// distinct banks per half-warp with the column-major ld VLD = 4 (mod 16).
+__device__ __forceinline__ int slot_row(int s) { return s ^ (s >> 2); }
+
+// buf (column-major ld VLD, 128 x 8) -> fragments
+__device__ __forceinline__ void frag_load(double (&a)[CH / 8][2], const double* __restrict__ buf) {
   const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
-  double* st = sm.st;
-  // W = R[8jb + i][8w + c] + sum_rows V[row][8jb + i] A[row][8w + c]   (C fragment: i = r8, c = 2 q4 + e)
-  double c0 = st[(8 * w + 2 * q4) * LD + 8 * jb + r8];
-  double c1 = st[(8 * w + 2 * q4 + 1) * LD + 8 * jb + r8];
-  double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;  // four independent chains
-  const double* vp = st + (8 * jb + r8) * LD + RR + q4;  // V^T fragment: V[4kk + q4][8jb + r8]
-  const double* ap = st + (8 * w + r8) * LD + RR + q4;   // A fragment:   A[4kk + q4][8w + r8]
-  const int nk = (crow + 3) >> 2;
-  int kk = 0;
-#pragma unroll 2
-  for (; kk + 3 < nk; kk += 4) {
-    dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
-    dmma(e0, e1, vp[4 * kk + 4], ap[4 * kk + 4]);
-    dmma(f0, f1, vp[4 * kk + 8], ap[4 * kk + 8]);
-    dmma(g0, g1, vp[4 * kk + 12], ap[4 * kk + 12]);
+  const double* p = buf + r8 * VLD;
+  const int o0 = slot_row(2 * q4), o1 = slot_row(2 * q4 + 1);
+#pragma unroll
+  for (int mt = 0; mt < CH / 8; ++mt) {
+    a[mt][0] = p[8 * mt + o0];
+    a[mt][1] = p[8 * mt + o1];
   }
-  for (; kk < nk; ++kk) dmma(c0, c1, vp[4 * kk], ap[4 * kk]);
-  c0 += e0 + (f0 + g0);
-  c1 += e1 + (f1 + g1);
-  // W' = T^T W (through the warp scratch: C fragment -> B fragment)
-  double* ws = sm.ws[w];
-  ws[r8 * 8 + 2 * q4] = c0;
-  ws[r8 * 8 + 2 * q4 + 1] = c1;
-  __syncwarp();
-  const double* Tj = sm.Tm[jb];
-  double d0 = 0.0, d1 = 0.0;
-  dmma(d0, d1, Tj[q4 * 8 + r8], ws[q4 * 8 + r8]);
-  dmma(d0, d1, Tj[(4 + q4) * 8 + r8], ws[(4 + q4) * 8 + r8]);
-  __syncwarp();
-  st[(8 * w + 2 * q4) * LD + 8 * jb + r8] -= d0;
-  st[(8 * w + 2 * q4 + 1) * LD + 8 * jb + r8] -= d1;
-  ws[r8 * 8 + 2 * q4] = d0;
-  ws[r8 * 8 + 2 * q4 + 1] = d1;
-  __syncwarp();
-  const double b0 = ws[q4 * 8 + r8], b1 = ws[(4 + q4) * 8 + r8];  // W' as B fragments (k = i)
-  // A_w[chunk] -= V W'   (A fragment: -V[8mt + r8][8jb + q4 (+4)])
-  const int nm = (crow + 7) >> 3;
-#pragma unroll 4
-  for (int mt = 0; mt < nm; ++mt) {
-    double* cp = st + (8 * w + 2 * q4) * LD + RR + 8 * mt + r8;
-    double x0 = cp[0], x1 = cp[LD];
-    const double va = -st[(8 * jb + q4) * LD + RR + 8 * mt + r8];
-    const double vb = -st[(8 * jb + 4 + q4) * LD + RR + 8 * mt + r8];
-    dmma(x0, x1, va, b0);
-    dmma(x0, x1, vb, b1);
-    cp[0] = x0;
-    cp[LD] = x1;
+}
+__device__ __forceinline__ void frag_store(const double (&a)[CH / 8][2], double* __restrict__ buf) {
+  const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
+  double* p = buf + r8 * VLD;
+  const int o0 = slot_row(2 * q4), o1 = slot_row(2 * q4 + 1);
+#pragma unroll
+  for (int mt = 0; mt < CH / 8; ++mt) {
+    p[8 * mt + o0] = a[mt][0];
+    p[8 * mt + o1] = a[mt][1];
   }
-  __syncwarp();
 }
 
-// Warp w factors its column block (reflectors j = 8w + jj, jj < nr), forms T_w, stores V into
-// the chunk rows of its columns; taus on the diagonal of T.  T is built column by column as the
-// reflectors appear (T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) V(:, 0:jj)^T v_jj, lane r keeping row r):
-// the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots v_jj^T a_c (c > jj)
-// and the column mass sigma: one warp reduction per reflector.
+// Apply the block staged in Vs (V column-major ld VLD, T behind it: block jb of the current stack)
+// to the cell's fragments (column block blk): all three products chain through registers.
+__device__ __forceinline__ void update_cell(Smem& sm, const double* __restrict__ Vs, double (&a)[CH / 8][2], int blk,
+                                            int jb) {
+  const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
+  // W^T[c][i] = R[8jb + i][8blk + c] + sum_rows A[row][c] V[row][i]   (C fragment: c = r8, i = 2 q4 + e)
+  double* rp = sm.st + (8 * blk + r8) * LD + 8 * jb;
+  double c0 = rp[2 * q4], c1 = rp[2 * q4 + 1];
+  double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;  // four independent chains
+  const double* v1 = Vs + r8 * VLD;
+  const int o0 = slot_row(2 * q4), o1 = slot_row(2 * q4 + 1);
+#pragma unroll
+  for (int mt = 0; mt < CH / 8; mt += 2) {
+    dmma(c0, c1, a[mt][0], v1[8 * mt + o0]);
+    dmma(e0, e1, a[mt][1], v1[8 * mt + o1]);
+    dmma(f0, f1, a[mt + 1][0], v1[8 * mt + 8 + o0]);
+    dmma(g0, g1, a[mt + 1][1], v1[8 * mt + 8 + o1]);
+  }
+  c0 += e0 + (f0 + g0);
+  c1 += e1 + (f1 + g1);
+  // W'^T[c][i'] = sum_i W^T[c][i] T[i][i'], i' = pi(2 q4 + e) = q4 + 4 e (B fragment column r8 -> i' = pi(r8))
+  const double* Ts = Vs + NB * VLD;
+  const int pr = (r8 >> 1) + 4 * (r8 & 1);
+  double d0 = 0.0, d1 = 0.0;
+  dmma(d0, d1, c0, Ts[(2 * q4) * 8 + pr]);
+  dmma(d0, d1, c1, Ts[(2 * q4 + 1) * 8 + pr]);
+  rp[q4] -= d0;
+  rp[q4 + 4] -= d1;
+  // A^T[c][slot] -= sum_i' W'^T[c][i'] V[row(slot)][i']
+  const double n0 = -d0, n1 = -d1;
+  const double* v2 = Vs + q4 * VLD + slot_row(r8);
+#pragma unroll
+  for (int mt = 0; mt < CH / 8; ++mt) {
+    dmma(a[mt][0], a[mt][1], n0, v2[8 * mt]);
+    dmma(a[mt][0], a[mt][1], n1, v2[4 * VLD + 8 * mt]);
+  }
+}
+
+// The warp factors column block blk of the current stack from buf (its chunk, column-major ld VLD,
+// rows >= the stack's rows zero): reflectors j = 8 blk + jj, T of the block; V (CH x 8, ld CH) and
+// T (8 x 8 row-major) go from the registers to Vout / Tout (global), columns < nr only.  T is built
+// column by column as the reflectors appear (T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) V(:, 0:jj)^T v_jj,
+// lane r keeping row r): the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots
+// v_jj^T a_c (c > jj) and the column mass sigma: one warp reduction per reflector.
 template <bool PROF>
-__device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, long long* fp) {
+__device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict__ buf, int blk, int nr,
+                                             double* __restrict__ Vout, double* __restrict__ Tout, long long* fp) {
   // Columns jj >= nr of a partial block are zero (chunk and R rows), so their steps below are
   // exact no-ops (sigma = alpha = 0: tau = 0, beta = 0): the loop runs all NB steps branch-free.
-  (void)nr;
-  (void)crow;
   const int lane = threadIdx.x & 31;
   long long f0 = PROF ? clock64() : 0, facc[5] = {0, 0, 0, 0, 0};  // phase cycles (flushed at the end)
   auto tick = [&](int slot) {
@@ -187,18 +227,18 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, 
 #pragma unroll
   for (int t = 0; t < 4; ++t)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) x[t][c] = st[(8 * w + c) * LD + RR + 32 * t + lane];  // rows >= crow are 0
+    for (int c = 0; c < NB; ++c) x[t][c] = buf[c * VLD + 32 * t + lane];
   double trow[NB];  // row `lane` of T (lanes 0..7)
 #pragma unroll
   for (int c = 0; c < NB; ++c) trow[c] = 0.0;
 #pragma unroll
   for (int jj = 0; jj < NB; ++jj) {
-    const int j = 8 * w + jj;
+    const int j = 8 * blk + jj;
     // R row j of this block (only reflector jj touches it: loads off the dependency chain)
     const double alpha = st[j * LD + j];
     double rj[NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) rj[c] = c > jj ? st[(8 * w + c) * LD + j] : 0.0;
+    for (int c = 0; c < NB; ++c) rj[c] = c > jj ? st[(8 * blk + c) * LD + j] : 0.0;
     // one reduction for sigma = ||x_jj||^2 (slot jj), the dots x_jj^T a_c (c > jj: the update)
     // and x_jj^T v_c (c < jj: for T), all with the unscaled x_jj
     double dt[NB];
@@ -246,54 +286,49 @@ __device__ __forceinline__ void factor_block(Smem& sm, int w, int nr, int crow, 
     if (lane == 0) {
 #pragma unroll
       for (int c = 0; c < NB; ++c)
-        if (c > jj) st[(8 * w + c) * LD + j] = rj[c];
+        if (c > jj) st[(8 * blk + c) * LD + j] = rj[c];
       st[j * LD + j] = beta;
     }
     tick(3);
   }
-  __syncwarp();
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int c = 0; c < NB; ++c)
+    if (c < nr) {
 #pragma unroll
-    for (int c = 0; c < NB; ++c) st[(8 * w + c) * LD + RR + 32 * t + lane] = x[t][c];
+      for (int t = 0; t < 4; ++t) __stcg(Vout + c * CH + 32 * t + lane, x[t][c]);
+    }
   if (lane < NB) {
 #pragma unroll
-    for (int i = 0; i < NB; ++i) sm.Tm[w][lane * 8 + i] = trow[i];
+    for (int i = 0; i < NB; ++i) __stcg(Tout + lane * 8 + i, trow[i]);
   }
-  __syncwarp();
   tick(4);
   if (PROF && lane == 0)
 #pragma unroll
     for (int i = 0; i < 5; ++i) fp[i] += facc[i];
 }
 
-// Initialise the mbarriers (once per launch, before the first stack) and zero the R block.
+// Zero the R block (all threads; the caller synchronises).
 __device__ __forceinline__ void init(Smem& sm) {
-  const int tid = threadIdx.x;
-  if (tid < C / NB) bar_init(&sm.ready[tid], 32);
-  for (int idx = tid; idx < C * LD; idx += T) sm.st[idx] = 0.0;
-  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (int idx = threadIdx.x; idx < C * LD; idx += T) sm.st[idx] = 0.0;
   __syncthreads();
 }
 
-// Zero the chunk rows (64 .. 191) of every column (before a loader fills them).
-__device__ __forceinline__ void zero_chunk(Smem& sm) {
-  for (int idx = threadIdx.x; idx < C * CH; idx += T) {
-    const int c = idx / CH, r = idx % CH;
-    sm.st[c * LD + RR + r] = 0.0;
-  }
+// Zero a chunk buffer (the warp's staging buffer) before a loader fills it (warp-synchronous).
+__device__ __forceinline__ void zero_buf(double* buf) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+#pragma unroll
+    for (int t = 0; t < CH / 32; ++t) buf[c * VLD + 32 * t + lane] = 0.0;
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- pipelined panel
-// The whole flat tree of a panel with no CTA barrier between stacks: warp w owns column block w
-// and loops over the stacks on its own -- apply the published blocks jb < w of stack q (consumer
-// arrival on used[jb] after each), factor its block, publish it, store its V and T, then (once
-// every later warp has applied its block: used[w]) load its columns of stack q+1 into the chunk
-// rows.  Warp 0 can thus start stack q+1 while the last warps still work on stack q: the stacks
-// flow through the warps as a wavefront (the data a warp reads from others are only the V / T of
-// published blocks; its own columns and their R rows are private to it).
-//   L.stacks(), L.crow(q) (rows of stack q), L.load(sm, q, w) (warp w fills rows 64.. of its
-//   columns for stack q, rows >= crow zero; warp-synchronous), out + q * stack_doubles(ncol).
+// The whole flat tree of a panel, one loop per warp, no CTA barrier between stacks (see the top).
+//   L.stacks(), L.crow(q) (rows of stack q), L.load(buf, q, jb) (the warp fills buf = the 128 x 8
+//   chunk of column block jb of stack q, column-major ld VLD, rows >= crow and columns >= ncol
+//   zero; warp-synchronous), out + q * stack_doubles(ncol).
+// On return (after a CTA barrier) sm.st holds R.
 template <class Loader>
 __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __restrict__ out,
                              long long* __restrict__ prof = nullptr) {
@@ -301,53 +336,64 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
   const int nact = (ncol + NB - 1) / NB;  // active column blocks (all factored: nrefl = ncol)
   const int S = L.stacks();
   const int64_t sd = stack_doubles(ncol);
-  if (tid < C / NB) {
-    bar_init(&sm.ready[tid], 32);
-    bar_init(&sm.used[tid], (uint32_t)(32 * max(1, nact - 1 - tid)));  // every lane of every consumer
-  }
-  for (int idx = tid; idx < C * RR; idx += T) sm.st[(idx / RR) * LD + idx % RR] = 0.0;  // R block = 0
+  if (tid < C / NB) sm.pub[tid] = 0;
+  if (tid < W) bar_init(&sm.bar[tid], 1);
+  for (int idx = tid; idx < C * LD; idx += T) sm.st[idx] = 0.0;  // R block = 0
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   if (w < nact) {
-    // prof (debugging, CTA 0): per warp cycles waiting for blocks, applying them, factoring, and
-    // storing + waiting for the release + loading the next stack
+    // prof (debugging, CTA 0): per warp cycles waiting for blocks (flag + TMA), applying them,
+    // factoring + storing, and loading
     long long t0 = (WY_PROF && prof) ? clock64() : 0, tw = 0, tu = 0, tf = 0, tl = 0;
-    L.load(sm, 0, w);
-    if (WY_PROF && prof) { tl += clock64() - t0; t0 = clock64(); }
+    double* buf = sm.Vb[w];
+    uint32_t ph = 0;
+    // this warp's column block: warps w and w + 4 share an SM sub-partition, so blocks jb and
+    // nact - 1 - jb (few + many updates per cell) are paired there
+    const int jb = w < 4 ? w : nact - 1 - (w - 4);
 #pragma unroll 1
     for (int q = 0; q < S; ++q) {
-      const int crow = L.crow(q);
-      const uint32_t par = (uint32_t)(q & 1);
-#pragma unroll 1
-      for (int jb = 0; jb < w; ++jb) {
-        bar_wait(&sm.ready[jb], par);
-        if (WY_PROF && prof) { const long long t = clock64(); tw += t - t0; t0 = t; }
-        update_block(sm, jb, w, crow);
-        bar_arrive(&sm.used[jb]);
-        if (WY_PROF && prof) { const long long t = clock64(); tu += t - t0; t0 = t; }
-      }
-      if (WY_PROF && prof && w == 3)
-        factor_block<true>(sm, w, min(NB, ncol - NB * w), crow, prof + 32);
-      else
-        factor_block<false>(sm, w, min(NB, ncol - NB * w), crow, nullptr);
-      bar_arrive(&sm.ready[w]);
-      if (WY_PROF && prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
-      // V (CH x 8 of this block, column-major ld CH) and T_w
       double* o = out + (int64_t)q * sd;
-      const int nc = min(NB, ncol - NB * w);
-#pragma unroll 4
-      for (int idx = lane; idx < CH * nc; idx += 32) {
-        const int c = idx / CH, r = idx % CH;
-        o[(int64_t)(NB * w + c) * CH + r] = sm.st[(NB * w + c) * LD + RR + r];
-      }
-      o[(int64_t)CH * ncol + 64 * w + lane] = sm.Tm[w][lane];
-      o[(int64_t)CH * ncol + 64 * w + 32 + lane] = sm.Tm[w][32 + lane];
-      if (q + 1 < S) {
-        if (w < nact - 1) bar_wait(&sm.used[w], par);  // every later warp is done with V_w, T_w
-        __syncwarp();
-        L.load(sm, q + 1, w);
-      }
+      L.load(buf, q, jb);
       if (WY_PROF && prof) { const long long t = clock64(); tl += t - t0; t0 = t; }
+      if (jb > 0) {
+        double a[CH / 8][2];
+        frag_load(a, buf);
+        pub_wait(&sm.pub[jb], q);  // R rows of the block from stack q - 1
+#pragma unroll 1
+        for (int j2 = 0; j2 < jb; ++j2) {
+          pub_wait(&sm.pub[j2], q + 1);
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("fence.proxy.async;" ::: "memory");
+            bar_expect(&sm.bar[w], (uint32_t)((NB * CH + 64) * sizeof(double)));
+            for (int c = 0; c < NB; ++c)
+              bulk_g2s(buf + c * VLD, o + (int64_t)(NB * j2 + c) * CH, CH * sizeof(double), &sm.bar[w]);
+            bulk_g2s(buf + NB * VLD, o + (int64_t)CH * ncol + 64 * j2, 64 * sizeof(double), &sm.bar[w]);
+          }
+          bar_wait(&sm.bar[w], ph);
+          ph ^= 1u;
+          if (WY_PROF && prof) { const long long t = clock64(); tw += t - t0; t0 = t; }
+          update_cell(sm, buf, a, jb, j2);
+          __syncwarp();
+          if (WY_PROF && prof) { const long long t = clock64(); tu += t - t0; t0 = t; }
+        }
+        frag_store(a, buf);
+        __syncwarp();
+      } else {
+        pub_wait(&sm.pub[0], q);
+      }
+      const int nc = min(NB, ncol - NB * jb);
+      double* Vo = o + (int64_t)NB * jb * CH;
+      double* To = o + (int64_t)CH * ncol + 64 * jb;
+      if (WY_PROF && prof && w == 3)
+        factor_block<true>(sm, buf, jb, nc, Vo, To, prof + 32);
+      else
+        factor_block<false>(sm, buf, jb, nc, Vo, To, nullptr);
+      __threadfence();
+      asm volatile("fence.proxy.async;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) pub_store(&sm.pub[jb], q + 1);
+      if (WY_PROF && prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
     }
     if (WY_PROF && prof && lane == 0) {
       prof[4 * w + 0] += tw;
@@ -359,16 +405,6 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
   __syncthreads();
 }
 
-// Zero rows 64.. of warp w's columns (before a loader fills them).
-__device__ __forceinline__ void zero_cols(Smem& sm, int w) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 0; c < NB; ++c)
-#pragma unroll
-    for (int t = 0; t < CH / 32; ++t) sm.st[(NB * w + c) * LD + RR + 32 * t + lane] = 0.0;
-  __syncwarp();
-}
-
 // ---------------------------------------------------------------- applications
 // Q [X; 0] for a factored panel: Q = (stack 0 blocks)(stack 1 blocks)..., each block
 // I - V T V^T, so the last stack's last block is applied first; the target's R-block rows start
@@ -377,7 +413,6 @@ __device__ __forceinline__ void zero_cols(Smem& sm, int w) {
 constexpr int AN = 32;           // target columns per pass
 constexpr int ALD = CH + 4;      // ld of the chunk target (132 = 4 mod 16)
 constexpr int RLD = RR;          // ld of the R-block target (few accesses: no padding)
-constexpr int VLD = CH + 4;      // ld of a staged V block
 constexpr int WLD = AN + 4;      // row stride of W (8 x AN)
 constexpr int NBUF = 2;          // staging ring depth (4 measured no faster on C4: the blocks are L2-resident)
 struct ASmem {
@@ -389,16 +424,6 @@ struct ASmem {
   double Wf[W * 64];             // per-warp 8 x 8 scratch: W' = T W as B fragments
   uint64_t bar[NBUF];
 };
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
-}
 
 __device__ __forceinline__ void apply_init(ASmem& sm) {
   for (int idx = threadIdx.x; idx < NBUF * NB * VLD; idx += T) (&sm.Vs[0][0])[idx] = 0.0;  // never-staged columns

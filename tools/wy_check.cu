@@ -22,12 +22,12 @@ struct RowLoader {  // row-major m x c matrix in stacks of cr rows
   int c, cr;
   __device__ int stacks() const { return (int)((m + cr - 1) / cr); }
   __device__ int crow(int q) const { return (int)(m - (int64_t)q * cr < cr ? m - (int64_t)q * cr : cr); }
-  __device__ void load(wy::Smem& sm, int q, int w) const {
+  __device__ void load(double* __restrict__ buf, int q, int jb) const {
     const int lane = threadIdx.x & 31;
-    wy::zero_cols(sm, w);
+    wy::zero_buf(buf);
     for (int r = lane; r < crow(q); r += 32)
-      for (int col = 8 * w; col < 8 * w + 8 && col < c; ++col)
-        sm.st[col * wy::LD + wy::RR + r] = A[((int64_t)q * cr + r) * c + col];
+      for (int col = 8 * jb; col < 8 * jb + 8 && col < c; ++col)
+        buf[(col - 8 * jb) * wy::VLD + r] = A[((int64_t)q * cr + r) * c + col];
     __syncwarp();
   }
 };
