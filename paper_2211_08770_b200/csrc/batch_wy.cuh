@@ -26,8 +26,9 @@
 // own loop over the stacks, cell (q, (w + q) mod nblk) -- the rotation balances the cells' cost
 // (jb updates + one factorisation) over the warps -- and waits only for pub[jb'] > q.
 //
-// Stored per stack: V_chunk (WY_CH x ncol, column-major ld WY_CH, rows beyond the chunk zero) and
-// T (ncol/8 blocks of 8 x 8, row-major) -- wy_apply applies them to thin targets.
+// Stored per stack and column block: V (WY_CH x 8, column-major ld VLD, rows beyond the chunk and
+// columns beyond the panel zero) and T (8 x 8, row-major) behind it -- wy::apply applies them to
+// thin targets.
 #pragma once
 
 #include "common.cuh"
@@ -51,10 +52,9 @@ constexpr int LD = RR + 4;    // ld of the R block (68 = 4 mod 16)
 constexpr int VLD = CH + 4;   // ld of a staged V block / chunk buffer (132 = 4 mod 16)
 constexpr int VBUF = NB * VLD + 64;  // staging buffer: V block (column-major ld VLD) + T (8 x 8 row-major)
 
-// doubles of one stack's stored factor: V (CH x ncol) + T (ceil(ncol/8) blocks x 64)
-__host__ __device__ inline int64_t stack_doubles(int ncol) {
-  return (int64_t)CH * ncol + 64 * ((ncol + NB - 1) / NB);
-}
+// doubles of one stack's stored factor: one record of VBUF doubles per column block -- V (CH x 8,
+// column-major ld VLD: the staging layout, so a block moves with ONE bulk copy) and its T behind it
+__host__ __device__ inline int64_t stack_doubles(int ncol) { return (int64_t)VBUF * ((ncol + NB - 1) / NB); }
 
 struct Smem {
   double st[C * LD];      // the R block: column-major ld LD, upper triangular (the rest stays zero)
@@ -62,6 +62,7 @@ struct Smem {
   double red[32];
   uint64_t bar[W];        // per-warp TMA completion barrier
   int pub[C / NB];        // stacks of block jb whose V / T are in global memory (monotone)
+  int next;               // next unclaimed cell (wavefront order)
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -203,8 +204,8 @@ __device__ __forceinline__ void update_cell(Smem& sm, const double* __restrict__
 }
 
 // The warp factors column block blk of the current stack from buf (its chunk, column-major ld VLD,
-// rows >= the stack's rows zero): reflectors j = 8 blk + jj, T of the block; V (CH x 8, ld CH) and
-// T (8 x 8 row-major) go from the registers to Vout / Tout (global), columns < nr only.  T is built
+// rows >= the stack's rows zero): reflectors j = 8 blk + jj, T of the block; V (CH x 8, ld VLD) and
+// T (8 x 8 row-major) go from the registers to Vout / Tout (global).  T is built
 // column by column as the reflectors appear (T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) V(:, 0:jj)^T v_jj,
 // lane r keeping row r): the dots v_c^T v_jj (c < jj) ride in the same butterfly as the update dots
 // v_jj^T a_c (c > jj) and the column mass sigma: one warp reduction per reflector.
@@ -291,12 +292,11 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
     }
     tick(3);
   }
+  (void)nr;  // columns >= nr are zero and stored as such (consumers copy whole records)
 #pragma unroll
   for (int c = 0; c < NB; ++c)
-    if (c < nr) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) __stcg(Vout + c * CH + 32 * t + lane, x[t][c]);
-    }
+    for (int t = 0; t < 4; ++t) __stcg(Vout + c * VLD + 32 * t + lane, x[t][c]);
   if (lane < NB) {
 #pragma unroll
     for (int i = 0; i < NB; ++i) __stcg(Tout + lane * 8 + i, trow[i]);
@@ -338,20 +338,34 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
   const int64_t sd = stack_doubles(ncol);
   if (tid < C / NB) sm.pub[tid] = 0;
   if (tid < W) bar_init(&sm.bar[tid], 1);
+  if (tid == 0) sm.next = 0;
   for (int idx = tid; idx < C * LD; idx += T) sm.st[idx] = 0.0;  // R block = 0
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
-  if (w < nact) {
+  {
     // prof (debugging, CTA 0): per warp cycles waiting for blocks (flag + TMA), applying them,
     // factoring + storing, and loading
     long long t0 = (WY_PROF && prof) ? clock64() : 0, tw = 0, tu = 0, tf = 0, tl = 0;
     double* buf = sm.Vb[w];
     uint32_t ph = 0;
-    // this warp's column block: warps w and w + 4 share an SM sub-partition, so blocks jb and
-    // nact - 1 - jb (few + many updates per cell) are paired there
-    const int jb = w < 4 ? w : nact - 1 - (w - 4);
+    // Cells are claimed in wavefront order (anti-diagonals t = q + jb, heavy cells -- large jb --
+    // first): every cell a claimed one depends on has a smaller index, so it is done or in the hands
+    // of a warp that waits for smaller indices only; the warps' loads stay balanced whatever jb costs.
+    const int ncell = S * nact;
+    int td = 0, base = 0;  // current diagonal and the index of its first cell
 #pragma unroll 1
-    for (int q = 0; q < S; ++q) {
+    while (true) {
+      int idx = 0;
+      if (lane == 0) idx = atomicAdd(&sm.next, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx >= ncell) break;
+      while (true) {
+        const int ds = min(S - 1, td) - max(0, td - (nact - 1)) + 1;
+        if (idx < base + ds) break;
+        base += ds;
+        ++td;
+      }
+      const int q = max(0, td - (nact - 1)) + (idx - base), jb = td - q;
       double* o = out + (int64_t)q * sd;
       L.load(buf, q, jb);
       if (WY_PROF && prof) { const long long t = clock64(); tl += t - t0; t0 = t; }
@@ -364,11 +378,9 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
           pub_wait(&sm.pub[j2], q + 1);
           __syncwarp();
           if (lane == 0) {
-            asm volatile("fence.proxy.async;" ::: "memory");
-            bar_expect(&sm.bar[w], (uint32_t)((NB * CH + 64) * sizeof(double)));
-            for (int c = 0; c < NB; ++c)
-              bulk_g2s(buf + c * VLD, o + (int64_t)(NB * j2 + c) * CH, CH * sizeof(double), &sm.bar[w]);
-            bulk_g2s(buf + NB * VLD, o + (int64_t)CH * ncol + 64 * j2, 64 * sizeof(double), &sm.bar[w]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bar_expect(&sm.bar[w], (uint32_t)(VBUF * sizeof(double)));
+            bulk_g2s(buf, o + (int64_t)j2 * VBUF, VBUF * sizeof(double), &sm.bar[w]);
           }
           bar_wait(&sm.bar[w], ph);
           ph ^= 1u;
@@ -382,13 +394,12 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
       } else {
         pub_wait(&sm.pub[0], q);
       }
-      const int nc = min(NB, ncol - NB * jb);
-      double* Vo = o + (int64_t)NB * jb * CH;
-      double* To = o + (int64_t)CH * ncol + 64 * jb;
+      double* Vo = o + (int64_t)jb * VBUF;
+      double* To = Vo + NB * VLD;
       if (WY_PROF && prof && w == 3)
-        factor_block<true>(sm, buf, jb, nc, Vo, To, prof + 32);
+        factor_block<true>(sm, buf, jb, min(NB, ncol - NB * jb), Vo, To, prof + 32);
       else
-        factor_block<false>(sm, buf, jb, nc, Vo, To, nullptr);
+        factor_block<false>(sm, buf, jb, min(NB, ncol - NB * jb), Vo, To, nullptr);
       __threadfence();
       asm volatile("fence.proxy.async;" ::: "memory");
       __syncwarp();
@@ -418,15 +429,13 @@ constexpr int NBUF = 2;          // staging ring depth (4 measured no faster on 
 struct ASmem {
   double Ct[AN * ALD];           // chunk rows of the target (column-major)
   double Rt[AN * RLD];           // R-block rows of the target (column-major)
-  double Vs[NBUF][NB * VLD];     // staged V blocks (column-major), a ring NBUF deep
-  double Ts[NBUF][64];
+  double VT[NBUF][VBUF];         // staged block records (V column-major ld VLD, then T), a ring NBUF deep
   double Wp[W][8 * 12];          // partial W tiles (8 x 8, row stride 12) per (column tile, k-split)
   double Wf[W * 64];             // per-warp 8 x 8 scratch: W' = T W as B fragments
   uint64_t bar[NBUF];
 };
 
 __device__ __forceinline__ void apply_init(ASmem& sm) {
-  for (int idx = threadIdx.x; idx < NBUF * NB * VLD; idx += T) (&sm.Vs[0][0])[idx] = 0.0;  // never-staged columns
   if (threadIdx.x == 0) {
     for (int b = 0; b < NBUF; ++b) bar_init(&sm.bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -436,12 +445,10 @@ __device__ __forceinline__ void apply_init(ASmem& sm) {
 
 // Stage V block jb of the stack factor F (and its T) into buffer b (thread 0).
 __device__ __forceinline__ void stage_block(ASmem& sm, const double* F, int ncol, int jb, int b) {
+  (void)ncol;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  const int nc = min(NB, ncol - NB * jb);
-  bar_expect(&sm.bar[b], (uint32_t)((nc * CH + 64) * sizeof(double)));
-  for (int c = 0; c < nc; ++c)
-    bulk_g2s(sm.Vs[b] + c * VLD, F + (int64_t)(NB * jb + c) * CH, CH * sizeof(double), &sm.bar[b]);
-  bulk_g2s(sm.Ts[b], F + (int64_t)CH * ncol + 64 * jb, 64 * sizeof(double), &sm.bar[b]);
+  bar_expect(&sm.bar[b], (uint32_t)(VBUF * sizeof(double)));
+  bulk_g2s(sm.VT[b], F + (int64_t)jb * VBUF, VBUF * sizeof(double), &sm.bar[b]);
 }
 
 // out[row * rs + col * cs] = (Q [X; 0])[row][col] for the m panel rows, X = src (ncx x nt,
@@ -496,7 +503,7 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
         bar_wait(&sm.bar[b], ph[b]);
         ph[b] ^= 1u;
         tk(0);
-        const double* Vs = sm.Vs[b];
+        const double* Vs = sm.VT[b];
         const bool first = (jb == nbr - 1);
         // ---- W = Rt[8jb + i][:] + V^T Ct (8 x ntp), split over (column tile, k range)
         {
@@ -541,7 +548,7 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
               b0 += sm.Wp[nti * ksp + ks][q4 * 12 + r8];
               b1 += sm.Wp[nti * ksp + ks][(4 + q4) * 12 + r8];
             }
-            const double* Tj = sm.Ts[b];
+            const double* Tj = sm.VT[b] + NB * VLD;
             double d0 = 0.0, d1 = 0.0;
             dmma(d0, d1, Tj[r8 * 8 + q4], b0);
             dmma(d0, d1, Tj[r8 * 8 + 4 + q4], b1);
