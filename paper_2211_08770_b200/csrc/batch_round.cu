@@ -1586,6 +1586,21 @@ struct R2LLoader {
     while (l + 1 < K && col >= S->off[kc][l + 1]) ++l;
     return l;
   }
+  // L2 prefetch of the term-core rows cell (q, jb) will read (issued a cell ahead, before the
+  // previous cell's factorisation)
+  __device__ void prefetch(int q, int jb) const {
+    if (last) return;
+    const int lane = threadIdx.x & 31, r8 = lane & 7;
+    const int i0 = q * ni, nq = min(ni, n - i0);
+    const int c0 = wy::NB * jb;
+    const int l0 = term(c0);
+    const int ra = S->r[l0][kc], rb = S->r[l0][kc + 1], a0 = c0 - S->off[kc][l0];
+    if (a0 + r8 >= ra) return;
+    for (int ii = lane >> 3; ii < nq; ii += 4) {
+      const char* p = reinterpret_cast<const char*>(cores[l0 * d + kc] + ((int64_t)(a0 + r8) * n + i0 + ii) * rb);
+      for (int off = 0; off < rb * 8; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+    }
+  }
   __device__ void load(double* __restrict__ buf, int q, int jb) const {
     const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
     const int i0 = q * ni, nq = min(ni, n - i0);
@@ -1609,41 +1624,86 @@ struct R2LLoader {
       const double* X = cores[l0 * d + kc];
       const int mtiles = (Rpk + 7) >> 3;
       const bool bok = a0 + r8 < ra && c0 + r8 < c1;
-#pragma unroll 1
-      for (int ii = 0; ii < nq; ++ii) {
-        const double* xr = X + ((int64_t)(a0 + r8) * n + i0 + ii) * rb;
+      if (rb <= 16) {
+        // one 16-wide beta slab: the L fragments of a tile group serve every mode index of the
+        // stack -- loaded once per group, then one short X load per mode index
 #pragma unroll 1
         for (int mg = 0; mg < mtiles; mg += 4) {
-          double acc[4][2];
+          double af[4][4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
-#pragma unroll 1
-          for (int be = 0; be < rb; be += 16) {
-            double af[4][4], bf[4];
+          for (int s4 = 0; s4 < 4; ++s4) {
+            const int beta = 4 * s4 + q4;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int bp = 8 * (mg + t) + r8;
+              af[t][s4] = (beta < rb && bp < Rpk) ? __ldg(L + (int64_t)bp * BR_C + ob + beta) : 0.0;
+            }
+          }
+#pragma unroll 2
+          for (int ii = 0; ii < nq; ++ii) {
+            const double* xr = X + ((int64_t)(a0 + r8) * n + i0 + ii) * rb;
+            double bf[4];
 #pragma unroll
             for (int s4 = 0; s4 < 4; ++s4) {
-              const int beta = be + 4 * s4 + q4;
-              const bool kok = beta < rb;
-              bf[s4] = (bok && kok) ? __ldg(xr + beta) : 0.0;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const int bp = 8 * (mg + t) + r8;
-                af[t][s4] = (kok && bp < Rpk) ? __ldg(L + (int64_t)bp * BR_C + ob + beta) : 0.0;
-              }
+              const int beta = 4 * s4 + q4;
+              bf[s4] = (bok && beta < rb) ? __ldg(xr + beta) : 0.0;
             }
+            double acc[4][2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll
             for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
               for (int t = 0; t < 4; ++t) wy::dmma(acc[t][0], acc[t][1], af[t][s4], bf[s4]);
-          }
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int bp = 8 * (mg + t) + r8;
-            if (bp < Rpk) {
-              const int ca = 2 * q4;
-              double* dst = buf + ca * wy::VLD + ii * Rpk + bp;
-              if (c0 + ca < c1 && a0 + ca < ra) dst[0] = acc[t][0];
-              if (c0 + ca + 1 < c1 && a0 + ca + 1 < ra) dst[wy::VLD] = acc[t][1];
+            for (int t = 0; t < 4; ++t) {
+              const int bp = 8 * (mg + t) + r8;
+              if (bp < Rpk) {
+                const int ca = 2 * q4;
+                double* dst = buf + ca * wy::VLD + ii * Rpk + bp;
+                if (c0 + ca < c1 && a0 + ca < ra) dst[0] = acc[t][0];
+                if (c0 + ca + 1 < c1 && a0 + ca + 1 < ra) dst[wy::VLD] = acc[t][1];
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ii = 0; ii < nq; ++ii) {
+          const double* xr = X + ((int64_t)(a0 + r8) * n + i0 + ii) * rb;
+  #pragma unroll 1
+          for (int mg = 0; mg < mtiles; mg += 4) {
+            double acc[4][2];
+  #pragma unroll
+            for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+  #pragma unroll 1
+            for (int be = 0; be < rb; be += 16) {
+              double af[4][4], bf[4];
+  #pragma unroll
+              for (int s4 = 0; s4 < 4; ++s4) {
+                const int beta = be + 4 * s4 + q4;
+                const bool kok = beta < rb;
+                bf[s4] = (bok && kok) ? __ldg(xr + beta) : 0.0;
+  #pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const int bp = 8 * (mg + t) + r8;
+                  af[t][s4] = (kok && bp < Rpk) ? __ldg(L + (int64_t)bp * BR_C + ob + beta) : 0.0;
+                }
+              }
+  #pragma unroll
+              for (int s4 = 0; s4 < 4; ++s4)
+  #pragma unroll
+                for (int t = 0; t < 4; ++t) wy::dmma(acc[t][0], acc[t][1], af[t][s4], bf[s4]);
+            }
+  #pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int bp = 8 * (mg + t) + r8;
+              if (bp < Rpk) {
+                const int ca = 2 * q4;
+                double* dst = buf + ca * wy::VLD + ii * Rpk + bp;
+                if (c0 + ca < c1 && a0 + ca < ra) dst[0] = acc[t][0];
+                if (c0 + ca + 1 < c1 && a0 + ca + 1 < ra) dst[wy::VLD] = acc[t][1];
+              }
             }
           }
         }
@@ -1724,6 +1784,13 @@ struct YLoader {
       for (int be = 0; be < rl; ++be) s += Lr[o + be] * __ldg(xp + be);
     }
     return s;
+  }
+  __device__ void prefetch(int q, int jb) const {
+    if (k == 1) return;
+    const int lane = threadIdx.x & 31;
+    const int rows = crow(q);
+    for (int r = lane; r < rows; r += 32)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(Z + ((int64_t)q * wy::CH + r) * cp + wy::NB * jb));
   }
   __device__ void load(double* __restrict__ buf, int q, int jb) const {
     const int lane = threadIdx.x & 31;

@@ -327,7 +327,7 @@ __device__ __forceinline__ void zero_buf(double* buf) {
 // The whole flat tree of a panel, one loop per warp, no CTA barrier between stacks (see the top).
 //   L.stacks(), L.crow(q) (rows of stack q), L.load(buf, q, jb) (the warp fills buf = the 128 x 8
 //   chunk of column block jb of stack q, column-major ld VLD, rows >= crow and columns >= ncol
-//   zero; warp-synchronous), out + q * stack_doubles(ncol).
+//   zero; warp-synchronous), L.prefetch(q, jb) (L2 prefetch hints for that load), out + q * stack_doubles(ncol).
 // On return (after a CTA barrier) sm.st holds R.
 template <class Loader>
 __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __restrict__ out,
@@ -353,19 +353,25 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
     // of a warp that waits for smaller indices only; the warps' loads stay balanced whatever jb costs.
     const int ncell = S * nact;
     int td = 0, base = 0;  // current diagonal and the index of its first cell
-#pragma unroll 1
-    while (true) {
+    auto claim = [&](int& cq, int& cjb) {  // next cell in wavefront order; false: none left
       int idx = 0;
       if (lane == 0) idx = atomicAdd(&sm.next, 1);
       idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (idx >= ncell) break;
+      if (idx >= ncell) return false;
       while (true) {
         const int ds = min(S - 1, td) - max(0, td - (nact - 1)) + 1;
         if (idx < base + ds) break;
         base += ds;
         ++td;
       }
-      const int q = max(0, td - (nact - 1)) + (idx - base), jb = td - q;
+      cq = max(0, td - (nact - 1)) + (idx - base);
+      cjb = td - cq;
+      return true;
+    };
+    int q = 0, jb = 0, qn = 0, jbn = 0;
+    bool more = claim(q, jb);
+#pragma unroll 1
+    while (more) {
       double* o = out + (int64_t)q * sd;
       L.load(buf, q, jb);
       if (WY_PROF && prof) { const long long t = clock64(); tl += t - t0; t0 = t; }
@@ -396,6 +402,10 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
       }
       double* Vo = o + (int64_t)jb * VBUF;
       double* To = Vo + NB * VLD;
+      // the next cell is claimed before the factorisation so that its operands can be prefetched
+      // (L2) behind it
+      more = claim(qn, jbn);
+      if (more) L.prefetch(qn, jbn);
       if (WY_PROF && prof && w == 3)
         factor_block<true>(sm, buf, jb, min(NB, ncol - NB * jb), Vo, To, prof + 32);
       else
@@ -405,6 +415,8 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
       __syncwarp();
       if (lane == 0) pub_store(&sm.pub[jb], q + 1);
       if (WY_PROF && prof) { const long long t = clock64(); tf += t - t0; t0 = t; }
+      q = qn;
+      jb = jbn;
     }
     if (WY_PROF && prof && lane == 0) {
       prof[4 * w + 0] += tw;

@@ -22,6 +22,7 @@ struct RowLoader {  // row-major m x c matrix in stacks of cr rows
   int c, cr;
   __device__ int stacks() const { return (int)((m + cr - 1) / cr); }
   __device__ int crow(int q) const { return (int)(m - (int64_t)q * cr < cr ? m - (int64_t)q * cr : cr); }
+  __device__ void prefetch(int, int) const {}
   __device__ void load(double* __restrict__ buf, int q, int jb) const {
     const int lane = threadIdx.x & 31;
     wy::zero_buf(buf);
