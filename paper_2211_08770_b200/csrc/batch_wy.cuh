@@ -382,6 +382,7 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
 #pragma unroll 1
         for (int j2 = 0; j2 < jb; ++j2) {
           pub_wait(&sm.pub[j2], q + 1);
+          if (WY_PROF && prof && w == 0 && lane == 0) prof[37] += clock64() - t0;  // flag part of warp 0's wait
           __syncwarp();
           if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -432,18 +433,21 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
 // Q [X; 0] for a factored panel: Q = (stack 0 blocks)(stack 1 blocks)..., each block
 // I - V T V^T, so the last stack's last block is applied first; the target's R-block rows start
 // as X and its chunk rows as 0 per stack (each chunk's rows are touched by its own stack only and
-// are final once that stack is applied).  Target columns in passes of AN; 3 CTAs per SM.
+// are final once that stack is applied).  Target columns in passes of AN.
+//
+// The chunk rows of the target live in REGISTERS as transposed accumulator fragments (C^T tiles,
+// 8 target columns x 8 rows, the slot permutation of frag_load): warp w keeps column tile
+// w mod ntl4 and a 1/ksp share of the rows.  Per block: W^T = Rt^T + C^T V (partial over the warp's
+// rows; the ksp partials of a column tile meet through shared memory -- the one CTA barrier of the
+// block), W'^T = W^T T^T, Rt rows -= W', C^T -= W'^T V^T, all DMMA with the accumulators doubling as
+// A operands.  V / T records arrive by one TMA bulk copy each, one block ahead (ring of NBUF).
 constexpr int AN = 32;           // target columns per pass
-constexpr int ALD = CH + 4;      // ld of the chunk target (132 = 4 mod 16)
 constexpr int RLD = RR;          // ld of the R-block target (few accesses: no padding)
-constexpr int WLD = AN + 4;      // row stride of W (8 x AN)
-constexpr int NBUF = 2;          // staging ring depth (4 measured no faster on C4: the blocks are L2-resident)
+constexpr int NBUF = 2;          // staging ring depth
 struct ASmem {
-  double Ct[AN * ALD];           // chunk rows of the target (column-major)
   double Rt[AN * RLD];           // R-block rows of the target (column-major)
-  double VT[NBUF][VBUF];         // staged block records (V column-major ld VLD, then T), a ring NBUF deep
-  double Wp[W][8 * 12];          // partial W tiles (8 x 8, row stride 12) per (column tile, k-split)
-  double Wf[W * 64];             // per-warp 8 x 8 scratch: W' = T W as B fragments
+  double VT[NBUF][VBUF];         // staged block records (V column-major ld VLD, then T)
+  double Wp[2][W][64];           // partial W^T fragments (lane-major), double-buffered by block parity
   uint64_t bar[NBUF];
 };
 
@@ -455,9 +459,8 @@ __device__ __forceinline__ void apply_init(ASmem& sm) {
   __syncthreads();
 }
 
-// Stage V block jb of the stack factor F (and its T) into buffer b (thread 0).
-__device__ __forceinline__ void stage_block(ASmem& sm, const double* F, int ncol, int jb, int b) {
-  (void)ncol;
+// Stage block jb of the stack factor F into buffer b (thread 0).
+__device__ __forceinline__ void stage_block(ASmem& sm, const double* F, int jb, int b) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   bar_expect(&sm.bar[b], (uint32_t)(VBUF * sizeof(double)));
   bulk_g2s(sm.VT[b], F + (int64_t)jb * VBUF, VBUF * sizeof(double), &sm.bar[b]);
@@ -481,118 +484,106 @@ __device__ void apply(ASmem& sm, uint32_t (&ph)[NBUF], const double* __restrict_
   const int S = (int)((m + cr - 1) / cr);
   const int nbr = (nrefl + NB - 1) / NB;
   const int64_t sd = stack_doubles(ncol);
+  const int tot = S * nbr;
+  const int o0 = slot_row(2 * q4), o1 = slot_row(2 * q4 + 1), pr8 = slot_row(r8);
+  const int pr = (r8 >> 1) + 4 * (r8 & 1);  // i' of B-fragment column r8 (W'^T comes out with i' = q4 + 4 e)
 #pragma unroll 1
   for (int t0 = 0; t0 < nt; t0 += AN) {
     const int ntp = min(AN, nt - t0), ntl = (ntp + 7) >> 3;
-    const int ntl4 = ntl == 3 ? 4 : ntl;               // a divisor of 8: each warp keeps one tile
-    const int ksp = 8 / ntl4;                          // k-splits of the W phase
-    __syncthreads();
+    const int ntl4 = ntl == 3 ? 4 : ntl;  // a divisor of 8: each warp keeps one column tile
+    const int ksp = 8 / ntl4;             // row shares per column tile
+    const int ntile = (CH / 8) / ksp;     // 8-row tiles per warp (2, 4 or 8)
+    const int nti = w % ntl4, rsp = w / ntl4, mt0 = rsp * ntile;
+    const bool on = nti < ntl;
+    __syncthreads();  // the previous pass is done with Rt and the ring
     for (int idx = tid; idx < AN * RR; idx += T) {
       const int c = idx / RR, r = idx % RR;
       sm.Rt[c * RLD + r] = (c < ntp && r < ncx) ? src[(int64_t)(t0 + c) * 64 + r] : 0.0;
     }
+    if (tid == 0) stage_block(sm, F0 + (int64_t)(S - 1) * sd, nbr - 1, 0);
+    __syncthreads();
+    double* rt = sm.Rt + (8 * nti + r8) * RLD;
 #pragma unroll 1
     for (int q = S - 1; q >= 0; --q) {
-      const double* F = F0 + (int64_t)q * sd;
       const int64_t row0 = (int64_t)q * cr;
       const int crow = (int)(m - row0 < cr ? m - row0 : cr);
-      const int nk = (crow + 3) >> 2, nm = (crow + 7) >> 3;
-      for (int idx = tid; idx < AN * CH; idx += T) sm.Ct[(idx / CH) * ALD + idx % CH] = 0.0;
-      __syncthreads();
+      double ct[CH / 16][2];
+#pragma unroll
+      for (int u = 0; u < CH / 16; ++u) ct[u][0] = ct[u][1] = 0.0;
 #pragma unroll 1
       for (int jb = nbr - 1; jb >= 0; --jb) {
-        // block sequence index over the whole pass (stacks descending, blocks descending): the
-        // ring is filled NBUF - 1 blocks ahead, across stack boundaries
-        const int tq = (S - 1 - q) * nbr + (nbr - 1 - jb), tot = S * nbr;
-        if (tid == 0) {
-          for (int u = (tq == 0 ? 0 : tq + NBUF - 1); u <= tq + NBUF - 1 && u < tot; ++u) {
-            const int uq = S - 1 - u / nbr, ujb = nbr - 1 - u % nbr;
-            stage_block(sm, F0 + (int64_t)uq * sd, ncol, ujb, u % NBUF);
-          }
-        }
-        const int b = tq % NBUF;
+        // block sequence index over the whole pass (stacks descending, blocks descending)
+        const int tq = (S - 1 - q) * nbr + (nbr - 1 - jb), b = tq % NBUF;
         tk(4);
         bar_wait(&sm.bar[b], ph[b]);
         ph[b] ^= 1u;
         tk(0);
         const double* Vs = sm.VT[b];
-        const bool first = (jb == nbr - 1);
-        // ---- W = Rt[8jb + i][:] + V^T Ct (8 x ntp), split over (column tile, k range)
-        {
-          const int nti = w / ksp, ks = w % ksp;
-          if (nti < ntl) {
-            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-            if (ks == 0) {
-              c0 = sm.Rt[(8 * nti + 2 * q4) * RLD + 8 * jb + r8];
-              c1 = sm.Rt[(8 * nti + 2 * q4 + 1) * RLD + 8 * jb + r8];
-            }
-            if (!first) {
-              const int k0 = (nk * ks) / ksp, k1 = (nk * (ks + 1)) / ksp;
-              const double* vp = Vs + r8 * VLD + q4;
-              const double* cp = sm.Ct + (8 * nti + r8) * ALD + q4;
-              int kk = k0;
-              double f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
-              for (; kk + 3 < k1; kk += 4) {
-                dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
-                dmma(e0, e1, vp[4 * kk + 4], cp[4 * kk + 4]);
-                dmma(f0, f1, vp[4 * kk + 8], cp[4 * kk + 8]);
-                dmma(g0, g1, vp[4 * kk + 12], cp[4 * kk + 12]);
-              }
-              for (; kk < k1; ++kk) dmma(c0, c1, vp[4 * kk], cp[4 * kk]);
-              e0 += f0 + g0;
-              e1 += f1 + g1;
-            }
-            double* wp = sm.Wp[w];
-            wp[r8 * 12 + 2 * q4] = c0 + e0;
-            wp[r8 * 12 + 2 * q4 + 1] = c1 + e1;
+        // ---- partial W^T[c][i] = Rt[8jb + i][c] (first row share) + sum over the warp's rows C^T V
+        if (on) {
+          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+          if (rsp == 0) {
+            c0 = rt[8 * jb + 2 * q4];
+            c1 = rt[8 * jb + 2 * q4 + 1];
           }
+          if (jb != nbr - 1) {  // (the chunk rows are still zero at a stack's first block)
+            const double* v1 = Vs + r8 * VLD + 8 * mt0;
+#pragma unroll
+            for (int u = 0; u < CH / 16; ++u)
+              if (u < ntile) {
+                dmma(c0, c1, ct[u][0], v1[8 * u + o0]);
+                dmma(e0, e1, ct[u][1], v1[8 * u + o1]);
+              }
+          }
+          *reinterpret_cast<double2*>(&sm.Wp[tq & 1][w][2 * lane]) = make_double2(c0 + e0, c1 + e1);
         }
         tk(1);
         __syncthreads();
         tk(2);
-        // ---- per warp: W' = T W of its column tile (nti = w mod ntl4: the same for every unit of
-        // this warp), R-block rows -= W' (one warp per tile), then C -= V W' over its units
-        {
-          const int nti = w % ntl4;
-          if (nti < ntl) {
-            double b0 = 0.0, b1 = 0.0;
-            for (int ks = 0; ks < ksp; ++ks) {
-              b0 += sm.Wp[nti * ksp + ks][q4 * 12 + r8];
-              b1 += sm.Wp[nti * ksp + ks][(4 + q4) * 12 + r8];
-            }
-            const double* Tj = sm.VT[b] + NB * VLD;
-            double d0 = 0.0, d1 = 0.0;
-            dmma(d0, d1, Tj[r8 * 8 + q4], b0);
-            dmma(d0, d1, Tj[r8 * 8 + 4 + q4], b1);
-            if (w == nti) {
-              sm.Rt[(8 * nti + 2 * q4) * RLD + 8 * jb + r8] -= d0;
-              sm.Rt[(8 * nti + 2 * q4 + 1) * RLD + 8 * jb + r8] -= d1;
-            }
-            double* ws = sm.Wf + w * 64;  // warp-private C -> B fragment exchange
-            ws[r8 * 8 + 2 * q4] = d0;
-            ws[r8 * 8 + 2 * q4 + 1] = d1;
-            __syncwarp();
-            const double f0 = ws[q4 * 8 + r8], f1 = ws[(4 + q4) * 8 + r8];
-#pragma unroll 4
-            for (int u = w; u < nm * ntl4; u += W) {
-              const int mt = u / ntl4;
-              double* cp = sm.Ct + (8 * nti + 2 * q4) * ALD + 8 * mt + r8;
-              double x0 = cp[0], x1 = cp[ALD];
-              dmma(x0, x1, -Vs[q4 * VLD + 8 * mt + r8], f0);
-              dmma(x0, x1, -Vs[(4 + q4) * VLD + 8 * mt + r8], f1);
-              cp[0] = x0;
-              cp[ALD] = x1;
-            }
+        // the ring: block tq + 1 goes into the buffer block tq - 1 used (every warp is past it)
+        if (tid == 0 && tq + 1 < tot) {
+          const int u = tq + 1, uq = S - 1 - u / nbr, ujb = nbr - 1 - u % nbr;
+          stage_block(sm, F0 + (int64_t)uq * sd, ujb, u % NBUF);
+        }
+        if (on) {
+          double s0 = 0.0, s1 = 0.0;
+          for (int ks = 0; ks < ksp; ++ks) {
+            const double2 pv = *reinterpret_cast<const double2*>(&sm.Wp[tq & 1][nti + ks * ntl4][2 * lane]);
+            s0 += pv.x;
+            s1 += pv.y;
           }
+          // W'^T[c][i'] = sum_i W^T[c][i] T[i'][i]
+          const double* Ts = Vs + NB * VLD + pr * 8;
+          double d0 = 0.0, d1 = 0.0;
+          dmma(d0, d1, s0, Ts[2 * q4]);
+          dmma(d0, d1, s1, Ts[2 * q4 + 1]);
+          if (rsp == 0) {
+            rt[8 * jb + q4] -= d0;
+            rt[8 * jb + q4 + 4] -= d1;
+          }
+          const double n0 = -d0, n1 = -d1;
+          const double* v2 = Vs + q4 * VLD + 8 * mt0 + pr8;
+#pragma unroll
+          for (int u = 0; u < CH / 16; ++u)
+            if (u < ntile) {
+              dmma(ct[u][0], ct[u][1], n0, v2[8 * u]);
+              dmma(ct[u][0], ct[u][1], n1, v2[4 * VLD + 8 * u]);
+            }
         }
         tk(3);
-        __syncthreads();
       }
-      for (int idx = tid; idx < ntp * crow; idx += T) {
-        const int c = idx / crow, r = idx % crow;
-        out[(row0 + r) * rs + (int64_t)(t0 + c) * cs] = sm.Ct[c * ALD + r];
+      // the stack's rows are final: registers -> out
+      const int col = 8 * nti + r8;
+      if (on && col < ntp) {
+        double* op = out + (int64_t)(t0 + col) * cs;
+#pragma unroll
+        for (int u = 0; u < CH / 16; ++u)
+          if (u < ntile) {
+            const int ra = 8 * (mt0 + u) + o0, rb = 8 * (mt0 + u) + o1;
+            if (ra < crow) op[(row0 + ra) * rs] = ct[u][0];
+            if (rb < crow) op[(row0 + rb) * rs] = ct[u][1];
+          }
       }
-      __syncthreads();  // every thread is done reading Ct before the next stack zeroes it
     }
   }
   __syncthreads();
