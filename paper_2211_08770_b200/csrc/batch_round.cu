@@ -1871,7 +1871,7 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k)
   }
 }
 
-__global__ void __launch_bounds__(wy::T, 2) br_l2r_apply_wy_kernel(BRArgs A, int k) {
+__global__ void __launch_bounds__(wy::T, 3) br_l2r_apply_wy_kernel(BRArgs A, int k) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   wy::ASmem& sm = *reinterpret_cast<wy::ASmem*>(br_smem_raw);
   const BRShape* S = A.sh;
