@@ -464,7 +464,7 @@ def main():
         traffic = None
     step_s = t_local / args.steps
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "batch_r2l_qr (br_r2l_kernel)",
+            "traffic": traffic, "kernel": "batch_r2l_qr (br_r2l_wy_kernel)",
             "launches": r2l["launches"], "avg_launch_us": 1e3 * r2l["ms"] / max(r2l["launches"], 1),
             "algorithmic_flops_per_launch": r2l_alg / max(r2l["launches"], 1),
             "share_of_kernel_time": r2l["ms"] / total_ms,

@@ -950,7 +950,18 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
   const int kk = nc + (nc & 1);
   bool conv = nc < 2;
 #pragma unroll 1
+  // Squared column norms are kept in n2 across a sweep (a rotation by t = tan(theta) that zeroes
+  // gamma moves them to alpha - t gamma and beta + t gamma) and recomputed exactly when a sweep
+  // starts -- so the sweep that declares convergence (no rotation at all) tests exact norms, and a
+  // rotation costs one dot product and one reduction instead of three.
+  double* n2 = sm.vb[1];
+  const double tol2 = tol * tol;
   for (int sweep = 0; sweep < BR_JAC_SWEEPS && !conv; ++sweep) {
+    for (int j = warp; j < nc; j += BR_W) {
+      const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
+      const double sq = warp_sum(x0 * x0 + x1 * x1);
+      if (lane == 0) n2[j] = sq;
+    }
     if (tid == 0) sm.flag = 0;
     __syncthreads();
 #pragma unroll 1
@@ -973,25 +984,22 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
         x[t] = act ? ca[row] : 0.0;
         y[t] = act ? cb[row] : 0.0;
       }
-      double al = 0.0, be = 0.0, ga = 0.0;
+      const double al = act ? n2[p0] : 0.0, be = act ? n2[p1] : 0.0;
+      double ga = 0.0;
 #pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        al += x[t] * x[t];
-        be += y[t] * y[t];
-        ga += x[t] * y[t];
-      }
+      for (int t = 0; t < RPL; ++t) ga += x[t] * y[t];
 #pragma unroll
-      for (int o = LPP / 2; o > 0; o >>= 1) {
-        al += __shfl_xor_sync(0xffffffffu, al, o);
-        be += __shfl_xor_sync(0xffffffffu, be, o);
-        ga += __shfl_xor_sync(0xffffffffu, ga, o);
-      }
+      for (int o = LPP / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
       const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tail2 || be > tail2) &&
-                       fabs(ga) > tol * sqrt(al * be);
+                       ga * ga > tol2 * (al * be);
       if (rot) {
         const double dd = be - al;
         const double t = (dd >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(dd) + sqrt(dd * dd + 4.0 * ga * ga));
         const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+        if (rl == 0) {
+          n2[p0] = al - t * ga;
+          n2[p1] = be + t * ga;
+        }
         double* va = sm.Aux + p0 * BR_C;
         double* vbp = sm.Aux + p1 * BR_C;
 #pragma unroll

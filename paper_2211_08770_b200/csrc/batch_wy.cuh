@@ -275,7 +275,10 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
       }
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) x[t][jj] *= scal;
+    for (int t = 0; t < 4; ++t) {
+      x[t][jj] *= scal;
+      __stcg(Vout + jj * VLD + 32 * t + lane, x[t][jj]);  // v_jj is final: its store drains behind the chain
+    }
     tick(2);
     {  // T(lane, jj) for lane < jj, T(jj, jj) = tau
       double tv = 0.0;
@@ -293,10 +296,6 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
     tick(3);
   }
   (void)nr;  // columns >= nr are zero and stored as such (consumers copy whole records)
-#pragma unroll
-  for (int c = 0; c < NB; ++c)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) __stcg(Vout + c * VLD + 32 * t + lane, x[t][c]);
   if (lane < NB) {
 #pragma unroll
     for (int i = 0; i < NB; ++i) __stcg(Tout + lane * 8 + i, trow[i]);
