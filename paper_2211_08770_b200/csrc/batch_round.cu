@@ -1581,6 +1581,11 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_apply_kernel(BRArgs A, int k) 
 // (the TT-sum's block-diagonal cores read in place).  A warp fills its own 8 columns: as DMMA tiles
 // (M = b', N = a, K = beta; L from the item's L slot, row-major ld 64, L2-resident) when they belong
 // to one term, else element by element.
+// CTAs per SM of the panel kernels (shared memory: packed R block + PW staging buffers)
+#ifndef WY_PANEL_CTAS
+#define WY_PANEL_CTAS 4
+#endif
+
 struct R2LLoader {
   const BRShape* S;
   const double* const* cores;
@@ -1737,7 +1742,7 @@ struct R2LLoader {
   }
 };
 
-__global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
+__global__ void __launch_bounds__(wy::PT, WY_PANEL_CTAS) br_r2l_wy_kernel(BRArgs A, int kc) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   wy::Smem& sm = *reinterpret_cast<wy::Smem*>(br_smem_raw);
   const BRShape* S = A.sh;
@@ -1755,21 +1760,25 @@ __global__ void __launch_bounds__(wy::T, 2) br_r2l_wy_kernel(BRArgs A, int kc) {
     // fewer rows than columns (one stack): A_k = I_m A_k -- the identity is a valid orthogonal Q and
     // R = A_k exactly (an augmented factorisation with m reflectors for c > m columns would lose
     // the columns whose leading block is rank deficient)
-    const int w = tid >> 5;
-    if (8 * w < c) ld.load(sm.Vb[w], 0, w);
+    const int w = tid >> 5, lane = tid & 31;
+    for (int idx = tid; idx < BR_C * BR_C; idx += wy::PT) Lout[idx] = 0.0;
     __syncthreads();
-    for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
-      const int row = idx / BR_C, col = idx % BR_C;
-      Lout[idx] = (row < rows && col < c) ? sm.Vb[col >> 3][(col & 7) * wy::VLD + row] : 0.0;
+    for (int jb = w; 8 * jb < c; jb += wy::PW) {  // block by block through the warp's staging buffer
+      ld.load(sm.Vb[w], 0, jb);
+      for (int idx = lane; idx < 8 * rows; idx += 32) {
+        const int cc = idx / rows, row = idx % rows, col = 8 * jb + cc;
+        if (col < c) Lout[row * BR_C + col] = sm.Vb[w][cc * wy::VLD + row];
+      }
+      __syncwarp();
     }
     return;
   }
   wy::factor_panel(sm, ld, c, A.V + (int64_t)b * S->vstride + S->voff[kc],
                    (A.dbg && blockIdx.x == 0) ? A.dbg + 32 : nullptr);
   // R (R'_{k-1} x c, row-major ld 64) -> L slot (k & 1)
-  for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
+  for (int idx = tid; idx < BR_C * BR_C; idx += wy::PT) {
     const int row = idx / BR_C, col = idx % BR_C;
-    Lout[idx] = (row < rows && col < c && row <= col) ? sm.st[col * wy::LD + row] : 0.0;
+    Lout[idx] = (row < rows && col < c && row <= col) ? sm.st[wy::ridx(row, col)] : 0.0;
   }
 }
 
@@ -1811,7 +1820,7 @@ struct YLoader {
 };
 
 // Left-to-right QR of a tall Y_k (p > 64 rows, cp columns) with the WY engine; R -> JM.
-__global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k) {
+__global__ void __launch_bounds__(wy::PT, WY_PANEL_CTAS) br_l2r_qr_wy_kernel(BRArgs A, int k) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   wy::Smem& sm = *reinterpret_cast<wy::Smem*>(br_smem_raw);
   const BRShape* S = A.sh;
@@ -1824,9 +1833,9 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k)
   double* out = A.out + (int64_t)b * S->ostride;
   const int n = S->n[kc], cp = S->Rp[k];
   if (k > 1 && sc[3] != 0.0) {  // ||x|| = 0: rank-1 zero tensor
-    for (int i = tid; i < n; i += wy::T) out[S->ooff[kc] + i] = 0.0;
+    for (int i = tid; i < n; i += wy::PT) out[S->ooff[kc] + i] = 0.0;
     if (k + 1 == d)
-      for (int i = tid; i < S->n[d - 1]; i += wy::T) out[S->ooff[d - 1] + i] = 0.0;
+      for (int i = tid; i < S->n[d - 1]; i += wy::PT) out[S->ooff[d - 1] + i] = 0.0;
     if (tid == 0) { rk[k] = 1; if (k + 1 == d) rk[d] = 1; }
     return;
   }
@@ -1836,20 +1845,29 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k)
   const double* Z = A.Z + (int64_t)b * 2 * S->zstride + (k & 1) * S->zstride;
   const double* const* cores = A.cores + (int64_t)gb * K * d;
   YLoader ld{S, Z, Lin + (int64_t)b * 2 * BR_C * BR_C, cores, k, (int)p, cp, K, d};
+  // the 64 x 64 matrix handed to the SVD (column-major ld 64), in the staging area: R of the tall
+  // Y_k unpacked, or a short Y_k itself
+  double* dense = &sm.Vb[0][0];
+  static_assert(sizeof(sm.Vb) >= sizeof(double) * BR_C * BR_C, "staging area holds the dense block");
   if (tall) {
     wy::factor_panel(sm, ld, cp, A.YV + (int64_t)b * S->ystride);
-  } else {
-    wy::init(sm);
-    for (int idx = tid; idx < p * cp; idx += wy::T) {
-      const int r = idx / cp, col = idx % cp;
-      sm.st[col * wy::LD + r] = ld.el(r, col);  // short Y_k: the Jacobi input is Y itself
+    for (int idx = tid; idx < BR_C * BR_C; idx += wy::PT) {
+      const int col = idx / BR_C, row = idx % BR_C;
+      dense[idx] = row <= col ? sm.st[wy::ridx(row, col)] : 0.0;
     }
+  } else {
+    for (int idx = tid; idx < BR_C * BR_C; idx += wy::PT) dense[idx] = 0.0;
     __syncthreads();
+    for (int idx = tid; idx < p * cp; idx += wy::PT) {
+      const int r = idx / cp, col = idx % cp;
+      dense[col * BR_C + r] = ld.el(r, col);  // short Y_k: the Jacobi input is Y itself
+    }
   }
+  __syncthreads();
   if (k == 1) {
     double q = 0.0;
-    for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
-      const double v = sm.st[(idx / BR_C) * wy::LD + idx % BR_C];
+    for (int idx = tid; idx < BR_C * BR_C; idx += wy::PT) {
+      const double v = dense[idx];
       q += v * v;
     }
     const double nrm = sqrt(block_sum(q, sm.red));
@@ -1865,17 +1883,17 @@ __global__ void __launch_bounds__(wy::T, 2) br_l2r_qr_wy_kernel(BRArgs A, int k)
       rk[d] = 1;
     }
     if (nrm == 0.0) {
-      for (int i = tid; i < n; i += wy::T) out[S->ooff[0] + i] = 0.0;
+      for (int i = tid; i < n; i += wy::PT) out[S->ooff[0] + i] = 0.0;
       if (d == 2)
-        for (int i = tid; i < S->n[1]; i += wy::T) out[S->ooff[1] + i] = 0.0;
+        for (int i = tid; i < S->n[1]; i += wy::PT) out[S->ooff[1] + i] = 0.0;
       if (tid == 0) { rk[1] = 1; rk[d] = 1; }
       return;
     }
   }
   double* jm = A.JM + (int64_t)b * BR_C * BR_C;  // column-major ld 64, zero outside
-  for (int idx = tid; idx < BR_C * BR_C; idx += wy::T) {
+  for (int idx = tid; idx < BR_C * BR_C; idx += wy::PT) {
     const int col = idx / BR_C, row = idx % BR_C;
-    jm[idx] = (col < cp && row <= (tall ? col : BR_C)) ? sm.st[col * wy::LD + row] : 0.0;
+    jm[idx] = (col < cp && row <= (tall ? col : BR_C)) ? dense[col * BR_C + row] : 0.0;
   }
 }
 
@@ -2206,7 +2224,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
                                                          : 2.0 * c * mm * mm - 2.0 * mm * mm * mm / 3.0));
         if (use_wy)
           TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
-                  br_r2l_wy_kernel<<<nb, wy::T, smem_wy, ctx->stream>>>(a, kc));
+                  br_r2l_wy_kernel<<<nb, wy::PT, smem_wy, ctx->stream>>>(a, kc));
         else
           TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
                   br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
@@ -2222,7 +2240,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       }
       for (int k = 1; k < d; ++k) {
         if (use_wy)
-          TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_wy_kernel<<<nb, wy::T, smem_wy, ctx->stream>>>(a, k));
+          TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_wy_kernel<<<nb, wy::PT, smem_wy, ctx->stream>>>(a, k));
         else
           TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
         TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_svd_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));

@@ -42,13 +42,18 @@
 namespace ttb {
 namespace wy {
 
-constexpr int T = 256;        // threads per CTA
-constexpr int W = T / 32;     // warps
+constexpr int T = 256;        // threads per CTA of the application kernel
+constexpr int W = T / 32;     // its warps
+#ifndef WY_PT
+#define WY_PT 128
+#endif
+constexpr int PT = WY_PT;     // threads per CTA of the panel factorisation
+constexpr int PW = PT / 32;   // its warps
 constexpr int C = 64;         // max columns
 constexpr int NB = 8;         // columns per reflector block
 constexpr int CH = 128;       // max chunk rows per stack
 constexpr int RR = 64;        // rows of the R block
-constexpr int LD = RR + 4;    // ld of the R block (68 = 4 mod 16)
+constexpr int RT = (C / NB) * (C / NB + 1) / 2 * 64;  // doubles of the packed R block: the 36 upper 8 x 8 tiles
 constexpr int VLD = CH + 4;   // ld of a staged V block / chunk buffer (132 = 4 mod 16)
 constexpr int VBUF = NB * VLD + 64;  // staging buffer: V block (column-major ld VLD) + T (8 x 8 row-major)
 
@@ -56,11 +61,18 @@ constexpr int VBUF = NB * VLD + 64;  // staging buffer: V block (column-major ld
 // column-major ld VLD: the staging layout, so a block moves with ONE bulk copy) and its T behind it
 __host__ __device__ inline int64_t stack_doubles(int ncol) { return (int64_t)VBUF * ((ncol + NB - 1) / NB); }
 
+// Packed R block: tile (bi <= bj) at (bj (bj + 1) / 2 + bi) * 64, column-major inside the tile (the
+// lower part of a diagonal tile stays zero).
+__host__ __device__ inline int ridx(int row, int col) {
+  const int bi = row >> 3, bj = col >> 3;
+  return (bj * (bj + 1) / 2 + bi) * 64 + (col & 7) * 8 + (row & 7);
+}
+
 struct Smem {
-  double st[C * LD];      // the R block: column-major ld LD, upper triangular (the rest stays zero)
-  double Vb[W][VBUF];     // per-warp staging: the cell's chunk (loader / factorisation) or a staged V + T
+  double st[RT];          // the R block, packed upper 8 x 8 tiles (ridx)
+  double Vb[PW][VBUF];    // per-warp staging: the cell's chunk (loader / factorisation) or a staged V + T
   double red[32];
-  uint64_t bar[W];        // per-warp TMA completion barrier
+  uint64_t bar[PW];       // per-warp TMA completion barrier
   int pub[C / NB];        // stacks of block jb whose V / T are in global memory (monotone)
   int next;               // next unclaimed cell (wavefront order)
 };
@@ -171,7 +183,7 @@ __device__ __forceinline__ void update_cell(Smem& sm, const double* __restrict__
                                             int jb) {
   const int lane = threadIdx.x & 31, q4 = lane & 3, r8 = lane >> 2;
   // W^T[c][i] = R[8jb + i][8blk + c] + sum_rows A[row][c] V[row][i]   (C fragment: c = r8, i = 2 q4 + e)
-  double* rp = sm.st + (8 * blk + r8) * LD + 8 * jb;
+  double* rp = sm.st + ridx(8 * jb, 8 * blk + r8);  // rows 8jb .. 8jb + 7 of the column: contiguous in tile (jb, blk)
   double c0 = rp[2 * q4], c1 = rp[2 * q4 + 1];
   double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;  // four independent chains
   const double* v1 = Vs + r8 * VLD;
@@ -224,6 +236,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
     }
   };
   double* st = sm.st;
+  const int db = ridx(8 * blk, 8 * blk);  // the block's diagonal tile
   double x[4][NB];
 #pragma unroll
   for (int t = 0; t < 4; ++t)
@@ -234,12 +247,11 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
   for (int c = 0; c < NB; ++c) trow[c] = 0.0;
 #pragma unroll
   for (int jj = 0; jj < NB; ++jj) {
-    const int j = 8 * blk + jj;
-    // R row j of this block (only reflector jj touches it: loads off the dependency chain)
-    const double alpha = st[j * LD + j];
+    // R row 8 blk + jj of this block (only reflector jj touches it: loads off the dependency chain)
+    const double alpha = st[db + jj * 8 + jj];
     double rj[NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) rj[c] = c > jj ? st[(8 * blk + c) * LD + j] : 0.0;
+    for (int c = 0; c < NB; ++c) rj[c] = c > jj ? st[db + c * 8 + jj] : 0.0;
     // one reduction for sigma = ||x_jj||^2 (slot jj), the dots x_jj^T a_c (c > jj: the update)
     // and x_jj^T v_c (c < jj: for T), all with the unscaled x_jj
     double dt[NB];
@@ -290,8 +302,8 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
     if (lane == 0) {
 #pragma unroll
       for (int c = 0; c < NB; ++c)
-        if (c > jj) st[(8 * blk + c) * LD + j] = rj[c];
-      st[j * LD + j] = beta;
+        if (c > jj) st[db + c * 8 + jj] = rj[c];
+      st[db + jj * 8 + jj] = beta;
     }
     tick(3);
   }
@@ -308,7 +320,7 @@ __device__ __forceinline__ void factor_block(Smem& sm, const double* __restrict_
 
 // Zero the R block (all threads; the caller synchronises).
 __device__ __forceinline__ void init(Smem& sm) {
-  for (int idx = threadIdx.x; idx < C * LD; idx += T) sm.st[idx] = 0.0;
+  for (int idx = threadIdx.x; idx < RT; idx += PT) sm.st[idx] = 0.0;
   __syncthreads();
 }
 
@@ -327,7 +339,7 @@ __device__ __forceinline__ void zero_buf(double* buf) {
 //   L.stacks(), L.crow(q) (rows of stack q), L.load(buf, q, jb) (the warp fills buf = the 128 x 8
 //   chunk of column block jb of stack q, column-major ld VLD, rows >= crow and columns >= ncol
 //   zero; warp-synchronous), L.prefetch(q, jb) (L2 prefetch hints for that load), out + q * stack_doubles(ncol).
-// On return (after a CTA barrier) sm.st holds R.
+// On return (after a CTA barrier) sm.st holds R (packed: ridx).
 template <class Loader>
 __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __restrict__ out,
                              long long* __restrict__ prof = nullptr) {
@@ -336,9 +348,9 @@ __device__ void factor_panel(Smem& sm, const Loader& L, int ncol, double* __rest
   const int S = L.stacks();
   const int64_t sd = stack_doubles(ncol);
   if (tid < C / NB) sm.pub[tid] = 0;
-  if (tid < W) bar_init(&sm.bar[tid], 1);
+  if (tid < PW) bar_init(&sm.bar[tid], 1);
   if (tid == 0) sm.next = 0;
-  for (int idx = tid; idx < C * LD; idx += T) sm.st[idx] = 0.0;  // R block = 0
+  for (int idx = tid; idx < RT; idx += PT) sm.st[idx] = 0.0;  // R block = 0
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   {

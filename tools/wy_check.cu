@@ -33,19 +33,19 @@ struct RowLoader {  // row-major m x c matrix in stacks of cr rows
   }
 };
 
-__global__ void __launch_bounds__(wy::T, 1) factor_kernel(const double* A, int64_t m, int c, int cr, double* F, double* R) {
+__global__ void __launch_bounds__(wy::PT, 1) factor_kernel(const double* A, int64_t m, int c, int cr, double* F, double* R) {
   extern __shared__ __align__(16) unsigned char raw[];
   wy::Smem& sm = *reinterpret_cast<wy::Smem*>(raw);
   RowLoader ld{A, m, c, cr};
   wy::factor_panel(sm, ld, c, F);
-  for (int idx = threadIdx.x; idx < c * c; idx += wy::T) {
+  for (int idx = threadIdx.x; idx < c * c; idx += wy::PT) {
     const int row = idx / c, col = idx % c;
-    R[idx] = row <= col ? sm.st[col * wy::LD + row] : 0.0;
+    R[idx] = row <= col ? sm.st[wy::ridx(row, col)] : 0.0;
   }
 }
 
 // timing: CTA b factors its own m x c matrix (A + b m c); CTA 0 records the per-warp counters
-__global__ void __launch_bounds__(wy::T, 2) time_kernel(const double* A, int64_t m, int c, int cr, double* F,
+__global__ void __launch_bounds__(wy::PT, 2) time_kernel(const double* A, int64_t m, int c, int cr, double* F,
                                                         long long* prof) {
   extern __shared__ __align__(16) unsigned char raw[];
   wy::Smem& sm = *reinterpret_cast<wy::Smem*>(raw);
@@ -74,7 +74,7 @@ static int time_main(int grid) {
   for (int it = 0; it < 3; ++it) {
     cudaMemset(dp, 0, sizeof(long long) * 64);
     cudaEventRecord(e0);
-    time_kernel<<<grid, wy::T, sizeof(wy::Smem)>>>(dA, m, c, cr, dF, dp);
+    time_kernel<<<grid, wy::PT, sizeof(wy::Smem)>>>(dA, m, c, cr, dF, dp);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
   }
@@ -141,7 +141,7 @@ int main(int argc, char** argv) {
     std::vector<double> X(64 * 64, 0.0);
     for (int j = 0; j < k; ++j) X[j * 64 + j] = 1.0;  // column-major ld 64: I_k
     cudaMemcpy(dX, X.data(), sizeof(double) * X.size(), cudaMemcpyHostToDevice);
-    factor_kernel<<<1, wy::T, sizeof(wy::Smem)>>>(dA, m, c, cr, dF, dR);
+    factor_kernel<<<1, wy::PT, sizeof(wy::Smem)>>>(dA, m, c, cr, dF, dR);
     apply_kernel<<<1, wy::T, sizeof(wy::ASmem)>>>(dX, k, k, dF, m, cr, c, dQ);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<double> R((size_t)c * c), Q((size_t)m * k);
