@@ -98,6 +98,7 @@ struct BRArgs {
   int jac_t;                   // tall splits: one-sided Jacobi on R_Y^T (rows of R) instead of R_Y
   int qrcp_svd;                // tall splits: rank-revealing QR of R_Y^T before the Jacobi (truncated)
   int item0;                   // global index of this wave's first item
+  int b0 = 0;                  // first item of this launch inside the wave (half-wave launches)
   long long* dbg;              // TT_B200_BR_DEBUG: CTA 0 phase cycle counters (else null)
 };
 
@@ -897,7 +898,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x, gb = A.item0 + b;
+  const int b = blockIdx.x + A.b0, gb = A.item0 + b;
   const int d = S->d, K = S->K;
   const int k = kc + 1;                 // 1-based core index, 2..d
   const int n = S->n[kc], Rpk = S->Rp[k], c = S->R[k - 1];
@@ -1207,7 +1208,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_l2r_qr_kernel(BRArgs A, int k) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x, gb = A.item0 + b;
+  const int b = blockIdx.x + A.b0, gb = A.item0 + b;
   const int d = S->d, K = S->K;
   const int kc = k - 1;
   const int tid = threadIdx.x;
@@ -1280,7 +1281,7 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   BRSmem& sm = *reinterpret_cast<BRSmem*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x + A.b0;
   const int d = S->d;
   const int kc = k - 1;
   const int tid = threadIdx.x;
@@ -1527,7 +1528,7 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_apply_kernel(BRArgs A, int k) 
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   BRSmemA& sm = *reinterpret_cast<BRSmemA*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x + A.b0;
   const int d = S->d;
   const int kc = k - 1;
   const int tid = threadIdx.x;
@@ -1746,7 +1747,7 @@ __global__ void __launch_bounds__(wy::PT, WY_PANEL_CTAS) br_r2l_wy_kernel(BRArgs
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   wy::Smem& sm = *reinterpret_cast<wy::Smem*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x, gb = A.item0 + b;
+  const int b = blockIdx.x + A.b0, gb = A.item0 + b;
   const int d = S->d, K = S->K;
   const int k = kc + 1;                 // 1-based core index, 2..d
   const int n = S->n[kc], Rpk = S->Rp[k], c = S->R[k - 1];
@@ -1824,7 +1825,7 @@ __global__ void __launch_bounds__(wy::PT, WY_PANEL_CTAS) br_l2r_qr_wy_kernel(BRA
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   wy::Smem& sm = *reinterpret_cast<wy::Smem*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x, gb = A.item0 + b;
+  const int b = blockIdx.x + A.b0, gb = A.item0 + b;
   const int d = S->d, K = S->K;
   const int kc = k - 1;
   const int tid = threadIdx.x;
@@ -1901,7 +1902,7 @@ __global__ void __launch_bounds__(wy::T, 3) br_l2r_apply_wy_kernel(BRArgs A, int
   extern __shared__ __align__(16) unsigned char br_smem_raw[];
   wy::ASmem& sm = *reinterpret_cast<wy::ASmem*>(br_smem_raw);
   const BRShape* S = A.sh;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x + A.b0;
   const int d = S->d;
   const int kc = k - 1;
   const int* rk = A.ranks + (int64_t)b * (d + 1);
@@ -2214,40 +2215,76 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         TTB_CUDA(cudaMemsetAsync(dbg.p, 0, 96 * sizeof(long long), ctx->stream));
       }
       a.dbg = dbg.p;
+      a.b0 = 0;
+      // the whole sweep of one range of the wave's items on one stream
+      auto run_seq = [&](const BRArgs& ah, int nh, cudaStream_t st) {
       for (int kc = d - 1; kc >= 1; --kc) {
-        const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
-        const double c = sh.R[kc];
-        double rl = 0.0;  // panel assembly: 2 r_k^(l) flops per element of term l's columns
-        for (int l = 0; l < K; ++l) rl += (double)sh.r[l][kc] * sh.r[l][kc + 1];
-        const double mm = (double)m;
-        const double fl = nb * (2.0 * mm * rl + (mm >= c ? 2.0 * mm * c * c - 2.0 * c * c * c / 3.0
-                                                         : 2.0 * c * mm * mm - 2.0 * mm * mm * mm / 3.0));
-        if (use_wy)
-          TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
-                  br_r2l_wy_kernel<<<nb, wy::PT, smem_wy, ctx->stream>>>(a, kc));
-        else
-          TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nb * (mm * c) * 2.0,
-                  br_r2l_kernel<<<nb, BR_T, smem, ctx->stream>>>(a, kc));
-        static const char* dump = std::getenv("TT_B200_BR_DUMP");  // debugging: item 0's R factors
-        if (dump && w0 == 0) {
-          std::vector<double> h(BR_C * BR_C);
-          TTB_CUDA(cudaMemcpyAsync(h.data(), L.p + ((kc + 1) & 1) * BR_C * BR_C, sizeof(double) * h.size(),
-                                   cudaMemcpyDeviceToHost, ctx->stream));
-          TTB_CUDA(cudaStreamSynchronize(ctx->stream));
-          FILE* f = std::fopen(dump, kc == d - 1 ? "wb" : "ab");
-          if (f) { std::fwrite(h.data(), sizeof(double), h.size(), f); std::fclose(f); }
+          const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
+          const double c = sh.R[kc];
+          double rl = 0.0;  // panel assembly: 2 r_k^(l) flops per element of term l's columns
+          for (int l = 0; l < K; ++l) rl += (double)sh.r[l][kc] * sh.r[l][kc + 1];
+          const double mm = (double)m;
+          const double fl = nh * (2.0 * mm * rl + (mm >= c ? 2.0 * mm * c * c - 2.0 * c * c * c / 3.0
+                                                           : 2.0 * c * mm * mm - 2.0 * mm * mm * mm / 3.0));
+          if (use_wy)
+            TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nh * (mm * c) * 2.0,
+                    br_r2l_wy_kernel<<<nh, wy::PT, smem_wy, st>>>(ah, kc));
+          else
+            TTB_RUN(ctx, "batch_r2l_qr", fl, 8.0 * nh * (mm * c) * 2.0,
+                    br_r2l_kernel<<<nh, BR_T, smem, st>>>(ah, kc));
+          static const char* dump = std::getenv("TT_B200_BR_DUMP");  // debugging: item 0's R factors
+          if (dump && w0 == 0) {
+            std::vector<double> h(BR_C * BR_C);
+            TTB_CUDA(cudaMemcpyAsync(h.data(), L.p + ((kc + 1) & 1) * BR_C * BR_C, sizeof(double) * h.size(),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+            TTB_CUDA(cudaStreamSynchronize(ctx->stream));
+            FILE* f = std::fopen(dump, kc == d - 1 ? "wb" : "ab");
+            if (f) { std::fwrite(h.data(), sizeof(double), h.size(), f); std::fclose(f); }
+          }
         }
-      }
-      for (int k = 1; k < d; ++k) {
-        if (use_wy)
-          TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_wy_kernel<<<nb, wy::PT, smem_wy, ctx->stream>>>(a, k));
-        else
-          TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
-        TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_svd_kernel<<<nb, BR_T, smem_q, ctx->stream>>>(a, k));
-        if (use_wy)
-          TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_wy_kernel<<<nb, wy::T, smem_wya, ctx->stream>>>(a, k));
-        else
-          TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nb, BR_T, smem_a, ctx->stream>>>(a, k));
+        for (int k = 1; k < d; ++k) {
+          if (use_wy)
+            TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_wy_kernel<<<nh, wy::PT, smem_wy, st>>>(ah, k));
+          else
+            TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_kernel<<<nh, BR_T, smem_q, st>>>(ah, k));
+          TTB_RUN(ctx, "batch_l2r_svd", 0.0, 0.0, br_l2r_svd_kernel<<<nh, BR_T, smem_q, st>>>(ah, k));
+          if (use_wy)
+            TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_wy_kernel<<<nh, wy::T, smem_wya, st>>>(ah, k));
+          else
+            TTB_RUN(ctx, "batch_l2r_apply", 0.0, 0.0, br_l2r_apply_kernel<<<nh, BR_T, smem_a, st>>>(ah, k));
+        }
+      };
+      // The wave in two (TT_B200_BR_SPLIT) parts on as many streams (items are independent): when a kernel of one half drains its
+      // last CTAs, the SMs it leaves take CTAs of the other half's kernel instead of idling, and
+      // kernels with different bottlenecks (DMMA applications, latency-bound Jacobi) share SMs.
+      // One stream when per-kernel timing (tt_ctx_profile), debugging or the dump is on.
+      static const char* split_env = std::getenv("TT_B200_BR_SPLIT");  // parts (1 = off), default 2
+      int parts = split_env ? std::atoi(split_env) : 2;
+      parts = std::max(1, std::min(parts, 4));
+      const bool split = use_wy && parts > 1 && !ctx->prof && !ctx->debug_sync && !dbg.p && nb >= 16 * ctx->num_sms &&
+                         !std::getenv("TT_B200_BR_DUMP");
+      if (split) {
+        if (!ctx->br_fork) TTB_CUDA(cudaEventCreateWithFlags(&ctx->br_fork, cudaEventDisableTiming));
+        for (int i = 0; i + 1 < parts; ++i)
+          if (!ctx->br_aux[i]) {
+            TTB_CUDA(cudaStreamCreateWithFlags(&ctx->br_aux[i], cudaStreamNonBlocking));
+            TTB_CUDA(cudaEventCreateWithFlags(&ctx->br_join[i], cudaEventDisableTiming));
+          }
+        TTB_CUDA(cudaEventRecord(ctx->br_fork, ctx->stream));
+        for (int i = 0; i < parts; ++i) {
+          const int lo = (int)((int64_t)nb * i / parts), hi = (int)((int64_t)nb * (i + 1) / parts);
+          BRArgs ai = a;
+          ai.b0 = lo;
+          cudaStream_t st = i == 0 ? ctx->stream : ctx->br_aux[i - 1];
+          if (i > 0) TTB_CUDA(cudaStreamWaitEvent(st, ctx->br_fork, 0));
+          run_seq(ai, hi - lo, st);
+          if (i > 0) {
+            TTB_CUDA(cudaEventRecord(ctx->br_join[i - 1], st));
+          }
+        }
+        for (int i = 0; i + 1 < parts; ++i) TTB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->br_join[i], 0));
+      } else {
+        run_seq(a, nb, ctx->stream);
       }
       if (dbg.p) {
         long long h[96];

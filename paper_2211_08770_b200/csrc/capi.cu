@@ -172,6 +172,11 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
   if (ctx->scratch) { cudaStreamSynchronize(ctx->stream); cudaFree(ctx->scratch); }
   host_pipe_release(ctx);
   comm_release(ctx);
+  for (int i = 0; i < 3; ++i) {
+    if (ctx->br_aux[i]) { cudaStreamSynchronize(ctx->br_aux[i]); cudaStreamDestroy(ctx->br_aux[i]); }
+    if (ctx->br_join[i]) cudaEventDestroy(ctx->br_join[i]);
+  }
+  if (ctx->br_fork) cudaEventDestroy(ctx->br_fork);
   delete ctx;
   return TT_OK;
 }

@@ -74,6 +74,10 @@ struct tt_ctx_s {
   // (one per direction: the two directions use different copy engines) and two device staging
   // buffers, so repeated calls allocate nothing
   cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
+  // batched engine: second stream for the other half of a wave (kernel tails of one half fill with
+  // the other half's CTAs) and its fork / join events
+  cudaStream_t br_aux[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t br_fork = nullptr, br_join[3] = {nullptr, nullptr, nullptr};
   double* hp_stage[2] = {nullptr, nullptr};
   size_t hp_stage_doubles = 0;
   // optional communicator (comm.cu): sharded Gram / dot batches / phase-2 roundings
