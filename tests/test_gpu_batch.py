@@ -325,3 +325,57 @@ def test_batch_c4_full_size_bench_config():
         refx = tt.tt_sum(terms[:2], [1.0, 1.0]) if b % 2 == 0 else terms[0]
         assert diff_norm(g, refx) <= 5e-9 * np.sqrt(2.0)
         _check_item(g, list(res.ranks[b]), terms, list(coeffs[b]), 1e-6, rounding.DEFAULT_FLOOR_C, norms=[1.0] * 4)
+
+
+@pytest.mark.parametrize("case", ["wide_terms", "five_blocks", "one_block", "odd_ranks"])
+def test_batch_panel_engine_paths(case):
+    """Shapes that steer the compact-WY panel engine (csrc/batch_wy.cuh) through each of its paths,
+    all with several 128-row stacks and a ragged last one: term ranks above 16 (the loader's general
+    beta-slab loop), 5 and 1 column blocks (cell order with fewer blocks than warps / a single
+    chain), column blocks that straddle two terms and ranks that are no multiples of 8."""
+    import paper_2211_08770_b200 as P
+    rng = _rng({"wide_terms": 71, "five_blocks": 72, "one_block": 73, "odd_ranks": 74}[case])
+    if case == "wide_terms":      # R = 60: two terms of rank 30, panels 37 * 60 = 2220 rows
+        d, n, ranks = 4, [9, 37, 37, 6], [[1, 9, 30, 6, 1], [1, 9, 30, 6, 1]]
+    elif case == "five_blocks":   # R_2 = 38: 5 column blocks, the last one partial
+        d, n, ranks = 4, [12, 33, 29, 12], [[1, 12, 19, 12, 1], [1, 12, 19, 12, 1]]
+    elif case == "one_block":     # R <= 8: one column block, one warp chain per stack
+        d, n, ranks = 4, [5, 40, 40, 5], [[1, 3, 4, 3, 1], [1, 3, 4, 3, 1]]
+    else:                         # three terms, blocks straddling terms, R'_k % 8 != 0
+        d, n, ranks = 5, [6, 23, 31, 17, 5], [[1, 5, 11, 7, 4, 1], [1, 3, 13, 9, 5, 1], [1, 6, 7, 10, 3, 1]]
+    K = len(ranks)
+    items = []
+    for b in range(3):
+        terms = [make_random_tt(d, n, r, rng) for r in ranks]
+        coeffs = [float(v) for v in rng.standard_normal(K)]
+        if b == 2 and ranks[0] == ranks[1]:  # near cancellation of the first two terms
+            terms[1] = terms[0]
+            coeffs[1] = -coeffs[0] * (1.0 - 2.0 ** -20)
+        items.append((terms, coeffs))
+    cores, coeffs = _stack(items)
+    for delta in (1e-9, 1e-3):
+        res = P.tt_round_batch_strided(ctx(), cores, coeffs, delta)
+        for b, (terms, cf) in enumerate(items):
+            _check_item(res.item_numpy(b), list(res.ranks[b]), terms, cf, delta, rounding.DEFAULT_FLOOR_C)
+
+
+def test_batch_two_stream_wave_small_items():
+    """A wave large enough to run as two halves on two streams (>= 16 x SMs items), with small
+    ragged items: a sample from both halves and the seam against the oracle, and every item's
+    ranks against a second call (bitwise reproducible: the cell scheduler orders work only)."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(75)
+    B, d, n = 2600, 3, [6, 21, 5]
+    ranks = [[1, 5, 4, 1], [1, 4, 5, 1]]
+    items = []
+    for b in range(B):
+        terms = [make_random_tt(d, n, r, rng) for r in ranks]
+        items.append((terms, [1.0, float(rng.standard_normal())]))
+    cores, coeffs = _stack(items)
+    res = P.tt_round_batch_strided(ctx(), cores, coeffs, 1e-8)
+    res2 = P.tt_round_batch_strided(ctx(), cores, coeffs, 1e-8)
+    assert np.array_equal(res.ranks, res2.ranks)
+    for b in (0, 1, 1299, 1300, 1301, 2599):
+        g = res.item_numpy(b)
+        assert all(np.array_equal(x, y) for x, y in zip(g, res2.item_numpy(b)))
+        _check_item(g, list(res.ranks[b]), items[b][0], items[b][1], 1e-8, rounding.DEFAULT_FLOOR_C)
