@@ -97,6 +97,7 @@ struct BRArgs {
   int keep_all;
   int jac_t;                   // tall splits: one-sided Jacobi on R_Y^T (rows of R) instead of R_Y
   int qrcp_svd;                // tall splits: rank-revealing QR of R_Y^T before the Jacobi (truncated)
+  int jac_lpp;                 // lanes per Jacobi column pair (0: by the pair count; TT_B200_BR_JLPP)
   int item0;                   // global index of this wave's first item
   int b0 = 0;                  // first item of this launch inside the wave (half-wave launches)
   long long* dbg;              // TT_B200_BR_DEBUG: CTA 0 phase cycle counters (else null)
@@ -957,13 +958,20 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
   // rotation costs one dot product and one reduction instead of three.
   double* n2 = sm.vb[1];
   const double tol2 = tol * tol;
+  // A sweep whose rotations were all tiny also ends the iteration (no confirming sweep): with
+  // rho_ij = |<c_i, c_j>| / (||c_i|| ||c_j||), a rotation of (p, q) moves rho_pj by at most
+  // kappa rho_qj, kappa = |sin| max(||c_p|| / ||c_q||, ||c_q|| / ||c_p||).  If every pair had
+  // rho <= e at its visit and every rotation kappa <= e, e^2 = tol / (32 kk), then no rho exceeds
+  // 2 e during the sweep (2 kk e << 1) and each drifts by at most 2 kk e 2 e = tol / 8 after its
+  // visit: all pairs end at <= 1.125 tol (A23).
+  const double tiny2 = tol / (32.0 * (double)kk);
   for (int sweep = 0; sweep < BR_JAC_SWEEPS && !conv; ++sweep) {
     for (int j = warp; j < nc; j += BR_W) {
       const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
       const double sq = warp_sum(x0 * x0 + x1 * x1);
       if (lane == 0) n2[j] = sq;
     }
-    if (tid == 0) sm.flag = 0;
+    if (tid == 0) { sm.flag = 0; sm.rho = 0; }  // sm.rho: a rotation of this sweep was not tiny (below)
     __syncthreads();
 #pragma unroll 1
     for (int r = 0; r < kk - 1; ++r) {
@@ -973,7 +981,11 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
       const int q = warp + pp * BR_W;
       int p0, p1;
       if (q == 0) { p0 = kk - 1; p1 = r; }
-      else { p0 = (r + q) % (kk - 1); p1 = (r + kk - 1 - q) % (kk - 1); }
+      else {  // (r + q) mod (kk - 1) and (r - q) mod (kk - 1): both sums lie below 2 (kk - 1)
+        p0 = r + q; p1 = r + kk - 1 - q;
+        if (p0 >= kk - 1) p0 -= kk - 1;
+        if (p1 >= kk - 1) p1 -= kk - 1;
+      }
       if (p0 > p1) { const int t = p0; p0 = p1; p1 = t; }
       const bool act = q < kk / 2 && p1 < nc && pp < NPW;
       double* ca = sm.Rs + (act ? p0 : 0) * BR_C;
@@ -993,10 +1005,19 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
       for (int o = LPP / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
       const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tail2 || be > tail2) &&
                        ga * ga > tol2 * (al * be);
+      bool big = false;
       if (rot) {
+        // tan(2 theta) = 2 gamma / (beta - alpha), the smaller angle: with h = hypot(dd, 2 gamma),
+        // cos^2 = (1 + |dd| / h) / 2, sin = sgn gamma / (h cos), t = sin / cos -- no cancellation in
+        // either, and two reciprocal square roots in sequence instead of sqrt -> divide -> rsqrt
         const double dd = be - al;
-        const double t = (dd >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(dd) + sqrt(dd * dd + 4.0 * ga * ga));
-        const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+        const double gs = dd >= 0.0 ? ga : -ga;
+        const double rh = rsqrt(dd * dd + 4.0 * ga * ga);
+        const double c2 = 0.5 + 0.5 * (fabs(dd) * rh);
+        const double rc = rsqrt(c2);
+        const double cs = c2 * rc, sn = (gs * rh) * rc;
+        const double t = sn * rc;
+        big = ga * ga > tiny2 * (al * be) || sn * sn * fmax(al, be) > tiny2 * fmin(al, be);
         if (rl == 0) {
           n2[p0] = al - t * ga;
           n2[p1] = be + t * ga;
@@ -1015,17 +1036,20 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
           }
         }
       }
-      if (__any_sync(0xffffffffu, rot) && lane == 0) sm.flag = 1;
+      if (__any_sync(0xffffffffu, rot)) {
+        const bool anybig = __any_sync(0xffffffffu, big);
+        if (lane == 0) { sm.flag = 1; if (anybig) sm.rho = 1; }
+      }
       __syncthreads();
     }
-    conv = (sm.flag == 0);
+    conv = (sm.flag == 0) || (sm.rho == 0);
     if (nsweeps && tid == 0) *nsweeps += 1;
     __syncthreads();
   }
   return conv;
 }
 
-__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail2, long long* nsweeps = nullptr) {
+__device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail2, int lpp, long long* nsweeps = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) sm.Aux[idx] = (idx % BR_C == idx / BR_C) ? 1.0 : 0.0;
   const double tol = sqrt((double)max(rows, 1)) * U_ROUND;
@@ -1038,8 +1062,13 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
   __syncthreads();
   const int pairs = (nc + (nc & 1)) / 2;
   bool conv;
-  if (pairs <= BR_W) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, nsweeps);
-  else if (pairs <= 2 * BR_W) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, nsweeps);
+  // lpp = 0: the widest layout whose pairs fill the 8 warps (shortest round); lpp = 8 / 16 / 32
+  // forces a layout (fewer, fuller warps issue fewer instructions per round: TT_B200_BR_JLPP)
+  if (lpp == 0) lpp = pairs <= BR_W ? 32 : pairs <= 2 * BR_W ? 16 : 8;
+  if (lpp == 32 && pairs > BR_W) lpp = 16;
+  if (lpp == 16 && pairs > 2 * BR_W) lpp = 8;
+  if (lpp == 32) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, nsweeps);
+  else if (lpp == 16) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, nsweeps);
   else conv = br_jacobi_rounds<8>(sm, nc, tol, negl, tail2, nsweeps);
   // singular values = column norms, sorted descending (ties: lower column first)
   for (int j = warp; j < nc; j += BR_W) {
@@ -1326,7 +1355,7 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
       sm.Rs[idx] = (i < kq && j < cp && j >= i) ? qx[j * BR_C + i] : 0.0;
     }
     __syncthreads();
-    const bool conv = kq < 1 || br_jacobi(sm, cp, kq, tau * tau / (double)(kq > 0 ? kq : 1),
+    const bool conv = kq < 1 || br_jacobi(sm, cp, kq, tau * tau / (double)(kq > 0 ? kq : 1), A.jac_lpp,
                                           (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
     if (prof) { const long long t = clock64(); A.dbg[81] += t - pt; pt = t; }
     if (tid == 0) {
@@ -1419,7 +1448,7 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
   const long long cj0 = clock64();
   static_assert(BR_C == 64, "tail2 below assumes nc <= 64");
   const double tail2 = (A.keep_all || A.max_rank > 0) ? 0.0 : sc[1] * sc[1] / (double)(cp > 0 ? cp : 1);
-  const bool conv = br_jacobi(sm, jrows, cp, tail2, (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
+  const bool conv = br_jacobi(sm, jrows, cp, tail2, A.jac_lpp, (A.dbg && blockIdx.x == 0) ? A.dbg + 11 : nullptr);
   if (A.dbg && blockIdx.x == 0 && tid == 0) A.dbg[8] += clock64() - cj0;
   if (tid == 0) {
     if (!conv) A.info[b] = 1;
@@ -2206,6 +2235,9 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         a.jac_t = (jt && jt[0] == '0') ? 0 : 1;
         static const char* qs = std::getenv("TT_B200_BR_QRCP");
         a.qrcp_svd = (qs && qs[0] == '0') ? 0 : 1;
+        static const char* jl = std::getenv("TT_B200_BR_JLPP");
+        const int jlv = jl ? std::atoi(jl) : 0;
+        a.jac_lpp = (jlv == 8 || jlv == 16 || jlv == 32) ? jlv : 0;
       }
       a.item0 = w0;
       const char* dbe = std::getenv("TT_B200_BR_DEBUG");
