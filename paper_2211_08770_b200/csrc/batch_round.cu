@@ -2025,6 +2025,7 @@ void batch_desc_shape(BatchDesc& in, int B, int K, int d, const int64_t* n, cons
 }
 
 void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut& res) {
+  TTB_RANGE("tt_round_batch");
   const char* hdbg = std::getenv("TT_B200_BR_DEBUG");
   const bool hd = hdbg && hdbg[0] == '1';
   const auto t_start = std::chrono::steady_clock::now();
@@ -2250,6 +2251,7 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
       a.b0 = 0;
       // the whole sweep of one range of the wave's items on one stream
       auto run_seq = [&](const BRArgs& ah, int nh, cudaStream_t st) {
+      nvtxRangePushA("tt_round_batch: right-to-left orthogonalisation");
       for (int kc = d - 1; kc >= 1; --kc) {
           const int64_t m = (int64_t)sh.n[kc] * sh.Rp[kc + 1];
           const double c = sh.R[kc];
@@ -2274,6 +2276,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
             if (f) { std::fwrite(h.data(), sizeof(double), h.size(), f); std::fclose(f); }
           }
         }
+        nvtxRangePop();
+        TTB_RANGE("tt_round_batch: left-to-right truncation");
         for (int k = 1; k < d; ++k) {
           if (use_wy)
             TTB_RUN(ctx, "batch_l2r_qr", 0.0, 0.0, br_l2r_qr_wy_kernel<<<nh, wy::PT, smem_wy, st>>>(ah, k));

@@ -2,6 +2,7 @@
 // warp/block reductions.  sm_100a only.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,6 +24,18 @@ struct Error {
 void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 #define TTB_CUDA(x) ::ttb::check_cuda((x), #x, __FILE__, __LINE__)
 #define TTB_LAUNCHED(ctx) do { (ctx)->launches++; TTB_CUDA(cudaGetLastError()); } while (0)
+// NVTX range (one range per rounding phase and driver step; header-only NVTX3, a
+// no-op unless a profiler is attached): TTB_RANGE("name") covers the enclosing scope.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define TTB_RANGE_CAT2(a, b) a##b
+#define TTB_RANGE_CAT(a, b) TTB_RANGE_CAT2(a, b)
+#define TTB_RANGE(name) ::ttb::NvtxRange TTB_RANGE_CAT(_ttb_range_, __LINE__)(name)
+
 // Profiled launch: TTB_RUN(ctx, "class", flops, bytes, kernel<<<...>>>(...));
 #define TTB_RUN(ctx, cls, fl, by, ...)                      \
   do {                                                      \

@@ -305,6 +305,7 @@ double round_cost_model(const SumInput& in) {
 // every rank returns every q_i.  The ledger records the calls in index order (Table 1 counts).
 std::vector<tt_tensor> round_independent(tt_ctx ctx, const std::vector<SumInput>& sums, const tt_round_opts& o,
                                          Ledger& led) {
+  TTB_RANGE("tt_orth: phase-2 independent roundings");
   const int m = (int)sums.size();
   std::vector<tt_tensor> Q((size_t)m, nullptr);
   auto free_all = [&] {
@@ -444,6 +445,8 @@ void run_gs(tt_ctx ctx, tt_orth_kind kind, int m, const std::vector<TTRef>& A, c
   const bool modified = (kind == TT_MGS || kind == TT_MGS2);
   std::vector<TTRef> QR;  // refs of finished q's
   for (int i = 0; i < m; ++i) {
+    const std::string step_name = "tt_orth: Gram-Schmidt step " + std::to_string(i + 1);
+    TTB_RANGE(step_name.c_str());
     TTRef base = A[(size_t)i];
     base.norm = an[(size_t)i];
     Owned prev(ctx);
@@ -491,10 +494,15 @@ void run_gs(tt_ctx ctx, tt_orth_kind kind, int m, const std::vector<TTRef>& A, c
 // ----------------------------------------------------------------- Gram (Alg. 5)
 void run_gram(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::vector<double>& an, const tt_orth_opts& o,
               std::vector<tt_tensor>& Q, std::vector<double>& R, Ledger& led, int* fail_index) {
+  TTB_RANGE("tt_orth: TT-Gram");
   std::vector<std::pair<const TTRef*, const TTRef*>> pr;
   for (int i = 0; i < m; ++i)
     for (int j = 0; j <= i; ++j) pr.push_back({&A[(size_t)i], &A[(size_t)j]});
-  std::vector<double> g = dots_host(ctx, pr);
+  std::vector<double> g;
+  {
+    TTB_RANGE("tt_orth: Gram matrix");
+    g = dots_host(ctx, pr);
+  }
   std::vector<double> G((size_t)m * m);
   size_t t = 0;
   for (int i = 0; i < m; ++i)
@@ -546,6 +554,8 @@ void run_householder(tt_ctx ctx, int m, const std::vector<TTRef>& A, const std::
   TTRef w = A[0];
   w.norm = an[0];
   for (int i = 1; i <= m; ++i) {
+    const std::string step_name = "tt_orth: Householder step " + std::to_string(i);
+    TTB_RANGE(step_name.c_str());
     // TTH-vec(w, {e_1..e_i}) with element reads <w, e_j> = w(phi(j))
     std::vector<int64_t> lins;
     for (int j = 1; j <= i; ++j) lins.push_back(j);

@@ -143,6 +143,7 @@ RRBound rr_bound(tt_ctx ctx, const SumInput& in) {
 }
 
 void right_to_left(tt_ctx ctx, const SumInput& in, Sweep& sw, const RRBound* rrb) {
+  TTB_RANGE("tt_round: right-to-left orthogonalisation");
   const bool rank_revealing = rrb != nullptr;
   const int d = in.d, K = in.K();
   std::vector<std::vector<int64_t>> off = offsets(in, sw.R);
@@ -342,6 +343,7 @@ tt_tensor materialise_sum(tt_ctx ctx, const SumInput& in) {
 }
 
 tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_round_info* info) {
+  TTB_RANGE("tt_round");
   const int d = in.d, K = in.K();
   if (K < 1) fail(TT_EINVAL, "TT-round needs at least one term");
   if (o.rel_tol < 0.0 || !(o.rel_tol == o.rel_tol)) fail(TT_EINVAL, "rel_tol must be >= 0");
@@ -408,6 +410,7 @@ tt_tensor round_sum(tt_ctx ctx, const SumInput& in, const tt_round_opts& o, tt_r
     return t;
   }
   // left-to-right truncation
+  TTB_RANGE("tt_round: left-to-right truncation");
   std::vector<int64_t> ranks((size_t)d + 1, 1);
   std::vector<DBuf> outc((size_t)d);
   DBuf Z = std::move(sw.C1);

@@ -379,3 +379,42 @@ def test_batch_two_stream_wave_small_items():
         g = res.item_numpy(b)
         assert all(np.array_equal(x, y) for x, y in zip(g, res2.item_numpy(b)))
         _check_item(g, list(res.ranks[b]), items[b][0], items[b][1], 1e-8, rounding.DEFAULT_FLOOR_C)
+
+
+def _diag_term(d, n, r, off, Q):
+    """sum_{j < r} (Q_1 e_{off+j}) x ... x (Q_d e_{off+j}): every unfolding has r singular values
+    equal to 1 (up to rounding)."""
+    cores = []
+    for k in range(d):
+        r0, r1 = (1 if k == 0 else r), (1 if k == d - 1 else r)
+        G = np.zeros((r0, n, r1))
+        for a in range(r):
+            G[0 if k == 0 else a, :, 0 if k == d - 1 else a] = Q[k][:, off + a]
+        cores.append(G)
+    return cores
+
+
+@pytest.mark.parametrize("r", [4, 8, 16])
+def test_batch_repeated_singular_values(r):
+    """Sums whose unfoldings carry r-fold repeated singular values (|c_l| each): Jacobi pairs with
+    equal column norms rotate by large angles however small their inner product is -- the case
+    the tiny-rotation stopping rule of the batched Jacobi (A23) has to count as not tiny.
+    Terms 1, 2 are kept (rank 2 r), terms 3, 4 (1e-9) fall below delta = 1e-6."""
+    import paper_2211_08770_b200 as P
+    d, n, K = 4, 64, 4
+    items = []
+    for seed in range(3):
+        rng = _rng(7700 + 10 * r + seed)
+        Q = [np.linalg.qr(rng.standard_normal((n, n)))[0] for _ in range(d)]
+        terms = [_diag_term(d, n, r, l * r, Q) for l in range(K)]
+        items.append((terms, [1.0, -1.0 if seed else 1.0, 1e-9, -1e-9]))
+    norms = [[tt.tt_norm(t) for t in terms] for terms, _ in items]
+    batch = [([dev(t, nr) for t, nr in zip(terms, nb)], coeffs) for (terms, coeffs), nb in zip(items, norms)]
+    outs = P.tt_round_batch(ctx(), batch, 1e-6)
+    for (terms, coeffs), nb, o in zip(items, norms, outs):
+        assert list(o.ranks) == [1] + [2 * r] * (d - 1) + [1]
+        _check_item(o.to_numpy(), o.ranks, terms, coeffs, 1e-6, rounding.DEFAULT_FLOOR_C, norms=nb)
+    # delta = 0 keeps all 4 r values: the full Jacobi on clustered values at two scales
+    outs = P.tt_round_batch(ctx(), batch, 0.0, floor_c=0.0)
+    for (terms, coeffs), nb, o in zip(items, norms, outs):
+        _check_item(o.to_numpy(), o.ranks, terms, coeffs, 0.0, 0.0, norms=nb)

@@ -17,6 +17,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--B", type=int, default=512)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--no-profile", action="store_true",
+                    help="no per-launch events: the wave runs split over the streams as in bench.py")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -34,7 +36,7 @@ def main():
     torch.cuda.synchronize()
     ranks = res.ranks[:4].tolist()
     del res
-    ctx.profile(True)
+    ctx.profile(not args.no_profile)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.reps):
@@ -43,7 +45,7 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.reps
-    rep = ctx.profile_report()
+    rep = ctx.profile_report() if not args.no_profile else {}
     ctx.profile(False)
     print(json.dumps({"B": args.B, "ms_per_batch": ms, "roundings_per_s": args.B / ms * 1e3, "ranks": ranks}))
     for k, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"]):

@@ -24,9 +24,9 @@ def details(rep):
 def raw(rep, names):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, v = rows[0], rows[2] if len(rows) > 2 else rows[1]
-    d = dict(zip(h, v))
-    return {n: d.get(n) for n in names}
+    h, u, v = rows[0], rows[1], rows[2] if len(rows) > 2 else rows[1]
+    d = dict(zip(h, zip(v, u)))
+    return {n: (" ".join(d[n]) if n in d else None) for n in names}
 
 
 def sass(rep, top):
@@ -54,7 +54,13 @@ if __name__ == "__main__":
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 10
     for kk, vv in details(rep).items():
         print(f"{kk}: {vv}")
-    r = raw(rep, ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    r = raw(rep, ["gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+                  "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
+                  "sm__warps_active.avg.pct_of_peak_sustained_active",
+                  "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+                  "smsp__inst_executed.sum",
+                  "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                   "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
                   "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "SM_C.TriageCompute.smsp__pipe_tensor_subpipe_dmma_cycles_active.avg", "sm__cycles_elapsed.avg",
                   "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__warps_issue_stalled_barrier_per_warp_active.pct"])
