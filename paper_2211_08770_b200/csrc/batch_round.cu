@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
 // rows -- the caller picks LPP so that a round's kk / 2 pairs fill the 8 warps.
 template <int LPP>
 __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol, double negl, double tail2,
-                                                 long long* nsweeps) {
+                                                 double isc, long long* nsweeps) {
   constexpr int RPL = BR_C / LPP, NPW = 32 / LPP;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = nc + (nc & 1);
@@ -969,7 +969,7 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
     for (int j = warp; j < nc; j += BR_W) {
       const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
       const double sq = warp_sum(x0 * x0 + x1 * x1);
-      if (lane == 0) n2[j] = sq;
+      if (lane == 0) n2[j] = sq * isc;
     }
     if (tid == 0) { sm.flag = 0; sm.rho = 0; }  // sm.rho: a rotation of this sweep was not tiny (below)
     __syncthreads();
@@ -1003,6 +1003,7 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
       for (int t = 0; t < RPL; ++t) ga += x[t] * y[t];
 #pragma unroll
       for (int o = LPP / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      ga *= isc;  // alpha, beta, gamma in units of 2^k ~ ||A||_F^2: their products stay in range
       const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tail2 || be > tail2) &&
                        ga * ga > tol2 * (al * be);
       bool big = false;
@@ -1058,7 +1059,15 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
   // relative test never settles, so they are left alone (their sigma stays <= u ||A||_F).
   double fro = 0.0;
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; fro += v * v; }
-  const double negl = block_sum(fro, sm.red) * U_ROUND * U_ROUND;
+  const double fro2 = block_sum(fro, sm.red);
+  // The rounds test products of squared norms (gamma^2 against alpha beta): all three are taken
+  // in units of 2^k ~ ||A||_F^2 (an exact scaling), so the tests neither underflow nor overflow
+  // for matrices whose squared norms are representable (||A||_F within ~1e-150 .. 1e150).
+  int ek = (fro2 > 0.0 && fro2 <= 1.7e308) ? ilogb(fro2) : 0;
+  ek = ek > 1000 ? 1000 : (ek < -1000 ? -1000 : ek);
+  const double isc = scalbn(1.0, -ek);
+  const double negl = fro2 * isc * U_ROUND * U_ROUND;
+  tail2 *= isc;
   __syncthreads();
   const int pairs = (nc + (nc & 1)) / 2;
   bool conv;
@@ -1067,9 +1076,9 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
   if (lpp == 0) lpp = pairs <= BR_W ? 32 : pairs <= 2 * BR_W ? 16 : 8;
   if (lpp == 32 && pairs > BR_W) lpp = 16;
   if (lpp == 16 && pairs > 2 * BR_W) lpp = 8;
-  if (lpp == 32) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, nsweeps);
-  else if (lpp == 16) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, nsweeps);
-  else conv = br_jacobi_rounds<8>(sm, nc, tol, negl, tail2, nsweeps);
+  if (lpp == 32) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, isc, nsweeps);
+  else if (lpp == 16) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, isc, nsweeps);
+  else conv = br_jacobi_rounds<8>(sm, nc, tol, negl, tail2, isc, nsweeps);
   // singular values = column norms, sorted descending (ties: lower column first)
   for (int j = warp; j < nc; j += BR_W) {
     const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
@@ -2361,6 +2370,8 @@ void run_batch(tt_ctx ctx, const BatchDesc& in, const tt_round_opts& o, BatchOut
         if (hinf[(size_t)b]) fail(TT_ENOCONV, "Jacobi SVD did not converge (batch item " + std::to_string(w0 + b) + ")");
       std::vector<double> hsc((size_t)nb * 4);
       std::memcpy(hsc.data(), piece(SC.p), sizeof(double) * hsc.size());
+      for (int b = 0; b < nb; ++b)  // value range (tt_b200.h): squared norms must be representable
+        if (!std::isfinite(hsc[(size_t)b * 4])) fail(TT_EINVAL, "batch item " + std::to_string(w0 + b) + ": ||x|| is not finite (input outside the value range, see tt_b200.h)");
       std::vector<int> hgm((size_t)nb);
       std::memcpy(hgm.data(), piece(GM.p), sizeof(int) * hgm.size());
       std::vector<int64_t> dst((size_t)nb * d), sz((size_t)nb * d);

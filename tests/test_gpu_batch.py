@@ -418,3 +418,34 @@ def test_batch_repeated_singular_values(r):
     outs = P.tt_round_batch(ctx(), batch, 0.0, floor_c=0.0)
     for (terms, coeffs), nb, o in zip(items, norms, outs):
         _check_item(o.to_numpy(), o.ranks, terms, coeffs, 0.0, 0.0, norms=nb)
+
+
+@pytest.mark.parametrize("e", [-120, -90, -60, 75, 90, 140])
+def test_batch_scaled_inputs(e):
+    """The value range of the path (include/tt_b200.h): the same sum scaled by 10^e must round to
+    the same ranks with the same relative error -- the Jacobi's tests on products of squared
+    norms run in units of ||A||_F^2 (exact power-of-two scaling)."""
+    import paper_2211_08770_b200 as P
+    rng = _rng(4242)
+    d, n = 5, [12, 20, 16, 20, 12]
+    ranks = [[1, 6, 9, 9, 6, 1], [1, 5, 8, 7, 5, 1], [1, 6, 9, 9, 6, 1]]
+    base = [make_random_tt(d, n, r, rng) for r in ranks]
+    base[2] = base[0]                      # near cancellation of terms 1 and 3
+    coeffs = [1.0, 0.5, -1.0 + 1e-9]
+    f = 10.0 ** e
+    terms = [[c * (f if k == 0 else 1.0) for k, c in enumerate(t)] for t in base]
+    norms = [tt.tt_norm(t) for t in terms]
+    batch = [([dev(t, nr) for t, nr in zip(terms, norms)], coeffs)] * 2
+    for o in P.tt_round_batch(ctx(), batch, 1e-6):
+        _check_item(o.to_numpy(), o.ranks, terms, coeffs, 1e-6, rounding.DEFAULT_FLOOR_C, norms=norms)
+
+
+def test_batch_overflowing_input_fails_loudly():
+    import paper_2211_08770_b200 as P
+    from paper_2211_08770_b200._native import TTError
+    rng = _rng(4243)
+    d, n = 3, [8, 8, 8]
+    t = make_random_tt(d, n, [1, 4, 4, 1], rng)
+    t[0] = t[0] * 1e200
+    with pytest.raises(TTError):
+        P.tt_round_batch(ctx(), [([dev(t, float("nan"))], [1.0])] * 2, 1e-6)
