@@ -971,6 +971,11 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
       const double sq = warp_sum(x0 * x0 + x1 * x1);
       if (lane == 0) n2[j] = sq * isc;
     }
+    // Small-small pairs are skipped for the first 12 sweeps only: when the threshold falls inside a
+    // cluster (tau at the noise level of a cancelling sum), skipped pairs of strongly correlated
+    // small columns couple the big-small rotations to first order and the iteration turns linear;
+    // from sweep 12 on every pair rotates (plain one-sided Jacobi, quadratic again).
+    const double tl2 = sweep < 12 ? tail2 : -1.0;
     if (tid == 0) { sm.flag = 0; sm.rho = 0; }  // sm.rho: a rotation of this sweep was not tiny (below)
     __syncthreads();
 #pragma unroll 1
@@ -1004,7 +1009,7 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
 #pragma unroll
       for (int o = LPP / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
       ga *= isc;  // alpha, beta, gamma in units of 2^k ~ ||A||_F^2: their products stay in range
-      const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tail2 || be > tail2) &&
+      const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tl2 || be > tl2) &&
                        ga * ga > tol2 * (al * be);
       bool big = false;
       if (rot) {
@@ -1354,7 +1359,12 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
     double e2 = 0.0;
     const bool prof = A.dbg && blockIdx.x == 0 && tid == 0;  // CTA 0 phase cycles (TT_B200_BR_DEBUG)
     long long pt = prof ? clock64() : 0;
-    const int kq = br_qrcp(sm, cp, cp, 1e-6 * tau * tau, taus, sm.cterm, nrm2, &e2);
+    // theta = min(1e-3, 1e-7 ||x|| / tau): the left vectors of [T^T E^T] are those of T^T up to
+    // ||E||^2 / gap (M M^T = T^T T + E^T E), so (theta tau)^2 <= 1e-14 ||x||^2 keeps that
+    // perturbation within ~100 u ||x||^2 / gap of the exact SVD's own sensitivity, for any delta;
+    // the first-order term E U~ enters the next core's target below.
+    const double th = fmin(1e-3, 1e-7 * sc[0] / tau);
+    const int kq = br_qrcp(sm, cp, cp, th * th * tau * tau, taus, sm.cterm, nrm2, &e2);
     if (prof) { const long long t = clock64(); A.dbg[80] += t - pt; A.dbg[84] += kq; A.dbg[85] += 1; pt = t; }
     for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) qx[idx] = sm.Rs[idx];
     if (tid < BR_C) qx[BR_C * BR_C + tid] = tid < kq ? taus[tid] : 0.0;
@@ -1396,7 +1406,9 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
           if (j < cp) tt[col * BR_C + sm.cterm[j]] = sg > 0.0 ? sm.Rs[sm.perm[col] * BR_C + j] / sg : 0.0;
           else tt[col * BR_C + j] = 0.0;
         }
-      // V_rho S = Q_X [J Sigma; 0] (second slot) and, for U = Y W, W = Q_X [J Sigma^-1; 0] (first)
+      // V_rho S = R_Y^T U_rho = Q_X [T; E] U~ = Q_X [J Sigma; E U~] (second slot) with U~ = C J / sigma
+      // (pivoted coordinates; E = the unreduced trailing block left in qx: rows and columns >= kq)
+      // and, for U = Y W, W = V_rho S Sigma^-2 = Q_X [J Sigma^-1; E U~ Sigma^-2] (first slot).
       // Targets of this warp: its columns col = warp + 8 i, each as J Sigma (second slot) and, for
       // U = Y W, J Sigma^-1 (first slot); up to 8 targets at a time take each reflector together
       // (one transposed butterfly per reflector for all of them).
@@ -1417,6 +1429,37 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
           const int pc = live ? sm.perm[col] : 0;
           y0[t] = live && lane < kq ? sm.Aux[pc * BR_C + lane] * f : 0.0;
           y1[t] = live && lane + 32 < kq ? sm.Aux[pc * BR_C + lane + 32] * f : 0.0;
+        }
+        if (kq < cp) {  // rows >= kq: E U~ (times sigma^-2 for the W targets)
+          const bool in0 = lane >= kq && lane < cp, in1 = lane + 32 >= kq && lane + 32 < cp;
+          const double* ccol[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int tg = g0 + t;
+            const int col = warp + BR_W * (use_gemm ? tg >> 1 : tg);
+            ccol[t] = sm.Rs + (tg < ntg ? sm.perm[col] : 0) * BR_C;
+          }
+#pragma unroll 1
+          for (int j = kq; j < cp; ++j) {
+            const double e0 = in0 ? qx[j * BR_C + lane] : 0.0;
+            const double e1 = in1 ? qx[j * BR_C + lane + 32] : 0.0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const double c = ccol[t][j];
+              y0[t] += e0 * c;
+              y1[t] += e1 * c;
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int tg = g0 + t;
+            const int col = warp + BR_W * (use_gemm ? tg >> 1 : tg);
+            const double sg = tg < ntg ? sm.sig[col] : 0.0;
+            const double h = sg > 0.0 ? 1.0 / sg : 0.0;
+            const bool wt = use_gemm && (tg & 1);  // one factor at a time: h^3 alone may overflow
+            if (in0) { y0[t] *= h; if (wt) { y0[t] *= h; y0[t] *= h; } }
+            if (in1) { y1[t] *= h; if (wt) { y1[t] *= h; y1[t] *= h; } }
+          }
         }
 #pragma unroll 1
         for (int i = kq - 1; i >= 0; --i) {  // Q_X = H_0 .. H_{kq-1}: H_{kq-1} first
@@ -1468,6 +1511,10 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
       // tail[rho] = sqrt(sum_{j >= rho} sigma_j^2), accumulated from the smallest value up
       double tail2 = 0.0;
       rho = nsv;
+      // A short wide Y_k (more columns than rows) leaves cp - nsv columns that are zero in exact
+      // arithmetic; with the small-small pairs not rotated they share the small columns' mass,
+      // which belongs to the tail (only the group's total is exact).
+      for (int r = cp - 1; r >= nsv; --r) tail2 += sm.sig[r] * sm.sig[r];
       for (int r = nsv - 1; r >= 1; --r) {
         tail2 += sm.sig[r] * sm.sig[r];
         if (sqrt(tail2) <= tau) rho = r; else break;

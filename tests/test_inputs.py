@@ -32,3 +32,20 @@ def test_terms_unit_norm_right_orthonormal_and_coefficients():
             for k in range(1, 5):
                 G = y[k].reshape(y[k].shape[0], -1)
                 assert np.abs(G @ G.T - np.eye(G.shape[0])).max() <= 1e-14
+
+
+def test_fuzz_batch_generator_is_deterministic_and_in_range():
+    """ttinputs.make_fuzz_batch: same seed, same bytes; formal ranks <= 64 (a cancelling item repeats
+    its first term as its last, so the items of a batch may differ in shape)."""
+    from ttinputs import make_fuzz_batch
+    for seed in (0, 31, 576, 943):
+        a, da, fa, desc = make_fuzz_batch(seed)
+        b, db, fb, _ = make_fuzz_batch(seed)
+        assert (da, fa) == (db, fb) and len(a) == len(b) >= 1
+        for (ta, ca), (tb, cb) in zip(a, b):
+            assert ca == cb
+            for x, y in zip(ta, tb):
+                assert all(np.array_equal(u, v) for u, v in zip(x, y))
+            d = len(ta[0])
+            for k in range(1, d):
+                assert sum(t[k].shape[0] for t in ta) <= 64

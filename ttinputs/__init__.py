@@ -13,6 +13,7 @@ from .generate import (  # noqa: F401
     make_shared_tail_set,
     make_batch_sums,
     make_batch_sums_stacked,
+    make_fuzz_batch,
     make_random_tt,
     tt_ranks_capped,
 )

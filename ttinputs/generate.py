@@ -220,3 +220,44 @@ CONFIGS = {
 
 def config_spec(name: str) -> ConfigSpec:
     return CONFIGS[name]
+
+
+def make_fuzz_batch(seed: int):
+    """Randomised batch for the batched engine's parity sweep (tools/fuzz_batch.py,
+    tests/test_gpu_batch.py): random order, mode sizes, term count and ranks (formal rank <= 64),
+    optionally graded rank slices (unfolding spectra over many decades), mixed term scales and --
+    only with the noise floor on -- near cancellation of the first and last term.  Returns
+    (items, delta, floor_c, description); items = [(terms, coeffs), ...].  floor_c is 0.0 (off) or
+    None (the caller's default constant)."""
+    rng = np.random.Generator(np.random.PCG64(50000 + seed))
+    d = int(rng.integers(2, 8))
+    n = [int(v) for v in rng.integers(1, 33, size=d)]
+    K = int(rng.integers(1, 6))
+    rmax = max(1, 64 // K)
+    ranks = [[1] + [int(v) for v in rng.integers(1, rmax + 1, size=d - 1)] + [1] for _ in range(K)]
+    delta = float(rng.choice([0.0, 1e-1, 1e-3, 1e-6, 1e-10, 1e-14]))
+    floor_off = delta == 0.0 or rng.random() < 0.3
+    graded = rng.random() < 0.5
+    mixed = rng.random() < 0.3
+    B = int(rng.integers(1, 4))
+    items = []
+    for _ in range(B):
+        terms = []
+        for r in ranks:
+            t = make_random_tt(d, n, r, rng)
+            if graded:
+                for k in range(d - 1):
+                    g = 10.0 ** (-rng.uniform(0, 16.0 / max(1, d - 1)) * np.arange(r[k + 1]) / max(1, r[k + 1] - 1))
+                    t[k] = t[k] * g[None, None, :]
+            if mixed:
+                t[0] = t[0] * 10.0 ** float(rng.integers(-40, 41))
+            terms.append(t)
+        coeffs = [float(v) for v in rng.standard_normal(K)]
+        cancel = K >= 2 and rng.random() < 0.3
+        if cancel and not floor_off:  # with the floor off the ranks of a cancelling sum are noise (A12)
+            terms[-1] = terms[0]
+            coeffs[-1] = -coeffs[0] * (1.0 + float(rng.choice([0.0, 1e-12, 1e-7])))
+        items.append((terms, coeffs))
+    desc = (f"seed {seed} d={d} n={n} K={K} ranks={ranks} delta={delta} floor={'off' if floor_off else 'on'} "
+            f"graded={graded} mixed={mixed}")
+    return items, delta, (0.0 if floor_off else None), desc
