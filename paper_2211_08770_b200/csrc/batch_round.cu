@@ -1413,6 +1413,9 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
       // U = Y W, J Sigma^-1 (first slot); up to 8 targets at a time take each reflector together
       // (one transposed butterfly per reflector for all of them).
       const int lane = tid & 31, warp = tid >> 5;
+      // E (rows and columns >= kq of the QRCP remainder) into the columns of Aux that J leaves free
+      for (int idx = tid + kq * BR_C; idx < cp * BR_C; idx += BR_T) sm.Aux[idx] = qx[idx];
+      __syncthreads();
       const int ncw = rho > warp ? (rho - warp + BR_W - 1) / BR_W : 0;
       const int ntg = ncw * (use_gemm ? 2 : 1);
       const double* taus_x = qx + BR_C * BR_C;
@@ -1441,8 +1444,8 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
           }
 #pragma unroll 1
           for (int j = kq; j < cp; ++j) {
-            const double e0 = in0 ? qx[j * BR_C + lane] : 0.0;
-            const double e1 = in1 ? qx[j * BR_C + lane + 32] : 0.0;
+            const double e0 = in0 ? sm.Aux[j * BR_C + lane] : 0.0;
+            const double e1 = in1 ? sm.Aux[j * BR_C + lane + 32] : 0.0;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
               const double c = ccol[t][j];
