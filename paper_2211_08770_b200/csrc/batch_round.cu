@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(BR_T, 2) br_r2l_kernel(BRArgs A, int kc) {
 // rows -- the caller picks LPP so that a round's kk / 2 pairs fill the 8 warps.
 template <int LPP>
 __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol, double negl, double tail2,
-                                                 double isc, long long* nsweeps) {
+                                                 long long* nsweeps) {
   constexpr int RPL = BR_C / LPP, NPW = 32 / LPP;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kk = nc + (nc & 1);
@@ -969,7 +969,7 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
     for (int j = warp; j < nc; j += BR_W) {
       const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
       const double sq = warp_sum(x0 * x0 + x1 * x1);
-      if (lane == 0) n2[j] = sq * isc;
+      if (lane == 0) n2[j] = sq;
     }
     // Small-small pairs are skipped for the first 12 sweeps only: when the threshold falls inside a
     // cluster (tau at the noise level of a cancelling sum), skipped pairs of strongly correlated
@@ -1008,7 +1008,6 @@ __device__ __forceinline__ bool br_jacobi_rounds(BRSmem& sm, int nc, double tol,
       for (int t = 0; t < RPL; ++t) ga += x[t] * y[t];
 #pragma unroll
       for (int o = LPP / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
-      ga *= isc;  // alpha, beta, gamma in units of 2^k ~ ||A||_F^2: their products stay in range
       const bool rot = act && ga != 0.0 && al > negl && be > negl && (al > tl2 || be > tl2) &&
                        ga * ga > tol2 * (al * be);
       bool big = false;
@@ -1064,15 +1063,22 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
   // relative test never settles, so they are left alone (their sigma stays <= u ||A||_F).
   double fro = 0.0;
   for (int idx = tid; idx < BR_C * BR_C; idx += BR_T) { const double v = sm.Rs[idx]; fro += v * v; }
-  const double fro2 = block_sum(fro, sm.red);
-  // The rounds test products of squared norms (gamma^2 against alpha beta): all three are taken
-  // in units of 2^k ~ ||A||_F^2 (an exact scaling), so the tests neither underflow nor overflow
-  // for matrices whose squared norms are representable (||A||_F within ~1e-150 .. 1e150).
-  int ek = (fro2 > 0.0 && fro2 <= 1.7e308) ? ilogb(fro2) : 0;
-  ek = ek > 1000 ? 1000 : (ek < -1000 ? -1000 : ek);
-  const double isc = scalbn(1.0, -ek);
-  const double negl = fro2 * isc * U_ROUND * U_ROUND;
-  tail2 *= isc;
+  double fro2 = block_sum(fro, sm.red);
+  // The rounds test products of squared norms (gamma^2 against alpha beta): a matrix whose
+  // ||A||_F^2 is far from 1 is scaled by a power of two first (exact) and scaled back after the
+  // rounds, so the tests neither underflow nor overflow for matrices whose squared norms are
+  // representable (||A||_F within ~1e-150 .. 1e150); ordinary inputs skip both passes.
+  int ek = (fro2 > 0.0 && fro2 <= 1.7e308) ? ilogb(fro2) / 2 : 0;
+  ek = ek > 500 ? 500 : (ek < -500 ? -500 : ek);
+  const bool scaled = ek >= 64 || ek <= -64;
+  __syncthreads();  // block_sum's scratch is reused below
+  if (scaled) {
+    const double f = scalbn(1.0, -ek);
+    for (int idx = tid; idx < BR_C * nc; idx += BR_T) sm.Rs[idx] *= f;
+    fro2 *= f * f;
+    tail2 *= f * f;
+  }
+  const double negl = fro2 * U_ROUND * U_ROUND;
   __syncthreads();
   const int pairs = (nc + (nc & 1)) / 2;
   bool conv;
@@ -1081,9 +1087,14 @@ __device__ __noinline__ bool br_jacobi(BRSmem& sm, int rows, int nc, double tail
   if (lpp == 0) lpp = pairs <= BR_W ? 32 : pairs <= 2 * BR_W ? 16 : 8;
   if (lpp == 32 && pairs > BR_W) lpp = 16;
   if (lpp == 16 && pairs > 2 * BR_W) lpp = 8;
-  if (lpp == 32) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, isc, nsweeps);
-  else if (lpp == 16) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, isc, nsweeps);
-  else conv = br_jacobi_rounds<8>(sm, nc, tol, negl, tail2, isc, nsweeps);
+  if (lpp == 32) conv = br_jacobi_rounds<32>(sm, nc, tol, negl, tail2, nsweeps);
+  else if (lpp == 16) conv = br_jacobi_rounds<16>(sm, nc, tol, negl, tail2, nsweeps);
+  else conv = br_jacobi_rounds<8>(sm, nc, tol, negl, tail2, nsweeps);
+  if (scaled) {
+    const double f = scalbn(1.0, ek);
+    for (int idx = tid; idx < BR_C * nc; idx += BR_T) sm.Rs[idx] *= f;
+    __syncthreads();
+  }
   // singular values = column norms, sorted descending (ties: lower column first)
   for (int j = warp; j < nc; j += BR_W) {
     const double x0 = sm.Rs[j * BR_C + lane], x1 = sm.Rs[j * BR_C + lane + 32];
