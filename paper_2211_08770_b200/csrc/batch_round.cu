@@ -1453,15 +1453,34 @@ __global__ void __launch_bounds__(BR_T, 3) br_l2r_svd_kernel(BRArgs A, int k) {
             const int col = warp + BR_W * (use_gemm ? tg >> 1 : tg);
             ccol[t] = sm.Rs + (tg < ntg ? sm.perm[col] : 0) * BR_C;
           }
+          if (use_gemm) {  // targets 2 u and 2 u + 1 share their column: one sum for both
 #pragma unroll 1
-          for (int j = kq; j < cp; ++j) {
-            const double e0 = in0 ? sm.Aux[j * BR_C + lane] : 0.0;
-            const double e1 = in1 ? sm.Aux[j * BR_C + lane + 32] : 0.0;
+            for (int j = kq; j < cp; ++j) {
+              const double e0 = in0 ? sm.Aux[j * BR_C + lane] : 0.0;
+              const double e1 = in1 ? sm.Aux[j * BR_C + lane + 32] : 0.0;
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const double c = ccol[t][j];
-              y0[t] += e0 * c;
-              y1[t] += e1 * c;
+              for (int u = 0; u < 4; ++u) {
+                const double c = ccol[2 * u][j];
+                y0[2 * u] += e0 * c;
+                y1[2 * u] += e1 * c;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (in0) y0[2 * u + 1] = y0[2 * u];
+              if (in1) y1[2 * u + 1] = y1[2 * u];
+            }
+          } else {
+#pragma unroll 1
+            for (int j = kq; j < cp; ++j) {
+              const double e0 = in0 ? sm.Aux[j * BR_C + lane] : 0.0;
+              const double e1 = in1 ? sm.Aux[j * BR_C + lane + 32] : 0.0;
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                const double c = ccol[t][j];
+                y0[t] += e0 * c;
+                y1[t] += e1 * c;
+              }
             }
           }
 #pragma unroll
