@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--seeds", type=int, default=200)
     ap.add_argument("--start", type=int, default=0)
     ap.add_argument("--only", default="", help="comma-separated seeds (verbose)")
+    ap.add_argument("--unknown-norms", action="store_true", help="term norms passed as NaN (computed on the device)")
+    ap.add_argument("--max-rank", type=int, default=0, help="cap every rank (tt_round_opts.max_rank)")
     ap.add_argument("--serial", action="store_true", help="each item through tt_round's sweep (TT_B200_SERIAL_BATCH=0)")
     args = ap.parse_args()
     import numpy as np
@@ -38,12 +40,15 @@ def main():
             print(f"  coeffs of item 0: {items[0][1]}")
         try:
             norms = [[tt.tt_norm(t) for t in terms] for terms, _ in items]
-            batch = [([dev(t, nr) for t, nr in zip(terms, nb)], coeffs) for (terms, coeffs), nb in zip(items, norms)]
+            un = float("nan") if args.unknown_norms else None
+            batch = [([dev(t, nr if un is None else un) for t, nr in zip(terms, nb)], coeffs)
+                     for (terms, coeffs), nb in zip(items, norms)]
+            mr = args.max_rank if args.max_rank > 0 else None
             if args.serial:
                 os.environ["TT_B200_SERIAL_BATCH"] = "0"
-                outs = [P.tt_round(ctx(), bt, bc, delta, floor_c=floor_c)[0] for bt, bc in batch]
+                outs = [P.tt_round(ctx(), bt, bc, delta, floor_c=floor_c, max_rank=args.max_rank)[0] for bt, bc in batch]
             else:
-                outs = P.tt_round_batch(ctx(), batch, delta, floor_c=floor_c)
+                outs = P.tt_round_batch(ctx(), batch, delta, floor_c=floor_c, max_rank=args.max_rank)
             for (terms, coeffs), nb, o in zip(items, norms, outs):
                 if args.only:
                     ref, info = rounding.tt_round_sum(terms, coeffs, delta, floor_c=floor_c, term_norms=nb)
@@ -56,7 +61,7 @@ def main():
                         r = info.ranks[k + 1]
                         lo, hi = max(0, r - 2), min(len(S), r + 2)
                         print(f"     split {k + 1}: sigma[{lo}:{hi}] = {S[lo:hi]}, tail(r) {np.sqrt(np.sum(S[r:] ** 2)):.3e}")
-                assert_round_parity(o.to_numpy(), o.ranks, terms, coeffs, delta, floor_c, nb, tag=f"fuzz{seed}")
+                assert_round_parity(o.to_numpy(), o.ranks, terms, coeffs, delta, floor_c, nb, max_rank=mr, tag=f"fuzz{seed}")
         except Exception as ex:  # noqa: BLE001
             fails += 1
             print(f"FAIL {tag}\n     {type(ex).__name__}: {str(ex)[:300]}", flush=True)
