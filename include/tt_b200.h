@@ -22,9 +22,10 @@
  *     valid until the next call on it).  No call throws or aborts.
  *   - Value range: the path forms squared norms (column masses, Householder and Jacobi
  *     quantities), so a tensor and every term of a sum must have its Frobenius norm within
- *     about 1e-140 .. 1e140 (checked against the oracle at 1e-120 and 1e140,
- *     tests/test_gpu_batch.py); tt_round_batch* fail with TT_EINVAL when an item's ||x|| comes
- *     out non-finite.  Scale such inputs by a power of two first (exact).
+ *     about 1e-120 .. 1e120 (roundings checked against the oracle at 1e-120 and 1e140,
+ *     tests/test_gpu_batch.py; the drivers against the closed form at 1e-100 and 1e100,
+ *     tools/orth_scale_probe.py); a rounding whose ||x|| comes out non-finite fails with
+ *     TT_EINVAL.  Scale such inputs by a power of two first (exact).
  *   - Ownership: tt_view arguments are BORROWED (never written; must stay valid until the
  *     call returns).  tt_tensor results are allocated by the library (their ranks are
  *     data-dependent) from the context's stream-ordered pool; release with
